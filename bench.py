@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the rotation-voting hot path (BASELINE.json metric, config 4).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one rot_vote_solve of BASELINE config 4 (N = 1e6 synthetic correspondences,
+1% inliers sigma = 0.01, 99% uniform outliers, eps = 0.05): setup, the whole certified
+coarse-to-fine vote, the fp64 recheck and the linear refinement -- every row of SURVEY §8(a).
+Inputs are resident in HBM before the timed region; L2 (126 MB) is flushed between timed
+steps by writing a 512 MB buffer outside the timed spans.  Multi-GPU (torchrun): the single
+problem's candidate cells are sharded across ranks (NCCL allgather per level, strong scaling);
+time is the max over ranks of the per-rank device time (CUDA events).
+
+--impl reference: the CPU oracle (oracle/, plain single-threaded C++), as it stands, timed on
+this host on a bounded sample of the same workload (this tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "corr×cell votes/s and ms/solve at N=1e6, 99% outliers, 1/2/4/8 B200"
+UNIT = "corr×cell votes/s"
+WORKLOAD = "cfg4: N=1e6 fp32 correspondences, 1% inliers (sigma=0.01), 99% uniform-S2 outliers, eps=0.05"
+FLOP_PER_PAIR = 18          # 9 FMA per (correspondence, cell) pair in the traceless 9-entry form
+SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0   # B200_PROFILING.md nominal table
+FP32_PEAK_TFLOPS = SM_COUNT * FP32_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 74.4 TFLOP/s
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--levels", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+# ---- clocks during the timed region (NVML) ------------------------------------------------------
+_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+            0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, device: int, period: float = 0.02):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period, self._stop = period, threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = get_r(self.h)
+                for bit, name in _REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---- CPU oracle leg --------------------------------------------------------------------------
+
+def oracle_sample(pr, seconds: float):
+    """The oracle (as it stands, one thread) counting blocks of the dominant level (B = 45,
+    bound threshold) of the same N = 1e6 problem until `seconds` of CPU work are done."""
+    import numpy as np
+
+    import oracle
+    oracle.build()
+    lins = oracle.candidates(45)
+    rng = np.random.default_rng(0)
+    lins = rng.permutation(lins)
+    done, t0, chunk = 0, time.perf_counter(), 25
+    while time.perf_counter() - t0 < seconds and done < lins.size:
+        sub = lins[done:done + chunk]
+        thr = np.array([oracle.cell_bound_threshold(45, int(l), pr.eps) for l in sub]) - 1e-5
+        oracle.count_cells(pr.x, pr.y, 45, sub, thr, band=0)
+        done += sub.size
+    dt = time.perf_counter() - t0
+    return done * pr.n / dt, done, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import datagen
+    pr = datagen.cfg4()
+    per_step = max(1.0, min(6.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(pr, per_step / 2)
+    vals, times = [], []
+    for _ in range(args.steps):
+        v, cells, dt = oracle_sample(pr, per_step)
+        vals.append(v)
+        times.append(dt)
+    value = sum(c for c in [v * t for v, t in zip(vals, times)]) / sum(times)
+    sample = (f"oracle counts of randomly chosen B=45 blocks (the dominant level of the solve) "
+              f"over all 1e6 correspondences, ~{per_step:.1f} s of one thread per step")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "cpu": _cpu_name()},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _cpu_name():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip() + f" ({os.cpu_count()} threads)"
+    except OSError:
+        pass
+    return None
+
+
+# ---- our arm -----------------------------------------------------------------------------------
+
+def _load_traffic():
+    p = os.path.join(ROOT, "profiles", "vote_kernel_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get("bytes_per_launch"), d
+    except (OSError, ValueError):
+        return None, None
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import datagen
+    from paper_2506_11547_b200 import RotVote, rot_vote_get_unique_id
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        idb = [rot_vote_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idb, src=0)
+        nccl_id = idb[0]
+    else:
+        nccl_id = None
+
+    pr = datagen.cfg4()
+    stream = torch.cuda.current_stream()
+    rv = RotVote(device=local, max_n=pr.n, rank=rank, world=world, nccl_id=nccl_id,
+                 stream=stream)
+    x = torch.from_numpy(pr.x).cuda()
+    y = torch.from_numpy(pr.y).cuda()
+    mask = torch.zeros((pr.n + 31) // 32, dtype=torch.int32, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        res = rv.solve(x, y, pr.eps, levels=args.levels, mask=mask)
+    barrier()
+    step_ms, vote_ms, vote_pairs, launches, vote_launches = [], 0.0, 0, 0, 0
+    pair_votes = res.pair_votes
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = rv.solve(x, y, pr.eps, levels=args.levels, mask=mask)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            vote_ms += r.vote_ms
+            vote_pairs += r.vote_pairs
+            launches += r.launches
+            vote_launches += r.vote_launches
+            assert (r.cell, r.votes) == (res.cell, res.votes)
+    barrier()
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    total_ms = float(total.item())
+    ms_per_step = total_ms / args.steps
+    value = pair_votes * args.steps / (total_ms / 1e3)
+
+    # end-to-end through the public API with host buffers (pinned), copies inside the timing
+    hx = torch.from_numpy(pr.x).pin_memory()
+    hy = torch.from_numpy(pr.y).pin_memory()
+    hmask = torch.zeros((pr.n + 31) // 32, dtype=torch.int32).pin_memory()
+    hxn, hyn, hmn = hx.numpy(), hy.numpy(), hmask.numpy().view(np.uint32)
+    rv.solve_host(hxn, hyn, pr.eps, levels=args.levels, mask=hmn)
+    barrier()
+    e2e_ms = []
+    for _ in range(args.e2e_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r2 = rv.solve_host(hxn, hyn, pr.eps, levels=args.levels, mask=hmn)
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = r2.pair_votes * args.e2e_steps / (float(e2e_t.item()) / 1e3)
+
+    achieved = vote_pairs * FLOP_PER_PAIR / (vote_ms / 1e3) / 1e12 if vote_ms > 0 else None
+    traffic, _ = _load_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "levels": args.levels or 5,
+                   "chain": [15, 45, 90, 180, 360], "l2": "flushed between steps (512 MB write)",
+                   "parallelism": f"cells sharded over {world} GPU(s)" if world > 1 else "1 GPU",
+                   "pair_votes_per_solve": pair_votes, "cells_per_phase": res.cells_per_phase},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": (achieved / FP32_PEAK_TFLOPS) if achieved else None,
+                     "traffic": traffic,
+                     "kernel": "rv_vote_kernel (K3), 18 flop per (corr, cell) pair",
+                     "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)",
+                     "vote_ms_per_step": vote_ms / args.steps,
+                     "vote_share_of_step": (vote_ms / args.steps) / ms_per_step},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(2 * pr.x.nbytes),
+                "d2h_bytes_per_step": int(hmask.numel() * 4),
+                "ms_per_step": sum(e2e_ms) / len(e2e_ms)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "result": {"cell": list(res.cell), "votes": res.votes, "n_inliers": res.n_inliers,
+                   "q": [float(v) for v in res.q]},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cells, dt = oracle_sample(pr, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{cells} B=45 blocks x 1e6 correspondences ({cells * pr.n:.3g} pair votes, "
+                      f"{dt:.1f} s, one thread): the oracle's count loop on the solve's dominant "
+                      f"level", "cpu": _cpu_name()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    rv.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

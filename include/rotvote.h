@@ -1,0 +1,197 @@
+/* ============================================================================
+ * rotvote.h -- C-ABI of librotvote, the B200 (sm_100a) rotation-voting hot path
+ * of arXiv 2506.11547 "Linearly Solving Robust Rotation Estimation".
+ *
+ * Citation keys: P:n = PAPER.md line n (the paper's LaTeX source); S:n =
+ * SPEC.md line n; "R#" = a reading listed in DESIGN.md §Readings.
+ *
+ * What the library computes:
+ *   Given N correspondences (x_i, y_i), find the block c of the paper's
+ *   stereographic accumulator grid (the cube [-1,1]^3 cut into B^3 blocks,
+ *   Alg. 1 line 1; B = 2/epsilon_grid = 360 at the paper's default
+ *   epsilon = 1/180) whose centre rotation q_c = P'(p_c) is
+ *   crossed by the most quaternion circles, i.e.
+ *       count(c) = #{ i : y_i^T R(q_c) x_i >= cos(eps) }      (R1, R2)
+ *   maximised over every block meeting the unit ball (hemisphere + equator,
+ *   P:409-411), ties -> lowest linear index (R7); then refine linearly on the
+ *   inlier set (Q q = 0 in least squares, computed as the top
+ *   eigenvector of sum_i M_i, Horn P:125-150, M_i of Appendix A).
+ *   The search is a certified coarse-to-fine branch and bound (R6) whose result
+ *   equals the exhaustive scan for every `levels`.
+ *
+ * Conventions
+ *   - quaternions are scalar-first [q0,q1,q2,q3], returned as the
+ *     hemisphere representative q3 <= 0 (tie rule S:361-369).
+ *   - x, y: contiguous row-major [n][3] float32 (any nonzero length: rows are
+ *     normalised).  DEVICE pointers on the context's device unless a
+ *     function says HOST.
+ *   - every call is ordered on cfg.stream and returns after its results are
+ *     written (host-synchronous).  One context per host thread / stream.
+ *   - return value: RV_OK (0) or a negative RV_E* code; the message is in
+ *     rot_vote_last_error(ctx).  No C++ exception crosses the ABI.
+ *   - multi-GPU (world > 1): every rank calls every entry point collectively
+ *     with identical arguments (its own device replica of x, y) and receives
+ *     identical results.
+ * ========================================================================== */
+#ifndef ROTVOTE_H_
+#define ROTVOTE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ---------------------------------------------------------- */
+#define RV_OK        0
+#define RV_EINVAL   -1  /* null pointer, n < 2, n > max_n, eps not in (0,pi),
+                           levels not in [0, chain_len], bad chain, rank/world mismatch */
+#define RV_EDATA    -2  /* a non-finite or zero-length x_i / y_i (cannot normalise) */
+#define RV_ECUDA    -3  /* CUDA runtime failure */
+#define RV_ENCCL    -4  /* NCCL failure (or libnccl.so.2 not loadable when world > 1) */
+#define RV_ENOMEM   -5  /* workspace allocation failed */
+
+/* ---- result flags ------------------------------------------------------------ */
+#define RV_REFINED     1  /* at least one refinement round succeeded */
+#define RV_DEGENERATE  2  /* a round had < 2 inliers or eigengap <= 1e-12*|lambda1|;
+                             q is the last good estimate (q_c* if round 1 failed) */
+#define RV_RECHECKED   4  /* the final level needed the fp64 near-threshold recheck */
+
+#define RV_MAX_CHAIN   8
+#define RV_MAX_PHASES 16
+
+/* Opaque context: owns every device workspace, pinned staging buffer, the
+ * CUDA stream binding and (world > 1) the NCCL communicator. */
+typedef struct rv_ctx rv_ctx;
+
+typedef struct {
+  int32_t device;        /* CUDA ordinal of this rank's GPU */
+  int32_t rank;          /* 0 for a single GPU */
+  int32_t world;         /* 1 for a single GPU; > 1: NCCL over NVLink, cells sharded */
+  const void* nccl_id;   /* HOST, 128-byte ncclUniqueId from rot_vote_get_unique_id on rank 0,
+                            broadcast by the caller; NULL when world == 1 */
+  int64_t max_n;         /* workspace sizing: solve with n > max_n -> RV_EINVAL
+                            (batched: total correspondences) */
+  int32_t max_problems;  /* batched sizing (>= 1) */
+  int32_t chain_len;     /* 0 -> default chain {5,15,45,90,180,360} */
+  int32_t chain[RV_MAX_CHAIN]; /* nested grid resolutions, each divides the next; the last is
+                            the paper's accumulator resolution B = 2/epsilon_grid */
+  int32_t refine_rounds; /* linear refinement rounds (R8); 2 */
+  float   guard;         /* fp32 guard band on the vote statistic (R10); 1e-5 */
+  void*   stream;        /* cudaStream_t to order all work on (NULL = legacy default) */
+  int32_t emulate_world; /* test hook: > 1 evaluates the cell shards of that many ranks one after
+                            another on this GPU (loopback); 0/1 = off.  Requires world == 1. */
+} rv_config;
+
+typedef struct {
+  double   q[4];          /* refined rotation, scalar-first, q3 <= 0 */
+  double   q_cell[4];     /* rotation of the winning block centre (before refinement) */
+  uint32_t votes;         /* exact count of the winning block */
+  uint32_t n_inliers;     /* |{i : s_i(q) >= cos(eps)}| at the returned q (popcount of the mask) */
+  int32_t  cell[3];       /* winning block (i,j,k) at the finest resolution */
+  int32_t  flags;         /* RV_REFINED | RV_DEGENERATE | RV_RECHECKED */
+  int32_t  B;             /* finest resolution */
+  int32_t  n_tied;        /* finest blocks sharing the winning count */
+  uint64_t pair_votes;    /* sum over every evaluated (correspondence, block) pair */
+  uint64_t cells_evaluated;
+  uint32_t lb_star;       /* certified lower bound used for pruning */
+  int32_t  n_phases;      /* entries used in cells_per_phase */
+  int64_t  cells_per_phase[RV_MAX_PHASES];
+  float    ms;            /* device time of the solve on cfg.stream (CUDA events) */
+  int32_t  n_rechecked;   /* blocks that needed the fp64 near-threshold recheck */
+  float    vote_ms;       /* summed device time of the K3 vote launches (CUDA events on cfg.stream) */
+  int32_t  launches;      /* kernels this call launched (all of librotvote's own) */
+  uint64_t vote_pairs;    /* (correspondence, block) pairs voted by K3 on this rank, padding excluded */
+  int32_t  vote_launches; /* K3 launches on this rank */
+  int32_t  pad_;
+} rv_result;
+
+/* ---- lifetime ------------------------------------------------------------------ */
+
+/* Fill *cfg with the defaults: device 0, rank 0, world 1, max_n 1<<20, max_problems 1,
+ * default chain, refine_rounds 2, guard 1e-5, stream NULL. */
+void rot_vote_default_config(rv_config* cfg);
+
+/* Create a context.  Allocates all workspace for cfg->max_n correspondences on
+ * cfg->device; world > 1 initialises NCCL (ncclCommInitRank, collective across
+ * ranks).  *out = NULL on failure.  Errors: RV_EINVAL, RV_ECUDA, RV_ENCCL, RV_ENOMEM. */
+int rot_vote_create(const rv_config* cfg, rv_ctx** out);
+
+/* Release everything the context owns.  NULL is a no-op. */
+void rot_vote_destroy(rv_ctx* ctx);
+
+/* Last error message of this context ("" if none); valid until the next call. */
+const char* rot_vote_last_error(const rv_ctx* ctx);
+
+/* Write a fresh 128-byte ncclUniqueId into id_out (HOST).  Call on rank 0 only.
+ * Returns RV_ENCCL when libnccl.so.2 cannot be loaded. */
+int rot_vote_get_unique_id(void* id_out);
+
+/* ---- the hot path ----------------------------------------------------------------- */
+
+/* Solve one problem (BASELINE north_star rot_vote_solve(x, y, N, eps, levels)).
+ *   x, y   DEVICE [n][3] float32, caller-owned, unchanged.
+ *   n      2 <= n <= max_n.
+ *   eps    inlier angle in radians (double), 0 < eps < pi (R1): i is an inlier of q iff
+ *          angle(R(q) x_i, y_i) <= eps, i.e. s_i(q) >= cos(eps) evaluated in double.
+ *   levels number of chain levels used, the last `levels` entries of the chain;
+ *          0 -> min(5, chain_len); 1 = exhaustive scan of the finest grid.
+ *          The result does not depend on it (certified search, R6).
+ *   out    HOST, filled on success.
+ *   inlier_mask DEVICE uint32[ceil(n/32)] (bit i%32 of word i/32 = inlier i, LSB
+ *          first) at the returned q, or NULL.
+ * Errors: RV_EINVAL, RV_EDATA, RV_ECUDA, RV_ENCCL, RV_ENOMEM. */
+int rot_vote_solve(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                   int32_t levels, rv_result* out, uint32_t* inlier_mask);
+
+/* Same as rot_vote_solve but x, y are HOST pointers and inlier_mask (if not NULL) is a
+ * HOST buffer: the copies to and from the device are part of the call (end-to-end API). */
+int rot_vote_solve_host(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                        int32_t levels, rv_result* out, uint32_t* inlier_mask);
+
+/* Solve P independent problems (BASELINE config 5).  Problem p is rows
+ * [offsets[p], offsets[p+1]) of x, y (DEVICE).  offsets: HOST int64[P+1], offsets[0] = 0,
+ * each problem has >= 2 rows, offsets[P] <= max_n, P <= max_problems.
+ * out: HOST rv_result[P].  masks: DEVICE, problem p's mask at word offset
+ * sum_{r<p} ceil(n_r/32), or NULL.
+ * world > 1: problems are sharded in contiguous ranges across ranks (no per-level
+ * collectives); the rv_result array is all-gathered so every rank returns all P results;
+ * each rank writes the masks of its own problems only. */
+int rot_vote_solve_batched(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets,
+                           int32_t P, double eps, int32_t levels, rv_result* out, uint32_t* masks);
+
+/* ---- the individual steps, exposed for parity tests ---------- */
+
+/* a1 (K1 rv_setup): normalise x_i, y_i and write the 9 independent entries of the traceless
+ * 4x4 form K_i with y^T R(q) x = q^T K_i q (= Appendix-A M):
+ *   k_out[j*n + i], j = 0..8 -> K00, K11, K22, K01, K02, K03, K12, K13, K23
+ *   (K33 = -(K00+K11+K22) since tr K_i = 0).  k_out: DEVICE float32[9*n].
+ * Computed in fp64 and rounded once to fp32.  Errors: RV_EDATA on a bad row. */
+int rot_vote_setup(rv_ctx* ctx, const float* x, const float* y, int64_t n, float* k_out);
+
+#define RV_MODE_BOUND 0  /* cnt_a = #{i : s32_i(q_c) >= cos(min(pi, eps + r(c))) - guard} (R6) */
+#define RV_MODE_FINAL 1  /* cnt_a = #{s32 >= cos(eps) - guard}, cnt_b = #{s32 >= cos(eps) + guard} */
+#define RV_MODE_EXACT 2  /* cnt_a = #{i : s_i(q_c) >= cos(eps)} exactly: fp32 vote with an fp64
+                            recheck of every pair within the guard band (K5) */
+
+/* a2-a5 (K3 rv_vote, K5 rv_recheck): vote m blocks of the B^3 grid.
+ *   lins   DEVICE uint32[m], block (i,j,k) -> (i*B + j)*B + k.
+ *   cnt_a  DEVICE uint32[m]; cnt_b DEVICE uint32[m] (RV_MODE_FINAL only, else may be NULL).
+ * s32 is the fp32 contraction phi(q_c) . k_i of the 9-entry forms. */
+int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t B,
+                         const uint32_t* lins, int64_t m, double eps, int32_t mode,
+                         uint32_t* cnt_a, uint32_t* cnt_b);
+
+/* a6 (K6 rv_inliers + K7 rv_eig4): `rounds` rounds of linear refinement from q0 (HOST
+ * double[4]); writes q_out (HOST double[4], canonical), flags (HOST, RV_REFINED /
+ * RV_DEGENERATE), n_inliers (HOST) and the mask at q_out (DEVICE, may be NULL).  Inlier
+ * decisions are made in fp64. q0 need not be normalised; rounds = 0 only evaluates the
+ * mask at the (normalised, hemisphere-canonical) q0. */
+int rot_vote_refine(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                    const double* q0, int32_t rounds, double* q_out, int32_t* flags,
+                    uint32_t* n_inliers, uint32_t* mask);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROTVOTE_H_ */

@@ -1,0 +1,68 @@
+/* ============================================================================
+ * rotvote_plan.h -- host-side search planner of librotvote (pure C++, no CUDA).
+ *
+ * The planner is the level loop of the certified coarse-to-fine search
+ * (reading R6).  It decides which blocks of
+ * which grid level are voted next and digests their counts; it never counts
+ * anything itself.  rot_vote_solve drives it with the GPU kernels; the tests
+ * drive it with counts from the CPU oracle and, for multi-rank checks, shard
+ * each request with rv_shard_range across gloo ranks.  Every rank that feeds
+ * identical counts holds an identical planner state.
+ *
+ * Request protocol:  while (rv_plan_request(p, &B, &mode, &m, &lins)) {
+ *     count the m blocks `lins` of the B^3 grid in `mode` (rotvote.h RV_MODE_*)
+ *     rv_plan_feed(p, cnt_a, cnt_b);            // cnt_b only for RV_MODE_FINAL
+ *   }  rv_plan_get_result(p, &res);
+ * Semantics of the counts per mode are those of rot_vote_count_cells.
+ * ========================================================================== */
+#ifndef ROTVOTE_PLAN_H_
+#define ROTVOTE_PLAN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rv_plan rv_plan;
+
+typedef struct {
+  uint32_t lin;          /* winning block at the finest resolution */
+  int32_t  B;            /* finest resolution */
+  uint32_t votes;        /* its exact count */
+  int32_t  n_tied;       /* finest blocks with the same count */
+  uint32_t lb_star;      /* lower bound used for pruning */
+  int32_t  n_rechecked;  /* blocks sent to RV_MODE_EXACT */
+  uint64_t pair_votes;   /* sum over requests of m * n */
+  uint64_t cells_evaluated;
+  int32_t  n_phases;
+  int64_t  cells_per_phase[16];
+} rv_plan_result;
+
+/* chain[chain_len] nested resolutions (each divides the next, 1 <= B <= 1625); levels in
+ * [0, chain_len] (0 -> min(5, chain_len)); n >= 1 correspondences; eps in (0, pi);
+ * guard >= 0.  Returns 0 or -1 (invalid) and sets *out. */
+int  rv_plan_create(const int32_t* chain, int32_t chain_len, int32_t levels, int64_t n,
+                    double eps, double guard, rv_plan** out);
+void rv_plan_destroy(rv_plan* p);
+
+/* 1 if a request is pending (outputs set; lins valid until the next feed), 0 when done. */
+int  rv_plan_request(const rv_plan* p, int32_t* B, int32_t* mode, int64_t* m,
+                     const uint32_t** lins);
+/* Feed the counts of the pending request (HOST arrays of m entries).  0 or -1. */
+int  rv_plan_feed(rv_plan* p, const uint32_t* cnt_a, const uint32_t* cnt_b);
+/* 0 when done and *out filled, -1 while requests are pending. */
+int  rv_plan_get_result(const rv_plan* p, rv_plan_result* out);
+
+/* Contiguous shard of a request of m blocks for `rank` of `world`:
+ * [m*rank/world, m*(rank+1)/world). */
+void rv_shard_range(int64_t m, int32_t rank, int32_t world, int64_t* begin, int64_t* end);
+
+/* Candidate blocks (meeting the closed unit ball) of the B^3 grid in ascending linear
+ * index; writes min(count, cap) entries to out (may be NULL) and returns the count. */
+int64_t rv_grid_candidates(int32_t B, uint32_t* out, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROTVOTE_PLAN_H_ */

@@ -1,0 +1,968 @@
+// rv_api.cpp -- the C-ABI of librotvote (include/rotvote.h): validation, workspace, the
+// level loop that drives the host planner (rv_plan.cpp) with the sm_100a kernels
+// (rv_kernels.cu), multi-GPU cell sharding over NCCL, refinement and result assembly.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>  // types only; the library is dlopen'ed (libnccl.so.2) when world > 1
+
+#include "../../include/rotvote.h"
+#include "../../include/rotvote_plan.h"
+#include "rv_geom.h"
+#include "rv_kernels.h"
+
+namespace {
+
+const int32_t kDefaultChain[6] = {5, 15, 45, 90, 180, 360};
+
+// ---- NCCL, loaded at run time -------------------------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+    a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.CommDestroy && a.GetErrorString;
+    if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+// ---- growable buffers ------------------------------------------------------------------------
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    size_t want = std::max<size_t>(n, cap * 3 / 2 + 64);
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// pinned host staging used as a bump allocator within one synchronous step
+struct Staging {
+  char* p = nullptr;
+  size_t cap = 0, used = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    size_t want = std::max<size_t>(n, cap * 3 / 2 + 4096);
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void reset() { used = 0; }
+  template <class T>
+  T* take(size_t n) {  // caller ensured capacity
+    size_t off = (used + 255) & ~(size_t)255;
+    used = off + n * sizeof(T);
+    return reinterpret_cast<T*>(p + off);
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+inline int64_t pad4(int64_t n) { return (n + 3) & ~(int64_t)3; }
+
+}  // namespace
+
+struct rv_ctx {
+  rv_config cfg{};
+  std::vector<int32_t> chain;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int num_sms = 148;
+  int vote_blocks_per_sm = 2;
+  ncclComm_t comm = nullptr;
+
+  DevBuf<float> k9;              // [9][stride]
+  int64_t stride = 0;
+  DevBuf<uint32_t> lins, cnt;    // request blocks, counts (gathered layout)
+  DevBuf<rv::VoteSeg> vsegs;
+  DevBuf<rv::VoteItem> vitems;
+  DevBuf<rv::RefSeg> rsegs;
+  DevBuf<rv::RefItem> ritems;
+  DevBuf<double> partials, qs;
+  DevBuf<int32_t> flags;
+  DevBuf<uint32_t> ninl;
+  DevBuf<int64_t> rows, koffs;
+  DevBuf<unsigned long long> bad;
+  DevBuf<float> hx, hy;          // device copies for rot_vote_solve_host
+  DevBuf<uint32_t> hmask;
+  DevBuf<char> gather;           // batched result all-gather
+  Staging up, down;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evv0 = nullptr, evv1 = nullptr;
+  // per-call counters reported in rv_result
+  float vote_ms = 0;
+  uint64_t vote_pairs = 0;
+  int32_t launches = 0, vote_launches = 0;
+  void reset_counters() { vote_ms = 0; vote_pairs = 0; launches = 0; vote_launches = 0; }
+
+  int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    err = buf;
+    return code;
+  }
+  int cuda_fail(cudaError_t e, const char* what) {
+    return fail(e == cudaErrorMemoryAllocation ? RV_ENOMEM : RV_ECUDA, "%s: %s", what,
+                cudaGetErrorString(e));
+  }
+  int effective_world() const {
+    if (cfg.world > 1) return cfg.world;
+    return cfg.emulate_world > 1 ? cfg.emulate_world : 1;
+  }
+};
+
+#define RV_CUDA(call, what)                               \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return ctx->cuda_fail(e_, what); \
+  } while (0)
+
+namespace {
+
+// ---- work decomposition ---------------------------------------------------------------------
+
+// Vote items for segments given as (n_cells, n_corr) pairs: cell blocks of kCellsPerBlock,
+// correspondence chunks chosen so the launch has >= ~16 waves of equal-cost blocks.
+void build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
+                      int slots, std::vector<rv::VoteItem>& items) {
+  items.clear();
+  double work = 0;
+  for (size_t s = 0; s < ncell.size(); ++s) {
+    int64_t cb = (ncell[s] + rv::kCellsPerBlock - 1) / rv::kCellsPerBlock;
+    work += (double)cb * (double)pad4(ncorr[s]);
+  }
+  int64_t chunk = (int64_t)std::ceil(work / ((double)slots * 16.0));
+  chunk = std::max<int64_t>(chunk, rv::kTile);
+  chunk = std::min<int64_t>(chunk, 1 << 16);
+  chunk = (chunk + rv::kTile - 1) / rv::kTile * rv::kTile;
+  for (size_t s = 0; s < ncell.size(); ++s) {
+    const int64_t n4 = pad4(ncorr[s]);
+    if (ncell[s] == 0 || n4 == 0) continue;
+    const int64_t cb = (ncell[s] + rv::kCellsPerBlock - 1) / rv::kCellsPerBlock;
+    const int64_t per = (ncell[s] + cb - 1) / cb;  // balanced cells per block
+    for (int64_t b = 0; b < cb; ++b) {
+      const int64_t c0 = b * per, nc = std::min(per, ncell[s] - c0);
+      if (nc <= 0) continue;
+      for (int64_t i0 = 0; i0 < n4; i0 += chunk)
+        items.push_back({(int32_t)s, (int32_t)c0, (int32_t)nc, (int32_t)i0,
+                         (int32_t)std::min(chunk, n4 - i0)});
+    }
+  }
+}
+
+void build_exact_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
+                       std::vector<rv::VoteItem>& items) {
+  items.clear();
+  const int64_t chunk = 1 << 16;
+  for (size_t s = 0; s < ncell.size(); ++s)
+    for (int64_t c = 0; c < ncell[s]; ++c)
+      for (int64_t i0 = 0; i0 < ncorr[s]; i0 += chunk)
+        items.push_back({(int32_t)s, (int32_t)c, 1, (int32_t)i0,
+                         (int32_t)std::min(chunk, ncorr[s] - i0)});
+}
+
+// ---- K1 for P problems ----------------------------------------------------------------------
+int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
+              std::vector<int64_t>& koff_out) {
+  koff_out.assign(P + 1, 0);
+  for (int32_t p = 0; p < P; ++p) koff_out[p + 1] = koff_out[p] + pad4(offsets[p + 1] - offsets[p]);
+  const int64_t total = koff_out[P];
+  if (total > ctx->stride) {
+    ctx->stride = pad4(total);
+    RV_CUDA(ctx->k9.ensure((size_t)9 * ctx->stride), "allocating K table");
+  }
+  RV_CUDA(ctx->rows.ensure(P + 1), "allocating offsets");
+  RV_CUDA(ctx->koffs.ensure(P + 1), "allocating offsets");
+  RV_CUDA(ctx->bad.ensure(1), "allocating flag");
+  RV_CUDA(ctx->up.ensure(2 * (P + 1) * sizeof(int64_t) + 1024), "allocating staging");
+  ctx->up.reset();
+  int64_t* hrows = ctx->up.take<int64_t>(P + 1);
+  int64_t* hk = ctx->up.take<int64_t>(P + 1);
+  std::memcpy(hrows, offsets, (P + 1) * sizeof(int64_t));
+  std::memcpy(hk, koff_out.data(), (P + 1) * sizeof(int64_t));
+  RV_CUDA(cudaMemcpyAsync(ctx->rows.p, hrows, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
+          "copying offsets");
+  RV_CUDA(cudaMemcpyAsync(ctx->koffs.p, hk, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
+          "copying offsets");
+  RV_CUDA(cudaMemsetAsync(ctx->bad.p, 0xff, sizeof(unsigned long long), ctx->stream), "memset");
+  rv::launch_setup(x, y, ctx->rows.p, ctx->koffs.p, P, total, ctx->k9.p, ctx->stride, ctx->bad.p,
+                   ctx->stream);
+  ctx->launches += 1;
+  RV_CUDA(cudaGetLastError(), "launching rv_setup");
+  return RV_OK;
+}
+
+int check_bad(rv_ctx* ctx) {
+  unsigned long long b = 0;
+  RV_CUDA(cudaMemcpyAsync(&b, ctx->bad.p, sizeof(b), cudaMemcpyDeviceToHost, ctx->stream),
+          "reading data flag");
+  RV_CUDA(cudaStreamSynchronize(ctx->stream), "rv_setup");
+  if (b != ~0ull)
+    return ctx->fail(RV_EDATA, "correspondence row %llu has a zero-length or non-finite vector", b);
+  return RV_OK;
+}
+
+// ---- one planner request (single problem), sharded over ranks --------------------------------
+// Counts land in cnt_a/cnt_b (HOST, m entries each).
+int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps, int32_t B,
+                 int32_t mode, int64_t m, const uint32_t* lins, uint32_t* cnt_a, uint32_t* cnt_b) {
+  const int W = ctx->effective_world();
+  const int64_t chunk = (m + W - 1) / W;
+  const int64_t per_rank = 2 * chunk;  // [a | b]
+  // ranks evaluated by this process
+  int r_lo = 0, r_hi = W;
+  if (ctx->cfg.world > 1) { r_lo = ctx->cfg.rank; r_hi = r_lo + 1; }
+  const int nr = r_hi - r_lo;
+
+  RV_CUDA(ctx->lins.ensure(std::max<int64_t>(1, chunk * nr)), "allocating block list");
+  // gathered counts [W][2*chunk] + (world>1) local [2*chunk]
+  const size_t cnt_need = (size_t)per_rank * W + (ctx->cfg.world > 1 ? per_rank : 0) + 1;
+  RV_CUDA(ctx->cnt.ensure(cnt_need), "allocating counts");
+  uint32_t* gathered = ctx->cnt.p;
+  uint32_t* local = ctx->cfg.world > 1 ? ctx->cnt.p + per_rank * W : nullptr;
+
+  std::vector<int64_t> ncell, ncorr;
+  std::vector<rv::VoteSeg> segs;
+  for (int r = r_lo; r < r_hi; ++r) {
+    int64_t b, e;
+    rv_shard_range(m, r, W, &b, &e);
+    rv::VoteSeg sg{};
+    sg.lins = ctx->lins.p + (int64_t)(r - r_lo) * chunk;
+    uint32_t* tgt = local ? local : gathered + (int64_t)r * per_rank;
+    sg.cnt_a = tgt;
+    sg.cnt_b = tgt + chunk;
+    sg.koff = 0;
+    sg.row = 0;
+    sg.n = (int32_t)n;
+    sg.B = B;
+    sg.eps = eps;
+    segs.push_back(sg);
+    ncell.push_back(e - b);
+    ncorr.push_back(n);
+  }
+  std::vector<rv::VoteItem> items;
+  if (mode == RV_MODE_EXACT) build_exact_items(ncell, ncorr, items);
+  else build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items);
+
+  RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
+  RV_CUDA(ctx->vitems.ensure(std::max<size_t>(1, items.size())), "allocating items");
+  RV_CUDA(ctx->up.ensure(chunk * nr * 4 + segs.size() * sizeof(rv::VoteSeg) +
+                         items.size() * sizeof(rv::VoteItem) + 4096),
+          "allocating staging");
+  RV_CUDA(ctx->down.ensure(per_rank * W * 4 + 256), "allocating staging");
+  ctx->up.reset();
+  uint32_t* hl = ctx->up.take<uint32_t>(std::max<int64_t>(1, chunk * nr));
+  for (int r = r_lo; r < r_hi; ++r) {
+    int64_t b, e;
+    rv_shard_range(m, r, W, &b, &e);
+    std::memcpy(hl + (int64_t)(r - r_lo) * chunk, lins + b, (e - b) * 4);
+  }
+  rv::VoteSeg* hs = ctx->up.take<rv::VoteSeg>(segs.size());
+  std::memcpy(hs, segs.data(), segs.size() * sizeof(rv::VoteSeg));
+  rv::VoteItem* hi = ctx->up.take<rv::VoteItem>(std::max<size_t>(1, items.size()));
+  if (!items.empty()) std::memcpy(hi, items.data(), items.size() * sizeof(rv::VoteItem));
+
+  cudaStream_t s = ctx->stream;
+  RV_CUDA(cudaMemcpyAsync(ctx->lins.p, hl, chunk * nr * 4, cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemcpyAsync(ctx->vsegs.p, hs, segs.size() * sizeof(rv::VoteSeg),
+                          cudaMemcpyHostToDevice, s), "H2D");
+  if (!items.empty())
+    RV_CUDA(cudaMemcpyAsync(ctx->vitems.p, hi, items.size() * sizeof(rv::VoteItem),
+                            cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemsetAsync(local ? local : gathered, 0,
+                          (local ? per_rank : per_rank * W) * sizeof(uint32_t), s), "memset");
+  if (mode == RV_MODE_EXACT) {
+    rv::launch_exact(ctx->k9.p, ctx->stride, x, y, ctx->vsegs.p, ctx->vitems.p,
+                     (int32_t)items.size(), ctx->cfg.guard, s);
+  } else {
+    RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
+    rv::launch_vote(mode, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
+                    (int32_t)items.size(), ctx->cfg.guard, s);
+    RV_CUDA(cudaEventRecord(ctx->evv1, s), "event");
+    for (int64_t c : ncell) ctx->vote_pairs += (uint64_t)c * (uint64_t)n;
+    ctx->vote_launches += 1;
+  }
+  ctx->launches += items.empty() ? 0 : 1;
+  RV_CUDA(cudaGetLastError(), "launching the vote kernel");
+  if (ctx->cfg.world > 1) {
+    ncclResult_t nr_ = nccl().AllGather(local, gathered, (size_t)per_rank, ncclUint32, ctx->comm, s);
+    if (nr_ != ncclSuccess)
+      return ctx->fail(RV_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(nr_));
+  }
+  ctx->down.reset();
+  uint32_t* hc = ctx->down.take<uint32_t>(per_rank * W);
+  RV_CUDA(cudaMemcpyAsync(hc, gathered, per_rank * W * 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "vote");
+  if (mode != RV_MODE_EXACT && !items.empty()) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->evv0, ctx->evv1);
+    ctx->vote_ms += ms;
+  }
+  for (int r = 0; r < W; ++r) {
+    int64_t b, e;
+    rv_shard_range(m, r, W, &b, &e);
+    std::memcpy(cnt_a + b, hc + (int64_t)r * per_rank, (e - b) * 4);
+    if (cnt_b) std::memcpy(cnt_b + b, hc + (int64_t)r * per_rank + chunk, (e - b) * 4);
+  }
+  return RV_OK;
+}
+
+// ---- refinement (K6/K7) for P problems --------------------------------------------------------
+// qs0: HOST [P][4] start rotations; writes q/flags/ninl (HOST) and masks (DEVICE, optional).
+int run_refine(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
+               const int32_t* prob_ids /* which problems (indices into offsets) */, double eps,
+               const double* qs0, int32_t rounds, const int64_t* mask_words, uint32_t* masks,
+               double* q_out, int32_t* flags_out, uint32_t* ninl_out) {
+  std::vector<rv::RefSeg> segs(P);
+  std::vector<rv::RefItem> items;
+  const double tau = std::cos(eps);
+  for (int32_t s = 0; s < P; ++s) {
+    const int32_t p = prob_ids ? prob_ids[s] : s;
+    const int64_t n = offsets[p + 1] - offsets[p];
+    segs[s].row = offsets[p];
+    segs[s].mask_word = mask_words ? mask_words[s] : 0;
+    segs[s].n = (int32_t)n;
+    segs[s].tau = tau;
+    segs[s].pad = 0;
+    segs[s].item_begin = (int32_t)items.size();
+    for (int64_t r0 = 0; r0 < n; r0 += rv::kRefRowsPerItem)
+      items.push_back({s, (int32_t)r0, (int32_t)std::min<int64_t>(rv::kRefRowsPerItem, n - r0)});
+    segs[s].item_end = (int32_t)items.size();
+  }
+  RV_CUDA(ctx->rsegs.ensure(P), "allocating");
+  RV_CUDA(ctx->ritems.ensure(items.size()), "allocating");
+  RV_CUDA(ctx->partials.ensure(items.size() * 10), "allocating");
+  RV_CUDA(ctx->qs.ensure((size_t)P * 4), "allocating");
+  RV_CUDA(ctx->flags.ensure(P), "allocating");
+  RV_CUDA(ctx->ninl.ensure(P), "allocating");
+  RV_CUDA(ctx->up.ensure(P * sizeof(rv::RefSeg) + items.size() * sizeof(rv::RefItem) + P * 32 + 4096),
+          "allocating staging");
+  RV_CUDA(ctx->down.ensure(P * (32 + 8) + 4096), "allocating staging");
+  ctx->up.reset();
+  rv::RefSeg* hs = ctx->up.take<rv::RefSeg>(P);
+  std::memcpy(hs, segs.data(), P * sizeof(rv::RefSeg));
+  rv::RefItem* hi = ctx->up.take<rv::RefItem>(items.size());
+  std::memcpy(hi, items.data(), items.size() * sizeof(rv::RefItem));
+  double* hq = ctx->up.take<double>((size_t)P * 4);
+  std::memcpy(hq, qs0, (size_t)P * 4 * sizeof(double));
+  cudaStream_t s = ctx->stream;
+  RV_CUDA(cudaMemcpyAsync(ctx->rsegs.p, hs, P * sizeof(rv::RefSeg), cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemcpyAsync(ctx->ritems.p, hi, items.size() * sizeof(rv::RefItem),
+                          cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemcpyAsync(ctx->qs.p, hq, (size_t)P * 32, cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemsetAsync(ctx->flags.p, 0, P * sizeof(int32_t), s), "memset");
+  for (int r = 0; r < rounds; ++r) {
+    rv::launch_inliers(x, y, ctx->rsegs.p, ctx->ritems.p, (int32_t)items.size(), ctx->qs.p, nullptr,
+                       ctx->partials.p, s);
+    rv::launch_eig(ctx->rsegs.p, P, ctx->partials.p, ctx->qs.p, ctx->flags.p, ctx->ninl.p, 0, s);
+  }
+  rv::launch_inliers(x, y, ctx->rsegs.p, ctx->ritems.p, (int32_t)items.size(), ctx->qs.p, masks,
+                     ctx->partials.p, s);
+  rv::launch_eig(ctx->rsegs.p, P, ctx->partials.p, ctx->qs.p, ctx->flags.p, ctx->ninl.p, 1, s);
+  ctx->launches += 2 * rounds + 2;
+  RV_CUDA(cudaGetLastError(), "launching refinement");
+  ctx->down.reset();
+  double* dq = ctx->down.take<double>((size_t)P * 4);
+  int32_t* df = ctx->down.take<int32_t>(P);
+  uint32_t* dn = ctx->down.take<uint32_t>(P);
+  RV_CUDA(cudaMemcpyAsync(dq, ctx->qs.p, (size_t)P * 32, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(df, ctx->flags.p, P * 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(dn, ctx->ninl.p, P * 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "refinement");
+  std::memcpy(q_out, dq, (size_t)P * 32);
+  for (int32_t p = 0; p < P; ++p) flags_out[p] = df[p] & (RV_REFINED | RV_DEGENERATE);
+  std::memcpy(ninl_out, dn, P * 4);
+  return RV_OK;
+}
+
+void canonicalize(double q[4]) {
+  bool flip;
+  if (q[3] < -1e-15) flip = false;
+  else if (q[3] > 1e-15) flip = true;
+  else {
+    flip = false;
+    for (int a = 0; a < 3; ++a)
+      if (q[a] != 0.0) { flip = q[a] < 0.0; break; }
+  }
+  if (flip)
+    for (int a = 0; a < 4; ++a) q[a] = -q[a];
+}
+
+void canonical_cell_quat(int32_t B, uint32_t lin, double q[4]) {
+  int32_t i, j, k;
+  rv::lin_to_ijk(lin, B, i, j, k);
+  rv::cell_quat(B, i, j, k, q);
+  canonicalize(q);
+}
+
+int validate_common(rv_ctx* ctx, const void* x, const void* y, double eps, int32_t levels) {
+  if (!ctx) return RV_EINVAL;
+  if (!x || !y) return ctx->fail(RV_EINVAL, "x and y must be non-null");
+  if (!(eps > 0.0) || !(eps < 3.141592653589793))
+    return ctx->fail(RV_EINVAL, "eps must lie in (0, pi), got %g", eps);
+  if (levels < 0 || levels > (int32_t)ctx->chain.size())
+    return ctx->fail(RV_EINVAL, "levels must lie in [0, %d], got %d", (int)ctx->chain.size(), levels);
+  return RV_OK;
+}
+
+void fill_result(const rv_plan_result& pr, rv_result* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->votes = pr.votes;
+  int32_t i, j, k;
+  rv::lin_to_ijk(pr.lin, pr.B, i, j, k);
+  out->cell[0] = i; out->cell[1] = j; out->cell[2] = k;
+  out->B = pr.B;
+  out->n_tied = pr.n_tied;
+  out->pair_votes = pr.pair_votes;
+  out->cells_evaluated = pr.cells_evaluated;
+  out->lb_star = pr.lb_star;
+  out->n_rechecked = pr.n_rechecked;
+  out->n_phases = std::min(pr.n_phases, (int32_t)RV_MAX_PHASES);
+  for (int p = 0; p < out->n_phases; ++p) out->cells_per_phase[p] = pr.cells_per_phase[p];
+  if (pr.n_rechecked > 0) out->flags |= RV_RECHECKED;
+  canonical_cell_quat(pr.B, pr.lin, out->q_cell);
+}
+
+int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps, int32_t levels,
+               rv_result* out, uint32_t* mask) {
+  if (int rc = validate_common(ctx, x, y, eps, levels)) return rc;
+  if (!out) return ctx->fail(RV_EINVAL, "out must be non-null");
+  if (n < 2) return ctx->fail(RV_EINVAL, "n must be >= 2 (got %lld)", (long long)n);
+  if (n > ctx->cfg.max_n)
+    return ctx->fail(RV_EINVAL, "n = %lld exceeds max_n = %lld", (long long)n,
+                     (long long)ctx->cfg.max_n);
+  cudaStream_t s = ctx->stream;
+  RV_CUDA(cudaEventRecord(ctx->ev0, s), "event");
+  const int64_t offs[2] = {0, n};
+  std::vector<int64_t> koff;
+  if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
+  if (int rc = check_bad(ctx)) return rc;
+
+  rv_plan* plan = nullptr;
+  if (rv_plan_create(ctx->chain.data(), (int32_t)ctx->chain.size(), levels, n, eps,
+                     (double)ctx->cfg.guard, &plan) != 0)
+    return ctx->fail(RV_EINVAL, "invalid search plan");
+  std::vector<uint32_t> ca, cb;
+  int32_t B, mode;
+  int64_t m;
+  const uint32_t* lins;
+  int rc = RV_OK;
+  while (rv_plan_request(plan, &B, &mode, &m, &lins)) {
+    ca.assign(m, 0);
+    cb.assign(m, 0);
+    rc = eval_request(ctx, x, y, n, eps, B, mode, m, lins, ca.data(), cb.data());
+    if (rc) break;
+    if (rv_plan_feed(plan, ca.data(), cb.data()) != 0) {
+      rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
+      break;
+    }
+  }
+  rv_plan_result pr{};
+  if (!rc) rv_plan_get_result(plan, &pr);
+  rv_plan_destroy(plan);
+  if (rc) return rc;
+
+  fill_result(pr, out);
+  int32_t fl = 0;
+  uint32_t ni = 0;
+  const int32_t pid = 0;
+  const int64_t mw = 0;
+  rc = run_refine(ctx, x, y, offs, 1, &pid, eps, out->q_cell, ctx->cfg.refine_rounds, &mw, mask,
+                  out->q, &fl, &ni);
+  if (rc) return rc;
+  out->flags |= fl;
+  out->n_inliers = ni;
+  RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
+  RV_CUDA(cudaEventSynchronize(ctx->ev1), "event");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  out->ms = ms;
+  out->vote_ms = ctx->vote_ms;
+  out->vote_pairs = ctx->vote_pairs;
+  out->launches = ctx->launches;
+  out->vote_launches = ctx->vote_launches;
+  return RV_OK;
+}
+
+
+// ---- batched: one launch per mode covers every active problem's request ----------------------
+struct BatchReq {
+  int32_t prob;        // local problem index
+  int32_t B, mode;
+  int64_t m;
+  const uint32_t* lins;
+};
+
+int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
+               const std::vector<int64_t>& koff, double eps, int32_t mode,
+               const std::vector<BatchReq>& reqs, std::vector<std::vector<uint32_t>>& ca,
+               std::vector<std::vector<uint32_t>>& cb) {
+  if (reqs.empty()) return RV_OK;
+  int64_t total = 0;
+  for (const BatchReq& r : reqs) total += r.m;
+  RV_CUDA(ctx->lins.ensure(total), "allocating block list");
+  RV_CUDA(ctx->cnt.ensure(2 * total), "allocating counts");
+  std::vector<int64_t> ncell, ncorr;
+  std::vector<rv::VoteSeg> segs;
+  int64_t off = 0;
+  for (const BatchReq& r : reqs) {
+    rv::VoteSeg sg{};
+    sg.lins = ctx->lins.p + off;
+    sg.cnt_a = ctx->cnt.p + off;
+    sg.cnt_b = ctx->cnt.p + total + off;
+    sg.koff = koff[r.prob];
+    sg.row = rows[r.prob];
+    sg.n = (int32_t)(rows[r.prob + 1] - rows[r.prob]);
+    sg.B = r.B;
+    sg.eps = eps;
+    segs.push_back(sg);
+    ncell.push_back(r.m);
+    ncorr.push_back(sg.n);
+    off += r.m;
+  }
+  std::vector<rv::VoteItem> items;
+  if (mode == RV_MODE_EXACT) build_exact_items(ncell, ncorr, items);
+  else build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items);
+  RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
+  RV_CUDA(ctx->vitems.ensure(std::max<size_t>(1, items.size())), "allocating items");
+  RV_CUDA(ctx->up.ensure(total * 4 + segs.size() * sizeof(rv::VoteSeg) +
+                         items.size() * sizeof(rv::VoteItem) + 4096), "allocating staging");
+  RV_CUDA(ctx->down.ensure(2 * total * 4 + 256), "allocating staging");
+  ctx->up.reset();
+  uint32_t* hl = ctx->up.take<uint32_t>(total);
+  off = 0;
+  for (const BatchReq& r : reqs) {
+    std::memcpy(hl + off, r.lins, r.m * 4);
+    off += r.m;
+  }
+  rv::VoteSeg* hs = ctx->up.take<rv::VoteSeg>(segs.size());
+  std::memcpy(hs, segs.data(), segs.size() * sizeof(rv::VoteSeg));
+  rv::VoteItem* hi = ctx->up.take<rv::VoteItem>(std::max<size_t>(1, items.size()));
+  if (!items.empty()) std::memcpy(hi, items.data(), items.size() * sizeof(rv::VoteItem));
+  cudaStream_t s = ctx->stream;
+  RV_CUDA(cudaMemcpyAsync(ctx->lins.p, hl, total * 4, cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemcpyAsync(ctx->vsegs.p, hs, segs.size() * sizeof(rv::VoteSeg),
+                          cudaMemcpyHostToDevice, s), "H2D");
+  if (!items.empty())
+    RV_CUDA(cudaMemcpyAsync(ctx->vitems.p, hi, items.size() * sizeof(rv::VoteItem),
+                            cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemsetAsync(ctx->cnt.p, 0, 2 * total * 4, s), "memset");
+  if (mode == RV_MODE_EXACT) {
+    rv::launch_exact(ctx->k9.p, ctx->stride, x, y, ctx->vsegs.p, ctx->vitems.p,
+                     (int32_t)items.size(), ctx->cfg.guard, s);
+  } else {
+    RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
+    rv::launch_vote(mode, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
+                    (int32_t)items.size(), ctx->cfg.guard, s);
+    RV_CUDA(cudaEventRecord(ctx->evv1, s), "event");
+    for (size_t q = 0; q < ncell.size(); ++q) ctx->vote_pairs += (uint64_t)ncell[q] * ncorr[q];
+    ctx->vote_launches += 1;
+  }
+  ctx->launches += items.empty() ? 0 : 1;
+  RV_CUDA(cudaGetLastError(), "launching the vote kernel");
+  ctx->down.reset();
+  uint32_t* hc = ctx->down.take<uint32_t>(2 * total);
+  RV_CUDA(cudaMemcpyAsync(hc, ctx->cnt.p, 2 * total * 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "batched vote");
+  if (mode != RV_MODE_EXACT && !items.empty()) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->evv0, ctx->evv1);
+    ctx->vote_ms += ms;
+  }
+  off = 0;
+  for (const BatchReq& r : reqs) {
+    ca[r.prob].assign(hc + off, hc + off + r.m);
+    cb[r.prob].assign(hc + total + off, hc + total + off + r.m);
+    off += r.m;
+  }
+  return RV_OK;
+}
+
+int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets,
+                       int32_t P, double eps, int32_t levels, rv_result* out, uint32_t* masks) {
+  if (int rc = validate_common(ctx, x, y, eps, levels)) return rc;
+  if (!offsets || !out) return ctx->fail(RV_EINVAL, "offsets and out must be non-null");
+  if (P < 1 || P > ctx->cfg.max_problems)
+    return ctx->fail(RV_EINVAL, "P = %d outside [1, max_problems = %d]", P, ctx->cfg.max_problems);
+  if (offsets[0] != 0) return ctx->fail(RV_EINVAL, "offsets[0] must be 0");
+  for (int32_t p = 0; p < P; ++p)
+    if (offsets[p + 1] - offsets[p] < 2)
+      return ctx->fail(RV_EINVAL, "problem %d has fewer than 2 correspondences", p);
+  if (offsets[P] > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "total rows exceed max_n");
+  cudaStream_t s = ctx->stream;
+  RV_CUDA(cudaEventRecord(ctx->ev0, s), "event");
+  const int W = ctx->cfg.world;
+  int64_t pb, pe;
+  rv_shard_range(P, ctx->cfg.rank, W, &pb, &pe);
+  const int32_t PL = (int32_t)(pe - pb);
+  std::vector<rv_result> local(PL);
+  if (PL > 0) {
+    std::vector<int64_t> rows(offsets + pb, offsets + pe + 1), koff;
+    if (int rc = run_setup(ctx, x, y, rows.data(), PL, koff)) return rc;
+    if (int rc = check_bad(ctx)) return rc;
+    std::vector<rv_plan*> plans(PL, nullptr);
+    int rc = RV_OK;
+    for (int32_t p = 0; p < PL && !rc; ++p)
+      if (rv_plan_create(ctx->chain.data(), (int32_t)ctx->chain.size(), levels,
+                         rows[p + 1] - rows[p], eps, (double)ctx->cfg.guard, &plans[p]) != 0)
+        rc = ctx->fail(RV_EINVAL, "invalid search plan");
+    std::vector<std::vector<uint32_t>> ca(PL), cb(PL);
+    while (!rc) {
+      std::vector<BatchReq> by_mode[3];
+      bool any = false;
+      for (int32_t p = 0; p < PL; ++p) {
+        BatchReq r;
+        r.prob = p;
+        if (rv_plan_request(plans[p], &r.B, &r.mode, &r.m, &r.lins)) {
+          by_mode[r.mode].push_back(r);
+          any = true;
+        }
+      }
+      if (!any) break;
+      for (int md = 0; md < 3 && !rc; ++md) {
+        rc = eval_batch(ctx, x, y, rows, koff, eps, md, by_mode[md], ca, cb);
+        for (const BatchReq& r : by_mode[md])
+          if (!rc && rv_plan_feed(plans[r.prob], ca[r.prob].data(), cb[r.prob].data()) != 0)
+            rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
+      }
+    }
+    std::vector<double> q0((size_t)PL * 4), qf((size_t)PL * 4);
+    std::vector<int32_t> fl(PL), ids(PL);
+    std::vector<uint32_t> ni(PL);
+    std::vector<int64_t> mw(PL);
+    if (!rc) {
+      int64_t w = 0;
+      for (int64_t p = 0; p < pb; ++p) w += (offsets[p + 1] - offsets[p] + 31) / 32;
+      for (int32_t p = 0; p < PL; ++p) {
+        rv_plan_result pr{};
+        rv_plan_get_result(plans[p], &pr);
+        fill_result(pr, &local[p]);
+        std::memcpy(&q0[4 * p], local[p].q_cell, 32);
+        ids[p] = p;
+        mw[p] = w;
+        w += (rows[p + 1] - rows[p] + 31) / 32;
+      }
+    }
+    for (rv_plan* pl : plans) rv_plan_destroy(pl);
+    if (rc) return rc;
+    // rows are absolute: refine over the local offsets table
+    rc = run_refine(ctx, x, y, rows.data(), PL, ids.data(), eps, q0.data(), ctx->cfg.refine_rounds,
+                    mw.data(), masks, qf.data(), fl.data(), ni.data());
+    if (rc) return rc;
+    for (int32_t p = 0; p < PL; ++p) {
+      std::memcpy(local[p].q, &qf[4 * p], 32);
+      local[p].flags |= fl[p];
+      local[p].n_inliers = ni[p];
+    }
+  }
+  RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
+  RV_CUDA(cudaEventSynchronize(ctx->ev1), "event");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  for (rv_result& r : local) {
+    r.ms = ms;
+    r.vote_ms = ctx->vote_ms;
+    r.vote_pairs = ctx->vote_pairs;
+    r.launches = ctx->launches;
+    r.vote_launches = ctx->vote_launches;
+  }
+  if (W == 1) {
+    std::memcpy(out, local.data(), (size_t)P * sizeof(rv_result));
+    return RV_OK;
+  }
+  // all-gather the per-rank result slices (fixed-size slots of ceil(P/W) results)
+  const int64_t chunk = (P + W - 1) / W;
+  const size_t slot = (size_t)chunk * sizeof(rv_result);
+  RV_CUDA(ctx->gather.ensure(slot * (W + 1)), "allocating");
+  RV_CUDA(ctx->up.ensure(slot + 256), "allocating staging");
+  RV_CUDA(ctx->down.ensure(slot * W + 256), "allocating staging");
+  ctx->up.reset();
+  char* hu = ctx->up.take<char>(slot);
+  std::memset(hu, 0, slot);
+  if (PL > 0) std::memcpy(hu, local.data(), (size_t)PL * sizeof(rv_result));
+  char* mine = ctx->gather.p + slot * W;
+  RV_CUDA(cudaMemcpyAsync(mine, hu, slot, cudaMemcpyHostToDevice, s), "H2D");
+  ncclResult_t nr = nccl().AllGather(mine, ctx->gather.p, slot, ncclChar, ctx->comm, s);
+  if (nr != ncclSuccess) return ctx->fail(RV_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(nr));
+  ctx->down.reset();
+  char* hd = ctx->down.take<char>(slot * W);
+  RV_CUDA(cudaMemcpyAsync(hd, ctx->gather.p, slot * W, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "gather");
+  for (int r = 0; r < W; ++r) {
+    int64_t b, e;
+    rv_shard_range(P, r, W, &b, &e);
+    std::memcpy(out + b, hd + slot * r, (size_t)(e - b) * sizeof(rv_result));
+  }
+  return RV_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+extern "C" {
+
+void rot_vote_default_config(rv_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->device = 0;
+  cfg->rank = 0;
+  cfg->world = 1;
+  cfg->nccl_id = nullptr;
+  cfg->max_n = 1 << 20;
+  cfg->max_problems = 1;
+  cfg->chain_len = 0;
+  cfg->refine_rounds = 2;
+  cfg->guard = 1e-5f;
+  cfg->stream = nullptr;
+  cfg->emulate_world = 0;
+}
+
+int rot_vote_get_unique_id(void* id_out) {
+  if (!id_out) return RV_EINVAL;
+  NcclApi& a = nccl();
+  if (!a.ok) return RV_ENCCL;
+  ncclUniqueId id;
+  if (a.GetUniqueId(&id) != ncclSuccess) return RV_ENCCL;
+  std::memcpy(id_out, &id, sizeof(id));
+  return RV_OK;
+}
+
+int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
+  if (!out) return RV_EINVAL;
+  *out = nullptr;
+  if (!cfg) return RV_EINVAL;
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return RV_EINVAL;
+  if (cfg->world > 1 && (!cfg->nccl_id || cfg->emulate_world > 1)) return RV_EINVAL;
+  if (cfg->max_n < 2 || cfg->max_n > ((int64_t)1 << 31) - 4096) return RV_EINVAL;
+  if (cfg->max_problems < 1 || cfg->refine_rounds < 0 || !(cfg->guard >= 0.0f)) return RV_EINVAL;
+  if (cfg->chain_len < 0 || cfg->chain_len > RV_MAX_CHAIN) return RV_EINVAL;
+  rv_ctx* ctx = new rv_ctx();
+  ctx->cfg = *cfg;
+  if (cfg->chain_len == 0) ctx->chain.assign(kDefaultChain, kDefaultChain + 6);
+  else ctx->chain.assign(cfg->chain, cfg->chain + cfg->chain_len);
+  for (size_t l = 0; l < ctx->chain.size(); ++l) {
+    if (ctx->chain[l] < 1 || ctx->chain[l] > 1625 ||
+        (l > 0 && ctx->chain[l] % ctx->chain[l - 1] != 0)) {
+      delete ctx;
+      return RV_EINVAL;
+    }
+  }
+  ctx->stream = (cudaStream_t)cfg->stream;
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->evv0);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->evv1);
+  if (e == cudaSuccess) {
+    ctx->stride = pad4(cfg->max_n) + 64;
+    e = ctx->k9.ensure((size_t)9 * ctx->stride);
+  }
+  if (e == cudaSuccess) e = ctx->bad.ensure(1);
+  if (e == cudaSuccess) e = ctx->up.ensure(1 << 20);
+  if (e == cudaSuccess) e = ctx->down.ensure(1 << 20);
+  if (e != cudaSuccess) {
+    int code = e == cudaErrorMemoryAllocation ? RV_ENOMEM : RV_ECUDA;
+    rot_vote_destroy(ctx);
+    return code;
+  }
+  if (cfg->world > 1) {
+    NcclApi& a = nccl();
+    if (!a.ok) {
+      rot_vote_destroy(ctx);
+      return RV_ENCCL;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_id, sizeof(id));
+    if (a.CommInitRank(&ctx->comm, cfg->world, id, cfg->rank) != ncclSuccess) {
+      ctx->comm = nullptr;
+      rot_vote_destroy(ctx);
+      return RV_ENCCL;
+    }
+  }
+  *out = ctx;
+  return RV_OK;
+}
+
+void rot_vote_destroy(rv_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
+  ctx->k9.release(); ctx->lins.release(); ctx->cnt.release(); ctx->vsegs.release();
+  ctx->vitems.release(); ctx->rsegs.release(); ctx->ritems.release(); ctx->partials.release();
+  ctx->qs.release(); ctx->flags.release(); ctx->ninl.release(); ctx->rows.release();
+  ctx->koffs.release(); ctx->bad.release(); ctx->hx.release(); ctx->hy.release();
+  ctx->hmask.release(); ctx->gather.release();
+  ctx->up.release(); ctx->down.release();
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->evv0) cudaEventDestroy(ctx->evv0);
+  if (ctx->evv1) cudaEventDestroy(ctx->evv1);
+  delete ctx;
+}
+
+const char* rot_vote_last_error(const rv_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int rot_vote_solve(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                   int32_t levels, rv_result* out, uint32_t* inlier_mask) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  ctx->reset_counters();
+  return solve_impl(ctx, x, y, n, eps, levels, out, inlier_mask);
+}
+
+int rot_vote_solve_host(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                        int32_t levels, rv_result* out, uint32_t* inlier_mask) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  ctx->reset_counters();
+  if (int rc = validate_common(ctx, x, y, eps, levels)) return rc;
+  if (n < 2 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
+  RV_CUDA(ctx->hx.ensure(3 * n), "allocating");
+  RV_CUDA(ctx->hy.ensure(3 * n), "allocating");
+  const int64_t words = (n + 31) / 32;
+  if (inlier_mask) RV_CUDA(ctx->hmask.ensure(words), "allocating");
+  RV_CUDA(cudaMemcpyAsync(ctx->hx.p, x, 12 * n, cudaMemcpyHostToDevice, ctx->stream), "H2D x");
+  RV_CUDA(cudaMemcpyAsync(ctx->hy.p, y, 12 * n, cudaMemcpyHostToDevice, ctx->stream), "H2D y");
+  int rc = solve_impl(ctx, ctx->hx.p, ctx->hy.p, n, eps, levels, out,
+                      inlier_mask ? ctx->hmask.p : nullptr);
+  if (rc) return rc;
+  if (inlier_mask) {
+    RV_CUDA(cudaMemcpyAsync(inlier_mask, ctx->hmask.p, words * 4, cudaMemcpyDeviceToHost,
+                            ctx->stream), "D2H mask");
+    RV_CUDA(cudaStreamSynchronize(ctx->stream), "D2H mask");
+  }
+  return RV_OK;
+}
+
+int rot_vote_solve_batched(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets,
+                           int32_t P, double eps, int32_t levels, rv_result* out, uint32_t* masks) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  ctx->reset_counters();
+  return solve_batched_impl(ctx, x, y, offsets, P, eps, levels, out, masks);
+}
+
+int rot_vote_setup(rv_ctx* ctx, const float* x, const float* y, int64_t n, float* k_out) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  if (!x || !y || !k_out) return ctx->fail(RV_EINVAL, "null pointer");
+  if (n < 1 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
+  const int64_t offs[2] = {0, n};
+  std::vector<int64_t> koff;
+  if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
+  for (int j = 0; j < 9; ++j)
+    RV_CUDA(cudaMemcpyAsync(k_out + (int64_t)j * n, ctx->k9.p + (int64_t)j * ctx->stride, n * 4,
+                            cudaMemcpyDeviceToDevice, ctx->stream), "copy K");
+  return check_bad(ctx);
+}
+
+int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t B,
+                         const uint32_t* lins, int64_t m, double eps, int32_t mode, uint32_t* cnt_a,
+                         uint32_t* cnt_b) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  if (int rc = validate_common(ctx, x, y, eps, 0)) return rc;
+  if (!lins || !cnt_a || (mode == RV_MODE_FINAL && !cnt_b) || m < 0)
+    return ctx->fail(RV_EINVAL, "null pointer");
+  if (mode < RV_MODE_BOUND || mode > RV_MODE_EXACT) return ctx->fail(RV_EINVAL, "bad mode");
+  if (B < 1 || B > 1625) return ctx->fail(RV_EINVAL, "bad B");
+  if (n < 1 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
+  if (m == 0) return RV_OK;
+  const int64_t offs[2] = {0, n};
+  std::vector<int64_t> koff;
+  if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
+  if (int rc = check_bad(ctx)) return rc;
+  std::vector<uint32_t> hl(m), ha(m), hb(m);
+  RV_CUDA(cudaMemcpyAsync(hl.data(), lins, m * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  RV_CUDA(cudaStreamSynchronize(ctx->stream), "D2H");
+  if (int rc = eval_request(ctx, x, y, n, eps, B, mode, m, hl.data(), ha.data(), hb.data()))
+    return rc;
+  RV_CUDA(cudaMemcpyAsync(cnt_a, ha.data(), m * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  if (mode == RV_MODE_FINAL)
+    RV_CUDA(cudaMemcpyAsync(cnt_b, hb.data(), m * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  RV_CUDA(cudaStreamSynchronize(ctx->stream), "H2D");
+  return RV_OK;
+}
+
+int rot_vote_refine(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                    const double* q0, int32_t rounds, double* q_out, int32_t* flags,
+                    uint32_t* n_inliers, uint32_t* mask) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  if (int rc = validate_common(ctx, x, y, eps, 0)) return rc;
+  if (!q0 || !q_out || rounds < 0) return ctx->fail(RV_EINVAL, "bad arguments");
+  if (n < 1 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
+  double q[4];
+  const double nq = std::sqrt(q0[0] * q0[0] + q0[1] * q0[1] + q0[2] * q0[2] + q0[3] * q0[3]);
+  if (!(nq > 0.0)) return ctx->fail(RV_EINVAL, "q0 must be nonzero");
+  for (int a = 0; a < 4; ++a) q[a] = q0[a] / nq;
+  canonicalize(q);
+  const int64_t offs[2] = {0, n};
+  const int32_t pid = 0;
+  const int64_t mw = 0;
+  int32_t fl = 0;
+  uint32_t ni = 0;
+  if (int rc = run_refine(ctx, x, y, offs, 1, &pid, eps, q, rounds, &mw, mask, q_out, &fl, &ni))
+    return rc;
+  if (flags) *flags = fl;
+  if (n_inliers) *n_inliers = ni;
+  return RV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,503 @@
+// rv_kernels.cu -- librotvote's hand-written sm_100a kernels.
+//
+//   K1 rv_setup    a1  normalise + 9-entry traceless quadratic form K_i (fp64 -> fp32 SoA)
+//   K3 rv_vote     a3  (cells x 9)·(9 x N) contraction on the FP32 pipe (FFMA2), thresholded
+//                      and counted in registers; K tiles staged in shared memory by the TMA
+//                      bulk-copy engine (cp.async.bulk + mbarrier), reused by 1024 blocks
+//   K5 rv_exact    a5  exact count: fp32 vote + fp64 recheck inside the guard band
+//   K6 rv_inliers  a6  fp64 inlier test, ballot -> mask words, partial sums of K over inliers
+//   K7 rv_eig      a6  fixed-order reduction + 4x4 cyclic Jacobi (fp64), top eigenvector
+//
+// Citations: P:n = PAPER.md line n.  The vote statistic s_i(q) = y^T R(q) x = q^T K_i q
+// (Appendix A) with K_i traceless, so 9 numbers per correspondence suffice:
+//   s = phi(q) . k,  phi = [q0²-q3², q1²-q3², q2²-q3², 2q0q1, 2q0q2, 2q0q3, 2q1q2, 2q1q3, 2q2q3].
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/rotvote.h"
+#include "rv_geom.h"
+#include "rv_kernels.h"
+
+namespace rv {
+
+// ------------------------------------------------------------------------------------------
+// K1 setup
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) rv_setup_kernel(const float* __restrict__ x,
+                                                       const float* __restrict__ y,
+                                                       const int64_t* __restrict__ rows,
+                                                       const int64_t* __restrict__ koffs,
+                                                       int32_t P, int64_t total_pad,
+                                                       float* __restrict__ k9, int64_t stride,
+                                                       unsigned long long* bad) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total_pad;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    // problem containing padded index g (binary search over koffs)
+    int32_t lo = 0, hi = P;
+    while (hi - lo > 1) {
+      int32_t mid = (lo + hi) >> 1;
+      if (koffs[mid] <= g) lo = mid; else hi = mid;
+    }
+    const int64_t i = g - koffs[lo];
+    const int64_t n = rows[lo + 1] - rows[lo];
+    double k[9];
+    if (i < n) {
+      const int64_t r = rows[lo] + i;
+      double a[3] = {x[3 * r], x[3 * r + 1], x[3 * r + 2]};
+      double b[3] = {y[3 * r], y[3 * r + 1], y[3 * r + 2]};
+      double na = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+      double nb = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+      if (!(na > 0.0) || !(nb > 0.0) || !isfinite(na) || !isfinite(nb)) {
+        atomicMin(bad, (unsigned long long)r);
+        na = nb = 1.0;
+      }
+      const double ia = 1.0 / na, ib = 1.0 / nb;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { a[c] *= ia; b[c] *= ib; }
+      k9_of(a, b, k);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 9; ++j) k[j] = 0.0;  // padding: s = 0 for every q
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) k9[j * stride + g] = (float)k[j];
+  }
+}
+
+void launch_setup(const float* x, const float* y, const int64_t* rows, const int64_t* koffs,
+                  int32_t P, int64_t total_pad, float* k9, int64_t stride,
+                  unsigned long long* bad, cudaStream_t s) {
+  int64_t blocks = (total_pad + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  rv_setup_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, y, rows, koffs, P, total_pad, k9, stride,
+                                                   bad);
+}
+
+// ------------------------------------------------------------------------------------------
+// TMA bulk-copy + mbarrier helpers (PTX, sm_90+ / sm_100a)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+__device__ __forceinline__ uint32_t sign_bit(float v) { return __float_as_uint(v) >> 31; }
+
+// ------------------------------------------------------------------------------------------
+// K3 vote
+// ------------------------------------------------------------------------------------------
+// Each thread owns kCellsPerThread blocks (cells): phi(q_c) lives in registers duplicated as
+// float2 so that one FFMA2 evaluates the same cell against two correspondences.  All threads
+// of the CTA stream the same K tile from shared memory (warp-broadcast LDS.128 of four
+// consecutive correspondences per row).  The threshold is folded into the accumulator's
+// initial value (s - t), and the count is the sign bit: cnt = processed - #negatives.
+template <int MODE>
+__global__ void __launch_bounds__(kVoteThreads, 2)
+    rv_vote_kernel(const float* __restrict__ k9, int64_t stride, const VoteSeg* __restrict__ segs,
+                   const VoteItem* __restrict__ items, float guard) {
+  __shared__ __align__(128) float sK[kStages][9][kTile];
+  __shared__ __align__(8) uint64_t full[kStages];
+
+  const VoteItem it = items[blockIdx.x];
+  const VoteSeg& sg = segs[it.seg];
+  const int tid = threadIdx.x;
+
+  float2 phi[kCellsPerThread][9];
+  float init[kCellsPerThread];
+  {
+    const int32_t B = sg.B;
+    const double tau = cos(sg.eps);
+#pragma unroll
+    for (int c = 0; c < kCellsPerThread; ++c) {
+      int e = tid + c * kVoteThreads;
+      if (e >= it.ncell) e = 0;  // inactive slot: recompute cell 0, never stored
+      const uint32_t lin = sg.lins[it.cell0 + e];
+      int32_t i, j, k;
+      lin_to_ijk(lin, B, i, j, k);
+      double q[4], f[9];
+      cell_quat(B, i, j, k, q);
+      phi9(q, f);
+#pragma unroll
+      for (int t = 0; t < 9; ++t) phi[c][t] = make_float2((float)f[t], (float)f[t]);
+      double thr = (MODE == RV_MODE_BOUND) ? bound_threshold(B, i, j, k, sg.eps) - guard
+                                           : tau - guard;
+      init[c] = (float)(-thr);
+    }
+  }
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int ntiles = (it.ni + kTile - 1) / kTile;
+  const float* base = k9 + sg.koff + it.i0;
+  auto issue = [&](int tile) {
+    const int st = tile % kStages;
+    const int cnt = min(kTile, it.ni - tile * kTile);
+    const uint32_t bytes = (uint32_t)cnt * 4u;
+    mbar_expect_tx(&full[st], bytes * 9u);
+#pragma unroll
+    for (int j = 0; j < 9; ++j)
+      tma_bulk_g2s(&sK[st][j][0], base + j * stride + (int64_t)tile * kTile, bytes, &full[st]);
+  };
+  if (tid == 0)
+    for (int t = 0; t < kStages && t < ntiles; ++t) issue(t);
+
+  uint32_t neg_a[kCellsPerThread], neg_b[kCellsPerThread];
+#pragma unroll
+  for (int c = 0; c < kCellsPerThread; ++c) neg_a[c] = neg_b[c] = 0;
+  const float two_g = 2.0f * guard;
+
+  for (int tile = 0; tile < ntiles; ++tile) {
+    const int st = tile % kStages;
+    mbar_wait(&full[st], (uint32_t)((tile / kStages) & 1));
+    const int cnt = min(kTile, it.ni - tile * kTile);
+    const float* sk = &sK[st][0][0];
+#pragma unroll 1
+    for (int i = 0; i < cnt; i += 4) {
+      float4 kk[9];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) kk[j] = *reinterpret_cast<const float4*>(sk + j * kTile + i);
+#pragma unroll
+      for (int c = 0; c < kCellsPerThread; ++c) {
+        float2 lo = make_float2(init[c], init[c]);
+        float2 hi = lo;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+          lo = __ffma2_rn(phi[c][j], make_float2(kk[j].x, kk[j].y), lo);
+          hi = __ffma2_rn(phi[c][j], make_float2(kk[j].z, kk[j].w), hi);
+        }
+        neg_a[c] += sign_bit(lo.x) + sign_bit(lo.y) + sign_bit(hi.x) + sign_bit(hi.y);
+        if (MODE == RV_MODE_FINAL) {
+          neg_b[c] += sign_bit(lo.x - two_g) + sign_bit(lo.y - two_g) + sign_bit(hi.x - two_g) +
+                      sign_bit(hi.y - two_g);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with stage st
+    if (tid == 0 && tile + kStages < ntiles) issue(tile + kStages);
+  }
+
+  // epilogue: counts = processed - negatives - zero-padding rows that counted as >= 0
+  const int valid = max(0, min(it.ni, sg.n - it.i0));
+  const uint32_t pad = (uint32_t)(it.ni - valid);
+#pragma unroll
+  for (int c = 0; c < kCellsPerThread; ++c) {
+    const int e = tid + c * kVoteThreads;
+    if (e >= it.ncell) continue;
+    uint32_t ca = (uint32_t)it.ni - neg_a[c] - (sign_bit(init[c]) ? 0u : pad);
+    atomicAdd(&sg.cnt_a[it.cell0 + e], ca);
+    if (MODE == RV_MODE_FINAL) {
+      uint32_t cb = (uint32_t)it.ni - neg_b[c] - (sign_bit(init[c] - two_g) ? 0u : pad);
+      atomicAdd(&sg.cnt_b[it.cell0 + e], cb);
+    }
+  }
+}
+
+void launch_vote(int mode, const float* k9, int64_t stride, const VoteSeg* segs,
+                 const VoteItem* items, int32_t n_items, float guard, cudaStream_t s) {
+  if (n_items <= 0) return;
+  if (mode == RV_MODE_BOUND)
+    rv_vote_kernel<RV_MODE_BOUND><<<n_items, kVoteThreads, 0, s>>>(k9, stride, segs, items, guard);
+  else
+    rv_vote_kernel<RV_MODE_FINAL><<<n_items, kVoteThreads, 0, s>>>(k9, stride, segs, items, guard);
+}
+
+// ------------------------------------------------------------------------------------------
+// K5 exact count
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) rv_exact_kernel(const float* __restrict__ k9,
+                                                       int64_t stride,
+                                                       const float* __restrict__ x,
+                                                       const float* __restrict__ y,
+                                                       const VoteSeg* __restrict__ segs,
+                                                       const VoteItem* __restrict__ items,
+                                                       float guard) {
+  const VoteItem it = items[blockIdx.x];
+  const VoteSeg& sg = segs[it.seg];
+  const uint32_t lin = sg.lins[it.cell0];
+  int32_t ci, cj, ck;
+  lin_to_ijk(lin, sg.B, ci, cj, ck);
+  double q[4], f64[9];
+  cell_quat(sg.B, ci, cj, ck, q);
+  phi9(q, f64);
+  float f32[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) f32[t] = (float)f64[t];
+  const double tau = cos(sg.eps);
+  const float init = (float)(-tau);
+
+  uint32_t cnt = 0;
+  const int end = min(it.i0 + it.ni, sg.n);
+  for (int i = it.i0 + threadIdx.x; i < end; i += blockDim.x) {
+    float s = init;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) s = fmaf(f32[t], k9[t * stride + sg.koff + i], s);
+    bool in;
+    if (fabsf(s) < guard) {  // near the threshold: decide in fp64 from the raw inputs
+      const int64_t r = sg.row + i;
+      double a[3] = {x[3 * r], x[3 * r + 1], x[3 * r + 2]};
+      double b[3] = {y[3 * r], y[3 * r + 1], y[3 * r + 2]};
+      const double ia = 1.0 / sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+      const double ib = 1.0 / sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { a[c] *= ia; b[c] *= ib; }
+      double k[9];
+      k9_of(a, b, k);
+      double s64 = 0.0;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) s64 = fma(f64[t], k[t], s64);
+      in = s64 >= tau;
+    } else {
+      in = s >= 0.0f;
+    }
+    cnt += in ? 1u : 0u;
+  }
+  // block reduction
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  __shared__ uint32_t ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    atomicAdd(&sg.cnt_a[it.cell0], t);
+  }
+}
+
+void launch_exact(const float* k9, int64_t stride, const float* x, const float* y,
+                  const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
+                  cudaStream_t s) {
+  if (n_items <= 0) return;
+  rv_exact_kernel<<<n_items, 256, 0, s>>>(k9, stride, x, y, segs, items, guard);
+}
+
+// ------------------------------------------------------------------------------------------
+// K6 inliers + partial sums
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRefThreads) rv_inliers_kernel(
+    const float* __restrict__ x, const float* __restrict__ y, const RefSeg* __restrict__ segs,
+    const RefItem* __restrict__ items, const double* __restrict__ qs, uint32_t* masks,
+    double* __restrict__ partials) {
+  const RefItem it = items[blockIdx.x];
+  const RefSeg& sg = segs[it.seg];
+  double q[4] = {qs[4 * it.seg], qs[4 * it.seg + 1], qs[4 * it.seg + 2], qs[4 * it.seg + 3]};
+  double f[9];
+  phi9(q, f);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[10];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) acc[t] = 0.0;
+  const int end = it.r0 + it.nr;
+  for (int base = it.r0 + warp * 32; base < end; base += kRefThreads) {
+    const int i = base + lane;
+    bool in = false;
+    double k[9];
+    if (i < end && i < sg.n) {
+      const int64_t r = sg.row + i;
+      double a[3] = {x[3 * r], x[3 * r + 1], x[3 * r + 2]};
+      double b[3] = {y[3 * r], y[3 * r + 1], y[3 * r + 2]};
+      const double ia = 1.0 / sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+      const double ib = 1.0 / sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { a[c] *= ia; b[c] *= ib; }
+      k9_of(a, b, k);
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) s = fma(f[t], k[t], s);
+      in = s >= sg.tau;
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, in);
+    if (masks && lane == 0 && base < sg.n) masks[sg.mask_word + (base >> 5)] = bal;
+    if (in) {
+#pragma unroll
+      for (int t = 0; t < 9; ++t) acc[t] += k[t];
+      acc[9] += 1.0;
+    }
+  }
+  // fixed-order reduction: warp butterfly, then warps in order
+#pragma unroll
+  for (int t = 0; t < 10; ++t)
+    for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_down_sync(0xffffffffu, acc[t], o);
+  __shared__ double ws[kRefThreads / 32][10];
+  if (lane == 0)
+#pragma unroll
+    for (int t = 0; t < 10; ++t) ws[warp][t] = acc[t];
+  __syncthreads();
+  if (threadIdx.x < 10) {
+    double s = 0.0;
+    for (int w = 0; w < kRefThreads / 32; ++w) s += ws[w][threadIdx.x];
+    partials[(int64_t)blockIdx.x * 10 + threadIdx.x] = s;
+  }
+}
+
+void launch_inliers(const float* x, const float* y, const RefSeg* segs, const RefItem* items,
+                    int32_t n_items, const double* qs, uint32_t* masks, double* partials,
+                    cudaStream_t s) {
+  if (n_items <= 0) return;
+  rv_inliers_kernel<<<n_items, kRefThreads, 0, s>>>(x, y, segs, items, qs, masks, partials);
+}
+
+// ------------------------------------------------------------------------------------------
+// K7 reduction + 4x4 symmetric eigen-solver (cyclic Jacobi, fp64)
+// ------------------------------------------------------------------------------------------
+constexpr int32_t kStop = 1 << 8;  // internal: a round failed, later rounds keep q
+
+__device__ void jacobi4(double A[4][4], double V[4][4]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) V[r][c] = (r == c) ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    double off = 0.0, diag = 0.0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      diag += A[r][r] * A[r][r];
+#pragma unroll
+      for (int c = r + 1; c < 4; ++c) off += A[r][c] * A[r][c];
+    }
+    if (off == 0.0 || off <= 1e-36 * diag) break;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int qq = p + 1; qq < 4; ++qq) {
+        const double apq = A[p][qq];
+        if (apq == 0.0) continue;
+        // rotation zeroing A[p][qq]: tan(2 phi) = 2 apq / (aqq - app)
+        const double zeta = (A[qq][qq] - A[p][p]) / (2.0 * apq);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = rsqrt(1.0 + t * t), s = t * c;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double akp = A[k][p], akq = A[k][qq];
+          A[k][p] = c * akp - s * akq;
+          A[k][qq] = s * akp + c * akq;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double apk = A[p][k], aqk = A[qq][k];
+          A[p][k] = c * apk - s * aqk;
+          A[qq][k] = s * apk + c * aqk;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double vkp = V[k][p], vkq = V[k][qq];
+          V[k][p] = c * vkp - s * vkq;
+          V[k][qq] = s * vkp + c * vkq;
+        }
+      }
+  }
+}
+
+__global__ void __launch_bounds__(kRefThreads) rv_eig_kernel(const RefSeg* __restrict__ segs,
+                                                             const double* __restrict__ partials,
+                                                             double* qs, int32_t* flags,
+                                                             uint32_t* ninl, int mode) {
+  const RefSeg& sg = segs[blockIdx.x];
+  __shared__ double red[kRefThreads][10];
+  double acc[10];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) acc[t] = 0.0;
+  for (int itm = sg.item_begin + threadIdx.x; itm < sg.item_end; itm += kRefThreads)
+#pragma unroll
+    for (int t = 0; t < 10; ++t) acc[t] += partials[(int64_t)itm * 10 + t];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) red[threadIdx.x][t] = acc[t];
+  __syncthreads();
+  for (int w = kRefThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+#pragma unroll
+      for (int t = 0; t < 10; ++t) red[threadIdx.x][t] += red[threadIdx.x + w][t];
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  const double* S = red[0];
+  const double count = S[9];
+  if (mode == 1) {
+    ninl[blockIdx.x] = (uint32_t)count;
+    return;
+  }
+  int32_t fl = flags[blockIdx.x];
+  if (fl & kStop) return;
+  if (count < 2.0) {
+    flags[blockIdx.x] = fl | RV_DEGENERATE | kStop;
+    return;
+  }
+  // S = sum K_i over inliers; K33 = -(K00 + K11 + K22) by tracelessness
+  double A[4][4] = {{S[0], S[3], S[4], S[5]},
+                    {S[3], S[1], S[6], S[7]},
+                    {S[4], S[6], S[2], S[8]},
+                    {S[5], S[7], S[8], -(S[0] + S[1] + S[2])}};
+  double V[4][4];
+  jacobi4(A, V);
+  int i0 = 0;
+  for (int r = 1; r < 4; ++r)
+    if (A[r][r] > A[i0][i0]) i0 = r;
+  double l2 = -1e300;
+  for (int r = 0; r < 4; ++r)
+    if (r != i0 && A[r][r] > l2) l2 = A[r][r];
+  const double l1 = A[i0][i0];
+  if (l1 - l2 <= 1e-12 * fabs(l1)) {
+    flags[blockIdx.x] = fl | RV_DEGENERATE | kStop;
+    return;
+  }
+  double v[4] = {V[0][i0], V[1][i0], V[2][i0], V[3][i0]};
+  const double nv = rsqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3]);
+  // hemisphere representative: q3 < 0; |q3| <= 1e-15 -> first nonzero of q0..q2 positive
+  bool flip;
+  if (v[3] * nv < -1e-15) flip = false;
+  else if (v[3] * nv > 1e-15) flip = true;
+  else {
+    flip = false;
+    for (int a = 0; a < 3; ++a)
+      if (v[a] != 0.0) { flip = v[a] < 0.0; break; }
+  }
+  const double sgn = flip ? -nv : nv;
+  for (int a = 0; a < 4; ++a) qs[4 * blockIdx.x + a] = v[a] * sgn;
+  flags[blockIdx.x] = fl | RV_REFINED;
+}
+
+void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* qs, int32_t* flags,
+                uint32_t* ninl, int mode, cudaStream_t s) {
+  if (P <= 0) return;
+  rv_eig_kernel<<<P, kRefThreads, 0, s>>>(segs, partials, qs, flags, ninl, mode);
+}
+
+}  // namespace rv

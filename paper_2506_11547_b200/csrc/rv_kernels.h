@@ -1,0 +1,75 @@
+// rv_kernels.h -- device-side descriptors and launchers of librotvote's sm_100a kernels.
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace rv {
+
+constexpr int kVoteThreads = 256;                  // K3 block
+constexpr int kCellsPerThread = 4;                 // K3 register blocking (cells per thread)
+constexpr int kCellsPerBlock = kVoteThreads * kCellsPerThread;
+constexpr int kTile = 256;                         // correspondences per TMA stage
+constexpr int kStages = 3;
+constexpr int kRefThreads = 256;                   // K6/K7 block
+constexpr int kRefRowsPerItem = 8192;              // K6 rows per block (multiple of 32)
+
+// One problem's block list for a vote launch.
+struct VoteSeg {
+  const uint32_t* lins;  // DEVICE block indices (lin at resolution B)
+  uint32_t* cnt_a;       // DEVICE counts (indexed like lins)
+  uint32_t* cnt_b;       // DEVICE second counts (RV_MODE_FINAL) or nullptr
+  int64_t koff;          // offset of the problem's rows in the 9-row K table (multiple of 4)
+  int64_t row;           // offset of the problem's rows in x, y
+  int32_t n;             // correspondences of the problem
+  int32_t B;             // grid resolution of lins
+  double eps;            // inlier angle
+};
+
+// One thread block of work: blocks [cell0, cell0+ncell) of segment seg against
+// correspondences [i0, i0+ni) of it (i0, ni multiples of 4; rows >= n are zero padding).
+struct VoteItem {
+  int32_t seg, cell0, ncell, i0, ni;
+};
+
+// One problem of a refinement launch.
+struct RefSeg {
+  int64_t row;           // offset of the problem's rows in x, y
+  int64_t mask_word;     // offset of the problem's mask in the mask buffer (words)
+  int32_t n;
+  int32_t item_begin, item_end;  // its K6 items
+  int32_t pad;
+  double tau;            // cos(eps)
+};
+struct RefItem {
+  int32_t seg, r0, nr;   // rows [r0, r0+nr) of the problem, r0 % 32 == 0
+};
+
+// K1: normalise + 9-entry K table (fp64 -> fp32), zero padding to pad4(n) per problem.
+// koffs[P+1] DEVICE padded offsets, rows[P+1] DEVICE row offsets.  bad: DEVICE int64,
+// atomicMin of the first row that cannot be normalised (init to INT64_MAX).
+void launch_setup(const float* x, const float* y, const int64_t* rows, const int64_t* koffs,
+                  int32_t P, int64_t total_pad, float* k9, int64_t stride,
+                  unsigned long long* bad, cudaStream_t s);
+
+// K3: fp32 FFMA2 vote over TMA-staged K tiles.  mode RV_MODE_BOUND / RV_MODE_FINAL.
+void launch_vote(int mode, const float* k9, int64_t stride, const VoteSeg* segs,
+                 const VoteItem* items, int32_t n_items, float guard, cudaStream_t s);
+
+// K5: exact counts (fp32 vote + fp64 recheck of |s32 - tau| < guard).  items: one block
+// per (block, correspondence chunk), ncell == 1.
+void launch_exact(const float* k9, int64_t stride, const float* x, const float* y,
+                  const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
+                  cudaStream_t s);
+
+// K6: fp64 inlier test at qs[seg] + partial sums of K over inliers (+ mask words).
+void launch_inliers(const float* x, const float* y, const RefSeg* segs, const RefItem* items,
+                    int32_t n_items, const double* qs, uint32_t* masks, double* partials,
+                    cudaStream_t s);
+
+// K7: per problem, reduce the partials in fixed order; mode 0: top-eigenvector refinement
+// step (cyclic Jacobi, fp64) updating qs/flags; mode 1: write the inlier count only.
+void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* qs,
+                int32_t* flags, uint32_t* ninl, int mode, cudaStream_t s);
+
+}  // namespace rv

@@ -1,0 +1,300 @@
+// rv_plan.cpp -- host planner of the certified coarse-to-fine search (include/rotvote_plan.h).
+//
+// Reading R6: on a chain of nested grids B_0 | B_1 | ... | B_{L-1}
+// (B_{L-1} = the paper's accumulator resolution),
+//   UB(c) = #{i : s_i(q_c) >= cos(min(pi, eps + r(c))) - guard}
+// bounds the count of every finest block whose centre lies in block c.  The search:
+//   1. level 0: UB of every candidate block;
+//   2. dive: from the level-0 block of largest excess UB - n(1 - t_c)/2 (t_c the unguarded
+//      bound threshold, n(1-t_c)/2 the uniform-outlier background, Archimedes), vote the
+//      children of its 3x3x3 neighbourhood level by level, re-ranking by excess, down to
+//      the finest level, where LB* = max #{s32 >= tau + guard} is a certified lower bound
+//      of the best exact count;
+//   3. branch and bound: keep blocks with UB >= LB* (ties kept), vote their children, ...;
+//   4. finest level: cnt_hi = #{s32 >= tau - guard} >= exact >= cnt_lo = #{s32 >= tau + guard};
+//      blocks with hi >= max lo and hi != lo get the exact fp64 recheck (RV_MODE_EXACT);
+//      winner = max exact count, ties -> lowest lin (R7).
+// The result equals the exhaustive scan of the finest grid for every chain and `levels`.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "../../include/rotvote.h"
+#include "../../include/rotvote_plan.h"
+#include "rv_geom.h"
+
+namespace {
+
+enum Phase { PH_L0, PH_DIVE, PH_BNB, PH_RECHECK, PH_DONE };
+
+std::vector<uint32_t> candidates_of(int32_t B) {
+  std::vector<uint32_t> out;
+  for (int32_t i = 0; i < B; ++i)
+    for (int32_t j = 0; j < B; ++j)
+      for (int32_t k = 0; k < B; ++k)
+        if (rv::is_candidate(B, i, j, k)) out.push_back(rv::ijk_to_lin(i, j, k, B));
+  return out;
+}
+
+}  // namespace
+
+struct rv_plan {
+  std::vector<int32_t> chain;
+  int64_t n = 0;
+  double eps = 0, guard = 0;
+  Phase phase = PH_L0;
+  int level = 0;
+  int32_t mode = RV_MODE_BOUND;
+  std::vector<uint32_t> cells;  // pending request
+
+  std::vector<uint32_t> l0_cells, l0_ub;
+  int64_t lb_star = 0;
+  // finest level
+  std::vector<uint32_t> fin_cells, fin_lo, fin_hi, recheck_idx;
+  rv_plan_result res{};
+
+  int last() const { return (int)chain.size() - 1; }
+  int32_t mode_for(int l) const { return l == last() ? RV_MODE_FINAL : RV_MODE_BOUND; }
+
+  void note_request() {
+    res.pair_votes += (uint64_t)cells.size() * (uint64_t)n;
+    res.cells_evaluated += cells.size();
+    if (res.n_phases < 16) res.cells_per_phase[res.n_phases++] = (int64_t)cells.size();
+  }
+
+  double excess(int32_t B, uint32_t lin, uint32_t ub) const {
+    int32_t i, j, k;
+    rv::lin_to_ijk(lin, B, i, j, k);
+    double t = rv::bound_threshold(B, i, j, k, eps);
+    return (double)ub - (double)n * (1.0 - t) * 0.5;
+  }
+
+  // index of the max-excess block, ties -> lowest lin (cells are ascending)
+  size_t best_excess(int32_t B, const std::vector<uint32_t>& c, const uint32_t* ub) const {
+    size_t best = 0;
+    double be = -1e300;
+    for (size_t e = 0; e < c.size(); ++e) {
+      double x = excess(B, c[e], ub[e]);
+      if (x > be) { be = x; best = e; }
+    }
+    return best;
+  }
+
+  // candidate children at level l+1 of a sorted list of level-l blocks (ascending output)
+  std::vector<uint32_t> children(int l, const std::vector<uint32_t>& parents) const {
+    const int32_t B = chain[l], Bc = chain[l + 1], f = Bc / B;
+    std::vector<uint32_t> out;
+    out.reserve(parents.size() * (size_t)(f * f * f));
+    for (uint32_t p : parents) {
+      int32_t i, j, k;
+      rv::lin_to_ijk(p, B, i, j, k);
+      for (int32_t a = 0; a < f; ++a)
+        for (int32_t b = 0; b < f; ++b)
+          for (int32_t c = 0; c < f; ++c) {
+            int32_t ci = f * i + a, cj = f * j + b, ck = f * k + c;
+            if (rv::is_candidate(Bc, ci, cj, ck)) out.push_back(rv::ijk_to_lin(ci, cj, ck, Bc));
+          }
+    }
+    std::sort(out.begin(), out.end());
+    return out;
+  }
+
+  std::vector<uint32_t> neighbourhood(int l, uint32_t lin) const {
+    const int32_t B = chain[l];
+    int32_t i, j, k;
+    rv::lin_to_ijk(lin, B, i, j, k);
+    std::vector<uint32_t> out;
+    for (int32_t a = -1; a <= 1; ++a)
+      for (int32_t b = -1; b <= 1; ++b)
+        for (int32_t c = -1; c <= 1; ++c) {
+          int32_t ni = i + a, nj = j + b, nk = k + c;
+          if (ni < 0 || nj < 0 || nk < 0 || ni >= B || nj >= B || nk >= B) continue;
+          if (rv::is_candidate(B, ni, nj, nk)) out.push_back(rv::ijk_to_lin(ni, nj, nk, B));
+        }
+    std::sort(out.begin(), out.end());
+    return out;
+  }
+
+  void start_bnb() {
+    std::vector<uint32_t> surv;
+    for (size_t e = 0; e < l0_cells.size(); ++e)
+      if ((int64_t)l0_ub[e] >= lb_star) surv.push_back(l0_cells[e]);
+    phase = PH_BNB;
+    level = 1;
+    mode = mode_for(level);
+    cells = children(0, surv);
+    note_request();
+  }
+
+  void finalize() {
+    // exact counts are known for blocks with lo == hi or rechecked; every other block
+    // has hi < max lo <= the best exact count, so it cannot win or tie.
+    std::vector<int64_t> exact(fin_cells.size(), -1);
+    for (size_t e = 0; e < fin_cells.size(); ++e)
+      if (fin_lo[e] == fin_hi[e]) exact[e] = fin_lo[e];
+    for (size_t r = 0; r < recheck_idx.size(); ++r) exact[recheck_idx[r]] = (int64_t)cells_exact[r];
+    int64_t best = -1;
+    uint32_t best_lin = 0;
+    int32_t tied = 0;
+    for (size_t e = 0; e < fin_cells.size(); ++e) {
+      if (exact[e] < 0) continue;
+      if (exact[e] > best) { best = exact[e]; best_lin = fin_cells[e]; tied = 1; }
+      else if (exact[e] == best) { ++tied; if (fin_cells[e] < best_lin) best_lin = fin_cells[e]; }
+    }
+    res.lin = best_lin;
+    res.B = chain.back();
+    res.votes = (uint32_t)(best < 0 ? 0 : best);
+    res.n_tied = tied;
+    res.lb_star = (uint32_t)lb_star;
+    res.n_rechecked = (int32_t)recheck_idx.size();
+    phase = PH_DONE;
+    cells.clear();
+  }
+
+  void enter_final(const uint32_t* a, const uint32_t* b) {
+    fin_cells = cells;
+    fin_hi.assign(a, a + cells.size());
+    fin_lo.assign(b, b + cells.size());
+    uint32_t L = 0;
+    for (uint32_t v : fin_lo) L = std::max(L, v);
+    recheck_idx.clear();
+    for (size_t e = 0; e < fin_cells.size(); ++e)
+      if (fin_hi[e] >= L && fin_hi[e] != fin_lo[e]) recheck_idx.push_back(e);
+    if (recheck_idx.empty()) { finalize(); return; }
+    phase = PH_RECHECK;
+    mode = RV_MODE_EXACT;
+    cells.clear();
+    for (size_t r : recheck_idx) cells.push_back(fin_cells[r]);
+    note_request();
+  }
+
+  std::vector<uint32_t> cells_exact;
+
+  int feed(const uint32_t* a, const uint32_t* b) {
+    if (phase == PH_DONE) return -1;
+    if (mode == RV_MODE_FINAL && (b == nullptr || a == nullptr)) return -1;
+    if (a == nullptr && !cells.empty()) return -1;
+    switch (phase) {
+      case PH_L0: {
+        if (mode == RV_MODE_FINAL) { enter_final(a, b); return 0; }  // levels == 1
+        l0_cells = cells;
+        l0_ub.assign(a, a + cells.size());
+        size_t s = best_excess(chain[0], l0_cells, l0_ub.data());
+        phase = PH_DIVE;
+        level = 1;
+        mode = mode_for(level);
+        cells = children(0, neighbourhood(0, l0_cells[s]));
+        note_request();
+        return 0;
+      }
+      case PH_DIVE: {
+        if (mode == RV_MODE_BOUND) {
+          size_t s = best_excess(chain[level], cells, a);
+          uint32_t pick = cells[s];
+          cells = children(level, neighbourhood(level, pick));
+          ++level;
+          mode = mode_for(level);
+          note_request();
+        } else {
+          lb_star = 0;
+          for (size_t e = 0; e < cells.size(); ++e) lb_star = std::max<int64_t>(lb_star, b[e]);
+          start_bnb();
+        }
+        return 0;
+      }
+      case PH_BNB: {
+        if (mode == RV_MODE_BOUND) {
+          std::vector<uint32_t> surv;
+          for (size_t e = 0; e < cells.size(); ++e)
+            if ((int64_t)a[e] >= lb_star) surv.push_back(cells[e]);
+          cells = children(level, surv);
+          ++level;
+          mode = mode_for(level);
+          note_request();
+        } else {
+          enter_final(a, b);
+        }
+        return 0;
+      }
+      case PH_RECHECK: {
+        cells_exact.assign(a, a + cells.size());
+        finalize();
+        return 0;
+      }
+      default:
+        return -1;
+    }
+  }
+};
+
+extern "C" {
+
+int rv_plan_create(const int32_t* chain, int32_t chain_len, int32_t levels, int64_t n, double eps,
+                   double guard, rv_plan** out) {
+  if (!out) return -1;
+  *out = nullptr;
+  if (!chain || chain_len < 1 || chain_len > RV_MAX_CHAIN || n < 1) return -1;
+  if (!(eps > 0.0) || !(eps < 3.141592653589793) || !(guard >= 0.0)) return -1;
+  for (int l = 0; l < chain_len; ++l) {
+    if (chain[l] < 1 || chain[l] > 1625) return -1;
+    if (l > 0 && chain[l] % chain[l - 1] != 0) return -1;
+  }
+  if (levels == 0) levels = chain_len < 5 ? chain_len : 5;
+  if (levels < 1 || levels > chain_len) return -1;
+  rv_plan* p = new rv_plan();
+  p->chain.assign(chain + (chain_len - levels), chain + chain_len);
+  p->n = n;
+  p->eps = eps;
+  p->guard = guard;
+  p->phase = PH_L0;
+  p->level = 0;
+  p->mode = p->mode_for(0);
+  p->cells = candidates_of(p->chain[0]);
+  p->note_request();
+  *out = p;
+  return 0;
+}
+
+void rv_plan_destroy(rv_plan* p) { delete p; }
+
+int rv_plan_request(const rv_plan* p, int32_t* B, int32_t* mode, int64_t* m, const uint32_t** lins) {
+  if (!p || p->phase == PH_DONE) return 0;
+  if (B) *B = p->chain[p->level];
+  if (mode) *mode = p->mode;
+  if (m) *m = (int64_t)p->cells.size();
+  if (lins) *lins = p->cells.data();
+  return 1;
+}
+
+int rv_plan_feed(rv_plan* p, const uint32_t* cnt_a, const uint32_t* cnt_b) {
+  if (!p) return -1;
+  return p->feed(cnt_a, cnt_b);
+}
+
+int rv_plan_get_result(const rv_plan* p, rv_plan_result* out) {
+  if (!p || !out || p->phase != PH_DONE) return -1;
+  *out = p->res;
+  return 0;
+}
+
+void rv_shard_range(int64_t m, int32_t rank, int32_t world, int64_t* begin, int64_t* end) {
+  if (world < 1) world = 1;
+  *begin = m * rank / world;
+  *end = m * (rank + 1) / world;
+}
+
+int64_t rv_grid_candidates(int32_t B, uint32_t* out, int64_t cap) {
+  if (B < 1 || B > 1625) return -1;
+  int64_t m = 0;
+  for (int32_t i = 0; i < B; ++i)
+    for (int32_t j = 0; j < B; ++j)
+      for (int32_t k = 0; k < B; ++k)
+        if (rv::is_candidate(B, i, j, k)) {
+          if (out && m < cap) out[m] = rv::ijk_to_lin(i, j, k, B);
+          ++m;
+        }
+  return m;
+}
+
+}  // extern "C"

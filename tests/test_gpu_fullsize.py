@@ -1,0 +1,81 @@
+"""Parity at BASELINE.json's full size (config 4: N = 1e6, 99% outliers, eps = 0.05) in the
+launch configuration bench.py times (default chain, levels = 0, one GPU).
+
+The oracle cannot afford the whole search in a unit-test budget every time, so the bar is
+checked on sampled outputs it computes one by one (exact count of the winning cell and of
+sampled cells at every level, refinement from the GPU's cell), plus -- marked slow -- the
+oracle's complete certified search (~2 min single-threaded)."""
+import math
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+GUARD = 1e-5
+BAND = 1e-5
+
+
+@pytest.fixture(scope="module")
+def setup():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_11547_b200 import RotVote, build
+    build.build()
+    oracle.build()
+    pr = datagen.cfg4()
+    rv = RotVote(max_n=pr.n)
+    x = torch.from_numpy(pr.x).cuda()
+    y = torch.from_numpy(pr.y).cuda()
+    res = rv.solve(x, y, pr.eps)
+    yield pr, rv, x, y, res
+    rv.close()
+
+
+def test_winner_exact_count_and_rotation(setup):
+    pr, rv, x, y, res = setup
+    tau = math.cos(pr.eps)
+    cnt, nr = oracle.count_cells(pr.x, pr.y, 360, [res.lin], tau, band=1e-12)
+    assert res.votes == cnt[0] and nr[0] == 0
+    q, fl, mask = oracle.refine(pr.x, pr.y, pr.eps, res.q_cell, rounds=2)
+    assert oracle.rotation_angle_between(res.q, q) < 1e-4
+    assert res.n_inliers == int(mask.sum())
+    from scipy.spatial.transform import Rotation as Rot
+    assert np.degrees(Rot.from_matrix(pr.R.T @ oracle.quat_to_R(res.q)).magnitude()) < 0.5
+    assert res.votes >= 9000
+
+
+def test_sampled_cells_every_level(setup):
+    from paper_2506_11547_b200 import RV_MODE_BOUND, RV_MODE_EXACT, RV_MODE_FINAL
+    pr, rv, x, y, res = setup
+    rng = np.random.default_rng(0)
+    tau = math.cos(pr.eps)
+    for B in (15, 45, 90, 180):
+        lins = np.sort(rng.choice(oracle.candidates(B), 24, replace=False)).astype(np.uint32)
+        got = rv.count_cells(x, y, B, lins, pr.eps, RV_MODE_BOUND)
+        thr = np.array([oracle.cell_bound_threshold(B, int(l), pr.eps) for l in lins]) - GUARD
+        lo, _ = oracle.count_cells(pr.x, pr.y, B, lins, thr + BAND, band=0)
+        hi, _ = oracle.count_cells(pr.x, pr.y, B, lins, thr - BAND, band=0)
+        assert np.all(got >= lo) and np.all(got <= hi), B
+    i, j, k = res.cell
+    lins = np.array(sorted({oracle.lin_of(360, i + a, j + b, k + c) for a in (-1, 0, 1)
+                            for b in (-1, 0, 1) for c in (-1, 0, 1)}), np.uint32)
+    a, b = rv.count_cells(x, y, 360, lins, pr.eps, RV_MODE_FINAL)
+    lo, _ = oracle.count_cells(pr.x, pr.y, 360, lins, tau - GUARD + BAND, band=0)
+    hi, _ = oracle.count_cells(pr.x, pr.y, 360, lins, tau - GUARD - BAND, band=0)
+    assert np.all(a >= lo) and np.all(a <= hi)
+    ex = rv.count_cells(x, y, 360, lins, pr.eps, RV_MODE_EXACT)
+    want, nr = oracle.count_cells(pr.x, pr.y, 360, lins, tau, band=1e-12)
+    assert np.array_equal(ex[nr == 0], want[nr == 0])
+    assert ex.max() == res.votes
+
+
+@pytest.mark.slow
+def test_full_oracle_search_agrees(setup):
+    pr, rv, x, y, res = setup
+    ref = oracle.solve(pr.x, pr.y, pr.eps)
+    assert (res.cell, res.votes, res.n_tied) == (ref.cell, ref.votes, ref.n_tied)
+    assert oracle.rotation_angle_between(res.q, ref.q) < 1e-4
