@@ -522,6 +522,8 @@ int32_t or_refine(const float* x, const float* y, int64_t n, double eps, const d
   const double tau = std::cos(eps);
   double q[4];
   std::memcpy(q, q0, sizeof(q));
+  const double nq0 = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  for (int a = 0; a < 4; ++a) q[a] /= nq0;  // a rotation is a unit quaternion
   or_canonicalize(q);
   int32_t fl = 0;
   for (int r = 0; r < rounds; ++r) {
