@@ -171,25 +171,34 @@ namespace {
 
 // ---- work decomposition ---------------------------------------------------------------------
 
-// Vote items for segments given as (n_cells, n_corr) pairs: cell blocks of kCellsPerBlock,
-// correspondence chunks chosen so the launch has >= ~16 waves of equal-cost blocks.
-void build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
-                      int slots, std::vector<rv::VoteItem>& items) {
+// Vote items for segments given as (n_cells, n_corr) pairs.  The CTA shape (groups G: a CTA
+// covers kCellsPerBlock/G cells) is chosen to waste the fewest thread slots; the
+// correspondence chunk gives >= ~8 waves of equal-cost CTAs while keeping each CTA above
+// ~1M pair votes so its prologue (cell rotations, thresholds, first TMA) stays negligible.
+int build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
+                     int slots, std::vector<rv::VoteItem>& items) {
   items.clear();
-  double work = 0;
-  for (size_t s = 0; s < ncell.size(); ++s) {
-    int64_t cb = (ncell[s] + rv::kCellsPerBlock - 1) / rv::kCellsPerBlock;
-    work += (double)cb * (double)pad4(ncorr[s]);
+  int groups = 1;
+  int64_t best_pad = -1;
+  for (int G : {1, 2, 4}) {
+    const int64_t cpb = rv::kCellsPerBlock / G;
+    int64_t padded = 0;
+    for (size_t s = 0; s < ncell.size(); ++s) padded += (ncell[s] + cpb - 1) / cpb * cpb;
+    if (best_pad < 0 || padded < best_pad) { best_pad = padded; groups = G; }
   }
-  int64_t chunk = (int64_t)std::ceil(work / ((double)slots * 16.0));
-  chunk = std::max<int64_t>(chunk, rv::kTile);
+  const int64_t cpb = rv::kCellsPerBlock / groups;
+  double work = 0;  // CTA-correspondence units
+  for (size_t s = 0; s < ncell.size(); ++s)
+    work += (double)((ncell[s] + cpb - 1) / cpb) * (double)pad4(ncorr[s]);
+  int64_t chunk = (int64_t)std::ceil(work / ((double)slots * 8.0));
+  chunk = std::max<int64_t>(chunk, (1 << 20) / cpb);
   chunk = std::min<int64_t>(chunk, 1 << 16);
   chunk = (chunk + rv::kTile - 1) / rv::kTile * rv::kTile;
   for (size_t s = 0; s < ncell.size(); ++s) {
     const int64_t n4 = pad4(ncorr[s]);
     if (ncell[s] == 0 || n4 == 0) continue;
-    const int64_t cb = (ncell[s] + rv::kCellsPerBlock - 1) / rv::kCellsPerBlock;
-    const int64_t per = (ncell[s] + cb - 1) / cb;  // balanced cells per block
+    const int64_t cb = (ncell[s] + cpb - 1) / cpb;
+    const int64_t per = (ncell[s] + cb - 1) / cb;  // balanced cells per CTA
     for (int64_t b = 0; b < cb; ++b) {
       const int64_t c0 = b * per, nc = std::min(per, ncell[s] - c0);
       if (nc <= 0) continue;
@@ -198,6 +207,7 @@ void build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64
                          (int32_t)std::min(chunk, n4 - i0)});
     }
   }
+  return groups;
 }
 
 void build_exact_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
@@ -291,8 +301,9 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
     ncorr.push_back(n);
   }
   std::vector<rv::VoteItem> items;
+  int groups = 1;
   if (mode == RV_MODE_EXACT) build_exact_items(ncell, ncorr, items);
-  else build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items);
+  else groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items);
 
   RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
   RV_CUDA(ctx->vitems.ensure(std::max<size_t>(1, items.size())), "allocating items");
@@ -326,7 +337,7 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
                      (int32_t)items.size(), ctx->cfg.guard, s);
   } else {
     RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
-    rv::launch_vote(mode, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
+    rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
                     (int32_t)items.size(), ctx->cfg.guard, s);
     RV_CUDA(cudaEventRecord(ctx->evv1, s), "event");
     for (int64_t c : ncell) ctx->vote_pairs += (uint64_t)c * (uint64_t)n;
@@ -571,8 +582,9 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     off += r.m;
   }
   std::vector<rv::VoteItem> items;
+  int groups = 1;
   if (mode == RV_MODE_EXACT) build_exact_items(ncell, ncorr, items);
-  else build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items);
+  else groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items);
   RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
   RV_CUDA(ctx->vitems.ensure(std::max<size_t>(1, items.size())), "allocating items");
   RV_CUDA(ctx->up.ensure(total * 4 + segs.size() * sizeof(rv::VoteSeg) +
@@ -602,7 +614,7 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                      (int32_t)items.size(), ctx->cfg.guard, s);
   } else {
     RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
-    rv::launch_vote(mode, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
+    rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
                     (int32_t)items.size(), ctx->cfg.guard, s);
     RV_CUDA(cudaEventRecord(ctx->evv1, s), "event");
     for (size_t q = 0; q < ncell.size(); ++q) ctx->vote_pairs += (uint64_t)ncell[q] * ncorr[q];

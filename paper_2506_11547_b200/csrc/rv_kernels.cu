@@ -120,30 +120,78 @@ __device__ __forceinline__ uint32_t sign_bit(float v) { return __float_as_uint(v
 // ------------------------------------------------------------------------------------------
 // K3 vote
 // ------------------------------------------------------------------------------------------
-// Each thread owns kCellsPerThread blocks (cells): phi(q_c) lives in registers duplicated as
-// float2 so that one FFMA2 evaluates the same cell against two correspondences.  All threads
-// of the CTA stream the same K tile from shared memory (warp-broadcast LDS.128 of four
-// consecutive correspondences per row).  The threshold is folded into the accumulator's
-// initial value (s - t), and the count is the sign bit: cnt = processed - #negatives.
-template <int MODE>
-__global__ void __launch_bounds__(kVoteThreads, 2)
+// Warp-specialised CTA: warps 0..7 vote, warp 8 is the TMA producer.  Each voting thread owns
+// kCellsPerThread blocks (cells): phi(q_c) and the threshold live in registers; one FFMA2
+// (scalar-broadcast phi operand) evaluates a cell against two correspondences.  The voters
+// form G groups; group g handles the 4-correspondence chunks g, g+G, ... of every tile, so a
+// CTA covers 1024/G cells (G > 1 keeps the thread slots full when a level has few cells).
+// K tiles (9 rows x kTile correspondences) arrive by cp.async.bulk into a kStages ring with
+// full/empty mbarriers; voters never block one another.  The threshold is folded into the
+// FMA chain's initial value, the count is the sign bit (cnt = processed - #negatives), and
+// the counts leave the CTA with one atomicAdd per cell.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// acc += sign bit of v; an opaque add keeps NVVM from re-associating the running sum into a
+// tree whose last add lands on the FMA pipe (IMAD); ptxas fuses shift+add into LEA.HI (ALU).
+__device__ __forceinline__ void add_sign(uint32_t& acc, float v) {
+  asm("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(__float_as_uint(v) >> 31));
+}
+
+template <int MODE, int G>
+__global__ void __launch_bounds__(kVoteThreads + 32, 2)
     rv_vote_kernel(const float* __restrict__ k9, int64_t stride, const VoteSeg* __restrict__ segs,
                    const VoteItem* __restrict__ items, float guard) {
+  constexpr int TPG = kVoteThreads / G;               // voting threads per group
+  constexpr int CPB = TPG * kCellsPerThread;          // cells per CTA
   __shared__ __align__(128) float sK[kStages][9][kTile];
-  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ uint32_t red[G > 1 ? 2 * kVoteThreads * kCellsPerThread : 1];
 
   const VoteItem it = items[blockIdx.x];
   const VoteSeg& sg = segs[it.seg];
   const int tid = threadIdx.x;
+  const int ntiles = (it.ni + kTile - 1) / kTile;
 
-  float2 phi[kCellsPerThread][9];
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kVoteThreads / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (tid >= kVoteThreads) {
+    // ---------------- producer warp ----------------
+    if (tid == kVoteThreads) {
+      const float* base = k9 + sg.koff + it.i0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int st = t % kStages;
+        if (t >= kStages) mbar_wait(&empty[st], (uint32_t)(((t / kStages) - 1) & 1));
+        const int cnt = min(kTile, it.ni - t * kTile);
+        const uint32_t bytes = (uint32_t)cnt * 4u;
+        mbar_expect_tx(&full[st], bytes * 9u);
+#pragma unroll
+        for (int j = 0; j < 9; ++j)
+          tma_bulk_g2s(&sK[st][j][0], base + j * stride + (int64_t)t * kTile, bytes, &full[st]);
+      }
+    }
+  }
+  // ---------------- voters ----------------
+  const int g = tid / TPG;           // group of this voter
+  const int local = tid % TPG;
+  float phi[kCellsPerThread][9];
   float init[kCellsPerThread];
-  {
+  uint32_t neg_a[kCellsPerThread], neg_b[kCellsPerThread];
+  const float two_g = 2.0f * guard;
+  if (tid < kVoteThreads) {
     const int32_t B = sg.B;
     const double tau = cos(sg.eps);
 #pragma unroll
     for (int c = 0; c < kCellsPerThread; ++c) {
-      int e = tid + c * kVoteThreads;
+      int e = local + c * TPG;
       if (e >= it.ncell) e = 0;  // inactive slot: recompute cell 0, never stored
       const uint32_t lin = sg.lins[it.cell0 + e];
       int32_t i, j, k;
@@ -152,92 +200,118 @@ __global__ void __launch_bounds__(kVoteThreads, 2)
       cell_quat(B, i, j, k, q);
       phi9(q, f);
 #pragma unroll
-      for (int t = 0; t < 9; ++t) phi[c][t] = make_float2((float)f[t], (float)f[t]);
+      for (int t = 0; t < 9; ++t) phi[c][t] = (float)f[t];
       double thr = (MODE == RV_MODE_BOUND) ? bound_threshold(B, i, j, k, sg.eps) - guard
                                            : tau - guard;
       init[c] = (float)(-thr);
+      neg_a[c] = neg_b[c] = 0;
     }
-  }
-
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  const int ntiles = (it.ni + kTile - 1) / kTile;
-  const float* base = k9 + sg.koff + it.i0;
-  auto issue = [&](int tile) {
-    const int st = tile % kStages;
-    const int cnt = min(kTile, it.ni - tile * kTile);
-    const uint32_t bytes = (uint32_t)cnt * 4u;
-    mbar_expect_tx(&full[st], bytes * 9u);
-#pragma unroll
-    for (int j = 0; j < 9; ++j)
-      tma_bulk_g2s(&sK[st][j][0], base + j * stride + (int64_t)tile * kTile, bytes, &full[st]);
-  };
-  if (tid == 0)
-    for (int t = 0; t < kStages && t < ntiles; ++t) issue(t);
-
-  uint32_t neg_a[kCellsPerThread], neg_b[kCellsPerThread];
-#pragma unroll
-  for (int c = 0; c < kCellsPerThread; ++c) neg_a[c] = neg_b[c] = 0;
-  const float two_g = 2.0f * guard;
-
-  for (int tile = 0; tile < ntiles; ++tile) {
-    const int st = tile % kStages;
-    mbar_wait(&full[st], (uint32_t)((tile / kStages) & 1));
-    const int cnt = min(kTile, it.ni - tile * kTile);
-    const float* sk = &sK[st][0][0];
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int t = 0; t < ntiles; ++t) {
+      const int st = t % kStages;
+      mbar_wait(&full[st], (uint32_t)((t / kStages) & 1));
+      const int cnt = min(kTile, it.ni - t * kTile);
+      const float* sk = &sK[st][0][0];
 #pragma unroll 1
-    for (int i = 0; i < cnt; i += 4) {
-      float4 kk[9];
+      for (int i = 4 * g; i < cnt; i += 4 * G) {
+        float4 kk[9];
 #pragma unroll
-      for (int j = 0; j < 9; ++j) kk[j] = *reinterpret_cast<const float4*>(sk + j * kTile + i);
+        for (int j = 0; j < 9; ++j) kk[j] = *reinterpret_cast<const float4*>(sk + j * kTile + i);
 #pragma unroll
-      for (int c = 0; c < kCellsPerThread; ++c) {
-        float2 lo = make_float2(init[c], init[c]);
-        float2 hi = lo;
+        for (int c = 0; c < kCellsPerThread; ++c) {
+          const float2 i2 = make_float2(init[c], init[c]);
+          float2 lo = i2, hi = i2;
 #pragma unroll
-        for (int j = 0; j < 9; ++j) {
-          lo = __ffma2_rn(phi[c][j], make_float2(kk[j].x, kk[j].y), lo);
-          hi = __ffma2_rn(phi[c][j], make_float2(kk[j].z, kk[j].w), hi);
-        }
-        neg_a[c] += sign_bit(lo.x) + sign_bit(lo.y) + sign_bit(hi.x) + sign_bit(hi.y);
-        if (MODE == RV_MODE_FINAL) {
-          neg_b[c] += sign_bit(lo.x - two_g) + sign_bit(lo.y - two_g) + sign_bit(hi.x - two_g) +
-                      sign_bit(hi.y - two_g);
+          for (int j = 0; j < 9; ++j) {
+            const float2 f2 = make_float2(phi[c][j], phi[c][j]);
+            lo = __ffma2_rn(f2, make_float2(kk[j].x, kk[j].y), lo);
+            hi = __ffma2_rn(f2, make_float2(kk[j].z, kk[j].w), hi);
+          }
+          add_sign(neg_a[c], lo.x);
+          add_sign(neg_a[c], lo.y);
+          add_sign(neg_a[c], hi.x);
+          add_sign(neg_a[c], hi.y);
+          if (MODE == RV_MODE_FINAL) {
+            add_sign(neg_b[c], lo.x - two_g);
+            add_sign(neg_b[c], lo.y - two_g);
+            add_sign(neg_b[c], hi.x - two_g);
+            add_sign(neg_b[c], hi.y - two_g);
+          }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
-    __syncthreads();  // every thread is done with stage st
-    if (tid == 0 && tile + kStages < ntiles) issue(tile + kStages);
+    (void)warp;
   }
 
   // epilogue: counts = processed - negatives - zero-padding rows that counted as >= 0
   const int valid = max(0, min(it.ni, sg.n - it.i0));
   const uint32_t pad = (uint32_t)(it.ni - valid);
+  if (G == 1) {
+    if (tid < kVoteThreads) {
 #pragma unroll
-  for (int c = 0; c < kCellsPerThread; ++c) {
-    const int e = tid + c * kVoteThreads;
-    if (e >= it.ncell) continue;
-    uint32_t ca = (uint32_t)it.ni - neg_a[c] - (sign_bit(init[c]) ? 0u : pad);
-    atomicAdd(&sg.cnt_a[it.cell0 + e], ca);
-    if (MODE == RV_MODE_FINAL) {
-      uint32_t cb = (uint32_t)it.ni - neg_b[c] - (sign_bit(init[c] - two_g) ? 0u : pad);
-      atomicAdd(&sg.cnt_b[it.cell0 + e], cb);
+      for (int c = 0; c < kCellsPerThread; ++c) {
+        const int e = local + c * TPG;
+        if (e >= it.ncell) continue;
+        uint32_t ca = (uint32_t)it.ni - neg_a[c] - (sign_bit(init[c]) ? 0u : pad);
+        atomicAdd(&sg.cnt_a[it.cell0 + e], ca);
+        if (MODE == RV_MODE_FINAL) {
+          uint32_t cb = (uint32_t)it.ni - neg_b[c] - (sign_bit(init[c] - two_g) ? 0u : pad);
+          atomicAdd(&sg.cnt_b[it.cell0 + e], cb);
+        }
+      }
+    }
+  } else {
+    if (tid < kVoteThreads) {
+#pragma unroll
+      for (int c = 0; c < kCellsPerThread; ++c) {
+        const int e = local + c * TPG;
+        red[g * CPB + e] = neg_a[c];
+        if (MODE == RV_MODE_FINAL) red[G * CPB + g * CPB + e] = neg_b[c];
+      }
+    }
+    __syncthreads();
+    if (tid < TPG) {
+#pragma unroll
+      for (int c = 0; c < kCellsPerThread; ++c) {
+        const int e = local + c * TPG;
+        if (e >= it.ncell) continue;
+        uint32_t na = 0, nb = 0;
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          na += red[q * CPB + e];
+          if (MODE == RV_MODE_FINAL) nb += red[G * CPB + q * CPB + e];
+        }
+        uint32_t ca = (uint32_t)it.ni - na - (sign_bit(init[c]) ? 0u : pad);
+        atomicAdd(&sg.cnt_a[it.cell0 + e], ca);
+        if (MODE == RV_MODE_FINAL) {
+          uint32_t cb = (uint32_t)it.ni - nb - (sign_bit(init[c] - two_g) ? 0u : pad);
+          atomicAdd(&sg.cnt_b[it.cell0 + e], cb);
+        }
+      }
     }
   }
 }
 
-void launch_vote(int mode, const float* k9, int64_t stride, const VoteSeg* segs,
+template <int MODE, int G>
+static void launch_vote_t(const float* k9, int64_t stride, const VoteSeg* segs,
+                          const VoteItem* items, int32_t n_items, float guard, cudaStream_t s) {
+  rv_vote_kernel<MODE, G><<<n_items, kVoteThreads + 32, 0, s>>>(k9, stride, segs, items, guard);
+}
+
+void launch_vote(int mode, int groups, const float* k9, int64_t stride, const VoteSeg* segs,
                  const VoteItem* items, int32_t n_items, float guard, cudaStream_t s) {
   if (n_items <= 0) return;
-  if (mode == RV_MODE_BOUND)
-    rv_vote_kernel<RV_MODE_BOUND><<<n_items, kVoteThreads, 0, s>>>(k9, stride, segs, items, guard);
-  else
-    rv_vote_kernel<RV_MODE_FINAL><<<n_items, kVoteThreads, 0, s>>>(k9, stride, segs, items, guard);
+  if (mode == RV_MODE_BOUND) {
+    if (groups == 4) launch_vote_t<RV_MODE_BOUND, 4>(k9, stride, segs, items, n_items, guard, s);
+    else if (groups == 2) launch_vote_t<RV_MODE_BOUND, 2>(k9, stride, segs, items, n_items, guard, s);
+    else launch_vote_t<RV_MODE_BOUND, 1>(k9, stride, segs, items, n_items, guard, s);
+  } else {
+    if (groups == 4) launch_vote_t<RV_MODE_FINAL, 4>(k9, stride, segs, items, n_items, guard, s);
+    else if (groups == 2) launch_vote_t<RV_MODE_FINAL, 2>(k9, stride, segs, items, n_items, guard, s);
+    else launch_vote_t<RV_MODE_FINAL, 1>(k9, stride, segs, items, n_items, guard, s);
+  }
 }
 
 // ------------------------------------------------------------------------------------------

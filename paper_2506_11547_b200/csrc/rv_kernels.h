@@ -10,7 +10,7 @@ constexpr int kVoteThreads = 256;                  // K3 block
 constexpr int kCellsPerThread = 4;                 // K3 register blocking (cells per thread)
 constexpr int kCellsPerBlock = kVoteThreads * kCellsPerThread;
 constexpr int kTile = 256;                         // correspondences per TMA stage
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kRefThreads = 256;                   // K6/K7 block
 constexpr int kRefRowsPerItem = 8192;              // K6 rows per block (multiple of 32)
 
@@ -52,8 +52,9 @@ void launch_setup(const float* x, const float* y, const int64_t* rows, const int
                   int32_t P, int64_t total_pad, float* k9, int64_t stride,
                   unsigned long long* bad, cudaStream_t s);
 
-// K3: fp32 FFMA2 vote over TMA-staged K tiles.  mode RV_MODE_BOUND / RV_MODE_FINAL.
-void launch_vote(int mode, const float* k9, int64_t stride, const VoteSeg* segs,
+// K3: fp32 FFMA2 vote over TMA-staged K tiles.  mode RV_MODE_BOUND / RV_MODE_FINAL;
+// groups in {1, 2, 4}: a CTA covers kCellsPerBlock / groups cells.
+void launch_vote(int mode, int groups, const float* k9, int64_t stride, const VoteSeg* segs,
                  const VoteItem* items, int32_t n_items, float guard, cudaStream_t s);
 
 // K5: exact counts (fp32 vote + fp64 recheck of |s32 - tau| < guard).  items: one block
