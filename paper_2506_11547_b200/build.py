@@ -28,18 +28,22 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: dict | None = None) -> str:
+    """Build the library (out/defines: tuning variants, e.g. {"RV_CPT": 6})."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-Wall", "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, f) for f in SOURCES], "-ldl", "-o", LIB + ".tmp"]
+           *[f"-D{k}={v}" for k, v in (defines or {}).items()],
+           *[os.path.join(CSRC, f) for f in SOURCES], "-ldl", "-o", target + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

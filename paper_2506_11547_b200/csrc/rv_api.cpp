@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -116,7 +117,8 @@ struct rv_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   int num_sms = 148;
-  int vote_blocks_per_sm = 2;
+  int vote_blocks_per_sm = rv::kVoteMinBlocks;
+  int force_groups = 0;  // tuning hook: RV_VOTE_GROUPS=1|2|4 forces the K3 CTA shape
   ncclComm_t comm = nullptr;
 
   DevBuf<float> k9;              // [9][stride]
@@ -176,16 +178,21 @@ namespace {
 // correspondence chunk gives >= ~8 waves of equal-cost CTAs while keeping each CTA above
 // ~1M pair votes so its prologue (cell rotations, thresholds, first TMA) stays negligible.
 int build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
-                     int slots, std::vector<rv::VoteItem>& items) {
+                     int slots, std::vector<rv::VoteItem>& items, int force_groups = 0) {
   items.clear();
+  // G = 1 unless a smaller CTA saves more than 5% of the thread slots
   int groups = 1;
-  int64_t best_pad = -1;
-  for (int G : {1, 2, 4}) {
+  int64_t pad1 = 0;
+  for (size_t s = 0; s < ncell.size(); ++s)
+    pad1 += (ncell[s] + rv::kCellsPerBlock - 1) / rv::kCellsPerBlock * rv::kCellsPerBlock;
+  int64_t best_pad = pad1;
+  for (int G : {2, 4}) {
     const int64_t cpb = rv::kCellsPerBlock / G;
     int64_t padded = 0;
     for (size_t s = 0; s < ncell.size(); ++s) padded += (ncell[s] + cpb - 1) / cpb * cpb;
-    if (best_pad < 0 || padded < best_pad) { best_pad = padded; groups = G; }
+    if (padded < best_pad && (double)padded < 0.95 * (double)pad1) { best_pad = padded; groups = G; }
   }
+  if (force_groups == 1 || force_groups == 2 || force_groups == 4) groups = force_groups;
   const int64_t cpb = rv::kCellsPerBlock / groups;
   double work = 0;  // CTA-correspondence units
   for (size_t s = 0; s < ncell.size(); ++s)
@@ -213,7 +220,7 @@ int build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64_
 void build_exact_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
                        std::vector<rv::VoteItem>& items) {
   items.clear();
-  const int64_t chunk = 1 << 16;
+  const int64_t chunk = 1 << 13;  // >= 1 wave of CTAs even for a single block at N = 1e6
   for (size_t s = 0; s < ncell.size(); ++s)
     for (int64_t c = 0; c < ncell[s]; ++c)
       for (int64_t i0 = 0; i0 < ncorr[s]; i0 += chunk)
@@ -303,7 +310,8 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
   std::vector<rv::VoteItem> items;
   int groups = 1;
   if (mode == RV_MODE_EXACT) build_exact_items(ncell, ncorr, items);
-  else groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items);
+  else groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items,
+                                 ctx->force_groups);
 
   RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
   RV_CUDA(ctx->vitems.ensure(std::max<size_t>(1, items.size())), "allocating items");
@@ -584,7 +592,8 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   std::vector<rv::VoteItem> items;
   int groups = 1;
   if (mode == RV_MODE_EXACT) build_exact_items(ncell, ncorr, items);
-  else groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items);
+  else groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items,
+                                 ctx->force_groups);
   RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
   RV_CUDA(ctx->vitems.ensure(std::max<size_t>(1, items.size())), "allocating items");
   RV_CUDA(ctx->up.ensure(total * 4 + segs.size() * sizeof(rv::VoteSeg) +
@@ -810,6 +819,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
     }
   }
   ctx->stream = (cudaStream_t)cfg->stream;
+  if (const char* fg = getenv("RV_VOTE_GROUPS")) ctx->force_groups = atoi(fg);
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);

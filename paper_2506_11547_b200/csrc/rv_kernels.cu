@@ -139,14 +139,15 @@ __device__ __forceinline__ void add_sign(uint32_t& acc, float v) {
 }
 
 template <int MODE, int G>
-__global__ void __launch_bounds__(kVoteThreads + 32, 2)
+__global__ void __launch_bounds__(kVoteThreads + 32, kVoteMinBlocks)
     rv_vote_kernel(const float* __restrict__ k9, int64_t stride, const VoteSeg* __restrict__ segs,
                    const VoteItem* __restrict__ items, float guard) {
   constexpr int TPG = kVoteThreads / G;               // voting threads per group
   constexpr int CPB = TPG * kCellsPerThread;          // cells per CTA
   __shared__ __align__(128) float sK[kStages][9][kTile];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  __shared__ uint32_t red[G > 1 ? 2 * kVoteThreads * kCellsPerThread : 1];
+  static_assert(2 * kVoteThreads * kCellsPerThread <= kStages * 9 * kTile, "red aliases sK");
+  uint32_t* red = reinterpret_cast<uint32_t*>(&sK[0][0][0]);  // epilogue only (G > 1)
 
   const VoteItem it = items[blockIdx.x];
   const VoteSeg& sg = segs[it.seg];
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(kVoteThreads + 32, 2)
       }
     }
   } else {
+    __syncthreads();  // every tile consumed: sK is free to hold the per-group partial counts
     if (tid < kVoteThreads) {
 #pragma unroll
       for (int c = 0; c < kCellsPerThread; ++c) {

@@ -6,13 +6,29 @@
 
 namespace rv {
 
-constexpr int kVoteThreads = 256;                  // K3 block
-constexpr int kCellsPerThread = 4;                 // K3 register blocking (cells per thread)
+#ifndef RV_CPT
+#define RV_CPT 4
+#endif
+#ifndef RV_TILE
+#define RV_TILE 256
+#endif
+#ifndef RV_STAGES
+#define RV_STAGES 4
+#endif
+#ifndef RV_VOTERS
+#define RV_VOTERS 256
+#endif
+#ifndef RV_MINB
+#define RV_MINB 2
+#endif
+constexpr int kVoteThreads = RV_VOTERS;            // K3 voting threads (+1 producer warp)
+constexpr int kVoteMinBlocks = RV_MINB;            // K3 CTAs per SM the registers are sized for
+constexpr int kCellsPerThread = RV_CPT;            // K3 register blocking (cells per thread)
 constexpr int kCellsPerBlock = kVoteThreads * kCellsPerThread;
-constexpr int kTile = 256;                         // correspondences per TMA stage
-constexpr int kStages = 4;
+constexpr int kTile = RV_TILE;                     // correspondences per TMA stage
+constexpr int kStages = RV_STAGES;
 constexpr int kRefThreads = 256;                   // K6/K7 block
-constexpr int kRefRowsPerItem = 8192;              // K6 rows per block (multiple of 32)
+constexpr int kRefRowsPerItem = 2048;              // K6 rows per block (multiple of 32)
 
 // One problem's block list for a vote launch.
 struct VoteSeg {

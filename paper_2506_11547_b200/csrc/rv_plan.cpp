@@ -70,33 +70,43 @@ struct rv_plan {
     return (double)ub - (double)n * (1.0 - t) * 0.5;
   }
 
-  // index of the max-excess block, ties -> lowest lin (cells are ascending)
+  // index of the max-excess block, ties -> lowest lin
   size_t best_excess(int32_t B, const std::vector<uint32_t>& c, const uint32_t* ub) const {
     size_t best = 0;
     double be = -1e300;
     for (size_t e = 0; e < c.size(); ++e) {
       double x = excess(B, c[e], ub[e]);
-      if (x > be) { be = x; best = e; }
+      if (x > be || (x == be && c[e] < c[best])) { be = x; best = e; }
     }
     return best;
   }
 
-  // candidate children at level l+1 of a sorted list of level-l blocks (ascending output)
+  // candidate children at level l+1 of level-l blocks, in generation order (parents in the
+  // given order, children in (a,b,c) order).  The order is deterministic, so every rank
+  // builds the identical list; no decision depends on it (ties are broken by lin).
   std::vector<uint32_t> children(int l, const std::vector<uint32_t>& parents) const {
     const int32_t B = chain[l], Bc = chain[l + 1], f = Bc / B;
     std::vector<uint32_t> out;
     out.reserve(parents.size() * (size_t)(f * f * f));
+    const int64_t BB = (int64_t)B * B;
     for (uint32_t p : parents) {
       int32_t i, j, k;
       rv::lin_to_ijk(p, B, i, j, k);
+      // (B * farthest corner distance)^2 <= B^2  =>  every child meets the ball
+      int64_t dmax2 = 0;
+      for (int32_t v : {i, j, k}) {
+        int64_t lo = 2 * (int64_t)v - B, hi = lo + 2;
+        int64_t d = std::max(lo < 0 ? -lo : lo, hi < 0 ? -hi : hi);
+        dmax2 += d * d;
+      }
+      const bool inside = dmax2 <= BB;
       for (int32_t a = 0; a < f; ++a)
         for (int32_t b = 0; b < f; ++b)
           for (int32_t c = 0; c < f; ++c) {
             int32_t ci = f * i + a, cj = f * j + b, ck = f * k + c;
-            if (rv::is_candidate(Bc, ci, cj, ck)) out.push_back(rv::ijk_to_lin(ci, cj, ck, Bc));
+            if (inside || rv::is_candidate(Bc, ci, cj, ck)) out.push_back(rv::ijk_to_lin(ci, cj, ck, Bc));
           }
     }
-    std::sort(out.begin(), out.end());
     return out;
   }
 

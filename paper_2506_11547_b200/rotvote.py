@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librotvote.so")
+LIB_PATH = os.environ.get("RV_LIB") or os.path.join(_HERE, "librotvote.so")  # RV_LIB: tuning variants
 
 RV_OK, RV_EINVAL, RV_EDATA, RV_ECUDA, RV_ENCCL, RV_ENOMEM = 0, -1, -2, -3, -4, -5
 RV_REFINED, RV_DEGENERATE, RV_RECHECKED = 1, 2, 4
