@@ -194,18 +194,36 @@ int build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64_
   }
   if (force_groups == 1 || force_groups == 2 || force_groups == 4) groups = force_groups;
   const int64_t cpb = rv::kCellsPerBlock / groups;
-  double work = 0;  // CTA-correspondence units
-  for (size_t s = 0; s < ncell.size(); ++s)
-    work += (double)((ncell[s] + cpb - 1) / cpb) * (double)pad4(ncorr[s]);
-  int64_t chunk = (int64_t)std::ceil(work / ((double)slots * 8.0));
-  chunk = std::max<int64_t>(chunk, (1 << 20) / cpb);
-  chunk = std::min<int64_t>(chunk, 1 << 16);
-  chunk = (chunk + rv::kTile - 1) / rv::kTile * rv::kTile;
+  // correspondence chunks: one chunk count per launch, picked so the CTA count fills whole
+  // waves (items / slots just below an integer), with 4..64 waves and CTAs of >= 2^20 pair
+  // slots (their prologue -- cell rotations, thresholds, first TMA -- stays negligible)
+  int64_t cbs = 0, nmax = 0;
+  for (size_t s = 0; s < ncell.size(); ++s) {
+    if (ncell[s] == 0 || ncorr[s] == 0) continue;
+    cbs += (ncell[s] + cpb - 1) / cpb;
+    nmax = std::max<int64_t>(nmax, pad4(ncorr[s]));
+  }
+  if (cbs == 0) return groups;
+  const int64_t min_chunk = std::min<int64_t>(nmax, std::max<int64_t>(256, (1 << 20) / cpb));
+  const int64_t max_nch = std::max<int64_t>(1, nmax / min_chunk);
+  int64_t best_nch = 1;
+  double best_eff = -1;
+  for (int64_t nch = 1; nch <= max_nch; ++nch) {
+    const int64_t items_n = cbs * nch;
+    const double waves = (double)items_n / slots;
+    if (waves > 64.0 && nch > 1) break;
+    const double eff = waves / std::ceil(waves);
+    // prefer >= 4 waves (dynamic balance), then the fullest last wave
+    const double score = eff - (waves < 4.0 ? 0.5 * (4.0 - waves) / 4.0 : 0.0);
+    if (score > best_eff + 1e-9) { best_eff = score; best_nch = nch; }
+  }
   for (size_t s = 0; s < ncell.size(); ++s) {
     const int64_t n4 = pad4(ncorr[s]);
     if (ncell[s] == 0 || n4 == 0) continue;
     const int64_t cb = (ncell[s] + cpb - 1) / cpb;
     const int64_t per = (ncell[s] + cb - 1) / cb;  // balanced cells per CTA
+    const int64_t nch = std::min<int64_t>(best_nch, std::max<int64_t>(1, n4 / 4));
+    const int64_t chunk = (n4 / 4 + nch - 1) / nch * 4;  // balanced, multiple of 4
     for (int64_t b = 0; b < cb; ++b) {
       const int64_t c0 = b * per, nc = std::min(per, ncell[s] - c0);
       if (nc <= 0) continue;
