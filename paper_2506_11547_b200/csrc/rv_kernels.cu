@@ -139,7 +139,7 @@ __device__ __forceinline__ void add_sign(uint32_t& acc, float v) {
 }
 
 template <int MODE, int G>
-__global__ void __launch_bounds__(kVoteThreads + 32, kVoteMinBlocks)
+__global__ void __launch_bounds__(kVoteThreads + kProducerThreads, kVoteMinBlocks)
     rv_vote_kernel(const float* __restrict__ k9, int64_t stride, const VoteSeg* __restrict__ segs,
                    const VoteItem* __restrict__ items, float guard) {
   constexpr int TPG = kVoteThreads / G;               // voting threads per group
@@ -163,37 +163,43 @@ __global__ void __launch_bounds__(kVoteThreads + 32, kVoteMinBlocks)
     mbar_fence_init();
   }
   __syncthreads();
-
-  if (tid >= kVoteThreads) {
-    // ---------------- producer warp ----------------
-    if (tid == kVoteThreads) {
-      const float* base = k9 + sg.koff + it.i0;
-      for (int t = 0; t < ntiles; ++t) {
-        const int st = t % kStages;
-        if (t >= kStages) mbar_wait(&empty[st], (uint32_t)(((t / kStages) - 1) & 1));
-        const int cnt = min(kTile, it.ni - t * kTile);
-        const uint32_t bytes = (uint32_t)cnt * 4u;
-        mbar_expect_tx(&full[st], bytes * 9u);
+  const float* kbase = k9 + sg.koff + it.i0;
+  auto issue = [&](int t) {  // TMA bulk copies of tile t (9 rows) into stage t % kStages
+    const int st = t % kStages;
+    const int cnt = min(kTile, it.ni - t * kTile);
+    const uint32_t bytes = (uint32_t)cnt * 4u;
+    mbar_expect_tx(&full[st], bytes * 9u);
 #pragma unroll
-        for (int j = 0; j < 9; ++j)
-          tma_bulk_g2s(&sK[st][j][0], base + j * stride + (int64_t)t * kTile, bytes, &full[st]);
+    for (int j = 0; j < 9; ++j)
+      tma_bulk_g2s(&sK[st][j][0], kbase + j * stride + (int64_t)t * kTile, bytes, &full[st]);
+  };
+
+  // ---------------- producer (RV_PIPE == 1: a dedicated warp) ----------------
+  if (kProducerThreads > 0 && tid >= kVoteThreads) {
+    if (tid == kVoteThreads)
+      for (int t = 0; t < ntiles; ++t) {
+        if (t >= kStages) mbar_wait(&empty[t % kStages], (uint32_t)(((t / kStages) - 1) & 1));
+        issue(t);
       }
-    }
   }
+  if (kProducerThreads == 0 && tid == 0)
+    for (int t = 0; t < kStages && t < ntiles; ++t) issue(t);
+
   // ---------------- voters ----------------
   const int g = tid / TPG;           // group of this voter
   const int local = tid % TPG;
+  const bool voter = tid < kVoteThreads;
   float phi[kCellsPerThread][9];
   float init[kCellsPerThread];
   uint32_t neg_a[kCellsPerThread], neg_b[kCellsPerThread];
   const float two_g = 2.0f * guard;
-  if (tid < kVoteThreads) {
+  {
     const int32_t B = sg.B;
     const double tau = cos(sg.eps);
 #pragma unroll
     for (int c = 0; c < kCellsPerThread; ++c) {
       int e = local + c * TPG;
-      if (e >= it.ncell) e = 0;  // inactive slot: recompute cell 0, never stored
+      if (e >= it.ncell || !voter) e = 0;  // inactive slot: recompute cell 0, never stored
       const uint32_t lin = sg.lins[it.cell0 + e];
       int32_t i, j, k;
       lin_to_ijk(lin, B, i, j, k);
@@ -207,7 +213,9 @@ __global__ void __launch_bounds__(kVoteThreads + 32, kVoteMinBlocks)
       init[c] = (float)(-thr);
       neg_a[c] = neg_b[c] = 0;
     }
-    const int warp = tid >> 5, lane = tid & 31;
+  }
+  if (voter) {
+    const int lane = tid & 31;
     for (int t = 0; t < ntiles; ++t) {
       const int st = t % kStages;
       mbar_wait(&full[st], (uint32_t)((t / kStages) & 1));
@@ -228,6 +236,7 @@ __global__ void __launch_bounds__(kVoteThreads + 32, kVoteMinBlocks)
             lo = __ffma2_rn(f2, make_float2(kk[j].x, kk[j].y), lo);
             hi = __ffma2_rn(f2, make_float2(kk[j].z, kk[j].w), hi);
           }
+#if RV_COUNT_ASM
           add_sign(neg_a[c], lo.x);
           add_sign(neg_a[c], lo.y);
           add_sign(neg_a[c], hi.x);
@@ -238,12 +247,22 @@ __global__ void __launch_bounds__(kVoteThreads + 32, kVoteMinBlocks)
             add_sign(neg_b[c], hi.x - two_g);
             add_sign(neg_b[c], hi.y - two_g);
           }
+#else
+          neg_a[c] += sign_bit(lo.x) + sign_bit(lo.y) + sign_bit(hi.x) + sign_bit(hi.y);
+          if (MODE == RV_MODE_FINAL)
+            neg_b[c] += sign_bit(lo.x - two_g) + sign_bit(lo.y - two_g) + sign_bit(hi.x - two_g) +
+                        sign_bit(hi.y - two_g);
+#endif
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      if (kProducerThreads > 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      } else {
+        __syncthreads();  // stage st fully consumed by every voter
+        if (tid == 0 && t + kStages < ntiles) issue(t + kStages);
+      }
     }
-    (void)warp;
   }
 
   // epilogue: counts = processed - negatives - zero-padding rows that counted as >= 0
@@ -299,7 +318,8 @@ __global__ void __launch_bounds__(kVoteThreads + 32, kVoteMinBlocks)
 template <int MODE, int G>
 static void launch_vote_t(const float* k9, int64_t stride, const VoteSeg* segs,
                           const VoteItem* items, int32_t n_items, float guard, cudaStream_t s) {
-  rv_vote_kernel<MODE, G><<<n_items, kVoteThreads + 32, 0, s>>>(k9, stride, segs, items, guard);
+  rv_vote_kernel<MODE, G><<<n_items, kVoteThreads + kProducerThreads, 0, s>>>(k9, stride, segs,
+                                                                             items, guard);
 }
 
 void launch_vote(int mode, int groups, const float* k9, int64_t stride, const VoteSeg* segs,

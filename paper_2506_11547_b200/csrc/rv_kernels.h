@@ -21,8 +21,15 @@ namespace rv {
 #ifndef RV_MINB
 #define RV_MINB 2
 #endif
+#ifndef RV_PIPE
+#define RV_PIPE 0   // 0: thread 0 refills a stage after a block barrier; 1: producer warp + mbarriers
+#endif
+#ifndef RV_COUNT_ASM
+#define RV_COUNT_ASM 0
+#endif
 constexpr int kVoteThreads = RV_VOTERS;            // K3 voting threads (+1 producer warp)
 constexpr int kVoteMinBlocks = RV_MINB;            // K3 CTAs per SM the registers are sized for
+constexpr int kProducerThreads = RV_PIPE ? 32 : 0; // dedicated TMA producer warp
 constexpr int kCellsPerThread = RV_CPT;            // K3 register blocking (cells per thread)
 constexpr int kCellsPerBlock = kVoteThreads * kCellsPerThread;
 constexpr int kTile = RV_TILE;                     // correspondences per TMA stage

@@ -10,11 +10,11 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VARIANTS = {"base": {},
-            "t512_s2": {"RV_TILE": 512, "RV_STAGES": 2},
-            "cpt2_minb3": {"RV_CPT": 2, "RV_MINB": 3},
-            "cpt4_v512_minb1": {"RV_VOTERS": 512, "RV_MINB": 1},
-            "cpt8_v256_minb1": {"RV_CPT": 8, "RV_MINB": 1}}
+VARIANTS = {"pipe0": {"RV_PIPE": 0}, "pipe0_s3": {"RV_PIPE": 0, "RV_STAGES": 3},
+            "pipe0_asm": {"RV_PIPE": 0, "RV_COUNT_ASM": 1}, "pipe1": {"RV_PIPE": 1},
+            "pipe1_asm": {"RV_PIPE": 1, "RV_COUNT_ASM": 1},
+            "pipe0_cpt2_minb3": {"RV_PIPE": 0, "RV_CPT": 2, "RV_MINB": 3},
+            "pipe0_t512_s2": {"RV_PIPE": 0, "RV_TILE": 512, "RV_STAGES": 2}}
 
 
 def build():
