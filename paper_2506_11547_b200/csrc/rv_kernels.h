@@ -25,7 +25,7 @@ namespace rv {
 #define RV_PIPE 0   // 0: thread 0 refills a stage after a block barrier; 1: producer warp + mbarriers
 #endif
 #ifndef RV_COUNT_ASM
-#define RV_COUNT_ASM 0
+#define RV_COUNT_ASM 1
 #endif
 constexpr int kVoteThreads = RV_VOTERS;            // K3 voting threads (+1 producer warp)
 constexpr int kVoteMinBlocks = RV_MINB;            // K3 CTAs per SM the registers are sized for
