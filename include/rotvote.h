@@ -69,7 +69,8 @@ typedef struct {
   int32_t rank;          /* 0 for a single GPU */
   int32_t world;         /* 1 for a single GPU; > 1: NCCL over NVLink, cells sharded */
   const void* nccl_id;   /* HOST, 128-byte ncclUniqueId from rot_vote_get_unique_id on rank 0,
-                            broadcast by the caller; NULL when world == 1 */
+                            broadcast by the caller; required when world > 1.  With world == 1 a
+                            non-NULL id creates a 1-rank communicator and takes the NCCL path. */
   int64_t max_n;         /* workspace sizing: solve with n > max_n -> RV_EINVAL
                             (batched: total correspondences) */
   int32_t max_problems;  /* batched sizing (>= 1) */

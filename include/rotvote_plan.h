@@ -49,6 +49,9 @@ void rv_plan_destroy(rv_plan* p);
 /* 1 if a request is pending (outputs set; lins valid until the next feed), 0 when done. */
 int  rv_plan_request(const rv_plan* p, int32_t* B, int32_t* mode, int64_t* m,
                      const uint32_t** lins);
+/* 1 if the pending request is the complete candidate list of its grid (level 0, or the
+ * exhaustive scan), i.e. identical to rv_grid_candidates(B); 0 otherwise. */
+int  rv_plan_request_is_full_grid(const rv_plan* p);
 /* Feed the counts of the pending request (HOST arrays of m entries).  0 or -1. */
 int  rv_plan_feed(rv_plan* p, const uint32_t* cnt_a, const uint32_t* cnt_b);
 /* 0 when done and *out filled, -1 while requests are pending. */

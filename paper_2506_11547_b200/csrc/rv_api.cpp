@@ -136,6 +136,9 @@ struct rv_ctx {
   DevBuf<float> hx, hy;          // device copies for rot_vote_solve_host
   DevBuf<uint32_t> hmask;
   DevBuf<char> gather;           // batched result all-gather
+  DevBuf<uint32_t> grid_list;    // device copy of one grid's full candidate list (batched L0)
+  int32_t grid_list_B = 0;
+  int64_t grid_list_m = 0;
   Staging up, down;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evv0 = nullptr, evv1 = nullptr;
   // per-call counters reported in rv_result
@@ -296,15 +299,16 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
   const int64_t per_rank = 2 * chunk;  // [a | b]
   // ranks evaluated by this process
   int r_lo = 0, r_hi = W;
-  if (ctx->cfg.world > 1) { r_lo = ctx->cfg.rank; r_hi = r_lo + 1; }
+  const bool nccl_path = ctx->comm != nullptr;  // world > 1, or world 1 with an NCCL id
+  if (nccl_path) { r_lo = ctx->cfg.rank; r_hi = r_lo + 1; }
   const int nr = r_hi - r_lo;
 
   RV_CUDA(ctx->lins.ensure(std::max<int64_t>(1, chunk * nr)), "allocating block list");
   // gathered counts [W][2*chunk] + (world>1) local [2*chunk]
-  const size_t cnt_need = (size_t)per_rank * W + (ctx->cfg.world > 1 ? per_rank : 0) + 1;
+  const size_t cnt_need = (size_t)per_rank * W + (nccl_path ? per_rank : 0) + 1;
   RV_CUDA(ctx->cnt.ensure(cnt_need), "allocating counts");
   uint32_t* gathered = ctx->cnt.p;
-  uint32_t* local = ctx->cfg.world > 1 ? ctx->cnt.p + per_rank * W : nullptr;
+  uint32_t* local = nccl_path ? ctx->cnt.p + per_rank * W : nullptr;
 
   std::vector<int64_t> ncell, ncorr;
   std::vector<rv::VoteSeg> segs;
@@ -371,7 +375,7 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
   }
   ctx->launches += items.empty() ? 0 : 1;
   RV_CUDA(cudaGetLastError(), "launching the vote kernel");
-  if (ctx->cfg.world > 1) {
+  if (nccl_path) {
     ncclResult_t nr_ = nccl().AllGather(local, gathered, (size_t)per_rank, ncclUint32, ctx->comm, s);
     if (nr_ != ncclSuccess)
       return ctx->fail(RV_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(nr_));
@@ -578,6 +582,7 @@ struct BatchReq {
   int32_t B, mode;
   int64_t m;
   const uint32_t* lins;
+  bool full_grid;      // the complete candidate list of B: served from one device copy
 };
 
 int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
@@ -585,16 +590,27 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                const std::vector<BatchReq>& reqs, std::vector<std::vector<uint32_t>>& ca,
                std::vector<std::vector<uint32_t>>& cb) {
   if (reqs.empty()) return RV_OK;
-  int64_t total = 0;
-  for (const BatchReq& r : reqs) total += r.m;
-  RV_CUDA(ctx->lins.ensure(total), "allocating block list");
+  int64_t total = 0, upload = 0;
+  for (const BatchReq& r : reqs) {
+    total += r.m;
+    if (!r.full_grid) upload += r.m;
+  }
+  for (const BatchReq& r : reqs)
+    if (r.full_grid && (ctx->grid_list_B != r.B || ctx->grid_list_m != r.m)) {
+      RV_CUDA(ctx->grid_list.ensure(r.m), "allocating grid list");
+      RV_CUDA(cudaMemcpy(ctx->grid_list.p, r.lins, r.m * 4, cudaMemcpyHostToDevice), "H2D grid");
+      ctx->grid_list_B = r.B;
+      ctx->grid_list_m = r.m;
+    }
+  RV_CUDA(ctx->lins.ensure(std::max<int64_t>(1, upload)), "allocating block list");
   RV_CUDA(ctx->cnt.ensure(2 * total), "allocating counts");
   std::vector<int64_t> ncell, ncorr;
   std::vector<rv::VoteSeg> segs;
-  int64_t off = 0;
+  int64_t off = 0, uoff = 0;
   for (const BatchReq& r : reqs) {
     rv::VoteSeg sg{};
-    sg.lins = ctx->lins.p + off;
+    sg.lins = r.full_grid ? ctx->grid_list.p : ctx->lins.p + uoff;
+    if (!r.full_grid) uoff += r.m;
     sg.cnt_a = ctx->cnt.p + off;
     sg.cnt_b = ctx->cnt.p + total + off;
     sg.koff = koff[r.prob];
@@ -614,13 +630,14 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                                  ctx->force_groups);
   RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
   RV_CUDA(ctx->vitems.ensure(std::max<size_t>(1, items.size())), "allocating items");
-  RV_CUDA(ctx->up.ensure(total * 4 + segs.size() * sizeof(rv::VoteSeg) +
+  RV_CUDA(ctx->up.ensure(upload * 4 + segs.size() * sizeof(rv::VoteSeg) +
                          items.size() * sizeof(rv::VoteItem) + 4096), "allocating staging");
   RV_CUDA(ctx->down.ensure(2 * total * 4 + 256), "allocating staging");
   ctx->up.reset();
-  uint32_t* hl = ctx->up.take<uint32_t>(total);
+  uint32_t* hl = ctx->up.take<uint32_t>(std::max<int64_t>(1, upload));
   off = 0;
   for (const BatchReq& r : reqs) {
+    if (r.full_grid) continue;
     std::memcpy(hl + off, r.lins, r.m * 4);
     off += r.m;
   }
@@ -629,13 +646,15 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   rv::VoteItem* hi = ctx->up.take<rv::VoteItem>(std::max<size_t>(1, items.size()));
   if (!items.empty()) std::memcpy(hi, items.data(), items.size() * sizeof(rv::VoteItem));
   cudaStream_t s = ctx->stream;
-  RV_CUDA(cudaMemcpyAsync(ctx->lins.p, hl, total * 4, cudaMemcpyHostToDevice, s), "H2D");
+  if (upload > 0)
+    RV_CUDA(cudaMemcpyAsync(ctx->lins.p, hl, upload * 4, cudaMemcpyHostToDevice, s), "H2D");
   RV_CUDA(cudaMemcpyAsync(ctx->vsegs.p, hs, segs.size() * sizeof(rv::VoteSeg),
                           cudaMemcpyHostToDevice, s), "H2D");
   if (!items.empty())
     RV_CUDA(cudaMemcpyAsync(ctx->vitems.p, hi, items.size() * sizeof(rv::VoteItem),
                             cudaMemcpyHostToDevice, s), "H2D");
-  RV_CUDA(cudaMemsetAsync(ctx->cnt.p, 0, 2 * total * 4, s), "memset");
+  const int64_t ncnt = (mode == RV_MODE_FINAL ? 2 : 1) * total;  // cnt_b only in FINAL mode
+  RV_CUDA(cudaMemsetAsync(ctx->cnt.p, 0, ncnt * 4, s), "memset");
   if (mode == RV_MODE_EXACT) {
     rv::launch_exact(ctx->k9.p, ctx->stride, x, y, ctx->vsegs.p, ctx->vitems.p,
                      (int32_t)items.size(), ctx->cfg.guard, s);
@@ -651,7 +670,7 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   RV_CUDA(cudaGetLastError(), "launching the vote kernel");
   ctx->down.reset();
   uint32_t* hc = ctx->down.take<uint32_t>(2 * total);
-  RV_CUDA(cudaMemcpyAsync(hc, ctx->cnt.p, 2 * total * 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hc, ctx->cnt.p, ncnt * 4, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaStreamSynchronize(s), "batched vote");
   if (mode != RV_MODE_EXACT && !items.empty()) {
     float ms = 0;
@@ -661,7 +680,7 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   off = 0;
   for (const BatchReq& r : reqs) {
     ca[r.prob].assign(hc + off, hc + off + r.m);
-    cb[r.prob].assign(hc + total + off, hc + total + off + r.m);
+    if (mode == RV_MODE_FINAL) cb[r.prob].assign(hc + total + off, hc + total + off + r.m);
     off += r.m;
   }
   return RV_OK;
@@ -703,6 +722,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
         BatchReq r;
         r.prob = p;
         if (rv_plan_request(plans[p], &r.B, &r.mode, &r.m, &r.lins)) {
+          r.full_grid = rv_plan_request_is_full_grid(plans[p]) != 0;
           by_mode[r.mode].push_back(r);
           any = true;
         }
@@ -755,7 +775,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
     r.launches = ctx->launches;
     r.vote_launches = ctx->vote_launches;
   }
-  if (W == 1) {
+  if (!ctx->comm) {
     std::memcpy(out, local.data(), (size_t)P * sizeof(rv_result));
     return RV_OK;
   }
@@ -822,6 +842,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
   if (!cfg) return RV_EINVAL;
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return RV_EINVAL;
   if (cfg->world > 1 && (!cfg->nccl_id || cfg->emulate_world > 1)) return RV_EINVAL;
+  if (cfg->nccl_id && cfg->emulate_world > 1) return RV_EINVAL;
   if (cfg->max_n < 2 || cfg->max_n > ((int64_t)1 << 31) - 4096) return RV_EINVAL;
   if (cfg->max_problems < 1 || cfg->refine_rounds < 0 || !(cfg->guard >= 0.0f)) return RV_EINVAL;
   if (cfg->chain_len < 0 || cfg->chain_len > RV_MAX_CHAIN) return RV_EINVAL;
@@ -856,7 +877,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
     rot_vote_destroy(ctx);
     return code;
   }
-  if (cfg->world > 1) {
+  if (cfg->nccl_id) {  // world > 1, or a 1-rank communicator (exercises the NCCL path)
     NcclApi& a = nccl();
     if (!a.ok) {
       rot_vote_destroy(ctx);
@@ -881,7 +902,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->vitems.release(); ctx->rsegs.release(); ctx->ritems.release(); ctx->partials.release();
   ctx->qs.release(); ctx->flags.release(); ctx->ninl.release(); ctx->rows.release();
   ctx->koffs.release(); ctx->bad.release(); ctx->hx.release(); ctx->hy.release();
-  ctx->hmask.release(); ctx->gather.release();
+  ctx->hmask.release(); ctx->gather.release(); ctx->grid_list.release();
   ctx->up.release(); ctx->down.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);

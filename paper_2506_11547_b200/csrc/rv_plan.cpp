@@ -277,6 +277,10 @@ int rv_plan_request(const rv_plan* p, int32_t* B, int32_t* mode, int64_t* m, con
   return 1;
 }
 
+int rv_plan_request_is_full_grid(const rv_plan* p) {
+  return p && p->phase == PH_L0 ? 1 : 0;
+}
+
 int rv_plan_feed(rv_plan* p, const uint32_t* cnt_a, const uint32_t* cnt_b) {
   if (!p) return -1;
   return p->feed(cnt_a, cnt_b);

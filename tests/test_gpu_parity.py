@@ -328,3 +328,26 @@ def test_determinism(rv, torch_cuda):
     b = rv.solve(x, y, pr.eps)
     assert (a.cell, a.votes, a.pair_votes) == (b.cell, b.votes, b.pair_votes)
     assert np.array_equal(a.q, b.q)
+
+
+def test_nccl_path_single_rank(torch_cuda):
+    """world = 1 with an NCCL id runs the sharded path through a real 1-rank communicator
+    (ncclCommInitRank + ncclAllGather of the counts, dlopen'ed libnccl) and must give the
+    same answer as the direct path; batched results go through the result all-gather."""
+    from paper_2506_11547_b200 import RotVote, rot_vote_get_unique_id
+    torch = torch_cuda
+    pr = datagen.cfg2(seed=3)
+    x, y = dev(torch, pr.x), dev(torch, pr.y)
+    plain = RotVote(max_n=1 << 16)
+    viaccl = RotVote(max_n=1 << 16, max_problems=8, nccl_id=rot_vote_get_unique_id())
+    a, b = plain.solve(x, y, pr.eps), viaccl.solve(x, y, pr.eps)
+    assert (a.cell, a.votes, a.n_tied, a.pair_votes) == (b.cell, b.votes, b.n_tied, b.pair_votes)
+    assert np.array_equal(a.q, b.q)
+    probs = [datagen.make_problem(500 + 37 * p, 100, 0.01, 0.05, seed=[4, p]) for p in range(5)]
+    bt = datagen.batch_of(probs, 0.05)
+    rb = viaccl.solve_batched(dev(torch, bt.x), dev(torch, bt.y), bt.offsets, bt.eps)
+    for p, r in zip(probs, rb):
+        s = plain.solve(dev(torch, p.x), dev(torch, p.y), bt.eps)
+        assert (r.cell, r.votes) == (s.cell, s.votes) and np.array_equal(r.q, s.q)
+    plain.close()
+    viaccl.close()
