@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -108,6 +109,29 @@ struct Staging {
 };
 
 inline int64_t pad4(int64_t n) { return (n + 3) & ~(int64_t)3; }
+
+// Host-side parallel loop for the per-problem planner work of batched solves (planners are
+// independent objects; each index is touched by exactly one thread).  RV_HOST_THREADS caps it.
+template <class F>
+void parallel_for(int64_t n, F f) {
+  static const int hw = [] {
+    int t = (int)std::thread::hardware_concurrency();
+    if (const char* e = getenv("RV_HOST_THREADS")) t = atoi(e);
+    return std::max(1, std::min(t, 32));
+  }();
+  const int T = (int)std::min<int64_t>(hw, (n + 63) / 64);
+  if (T <= 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T);
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      for (int64_t i = n * t / T; i < n * (t + 1) / T; ++i) f(i);
+    });
+  for (std::thread& x : th) x.join();
+}
 
 }  // namespace
 
@@ -710,10 +734,12 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
     if (int rc = check_bad(ctx)) return rc;
     std::vector<rv_plan*> plans(PL, nullptr);
     int rc = RV_OK;
+    parallel_for(PL, [&](int64_t p) {
+      rv_plan_create(ctx->chain.data(), (int32_t)ctx->chain.size(), levels,
+                     rows[p + 1] - rows[p], eps, (double)ctx->cfg.guard, &plans[p]);
+    });
     for (int32_t p = 0; p < PL && !rc; ++p)
-      if (rv_plan_create(ctx->chain.data(), (int32_t)ctx->chain.size(), levels,
-                         rows[p + 1] - rows[p], eps, (double)ctx->cfg.guard, &plans[p]) != 0)
-        rc = ctx->fail(RV_EINVAL, "invalid search plan");
+      if (!plans[p]) rc = ctx->fail(RV_EINVAL, "invalid search plan");
     std::vector<std::vector<uint32_t>> ca(PL), cb(PL);
     while (!rc) {
       std::vector<BatchReq> by_mode[3];
@@ -730,9 +756,15 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
       if (!any) break;
       for (int md = 0; md < 3 && !rc; ++md) {
         rc = eval_batch(ctx, x, y, rows, koff, eps, md, by_mode[md], ca, cb);
-        for (const BatchReq& r : by_mode[md])
-          if (!rc && rv_plan_feed(plans[r.prob], ca[r.prob].data(), cb[r.prob].data()) != 0)
-            rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
+        if (rc) break;
+        const std::vector<BatchReq>& grp = by_mode[md];
+        std::vector<int> bad(grp.size(), 0);
+        parallel_for((int64_t)grp.size(), [&](int64_t q) {
+          const BatchReq& r = grp[q];
+          bad[q] = rv_plan_feed(plans[r.prob], ca[r.prob].data(), cb[r.prob].data()) != 0;
+        });
+        for (int b : bad)
+          if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
       }
     }
     std::vector<double> q0((size_t)PL * 4), qf((size_t)PL * 4);

@@ -18,6 +18,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "../../include/rotvote.h"
@@ -35,6 +38,44 @@ std::vector<uint32_t> candidates_of(int32_t B) {
       for (int32_t k = 0; k < B; ++k)
         if (rv::is_candidate(B, i, j, k)) out.push_back(rv::ijk_to_lin(i, j, k, B));
   return out;
+}
+
+// Process-wide caches of a grid's candidate list and of the per-candidate uniform-outlier
+// background (1 - cos(min(pi, eps + r(c))))/2 (batched solves create thousands of planners
+// on the same grid and eps).  Entries are never erased, so references stay valid.
+struct GridCache {
+  std::vector<uint32_t> cand;
+  std::map<uint64_t, std::vector<double>> bg;  // keyed by the bits of eps
+};
+std::mutex g_cache_mu;
+std::map<int32_t, std::unique_ptr<GridCache>> g_cache;
+
+GridCache& grid_cache(int32_t B) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  std::unique_ptr<GridCache>& e = g_cache[B];
+  if (!e) {
+    e.reset(new GridCache());
+    e->cand = candidates_of(B);
+  }
+  return *e;
+}
+
+const std::vector<double>* grid_background(int32_t B, double eps) {
+  GridCache& gc = grid_cache(B);
+  uint64_t key;
+  std::memcpy(&key, &eps, sizeof(key));
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = gc.bg.find(key);
+  if (it != gc.bg.end()) return &it->second;
+  if (gc.bg.size() >= 64) return nullptr;  // bounded: fall back to direct evaluation
+  std::vector<double>& v = gc.bg[key];
+  v.resize(gc.cand.size());
+  for (size_t e = 0; e < gc.cand.size(); ++e) {
+    int32_t i, j, k;
+    rv::lin_to_ijk(gc.cand[e], B, i, j, k);
+    v[e] = (1.0 - rv::bound_threshold(B, i, j, k, eps)) * 0.5;
+  }
+  return &v;
 }
 
 }  // namespace
@@ -190,7 +231,16 @@ struct rv_plan {
         if (mode == RV_MODE_FINAL) { enter_final(a, b); return 0; }  // levels == 1
         l0_cells = cells;
         l0_ub.assign(a, a + cells.size());
-        size_t s = best_excess(chain[0], l0_cells, l0_ub.data());
+        size_t s = 0;
+        if (const std::vector<double>* bg = grid_background(chain[0], eps)) {
+          double be = -1e300;
+          for (size_t e = 0; e < l0_cells.size(); ++e) {  // cached (1 - t_c)/2, same order
+            const double x = (double)l0_ub[e] - (double)n * (*bg)[e];
+            if (x > be || (x == be && l0_cells[e] < l0_cells[s])) { be = x; s = e; }
+          }
+        } else {
+          s = best_excess(chain[0], l0_cells, l0_ub.data());
+        }
         phase = PH_DIVE;
         level = 1;
         mode = mode_for(level);
@@ -260,7 +310,7 @@ int rv_plan_create(const int32_t* chain, int32_t chain_len, int32_t levels, int6
   p->phase = PH_L0;
   p->level = 0;
   p->mode = p->mode_for(0);
-  p->cells = candidates_of(p->chain[0]);
+  p->cells = grid_cache(p->chain[0]).cand;
   p->note_request();
   *out = p;
   return 0;
