@@ -40,6 +40,17 @@ std::vector<uint32_t> candidates_of(int32_t B) {
   return out;
 }
 
+// Centre of block (i,j,k) inside the closed unit ball (its rotation is in the q3 <= 0
+// hemisphere proper).  Blocks that merely touch the ball from outside represent rotations of
+// the far side; the dive starts and steps only through inside blocks when there are any
+// (a heuristic -- the certified pruning is unaffected).
+bool centre_inside(int32_t B, uint32_t lin) {
+  int32_t i, j, k;
+  rv::lin_to_ijk(lin, B, i, j, k);
+  const int64_t a = 2 * (int64_t)i + 1 - B, b = 2 * (int64_t)j + 1 - B, c = 2 * (int64_t)k + 1 - B;
+  return a * a + b * b + c * c <= (int64_t)B * B;
+}
+
 // Process-wide caches of a grid's candidate list and of the per-candidate uniform-outlier
 // background (1 - cos(min(pi, eps + r(c))))/2 (batched solves create thousands of planners
 // on the same grid and eps).  Entries are never erased, so references stay valid.
@@ -111,13 +122,18 @@ struct rv_plan {
     return (double)ub - (double)n * (1.0 - t) * 0.5;
   }
 
-  // index of the max-excess block, ties -> lowest lin
-  size_t best_excess(int32_t B, const std::vector<uint32_t>& c, const uint32_t* ub) const {
+  // index of the max-excess block (blocks with their centre inside the ball first), ties ->
+  // lowest lin
+  size_t best_excess(int32_t B, const std::vector<uint32_t>& c, const uint32_t* ub,
+                     const double* bg = nullptr) const {
     size_t best = 0;
     double be = -1e300;
+    bool bin = false;
     for (size_t e = 0; e < c.size(); ++e) {
-      double x = excess(B, c[e], ub[e]);
-      if (x > be || (x == be && c[e] < c[best])) { be = x; best = e; }
+      const bool in = centre_inside(B, c[e]);
+      if (bin && !in) continue;
+      const double x = bg ? (double)ub[e] - (double)n * bg[e] : excess(B, c[e], ub[e]);
+      if ((in && !bin) || x > be || (x == be && c[e] < c[best])) { be = x; best = e; bin = in; }
     }
     return best;
   }
@@ -231,16 +247,8 @@ struct rv_plan {
         if (mode == RV_MODE_FINAL) { enter_final(a, b); return 0; }  // levels == 1
         l0_cells = cells;
         l0_ub.assign(a, a + cells.size());
-        size_t s = 0;
-        if (const std::vector<double>* bg = grid_background(chain[0], eps)) {
-          double be = -1e300;
-          for (size_t e = 0; e < l0_cells.size(); ++e) {  // cached (1 - t_c)/2, same order
-            const double x = (double)l0_ub[e] - (double)n * (*bg)[e];
-            if (x > be || (x == be && l0_cells[e] < l0_cells[s])) { be = x; s = e; }
-          }
-        } else {
-          s = best_excess(chain[0], l0_cells, l0_ub.data());
-        }
+        const std::vector<double>* bg = grid_background(chain[0], eps);  // (1 - t_c)/2, cached
+        size_t s = best_excess(chain[0], l0_cells, l0_ub.data(), bg ? bg->data() : nullptr);
         phase = PH_DIVE;
         level = 1;
         mode = mode_for(level);
