@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -109,6 +110,19 @@ struct Staging {
 };
 
 inline int64_t pad4(int64_t n) { return (n + 3) & ~(int64_t)3; }
+
+// RV_TRACE=1: host-side phase timings of batched solves on stderr (tuning aid)
+struct Trace {
+  bool on = getenv("RV_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[rv] %-28s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
 
 // Host-side parallel loop for the per-problem planner work of batched solves (planners are
 // independent objects; each index is touched by exactly one thread).  RV_HOST_THREADS caps it.
@@ -728,10 +742,12 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
   rv_shard_range(P, ctx->cfg.rank, W, &pb, &pe);
   const int32_t PL = (int32_t)(pe - pb);
   std::vector<rv_result> local(PL);
+  Trace tr;
   if (PL > 0) {
     std::vector<int64_t> rows(offsets + pb, offsets + pe + 1), koff;
     if (int rc = run_setup(ctx, x, y, rows.data(), PL, koff)) return rc;
     if (int rc = check_bad(ctx)) return rc;
+    tr.mark("setup");
     std::vector<rv_plan*> plans(PL, nullptr);
     int rc = RV_OK;
     parallel_for(PL, [&](int64_t p) {
@@ -740,6 +756,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
     });
     for (int32_t p = 0; p < PL && !rc; ++p)
       if (!plans[p]) rc = ctx->fail(RV_EINVAL, "invalid search plan");
+    tr.mark("plans created");
     std::vector<std::vector<uint32_t>> ca(PL), cb(PL);
     while (!rc) {
       std::vector<BatchReq> by_mode[3];
@@ -754,9 +771,12 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
         }
       }
       if (!any) break;
+      tr.mark("requests gathered");
       for (int md = 0; md < 3 && !rc; ++md) {
+        if (by_mode[md].empty()) continue;
         rc = eval_batch(ctx, x, y, rows, koff, eps, md, by_mode[md], ca, cb);
         if (rc) break;
+        tr.mark(md == 0 ? "  eval bound" : md == 1 ? "  eval final" : "  eval exact");
         const std::vector<BatchReq>& grp = by_mode[md];
         std::vector<int> bad(grp.size(), 0);
         parallel_for((int64_t)grp.size(), [&](int64_t q) {
@@ -765,6 +785,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
         });
         for (int b : bad)
           if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
+        tr.mark("  feed");
       }
     }
     std::vector<double> q0((size_t)PL * 4), qf((size_t)PL * 4);
@@ -786,10 +807,12 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
     }
     for (rv_plan* pl : plans) rv_plan_destroy(pl);
     if (rc) return rc;
+    tr.mark("results");
     // rows are absolute: refine over the local offsets table
     rc = run_refine(ctx, x, y, rows.data(), PL, ids.data(), eps, q0.data(), ctx->cfg.refine_rounds,
                     mw.data(), masks, qf.data(), fl.data(), ni.data());
     if (rc) return rc;
+    tr.mark("refine");
     for (int32_t p = 0; p < PL; ++p) {
       std::memcpy(local[p].q, &qf[4 * p], 32);
       local[p].flags |= fl[p];
