@@ -10,11 +10,12 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VARIANTS = {"pipe0": {"RV_PIPE": 0}, "pipe0_s3": {"RV_PIPE": 0, "RV_STAGES": 3},
-            "pipe0_asm": {"RV_PIPE": 0, "RV_COUNT_ASM": 1}, "pipe1": {"RV_PIPE": 1},
-            "pipe1_asm": {"RV_PIPE": 1, "RV_COUNT_ASM": 1},
-            "pipe0_cpt2_minb3": {"RV_PIPE": 0, "RV_CPT": 2, "RV_MINB": 3},
-            "pipe0_t512_s2": {"RV_PIPE": 0, "RV_TILE": 512, "RV_STAGES": 2}}
+VARIANTS = {"base": {},
+            "cpt8_v128_minb3": {"RV_CPT": 8, "RV_VOTERS": 128, "RV_MINB": 3},
+            "cpt6_v128_minb4": {"RV_CPT": 6, "RV_VOTERS": 128, "RV_MINB": 4},
+            "cpt4_v128_minb4": {"RV_CPT": 4, "RV_VOTERS": 128, "RV_MINB": 4},
+            "cpt8_v128_minb3_s3": {"RV_CPT": 8, "RV_VOTERS": 128, "RV_MINB": 3, "RV_STAGES": 3},
+            "cpt6_v192_minb2": {"RV_CPT": 6, "RV_VOTERS": 192, "RV_MINB": 2}}
 
 
 def build():
