@@ -82,6 +82,8 @@ typedef struct {
   void*   stream;        /* cudaStream_t to order all work on (NULL = legacy default) */
   int32_t emulate_world; /* test hook: > 1 evaluates the cell shards of that many ranks one after
                             another on this GPU (loopback); 0/1 = off.  Requires world == 1. */
+  int32_t tensor_vote;   /* 1: bound-level votes on the tensor cores (K3-TC, tcgen05, fp16-split
+                            operands, fp32 accumulation); 0: FP32-pipe FFMA2 vote everywhere */
 } rv_config;
 
 typedef struct {
@@ -174,6 +176,7 @@ int rot_vote_setup(rv_ctx* ctx, const float* x, const float* y, int64_t n, float
 #define RV_MODE_FINAL 1  /* cnt_a = #{s32 >= cos(eps) - guard}, cnt_b = #{s32 >= cos(eps) + guard} */
 #define RV_MODE_EXACT 2  /* cnt_a = #{i : s_i(q_c) >= cos(eps)} exactly: fp32 vote with an fp64
                             recheck of every pair within the guard band (K5) */
+#define RV_MODE_BOUND_TC 3 /* RV_MODE_BOUND evaluated by K3-TC (context with tensor_vote = 1) */
 
 /* a2-a5 (K3 rv_vote, K5 rv_recheck): vote m blocks of the B^3 grid.
  *   lins   DEVICE uint32[m], block (i,j,k) -> (i*B + j)*B + k.
@@ -182,6 +185,13 @@ int rot_vote_setup(rv_ctx* ctx, const float* x, const float* y, int64_t n, float
 int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t B,
                          const uint32_t* lins, int64_t m, double eps, int32_t mode,
                          uint32_t* cnt_a, uint32_t* cnt_b);
+
+/* Test hook for K3-TC's arithmetic: the raw tensor-core scores S' = s_tc - t of m blocks
+ * (bound threshold t as RV_MODE_BOUND) against every correspondence.  out: DEVICE float
+ * [m][ld] with ld = n rounded up to 256; columns >= n hold -1 (padding rows).  Needs a
+ * context created with tensor_vote = 1. */
+int rot_vote_debug_tc_scores(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t B,
+                             const uint32_t* lins, int64_t m, double eps, float* out);
 
 /* a6 (K6 rv_inliers + K7 rv_eig4): `rounds` rounds of linear refinement from q0 (HOST
  * double[4]); writes q_out (HOST double[4], canonical), flags (HOST, RV_REFINED /

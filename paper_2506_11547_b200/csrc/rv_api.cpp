@@ -161,6 +161,10 @@ struct rv_ctx {
 
   DevBuf<float> k9;              // [9][stride]
   int64_t stride = 0;
+  DevBuf<uint8_t> tctab;         // K3-TC table, 64 B per (padded) row
+  DevBuf<int64_t> toffs;         // per-problem row offsets in tctab
+  bool tc_on = false;            // cfg.tensor_vote: BOUND levels on tcgen05
+  std::vector<int64_t> tc_toff;  // host copy of toffs for the current setup
   DevBuf<uint32_t> lins, cnt;    // request blocks, counts (gathered layout)
   DevBuf<rv::VoteSeg> vsegs;
   DevBuf<rv::VoteItem> vitems;
@@ -276,6 +280,46 @@ int build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64_
   return groups;
 }
 
+// K3-TC items: CTAs of <= kTcM cells (one CTA per SM: 512 TMEM columns), correspondence
+// chunks of whole kTcN tiles; chunk count chosen, as for K3, to fill whole waves.
+void build_tc_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
+                    int slots, std::vector<rv::VoteItem>& items) {
+  items.clear();
+  int64_t cbs = 0, tmax = 0;
+  for (size_t s = 0; s < ncell.size(); ++s) {
+    if (ncell[s] == 0 || ncorr[s] == 0) continue;
+    cbs += (ncell[s] + rv::kTcM - 1) / rv::kTcM;
+    tmax = std::max<int64_t>(tmax, (ncorr[s] + rv::kTcN - 1) / rv::kTcN);
+  }
+  if (cbs == 0) return;
+  const int64_t min_tiles = std::min<int64_t>(tmax, 8);
+  const int64_t max_nch = std::max<int64_t>(1, tmax / std::max<int64_t>(1, min_tiles));
+  int64_t best_nch = 1;
+  double best = -1;
+  for (int64_t nch = 1; nch <= max_nch; ++nch) {
+    const double waves = (double)(cbs * nch) / slots;
+    if (waves > 64.0 && nch > 1) break;
+    const double eff = waves / std::ceil(waves);
+    const double score = eff - (waves < 4.0 ? 0.5 * (4.0 - waves) / 4.0 : 0.0);
+    if (score > best + 1e-9) { best = score; best_nch = nch; }
+  }
+  for (size_t s = 0; s < ncell.size(); ++s) {
+    if (ncell[s] == 0 || ncorr[s] == 0) continue;
+    const int64_t nt = (ncorr[s] + rv::kTcN - 1) / rv::kTcN;
+    const int64_t cb = (ncell[s] + rv::kTcM - 1) / rv::kTcM;
+    const int64_t per = (ncell[s] + cb - 1) / cb;
+    const int64_t nch = std::min<int64_t>(best_nch, nt);
+    const int64_t ct = (nt + nch - 1) / nch;  // tiles per chunk
+    for (int64_t b = 0; b < cb; ++b) {
+      const int64_t c0 = b * per, nc = std::min(per, ncell[s] - c0);
+      if (nc <= 0) continue;
+      for (int64_t t0 = 0; t0 < nt; t0 += ct)
+        items.push_back({(int32_t)s, (int32_t)c0, (int32_t)nc, (int32_t)(t0 * rv::kTcN),
+                         (int32_t)(std::min(ct, nt - t0) * rv::kTcN)});
+    }
+  }
+}
+
 void build_exact_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
                        std::vector<rv::VoteItem>& items) {
   items.clear();
@@ -300,7 +344,7 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
   RV_CUDA(ctx->rows.ensure(P + 1), "allocating offsets");
   RV_CUDA(ctx->koffs.ensure(P + 1), "allocating offsets");
   RV_CUDA(ctx->bad.ensure(1), "allocating flag");
-  RV_CUDA(ctx->up.ensure(2 * (P + 1) * sizeof(int64_t) + 1024), "allocating staging");
+  RV_CUDA(ctx->up.ensure(3 * (P + 1) * sizeof(int64_t) + 2048), "allocating staging");
   ctx->up.reset();
   int64_t* hrows = ctx->up.take<int64_t>(P + 1);
   int64_t* hk = ctx->up.take<int64_t>(P + 1);
@@ -314,6 +358,22 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
   rv::launch_setup(x, y, ctx->rows.p, ctx->koffs.p, P, total, ctx->k9.p, ctx->stride, ctx->bad.p,
                    ctx->stream);
   ctx->launches += 1;
+  if (ctx->tc_on) {
+    std::vector<int64_t> toff(P + 1, 0);
+    for (int32_t p = 0; p < P; ++p) {
+      const int64_t np = offsets[p + 1] - offsets[p];
+      toff[p + 1] = toff[p] + (np + rv::kTcN - 1) / rv::kTcN * rv::kTcN;
+    }
+    RV_CUDA(ctx->tctab.ensure((size_t)toff[P] * 64), "allocating K3-TC table");
+    RV_CUDA(ctx->toffs.ensure(P + 1), "allocating offsets");
+    int64_t* ht = ctx->up.take<int64_t>(P + 1);  // staging sized for it above
+    std::memcpy(ht, toff.data(), (P + 1) * sizeof(int64_t));
+    RV_CUDA(cudaMemcpyAsync(ctx->toffs.p, ht, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
+            "copying offsets");
+    rv::launch_setup_tc(x, y, ctx->rows.p, ctx->toffs.p, P, toff[P], ctx->tctab.p, ctx->stream);
+    ctx->launches += 1;
+    ctx->tc_toff = toff;
+  }
   RV_CUDA(cudaGetLastError(), "launching rv_setup");
   return RV_OK;
 }
@@ -369,9 +429,18 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
   }
   std::vector<rv::VoteItem> items;
   int groups = 1;
-  if (mode == RV_MODE_EXACT) build_exact_items(ncell, ncorr, items);
-  else groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items,
-                                 ctx->force_groups);
+  const bool use_tc = mode == RV_MODE_BOUND_TC || (mode == RV_MODE_BOUND && ctx->tc_on);
+  if (mode == RV_MODE_BOUND_TC && !ctx->tc_on)
+    return ctx->fail(RV_EINVAL, "RV_MODE_BOUND_TC needs a context created with tensor_vote = 1");
+  if (use_tc) {
+    for (rv::VoteSeg& sg : segs) sg.koff = ctx->tc_toff[0];
+    build_tc_items(ncell, ncorr, ctx->num_sms, items);
+  } else if (mode == RV_MODE_EXACT) {
+    build_exact_items(ncell, ncorr, items);
+  } else {
+    groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items,
+                              ctx->force_groups);
+  }
 
   RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
   RV_CUDA(ctx->vitems.ensure(std::max<size_t>(1, items.size())), "allocating items");
@@ -405,8 +474,12 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
                      (int32_t)items.size(), ctx->cfg.guard, s);
   } else {
     RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
-    rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
-                    (int32_t)items.size(), ctx->cfg.guard, s);
+    if (use_tc)
+      rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
+                         ctx->cfg.guard, nullptr, 0, s);
+    else
+      rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
+                      (int32_t)items.size(), ctx->cfg.guard, s);
     RV_CUDA(cudaEventRecord(ctx->evv1, s), "event");
     for (int64_t c : ncell) ctx->vote_pairs += (uint64_t)c * (uint64_t)n;
     ctx->vote_launches += 1;
@@ -663,9 +736,16 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   }
   std::vector<rv::VoteItem> items;
   int groups = 1;
-  if (mode == RV_MODE_EXACT) build_exact_items(ncell, ncorr, items);
-  else groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items,
-                                 ctx->force_groups);
+  const bool use_tc = mode == RV_MODE_BOUND && ctx->tc_on;
+  if (use_tc) {
+    for (size_t q = 0; q < reqs.size(); ++q) segs[q].koff = ctx->tc_toff[reqs[q].prob];
+    build_tc_items(ncell, ncorr, ctx->num_sms, items);
+  } else if (mode == RV_MODE_EXACT) {
+    build_exact_items(ncell, ncorr, items);
+  } else {
+    groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items,
+                              ctx->force_groups);
+  }
   RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
   RV_CUDA(ctx->vitems.ensure(std::max<size_t>(1, items.size())), "allocating items");
   RV_CUDA(ctx->up.ensure(upload * 4 + segs.size() * sizeof(rv::VoteSeg) +
@@ -698,8 +778,12 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                      (int32_t)items.size(), ctx->cfg.guard, s);
   } else {
     RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
-    rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
-                    (int32_t)items.size(), ctx->cfg.guard, s);
+    if (use_tc)
+      rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
+                         ctx->cfg.guard, nullptr, 0, s);
+    else
+      rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
+                      (int32_t)items.size(), ctx->cfg.guard, s);
     RV_CUDA(cudaEventRecord(ctx->evv1, s), "event");
     for (size_t q = 0; q < ncell.size(); ++q) ctx->vote_pairs += (uint64_t)ncell[q] * ncorr[q];
     ctx->vote_launches += 1;
@@ -879,6 +963,7 @@ void rot_vote_default_config(rv_config* cfg) {
   cfg->guard = 1e-5f;
   cfg->stream = nullptr;
   cfg->emulate_world = 0;
+  cfg->tensor_vote = 0;
 }
 
 int rot_vote_get_unique_id(void* id_out) {
@@ -913,6 +998,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
     }
   }
   ctx->stream = (cudaStream_t)cfg->stream;
+  ctx->tc_on = cfg->tensor_vote != 0;
   if (const char* fg = getenv("RV_VOTE_GROUPS")) ctx->force_groups = atoi(fg);
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -953,6 +1039,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
 void rot_vote_destroy(rv_ctx* ctx) {
   if (!ctx) return;
   if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
+  ctx->tctab.release(); ctx->toffs.release();
   ctx->k9.release(); ctx->lins.release(); ctx->cnt.release(); ctx->vsegs.release();
   ctx->vitems.release(); ctx->rsegs.release(); ctx->ritems.release(); ctx->partials.release();
   ctx->qs.release(); ctx->flags.release(); ctx->ninl.release(); ctx->rows.release();
@@ -1035,7 +1122,7 @@ int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n,
   if (int rc = validate_common(ctx, x, y, eps, 0)) return rc;
   if (!lins || !cnt_a || (mode == RV_MODE_FINAL && !cnt_b) || m < 0)
     return ctx->fail(RV_EINVAL, "null pointer");
-  if (mode < RV_MODE_BOUND || mode > RV_MODE_EXACT) return ctx->fail(RV_EINVAL, "bad mode");
+  if (mode < RV_MODE_BOUND || mode > RV_MODE_BOUND_TC) return ctx->fail(RV_EINVAL, "bad mode");
   if (B < 1 || B > 1625) return ctx->fail(RV_EINVAL, "bad B");
   if (n < 1 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
   if (m == 0) return RV_OK;
@@ -1052,6 +1139,43 @@ int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n,
   if (mode == RV_MODE_FINAL)
     RV_CUDA(cudaMemcpyAsync(cnt_b, hb.data(), m * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
   RV_CUDA(cudaStreamSynchronize(ctx->stream), "H2D");
+  return RV_OK;
+}
+
+int rot_vote_debug_tc_scores(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t B,
+                             const uint32_t* lins, int64_t m, double eps, float* out) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  if (int rc = validate_common(ctx, x, y, eps, 0)) return rc;
+  if (!ctx->tc_on) return ctx->fail(RV_EINVAL, "needs a context created with tensor_vote = 1");
+  if (!lins || !out || m < 1 || B < 1 || B > 1625) return ctx->fail(RV_EINVAL, "bad arguments");
+  if (n < 1 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
+  const int64_t offs[2] = {0, n};
+  std::vector<int64_t> koff;
+  if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
+  if (int rc = check_bad(ctx)) return rc;
+  const int64_t ld = (n + rv::kTcN - 1) / rv::kTcN * rv::kTcN;
+  rv::VoteSeg sg{};
+  sg.lins = lins;
+  sg.cnt_a = nullptr;
+  sg.cnt_b = nullptr;
+  sg.koff = 0;
+  sg.row = 0;
+  sg.n = (int32_t)n;
+  sg.B = B;
+  sg.eps = eps;
+  std::vector<rv::VoteItem> items;
+  build_tc_items({m}, {n}, ctx->num_sms, items);
+  RV_CUDA(ctx->vsegs.ensure(1), "allocating");
+  RV_CUDA(ctx->vitems.ensure(items.size()), "allocating");
+  RV_CUDA(cudaMemcpy(ctx->vsegs.p, &sg, sizeof(sg), cudaMemcpyHostToDevice), "H2D");
+  RV_CUDA(cudaMemcpy(ctx->vitems.p, items.data(), items.size() * sizeof(rv::VoteItem),
+                     cudaMemcpyHostToDevice), "H2D");
+  rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
+                     ctx->cfg.guard, out, ld, ctx->stream);
+  RV_CUDA(cudaGetLastError(), "launching K3-TC");
+  RV_CUDA(cudaStreamSynchronize(ctx->stream), "K3-TC");
   return RV_OK;
 }
 

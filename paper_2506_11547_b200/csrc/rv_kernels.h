@@ -34,6 +34,9 @@ constexpr int kCellsPerThread = RV_CPT;            // K3 register blocking (cell
 constexpr int kCellsPerBlock = kVoteThreads * kCellsPerThread;
 constexpr int kTile = RV_TILE;                     // correspondences per TMA stage
 constexpr int kStages = RV_STAGES;
+constexpr int kTcN = 256;                          // K3-TC: correspondences per tile (MMA N)
+constexpr int kTcM = 128;                          // K3-TC: cells per CTA (MMA M, TMEM lanes)
+constexpr int kTcStages = 7;                       // K3-TC: 16 KB tiles in flight (also pins 1 CTA/SM)
 constexpr int kRefThreads = 256;                   // K6/K7 block
 constexpr int kRefRowsPerItem = 2048;              // K6 rows per block (multiple of 32)
 
@@ -79,6 +82,17 @@ void launch_setup(const float* x, const float* y, const int64_t* rows, const int
 // groups in {1, 2, 4}: a CTA covers kCellsPerBlock / groups cells.
 void launch_vote(int mode, int groups, const float* k9, int64_t stride, const VoteSeg* segs,
                  const VoteItem* items, int32_t n_items, float guard, cudaStream_t s);
+
+// K1-TC: fp16-split correspondence table for the tensor-core vote (64 B per row,
+// interleaved K-major layout, each problem padded to a multiple of kTcN rows).
+void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const int64_t* toffs,
+                     int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s);
+
+// K3-TC: BOUND-mode vote on tcgen05 (items: ncell <= kTcM, i0/ni multiples of kTcN, koff
+// in table rows).  dump != nullptr writes the raw scores S' = s - t instead of counting
+// (test hook): dump[cell * dump_ld + correspondence].
+void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* items,
+                    int32_t n_items, float guard, float* dump, int64_t dump_ld, cudaStream_t s);
 
 // K5: exact counts (fp32 vote + fp64 recheck of |s32 - tau| < guard).  items: one block
 // per (block, correspondence chunk), ncell == 1.

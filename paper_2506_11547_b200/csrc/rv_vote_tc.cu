@@ -1,0 +1,384 @@
+// rv_vote_tc.cu -- K3-TC: the vote contraction on the 5th-generation tensor cores (tcgen05).
+//
+// SURVEY §8(f) NEXT-1.  For a CTA of 128 cells and a stream of 256-correspondence tiles the
+// scores S'[c][i] = phi(q_c) . k_i - t_c are one (128 x 32) . (32 x 256) fp16 MMA with fp32
+// accumulation, split so the products stay fp32-grade:
+//   k   = k_hi + k_lo,  phi = phi_hi + phi_lo  (fp16 each),
+//   S' ~= k_hi.phi_hi + k_hi.phi_lo + k_lo.phi_hi + 1.(-t_hi) + 1.(-t_lo)
+// laid out along K = 32:  A row (cell) = [phi_hi | phi_lo | phi_hi | -t_hi, -t_lo, -1, 0, 0]
+//                         B row (corr) = [k_hi   | k_hi   | k_lo   |  1,     1,    p, 0, 0]
+// with p = 0 for a correspondence and p = 1 for a padding row (S' = -1: never counted).
+// The count is then the sign bit of the accumulator, read from TMEM by 4 epilogue warps
+// (tcgen05.ld 32x32b: TMEM lane = cell, column = correspondence), so the FP32 pipe does one
+// LEA.HI per pair instead of the 9-FMA contraction.
+//
+// CTA roles: warp 0 lane 0 = TMA producer (one 16 KB cp.async.bulk per tile into a ring of
+// kTcStages), warp 1 = TMEM allocator + single-thread MMA issuer (2 x tcgen05.mma K=16 per
+// tile, accumulators double-buffered in 2 x 256 TMEM columns), warps 2..5 = epilogue.
+// Completion flows through mbarriers: full[s] (TMA tx), empty[s] (tcgen05.commit),
+// tfull[b] (tcgen05.commit), tempty[b] (4 epilogue warps).
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/rotvote.h"
+#include "rv_geom.h"
+#include "rv_kernels.h"
+
+namespace rv {
+
+namespace {
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(b))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, no swizzle ("interleaved" core matrices of
+// 8 rows x 16 bytes): start>>4 [0,14), LBO>>4 [16,30) = stride between the two 8-element K
+// chunks of one MMA, SBO>>4 [32,46) = stride between 8-row groups, version 1 at [46,48).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+// instruction descriptor kind::f16: D f32 [4,6)=1, A/B f16 (0), K-major both,
+// N>>3 at [17,23), M>>4 at [24,29)
+constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(b))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+#define RV_LD32(r, base)                                                                          \
+  asm volatile(                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"              \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),      \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),  \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),             \
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),             \
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])              \
+      : "r"(base))
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void add_sign_u(uint32_t& acc, uint32_t bits) {
+  asm("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(bits >> 31));
+}
+
+// byte offset of element (row, col) in the interleaved K-major layout of 32 fp16 columns:
+// 8-row groups of 512 B, each holding four 8x(8 fp16) core matrices of 128 B.
+__device__ __forceinline__ uint32_t il_off(int row, int col) {
+  return (uint32_t)((row >> 3) * 512 + (col >> 3) * 128 + (row & 7) * 16 + (col & 7) * 2);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// K1-TC: the fp16-split correspondence table, 64 B per correspondence, interleaved layout,
+// each problem padded to a multiple of kTcN rows (padding rows score -1).
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restrict__ x,
+                                                          const float* __restrict__ y,
+                                                          const int64_t* __restrict__ rows,
+                                                          const int64_t* __restrict__ toffs,
+                                                          int32_t P, int64_t total_pad,
+                                                          uint8_t* __restrict__ tab) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total_pad;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int32_t lo = 0, hi = P;
+    while (hi - lo > 1) {
+      int32_t mid = (lo + hi) >> 1;
+      if (toffs[mid] <= g) lo = mid; else hi = mid;
+    }
+    const int64_t i = g - toffs[lo];
+    const int64_t n = rows[lo + 1] - rows[lo];
+    __half v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = __float2half_rn(0.0f);
+    if (i < n) {
+      const int64_t r = rows[lo] + i;
+      double a[3] = {x[3 * r], x[3 * r + 1], x[3 * r + 2]};
+      double b[3] = {y[3 * r], y[3 * r + 1], y[3 * r + 2]};
+      const double ia = 1.0 / sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+      const double ib = 1.0 / sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { a[c] *= ia; b[c] *= ib; }
+      double k[9];
+      k9_of(a, b, k);
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        const __half h = __double2half(k[j]);
+        const __half l = __double2half(k[j] - (double)__half2float(h));
+        v[j] = h;
+        v[9 + j] = h;
+        v[18 + j] = l;
+      }
+      v[27] = __float2half_rn(1.0f);
+      v[28] = __float2half_rn(1.0f);
+    } else {
+      v[29] = __float2half_rn(1.0f);  // padding row: S' = -1
+    }
+    // row g of the whole table: group g>>3, 4 chunks of 16 B
+    uint8_t* rowp = tab + (g >> 3) * 512 + (g & 7) * 16;
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      uint4 w;
+      __half* hw = reinterpret_cast<__half*>(&w);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) hw[e] = v[ch * 8 + e];
+      *reinterpret_cast<uint4*>(rowp + ch * 128) = w;
+    }
+  }
+}
+
+void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const int64_t* toffs,
+                     int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s) {
+  int64_t blocks = (total_pad + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  rv_setup_tc_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, y, rows, toffs, P, total_pad, tab);
+}
+
+// ------------------------------------------------------------------------------------------
+// K3-TC
+// ------------------------------------------------------------------------------------------
+constexpr int kTcThreads = 192;  // 6 warps
+constexpr int kTcAccCols = 2 * kTcN;
+constexpr uint32_t kTileBytes = kTcN * 64;  // 16 KB
+
+struct __align__(1024) TcSmem {
+  uint8_t b[kTcStages][kTileBytes];  // correspondence tiles
+  uint8_t a[128 * 64];               // 128 cells x 32 fp16
+  uint64_t full[kTcStages], empty[kTcStages], tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+template <bool DUMP>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    rv_vote_tc_kernel(const uint8_t* __restrict__ tab, const VoteSeg* __restrict__ segs,
+                      const VoteItem* __restrict__ items, float guard, float* dump,
+                      int64_t dump_ld) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  TcSmem& sm = *reinterpret_cast<TcSmem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const VoteItem it = items[blockIdx.x];
+  const VoteSeg& sg = segs[it.seg];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = it.ni / kTcN;  // it.i0, it.ni are multiples of kTcN
+
+  // ---- prologue: TMEM, barriers, the A operand ----
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(&sm.tmem_base)),
+                 "r"(kTcAccCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      bar_init(&sm.full[s], 1);
+      bar_init(&sm.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      bar_init(&sm.tfull[b], 1);
+      bar_init(&sm.tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // epilogue thread <-> TMEM lane <-> cell of the CTA
+  const int m = 32 * (warp & 3) + lane;
+  float init_f = 0.0f;
+  if (warp >= 2) {
+    __half v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = __float2half_rn(0.0f);
+    if (m < it.ncell) {
+      const uint32_t lin = sg.lins[it.cell0 + m];
+      int32_t i, j, k;
+      lin_to_ijk(lin, sg.B, i, j, k);
+      double q[4], f[9];
+      cell_quat(sg.B, i, j, k, q);
+      phi9(q, f);
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const __half h = __double2half(f[t]);
+        const __half l = __double2half(f[t] - (double)__half2float(h));
+        v[t] = h;
+        v[9 + t] = l;
+        v[18 + t] = h;
+      }
+      const double thr = bound_threshold(sg.B, i, j, k, sg.eps) - guard;
+      const __half th = __double2half(-thr);
+      const __half tl = __double2half(-thr - (double)__half2float(th));
+      v[27] = th;
+      v[28] = tl;
+      v[29] = __float2half_rn(-1.0f);
+      init_f = (float)(-thr);
+    }
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      uint4 w;
+      __half* hw = reinterpret_cast<__half*>(&w);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) hw[e] = v[ch * 8 + e];
+      *reinterpret_cast<uint4*>(&sm.a[il_off(m, ch * 8)]) = w;
+    }
+    // generic-proxy smem writes -> visible to the tensor core (async proxy)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint8_t* src = tab + (sg.koff + it.i0) * 64;
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t % kTcStages;
+        if (t >= kTcStages) bar_wait(&sm.empty[s], (uint32_t)(((t / kTcStages) - 1) & 1));
+        bar_expect_tx(&sm.full[s], kTileBytes);
+        bulk_g2s(sm.b[s], src + (int64_t)t * kTileBytes, kTileBytes, &sm.full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t a0 = su32(sm.a);
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t % kTcStages, b = t & 1;
+        bar_wait(&sm.full[s], (uint32_t)((t / kTcStages) & 1));
+        if (t >= 2) bar_wait(&sm.tempty[b], (uint32_t)(((t >> 1) - 1) & 1));
+        tc_fence_after();
+        const uint32_t b0 = su32(sm.b[s]);
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          mma_f16(tmem + (uint32_t)(b * kTcN), smem_desc(a0 + 256 * k, 128, 512),
+                  smem_desc(b0 + 256 * k, 128, 512), (uint32_t)k);
+        mma_commit(&sm.empty[s]);  // smem slot free once these MMAs completed
+        mma_commit(&sm.tfull[b]);  // accumulator b ready
+      }
+    }
+  } else {
+    // ---------------- epilogue: count sign bits (warps 2..5) ----------------
+    const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    uint32_t neg = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int b = t & 1;
+      bar_wait(&sm.tfull[b], (uint32_t)((t >> 1) & 1));
+      tc_fence_after();
+#pragma unroll
+      for (int q = 0; q < kTcN / 64; ++q) {
+        uint32_t r0[32], r1[32];
+        RV_LD32(r0, lane_addr + (uint32_t)(b * kTcN + q * 64));
+        RV_LD32(r1, lane_addr + (uint32_t)(b * kTcN + q * 64 + 32));
+        tmem_wait_ld();
+        if (DUMP) {
+          if (m < it.ncell)
+            for (int e = 0; e < 64; ++e) {
+              const int col = q * 64 + e;
+              const uint32_t bits = e < 32 ? r0[e] : r1[e - 32];
+              dump[(int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col] =
+                  __uint_as_float(bits);
+            }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            add_sign_u(neg, r0[e]);
+            add_sign_u(neg, r1[e]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(&sm.tempty[b]);
+    }
+    if (!DUMP && m < it.ncell) {
+      // rows of the chunk: real correspondences score phi.k - t; padding rows score -1
+      const uint32_t cnt = (uint32_t)it.ni - neg;
+      atomicAdd(&sg.cnt_a[it.cell0 + m], cnt);
+    }
+  }
+  (void)init_f;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTcAccCols));
+  }
+}
+
+size_t tc_smem_bytes() { return sizeof(TcSmem) + 1024; }
+
+void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* items,
+                    int32_t n_items, float guard, float* dump, int64_t dump_ld, cudaStream_t s) {
+  if (n_items <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rv_vote_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tc_smem_bytes());
+    cudaFuncSetAttribute(rv_vote_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tc_smem_bytes());
+    attr = true;
+  }
+  if (dump)
+    rv_vote_tc_kernel<true><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(tab, segs, items, guard,
+                                                                         dump, dump_ld);
+  else
+    rv_vote_tc_kernel<false><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(tab, segs, items,
+                                                                          guard, nullptr, 0);
+}
+
+}  // namespace rv

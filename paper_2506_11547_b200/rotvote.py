@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("RV_LIB") or os.path.join(_HERE, "librotvote.so")  # R
 
 RV_OK, RV_EINVAL, RV_EDATA, RV_ECUDA, RV_ENCCL, RV_ENOMEM = 0, -1, -2, -3, -4, -5
 RV_REFINED, RV_DEGENERATE, RV_RECHECKED = 1, 2, 4
-RV_MODE_BOUND, RV_MODE_FINAL, RV_MODE_EXACT = 0, 1, 2
+RV_MODE_BOUND, RV_MODE_FINAL, RV_MODE_EXACT, RV_MODE_BOUND_TC = 0, 1, 2, 3
 RV_MAX_CHAIN, RV_MAX_PHASES = 8, 16
 DEFAULT_CHAIN = (5, 15, 45, 90, 180, 360)
 
@@ -40,7 +40,7 @@ class rv_config(C.Structure):
                 ("nccl_id", C.c_void_p), ("max_n", C.c_int64), ("max_problems", C.c_int32),
                 ("chain_len", C.c_int32), ("chain", C.c_int32 * RV_MAX_CHAIN),
                 ("refine_rounds", C.c_int32), ("guard", C.c_float), ("stream", C.c_void_p),
-                ("emulate_world", C.c_int32)]
+                ("emulate_world", C.c_int32), ("tensor_vote", C.c_int32)]
 
 
 class rv_result(C.Structure):
@@ -87,6 +87,8 @@ def lib() -> C.CDLL:
     L.rot_vote_setup.argtypes = [vp, vp, vp, i64, vp]
     L.rot_vote_count_cells.argtypes = [vp, vp, vp, i64, i32, vp, i64, dbl, i32, vp, vp]
     L.rot_vote_refine.argtypes = [vp, vp, vp, i64, dbl, vp, i32, vp, vp, vp, vp]
+    L.rot_vote_debug_tc_scores.argtypes = [vp, vp, vp, i64, i32, vp, i64, dbl, vp]
+    L.rv_plan_request_is_full_grid.argtypes = [vp]
     L.rv_plan_create.argtypes = [vp, i32, i32, i64, dbl, dbl, C.POINTER(vp)]
     L.rv_plan_destroy.argtypes = [vp]
     L.rv_plan_destroy.restype = None
@@ -188,7 +190,7 @@ class RotVote:
     def __init__(self, device: int = 0, max_n: int = 1 << 20, max_problems: int = 1,
                  chain=None, refine_rounds: int = 2, guard: float = 1e-5, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 emulate_world: int = 0):
+                 emulate_world: int = 0, tensor_vote: bool = False):
         import torch
         cfg = rot_vote_default_config()
         cfg.device = device
@@ -210,6 +212,7 @@ class RotVote:
         self.stream = stream
         cfg.stream = C.c_void_p(stream.cuda_stream)
         cfg.emulate_world = int(emulate_world)
+        cfg.tensor_vote = int(bool(tensor_vote))
         self.cfg = cfg
         self.device = device
         self.chain = tuple(chain) if chain is not None else DEFAULT_CHAIN
@@ -286,6 +289,18 @@ class RotVote:
         ca = a.cpu().numpy().view(np.uint32)
         cb = b.cpu().numpy().view(np.uint32)
         return (ca, cb) if mode == RV_MODE_FINAL else ca
+
+    def debug_tc_scores(self, x, y, B: int, lins, eps: float):
+        """Raw K3-TC scores S' = s_tc - t (bound threshold), float32 [m, ceil(n/256)*256]."""
+        import torch
+        lins = torch.as_tensor(np.asarray(lins, np.uint32).view(np.int32), device=x.device)
+        m, n = lins.numel(), x.shape[0]
+        ld = (n + 255) // 256 * 256
+        out = torch.empty((m, ld), dtype=torch.float32, device=x.device)
+        _check(self.ctx, lib().rot_vote_debug_tc_scores(
+            self.ctx, _dptr(x, torch.float32, "x"), _dptr(y, torch.float32, "y"), n, int(B),
+            lins.data_ptr(), m, float(eps), out.data_ptr()))
+        return out.cpu().numpy()
 
     def refine(self, x, y, eps: float, q0, rounds: int = 2, mask=None):
         import torch
