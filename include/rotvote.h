@@ -176,7 +176,9 @@ int rot_vote_setup(rv_ctx* ctx, const float* x, const float* y, int64_t n, float
 #define RV_MODE_FINAL 1  /* cnt_a = #{s32 >= cos(eps) - guard}, cnt_b = #{s32 >= cos(eps) + guard} */
 #define RV_MODE_EXACT 2  /* cnt_a = #{i : s_i(q_c) >= cos(eps)} exactly: fp32 vote with an fp64
                             recheck of every pair within the guard band (K5) */
-#define RV_MODE_BOUND_TC 3 /* RV_MODE_BOUND evaluated by K3-TC (context with tensor_vote = 1) */
+#define RV_MODE_BOUND_TC 3 /* RV_MODE_BOUND evaluated by K3-TC (context with tensor_vote = 1):
+                              cnt_a = #{s_tc >= cos(min(pi, eps + r(c))) - guard - 1.5e-5}, the extra
+                              1.5e-5 covering the worst-case error of the fp16-split MMA */
 
 /* a2-a5 (K3 rv_vote, K5 rv_recheck): vote m blocks of the B^3 grid.
  *   lins   DEVICE uint32[m], block (i,j,k) -> (i*B + j)*B + k.
@@ -187,7 +189,7 @@ int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n,
                          uint32_t* cnt_a, uint32_t* cnt_b);
 
 /* Test hook for K3-TC's arithmetic: the raw tensor-core scores S' = s_tc - t of m blocks
- * (bound threshold t as RV_MODE_BOUND) against every correspondence.  out: DEVICE float
+ * (t = the RV_MODE_BOUND_TC threshold, guard included) against every correspondence.  out: DEVICE float
  * [m][ld] with ld = n rounded up to 256; columns >= n hold -1 (padding rows).  Needs a
  * context created with tensor_vote = 1. */
 int rot_vote_debug_tc_scores(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t B,
