@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--vote", default="tc", choices=["tc", "ffma2"],
+                    help="bound levels on the tensor cores (K3-TC) or the FP32 pipe (K3)")
     ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg5"],
                     help="cfg5 (4096 x 1000 batched problems) is an extra measurement, "
                          "not the metric's bench line")
@@ -205,7 +207,7 @@ def run_ours(args):
     pr = datagen.cfg4()
     stream = torch.cuda.current_stream()
     rv = RotVote(device=local, max_n=pr.n, rank=rank, world=world, nccl_id=nccl_id,
-                 stream=stream)
+                 stream=stream, tensor_vote=(args.vote == "tc"))
     x = torch.from_numpy(pr.x).cuda()
     y = torch.from_numpy(pr.y).cuda()
     mask = torch.zeros((pr.n + 31) // 32, dtype=torch.int32, device="cuda")
@@ -309,7 +311,7 @@ def run_batched(args):
     import datagen
     from paper_2506_11547_b200 import RotVote
     bt = datagen.cfg5()
-    rv = RotVote(max_n=bt.x.shape[0], max_problems=4096)
+    rv = RotVote(max_n=bt.x.shape[0], max_problems=4096, tensor_vote=(args.vote == "tc"))
     x = torch.from_numpy(bt.x).cuda()
     y = torch.from_numpy(bt.y).cuda()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
