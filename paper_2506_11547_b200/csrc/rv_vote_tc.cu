@@ -8,15 +8,17 @@
 // laid out along K = 32:  A row (cell) = [phi_hi | phi_lo | phi_hi | -t_hi, -t_lo, -1, 0, 0]
 //                         B row (corr) = [k_hi   | k_hi   | k_lo   |  1,     1,    p, 0, 0]
 // with p = 0 for a correspondence and p = 1 for a padding row (S' = -1: never counted).
-// The count is then the sign bit of the accumulator, read from TMEM by 4 epilogue warps
-// (tcgen05.ld 32x32b: TMEM lane = cell, column = correspondence), so the FP32 pipe does one
-// LEA.HI per pair instead of the 9-FMA contraction.
+// The count is then the sign bit of the accumulator, read from TMEM by the epilogue warps
+// (tcgen05.ld 32x32b: TMEM lane = cell, column = correspondence), so the SM's integer pipes do
+// one instruction per pair instead of the FP32 pipe's 9-FMA contraction.
 //
 // CTA roles: warp 0 lane 0 = TMA producer (one 16 KB cp.async.bulk per tile into a ring of
 // kTcStages), warp 1 = TMEM allocator + single-thread MMA issuer (2 x tcgen05.mma K=16 per
-// tile, accumulators double-buffered in 2 x 256 TMEM columns), warps 2..5 = epilogue.
+// tile, accumulators double-buffered in 2 x 256 TMEM columns), warps 2..9 = epilogue: warp w
+// reads TMEM lanes 32*(w%4).. (its cells) and half of the tile's columns; the sign count runs
+// as independent chains split between the ALU pipe (LEA.HI) and the FMA pipe (IMAD.HI).
 // Completion flows through mbarriers: full[s] (TMA tx), empty[s] (tcgen05.commit),
-// tfull[b] (tcgen05.commit), tempty[b] (4 epilogue warps).
+// tfull[b] (tcgen05.commit), tempty[b] (the 8 epilogue warps).
 #include <cstdint>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -112,8 +114,13 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void add_sign_u(uint32_t& acc, uint32_t bits) {
+// Sign-bit counting on two pipes: acc += bits >> 31 fuses to LEA.HI (ALU pipe);
+// acc += hi32(bits * 2) is IMAD.HI (FMA pipe) when the 2 is a runtime register.
+__device__ __forceinline__ void add_sign_alu(uint32_t& acc, uint32_t bits) {
   asm("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(bits >> 31));
+}
+__device__ __forceinline__ void add_sign_fma(uint32_t& acc, uint32_t bits, uint32_t two) {
+  asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(bits), "r"(two));
 }
 
 // byte offset of element (row, col) in the interleaved K-major layout of 32 fp16 columns:
@@ -193,7 +200,8 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 // ------------------------------------------------------------------------------------------
 // K3-TC
 // ------------------------------------------------------------------------------------------
-constexpr int kTcThreads = 192;  // 6 warps
+constexpr int kTcEpiWarps = 8;
+constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, 8 epilogue warps
 constexpr int kTcAccCols = 2 * kTcN;
 constexpr uint32_t kTileBytes = kTcN * 64;  // 16 KB
 
@@ -231,14 +239,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       bar_init(&sm.tfull[b], 1);
-      bar_init(&sm.tempty[b], 4);
+      bar_init(&sm.tempty[b], kTcEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // epilogue thread <-> TMEM lane <-> cell of the CTA
   const int m = 32 * (warp & 3) + lane;
   float init_f = 0.0f;
-  if (warp >= 2) {
+  if (warp >= 2 && warp < 6) {  // one writer per A row
     __half v[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) v[c] = __float2half_rn(0.0f);
@@ -311,32 +319,40 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue: count sign bits (warps 2..5) ----------------
+    // ---------------- epilogue: count sign bits (warps 2..9) ----------------
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-    uint32_t neg = 0;
+    const int half = (warp - 2) >> 2;          // which 128 columns of the tile
+    const uint32_t two = guard > -1.0f ? 2u : 3u;  // a runtime 2 (keeps IMAD.HI)
+    uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, n4 = 0, n5 = 0, n6 = 0, n7 = 0;
     for (int t = 0; t < ntiles; ++t) {
       const int b = t & 1;
       bar_wait(&sm.tfull[b], (uint32_t)((t >> 1) & 1));
       tc_fence_after();
 #pragma unroll
-      for (int q = 0; q < kTcN / 64; ++q) {
+      for (int q = 0; q < kTcN / 128; ++q) {
+        const int col0 = half * (kTcN / 2) + q * 64;
         uint32_t r0[32], r1[32];
-        RV_LD32(r0, lane_addr + (uint32_t)(b * kTcN + q * 64));
-        RV_LD32(r1, lane_addr + (uint32_t)(b * kTcN + q * 64 + 32));
+        RV_LD32(r0, lane_addr + (uint32_t)(b * kTcN + col0));
+        RV_LD32(r1, lane_addr + (uint32_t)(b * kTcN + col0 + 32));
         tmem_wait_ld();
         if (DUMP) {
           if (m < it.ncell)
             for (int e = 0; e < 64; ++e) {
-              const int col = q * 64 + e;
               const uint32_t bits = e < 32 ? r0[e] : r1[e - 32];
-              dump[(int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col] =
+              dump[(int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col0 + e] =
                   __uint_as_float(bits);
             }
         } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            add_sign_u(neg, r0[e]);
-            add_sign_u(neg, r1[e]);
+          for (int e = 0; e < 32; e += 4) {
+            add_sign_alu(n0, r0[e]);
+            add_sign_fma(n1, r0[e + 1], two);
+            add_sign_alu(n2, r0[e + 2]);
+            add_sign_fma(n3, r0[e + 3], two);
+            add_sign_alu(n4, r1[e]);
+            add_sign_fma(n5, r1[e + 1], two);
+            add_sign_alu(n6, r1[e + 2]);
+            add_sign_fma(n7, r1[e + 3], two);
           }
         }
       }
@@ -346,7 +362,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     if (!DUMP && m < it.ncell) {
       // rows of the chunk: real correspondences score phi.k - t; padding rows score -1
-      const uint32_t cnt = (uint32_t)it.ni - neg;
+      const uint32_t neg = (n0 + n1) + (n2 + n3) + (n4 + n5) + (n6 + n7);
+      const uint32_t cnt = (uint32_t)(it.ni / 2) - neg;  // this warp saw half the columns
       atomicAdd(&sg.cnt_a[it.cell0 + m], cnt);
     }
   }
