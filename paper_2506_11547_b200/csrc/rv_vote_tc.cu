@@ -328,37 +328,39 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int b = t & 1;
       bar_wait(&sm.tfull[b], (uint32_t)((t >> 1) & 1));
       tc_fence_after();
-#pragma unroll
-      for (int q = 0; q < kTcN / 128; ++q) {
-        const int col0 = half * (kTcN / 2) + q * 64;
-        uint32_t r0[32], r1[32];
-        RV_LD32(r0, lane_addr + (uint32_t)(b * kTcN + col0));
-        RV_LD32(r1, lane_addr + (uint32_t)(b * kTcN + col0 + 32));
-        tmem_wait_ld();
-        if (DUMP) {
-          if (m < it.ncell)
-            for (int e = 0; e < 64; ++e) {
-              const uint32_t bits = e < 32 ? r0[e] : r1[e - 32];
-              dump[(int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col0 + e] =
-                  __uint_as_float(bits);
-            }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            add_sign_alu(n0, r0[e]);
-            add_sign_fma(n1, r0[e + 1], two);
-            add_sign_alu(n2, r0[e + 2]);
-            add_sign_fma(n3, r0[e + 3], two);
-            add_sign_alu(n4, r1[e]);
-            add_sign_fma(n5, r1[e + 1], two);
-            add_sign_alu(n6, r1[e + 2]);
-            add_sign_fma(n7, r1[e + 3], two);
-          }
-        }
-      }
+      // this warp's 128 columns of accumulator b -> registers, then hand the buffer back to
+      // the MMA issuer before counting (the count overlaps the next MMA)
+      const int col0 = half * (kTcN / 2);
+      uint32_t r0[32], r1[32], r2[32], r3[32];
+      RV_LD32(r0, lane_addr + (uint32_t)(b * kTcN + col0));
+      RV_LD32(r1, lane_addr + (uint32_t)(b * kTcN + col0 + 32));
+      RV_LD32(r2, lane_addr + (uint32_t)(b * kTcN + col0 + 64));
+      RV_LD32(r3, lane_addr + (uint32_t)(b * kTcN + col0 + 96));
+      tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(&sm.tempty[b]);
+      if (DUMP) {
+        if (m < it.ncell)
+          for (int e = 0; e < 128; ++e) {
+            const uint32_t bits = e < 32 ? r0[e] : e < 64 ? r1[e - 32] : e < 96 ? r2[e - 64]
+                                                                          : r3[e - 96];
+            dump[(int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col0 + e] =
+                __uint_as_float(bits);
+          }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          add_sign_alu(n0, r0[e]);
+          add_sign_fma(n1, r0[e + 1], two);
+          add_sign_alu(n2, r1[e]);
+          add_sign_fma(n3, r1[e + 1], two);
+          add_sign_alu(n4, r2[e]);
+          add_sign_fma(n5, r2[e + 1], two);
+          add_sign_alu(n6, r3[e]);
+          add_sign_fma(n7, r3[e + 1], two);
+        }
+      }
     }
     if (!DUMP && m < it.ncell) {
       // rows of the chunk: real correspondences score phi.k - t; padding rows score -1
