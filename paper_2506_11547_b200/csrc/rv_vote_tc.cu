@@ -14,11 +14,11 @@
 //
 // CTA roles: warp 0 lane 0 = TMA producer (one 16 KB cp.async.bulk per tile into a ring of
 // kTcStages), warp 1 = TMEM allocator + single-thread MMA issuer (2 x tcgen05.mma K=16 per
-// tile, accumulators double-buffered in 2 x 256 TMEM columns), warps 2..9 = epilogue: warp w
-// reads TMEM lanes 32*(w%4).. (its cells) and half of the tile's columns; the sign count runs
+// tile, accumulators double-buffered in 2 x 256 TMEM columns), warps 2..17 = epilogue: warp w
+// reads TMEM lanes 32*(w%4).. (its cells) and a quarter of the tile's columns; the count runs
 // as independent chains split between the ALU pipe (LEA.HI) and the FMA pipe (IMAD.HI).
 // Completion flows through mbarriers: full[s] (TMA tx), empty[s] (tcgen05.commit),
-// tfull[b] (tcgen05.commit), tempty[b] (the 8 epilogue warps).
+// tfull[b] (tcgen05.commit), tempty[b] (the 16 epilogue warps).
 #include <cstdint>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -200,8 +200,9 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 // ------------------------------------------------------------------------------------------
 // K3-TC
 // ------------------------------------------------------------------------------------------
-constexpr int kTcEpiWarps = 8;
-constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, 8 epilogue warps
+constexpr int kTcEpiWarps = 16;
+constexpr int kTcColsPerWarp = kTcN * 4 / kTcEpiWarps;  // each lane quarter has kTcEpiWarps/4 warps
+constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, epilogue warps
 constexpr int kTcAccCols = 2 * kTcN;
 constexpr uint32_t kTileBytes = kTcN * 64;  // 16 KB
 
@@ -321,51 +322,48 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else {
     // ---------------- epilogue: count sign bits (warps 2..9) ----------------
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-    const int half = (warp - 2) >> 2;          // which 128 columns of the tile
+    const int part = (warp - 2) >> 2;          // which kTcColsPerWarp columns of the tile
     const uint32_t two = guard > -1.0f ? 2u : 3u;  // a runtime 2 (keeps IMAD.HI)
     uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, n4 = 0, n5 = 0, n6 = 0, n7 = 0;
     for (int t = 0; t < ntiles; ++t) {
       const int b = t & 1;
       bar_wait(&sm.tfull[b], (uint32_t)((t >> 1) & 1));
       tc_fence_after();
-      // this warp's 128 columns of accumulator b -> registers, then hand the buffer back to
-      // the MMA issuer before counting (the count overlaps the next MMA)
-      const int col0 = half * (kTcN / 2);
-      uint32_t r0[32], r1[32], r2[32], r3[32];
+      // this warp's columns of accumulator b -> registers, then hand the buffer back to the
+      // MMA issuer before counting (the count overlaps the next MMA)
+      const int col0 = part * kTcColsPerWarp;
+      uint32_t r0[32], r1[32];
       RV_LD32(r0, lane_addr + (uint32_t)(b * kTcN + col0));
       RV_LD32(r1, lane_addr + (uint32_t)(b * kTcN + col0 + 32));
-      RV_LD32(r2, lane_addr + (uint32_t)(b * kTcN + col0 + 64));
-      RV_LD32(r3, lane_addr + (uint32_t)(b * kTcN + col0 + 96));
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(&sm.tempty[b]);
       if (DUMP) {
         if (m < it.ncell)
-          for (int e = 0; e < 128; ++e) {
-            const uint32_t bits = e < 32 ? r0[e] : e < 64 ? r1[e - 32] : e < 96 ? r2[e - 64]
-                                                                          : r3[e - 96];
+          for (int e = 0; e < 64; ++e) {
+            const uint32_t bits = e < 32 ? r0[e] : r1[e - 32];
             dump[(int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col0 + e] =
                 __uint_as_float(bits);
           }
       } else {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
+        for (int e = 0; e < 32; e += 4) {
           add_sign_alu(n0, r0[e]);
           add_sign_fma(n1, r0[e + 1], two);
-          add_sign_alu(n2, r1[e]);
-          add_sign_fma(n3, r1[e + 1], two);
-          add_sign_alu(n4, r2[e]);
-          add_sign_fma(n5, r2[e + 1], two);
-          add_sign_alu(n6, r3[e]);
-          add_sign_fma(n7, r3[e + 1], two);
+          add_sign_alu(n2, r0[e + 2]);
+          add_sign_fma(n3, r0[e + 3], two);
+          add_sign_alu(n4, r1[e]);
+          add_sign_fma(n5, r1[e + 1], two);
+          add_sign_alu(n6, r1[e + 2]);
+          add_sign_fma(n7, r1[e + 3], two);
         }
       }
     }
     if (!DUMP && m < it.ncell) {
       // rows of the chunk: real correspondences score phi.k - t; padding rows score -1
       const uint32_t neg = (n0 + n1) + (n2 + n3) + (n4 + n5) + (n6 + n7);
-      const uint32_t cnt = (uint32_t)(it.ni / 2) - neg;  // this warp saw half the columns
+      const uint32_t cnt = (uint32_t)(it.ni / (kTcEpiWarps / 4)) - neg;  // its share of columns
       atomicAdd(&sg.cnt_a[it.cell0 + m], cnt);
     }
   }
