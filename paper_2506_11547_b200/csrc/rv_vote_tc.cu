@@ -20,6 +20,7 @@
 // Completion flows through mbarriers: full[s] (TMA tx), empty[s] (tcgen05.commit),
 // tfull[b] (tcgen05.commit), tempty[b] (the 16 epilogue warps).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -213,7 +214,8 @@ struct __align__(1024) TcSmem {
   uint32_t tmem_base;
 };
 
-template <bool DUMP>
+// ABL (ablation, tuning only): bit0 skip the count, bit1 skip the MMAs, bit2 skip the TMA
+template <bool DUMP, int ABL = 0>
 __global__ void __launch_bounds__(kTcThreads, 1)
     rv_vote_tc_kernel(const uint8_t* __restrict__ tab, const VoteSeg* __restrict__ segs,
                       const VoteItem* __restrict__ items, float guard, float* dump,
@@ -297,8 +299,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int t = 0; t < ntiles; ++t) {
         const int s = t % kTcStages;
         if (t >= kTcStages) bar_wait(&sm.empty[s], (uint32_t)(((t / kTcStages) - 1) & 1));
-        bar_expect_tx(&sm.full[s], kTileBytes);
-        bulk_g2s(sm.b[s], src + (int64_t)t * kTileBytes, kTileBytes, &sm.full[s]);
+        if (ABL & 4) {
+          bar_arrive(&sm.full[s]);
+        } else {
+          bar_expect_tx(&sm.full[s], kTileBytes);
+          bulk_g2s(sm.b[s], src + (int64_t)t * kTileBytes, kTileBytes, &sm.full[s]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -311,10 +317,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (t >= 2) bar_wait(&sm.tempty[b], (uint32_t)(((t >> 1) - 1) & 1));
         tc_fence_after();
         const uint32_t b0 = su32(sm.b[s]);
+        if (!(ABL & 2)) {
 #pragma unroll
-        for (int k = 0; k < 2; ++k)
-          mma_f16(tmem + (uint32_t)(b * kTcN), smem_desc(a0 + 256 * k, 128, 512),
-                  smem_desc(b0 + 256 * k, 128, 512), (uint32_t)k);
+          for (int k = 0; k < 2; ++k)
+            mma_f16(tmem + (uint32_t)(b * kTcN), smem_desc(a0 + 256 * k, 128, 512),
+                    smem_desc(b0 + 256 * k, 128, 512), (uint32_t)k);
+        }
         mma_commit(&sm.empty[s]);  // smem slot free once these MMAs completed
         mma_commit(&sm.tfull[b]);  // accumulator b ready
       }
@@ -339,7 +347,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(&sm.tempty[b]);
-      if (DUMP) {
+      if (ABL & 1) {
+        n0 += r0[0] ^ r1[31];
+      } else if (DUMP) {
         if (m < it.ncell)
           for (int e = 0; e < 64; ++e) {
             const uint32_t bits = e < 32 ? r0[e] : r1[e - 32];
@@ -390,10 +400,25 @@ void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* ite
                          (int)tc_smem_bytes());
     attr = true;
   }
+  static const int abl = [] {
+    const char* e = getenv("RV_TC_ABLATE");  // tuning only: skip pipeline stages (wrong counts)
+    return e ? atoi(e) : 0;
+  }();
   if (dump)
     rv_vote_tc_kernel<true><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(tab, segs, items, guard,
                                                                          dump, dump_ld);
-  else
+  else if (abl != 0) {
+#define RV_ABL_CASE(A)                                                                           \
+  case A:                                                                                        \
+    cudaFuncSetAttribute(rv_vote_tc_kernel<false, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)tc_smem_bytes());                                                  \
+    rv_vote_tc_kernel<false, A><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(tab, segs, items,   \
+                                                                             guard, nullptr, 0); \
+    break;
+    switch (abl) { RV_ABL_CASE(1) RV_ABL_CASE(2) RV_ABL_CASE(3) RV_ABL_CASE(4) RV_ABL_CASE(5)
+                   RV_ABL_CASE(6) RV_ABL_CASE(7) default: break; }
+#undef RV_ABL_CASE
+  } else
     rv_vote_tc_kernel<false><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(tab, segs, items,
                                                                           guard, nullptr, 0);
 }
