@@ -192,6 +192,10 @@ struct rv_ctx {
   uint64_t vote_pairs = 0;
   int32_t launches = 0, vote_launches = 0;
   void reset_counters() { vote_ms = 0; vote_pairs = 0; launches = 0; vote_launches = 0; }
+  Trace* trace = nullptr;  // RV_TRACE=1: host phase timings
+  void mark(const char* what) {
+    if (trace) trace->mark(what);
+  }
 
   int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -498,7 +502,9 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
   ctx->down.reset();
   uint32_t* hc = ctx->down.take<uint32_t>(per_rank * W);
   RV_CUDA(cudaMemcpyAsync(hc, gathered, per_rank * W * 4, cudaMemcpyDeviceToHost, s), "D2H");
+  ctx->mark("  launched");
   RV_CUDA(cudaStreamSynchronize(s), "vote");
+  ctx->mark("  synced");
   if (mode != RV_MODE_EXACT && !items.empty()) {
     float ms = 0;
     cudaEventElapsedTime(&ms, ctx->evv0, ctx->evv1);
@@ -644,10 +650,14 @@ int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double ep
   if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
   if (int rc = check_bad(ctx)) return rc;
 
+  Trace tr;
+  ctx->trace = tr.on ? &tr : nullptr;
+  ctx->mark("setup");
   rv_plan* plan = nullptr;
   if (rv_plan_create(ctx->chain.data(), (int32_t)ctx->chain.size(), levels, n, eps,
                      (double)ctx->cfg.guard, &plan) != 0)
     return ctx->fail(RV_EINVAL, "invalid search plan");
+  ctx->mark("plan");
   std::vector<uint32_t> ca, cb;
   int32_t B, mode;
   int64_t m;
@@ -662,6 +672,7 @@ int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double ep
       rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
       break;
     }
+    ctx->mark("  fed");
   }
   rv_plan_result pr{};
   if (!rc) rv_plan_get_result(plan, &pr);
@@ -675,6 +686,8 @@ int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double ep
   const int64_t mw = 0;
   rc = run_refine(ctx, x, y, offs, 1, &pid, eps, out->q_cell, ctx->cfg.refine_rounds, &mw, mask,
                   out->q, &fl, &ni);
+  ctx->mark("refine");
+  ctx->trace = nullptr;
   if (rc) return rc;
   out->flags |= fl;
   out->n_inliers = ni;

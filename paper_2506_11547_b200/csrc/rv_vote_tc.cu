@@ -14,11 +14,11 @@
 //
 // CTA roles: warp 0 lane 0 = TMA producer (one 16 KB cp.async.bulk per tile into a ring of
 // kTcStages), warp 1 = TMEM allocator + single-thread MMA issuer (2 x tcgen05.mma K=16 per
-// tile, accumulators double-buffered in 2 x 256 TMEM columns), warps 2..17 = epilogue: warp w
-// reads TMEM lanes 32*(w%4).. (its cells) and a quarter of the tile's columns; the count runs
+// tile, accumulators double-buffered in 2 x 256 TMEM columns), warps 2..9 = epilogue: warp w
+// reads TMEM lanes 32*(w%4).. (its cells) and half of the tile's columns; the count runs
 // as independent chains split between the ALU pipe (LEA.HI) and the FMA pipe (IMAD.HI).
 // Completion flows through mbarriers: full[s] (TMA tx), empty[s] (tcgen05.commit),
-// tfull[b] (tcgen05.commit), tempty[b] (the 16 epilogue warps).
+// tfull[b] (tcgen05.commit), tempty[b] (the 8 epilogue warps).
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_fp16.h>
@@ -201,7 +201,7 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 // ------------------------------------------------------------------------------------------
 // K3-TC
 // ------------------------------------------------------------------------------------------
-constexpr int kTcEpiWarps = 16;
+constexpr int kTcEpiWarps = 8;
 constexpr int kTcColsPerWarp = kTcN * 4 / kTcEpiWarps;  // each lane quarter has kTcEpiWarps/4 warps
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, epilogue warps
 constexpr int kTcAccCols = 2 * kTcN;
@@ -340,33 +340,39 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // this warp's columns of accumulator b -> registers, then hand the buffer back to the
       // MMA issuer before counting (the count overlaps the next MMA)
       const int col0 = part * kTcColsPerWarp;
-      uint32_t r0[32], r1[32];
+      uint32_t r0[32], r1[32], r2[32], r3[32];
       RV_LD32(r0, lane_addr + (uint32_t)(b * kTcN + col0));
       RV_LD32(r1, lane_addr + (uint32_t)(b * kTcN + col0 + 32));
+      RV_LD32(r2, lane_addr + (uint32_t)(b * kTcN + col0 + 64));
+      RV_LD32(r3, lane_addr + (uint32_t)(b * kTcN + col0 + 96));
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(&sm.tempty[b]);
       if (ABL & 1) {
-        n0 += r0[0] ^ r1[31];
+        n0 += r0[0] ^ r1[31] ^ r2[5] ^ r3[7];
       } else if (DUMP) {
-        if (m < it.ncell)
-          for (int e = 0; e < 64; ++e) {
-            const uint32_t bits = e < 32 ? r0[e] : r1[e - 32];
-            dump[(int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col0 + e] =
-                __uint_as_float(bits);
+        if (m < it.ncell) {
+          float* drow = dump + (int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col0;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            drow[e] = __uint_as_float(r0[e]);
+            drow[32 + e] = __uint_as_float(r1[e]);
+            drow[64 + e] = __uint_as_float(r2[e]);
+            drow[96 + e] = __uint_as_float(r3[e]);
           }
+        }
       } else {
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
+        for (int e = 0; e < 32; e += 2) {
           add_sign_alu(n0, r0[e]);
           add_sign_fma(n1, r0[e + 1], two);
-          add_sign_alu(n2, r0[e + 2]);
-          add_sign_fma(n3, r0[e + 3], two);
-          add_sign_alu(n4, r1[e]);
-          add_sign_fma(n5, r1[e + 1], two);
-          add_sign_alu(n6, r1[e + 2]);
-          add_sign_fma(n7, r1[e + 3], two);
+          add_sign_alu(n2, r1[e]);
+          add_sign_fma(n3, r1[e + 1], two);
+          add_sign_alu(n4, r2[e]);
+          add_sign_fma(n5, r2[e + 1], two);
+          add_sign_alu(n6, r3[e]);
+          add_sign_fma(n7, r3[e + 1], two);
         }
       }
     }
