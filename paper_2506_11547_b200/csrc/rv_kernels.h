@@ -24,6 +24,9 @@ namespace rv {
 #ifndef RV_PIPE
 #define RV_PIPE 0   // 0: thread 0 refills a stage after a block barrier; 1: producer warp + mbarriers
 #endif
+#ifndef RV_TC_COUNT_ALU_ONLY
+#define RV_TC_COUNT_ALU_ONLY 0
+#endif
 #ifndef RV_COUNT_ASM
 #define RV_COUNT_ASM 1
 #endif

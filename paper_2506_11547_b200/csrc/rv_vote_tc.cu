@@ -121,7 +121,12 @@ __device__ __forceinline__ void add_sign_alu(uint32_t& acc, uint32_t bits) {
   asm("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(bits >> 31));
 }
 __device__ __forceinline__ void add_sign_fma(uint32_t& acc, uint32_t bits, uint32_t two) {
+#if RV_TC_COUNT_ALU_ONLY
+  (void)two;
+  asm("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(bits >> 31));
+#else
   asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(bits), "r"(two));
+#endif
 }
 
 // byte offset of element (row, col) in the interleaved K-major layout of 32 fp16 columns:
