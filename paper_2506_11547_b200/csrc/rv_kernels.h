@@ -25,7 +25,7 @@ namespace rv {
 #define RV_PIPE 0   // 0: thread 0 refills a stage after a block barrier; 1: producer warp + mbarriers
 #endif
 #ifndef RV_TC_COUNT_ALU_ONLY
-#define RV_TC_COUNT_ALU_ONLY 0
+#define RV_TC_COUNT_ALU_ONLY 1
 #endif
 #ifndef RV_COUNT_ASM
 #define RV_COUNT_ASM 1
@@ -37,7 +37,11 @@ constexpr int kCellsPerThread = RV_CPT;            // K3 register blocking (cell
 constexpr int kCellsPerBlock = kVoteThreads * kCellsPerThread;
 constexpr int kTile = RV_TILE;                     // correspondences per TMA stage
 constexpr int kStages = RV_STAGES;
-constexpr int kTcN = 256;                          // K3-TC: correspondences per tile (MMA N)
+#ifndef RV_TC_N
+#define RV_TC_N 256
+#endif
+constexpr int kTcN = RV_TC_N;                      // K3-TC: correspondences per tile (MMA N)
+constexpr int kTcAcc = 512 / kTcN;                 // K3-TC: TMEM accumulator buffers (512 columns)
 constexpr int kTcM = 128;                          // K3-TC: cells per CTA (MMA M, TMEM lanes)
 constexpr int kTcStages = 7;                       // K3-TC: 16 KB tiles in flight (also pins 1 CTA/SM)
 constexpr int kRefThreads = 256;                   // K6/K7 block

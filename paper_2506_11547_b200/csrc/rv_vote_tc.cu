@@ -117,15 +117,17 @@ __device__ __forceinline__ void tmem_wait_ld() {
 }
 // Sign-bit counting on two pipes: acc += bits >> 31 fuses to LEA.HI (ALU pipe);
 // acc += hi32(bits * 2) is IMAD.HI (FMA pipe) when the 2 is a runtime register.
+// (volatile: tcgen05.ld destinations may only be read after tcgen05.wait::ld, so the counts
+// must not be hoisted above it)
 __device__ __forceinline__ void add_sign_alu(uint32_t& acc, uint32_t bits) {
-  asm("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(bits >> 31));
+  asm volatile("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(bits >> 31));
 }
 __device__ __forceinline__ void add_sign_fma(uint32_t& acc, uint32_t bits, uint32_t two) {
 #if RV_TC_COUNT_ALU_ONLY
   (void)two;
-  asm("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(bits >> 31));
+  asm volatile("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(bits >> 31));
 #else
-  asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(bits), "r"(two));
+  asm volatile("mad.hi.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(bits), "r"(two));
 #endif
 }
 
@@ -207,15 +209,14 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 // K3-TC
 // ------------------------------------------------------------------------------------------
 constexpr int kTcEpiWarps = 8;
-constexpr int kTcColsPerWarp = kTcN * 4 / kTcEpiWarps;  // each lane quarter has kTcEpiWarps/4 warps
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, epilogue warps
-constexpr int kTcAccCols = 2 * kTcN;
-constexpr uint32_t kTileBytes = kTcN * 64;  // 16 KB
+constexpr int kTcAccCols = kTcAcc * kTcN;  // = 512: the whole TMEM
+constexpr uint32_t kTileBytes = kTcN * 64;  // 16 KB at N = 256
 
 struct __align__(1024) TcSmem {
   uint8_t b[kTcStages][kTileBytes];  // correspondence tiles
   uint8_t a[128 * 64];               // 128 cells x 32 fp16
-  uint64_t full[kTcStages], empty[kTcStages], tfull[2], tempty[2];
+  uint64_t full[kTcStages], empty[kTcStages], tfull[kTcAcc], tempty[kTcAcc];
   uint32_t tmem_base;
 };
 
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       bar_init(&sm.full[s], 1);
       bar_init(&sm.empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kTcAcc; ++b) {
       bar_init(&sm.tfull[b], 1);
       bar_init(&sm.tempty[b], kTcEpiWarps);
     }
@@ -317,9 +318,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       const uint32_t a0 = su32(sm.a);
       for (int t = 0; t < ntiles; ++t) {
-        const int s = t % kTcStages, b = t & 1;
+        const int s = t % kTcStages, b = t % kTcAcc;
         bar_wait(&sm.full[s], (uint32_t)((t / kTcStages) & 1));
-        if (t >= 2) bar_wait(&sm.tempty[b], (uint32_t)(((t >> 1) - 1) & 1));
+        if (t >= kTcAcc) bar_wait(&sm.tempty[b], (uint32_t)(((t / kTcAcc) - 1) & 1));
         tc_fence_after();
         const uint32_t b0 = su32(sm.b[s]);
         if (!(ABL & 2)) {
@@ -335,56 +336,54 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else {
     // ---------------- epilogue: count sign bits (warps 2..9) ----------------
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-    const int part = (warp - 2) >> 2;          // which kTcColsPerWarp columns of the tile
+    const int half = (warp - 2) >> 2;          // which half of the tile's columns
     const uint32_t two = guard > -1.0f ? 2u : 3u;  // a runtime 2 (keeps IMAD.HI)
     uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, n4 = 0, n5 = 0, n6 = 0, n7 = 0;
+    constexpr int kLd = kTcN / 2 / 32;  // tcgen05.ld x32 per warp per tile
     for (int t = 0; t < ntiles; ++t) {
-      const int b = t & 1;
-      bar_wait(&sm.tfull[b], (uint32_t)((t >> 1) & 1));
+      const int b = t % kTcAcc;
+      bar_wait(&sm.tfull[b], (uint32_t)((t / kTcAcc) & 1));
       tc_fence_after();
-      // this warp's columns of accumulator b -> registers, then hand the buffer back to the
-      // MMA issuer before counting (the count overlaps the next MMA)
-      const int col0 = part * kTcColsPerWarp;
-      uint32_t r0[32], r1[32], r2[32], r3[32];
-      RV_LD32(r0, lane_addr + (uint32_t)(b * kTcN + col0));
-      RV_LD32(r1, lane_addr + (uint32_t)(b * kTcN + col0 + 32));
-      RV_LD32(r2, lane_addr + (uint32_t)(b * kTcN + col0 + 64));
-      RV_LD32(r3, lane_addr + (uint32_t)(b * kTcN + col0 + 96));
+      // this warp's half of accumulator b -> registers, then hand the buffer back to the MMA
+      // issuer before counting (the count overlaps the next MMAs)
+      const int col0 = half * (kTcN / 2);
+      uint32_t r[kLd][32];
+#pragma unroll
+      for (int q = 0; q < kLd; ++q) RV_LD32(r[q], lane_addr + (uint32_t)(b * kTcN + col0 + 32 * q));
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(&sm.tempty[b]);
       if (ABL & 1) {
-        n0 += r0[0] ^ r1[31] ^ r2[5] ^ r3[7];
+        n0 += r[0][0] ^ r[kLd - 1][31];
       } else if (DUMP) {
         if (m < it.ncell) {
           float* drow = dump + (int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col0;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            drow[e] = __uint_as_float(r0[e]);
-            drow[32 + e] = __uint_as_float(r1[e]);
-            drow[64 + e] = __uint_as_float(r2[e]);
-            drow[96 + e] = __uint_as_float(r3[e]);
-          }
+          for (int q = 0; q < kLd; ++q)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) drow[32 * q + e] = __uint_as_float(r[q][e]);
         }
       } else {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          add_sign_alu(n0, r0[e]);
-          add_sign_fma(n1, r0[e + 1], two);
-          add_sign_alu(n2, r1[e]);
-          add_sign_fma(n3, r1[e + 1], two);
-          add_sign_alu(n4, r2[e]);
-          add_sign_fma(n5, r2[e + 1], two);
-          add_sign_alu(n6, r3[e]);
-          add_sign_fma(n7, r3[e + 1], two);
-        }
+        for (int q = 0; q < kLd; ++q)
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            add_sign_alu(n0, r[q][e]);
+            add_sign_fma(n1, r[q][e + 1], two);
+            add_sign_alu(n2, r[q][e + 2]);
+            add_sign_fma(n3, r[q][e + 3], two);
+            add_sign_alu(n4, r[q][e + 4]);
+            add_sign_fma(n5, r[q][e + 5], two);
+            add_sign_alu(n6, r[q][e + 6]);
+            add_sign_fma(n7, r[q][e + 7], two);
+          }
       }
     }
     if (!DUMP && m < it.ncell) {
       // rows of the chunk: real correspondences score phi.k - t; padding rows score -1
       const uint32_t neg = (n0 + n1) + (n2 + n3) + (n4 + n5) + (n6 + n7);
-      const uint32_t cnt = (uint32_t)(it.ni / (kTcEpiWarps / 4)) - neg;  // its share of columns
+      const uint32_t cnt = (uint32_t)(it.ni / 2) - neg;  // this warp saw half of the columns
       atomicAdd(&sg.cnt_a[it.cell0 + m], cnt);
     }
   }

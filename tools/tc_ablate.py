@@ -17,5 +17,5 @@ if len(sys.argv) > 1:
         ts.append(e0.elapsed_time(e1))
     print(json.dumps({"ablate": int(sys.argv[1]), "ms": min(ts)}), flush=True)
 else:
-    for a in (0, 1, 2, 4, 3, 6, 5, 7):
+    for a in [int(v) for v in os.environ.get("ABL_LIST", "0,1,2,4,3,6,5,7").split(",")]:
         subprocess.run([sys.executable, __file__, str(a)], env=dict(os.environ, RV_TC_ABLATE=str(a)), timeout=300)
