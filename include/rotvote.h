@@ -179,6 +179,8 @@ int rot_vote_setup(rv_ctx* ctx, const float* x, const float* y, int64_t n, float
 #define RV_MODE_BOUND_TC 3 /* RV_MODE_BOUND evaluated by K3-TC (context with tensor_vote = 1):
                               cnt_a = #{s_tc >= cos(min(pi, eps + r(c))) - guard - 1.5e-5}, the extra
                               1.5e-5 covering the worst-case error of the fp16-split MMA */
+#define RV_MODE_FINAL_TC 4 /* RV_MODE_FINAL evaluated by K3-TC: cnt_a = #{s_tc >= cos(eps) - guard
+                              - 1.5e-5}, cnt_b = #{s_tc >= cos(eps) + guard + 1.5e-5} */
 
 /* a2-a5 (K3 rv_vote, K5 rv_recheck): vote m blocks of the B^3 grid.
  *   lins   DEVICE uint32[m], block (i,j,k) -> (i*B + j)*B + k.
@@ -187,6 +189,8 @@ int rot_vote_setup(rv_ctx* ctx, const float* x, const float* y, int64_t n, float
 int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t B,
                          const uint32_t* lins, int64_t m, double eps, int32_t mode,
                          uint32_t* cnt_a, uint32_t* cnt_b);
+/* (With tensor_vote = 1 the solve uses K3-TC for RV_MODE_BOUND and RV_MODE_FINAL requests;
+ *  the planner's guarantees only need cnt_b <= exact <= cnt_a, which the wider band keeps.) */
 
 /* Test hook for K3-TC's arithmetic: the raw tensor-core scores S' = s_tc - t of m blocks
  * (t = the RV_MODE_BOUND_TC threshold, guard included) against every correspondence.  out: DEVICE float

@@ -291,12 +291,12 @@ int build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64_
 // K3-TC items: CTAs of <= kTcM cells (one CTA per SM: 512 TMEM columns), correspondence
 // chunks of whole kTcN tiles; chunk count chosen, as for K3, to fill whole waves.
 void build_tc_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
-                    int slots, std::vector<rv::VoteItem>& items) {
+                    int slots, std::vector<rv::VoteItem>& items, int64_t cpb = rv::kTcM) {
   items.clear();
   int64_t cbs = 0, tmax = 0;
   for (size_t s = 0; s < ncell.size(); ++s) {
     if (ncell[s] == 0 || ncorr[s] == 0) continue;
-    cbs += (ncell[s] + rv::kTcM - 1) / rv::kTcM;
+    cbs += (ncell[s] + cpb - 1) / cpb;
     tmax = std::max<int64_t>(tmax, (ncorr[s] + rv::kTcN - 1) / rv::kTcN);
   }
   if (cbs == 0) return;
@@ -314,7 +314,7 @@ void build_tc_items(const std::vector<int64_t>& ncell, const std::vector<int64_t
   for (size_t s = 0; s < ncell.size(); ++s) {
     if (ncell[s] == 0 || ncorr[s] == 0) continue;
     const int64_t nt = (ncorr[s] + rv::kTcN - 1) / rv::kTcN;
-    const int64_t cb = (ncell[s] + rv::kTcM - 1) / rv::kTcM;
+    const int64_t cb = (ncell[s] + cpb - 1) / cpb;
     const int64_t per = (ncell[s] + cb - 1) / cb;
     const int64_t nch = std::min<int64_t>(best_nch, nt);
     const int64_t ct = (nt + nch - 1) / nch;  // tiles per chunk
@@ -437,12 +437,13 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
   }
   std::vector<rv::VoteItem> items;
   int groups = 1;
-  const bool use_tc = mode == RV_MODE_BOUND_TC || (mode == RV_MODE_BOUND && ctx->tc_on);
-  if (mode == RV_MODE_BOUND_TC && !ctx->tc_on)
-    return ctx->fail(RV_EINVAL, "RV_MODE_BOUND_TC needs a context created with tensor_vote = 1");
+  const bool tc_final = mode == RV_MODE_FINAL_TC || (mode == RV_MODE_FINAL && ctx->tc_on);
+  const bool use_tc = tc_final || mode == RV_MODE_BOUND_TC || (mode == RV_MODE_BOUND && ctx->tc_on);
+  if ((mode == RV_MODE_BOUND_TC || mode == RV_MODE_FINAL_TC) && !ctx->tc_on)
+    return ctx->fail(RV_EINVAL, "the _TC modes need a context created with tensor_vote = 1");
   if (use_tc) {
     for (rv::VoteSeg& sg : segs) sg.koff = ctx->tc_toff[0];
-    build_tc_items(ncell, ncorr, ctx->num_sms, items);
+    build_tc_items(ncell, ncorr, ctx->num_sms, items, tc_final ? rv::kTcM / 2 : rv::kTcM);
   } else if (mode == RV_MODE_EXACT) {
     build_exact_items(ncell, ncorr, items);
   } else {
@@ -484,7 +485,7 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
     RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
     if (use_tc)
       rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
-                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s);
+                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, tc_final);
     else
       rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
                       (int32_t)items.size(), ctx->cfg.guard, s);
@@ -753,10 +754,11 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   }
   std::vector<rv::VoteItem> items;
   int groups = 1;
-  const bool use_tc = mode == RV_MODE_BOUND && ctx->tc_on;
+  const bool tc_final = mode == RV_MODE_FINAL && ctx->tc_on;
+  const bool use_tc = tc_final || (mode == RV_MODE_BOUND && ctx->tc_on);
   if (use_tc) {
     for (size_t q = 0; q < reqs.size(); ++q) segs[q].koff = ctx->tc_toff[reqs[q].prob];
-    build_tc_items(ncell, ncorr, ctx->num_sms, items);
+    build_tc_items(ncell, ncorr, ctx->num_sms, items, tc_final ? rv::kTcM / 2 : rv::kTcM);
   } else if (mode == RV_MODE_EXACT) {
     build_exact_items(ncell, ncorr, items);
   } else {
@@ -797,7 +799,7 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
     if (use_tc)
       rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
-                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s);
+                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, tc_final);
     else
       rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
                       (int32_t)items.size(), ctx->cfg.guard, s);
@@ -1137,9 +1139,9 @@ int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n,
   ctx->err.clear();
   cudaSetDevice(ctx->cfg.device);
   if (int rc = validate_common(ctx, x, y, eps, 0)) return rc;
-  if (!lins || !cnt_a || (mode == RV_MODE_FINAL && !cnt_b) || m < 0)
+  if (!lins || !cnt_a || ((mode == RV_MODE_FINAL || mode == RV_MODE_FINAL_TC) && !cnt_b) || m < 0)
     return ctx->fail(RV_EINVAL, "null pointer");
-  if (mode < RV_MODE_BOUND || mode > RV_MODE_BOUND_TC) return ctx->fail(RV_EINVAL, "bad mode");
+  if (mode < RV_MODE_BOUND || mode > RV_MODE_FINAL_TC) return ctx->fail(RV_EINVAL, "bad mode");
   if (B < 1 || B > 1625) return ctx->fail(RV_EINVAL, "bad B");
   if (n < 1 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
   if (m == 0) return RV_OK;
@@ -1153,7 +1155,7 @@ int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n,
   if (int rc = eval_request(ctx, x, y, n, eps, B, mode, m, hl.data(), ha.data(), hb.data()))
     return rc;
   RV_CUDA(cudaMemcpyAsync(cnt_a, ha.data(), m * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-  if (mode == RV_MODE_FINAL)
+  if (mode == RV_MODE_FINAL || mode == RV_MODE_FINAL_TC)
     RV_CUDA(cudaMemcpyAsync(cnt_b, hb.data(), m * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
   RV_CUDA(cudaStreamSynchronize(ctx->stream), "H2D");
   return RV_OK;

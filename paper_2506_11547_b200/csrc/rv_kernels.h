@@ -96,10 +96,11 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
                      int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s);
 
 // K3-TC: BOUND-mode vote on tcgen05 (items: ncell <= kTcM, i0/ni multiples of kTcN, koff
-// in table rows).  dump != nullptr writes the raw scores S' = s - t instead of counting
+// in table rows); final_mode: RV_MODE_FINAL counts at tau -/+ guard (items: ncell <= kTcM/2).  dump != nullptr writes the raw scores S' = s - t instead of counting
 // (test hook): dump[cell * dump_ld + correspondence].
 void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* items,
-                    int32_t n_items, float guard, float* dump, int64_t dump_ld, cudaStream_t s);
+                    int32_t n_items, float guard, float* dump, int64_t dump_ld, cudaStream_t s,
+                    bool final_mode = false);
 
 // K5: exact counts (fp32 vote + fp64 recheck of |s32 - tau| < guard).  items: one block
 // per (block, correspondence chunk), ncell == 1.

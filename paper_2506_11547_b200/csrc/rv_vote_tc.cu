@@ -220,8 +220,10 @@ struct __align__(1024) TcSmem {
   uint32_t tmem_base;
 };
 
+// FIN: RV_MODE_FINAL -- two A rows per cell (TMEM lanes 2c, 2c+1) carry the thresholds
+//      tau - g' (cnt_a) and tau + g' (cnt_b), so a CTA covers kTcM/2 cells.
 // ABL (ablation, tuning only): bit0 skip the count, bit1 skip the MMAs, bit2 skip the TMA
-template <bool DUMP, int ABL = 0>
+template <bool DUMP, int ABL = 0, bool FIN = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
     rv_vote_tc_kernel(const uint8_t* __restrict__ tab, const VoteSeg* __restrict__ segs,
                       const VoteItem* __restrict__ items, float guard, float* dump,
@@ -255,12 +257,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // epilogue thread <-> TMEM lane <-> cell of the CTA
   const int m = 32 * (warp & 3) + lane;
   float init_f = 0.0f;
+  const int cell = FIN ? (m >> 1) : m;  // cell of TMEM lane / A row m
   if (warp >= 2 && warp < 6) {  // one writer per A row
     __half v[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) v[c] = __float2half_rn(0.0f);
-    if (m < it.ncell) {
-      const uint32_t lin = sg.lins[it.cell0 + m];
+    if (cell < it.ncell) {
+      const uint32_t lin = sg.lins[it.cell0 + cell];
       int32_t i, j, k;
       lin_to_ijk(lin, sg.B, i, j, k);
       double q[4], f[9];
@@ -274,7 +277,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         v[9 + t] = l;
         v[18 + t] = h;
       }
-      const double thr = bound_threshold(sg.B, i, j, k, sg.eps) - guard;
+      const double thr = FIN ? cos(sg.eps) + ((m & 1) ? guard : -guard)
+                             : bound_threshold(sg.B, i, j, k, sg.eps) - guard;
       const __half th = __double2half(-thr);
       const __half tl = __double2half(-thr - (double)__half2float(th));
       v[27] = th;
@@ -357,8 +361,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (ABL & 1) {
         n0 += r[0][0] ^ r[kLd - 1][31];
       } else if (DUMP) {
-        if (m < it.ncell) {
-          float* drow = dump + (int64_t)(it.cell0 + m) * dump_ld + it.i0 + (int64_t)t * kTcN + col0;
+        if (cell < it.ncell) {
+          float* drow = dump + (int64_t)(it.cell0 + cell) * dump_ld + it.i0 + (int64_t)t * kTcN + col0;
 #pragma unroll
           for (int q = 0; q < kLd; ++q)
 #pragma unroll
@@ -380,11 +384,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
       }
     }
-    if (!DUMP && m < it.ncell) {
+    if (!DUMP && cell < it.ncell) {
       // rows of the chunk: real correspondences score phi.k - t; padding rows score -1
       const uint32_t neg = (n0 + n1) + (n2 + n3) + (n4 + n5) + (n6 + n7);
       const uint32_t cnt = (uint32_t)(it.ni / 2) - neg;  // this warp saw half of the columns
-      atomicAdd(&sg.cnt_a[it.cell0 + m], cnt);
+      atomicAdd(FIN && (m & 1) ? &sg.cnt_b[it.cell0 + cell] : &sg.cnt_a[it.cell0 + cell], cnt);
     }
   }
   (void)init_f;
@@ -400,7 +404,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 size_t tc_smem_bytes() { return sizeof(TcSmem) + 1024; }
 
 void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* items,
-                    int32_t n_items, float guard, float* dump, int64_t dump_ld, cudaStream_t s) {
+                    int32_t n_items, float guard, float* dump, int64_t dump_ld, cudaStream_t s,
+                    bool final_mode) {
   if (n_items <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -408,7 +413,14 @@ void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* ite
                          (int)tc_smem_bytes());
     cudaFuncSetAttribute(rv_vote_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)tc_smem_bytes());
+    cudaFuncSetAttribute(rv_vote_tc_kernel<false, 0, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes());
     attr = true;
+  }
+  if (final_mode) {
+    rv_vote_tc_kernel<false, 0, true><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(
+        tab, segs, items, guard, nullptr, 0);
+    return;
   }
   static const int abl = [] {
     const char* e = getenv("RV_TC_ABLATE");  // tuning only: skip pipeline stages (wrong counts)

@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("RV_LIB") or os.path.join(_HERE, "librotvote.so")  # R
 
 RV_OK, RV_EINVAL, RV_EDATA, RV_ECUDA, RV_ENCCL, RV_ENOMEM = 0, -1, -2, -3, -4, -5
 RV_REFINED, RV_DEGENERATE, RV_RECHECKED = 1, 2, 4
-RV_MODE_BOUND, RV_MODE_FINAL, RV_MODE_EXACT, RV_MODE_BOUND_TC = 0, 1, 2, 3
+RV_MODE_BOUND, RV_MODE_FINAL, RV_MODE_EXACT, RV_MODE_BOUND_TC, RV_MODE_FINAL_TC = 0, 1, 2, 3, 4
 RV_MAX_CHAIN, RV_MAX_PHASES = 8, 16
 DEFAULT_CHAIN = (5, 15, 45, 90, 180, 360)
 
@@ -288,7 +288,7 @@ class RotVote:
             int(B), lins.data_ptr(), m, float(eps), int(mode), a.data_ptr(), b.data_ptr()))
         ca = a.cpu().numpy().view(np.uint32)
         cb = b.cpu().numpy().view(np.uint32)
-        return (ca, cb) if mode == RV_MODE_FINAL else ca
+        return (ca, cb) if mode in (RV_MODE_FINAL, RV_MODE_FINAL_TC) else ca
 
     def debug_tc_scores(self, x, y, B: int, lins, eps: float):
         """Raw K3-TC scores S' = s_tc - t (bound threshold), float32 [m, ceil(n/256)*256]."""

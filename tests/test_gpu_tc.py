@@ -116,3 +116,27 @@ def test_tc_fullsize_cfg4(rvtc, torch_cuda):
     assert np.array_equal(a.q, b.q)
     cnt, nr = oracle.count_cells(pr.x, pr.y, 360, [a.lin], math.cos(pr.eps), band=1e-12)
     assert a.votes == cnt[0]
+
+
+@pytest.mark.parametrize("n", [100, 10000, 70001])
+def test_tc_final_counts_parity(rvtc, torch_cuda, n):
+    """RV_MODE_FINAL_TC: two thresholds per cell (two TMEM lanes); cnt_b <= exact <= cnt_a."""
+    from paper_2506_11547_b200 import RV_MODE_FINAL_TC
+    torch = torch_cuda
+    pr = datagen.make_problem(n, n // 10, 0.01, 0.05, seed=8)
+    x, y = dev(torch, pr.x), dev(torch, pr.y)
+    rng = np.random.default_rng(2)
+    tau = math.cos(pr.eps)
+    ref = oracle.solve(pr.x, pr.y, pr.eps)
+    i, j, k = ref.cell
+    near = [oracle.lin_of(360, i + a, j + b, k + c) for a in (-1, 0, 1) for b in (-1, 0, 1)
+            for c in (-1, 0, 1)]
+    lins = np.unique(np.concatenate([rng.choice(oracle.candidates(360), 300, replace=False),
+                                     near]).astype(np.uint32))
+    a, b = rvtc.count_cells(x, y, 360, lins, pr.eps, RV_MODE_FINAL_TC)
+    for cnt, thr in ((a, tau - GUARD_TC), (b, tau + GUARD_TC)):
+        lo, _ = oracle.count_cells(pr.x, pr.y, 360, lins, thr + BAND, band=0)
+        hi, _ = oracle.count_cells(pr.x, pr.y, 360, lins, thr - BAND, band=0)
+        assert np.all(cnt >= lo) and np.all(cnt <= hi)
+    exact, _ = oracle.count_cells(pr.x, pr.y, 360, lins, tau, band=0)
+    assert np.all(b <= exact) and np.all(exact <= a)
