@@ -34,6 +34,17 @@ WORKLOAD = "cfg4: N=1e6 fp32 correspondences, 1% inliers (sigma=0.01), 99% unifo
 FLOP_PER_PAIR = 18          # 9 FMA per (correspondence, cell) pair in the traceless 9-entry form
 SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0   # B200_PROFILING.md nominal table
 FP32_PEAK_TFLOPS = SM_COUNT * FP32_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 74.4 TFLOP/s
+# K3-TC epilogue bound: every pair's fp32 score leaves TMEM through tcgen05.ld (64 B/clk per
+# SMSP) and costs one ALU sign-count instruction lane (16 lanes/clk per SMSP): 64 pairs/clk/SM.
+TC_EPI_PEAK_PAIRS = SM_COUNT * 4 * 16 * SM_MAX_MHZ * 1e6          # 1.86e13 pairs/s
+MMA_FLOP_PER_PAIR = 64     # executed on the tensor pipe: K = 32 (3 fp16 split terms + threshold + pad)
+
+
+def measured_peak(key, fallback):
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))[key]), "measured"
+    except (OSError, ValueError, KeyError):
+        return fallback, "fallback"
 
 
 def parse():
@@ -172,8 +183,9 @@ def _cpu_name():
 
 # ---- our arm -----------------------------------------------------------------------------------
 
-def _load_traffic():
-    p = os.path.join(ROOT, "profiles", "vote_kernel_traffic.json")
+def _load_traffic(path="ffma2"):
+    name = "vote_tc_kernel_traffic.json" if path == "tc" else "vote_kernel_traffic.json"
+    p = os.path.join(ROOT, "profiles", name)
     try:
         d = json.load(open(p))
         return d.get("bytes_per_launch"), d
@@ -265,22 +277,44 @@ def run_ours(args):
     e2e_value = r2.pair_votes * args.e2e_steps / (float(e2e_t.item()) / 1e3)
 
     achieved = vote_pairs * FLOP_PER_PAIR / (vote_ms / 1e3) / 1e12 if vote_ms > 0 else None
-    traffic, _ = _load_traffic()
+    traffic, _ = _load_traffic(args.vote)
+    if args.vote == "tc":
+        # the contraction runs on the tensor cores: fp16 dense peak (= the measured bf16 rate)
+        peak, src = measured_peak("bf16_tflops", 1590.0)
+        pairs_s = vote_pairs / (vote_ms / 1e3)
+        roofline = {
+            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "rv_vote_tc_kernel (K3-TC, tcgen05 kind::f16, fp16-split, fp32 TMEM accum)",
+            "peak_source": f"{src} dense bf16/fp16 tensor peak (MEASURED_PEAKS.json bf16_tflops)",
+            "flop_per_pair": FLOP_PER_PAIR,
+            "executed_mma_tflops": pairs_s * MMA_FLOP_PER_PAIR / 1e12,
+            "executed_mma_frac": pairs_s * MMA_FLOP_PER_PAIR / 1e12 / peak,
+            "epilogue_bound": {
+                "what": "TMEM->RF readout (tcgen05.ld 64 B/clk/SMSP, 4 B/pair) and the ALU sign "
+                        "count (16 lanes/clk/SMSP): 64 pairs/clk/SM at 1965 MHz",
+                "peak_pairs_per_s": TC_EPI_PEAK_PAIRS, "achieved_pairs_per_s": pairs_s,
+                "frac": pairs_s / TC_EPI_PEAK_PAIRS},
+            "vote_ms_per_step": vote_ms / args.steps,
+            "vote_share_of_step": (vote_ms / args.steps) / ms_per_step}
+    else:
+        roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": (achieved / FP32_PEAK_TFLOPS) if achieved else None,
+                    "traffic": traffic,
+                    "kernel": "rv_vote_kernel (K3, FFMA2), 18 flop per (corr, cell) pair",
+                    "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)",
+                    "vote_ms_per_step": vote_ms / args.steps,
+                    "vote_share_of_step": (vote_ms / args.steps) / ms_per_step}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "levels": args.levels or 5,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f16x3-split/f32" if args.vote == "tc" else "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "levels": args.levels or 5, "vote_path": args.vote,
                    "chain": [15, 45, 90, 180, 360], "l2": "flushed between steps (512 MB write)",
                    "parallelism": f"cells sharded over {world} GPU(s)" if world > 1 else "1 GPU",
                    "pair_votes_per_solve": pair_votes, "cells_per_phase": res.cells_per_phase},
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": (achieved / FP32_PEAK_TFLOPS) if achieved else None,
-                     "traffic": traffic,
-                     "kernel": "rv_vote_kernel (K3), 18 flop per (corr, cell) pair",
-                     "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)",
-                     "vote_ms_per_step": vote_ms / args.steps,
-                     "vote_share_of_step": (vote_ms / args.steps) / ms_per_step},
+        "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(2 * pr.x.nbytes),
                 "d2h_bytes_per_step": int(hmask.numel() * 4),
                 "ms_per_step": sum(e2e_ms) / len(e2e_ms)},
