@@ -208,7 +208,11 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 // ------------------------------------------------------------------------------------------
 // K3-TC
 // ------------------------------------------------------------------------------------------
-constexpr int kTcEpiWarps = 8;
+#ifndef RV_TC_EPI_WARPS
+#define RV_TC_EPI_WARPS 8
+#endif
+constexpr int kTcEpiWarps = RV_TC_EPI_WARPS;  // multiple of 4 (one lane quarter per SMSP)
+constexpr int kTcSplit = kTcEpiWarps / 4;     // warps sharing a lane quarter (column split)
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, epilogue warps
 constexpr int kTcAccCols = kTcAcc * kTcN;  // = 512: the whole TMEM
 constexpr uint32_t kTileBytes = kTcN * 64;  // 16 KB at N = 256
@@ -340,17 +344,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else {
     // ---------------- epilogue: count sign bits (warps 2..9) ----------------
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-    const int half = (warp - 2) >> 2;          // which half of the tile's columns
+    const int half = (warp - 2) >> 2;          // which 1/kTcSplit of the tile's columns
     const uint32_t two = guard > -1.0f ? 2u : 3u;  // a runtime 2 (keeps IMAD.HI)
     uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, n4 = 0, n5 = 0, n6 = 0, n7 = 0;
-    constexpr int kLd = kTcN / 2 / 32;  // tcgen05.ld x32 per warp per tile
+    constexpr int kLd = kTcN / kTcSplit / 32;  // tcgen05.ld x32 per warp per tile
     for (int t = 0; t < ntiles; ++t) {
       const int b = t % kTcAcc;
       bar_wait(&sm.tfull[b], (uint32_t)((t / kTcAcc) & 1));
       tc_fence_after();
       // this warp's half of accumulator b -> registers, then hand the buffer back to the MMA
       // issuer before counting (the count overlaps the next MMAs)
-      const int col0 = half * (kTcN / 2);
+      const int col0 = half * (kTcN / kTcSplit);
       uint32_t r[kLd][32];
 #pragma unroll
       for (int q = 0; q < kLd; ++q) RV_LD32(r[q], lane_addr + (uint32_t)(b * kTcN + col0 + 32 * q));
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (!DUMP && cell < it.ncell) {
       // rows of the chunk: real correspondences score phi.k - t; padding rows score -1
       const uint32_t neg = (n0 + n1) + (n2 + n3) + (n4 + n5) + (n6 + n7);
-      const uint32_t cnt = (uint32_t)(it.ni / 2) - neg;  // this warp saw half of the columns
+      const uint32_t cnt = (uint32_t)(it.ni / kTcSplit) - neg;  // its share of the columns
       atomicAdd(FIN && (m & 1) ? &sg.cnt_b[it.cell0 + cell] : &sg.cnt_a[it.cell0 + cell], cnt);
     }
   }
