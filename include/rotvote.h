@@ -112,7 +112,7 @@ typedef struct {
 /* ---- lifetime ------------------------------------------------------------------ */
 
 /* Fill *cfg with the defaults: device 0, rank 0, world 1, max_n 1<<20, max_problems 1,
- * default chain, refine_rounds 2, guard 1e-5, stream NULL. */
+ * default chain, refine_rounds 2, guard 1e-5, stream NULL, tensor_vote 1. */
 void rot_vote_default_config(rv_config* cfg);
 
 /* Create a context.  Allocates all workspace for cfg->max_n correspondences on
@@ -189,8 +189,9 @@ int rot_vote_setup(rv_ctx* ctx, const float* x, const float* y, int64_t n, float
 int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t B,
                          const uint32_t* lins, int64_t m, double eps, int32_t mode,
                          uint32_t* cnt_a, uint32_t* cnt_b);
-/* (With tensor_vote = 1 the solve uses K3-TC for RV_MODE_BOUND and RV_MODE_FINAL requests;
- *  the planner's guarantees only need cnt_b <= exact <= cnt_a, which the wider band keeps.) */
+/* rot_vote_count_cells maps modes to kernels literally (BOUND/FINAL: K3 on the FP32 pipe;
+ * BOUND_TC/FINAL_TC: K3-TC).  The solve with tensor_vote = 1 sends its bound and final levels
+ * to K3-TC: the planner only needs cnt_b <= exact <= cnt_a, which the wider band keeps. */
 
 /* Test hook for K3-TC's arithmetic: the raw tensor-core scores S' = s_tc - t of m blocks
  * (t = the RV_MODE_BOUND_TC threshold, guard included) against every correspondence.  out: DEVICE float

@@ -398,8 +398,11 @@ int check_bad(rv_ctx* ctx) {
 
 // ---- one planner request (single problem), sharded over ranks --------------------------------
 // Counts land in cnt_a/cnt_b (HOST, m entries each).
+// auto_tc: RV_MODE_BOUND / RV_MODE_FINAL go to K3-TC when the context has tensor_vote (the
+// solve); false keeps the explicit mode -> kernel mapping of rot_vote_count_cells.
 int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps, int32_t B,
-                 int32_t mode, int64_t m, const uint32_t* lins, uint32_t* cnt_a, uint32_t* cnt_b) {
+                 int32_t mode, int64_t m, const uint32_t* lins, uint32_t* cnt_a, uint32_t* cnt_b,
+                 bool auto_tc = true) {
   const int W = ctx->effective_world();
   const int64_t chunk = (m + W - 1) / W;
   const int64_t per_rank = 2 * chunk;  // [a | b]
@@ -437,8 +440,9 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
   }
   std::vector<rv::VoteItem> items;
   int groups = 1;
-  const bool tc_final = mode == RV_MODE_FINAL_TC || (mode == RV_MODE_FINAL && ctx->tc_on);
-  const bool use_tc = tc_final || mode == RV_MODE_BOUND_TC || (mode == RV_MODE_BOUND && ctx->tc_on);
+  const bool tc_auto = auto_tc && ctx->tc_on;
+  const bool tc_final = mode == RV_MODE_FINAL_TC || (mode == RV_MODE_FINAL && tc_auto);
+  const bool use_tc = tc_final || mode == RV_MODE_BOUND_TC || (mode == RV_MODE_BOUND && tc_auto);
   if ((mode == RV_MODE_BOUND_TC || mode == RV_MODE_FINAL_TC) && !ctx->tc_on)
     return ctx->fail(RV_EINVAL, "the _TC modes need a context created with tensor_vote = 1");
   if (use_tc) {
@@ -982,7 +986,7 @@ void rot_vote_default_config(rv_config* cfg) {
   cfg->guard = 1e-5f;
   cfg->stream = nullptr;
   cfg->emulate_world = 0;
-  cfg->tensor_vote = 0;
+  cfg->tensor_vote = 1;
 }
 
 int rot_vote_get_unique_id(void* id_out) {
@@ -1152,7 +1156,8 @@ int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n,
   std::vector<uint32_t> hl(m), ha(m), hb(m);
   RV_CUDA(cudaMemcpyAsync(hl.data(), lins, m * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
   RV_CUDA(cudaStreamSynchronize(ctx->stream), "D2H");
-  if (int rc = eval_request(ctx, x, y, n, eps, B, mode, m, hl.data(), ha.data(), hb.data()))
+  if (int rc = eval_request(ctx, x, y, n, eps, B, mode, m, hl.data(), ha.data(), hb.data(),
+                            /*auto_tc=*/false))
     return rc;
   RV_CUDA(cudaMemcpyAsync(cnt_a, ha.data(), m * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
   if (mode == RV_MODE_FINAL || mode == RV_MODE_FINAL_TC)

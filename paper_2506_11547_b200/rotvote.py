@@ -190,7 +190,7 @@ class RotVote:
     def __init__(self, device: int = 0, max_n: int = 1 << 20, max_problems: int = 1,
                  chain=None, refine_rounds: int = 2, guard: float = 1e-5, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 emulate_world: int = 0, tensor_vote: bool = False):
+                 emulate_world: int = 0, tensor_vote: bool = True):
         import torch
         cfg = rot_vote_default_config()
         cfg.device = device

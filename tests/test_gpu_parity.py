@@ -1,5 +1,9 @@
 """GPU parity: every step of the CUDA path (through the C-ABI) against the CPU oracle.
 
+These tests pin the FP32-pipe vote kernel (K3, contexts with tensor_vote=False); the
+tensor-core path (K3-TC, the default) has its own file, test_gpu_tc.py, and the solves there
+and in test_gpu_fullsize.py run the default path.
+
 Bar (BASELINE north_star):
   * counts: every (cell, correspondence) pair more than 1e-5 from the threshold in use is
     decided identically -> GPU count in [#{s >= t + 1e-5}, #{s >= t - 1e-5}] (oracle, fp64);
@@ -34,7 +38,7 @@ def rv(torch_cuda):
     from paper_2506_11547_b200 import RotVote, build
     build.build()
     oracle.build()
-    ctx = RotVote(device=0, max_n=4096 * 1000 + 4096, max_problems=4096)
+    ctx = RotVote(device=0, max_n=4096 * 1000 + 4096, max_problems=4096, tensor_vote=False)
     yield ctx
     ctx.close()
 
@@ -190,7 +194,7 @@ def test_loopback_sharding_is_invariant(torch_cuda):
     x, y = dev(torch, pr.x), dev(torch, pr.y)
     outs = []
     for W in (1, 2, 3, 8):
-        ctx = RotVote(max_n=1 << 16, emulate_world=W)
+        ctx = RotVote(max_n=1 << 16, emulate_world=W, tensor_vote=False)
         outs.append(ctx.solve(x, y, pr.eps))
         ctx.close()
     for r in outs[1:]:
@@ -312,7 +316,7 @@ def test_edge_cases(rv, torch_cuda):
     check_solution(r, ref)
     # n > max_n
     from paper_2506_11547_b200 import RotVote
-    small = RotVote(max_n=100)
+    small = RotVote(max_n=100, tensor_vote=False)
     with pytest.raises(RotVoteError) as e:
         small.solve(x, y, 0.05) if x.shape[0] > 100 else small.solve(
             dev(torch, np.tile(pr.x, (2, 1))), dev(torch, np.tile(pr.y, (2, 1))), 0.05)
@@ -338,8 +342,9 @@ def test_nccl_path_single_rank(torch_cuda):
     torch = torch_cuda
     pr = datagen.cfg2(seed=3)
     x, y = dev(torch, pr.x), dev(torch, pr.y)
-    plain = RotVote(max_n=1 << 16)
-    viaccl = RotVote(max_n=1 << 16, max_problems=8, nccl_id=rot_vote_get_unique_id())
+    plain = RotVote(max_n=1 << 16, tensor_vote=False)
+    viaccl = RotVote(max_n=1 << 16, max_problems=8, nccl_id=rot_vote_get_unique_id(),
+                     tensor_vote=False)
     a, b = plain.solve(x, y, pr.eps), viaccl.solve(x, y, pr.eps)
     assert (a.cell, a.votes, a.n_tied, a.pair_votes) == (b.cell, b.votes, b.n_tied, b.pair_votes)
     assert np.array_equal(a.q, b.q)

@@ -109,7 +109,7 @@ def test_tc_fullsize_cfg4(rvtc, torch_cuda):
     pr = datagen.cfg4()
     x, y = dev(torch, pr.x), dev(torch, pr.y)
     a = rvtc.solve(x, y, pr.eps)
-    f = RotVote(max_n=pr.n)
+    f = RotVote(max_n=pr.n, tensor_vote=False)
     b = f.solve(x, y, pr.eps)
     f.close()
     assert (a.cell, a.votes, a.n_tied) == (b.cell, b.votes, b.n_tied)
@@ -140,3 +140,22 @@ def test_tc_final_counts_parity(rvtc, torch_cuda, n):
         assert np.all(cnt >= lo) and np.all(cnt <= hi)
     exact, _ = oracle.count_cells(pr.x, pr.y, 360, lins, tau, band=0)
     assert np.all(b <= exact) and np.all(exact <= a)
+
+
+def test_tc_loopback_and_nccl_paths(torch_cuda):
+    """The sharded paths (loopback ranks, 1-rank NCCL communicator) with the tensor-core
+    vote give the direct answer."""
+    from paper_2506_11547_b200 import RotVote, rot_vote_get_unique_id
+    torch = torch_cuda
+    pr = datagen.cfg2(seed=9)
+    x, y = dev(torch, pr.x), dev(torch, pr.y)
+    base = RotVote(max_n=1 << 16)
+    ref = base.solve(x, y, pr.eps)
+    for ctx in (RotVote(max_n=1 << 16, emulate_world=3),
+                RotVote(max_n=1 << 16, nccl_id=rot_vote_get_unique_id())):
+        r = ctx.solve(x, y, pr.eps)
+        assert (r.cell, r.votes, r.n_tied, r.pair_votes) == (ref.cell, ref.votes, ref.n_tied,
+                                                             ref.pair_votes)
+        assert np.array_equal(r.q, ref.q)
+        ctx.close()
+    base.close()
