@@ -52,6 +52,21 @@ int  rv_plan_request(const rv_plan* p, int32_t* B, int32_t* mode, int64_t* m,
 /* 1 if the pending request is the complete candidate list of its grid (level 0, or the
  * exhaustive scan), i.e. identical to rv_grid_candidates(B); 0 otherwise. */
 int  rv_plan_request_is_full_grid(const rv_plan* p);
+/* Level 0 reduced by the caller (batched solves keep level-0 counts on the device).
+ * rv_plan_feed_l0_start replaces rv_plan_feed for a level-0 RV_MODE_BOUND request: `start` is
+ * the index (into that request) of the dive's first block, the one rv_plan_feed would pick --
+ * max excess UB - n*bg[e] with bg = rv_plan_l0_background, blocks with their centre inside the
+ * ball first, ties -> lowest index.  After the dive the plan has no request and
+ * rv_plan_needs_l0_survivors returns 1 with the pruning bound; the caller then passes the
+ * indices of the level-0 blocks with UB >= lb_star (ascending) to rv_plan_feed_l0_survivors.
+ * All return 0 / -1 (wrong state or index). */
+int  rv_plan_feed_l0_start(rv_plan* p, int64_t start);
+int  rv_plan_needs_l0_survivors(const rv_plan* p, int64_t* lb_star);
+int  rv_plan_feed_l0_survivors(rv_plan* p, const int32_t* idx, int64_t k);
+/* The cached per-candidate background (1 - cos(min(pi, eps + r(c))))/2 of the full grid B, in
+ * rv_grid_candidates order (HOST, valid for the process lifetime); NULL when not cached. */
+const double* rv_plan_l0_background(int32_t B, double eps, int64_t* m);
+
 /* Feed the counts of the pending request (HOST arrays of m entries).  0 or -1. */
 int  rv_plan_feed(rv_plan* p, const uint32_t* cnt_a, const uint32_t* cnt_b);
 /* 0 when done and *out filled, -1 while requests are pending. */

@@ -183,6 +183,12 @@ struct rv_ctx {
   DevBuf<uint32_t> hmask;
   DevBuf<char> gather;           // batched result all-gather
   DevBuf<uint32_t> grid_list;    // device copy of one grid's full candidate list (batched L0)
+  DevBuf<uint32_t> l0cnt;        // batched level-0 counts kept on the device [P][m0]
+  DevBuf<double> l0bg;           // device copy of the level-0 background table
+  int32_t l0bg_B = 0;
+  double l0bg_eps = 0;
+  DevBuf<int32_t> l0idx;         // K4 outputs / survivor indices
+  DevBuf<int64_t> l0aux;         // lb / offsets for K4
   int32_t grid_list_B = 0;
   int64_t grid_list_m = 0;
   Staging up, down;
@@ -718,10 +724,12 @@ struct BatchReq {
   bool full_grid;      // the complete candidate list of B: served from one device copy
 };
 
+// keep_dev != nullptr: the cnt_a counts stay on the device (copied to keep_dev, request order)
+// and nothing is read back (level 0 of a batched solve, reduced by the K4 kernels).
 int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
                const std::vector<int64_t>& koff, double eps, int32_t mode,
                const std::vector<BatchReq>& reqs, std::vector<std::vector<uint32_t>>& ca,
-               std::vector<std::vector<uint32_t>>& cb) {
+               std::vector<std::vector<uint32_t>>& cb, uint32_t* keep_dev = nullptr) {
   if (reqs.empty()) return RV_OK;
   int64_t total = 0, upload = 0;
   for (const BatchReq& r : reqs) {
@@ -813,6 +821,16 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   }
   ctx->launches += items.empty() ? 0 : 1;
   RV_CUDA(cudaGetLastError(), "launching the vote kernel");
+  if (keep_dev) {
+    RV_CUDA(cudaMemcpyAsync(keep_dev, ctx->cnt.p, total * 4, cudaMemcpyDeviceToDevice, s), "D2D");
+    RV_CUDA(cudaStreamSynchronize(s), "batched vote");
+    if (mode != RV_MODE_EXACT && !items.empty()) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ctx->evv0, ctx->evv1);
+      ctx->vote_ms += ms;
+    }
+    return RV_OK;
+  }
   ctx->down.reset();
   uint32_t* hc = ctx->down.take<uint32_t>(2 * total);
   RV_CUDA(cudaMemcpyAsync(hc, ctx->cnt.p, ncnt * 4, cudaMemcpyDeviceToHost, s), "D2H");
@@ -865,6 +883,8 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
       if (!plans[p]) rc = ctx->fail(RV_EINVAL, "invalid search plan");
     tr.mark("plans created");
     std::vector<std::vector<uint32_t>> ca(PL), cb(PL);
+    bool l0_on_device = false;
+    int64_t m0 = 0;
     while (!rc) {
       std::vector<BatchReq> by_mode[3];
       bool any = false;
@@ -879,6 +899,44 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
       }
       if (!any) break;
       tr.mark("requests gathered");
+      // level 0 of a batch (every problem, same full grid, bound mode): reduce on the device
+      const std::vector<BatchReq>& g0 = by_mode[RV_MODE_BOUND];
+      bool l0_reduce = PL >= 2 && (int64_t)g0.size() == PL && !by_mode[1].size() &&
+                       !by_mode[2].size();
+      for (const BatchReq& r : g0) l0_reduce = l0_reduce && r.full_grid && r.m == g0[0].m;
+      if (l0_reduce) {
+        int64_t mbg = 0;
+        const double* bgh = rv_plan_l0_background(g0[0].B, eps, &mbg);
+        l0_reduce = bgh && mbg == g0[0].m;
+        if (l0_reduce) {
+          m0 = g0[0].m;
+          RV_CUDA(ctx->l0cnt.ensure((size_t)PL * m0), "allocating level-0 counts");
+          if (ctx->l0bg_B != g0[0].B || ctx->l0bg_eps != eps || ctx->l0bg.cap < (size_t)m0) {
+            RV_CUDA(ctx->l0bg.ensure(m0), "allocating");
+            RV_CUDA(cudaMemcpy(ctx->l0bg.p, bgh, m0 * sizeof(double), cudaMemcpyHostToDevice),
+                    "H2D background");
+            ctx->l0bg_B = g0[0].B;
+            ctx->l0bg_eps = eps;
+          }
+          rc = eval_batch(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, g0, ca, cb, ctx->l0cnt.p);
+          if (rc) break;
+          RV_CUDA(ctx->l0idx.ensure(PL), "allocating");
+          rv::launch_l0_argmax(ctx->l0cnt.p, m0, ctx->grid_list.p, g0[0].B, ctx->l0bg.p,
+                               ctx->rows.p, PL, ctx->l0idx.p, ctx->stream);
+          ctx->launches += 1;
+          std::vector<int32_t> start(PL);
+          RV_CUDA(cudaMemcpyAsync(start.data(), ctx->l0idx.p, PL * 4, cudaMemcpyDeviceToHost,
+                                  ctx->stream), "D2H");
+          RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 argmax");
+          std::vector<int> bad(PL, 0);
+          parallel_for(PL, [&](int64_t p) { bad[p] = rv_plan_feed_l0_start(plans[p], start[p]); });
+          for (int b : bad)
+            if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected the level-0 start");
+          l0_on_device = true;
+          tr.mark("  level 0 on device");
+          continue;
+        }
+      }
       for (int md = 0; md < 3 && !rc; ++md) {
         if (by_mode[md].empty()) continue;
         rc = eval_batch(ctx, x, y, rows, koff, eps, md, by_mode[md], ca, cb);
@@ -894,6 +952,50 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
           if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
         tr.mark("  feed");
       }
+      if (rc || !l0_on_device) continue;
+      // plans whose dive ended: compact their level-0 survivors (UB >= lb*) on the device
+      std::vector<int32_t> need;
+      std::vector<int64_t> lbs;
+      for (int32_t p = 0; p < PL; ++p) {
+        int64_t lb = 0;
+        if (rv_plan_needs_l0_survivors(plans[p], &lb)) {
+          need.push_back(p);
+          lbs.push_back(lb);
+        }
+      }
+      if (need.empty()) continue;
+      const int32_t J = (int32_t)need.size();
+      RV_CUDA(ctx->l0idx.ensure(2 * (size_t)J + 1), "allocating");
+      RV_CUDA(ctx->l0aux.ensure(2 * (size_t)J + 1), "allocating");
+      int32_t* dprob = ctx->l0idx.p;
+      int32_t* dcnt = ctx->l0idx.p + J;
+      int64_t* dlb = ctx->l0aux.p;
+      int64_t* doff = ctx->l0aux.p + J;
+      RV_CUDA(cudaMemcpyAsync(dprob, need.data(), J * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+      RV_CUDA(cudaMemcpyAsync(dlb, lbs.data(), J * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+      rv::launch_l0_survivors(ctx->l0cnt.p, m0, dprob, dlb, nullptr, J, dcnt, nullptr, ctx->stream);
+      std::vector<int32_t> k(J);
+      RV_CUDA(cudaMemcpyAsync(k.data(), dcnt, J * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+      RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
+      std::vector<int64_t> offv(J + 1, 0);
+      for (int32_t j = 0; j < J; ++j) offv[j + 1] = offv[j] + k[j];
+      DevBuf<int32_t> surv;
+      RV_CUDA(surv.ensure(std::max<int64_t>(1, offv[J])), "allocating");
+      RV_CUDA(cudaMemcpyAsync(doff, offv.data(), J * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+      rv::launch_l0_survivors(ctx->l0cnt.p, m0, dprob, dlb, doff, J, nullptr, surv.p, ctx->stream);
+      ctx->launches += 2;
+      std::vector<int32_t> idx(std::max<int64_t>(1, offv[J]));
+      RV_CUDA(cudaMemcpyAsync(idx.data(), surv.p, offv[J] * 4, cudaMemcpyDeviceToHost, ctx->stream),
+              "D2H");
+      RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
+      surv.release();
+      std::vector<int> bad(J, 0);
+      parallel_for(J, [&](int64_t j) {
+        bad[j] = rv_plan_feed_l0_survivors(plans[need[j]], idx.data() + offv[j], k[j]);
+      });
+      for (int b : bad)
+        if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected the level-0 survivors");
+      tr.mark("  level-0 survivors");
     }
     std::vector<double> q0((size_t)PL * 4), qf((size_t)PL * 4);
     std::vector<int32_t> fl(PL), ids(PL);
@@ -1068,6 +1170,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->qs.release(); ctx->flags.release(); ctx->ninl.release(); ctx->rows.release();
   ctx->koffs.release(); ctx->bad.release(); ctx->hx.release(); ctx->hy.release();
   ctx->hmask.release(); ctx->gather.release(); ctx->grid_list.release();
+  ctx->l0cnt.release(); ctx->l0bg.release(); ctx->l0idx.release(); ctx->l0aux.release();
   ctx->up.release(); ctx->down.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);

@@ -47,6 +47,15 @@ RV_HD bool is_candidate(int32_t B, int32_t i, int32_t j, int32_t k) {
   return dmin2_scaled(B, i, j, k) <= (int64_t)B * B;
 }
 
+// Centre of block (i,j,k) inside the closed unit ball (its rotation lies in the q3 <= 0
+// hemisphere proper); used by the dive heuristic only.
+RV_HD bool centre_inside(int32_t B, uint32_t lin) {
+  int32_t i, j, k;
+  lin_to_ijk(lin, B, i, j, k);
+  const int64_t a = 2 * (int64_t)i + 1 - B, b = 2 * (int64_t)j + 1 - B, c = 2 * (int64_t)k + 1 - B;
+  return a * a + b * b + c * c <= (int64_t)B * B;
+}
+
 // Reading R6: every rotation of the block lies within rotation angle
 //   r(c) = 2 * (2 / (1 + dmin^2)) * sqrt(3) / B
 // of R(q_c): the half diagonal sqrt(3)/B times the largest conformal factor of P'

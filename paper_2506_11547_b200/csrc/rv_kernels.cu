@@ -597,3 +597,97 @@ void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* q
 }
 
 }  // namespace rv
+
+namespace rv {
+
+// ------------------------------------------------------------------------------------------
+// K4 (batched): level-0 reductions on the device, one CTA per problem.  cnt is [P][m0] (the
+// level-0 UB counts of every problem against the shared candidate list lins[m0]).
+// ------------------------------------------------------------------------------------------
+// dive start: max excess UB - n*bg[e], blocks with their centre inside the ball first, ties ->
+// lowest index (the same key, in the same double arithmetic, as the host planner)
+__global__ void __launch_bounds__(256) rv_l0_argmax_kernel(const uint32_t* __restrict__ cnt,
+                                                           int64_t m0,
+                                                           const uint32_t* __restrict__ lins,
+                                                           int32_t B, const double* __restrict__ bg,
+                                                           const int64_t* __restrict__ rows,
+                                                           int32_t* out) {
+  const int p = blockIdx.x;
+  const double n = (double)(rows[p + 1] - rows[p]);
+  const uint32_t* c = cnt + (int64_t)p * m0;
+  int best = -1, bin = 0;
+  double bx = -1e300;
+  for (int e = threadIdx.x; e < m0; e += blockDim.x) {
+    const int in = centre_inside(B, lins[e]) ? 1 : 0;
+    const double x = (double)c[e] - n * bg[e];
+    if (best < 0 || in > bin || (in == bin && (x > bx || (x == bx && e < best)))) {
+      best = e; bin = in; bx = x;
+    }
+  }
+  __shared__ int sb[256], si[256];
+  __shared__ double sx[256];
+  sb[threadIdx.x] = best; si[threadIdx.x] = bin; sx[threadIdx.x] = bx;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const int o = threadIdx.x + w;
+      const int b2 = sb[o];
+      if (b2 >= 0) {
+        const int b1 = sb[threadIdx.x];
+        const bool take = b1 < 0 || si[o] > si[threadIdx.x] ||
+                          (si[o] == si[threadIdx.x] &&
+                           (sx[o] > sx[threadIdx.x] || (sx[o] == sx[threadIdx.x] && b2 < b1)));
+        if (take) { sb[threadIdx.x] = b2; si[threadIdx.x] = si[o]; sx[threadIdx.x] = sx[o]; }
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[p] = sb[0];
+}
+
+// survivors (UB >= lb) of the listed problems: count pass (outc != nullptr) or compaction pass
+// (ascending indices at out + off[j]); problems[j], lb[j] per listed problem j = blockIdx.x
+__global__ void __launch_bounds__(256) rv_l0_survivors_kernel(const uint32_t* __restrict__ cnt,
+                                                              int64_t m0,
+                                                              const int32_t* __restrict__ problems,
+                                                              const int64_t* __restrict__ lb,
+                                                              const int64_t* __restrict__ off,
+                                                              int32_t* outc, int32_t* out) {
+  const int j = blockIdx.x;
+  const uint32_t* c = cnt + (int64_t)problems[j] * m0;
+  const int64_t L = lb[j];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int wsum[8];
+  int base = 0;
+  for (int64_t e0 = 0; e0 < m0; e0 += blockDim.x) {
+    const int64_t e = e0 + threadIdx.x;
+    const bool keep = e < m0 && (int64_t)c[e] >= L;
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      if (w < warp) before += wsum[w];
+      total += wsum[w];
+    }
+    if (out && keep) out[off[j] + base + before + __popc(bal & ((1u << lane) - 1u))] = (int32_t)e;
+    base += total;
+    __syncthreads();
+  }
+  if (outc && threadIdx.x == 0) outc[j] = base;
+}
+
+void launch_l0_argmax(const uint32_t* cnt, int64_t m0, const uint32_t* lins, int32_t B,
+                      const double* bg, const int64_t* rows, int32_t P, int32_t* out,
+                      cudaStream_t s) {
+  if (P > 0) rv_l0_argmax_kernel<<<P, 256, 0, s>>>(cnt, m0, lins, B, bg, rows, out);
+}
+
+void launch_l0_survivors(const uint32_t* cnt, int64_t m0, const int32_t* problems,
+                         const int64_t* lb, const int64_t* off, int32_t J, int32_t* outc,
+                         int32_t* out, cudaStream_t s) {
+  if (J > 0)
+    rv_l0_survivors_kernel<<<J, 256, 0, s>>>(cnt, m0, problems, lb, off, outc, out);
+}
+
+}  // namespace rv

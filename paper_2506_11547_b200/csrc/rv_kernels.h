@@ -102,6 +102,17 @@ void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* ite
                     int32_t n_items, float guard, float* dump, int64_t dump_ld, cudaStream_t s,
                     bool final_mode = false);
 
+// K4 (batched): level-0 reductions, one CTA per problem.  argmax: the dive's start index per
+// problem (planner key, see rv_plan_feed_l0_start).  survivors: outc != nullptr counts the
+// blocks with UB >= lb[j] of problem problems[j]; otherwise writes their indices ascending at
+// out + off[j].
+void launch_l0_argmax(const uint32_t* cnt, int64_t m0, const uint32_t* lins, int32_t B,
+                      const double* bg, const int64_t* rows, int32_t P, int32_t* out,
+                      cudaStream_t s);
+void launch_l0_survivors(const uint32_t* cnt, int64_t m0, const int32_t* problems,
+                         const int64_t* lb, const int64_t* off, int32_t J, int32_t* outc,
+                         int32_t* out, cudaStream_t s);
+
 // K5: exact counts (fp32 vote + fp64 recheck of |s32 - tau| < guard).  items: one block
 // per (block, correspondence chunk), ncell == 1.
 void launch_exact(const float* k9, int64_t stride, const float* x, const float* y,

@@ -29,7 +29,7 @@
 
 namespace {
 
-enum Phase { PH_L0, PH_DIVE, PH_BNB, PH_RECHECK, PH_DONE };
+enum Phase { PH_L0, PH_DIVE, PH_NEED_SURV, PH_BNB, PH_RECHECK, PH_DONE };
 
 std::vector<uint32_t> candidates_of(int32_t B) {
   std::vector<uint32_t> out;
@@ -40,16 +40,10 @@ std::vector<uint32_t> candidates_of(int32_t B) {
   return out;
 }
 
-// Centre of block (i,j,k) inside the closed unit ball (its rotation is in the q3 <= 0
-// hemisphere proper).  Blocks that merely touch the ball from outside represent rotations of
-// the far side; the dive starts and steps only through inside blocks when there are any
+// The dive starts and steps only through blocks whose centre lies inside the ball when there
+// are any: blocks that merely touch the ball from outside represent rotations of the far side
 // (a heuristic -- the certified pruning is unaffected).
-bool centre_inside(int32_t B, uint32_t lin) {
-  int32_t i, j, k;
-  rv::lin_to_ijk(lin, B, i, j, k);
-  const int64_t a = 2 * (int64_t)i + 1 - B, b = 2 * (int64_t)j + 1 - B, c = 2 * (int64_t)k + 1 - B;
-  return a * a + b * b + c * c <= (int64_t)B * B;
-}
+using rv::centre_inside;
 
 // Process-wide caches of a grid's candidate list and of the per-candidate uniform-outlier
 // background (1 - cos(min(pi, eps + r(c))))/2 (batched solves create thousands of planners
@@ -101,6 +95,7 @@ struct rv_plan {
   std::vector<uint32_t> cells;  // pending request
 
   std::vector<uint32_t> l0_cells, l0_ub;
+  bool l0_ext = false;  // level 0 reduced by the caller (rv_plan_feed_l0_start / _survivors)
   int64_t lb_star = 0;
   // finest level
   std::vector<uint32_t> fin_cells, fin_lo, fin_hi, recheck_idx;
@@ -187,10 +182,20 @@ struct rv_plan {
     std::vector<uint32_t> surv;
     for (size_t e = 0; e < l0_cells.size(); ++e)
       if ((int64_t)l0_ub[e] >= lb_star) surv.push_back(l0_cells[e]);
+    start_bnb_from(surv);
+  }
+  void start_bnb_from(const std::vector<uint32_t>& surv) {
     phase = PH_BNB;
     level = 1;
     mode = mode_for(level);
     cells = children(0, surv);
+    note_request();
+  }
+  void start_dive(size_t s) {
+    phase = PH_DIVE;
+    level = 1;
+    mode = mode_for(level);
+    cells = children(0, neighbourhood(0, l0_cells[s]));
     note_request();
   }
 
@@ -249,11 +254,7 @@ struct rv_plan {
         l0_ub.assign(a, a + cells.size());
         const std::vector<double>* bg = grid_background(chain[0], eps);  // (1 - t_c)/2, cached
         size_t s = best_excess(chain[0], l0_cells, l0_ub.data(), bg ? bg->data() : nullptr);
-        phase = PH_DIVE;
-        level = 1;
-        mode = mode_for(level);
-        cells = children(0, neighbourhood(0, l0_cells[s]));
-        note_request();
+        start_dive(s);
         return 0;
       }
       case PH_DIVE: {
@@ -267,7 +268,12 @@ struct rv_plan {
         } else {
           lb_star = 0;
           for (size_t e = 0; e < cells.size(); ++e) lb_star = std::max<int64_t>(lb_star, b[e]);
-          start_bnb();
+          if (l0_ext) {  // the caller compacts the level-0 survivors (UB >= lb_star)
+            phase = PH_NEED_SURV;
+            cells.clear();
+          } else {
+            start_bnb();
+          }
         }
         return 0;
       }
@@ -327,12 +333,40 @@ int rv_plan_create(const int32_t* chain, int32_t chain_len, int32_t levels, int6
 void rv_plan_destroy(rv_plan* p) { delete p; }
 
 int rv_plan_request(const rv_plan* p, int32_t* B, int32_t* mode, int64_t* m, const uint32_t** lins) {
-  if (!p || p->phase == PH_DONE) return 0;
+  if (!p || p->phase == PH_DONE || p->phase == PH_NEED_SURV) return 0;
   if (B) *B = p->chain[p->level];
   if (mode) *mode = p->mode;
   if (m) *m = (int64_t)p->cells.size();
   if (lins) *lins = p->cells.data();
   return 1;
+}
+
+int rv_plan_feed_l0_start(rv_plan* p, int64_t start) {
+  if (!p || p->phase != PH_L0 || p->mode != RV_MODE_BOUND) return -1;
+  if (start < 0 || start >= (int64_t)p->cells.size()) return -1;
+  p->l0_cells = p->cells;
+  p->l0_ub.clear();
+  p->l0_ext = true;
+  p->start_dive((size_t)start);
+  return 0;
+}
+
+int rv_plan_needs_l0_survivors(const rv_plan* p, int64_t* lb_star) {
+  if (!p || p->phase != PH_NEED_SURV) return 0;
+  if (lb_star) *lb_star = p->lb_star;
+  return 1;
+}
+
+int rv_plan_feed_l0_survivors(rv_plan* p, const int32_t* idx, int64_t k) {
+  if (!p || p->phase != PH_NEED_SURV || k < 0 || (k > 0 && !idx)) return -1;
+  std::vector<uint32_t> surv;
+  surv.reserve(k);
+  for (int64_t e = 0; e < k; ++e) {
+    if (idx[e] < 0 || idx[e] >= (int64_t)p->l0_cells.size()) return -1;
+    surv.push_back(p->l0_cells[idx[e]]);
+  }
+  p->start_bnb_from(surv);
+  return 0;
 }
 
 int rv_plan_request_is_full_grid(const rv_plan* p) {
@@ -342,6 +376,12 @@ int rv_plan_request_is_full_grid(const rv_plan* p) {
 int rv_plan_feed(rv_plan* p, const uint32_t* cnt_a, const uint32_t* cnt_b) {
   if (!p) return -1;
   return p->feed(cnt_a, cnt_b);
+}
+
+const double* rv_plan_l0_background(int32_t B, double eps, int64_t* m) {
+  const std::vector<double>* bg = grid_background(B, eps);
+  if (m) *m = bg ? (int64_t)bg->size() : 0;
+  return bg ? bg->data() : nullptr;
 }
 
 int rv_plan_get_result(const rv_plan* p, rv_plan_result* out) {

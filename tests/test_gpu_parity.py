@@ -270,6 +270,8 @@ def test_batched_cfg5_equals_single_solves(rv, torch_cuda):
         single = rv.solve(dev(torch, pr.x), dev(torch, pr.y), bt.eps)
         assert (res[p].cell, res[p].votes, res[p].n_tied) == (single.cell, single.votes, single.n_tied)
         assert np.array_equal(res[p].q, single.q)
+        # the device-side level-0 reduction takes the host planner's decisions
+        assert res[p].cells_per_phase == single.cells_per_phase
         ref = oracle.solve(pr.x, pr.y, bt.eps)
         check_solution(res[p], ref)
     from scipy.spatial.transform import Rotation as Rot

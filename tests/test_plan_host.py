@@ -81,3 +81,50 @@ def test_planner_request_protocol():
     assert B == 5 and mode == rvmod.RV_MODE_BOUND and np.all(np.diff(lins.astype(np.int64)) > 0)
     with pytest.raises(ValueError):
         plan.result()
+
+
+def test_planner_external_level0_protocol():
+    """rv_plan_feed_l0_start / rv_plan_feed_l0_survivors (the batched solve's device-side
+    level-0 reduction) reach the same result and cells as feeding level 0 directly."""
+    import ctypes as C
+    from planner_util import oracle_counts
+    L = rvmod.lib()
+    L.rv_plan_feed_l0_start.argtypes = [C.c_void_p, C.c_int64]
+    L.rv_plan_needs_l0_survivors.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    L.rv_plan_feed_l0_survivors.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    L.rv_plan_l0_background.argtypes = [C.c_int32, C.c_double, C.POINTER(C.c_int64)]
+    L.rv_plan_l0_background.restype = C.POINTER(C.c_double)
+    rng = np.random.default_rng(31)
+    for trial in range(25):
+        n = int(rng.integers(5, 400))
+        eps = float(rng.choice([0.05, 0.1, 0.3]))
+        pr = datagen.make_problem(n, n // 4, 0.01, eps, seed=int(rng.integers(1 << 30)))
+        chain = (5, 15, 45, 90)
+        ref = run_plan(pr.x, pr.y, eps, chain, 0)
+        plan = rvmod.Plan(chain, 0, n, eps)
+        B, mode, lins = plan.request()
+        ub, _ = oracle_counts(pr.x, pr.y, eps, B, mode, lins)
+        m = C.c_int64()
+        bgp = L.rv_plan_l0_background(B, eps, C.byref(m))
+        bg = np.ctypeslib.as_array(bgp, shape=(m.value,))
+        # the documented key: centre inside first, then max excess, ties -> lowest index
+        ijk = np.stack([lins // (B * B), (lins // B) % B, lins % B], 1).astype(np.int64)
+        inside = (((2 * ijk + 1 - B) ** 2).sum(1) <= B * B)
+        excess = ub.astype(np.float64) - float(n) * bg
+        order = sorted(range(lins.size), key=lambda e: (-int(inside[e]), -excess[e], e))
+        assert L.rv_plan_feed_l0_start(plan.h, order[0]) == 0
+        while True:
+            lb = C.c_int64()
+            if L.rv_plan_needs_l0_survivors(plan.h, C.byref(lb)):
+                surv = np.flatnonzero(ub.astype(np.int64) >= lb.value).astype(np.int32)
+                assert L.rv_plan_feed_l0_survivors(plan.h, surv.ctypes.data, surv.size) == 0
+                continue
+            req = plan.request()
+            if req is None:
+                break
+            B2, mode2, l2 = req
+            a, b = oracle_counts(pr.x, pr.y, eps, B2, mode2, l2)
+            plan.feed(a, b)
+        r = plan.result()
+        assert (r.lin, r.votes, r.n_tied, r.cells_evaluated) == (ref.lin, ref.votes, ref.n_tied,
+                                                                 ref.cells_evaluated)
