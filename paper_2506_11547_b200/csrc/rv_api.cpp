@@ -20,6 +20,7 @@
 #include "../../include/rotvote.h"
 #include "../../include/rotvote_plan.h"
 #include "rv_geom.h"
+#include "rv_dplan.h"
 #include "rv_kernels.h"
 
 namespace {
@@ -191,13 +192,31 @@ struct rv_ctx {
   DevBuf<int64_t> l0aux;         // lb / offsets for K4
   int32_t grid_list_B = 0;
   int64_t grid_list_m = 0;
+  std::vector<uint32_t> grid_host;  // candidate list of grid_host_B (host)
+  int32_t grid_host_B = 0;
+  // device-resident batched level loop (rv_dplan.cu): ping-pong block lists + counts, the
+  // per-problem offsets/counts/picks/bounds, the recheck lists and the winners
+  DevBuf<uint32_t> dp_lins[2], dp_ca[2], dp_cb[2];
+  DevBuf<int64_t> dp_off[2], dp_lb, dp_roff;
+  DevBuf<int32_t> dp_cnt[2], dp_rcnt, dp_rlist, dp_res;
+  DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex;
+  DevBuf<int32_t> l0surv;        // host-planner batched path: level-0 survivor indices
+  bool vote_pending = false;     // evv0/evv1 bracket a vote launch not yet accounted
+  void collect_vote_ms() {
+    if (!vote_pending) return;
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, evv0, evv1) == cudaSuccess) vote_ms += ms;
+    vote_pending = false;
+  }
   Staging up, down;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evv0 = nullptr, evv1 = nullptr;
   // per-call counters reported in rv_result
   float vote_ms = 0;
   uint64_t vote_pairs = 0;
   int32_t launches = 0, vote_launches = 0;
-  void reset_counters() { vote_ms = 0; vote_pairs = 0; launches = 0; vote_launches = 0; }
+  void reset_counters() {
+    vote_ms = 0; vote_pairs = 0; launches = 0; vote_launches = 0; vote_pending = false;
+  }
   Trace* trace = nullptr;  // RV_TRACE=1: host phase timings
   void mark(const char* what) {
     if (trace) trace->mark(what);
@@ -849,6 +868,274 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   return RV_OK;
 }
 
+// ---- batched: the level loop on the device (rv_dplan.cu) --------------------------------------
+// Vote per-problem block lists that already live on the device: problem p's list is
+// dlins + hoff[p] (hcnt[p] blocks), its counts land at dca / dcb + hoff[p]; span = the extent
+// of the count arrays to clear.  Asynchronous; the small host arrays go through pageable
+// copies (staged by the driver on the call), so nothing host-side needs to outlive it.
+int vote_lists(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
+               const std::vector<int64_t>& koff, double eps, int32_t mode, int32_t B,
+               const uint32_t* dlins, const std::vector<int64_t>& hoff,
+               const std::vector<int32_t>& hcnt, int64_t span, uint32_t* dca, uint32_t* dcb) {
+  const int32_t PL = (int32_t)hcnt.size();
+  const bool use_tc = ctx->tc_on && mode != RV_MODE_EXACT;
+  const bool tc_final = use_tc && mode == RV_MODE_FINAL;
+  std::vector<int64_t> ncell, ncorr;
+  std::vector<rv::VoteSeg> segs;
+  for (int32_t p = 0; p < PL; ++p) {
+    if (hcnt[p] == 0) continue;
+    rv::VoteSeg sg{};
+    sg.lins = dlins + hoff[p];
+    sg.cnt_a = dca + hoff[p];
+    sg.cnt_b = dcb + hoff[p];
+    sg.koff = use_tc ? ctx->tc_toff[p] : koff[p];
+    sg.row = rows[p];
+    sg.n = (int32_t)(rows[p + 1] - rows[p]);
+    sg.B = B;
+    sg.eps = eps;
+    segs.push_back(sg);
+    ncell.push_back(hcnt[p]);
+    ncorr.push_back(sg.n);
+  }
+  if (segs.empty()) return RV_OK;
+  std::vector<rv::VoteItem> items;
+  int groups = 1;
+  if (use_tc)
+    build_tc_items(ncell, ncorr, ctx->num_sms, items, tc_final ? rv::kTcM / 2 : rv::kTcM);
+  else if (mode == RV_MODE_EXACT)
+    build_exact_items(ncell, ncorr, items);
+  else
+    groups = build_vote_items(ncell, ncorr, ctx->num_sms * ctx->vote_blocks_per_sm, items,
+                              ctx->force_groups);
+  if (items.empty()) return RV_OK;
+  RV_CUDA(ctx->vsegs.ensure(segs.size()), "allocating segments");
+  RV_CUDA(ctx->vitems.ensure(items.size()), "allocating items");
+  cudaStream_t s = ctx->stream;
+  RV_CUDA(cudaMemcpyAsync(ctx->vsegs.p, segs.data(), segs.size() * sizeof(rv::VoteSeg),
+                          cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemcpyAsync(ctx->vitems.p, items.data(), items.size() * sizeof(rv::VoteItem),
+                          cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemsetAsync(dca, 0, span * 4, s), "memset");
+  if (mode == RV_MODE_FINAL) RV_CUDA(cudaMemsetAsync(dcb, 0, span * 4, s), "memset");
+  if (mode == RV_MODE_EXACT) {
+    rv::launch_exact(ctx->k9.p, ctx->stride, x, y, ctx->vsegs.p, ctx->vitems.p,
+                     (int32_t)items.size(), ctx->cfg.guard, s);
+  } else {
+    ctx->collect_vote_ms();
+    RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
+    if (use_tc)
+      rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
+                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, tc_final);
+    else
+      rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
+                      (int32_t)items.size(), ctx->cfg.guard, s);
+    RV_CUDA(cudaEventRecord(ctx->evv1, s), "event");
+    ctx->vote_pending = true;
+    for (size_t q = 0; q < ncell.size(); ++q) ctx->vote_pairs += (uint64_t)ncell[q] * ncorr[q];
+    ctx->vote_launches += 1;
+  }
+  ctx->launches += 1;
+  RV_CUDA(cudaGetLastError(), "launching the vote kernel");
+  return RV_OK;
+}
+
+// D2H of PL per-problem counts through the pinned staging, then a stream sync.
+int read_counts(rv_ctx* ctx, const int32_t* dcnt, int32_t PL, std::vector<int32_t>& h) {
+  RV_CUDA(ctx->down.ensure((size_t)PL * 4 + 256), "allocating staging");
+  ctx->down.reset();
+  int32_t* hc = ctx->down.take<int32_t>(PL);
+  RV_CUDA(cudaMemcpyAsync(hc, dcnt, (size_t)PL * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  RV_CUDA(cudaStreamSynchronize(ctx->stream), "batched level");
+  ctx->collect_vote_ms();
+  h.assign(hc, hc + PL);
+  return RV_OK;
+}
+
+// true when the device level loop applies: >= 2 levels and a cached level-0 background
+bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps) {
+  if (levels_eff < 2) return false;
+  if (const char* e = getenv("RV_HOST_PLAN"))
+    if (atoi(e) != 0) return false;
+  int64_t mbg = 0;
+  return rv_plan_l0_background(B0, eps, &mbg) != nullptr && mbg > 0;
+}
+
+// The certified search of rv_plan.cpp for PL problems at once, every decision on the device
+// (rv_dplan.cu); the host reads back one count array per level to size the next launch.
+// ch = the `levels` resolutions searched (ch.size() >= 2).  Fills res[p].
+int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
+                        const std::vector<int64_t>& rows, const std::vector<int64_t>& koff,
+                        int32_t PL, double eps, const std::vector<int32_t>& ch,
+                        std::vector<rv_plan_result>& res, Trace& tr) {
+  const int L = (int)ch.size();
+  cudaStream_t s = ctx->stream;
+  std::vector<std::vector<int32_t>> phases;  // per phase: blocks per problem
+  // ---- level 0: every problem votes the full candidate grid; counts stay on the device
+  const int32_t B0 = ch[0];
+  const int64_t m0 = rv_grid_candidates(B0, nullptr, 0);
+  if (ctx->grid_host_B != B0) {
+    ctx->grid_host.resize(m0);
+    rv_grid_candidates(B0, ctx->grid_host.data(), m0);
+    ctx->grid_host_B = B0;
+  }
+  int64_t mbg = 0;
+  const double* bgh = rv_plan_l0_background(B0, eps, &mbg);
+  if (!bgh || mbg != m0) return ctx->fail(RV_ECUDA, "internal: level-0 background unavailable");
+  RV_CUDA(ctx->l0cnt.ensure((size_t)PL * m0), "allocating level-0 counts");
+  if (ctx->l0bg_B != B0 || ctx->l0bg_eps != eps || ctx->l0bg.cap < (size_t)m0) {
+    RV_CUDA(ctx->l0bg.ensure(m0), "allocating");
+    RV_CUDA(cudaMemcpy(ctx->l0bg.p, bgh, m0 * sizeof(double), cudaMemcpyHostToDevice),
+            "H2D background");
+    ctx->l0bg_B = B0;
+    ctx->l0bg_eps = eps;
+  }
+  {
+    std::vector<BatchReq> g0(PL);
+    for (int32_t p = 0; p < PL; ++p) g0[p] = {p, B0, RV_MODE_BOUND, m0, ctx->grid_host.data(), true};
+    std::vector<std::vector<uint32_t>> unused;
+    if (int rc = eval_batch(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, g0, unused, unused,
+                            ctx->l0cnt.p))
+      return rc;
+  }
+  phases.emplace_back(PL, (int32_t)m0);
+  RV_CUDA(ctx->l0idx.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_pick.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_lb.ensure(PL), "allocating");
+  rv::launch_l0_argmax(ctx->l0cnt.p, m0, ctx->grid_list.p, B0, ctx->l0bg.p, ctx->rows.p, PL,
+                       ctx->l0idx.p, s);
+  ctx->launches += 1;
+  tr.mark("  level 0");
+  std::vector<int32_t> hcnt;
+  std::vector<int64_t> hoff(PL + 1);
+  // ---- dive: the 27-neighbourhood of the pick, level by level; lb* at the finest level
+  for (int l = 1; l < L; ++l) {
+    const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1], cap = 27 * f * f * f;
+    const size_t span = (size_t)PL * cap;
+    RV_CUDA(ctx->dp_lins[0].ensure(span), "allocating");
+    RV_CUDA(ctx->dp_ca[0].ensure(span), "allocating");
+    RV_CUDA(ctx->dp_cb[0].ensure(span), "allocating");
+    RV_CUDA(ctx->dp_cnt[0].ensure(PL), "allocating");
+    RV_CUDA(ctx->dp_off[0].ensure(PL + 1), "allocating");
+    rv::dp_launch_dive_children(ctx->dp_pick.p, ctx->l0idx.p, l == 1 ? ctx->grid_list.p : nullptr,
+                                Bp, f, ctx->dp_lins[0].p, cap, ctx->dp_cnt[0].p, PL, s);
+    ctx->launches += 1;
+    if (int rc = read_counts(ctx, ctx->dp_cnt[0].p, PL, hcnt)) return rc;
+    for (int32_t p = 0; p <= PL; ++p) hoff[p] = (int64_t)p * cap;
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_off[0].p, hoff.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+            "H2D");
+    const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
+    if (int rc = vote_lists(ctx, x, y, rows, koff, eps, mode, ch[l], ctx->dp_lins[0].p, hoff, hcnt,
+                            (int64_t)span, ctx->dp_ca[0].p, ctx->dp_cb[0].p))
+      return rc;
+    if (mode == RV_MODE_BOUND)
+      rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, ctx->dp_off[0].p,
+                              ctx->dp_cnt[0].p, ch[l], eps, ctx->rows.p, ctx->dp_pick.p, PL, s);
+    else
+      rv::dp_launch_max_lo(ctx->dp_cb[0].p, ctx->dp_off[0].p, ctx->dp_cnt[0].p, ctx->dp_lb.p, PL, s);
+    ctx->launches += 1;
+    phases.push_back(hcnt);
+    tr.mark("  dive level");
+  }
+  // ---- branch and bound from the level-0 survivors (UB >= lb*)
+  int cur = -1;  // -1: parents = the shared level-0 grid
+  for (int l = 1; l < L; ++l) {
+    const int nb = cur == 0 ? 1 : 0;
+    const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1];
+    const uint32_t* plins = cur < 0 ? ctx->grid_list.p : ctx->dp_lins[cur].p;
+    const int64_t* poff = cur < 0 ? nullptr : ctx->dp_off[cur].p;
+    const uint32_t* pub = cur < 0 ? ctx->l0cnt.p : ctx->dp_ca[cur].p;
+    const int32_t* pcnt = cur < 0 ? nullptr : ctx->dp_cnt[cur].p;
+    const int64_t shared_m = cur < 0 ? m0 : 0;
+    RV_CUDA(ctx->dp_cnt[nb].ensure(PL), "allocating");
+    RV_CUDA(ctx->dp_off[nb].ensure(PL + 1), "allocating");
+    rv::dp_launch_bnb_children(plins, poff, pub, poff, pcnt, shared_m, ctx->dp_lb.p, Bp, f, nullptr,
+                               nullptr, ctx->dp_cnt[nb].p, PL, s);
+    ctx->launches += 1;
+    if (int rc = read_counts(ctx, ctx->dp_cnt[nb].p, PL, hcnt)) return rc;
+    hoff[0] = 0;
+    for (int32_t p = 0; p < PL; ++p) hoff[p + 1] = hoff[p] + hcnt[p];
+    const int64_t total = hoff[PL];
+    RV_CUDA(ctx->dp_lins[nb].ensure(std::max<int64_t>(1, total)), "allocating");
+    RV_CUDA(ctx->dp_ca[nb].ensure(std::max<int64_t>(1, total)), "allocating");
+    RV_CUDA(ctx->dp_cb[nb].ensure(std::max<int64_t>(1, total)), "allocating");
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_off[nb].p, hoff.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+            "H2D");
+    rv::dp_launch_bnb_children(plins, poff, pub, poff, pcnt, shared_m, ctx->dp_lb.p, Bp, f,
+                               ctx->dp_lins[nb].p, ctx->dp_off[nb].p, nullptr, PL, s);
+    ctx->launches += 1;
+    const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
+    if (int rc = vote_lists(ctx, x, y, rows, koff, eps, mode, ch[l], ctx->dp_lins[nb].p, hoff, hcnt,
+                            total, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p))
+      return rc;
+    phases.push_back(hcnt);
+    cur = nb;
+    tr.mark("  bnb level");
+  }
+  // ---- finest level: recheck hi >= max lo, hi != lo exactly; winner per problem
+  const uint32_t* flins = ctx->dp_lins[cur].p;
+  const uint32_t* fhi = ctx->dp_ca[cur].p;
+  const uint32_t* flo = ctx->dp_cb[cur].p;
+  const int64_t* foff = ctx->dp_off[cur].p;
+  const int32_t* fcnt = ctx->dp_cnt[cur].p;
+  RV_CUDA(ctx->dp_rcnt.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_roff.ensure(PL + 1), "allocating");
+  rv::dp_launch_recheck_set(fhi, flo, foff, fcnt, ctx->dp_rcnt.p, nullptr, nullptr, PL, s);
+  ctx->launches += 1;
+  std::vector<int32_t> rcnt;
+  if (int rc = read_counts(ctx, ctx->dp_rcnt.p, PL, rcnt)) return rc;
+  std::vector<int64_t> roff(PL + 1, 0);
+  for (int32_t p = 0; p < PL; ++p) roff[p + 1] = roff[p] + rcnt[p];
+  const int64_t rtotal = roff[PL];
+  RV_CUDA(ctx->dp_rlist.ensure(std::max<int64_t>(1, rtotal)), "allocating");
+  RV_CUDA(ctx->dp_rlins.ensure(std::max<int64_t>(1, rtotal)), "allocating");
+  RV_CUDA(ctx->dp_ex.ensure(std::max<int64_t>(1, rtotal)), "allocating");
+  RV_CUDA(ctx->dp_res.ensure(3 * (size_t)PL), "allocating");
+  RV_CUDA(cudaMemcpyAsync(ctx->dp_roff.p, roff.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+          "H2D");
+  if (rtotal > 0) {
+    rv::dp_launch_recheck_set(fhi, flo, foff, fcnt, nullptr, ctx->dp_roff.p, ctx->dp_rlist.p, PL, s);
+    rv::dp_launch_gather(flins, foff, ctx->dp_roff.p, ctx->dp_rcnt.p, ctx->dp_rlist.p,
+                         ctx->dp_rlins.p, PL, s);
+    ctx->launches += 2;
+    if (int rc = vote_lists(ctx, x, y, rows, koff, eps, RV_MODE_EXACT, ch[L - 1], ctx->dp_rlins.p,
+                            roff, rcnt, rtotal, ctx->dp_ex.p, ctx->dp_ex.p))
+      return rc;
+    phases.push_back(rcnt);
+  }
+  rv::dp_launch_finalize(flins, fhi, flo, foff, fcnt, ctx->dp_ex.p, ctx->dp_roff.p, ctx->dp_rcnt.p,
+                         ctx->dp_rlist.p, ctx->dp_res.p, PL, s);
+  ctx->launches += 1;
+  RV_CUDA(cudaGetLastError(), "launching the level loop");
+  RV_CUDA(ctx->down.ensure((size_t)PL * 20 + 512), "allocating staging");
+  ctx->down.reset();
+  int32_t* hres = ctx->down.take<int32_t>(3 * (size_t)PL);
+  int64_t* hlb = ctx->down.take<int64_t>(PL);
+  RV_CUDA(cudaMemcpyAsync(hres, ctx->dp_res.p, 12 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hlb, ctx->dp_lb.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "batched finalize");
+  ctx->collect_vote_ms();
+  tr.mark("  finalize");
+  res.assign(PL, rv_plan_result{});
+  for (int32_t p = 0; p < PL; ++p) {
+    rv_plan_result& r = res[p];
+    const uint64_t n = (uint64_t)(rows[p + 1] - rows[p]);
+    r.lin = (uint32_t)hres[3 * p];
+    r.B = ch[L - 1];
+    r.votes = (uint32_t)hres[3 * p + 1];
+    r.n_tied = hres[3 * p + 2];
+    r.lb_star = (uint32_t)hlb[p];
+    r.n_rechecked = rcnt[p];
+    for (size_t ph = 0; ph < phases.size(); ++ph) {
+      const int64_t c = phases[ph][p];
+      if (ph + 1 == phases.size() && rtotal > 0 && rcnt[p] == 0) break;  // no recheck phase
+      r.pair_votes += (uint64_t)c * n;
+      r.cells_evaluated += (uint64_t)c;
+      if (r.n_phases < 16) r.cells_per_phase[r.n_phases++] = c;
+    }
+  }
+  return RV_OK;
+}
+
 int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets,
                        int32_t P, double eps, int32_t levels, rv_result* out, uint32_t* masks) {
   if (int rc = validate_common(ctx, x, y, eps, levels)) return rc;
@@ -873,149 +1160,156 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
     if (int rc = run_setup(ctx, x, y, rows.data(), PL, koff)) return rc;
     if (int rc = check_bad(ctx)) return rc;
     tr.mark("setup");
-    std::vector<rv_plan*> plans(PL, nullptr);
     int rc = RV_OK;
-    parallel_for(PL, [&](int64_t p) {
-      rv_plan_create(ctx->chain.data(), (int32_t)ctx->chain.size(), levels,
-                     rows[p + 1] - rows[p], eps, (double)ctx->cfg.guard, &plans[p]);
-    });
-    for (int32_t p = 0; p < PL && !rc; ++p)
-      if (!plans[p]) rc = ctx->fail(RV_EINVAL, "invalid search plan");
-    tr.mark("plans created");
-    std::vector<std::vector<uint32_t>> ca(PL), cb(PL);
-    bool l0_on_device = false;
-    int64_t m0 = 0;
-    while (!rc) {
-      std::vector<BatchReq> by_mode[3];
-      bool any = false;
-      for (int32_t p = 0; p < PL; ++p) {
-        BatchReq r;
-        r.prob = p;
-        if (rv_plan_request(plans[p], &r.B, &r.mode, &r.m, &r.lins)) {
-          r.full_grid = rv_plan_request_is_full_grid(plans[p]) != 0;
-          by_mode[r.mode].push_back(r);
-          any = true;
-        }
-      }
-      if (!any) break;
-      tr.mark("requests gathered");
-      // level 0 of a batch (every problem, same full grid, bound mode): reduce on the device
-      const std::vector<BatchReq>& g0 = by_mode[RV_MODE_BOUND];
-      bool l0_reduce = PL >= 2 && (int64_t)g0.size() == PL && !by_mode[1].size() &&
-                       !by_mode[2].size();
-      for (const BatchReq& r : g0) l0_reduce = l0_reduce && r.full_grid && r.m == g0[0].m;
-      if (l0_reduce) {
-        int64_t mbg = 0;
-        const double* bgh = rv_plan_l0_background(g0[0].B, eps, &mbg);
-        l0_reduce = bgh && mbg == g0[0].m;
-        if (l0_reduce) {
-          m0 = g0[0].m;
-          RV_CUDA(ctx->l0cnt.ensure((size_t)PL * m0), "allocating level-0 counts");
-          if (ctx->l0bg_B != g0[0].B || ctx->l0bg_eps != eps || ctx->l0bg.cap < (size_t)m0) {
-            RV_CUDA(ctx->l0bg.ensure(m0), "allocating");
-            RV_CUDA(cudaMemcpy(ctx->l0bg.p, bgh, m0 * sizeof(double), cudaMemcpyHostToDevice),
-                    "H2D background");
-            ctx->l0bg_B = g0[0].B;
-            ctx->l0bg_eps = eps;
+    const int32_t lev = levels == 0 ? std::min<int32_t>(5, (int32_t)ctx->chain.size()) : levels;
+    const std::vector<int32_t> ch(ctx->chain.end() - lev, ctx->chain.end());
+    std::vector<rv_plan_result> pres(PL);
+    if (dplan_applies(ctx, lev, ch[0], eps)) {
+      rc = solve_batched_dplan(ctx, x, y, rows, koff, PL, eps, ch, pres, tr);
+      if (rc) return rc;
+    } else {
+      std::vector<rv_plan*> plans(PL, nullptr);
+      parallel_for(PL, [&](int64_t p) {
+        rv_plan_create(ctx->chain.data(), (int32_t)ctx->chain.size(), levels,
+                       rows[p + 1] - rows[p], eps, (double)ctx->cfg.guard, &plans[p]);
+      });
+      for (int32_t p = 0; p < PL && !rc; ++p)
+        if (!plans[p]) rc = ctx->fail(RV_EINVAL, "invalid search plan");
+      tr.mark("plans created");
+      std::vector<std::vector<uint32_t>> ca(PL), cb(PL);
+      bool l0_on_device = false;
+      int64_t m0 = 0;
+      while (!rc) {
+        std::vector<BatchReq> by_mode[3];
+        bool any = false;
+        for (int32_t p = 0; p < PL; ++p) {
+          BatchReq r;
+          r.prob = p;
+          if (rv_plan_request(plans[p], &r.B, &r.mode, &r.m, &r.lins)) {
+            r.full_grid = rv_plan_request_is_full_grid(plans[p]) != 0;
+            by_mode[r.mode].push_back(r);
+            any = true;
           }
-          rc = eval_batch(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, g0, ca, cb, ctx->l0cnt.p);
-          if (rc) break;
-          RV_CUDA(ctx->l0idx.ensure(PL), "allocating");
-          rv::launch_l0_argmax(ctx->l0cnt.p, m0, ctx->grid_list.p, g0[0].B, ctx->l0bg.p,
-                               ctx->rows.p, PL, ctx->l0idx.p, ctx->stream);
-          ctx->launches += 1;
-          std::vector<int32_t> start(PL);
-          RV_CUDA(cudaMemcpyAsync(start.data(), ctx->l0idx.p, PL * 4, cudaMemcpyDeviceToHost,
-                                  ctx->stream), "D2H");
-          RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 argmax");
-          std::vector<int> bad(PL, 0);
-          parallel_for(PL, [&](int64_t p) { bad[p] = rv_plan_feed_l0_start(plans[p], start[p]); });
-          for (int b : bad)
-            if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected the level-0 start");
-          l0_on_device = true;
-          tr.mark("  level 0 on device");
-          continue;
         }
-      }
-      for (int md = 0; md < 3 && !rc; ++md) {
-        if (by_mode[md].empty()) continue;
-        rc = eval_batch(ctx, x, y, rows, koff, eps, md, by_mode[md], ca, cb);
-        if (rc) break;
-        tr.mark(md == 0 ? "  eval bound" : md == 1 ? "  eval final" : "  eval exact");
-        const std::vector<BatchReq>& grp = by_mode[md];
-        std::vector<int> bad(grp.size(), 0);
-        parallel_for((int64_t)grp.size(), [&](int64_t q) {
-          const BatchReq& r = grp[q];
-          bad[q] = rv_plan_feed(plans[r.prob], ca[r.prob].data(), cb[r.prob].data()) != 0;
+        if (!any) break;
+        tr.mark("requests gathered");
+        // level 0 of a batch (every problem, same full grid, bound mode): reduce on the device
+        const std::vector<BatchReq>& g0 = by_mode[RV_MODE_BOUND];
+        bool l0_reduce = PL >= 2 && (int64_t)g0.size() == PL && !by_mode[1].size() &&
+                         !by_mode[2].size();
+        for (const BatchReq& r : g0) l0_reduce = l0_reduce && r.full_grid && r.m == g0[0].m;
+        if (l0_reduce) {
+          int64_t mbg = 0;
+          const double* bgh = rv_plan_l0_background(g0[0].B, eps, &mbg);
+          l0_reduce = bgh && mbg == g0[0].m;
+          if (l0_reduce) {
+            m0 = g0[0].m;
+            RV_CUDA(ctx->l0cnt.ensure((size_t)PL * m0), "allocating level-0 counts");
+            if (ctx->l0bg_B != g0[0].B || ctx->l0bg_eps != eps || ctx->l0bg.cap < (size_t)m0) {
+              RV_CUDA(ctx->l0bg.ensure(m0), "allocating");
+              RV_CUDA(cudaMemcpy(ctx->l0bg.p, bgh, m0 * sizeof(double), cudaMemcpyHostToDevice),
+                      "H2D background");
+              ctx->l0bg_B = g0[0].B;
+              ctx->l0bg_eps = eps;
+            }
+            rc = eval_batch(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, g0, ca, cb, ctx->l0cnt.p);
+            if (rc) break;
+            RV_CUDA(ctx->l0idx.ensure(PL), "allocating");
+            rv::launch_l0_argmax(ctx->l0cnt.p, m0, ctx->grid_list.p, g0[0].B, ctx->l0bg.p,
+                                 ctx->rows.p, PL, ctx->l0idx.p, ctx->stream);
+            ctx->launches += 1;
+            std::vector<int32_t> start(PL);
+            RV_CUDA(cudaMemcpyAsync(start.data(), ctx->l0idx.p, PL * 4, cudaMemcpyDeviceToHost,
+                                    ctx->stream), "D2H");
+            RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 argmax");
+            std::vector<int> bad(PL, 0);
+            parallel_for(PL, [&](int64_t p) { bad[p] = rv_plan_feed_l0_start(plans[p], start[p]); });
+            for (int b : bad)
+              if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected the level-0 start");
+            l0_on_device = true;
+            tr.mark("  level 0 on device");
+            continue;
+          }
+        }
+        for (int md = 0; md < 3 && !rc; ++md) {
+          if (by_mode[md].empty()) continue;
+          rc = eval_batch(ctx, x, y, rows, koff, eps, md, by_mode[md], ca, cb);
+          if (rc) break;
+          tr.mark(md == 0 ? "  eval bound" : md == 1 ? "  eval final" : "  eval exact");
+          const std::vector<BatchReq>& grp = by_mode[md];
+          std::vector<int> bad(grp.size(), 0);
+          parallel_for((int64_t)grp.size(), [&](int64_t q) {
+            const BatchReq& r = grp[q];
+            bad[q] = rv_plan_feed(plans[r.prob], ca[r.prob].data(), cb[r.prob].data()) != 0;
+          });
+          for (int b : bad)
+            if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
+          tr.mark("  feed");
+        }
+        if (rc || !l0_on_device) continue;
+        // plans whose dive ended: compact their level-0 survivors (UB >= lb*) on the device
+        std::vector<int32_t> need;
+        std::vector<int64_t> lbs;
+        for (int32_t p = 0; p < PL; ++p) {
+          int64_t lb = 0;
+          if (rv_plan_needs_l0_survivors(plans[p], &lb)) {
+            need.push_back(p);
+            lbs.push_back(lb);
+          }
+        }
+        if (need.empty()) continue;
+        const int32_t J = (int32_t)need.size();
+        RV_CUDA(ctx->l0idx.ensure(2 * (size_t)J + 1), "allocating");
+        RV_CUDA(ctx->l0aux.ensure(2 * (size_t)J + 1), "allocating");
+        int32_t* dprob = ctx->l0idx.p;
+        int32_t* dcnt = ctx->l0idx.p + J;
+        int64_t* dlb = ctx->l0aux.p;
+        int64_t* doff = ctx->l0aux.p + J;
+        RV_CUDA(cudaMemcpyAsync(dprob, need.data(), J * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        RV_CUDA(cudaMemcpyAsync(dlb, lbs.data(), J * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        rv::launch_l0_survivors(ctx->l0cnt.p, m0, dprob, dlb, nullptr, J, dcnt, nullptr, ctx->stream);
+        std::vector<int32_t> k(J);
+        RV_CUDA(cudaMemcpyAsync(k.data(), dcnt, J * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
+        std::vector<int64_t> offv(J + 1, 0);
+        for (int32_t j = 0; j < J; ++j) offv[j + 1] = offv[j] + k[j];
+        DevBuf<int32_t>& surv = ctx->l0surv;
+        RV_CUDA(surv.ensure(std::max<int64_t>(1, offv[J])), "allocating");
+        RV_CUDA(cudaMemcpyAsync(doff, offv.data(), J * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        rv::launch_l0_survivors(ctx->l0cnt.p, m0, dprob, dlb, doff, J, nullptr, surv.p, ctx->stream);
+        ctx->launches += 2;
+        std::vector<int32_t> idx(std::max<int64_t>(1, offv[J]));
+        RV_CUDA(cudaMemcpyAsync(idx.data(), surv.p, offv[J] * 4, cudaMemcpyDeviceToHost, ctx->stream),
+                "D2H");
+        RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
+        std::vector<int> bad(J, 0);
+        parallel_for(J, [&](int64_t j) {
+          bad[j] = rv_plan_feed_l0_survivors(plans[need[j]], idx.data() + offv[j], k[j]);
         });
         for (int b : bad)
-          if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
-        tr.mark("  feed");
+          if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected the level-0 survivors");
+        tr.mark("  level-0 survivors");
       }
-      if (rc || !l0_on_device) continue;
-      // plans whose dive ended: compact their level-0 survivors (UB >= lb*) on the device
-      std::vector<int32_t> need;
-      std::vector<int64_t> lbs;
-      for (int32_t p = 0; p < PL; ++p) {
-        int64_t lb = 0;
-        if (rv_plan_needs_l0_survivors(plans[p], &lb)) {
-          need.push_back(p);
-          lbs.push_back(lb);
-        }
-      }
-      if (need.empty()) continue;
-      const int32_t J = (int32_t)need.size();
-      RV_CUDA(ctx->l0idx.ensure(2 * (size_t)J + 1), "allocating");
-      RV_CUDA(ctx->l0aux.ensure(2 * (size_t)J + 1), "allocating");
-      int32_t* dprob = ctx->l0idx.p;
-      int32_t* dcnt = ctx->l0idx.p + J;
-      int64_t* dlb = ctx->l0aux.p;
-      int64_t* doff = ctx->l0aux.p + J;
-      RV_CUDA(cudaMemcpyAsync(dprob, need.data(), J * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-      RV_CUDA(cudaMemcpyAsync(dlb, lbs.data(), J * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-      rv::launch_l0_survivors(ctx->l0cnt.p, m0, dprob, dlb, nullptr, J, dcnt, nullptr, ctx->stream);
-      std::vector<int32_t> k(J);
-      RV_CUDA(cudaMemcpyAsync(k.data(), dcnt, J * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-      RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
-      std::vector<int64_t> offv(J + 1, 0);
-      for (int32_t j = 0; j < J; ++j) offv[j + 1] = offv[j] + k[j];
-      DevBuf<int32_t> surv;
-      RV_CUDA(surv.ensure(std::max<int64_t>(1, offv[J])), "allocating");
-      RV_CUDA(cudaMemcpyAsync(doff, offv.data(), J * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-      rv::launch_l0_survivors(ctx->l0cnt.p, m0, dprob, dlb, doff, J, nullptr, surv.p, ctx->stream);
-      ctx->launches += 2;
-      std::vector<int32_t> idx(std::max<int64_t>(1, offv[J]));
-      RV_CUDA(cudaMemcpyAsync(idx.data(), surv.p, offv[J] * 4, cudaMemcpyDeviceToHost, ctx->stream),
-              "D2H");
-      RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
-      surv.release();
-      std::vector<int> bad(J, 0);
-      parallel_for(J, [&](int64_t j) {
-        bad[j] = rv_plan_feed_l0_survivors(plans[need[j]], idx.data() + offv[j], k[j]);
-      });
-      for (int b : bad)
-        if (b) rc = ctx->fail(RV_ECUDA, "internal: planner rejected the level-0 survivors");
-      tr.mark("  level-0 survivors");
+      if (!rc)
+        for (int32_t p = 0; p < PL; ++p) rv_plan_get_result(plans[p], &pres[p]);
+      for (rv_plan* pl : plans) rv_plan_destroy(pl);
+      if (rc) return rc;
     }
     std::vector<double> q0((size_t)PL * 4), qf((size_t)PL * 4);
     std::vector<int32_t> fl(PL), ids(PL);
     std::vector<uint32_t> ni(PL);
     std::vector<int64_t> mw(PL);
-    if (!rc) {
+    {
       int64_t w = 0;
       for (int64_t p = 0; p < pb; ++p) w += (offsets[p + 1] - offsets[p] + 31) / 32;
       for (int32_t p = 0; p < PL; ++p) {
-        rv_plan_result pr{};
-        rv_plan_get_result(plans[p], &pr);
-        fill_result(pr, &local[p]);
+        fill_result(pres[p], &local[p]);
         std::memcpy(&q0[4 * p], local[p].q_cell, 32);
         ids[p] = p;
         mw[p] = w;
         w += (rows[p + 1] - rows[p] + 31) / 32;
       }
     }
-    for (rv_plan* pl : plans) rv_plan_destroy(pl);
-    if (rc) return rc;
     tr.mark("results");
     // rows are absolute: refine over the local offsets table
     rc = run_refine(ctx, x, y, rows.data(), PL, ids.data(), eps, q0.data(), ctx->cfg.refine_rounds,
@@ -1171,6 +1465,13 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->koffs.release(); ctx->bad.release(); ctx->hx.release(); ctx->hy.release();
   ctx->hmask.release(); ctx->gather.release(); ctx->grid_list.release();
   ctx->l0cnt.release(); ctx->l0bg.release(); ctx->l0idx.release(); ctx->l0aux.release();
+  ctx->l0surv.release();
+  for (int b = 0; b < 2; ++b) {
+    ctx->dp_lins[b].release(); ctx->dp_ca[b].release(); ctx->dp_cb[b].release();
+    ctx->dp_off[b].release(); ctx->dp_cnt[b].release();
+  }
+  ctx->dp_lb.release(); ctx->dp_roff.release(); ctx->dp_rcnt.release(); ctx->dp_rlist.release();
+  ctx->dp_res.release(); ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release();
   ctx->up.release(); ctx->down.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);

@@ -1,0 +1,136 @@
+"""The device-resident level loop of batched solves (csrc/rv_dplan.cu) against the host
+planner (rv_plan.cpp, forced with RV_HOST_PLAN=1) and the oracle.
+
+The device loop takes the planner's decisions on the GPU; it must return the same winner,
+votes, ties, lb* and recheck sets as the host planner on every problem, for several chains
+and `levels`, ragged sizes (n = 2 ... 3000), both vote paths (FP32 and tensor core), and its
+per-phase block counts must be the host planner's (dive picks compare excess values computed
+with the device's cos(); a last-ulp difference could only reorder an exact tie, so a tiny
+fraction of mismatching phase lists is tolerated and reported)."""
+import os
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+
+
+def host_plan(fn):
+    os.environ["RV_HOST_PLAN"] = "1"
+    try:
+        return fn()
+    finally:
+        del os.environ["RV_HOST_PLAN"]
+
+
+def compare(res_d, res_h, strict_phases=False):
+    mism = 0
+    for p, (a, b) in enumerate(zip(res_d, res_h)):
+        assert (a.cell, a.votes, a.n_tied) == (b.cell, b.votes, b.n_tied), p
+        assert np.array_equal(a.q, b.q), p
+        assert (a.n_inliers, a.flags) == (b.n_inliers, b.flags), p
+        if a.cells_per_phase != b.cells_per_phase:
+            mism += 1
+        else:
+            assert (a.lb_star, a.n_rechecked, a.cells_evaluated, a.pair_votes) == \
+                   (b.lb_star, b.n_rechecked, b.cells_evaluated, b.pair_votes), p
+    if strict_phases:
+        assert mism == 0
+    assert mism <= max(1, len(res_d) // 500), mism
+    return mism
+
+
+def ragged_batch(seed, P, nmax, eps):
+    rng = np.random.default_rng(seed)
+    probs = []
+    for p in range(P):
+        n = int(rng.integers(2, nmax))
+        probs.append(datagen.make_problem(n, int(rng.integers(0, n + 1)),
+                                          float(rng.uniform(0.0, 0.03)), eps, seed=[seed, p]))
+    return datagen.batch_of(probs, eps)
+
+
+@pytest.mark.parametrize("tensor_vote", [False, True])
+@pytest.mark.parametrize("chain,levels", [(None, 0), ((5, 15, 45), 2), ((15, 45, 90, 180), 3), ((4, 8, 16, 32), 4),
+                                          ((3, 9, 27, 81), 3), ((6, 18, 90), 3)])
+def test_device_loop_equals_host_planner(torch_cuda, tensor_vote, chain, levels):
+    from paper_2506_11547_b200 import RotVote
+    torch = torch_cuda
+    bt = ragged_batch(5 + levels, 96, 3000, 0.1)
+    ctx = RotVote(max_n=int(bt.offsets[-1]) + 16, max_problems=96, chain=chain,
+                  tensor_vote=tensor_vote)
+    try:
+        x, y = dev(torch, bt.x), dev(torch, bt.y)
+        rd = ctx.solve_batched(x, y, bt.offsets, bt.eps, levels=levels)
+        rh = host_plan(lambda: ctx.solve_batched(x, y, bt.offsets, bt.eps, levels=levels))
+        compare(rd, rh)
+        # and the oracle (certified == exhaustive) on a sample
+        for p in range(0, 96, 17):
+            pr = bt.problems[p]
+            ref = oracle.solve(pr.x, pr.y, bt.eps, chain=ctx.chain,
+                               levels=levels if levels else min(5, len(ctx.chain)))
+            assert (rd[p].votes, rd[p].n_tied) == (ref.votes, ref.n_tied), p
+    finally:
+        ctx.close()
+
+
+def test_device_loop_cfg5_equals_host_planner(torch_cuda):
+    from paper_2506_11547_b200 import RotVote
+    torch = torch_cuda
+    bt = datagen.cfg5()
+    ctx = RotVote(max_n=int(bt.offsets[-1]) + 16, max_problems=4096, tensor_vote=True)
+    try:
+        x, y = dev(torch, bt.x), dev(torch, bt.y)
+        rd = ctx.solve_batched(x, y, bt.offsets, bt.eps)
+        rh = host_plan(lambda: ctx.solve_batched(x, y, bt.offsets, bt.eps))
+        mism = compare(rd, rh)
+        print("cfg5 phase-list mismatches:", mism)
+        # repeated calls reuse the context's buffers and give identical answers
+        rd2 = ctx.solve_batched(x, y, bt.offsets, bt.eps)
+        for a, b in zip(rd, rd2):
+            assert (a.cell, a.votes, a.cells_per_phase) == (b.cell, b.votes, b.cells_per_phase)
+    finally:
+        ctx.close()
+
+
+def test_device_loop_degenerate_batches(torch_cuda):
+    """n = 2 problems, all-outlier problems, exact antipodal pairs (y = -x), one problem."""
+    from paper_2506_11547_b200 import RotVote
+    torch = torch_cuda
+    probs = [datagen.make_problem(2, 2, 0.0, 0.2, seed=1),
+             datagen.make_problem(2, 0, 0.0, 0.2, seed=2),
+             datagen.make_problem(50, 0, 0.0, 0.2, seed=3),
+             datagen.make_problem(300, 300, 0.0, 0.2, seed=4)]
+    anti = datagen.make_problem(40, 0, 0.0, 0.2, seed=5)
+    anti.y[:] = -anti.x
+    probs.append(anti)
+    bt = datagen.batch_of(probs, 0.2)
+    ctx = RotVote(max_n=4096, max_problems=8)
+    try:
+        x, y = dev(torch, bt.x), dev(torch, bt.y)
+        rd = ctx.solve_batched(x, y, bt.offsets, bt.eps)
+        rh = host_plan(lambda: ctx.solve_batched(x, y, bt.offsets, bt.eps))
+        compare(rd, rh, strict_phases=True)
+        for pr, r in zip(probs, rd):
+            ref = oracle.solve(pr.x, pr.y, bt.eps)
+            assert (r.votes, r.n_tied) == (ref.votes, ref.n_tied)
+        one = datagen.batch_of(probs[3:4], 0.2)
+        r1 = ctx.solve_batched(dev(torch, one.x), dev(torch, one.y), one.offsets, one.eps)
+        assert (r1[0].cell, r1[0].votes) == (rd[3].cell, rd[3].votes)
+    finally:
+        ctx.close()
