@@ -1,3 +1,4 @@
+
 #!/usr/bin/env python
 """Benchmark of the rotation-voting hot path (BASELINE.json metric, config 4).
 
@@ -193,29 +194,68 @@ def _load_traffic(path="ffma2"):
         return None, None
 
 
+def _roofline(args, vote_pairs, vote_ms, ms_per_step):
+    """The dominant kernel's roofline entry from the library's own CUDA-event vote timing
+    (rv_result.vote_ms: events recorded on the library's stream around every vote launch)."""
+    steps = args.steps
+    achieved = vote_pairs * FLOP_PER_PAIR / (vote_ms / 1e3) / 1e12 if vote_ms > 0 else None
+    traffic, _ = _load_traffic(args.vote)
+    if args.vote == "tc":
+        # the contraction runs on the tensor cores: fp16 dense peak (= the measured bf16 rate)
+        peak, src = measured_peak("bf16_tflops", 1590.0)
+        pairs_s = vote_pairs / (vote_ms / 1e3)
+        return {
+            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "rv_vote_tc_kernel (K3-TC, tcgen05 kind::f16, fp16-split, fp32 TMEM accum)",
+            "peak_source": f"{src} dense bf16/fp16 tensor peak (MEASURED_PEAKS.json bf16_tflops)",
+            "flop_per_pair": FLOP_PER_PAIR,
+            "executed_mma_tflops": pairs_s * MMA_FLOP_PER_PAIR / 1e12,
+            "executed_mma_frac": pairs_s * MMA_FLOP_PER_PAIR / 1e12 / peak,
+            "epilogue_bound": {
+                "what": "TMEM->RF readout (tcgen05.ld 64 B/clk/SMSP, 4 B/pair) and the ALU sign "
+                        "count (16 lanes/clk/SMSP): 64 pairs/clk/SM at 1965 MHz",
+                "peak_pairs_per_s": TC_EPI_PEAK_PAIRS, "achieved_pairs_per_s": pairs_s,
+                "frac": pairs_s / TC_EPI_PEAK_PAIRS},
+            "vote_ms_per_step": vote_ms / steps,
+            "vote_share_of_step": (vote_ms / steps) / ms_per_step}
+    return {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": (achieved / FP32_PEAK_TFLOPS) if achieved else None,
+            "traffic": traffic,
+            "kernel": "rv_vote_kernel (K3, FFMA2), 18 flop per (corr, cell) pair",
+            "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)",
+            "vote_ms_per_step": vote_ms / steps,
+            "vote_share_of_step": (vote_ms / steps) / ms_per_step}
+
+
+def _dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2506_11547_b200 import rot_vote_get_unique_id
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        idb = [rot_vote_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idb, src=0)
+        nccl_id = idb[0]
+    return world, rank, local, nccl_id
+
+
 def run_ours(args):
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import datagen
-    from paper_2506_11547_b200 import RotVote, rot_vote_get_unique_id
+    from paper_2506_11547_b200 import RotVote
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        idb = [rot_vote_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(idb, src=0)
-        nccl_id = idb[0]
-    else:
-        nccl_id = None
-
+    world, rank, local, nccl_id = _dist_setup(args)
     pr = datagen.cfg4()
     stream = torch.cuda.current_stream()
     rv = RotVote(device=local, max_n=pr.n, rank=rank, world=world, nccl_id=nccl_id,
@@ -276,35 +316,7 @@ def run_ours(args):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = r2.pair_votes * args.e2e_steps / (float(e2e_t.item()) / 1e3)
 
-    achieved = vote_pairs * FLOP_PER_PAIR / (vote_ms / 1e3) / 1e12 if vote_ms > 0 else None
-    traffic, _ = _load_traffic(args.vote)
-    if args.vote == "tc":
-        # the contraction runs on the tensor cores: fp16 dense peak (= the measured bf16 rate)
-        peak, src = measured_peak("bf16_tflops", 1590.0)
-        pairs_s = vote_pairs / (vote_ms / 1e3)
-        roofline = {
-            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": traffic,
-            "kernel": "rv_vote_tc_kernel (K3-TC, tcgen05 kind::f16, fp16-split, fp32 TMEM accum)",
-            "peak_source": f"{src} dense bf16/fp16 tensor peak (MEASURED_PEAKS.json bf16_tflops)",
-            "flop_per_pair": FLOP_PER_PAIR,
-            "executed_mma_tflops": pairs_s * MMA_FLOP_PER_PAIR / 1e12,
-            "executed_mma_frac": pairs_s * MMA_FLOP_PER_PAIR / 1e12 / peak,
-            "epilogue_bound": {
-                "what": "TMEM->RF readout (tcgen05.ld 64 B/clk/SMSP, 4 B/pair) and the ALU sign "
-                        "count (16 lanes/clk/SMSP): 64 pairs/clk/SM at 1965 MHz",
-                "peak_pairs_per_s": TC_EPI_PEAK_PAIRS, "achieved_pairs_per_s": pairs_s,
-                "frac": pairs_s / TC_EPI_PEAK_PAIRS},
-            "vote_ms_per_step": vote_ms / args.steps,
-            "vote_share_of_step": (vote_ms / args.steps) / ms_per_step}
-    else:
-        roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": (achieved / FP32_PEAK_TFLOPS) if achieved else None,
-                    "traffic": traffic,
-                    "kernel": "rv_vote_kernel (K3, FFMA2), 18 flop per (corr, cell) pair",
-                    "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)",
-                    "vote_ms_per_step": vote_ms / args.steps,
-                    "vote_share_of_step": (vote_ms / args.steps) / ms_per_step}
+    roofline = _roofline(args, vote_pairs, vote_ms, ms_per_step)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -339,44 +351,107 @@ def run_ours(args):
 
 
 def run_batched(args):
-    """Extra line: BASELINE config 5 (4096 independent problems x N=1000), one GPU."""
+    """BASELINE config 5: 4096 independent problems x N=1000 in one rot_vote_solve_batched call
+    per step; under torchrun the library shards the problems over the ranks (no data-path
+    collective; one result all-gather)."""
+    import numpy as np
     import torch
+    import torch.distributed as dist
 
     import datagen
     from paper_2506_11547_b200 import RotVote
+    world, rank, local, nccl_id = _dist_setup(args)
     bt = datagen.cfg5()
-    rv = RotVote(max_n=bt.x.shape[0], max_problems=4096, tensor_vote=(args.vote == "tc"))
+    stream = torch.cuda.current_stream()
+    rv = RotVote(device=local, max_n=bt.x.shape[0], max_problems=4096, rank=rank, world=world,
+                 nccl_id=nccl_id, stream=stream, tensor_vote=(args.vote == "tc"))
     x = torch.from_numpy(bt.x).cuda()
     y = torch.from_numpy(bt.y).cuda()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
     for _ in range(max(3, args.warmup)):
         res = rv.solve_batched(x, y, bt.offsets, bt.eps)
-    torch.cuda.synchronize()
-    ms, vote_ms, vote_pairs = [], 0.0, 0
-    with ClockSampler(0) as clk:
+    ref_votes = np.array([r.votes for r in res])
+    ref_cell = np.array([r.cell for r in res])
+    barrier()
+    step_ms, vote_ms, vote_pairs, launches = [], 0.0, 0, 0
+    with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            r = rv.solve_batched(x, y, bt.offsets, bt.eps)
+            r = rv.solve_batched(x, y, bt.offsets, bt.eps, raw=True)
             e1.record(stream)
             e1.synchronize()
-            ms.append(e0.elapsed_time(e1))
-            vote_ms += r[0].vote_ms
-            vote_pairs += r[0].vote_pairs
+            step_ms.append(e0.elapsed_time(e1))
+            vote_ms += float(r["vote_ms"][0])            # this rank's vote kernels
+            vote_pairs += int(r["vote_pairs"][0])
+            launches += int(r["launches"][0])
+            assert np.array_equal(r["votes"], ref_votes) and np.array_equal(r["cell"], ref_cell)
+    barrier()
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    total_ms = float(total.item())
+    ms_per_step = total_ms / args.steps
     pv = sum(p.pair_votes for p in res)
-    t = sum(ms) / len(ms)
-    ach = vote_pairs * FLOP_PER_PAIR / (vote_ms / 1e3) / 1e12
-    print(json.dumps({"metric": "corr×cell votes/s, batched", "value": pv / (t / 1e3), "unit": UNIT,
-                      "n_gpus": 1, "steps": args.steps, "ms_per_step": t,
-                      "config": {"workload": "cfg5: 4096 problems x N=1000, 80% outliers, eps=0.09",
-                                 "pair_votes_per_step": pv},
-                      "roofline": {"bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS,
-                                   "frac": ach / FP32_PEAK_TFLOPS,
-                                   "vote_share_of_step": vote_ms / args.steps / t},
-                      "clocks": clk.summary()}), flush=True)
+    value = pv * args.steps / (total_ms / 1e3)
+
+    # end to end: pinned host inputs copied in and the per-problem rotations read out, per step
+    hx = torch.from_numpy(bt.x).pin_memory()
+    hy = torch.from_numpy(bt.y).pin_memory()
+    e2e_ms = []
+    for _ in range(args.e2e_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xd = hx.cuda(non_blocking=True)
+        yd = hy.cuda(non_blocking=True)
+        r2 = rv.solve_batched(xd, yd, bt.offsets, bt.eps, raw=True)  # results land on the host
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = pv * args.e2e_steps / (float(e2e_t.item()) / 1e3)
+    from scipy.spatial.transform import Rotation as Rot
+    errs = np.array([np.degrees(Rot.from_matrix(p.R.T @ _quat_to_R(q.q)).magnitude())
+                     for p, q in zip(bt.problems, res)])
+    line = {
+        "metric": METRIC + " [batched config 5]", "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f16x3-split/f32" if args.vote == "tc" else "f32", "data": "synthetic",
+        "config": {"workload": "cfg5: 4096 problems x N=1000, 80% outliers, sigma~U[0.005,0.03], "
+                               "eps=0.09", "vote_path": args.vote,
+                   "l2": "flushed between steps (512 MB write)",
+                   "parallelism": f"problems sharded over {world} GPU(s)" if world > 1 else "1 GPU",
+                   "pair_votes_per_step": pv, "solves_per_s": 4096 / (ms_per_step / 1e3),
+                   "success_rate_5deg": float(np.mean(errs < 5.0))},
+        "roofline": _roofline(args, vote_pairs, vote_ms, ms_per_step),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(bt.x.nbytes + bt.y.nbytes),
+                "d2h_bytes_per_step": int(4096 * 8 * 4), "ms_per_step": sum(e2e_ms) / len(e2e_ms)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    rv.close()
+    if world > 1:
+        dist.destroy_process_group()
     return 0
+
+
+def _quat_to_R(q):
+    import numpy as np
+    w, a, b, c = q
+    return np.array([[w * w + a * a - b * b - c * c, 2 * (a * b - w * c), 2 * (a * c + w * b)],
+                     [2 * (a * b + w * c), w * w - a * a + b * b - c * c, 2 * (b * c - w * a)],
+                     [2 * (a * c - w * b), 2 * (b * c + w * a), w * w - a * a - b * b + c * c]])
 
 
 def main():

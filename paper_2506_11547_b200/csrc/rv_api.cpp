@@ -197,10 +197,13 @@ struct rv_ctx {
   // device-resident batched level loop (rv_dplan.cu): ping-pong block lists + counts, the
   // per-problem offsets/counts/picks/bounds, the recheck lists and the winners
   DevBuf<uint32_t> dp_lins[2], dp_ca[2], dp_cb[2];
-  DevBuf<int64_t> dp_off[2], dp_lb, dp_roff;
-  DevBuf<int32_t> dp_cnt[2], dp_rcnt, dp_rlist, dp_res;
-  DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex;
+  DevBuf<int64_t> dp_off[2], dp_lb, dp_act;
+  DevBuf<int32_t> dp_cnt[2], dp_rcnt, dp_ties;
+  DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex, dp_lmax;
+  DevBuf<unsigned long long> dp_best;
   DevBuf<int32_t> l0surv;        // host-planner batched path: level-0 survivor indices
+  DevBuf<uint8_t> atab;          // K3-TC A-operand blocks (K2-TC)
+  DevBuf<rv::ABlock> ablk;
   bool vote_pending = false;     // evv0/evv1 bracket a vote launch not yet accounted
   void collect_vote_ms() {
     if (!vote_pending) return;
@@ -313,11 +316,16 @@ int build_vote_items(const std::vector<int64_t>& ncell, const std::vector<int64_
   return groups;
 }
 
-// K3-TC items: CTAs of <= kTcM cells (one CTA per SM: 512 TMEM columns), correspondence
-// chunks of whole kTcN tiles; chunk count chosen, as for K3, to fill whole waves.
+// K3-TC items: <= cpb cells (kTcM, or kTcM/2 rows-pairs in FINAL mode) x a correspondence
+// chunk of whole kTcN tiles; chunk count chosen, as for K3, to fill whole waves of the
+// persistent kernel's CTAs.  ablocks: the distinct A-operand blocks (K2-TC); a segment whose
+// block list equals the previous segment's (same seg_key, same cell count -- the shared
+// level-0 grid of a batch) reuses its blocks.
 void build_tc_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
-                    int slots, std::vector<rv::VoteItem>& items, int64_t cpb = rv::kTcM) {
+                    int slots, std::vector<rv::VoteItem>& items, std::vector<rv::ABlock>& ablocks,
+                    int64_t cpb = rv::kTcM, const std::vector<const void*>* seg_key = nullptr) {
   items.clear();
+  ablocks.clear();
   int64_t cbs = 0, tmax = 0;
   for (size_t s = 0; s < ncell.size(); ++s) {
     if (ncell[s] == 0 || ncorr[s] == 0) continue;
@@ -336,6 +344,8 @@ void build_tc_items(const std::vector<int64_t>& ncell, const std::vector<int64_t
     const double score = eff - (waves < 4.0 ? 0.5 * (4.0 - waves) / 4.0 : 0.0);
     if (score > best + 1e-9) { best = score; best_nch = nch; }
   }
+  int64_t last = -1;
+  int32_t last_base = 0;
   for (size_t s = 0; s < ncell.size(); ++s) {
     if (ncell[s] == 0 || ncorr[s] == 0) continue;
     const int64_t nt = (ncorr[s] + rv::kTcN - 1) / rv::kTcN;
@@ -343,12 +353,24 @@ void build_tc_items(const std::vector<int64_t>& ncell, const std::vector<int64_t
     const int64_t per = (ncell[s] + cb - 1) / cb;
     const int64_t nch = std::min<int64_t>(best_nch, nt);
     const int64_t ct = (nt + nch - 1) / nch;  // tiles per chunk
+    int32_t base;
+    if (seg_key && last >= 0 && (*seg_key)[s] == (*seg_key)[last] && ncell[s] == ncell[last]) {
+      base = last_base;
+    } else {
+      base = (int32_t)ablocks.size();
+      for (int64_t b = 0; b < cb; ++b) {
+        const int64_t c0 = b * per, nc = std::min(per, ncell[s] - c0);
+        if (nc > 0) ablocks.push_back({(int32_t)s, (int32_t)c0, (int32_t)nc, 0});
+      }
+    }
+    last = (int64_t)s;
+    last_base = base;
     for (int64_t b = 0; b < cb; ++b) {
       const int64_t c0 = b * per, nc = std::min(per, ncell[s] - c0);
       if (nc <= 0) continue;
       for (int64_t t0 = 0; t0 < nt; t0 += ct)
         items.push_back({(int32_t)s, (int32_t)c0, (int32_t)nc, (int32_t)(t0 * rv::kTcN),
-                         (int32_t)(std::min(ct, nt - t0) * rv::kTcN)});
+                         (int32_t)(std::min(ct, nt - t0) * rv::kTcN), base + (int32_t)b});
     }
   }
 }
@@ -362,6 +384,22 @@ void build_exact_items(const std::vector<int64_t>& ncell, const std::vector<int6
       for (int64_t i0 = 0; i0 < ncorr[s]; i0 += chunk)
         items.push_back({(int32_t)s, (int32_t)c, 1, (int32_t)i0,
                          (int32_t)std::min(chunk, ncorr[s] - i0)});
+}
+
+// K2-TC + K3-TC over the items already in ctx->vitems (segments in ctx->vsegs).  The block
+// list goes through a pageable copy (staged on the call).  Asynchronous.
+int launch_tc(rv_ctx* ctx, const std::vector<rv::ABlock>& ab, int32_t n_items, bool fin,
+              float* dump = nullptr, int64_t ld = 0) {
+  if (ab.empty() || n_items <= 0) return RV_OK;
+  RV_CUDA(ctx->ablk.ensure(ab.size()), "allocating A blocks");
+  RV_CUDA(ctx->atab.ensure(ab.size() * (size_t)rv::kTcABlockBytes), "allocating A table");
+  RV_CUDA(cudaMemcpyAsync(ctx->ablk.p, ab.data(), ab.size() * sizeof(rv::ABlock),
+                          cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  rv::launch_vote_tc(ctx->tctab.p, ctx->atab.p, ctx->ablk.p, (int32_t)ab.size(), ctx->vsegs.p,
+                     ctx->vitems.p, n_items, ctx->cfg.guard + kTcExtraGuard, dump, ld,
+                     ctx->stream, fin);
+  ctx->launches += 1;  // K2-TC (the vote launch is counted by the caller)
+  return RV_OK;
 }
 
 // ---- K1 for P problems ----------------------------------------------------------------------
@@ -464,6 +502,7 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
     ncorr.push_back(n);
   }
   std::vector<rv::VoteItem> items;
+  std::vector<rv::ABlock> ablocks;
   int groups = 1;
   const bool tc_auto = auto_tc && ctx->tc_on;
   const bool tc_final = mode == RV_MODE_FINAL_TC || (mode == RV_MODE_FINAL && tc_auto);
@@ -472,7 +511,7 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
     return ctx->fail(RV_EINVAL, "the _TC modes need a context created with tensor_vote = 1");
   if (use_tc) {
     for (rv::VoteSeg& sg : segs) sg.koff = ctx->tc_toff[0];
-    build_tc_items(ncell, ncorr, ctx->num_sms, items, tc_final ? rv::kTcM / 2 : rv::kTcM);
+    build_tc_items(ncell, ncorr, ctx->num_sms, items, ablocks, tc_final ? rv::kTcM / 2 : rv::kTcM);
   } else if (mode == RV_MODE_EXACT) {
     build_exact_items(ncell, ncorr, items);
   } else {
@@ -513,8 +552,9 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
   } else {
     RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
     if (use_tc)
-      rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
-                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, tc_final);
+      {
+        if (int rc = launch_tc(ctx, ablocks, (int32_t)items.size(), tc_final)) return rc;
+      }
     else
       rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
                       (int32_t)items.size(), ctx->cfg.guard, s);
@@ -784,12 +824,16 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     off += r.m;
   }
   std::vector<rv::VoteItem> items;
+  std::vector<rv::ABlock> ablocks;
   int groups = 1;
   const bool tc_final = mode == RV_MODE_FINAL && ctx->tc_on;
   const bool use_tc = tc_final || (mode == RV_MODE_BOUND && ctx->tc_on);
   if (use_tc) {
     for (size_t q = 0; q < reqs.size(); ++q) segs[q].koff = ctx->tc_toff[reqs[q].prob];
-    build_tc_items(ncell, ncorr, ctx->num_sms, items, tc_final ? rv::kTcM / 2 : rv::kTcM);
+    std::vector<const void*> keys(segs.size());
+    for (size_t q = 0; q < segs.size(); ++q) keys[q] = segs[q].lins;
+    build_tc_items(ncell, ncorr, ctx->num_sms, items, ablocks, tc_final ? rv::kTcM / 2 : rv::kTcM,
+                   &keys);
   } else if (mode == RV_MODE_EXACT) {
     build_exact_items(ncell, ncorr, items);
   } else {
@@ -829,8 +873,9 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   } else {
     RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
     if (use_tc)
-      rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
-                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, tc_final);
+      {
+        if (int rc = launch_tc(ctx, ablocks, (int32_t)items.size(), tc_final)) return rc;
+      }
     else
       rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
                       (int32_t)items.size(), ctx->cfg.guard, s);
@@ -899,9 +944,10 @@ int vote_lists(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   }
   if (segs.empty()) return RV_OK;
   std::vector<rv::VoteItem> items;
+  std::vector<rv::ABlock> ablocks;
   int groups = 1;
   if (use_tc)
-    build_tc_items(ncell, ncorr, ctx->num_sms, items, tc_final ? rv::kTcM / 2 : rv::kTcM);
+    build_tc_items(ncell, ncorr, ctx->num_sms, items, ablocks, tc_final ? rv::kTcM / 2 : rv::kTcM);
   else if (mode == RV_MODE_EXACT)
     build_exact_items(ncell, ncorr, items);
   else
@@ -915,8 +961,10 @@ int vote_lists(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                           cudaMemcpyHostToDevice, s), "H2D");
   RV_CUDA(cudaMemcpyAsync(ctx->vitems.p, items.data(), items.size() * sizeof(rv::VoteItem),
                           cudaMemcpyHostToDevice, s), "H2D");
-  RV_CUDA(cudaMemsetAsync(dca, 0, span * 4, s), "memset");
-  if (mode == RV_MODE_FINAL) RV_CUDA(cudaMemsetAsync(dcb, 0, span * 4, s), "memset");
+  if (span > 0) {  // span 0: the caller's list kernel zeroed the count slots
+    RV_CUDA(cudaMemsetAsync(dca, 0, span * 4, s), "memset");
+    if (mode == RV_MODE_FINAL) RV_CUDA(cudaMemsetAsync(dcb, 0, span * 4, s), "memset");
+  }
   if (mode == RV_MODE_EXACT) {
     rv::launch_exact(ctx->k9.p, ctx->stride, x, y, ctx->vsegs.p, ctx->vitems.p,
                      (int32_t)items.size(), ctx->cfg.guard, s);
@@ -924,8 +972,9 @@ int vote_lists(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     ctx->collect_vote_ms();
     RV_CUDA(cudaEventRecord(ctx->evv0, s), "event");
     if (use_tc)
-      rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
-                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, tc_final);
+      {
+        if (int rc = launch_tc(ctx, ablocks, (int32_t)items.size(), tc_final)) return rc;
+      }
     else
       rv::launch_vote(mode, groups, ctx->k9.p, ctx->stride, ctx->vsegs.p, ctx->vitems.p,
                       (int32_t)items.size(), ctx->cfg.guard, s);
@@ -1036,81 +1085,99 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     phases.push_back(hcnt);
     tr.mark("  dive level");
   }
-  // ---- branch and bound from the level-0 survivors (UB >= lb*)
-  int cur = -1;  // -1: parents = the shared level-0 grid
+  // ---- branch and bound from the level-0 survivors (UB >= lb*).  A level's list of problem
+  // p has pact[p+1] - pact[p] entries stored from pcap[p]; its children get the capacity
+  // region (parents x f^3) starting at pact[p] * f^3.
+  std::vector<int64_t> pact(PL + 1);
+  for (int32_t p = 0; p <= PL; ++p) pact[p] = (int64_t)p * m0;  // the shared grid: act == cap
+  const uint32_t* plins = ctx->grid_list.p;
+  const uint32_t* pub = ctx->l0cnt.p;
+  bool shared = true;
+  int cur = -1;
+  RV_CUDA(ctx->dp_act.ensure(PL + 1), "allocating");
   for (int l = 1; l < L; ++l) {
     const int nb = cur == 0 ? 1 : 0;
     const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1];
-    const uint32_t* plins = cur < 0 ? ctx->grid_list.p : ctx->dp_lins[cur].p;
-    const int64_t* poff = cur < 0 ? nullptr : ctx->dp_off[cur].p;
-    const uint32_t* pub = cur < 0 ? ctx->l0cnt.p : ctx->dp_ca[cur].p;
-    const int32_t* pcnt = cur < 0 ? nullptr : ctx->dp_cnt[cur].p;
-    const int64_t shared_m = cur < 0 ? m0 : 0;
+    const int64_t f3 = (int64_t)f * f * f;
+    std::vector<int64_t> ccap(PL + 1);
+    for (int32_t p = 0; p <= PL; ++p) ccap[p] = pact[p] * f3;
+    const int64_t cap_total = std::max<int64_t>(1, ccap[PL]);
+    RV_CUDA(ctx->dp_lins[nb].ensure(cap_total), "allocating");
+    RV_CUDA(ctx->dp_ca[nb].ensure(cap_total), "allocating");
+    RV_CUDA(ctx->dp_cb[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_cnt[nb].ensure(PL), "allocating");
     RV_CUDA(ctx->dp_off[nb].ensure(PL + 1), "allocating");
-    rv::dp_launch_bnb_children(plins, poff, pub, poff, pcnt, shared_m, ctx->dp_lb.p, Bp, f, nullptr,
-                               nullptr, ctx->dp_cnt[nb].p, PL, s);
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_act.p, pact.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+            "H2D");
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_off[nb].p, ccap.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+            "H2D");
+    RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
+    rv::dp_launch_bnb_expand(plins, shared, ctx->dp_act.p, shared ? ctx->dp_act.p : ctx->dp_off[cur].p,
+                             pub, ctx->dp_lb.p, PL, pact[PL], Bp, f, ctx->dp_off[nb].p,
+                             ctx->dp_lins[nb].p, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p,
+                             ctx->dp_cnt[nb].p, s);
     ctx->launches += 1;
     if (int rc = read_counts(ctx, ctx->dp_cnt[nb].p, PL, hcnt)) return rc;
-    hoff[0] = 0;
-    for (int32_t p = 0; p < PL; ++p) hoff[p + 1] = hoff[p] + hcnt[p];
-    const int64_t total = hoff[PL];
-    RV_CUDA(ctx->dp_lins[nb].ensure(std::max<int64_t>(1, total)), "allocating");
-    RV_CUDA(ctx->dp_ca[nb].ensure(std::max<int64_t>(1, total)), "allocating");
-    RV_CUDA(ctx->dp_cb[nb].ensure(std::max<int64_t>(1, total)), "allocating");
-    RV_CUDA(cudaMemcpyAsync(ctx->dp_off[nb].p, hoff.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
-            "H2D");
-    rv::dp_launch_bnb_children(plins, poff, pub, poff, pcnt, shared_m, ctx->dp_lb.p, Bp, f,
-                               ctx->dp_lins[nb].p, ctx->dp_off[nb].p, nullptr, PL, s);
-    ctx->launches += 1;
     const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
-    if (int rc = vote_lists(ctx, x, y, rows, koff, eps, mode, ch[l], ctx->dp_lins[nb].p, hoff, hcnt,
-                            total, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p))
+    // the expand kernel zeroed the count slots: no clear (span 0)
+    if (int rc = vote_lists(ctx, x, y, rows, koff, eps, mode, ch[l], ctx->dp_lins[nb].p, ccap, hcnt,
+                            0, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p))
       return rc;
     phases.push_back(hcnt);
+    pact[0] = 0;
+    for (int32_t p = 0; p < PL; ++p) pact[p + 1] = pact[p] + hcnt[p];
+    plins = ctx->dp_lins[nb].p;
+    pub = ctx->dp_ca[nb].p;
+    shared = false;
     cur = nb;
     tr.mark("  bnb level");
   }
-  // ---- finest level: recheck hi >= max lo, hi != lo exactly; winner per problem
+  // ---- finest level: max lo, exact-known blocks, recheck of hi >= max lo, hi != lo; winner
+  const int64_t ftotal = pact[PL];
   const uint32_t* flins = ctx->dp_lins[cur].p;
   const uint32_t* fhi = ctx->dp_ca[cur].p;
   const uint32_t* flo = ctx->dp_cb[cur].p;
-  const int64_t* foff = ctx->dp_off[cur].p;
-  const int32_t* fcnt = ctx->dp_cnt[cur].p;
+  const int64_t* fcap = ctx->dp_off[cur].p;
   RV_CUDA(ctx->dp_rcnt.ensure(PL), "allocating");
-  RV_CUDA(ctx->dp_roff.ensure(PL + 1), "allocating");
-  rv::dp_launch_recheck_set(fhi, flo, foff, fcnt, ctx->dp_rcnt.p, nullptr, nullptr, PL, s);
-  ctx->launches += 1;
+  RV_CUDA(ctx->dp_lmax.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_best.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_ties.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_rlins.ensure(std::max<int64_t>(1, ftotal)), "allocating");
+  RV_CUDA(ctx->dp_ex.ensure(std::max<int64_t>(1, ftotal)), "allocating");
+  RV_CUDA(cudaMemcpyAsync(ctx->dp_act.p, pact.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+          "H2D");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_rcnt.p, 0, PL * 4, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_lmax.p, 0, PL * 4, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_best.p, 0, PL * 8, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_ties.p, 0, PL * 4, s), "memset");
+  rv::dp_launch_final_max(ctx->dp_act.p, fcap, flo, PL, ftotal, ctx->dp_lmax.p, s);
+  rv::dp_launch_final_split(ctx->dp_act.p, fcap, flins, fhi, flo, ctx->dp_lmax.p, PL, ftotal,
+                            ctx->dp_best.p, ctx->dp_rlins.p, ctx->dp_rcnt.p, s);
+  ctx->launches += 2;
   std::vector<int32_t> rcnt;
   if (int rc = read_counts(ctx, ctx->dp_rcnt.p, PL, rcnt)) return rc;
-  std::vector<int64_t> roff(PL + 1, 0);
-  for (int32_t p = 0; p < PL; ++p) roff[p + 1] = roff[p] + rcnt[p];
-  const int64_t rtotal = roff[PL];
-  RV_CUDA(ctx->dp_rlist.ensure(std::max<int64_t>(1, rtotal)), "allocating");
-  RV_CUDA(ctx->dp_rlins.ensure(std::max<int64_t>(1, rtotal)), "allocating");
-  RV_CUDA(ctx->dp_ex.ensure(std::max<int64_t>(1, rtotal)), "allocating");
-  RV_CUDA(ctx->dp_res.ensure(3 * (size_t)PL), "allocating");
-  RV_CUDA(cudaMemcpyAsync(ctx->dp_roff.p, roff.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
-          "H2D");
+  int64_t rtotal = 0;
+  for (int32_t p = 0; p < PL; ++p) rtotal += rcnt[p];
   if (rtotal > 0) {
-    rv::dp_launch_recheck_set(fhi, flo, foff, fcnt, nullptr, ctx->dp_roff.p, ctx->dp_rlist.p, PL, s);
-    rv::dp_launch_gather(flins, foff, ctx->dp_roff.p, ctx->dp_rcnt.p, ctx->dp_rlist.p,
-                         ctx->dp_rlins.p, PL, s);
-    ctx->launches += 2;
     if (int rc = vote_lists(ctx, x, y, rows, koff, eps, RV_MODE_EXACT, ch[L - 1], ctx->dp_rlins.p,
-                            roff, rcnt, rtotal, ctx->dp_ex.p, ctx->dp_ex.p))
+                            pact, rcnt, std::max<int64_t>(1, ftotal), ctx->dp_ex.p, ctx->dp_ex.p))
       return rc;
+    rv::dp_launch_final_rechecked(ctx->dp_act.p, ctx->dp_rcnt.p, ctx->dp_rlins.p, ctx->dp_ex.p, PL,
+                                  ftotal, ctx->dp_best.p, s);
+    ctx->launches += 1;
     phases.push_back(rcnt);
   }
-  rv::dp_launch_finalize(flins, fhi, flo, foff, fcnt, ctx->dp_ex.p, ctx->dp_roff.p, ctx->dp_rcnt.p,
-                         ctx->dp_rlist.p, ctx->dp_res.p, PL, s);
+  rv::dp_launch_final_ties(ctx->dp_act.p, fcap, fhi, flo, ctx->dp_rcnt.p, ctx->dp_ex.p, PL, ftotal,
+                           ctx->dp_best.p, ctx->dp_ties.p, s);
   ctx->launches += 1;
   RV_CUDA(cudaGetLastError(), "launching the level loop");
-  RV_CUDA(ctx->down.ensure((size_t)PL * 20 + 512), "allocating staging");
+  RV_CUDA(ctx->down.ensure((size_t)PL * 24 + 512), "allocating staging");
   ctx->down.reset();
-  int32_t* hres = ctx->down.take<int32_t>(3 * (size_t)PL);
+  unsigned long long* hbest = ctx->down.take<unsigned long long>(PL);
+  int32_t* hties = ctx->down.take<int32_t>(PL);
   int64_t* hlb = ctx->down.take<int64_t>(PL);
-  RV_CUDA(cudaMemcpyAsync(hres, ctx->dp_res.p, 12 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hbest, ctx->dp_best.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hties, ctx->dp_ties.p, 4 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hlb, ctx->dp_lb.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaStreamSynchronize(s), "batched finalize");
   ctx->collect_vote_ms();
@@ -1119,10 +1186,10 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   for (int32_t p = 0; p < PL; ++p) {
     rv_plan_result& r = res[p];
     const uint64_t n = (uint64_t)(rows[p + 1] - rows[p]);
-    r.lin = (uint32_t)hres[3 * p];
+    r.votes = (uint32_t)(hbest[p] >> 32);
+    r.lin = hbest[p] ? 0xffffffffu - (uint32_t)(hbest[p] & 0xffffffffu) : 0u;
     r.B = ch[L - 1];
-    r.votes = (uint32_t)hres[3 * p + 1];
-    r.n_tied = hres[3 * p + 2];
+    r.n_tied = hties[p];
     r.lb_star = (uint32_t)hlb[p];
     r.n_rechecked = rcnt[p];
     for (size_t ph = 0; ph < phases.size(); ++ph) {
@@ -1465,13 +1532,14 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->koffs.release(); ctx->bad.release(); ctx->hx.release(); ctx->hy.release();
   ctx->hmask.release(); ctx->gather.release(); ctx->grid_list.release();
   ctx->l0cnt.release(); ctx->l0bg.release(); ctx->l0idx.release(); ctx->l0aux.release();
-  ctx->l0surv.release();
+  ctx->l0surv.release(); ctx->atab.release(); ctx->ablk.release();
   for (int b = 0; b < 2; ++b) {
     ctx->dp_lins[b].release(); ctx->dp_ca[b].release(); ctx->dp_cb[b].release();
     ctx->dp_off[b].release(); ctx->dp_cnt[b].release();
   }
-  ctx->dp_lb.release(); ctx->dp_roff.release(); ctx->dp_rcnt.release(); ctx->dp_rlist.release();
-  ctx->dp_res.release(); ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release();
+  ctx->dp_lb.release(); ctx->dp_act.release(); ctx->dp_rcnt.release(); ctx->dp_ties.release();
+  ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release(); ctx->dp_lmax.release();
+  ctx->dp_best.release();
   ctx->up.release(); ctx->down.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -1594,14 +1662,14 @@ int rot_vote_debug_tc_scores(rv_ctx* ctx, const float* x, const float* y, int64_
   sg.B = B;
   sg.eps = eps;
   std::vector<rv::VoteItem> items;
-  build_tc_items({m}, {n}, ctx->num_sms, items);
+  std::vector<rv::ABlock> ablocks;
+  build_tc_items({m}, {n}, ctx->num_sms, items, ablocks);
   RV_CUDA(ctx->vsegs.ensure(1), "allocating");
   RV_CUDA(ctx->vitems.ensure(items.size()), "allocating");
   RV_CUDA(cudaMemcpy(ctx->vsegs.p, &sg, sizeof(sg), cudaMemcpyHostToDevice), "H2D");
   RV_CUDA(cudaMemcpy(ctx->vitems.p, items.data(), items.size() * sizeof(rv::VoteItem),
                      cudaMemcpyHostToDevice), "H2D");
-  rv::launch_vote_tc(ctx->tctab.p, ctx->vsegs.p, ctx->vitems.p, (int32_t)items.size(),
-                     ctx->cfg.guard + kTcExtraGuard, out, ld, ctx->stream);
+  if (int rc = launch_tc(ctx, ablocks, (int32_t)items.size(), false, out, ld)) return rc;
   RV_CUDA(cudaGetLastError(), "launching K3-TC");
   RV_CUDA(cudaStreamSynchronize(ctx->stream), "K3-TC");
   return RV_OK;

@@ -8,10 +8,12 @@
 //   dive:  children of the 27-neighbourhood of the pick (neighbours in ascending lin, children
 //          in (a,b,c) order); pick = max excess UB - n*bg (centre inside the ball first, ties
 //          -> lowest lin); at the finest level lb* = max cnt_b;
-//   BnB:   parents with UB >= lb*, their candidate children in parent order;
+//   BnB:   parents with UB >= lb*, their candidate children;
 //   final: L = max lo; recheck the blocks with hi >= L and hi != lo; winner = max exact count,
-//          ties -> lowest lin.
-// Ordered compaction inside a CTA uses warp ballots + a CTA-wide exclusive scan.
+//          ties -> lowest lin (a packed 64-bit atomicMax of (count, ~lin)).
+// The dive's lists are built per problem (one CTA, ordered compaction by warp ballots + a
+// CTA-wide scan); the BnB and final-level kernels are flat (one thread per list entry of all
+// problems, per-problem atomic slot allocation).
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -163,138 +165,129 @@ __global__ void __launch_bounds__(kDpThreads) dp_max_lo(const uint32_t* __restri
   }
 }
 
-// BnB children of the parents with UB >= lb[p].  Parent list of problem p: lins + poff[p]
-// (or the shared grid list when shared != 0) with counts ub + uoff[p], pcnt[p] entries.
-// count pass (out == nullptr): ccnt[p] = number of candidate children; write pass: children
-// in parent order at out + coff[p].
-__global__ void __launch_bounds__(kDpThreads) dp_bnb_children(
-    const uint32_t* __restrict__ lins, const int64_t* __restrict__ poff,
-    const uint32_t* __restrict__ ub, const int64_t* __restrict__ uoff,
-    const int32_t* __restrict__ pcnt, int64_t shared_m, const int64_t* __restrict__ lb,
-    int32_t Bp, int32_t f, uint32_t* out, const int64_t* __restrict__ coff, int32_t* ccnt) {
-  const int p = blockIdx.x;
-  __shared__ int wsum[kDpThreads / 32];
-  __shared__ uint32_t sp[kDpThreads];  // survivors of the current parent chunk, in order
-  const int64_t po = shared_m ? 0 : poff[p];
-  const int64_t uo = shared_m ? (int64_t)p * shared_m : uoff[p];
-  const int m = shared_m ? (int)shared_m : pcnt[p];
-  const int f3 = f * f * f;
+// ---- flat list kernels: one thread per list entry of all problems ----------------------------
+// A level's list of problem p holds act_off[p+1] - act_off[p] entries stored from cap[p]
+// (capacity layout: a problem's children are bounded by its parents x f^3).  The order of
+// the entries inside a problem's list is not deterministic (atomic slot allocation) and
+// never matters: every decision is a max with ties broken by the lowest lin.
+__device__ __forceinline__ int find_problem(const int64_t* __restrict__ act_off, int32_t P,
+                                            int64_t g) {
+  int lo = 0, hi = P;  // last p with act_off[p] <= g
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (act_off[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// BnB: candidate children (Bc = f*Bp) of the parents with UB >= lb[p], appended to problem
+// p's child region ccap[p] (count ccnt[p], zeroed by the caller); their count slots are
+// zeroed here.  shared_lins: the parents' lins are plins[e] (the level-0 grid shared by all
+// problems), else plins[pcap[p] + e].
+__global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared_lins,
+                              const int64_t* __restrict__ act_off, const int64_t* __restrict__ pcap,
+                              const uint32_t* __restrict__ pub, const int64_t* __restrict__ lb,
+                              int32_t P, int32_t Bp, int32_t f, const int64_t* __restrict__ ccap,
+                              uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt) {
+  const int64_t total = act_off[P];
   const int32_t Bc = Bp * f;
-  const int64_t L = lb[p];
-  int base = 0;
-  for (int c0 = 0; c0 < m; c0 += kDpThreads) {
-    // 1. the chunk's survivors (UB >= lb*), compacted in parent order
-    const int par = c0 + threadIdx.x;
-    const bool surv = par < m && (int64_t)ub[uo + par] >= L;
-    int ns;
-    const int spos = cta_rank(surv, &ns, wsum);
-    if (surv) sp[spos] = lins[po + par];
-    __syncthreads();
-    // 2. their candidate children, (parent, a, b, c) order
-    for (int e0 = 0; e0 < ns * f3; e0 += kDpThreads) {
-      const int e = e0 + threadIdx.x;
-      bool keep = false;
-      uint32_t lin = 0;
-      if (e < ns * f3) {
-        int32_t i, j, k;
-        lin_to_ijk(sp[e / f3], Bp, i, j, k);
-        const int r = e % f3, a = r / (f * f), b = (r / f) % f, c = r % f;
-        const int32_t ci = f * i + a, cj = f * j + b, ck = f * k + c;
-        keep = is_candidate(Bc, ci, cj, ck);
-        lin = ijk_to_lin(ci, cj, ck, Bc);
-      }
-      int tot;
-      const int pos = cta_rank(keep, &tot, wsum);
-      if (out && keep) out[coff[p] + base + pos] = lin;
-      base += tot;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int p = find_problem(act_off, P, g);
+    const int64_t e = g - act_off[p], idx = pcap[p] + e;
+    if ((int64_t)pub[idx] < lb[p]) continue;
+    int32_t i, j, k;
+    lin_to_ijk(shared_lins ? plins[e] : plins[idx], Bp, i, j, k);
+    int c = 0;
+    for (int a = 0; a < f; ++a)
+      for (int b = 0; b < f; ++b)
+        for (int d = 0; d < f; ++d) c += is_candidate(Bc, f * i + a, f * j + b, f * k + d) ? 1 : 0;
+    if (c == 0) continue;
+    int64_t w = ccap[p] + atomicAdd(&ccnt[p], c);
+    for (int a = 0; a < f; ++a)
+      for (int b = 0; b < f; ++b)
+        for (int d = 0; d < f; ++d) {
+          const int32_t ci = f * i + a, cj = f * j + b, ck = f * k + d;
+          if (!is_candidate(Bc, ci, cj, ck)) continue;
+          clins[w] = ijk_to_lin(ci, cj, ck, Bc);
+          ca[w] = 0;
+          cb[w] = 0;
+          ++w;
+        }
+  }
+}
+
+// finest level, pass 1: Lmax[p] = max lo (zeroed by the caller)
+__global__ void dp_final_max(const int64_t* __restrict__ act_off, const int64_t* __restrict__ cap,
+                             const uint32_t* __restrict__ lo, int32_t P, uint32_t* Lmax) {
+  const int64_t total = act_off[P];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int p = find_problem(act_off, P, g);
+    atomicMax(&Lmax[p], lo[cap[p] + g - act_off[p]]);
+  }
+}
+
+__device__ __forceinline__ unsigned long long win_key(uint32_t votes, uint32_t lin) {
+  return ((unsigned long long)votes << 32) | (unsigned long long)(0xffffffffu - lin);
+}
+
+// finest level, pass 2: blocks with hi == lo offer their (exact) count to best[p]; blocks
+// with hi >= Lmax[p], hi != lo go to the recheck list of problem p (region act_off[p], count
+// rcnt[p]; both zeroed by the caller)
+__global__ void dp_final_split(const int64_t* __restrict__ act_off, const int64_t* __restrict__ cap,
+                               const uint32_t* __restrict__ lins, const uint32_t* __restrict__ hi,
+                               const uint32_t* __restrict__ lo, const uint32_t* __restrict__ Lmax,
+                               int32_t P, unsigned long long* best, uint32_t* rlins,
+                               int32_t* rcnt) {
+  const int64_t total = act_off[P];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int p = find_problem(act_off, P, g);
+    const int64_t idx = cap[p] + g - act_off[p];
+    const uint32_t h = hi[idx], l = lo[idx];
+    if (h == l) {
+      atomicMax(&best[p], win_key(l, lins[idx]));
+    } else if (h >= Lmax[p]) {
+      rlins[act_off[p] + atomicAdd(&rcnt[p], 1)] = lins[idx];
     }
-    __syncthreads();  // sp is rewritten by the next chunk
   }
-  if (!out && threadIdx.x == 0) ccnt[p] = base;
 }
 
-// Finest level: L[p] = max lo; recheck set = blocks with hi >= L and hi != lo (count pass /
-// ordered write of their list positions at rlist + roff[p]).
-__global__ void __launch_bounds__(kDpThreads) dp_recheck_set(
-    const uint32_t* __restrict__ hi, const uint32_t* __restrict__ lo,
-    const int64_t* __restrict__ off, const int32_t* __restrict__ cnt, int32_t* rcnt,
-    const int64_t* __restrict__ roff, int32_t* rlist) {
-  const int p = blockIdx.x;
-  __shared__ int wsum[kDpThreads / 32];
-  __shared__ uint32_t Ls;
-  uint32_t mx = 0;
-  for (int e = threadIdx.x; e < cnt[p]; e += blockDim.x) mx = max(mx, lo[off[p] + e]);
-  for (int s = 16; s > 0; s >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, s));
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = (int)mx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t r = 0;
-    for (int i = 0; i < kDpThreads / 32; ++i) r = max(r, (uint32_t)wsum[i]);
-    Ls = r;
+// finest level, pass 3 (after the exact recheck): rechecked blocks offer their exact counts
+__global__ void dp_final_rechecked(const int64_t* __restrict__ act_off,
+                                   const int32_t* __restrict__ rcnt,
+                                   const uint32_t* __restrict__ rlins,
+                                   const uint32_t* __restrict__ ex, int32_t P,
+                                   unsigned long long* best) {
+  const int64_t total = act_off[P];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int p = find_problem(act_off, P, g);
+    if (g - act_off[p] >= rcnt[p]) continue;
+    atomicMax(&best[p], win_key(ex[g], rlins[g]));
   }
-  __syncthreads();
-  const uint32_t L = Ls;
-  int base = 0;
-  for (int e0 = 0; e0 < cnt[p]; e0 += kDpThreads) {
-    const int e = e0 + threadIdx.x;
-    const bool keep = e < cnt[p] && hi[off[p] + e] >= L && hi[off[p] + e] != lo[off[p] + e];
-    int tot;
-    const int pos = cta_rank(keep, &tot, wsum);
-    if (rlist && keep) rlist[roff[p] + base + pos] = e;
-    base += tot;
-  }
-  if (!rlist && threadIdx.x == 0) rcnt[p] = base;
 }
 
-// Gather the lins of the recheck list (positions rlist) into rlins (same layout).
-__global__ void dp_gather(const uint32_t* __restrict__ lins, const int64_t* __restrict__ off,
-                          const int64_t* __restrict__ roff, const int32_t* __restrict__ rcnt,
-                          const int32_t* __restrict__ rlist, uint32_t* rlins) {
-  const int p = blockIdx.x;
-  for (int e = threadIdx.x; e < rcnt[p]; e += blockDim.x)
-    rlins[roff[p] + e] = lins[off[p] + rlist[roff[p] + e]];
-}
-
-// Winner per problem: exact count = lo where lo == hi, the rechecked count where rechecked;
-// max, ties -> lowest lin.  res[p] = {lin, votes, n_tied}.
-__global__ void __launch_bounds__(kDpThreads) dp_finalize(
-    const uint32_t* __restrict__ lins, const uint32_t* __restrict__ hi,
-    const uint32_t* __restrict__ lo, const int64_t* __restrict__ off,
-    const int32_t* __restrict__ cnt, const uint32_t* __restrict__ ex,
-    const int64_t* __restrict__ roff, const int32_t* __restrict__ rcnt,
-    const int32_t* __restrict__ rlist, int32_t* res) {
-  const int p = blockIdx.x;
-  __shared__ int64_t best[kDpThreads];
-  __shared__ uint32_t blin[kDpThreads];
-  __shared__ int32_t ties[kDpThreads];
-  int64_t b = -1;
-  uint32_t bl = 0xffffffffu;
-  int32_t t = 0;
-  auto offer = [&](int64_t v, uint32_t lin) {
-    if (v > b) { b = v; bl = lin; t = 1; }
-    else if (v == b) { ++t; if (lin < bl) bl = lin; }
-  };
-  for (int e = threadIdx.x; e < cnt[p]; e += blockDim.x)
-    if (hi[off[p] + e] == lo[off[p] + e]) offer(lo[off[p] + e], lins[off[p] + e]);
-  for (int e = threadIdx.x; e < rcnt[p]; e += blockDim.x)
-    offer(ex[roff[p] + e], lins[off[p] + rlist[roff[p] + e]]);
-  best[threadIdx.x] = b; blin[threadIdx.x] = bl; ties[threadIdx.x] = t;
-  __syncthreads();
-  for (int w = kDpThreads / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      const int o = threadIdx.x + w, s = threadIdx.x;
-      if (best[o] > best[s]) { best[s] = best[o]; blin[s] = blin[o]; ties[s] = ties[o]; }
-      else if (best[o] == best[s] && best[o] >= 0) {
-        ties[s] += ties[o];
-        if (blin[o] < blin[s]) blin[s] = blin[o];
-      }
+// finest level, pass 4: ties[p] = exact-known blocks with the winning count (zeroed by the
+// caller).  Blocks neither exact nor rechecked have hi < Lmax <= the best count.
+__global__ void dp_final_ties(const int64_t* __restrict__ act_off, const int64_t* __restrict__ cap,
+                              const uint32_t* __restrict__ hi, const uint32_t* __restrict__ lo,
+                              const int32_t* __restrict__ rcnt, const uint32_t* __restrict__ ex,
+                              int32_t P, const unsigned long long* __restrict__ best,
+                              int32_t* ties) {
+  const int64_t total = act_off[P];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < 2 * total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = g < total ? g : g - total;
+    const int p = find_problem(act_off, P, h);
+    const uint32_t bv = (uint32_t)(best[p] >> 32);
+    if (g < total) {
+      const int64_t idx = cap[p] + h - act_off[p];
+      if (hi[idx] == lo[idx] && lo[idx] == bv) atomicAdd(&ties[p], 1);
+    } else if (h - act_off[p] < rcnt[p] && ex[h] == bv) {
+      atomicAdd(&ties[p], 1);
     }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    res[3 * p] = (int32_t)blin[0];
-    res[3 * p + 1] = (int32_t)(best[0] < 0 ? 0 : best[0]);
-    res[3 * p + 2] = ties[0];
   }
 }
 
@@ -313,28 +306,43 @@ void dp_launch_max_lo(const uint32_t* b, const int64_t* off, const int32_t* cnt,
                       int32_t P, cudaStream_t s) {
   dp_max_lo<<<P, kDpThreads, 0, s>>>(b, off, cnt, lb);
 }
-void dp_launch_bnb_children(const uint32_t* lins, const int64_t* poff, const uint32_t* ub,
-                            const int64_t* uoff, const int32_t* pcnt, int64_t shared_m,
-                            const int64_t* lb, int32_t Bp, int32_t f, uint32_t* out,
-                            const int64_t* coff, int32_t* ccnt, int32_t P, cudaStream_t s) {
-  dp_bnb_children<<<P, kDpThreads, 0, s>>>(lins, poff, ub, uoff, pcnt, shared_m, lb, Bp, f, out,
-                                           coff, ccnt);
+namespace {
+inline unsigned flat_grid(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  return (unsigned)(b < 1 ? 1 : b);
 }
-void dp_launch_recheck_set(const uint32_t* hi, const uint32_t* lo, const int64_t* off,
-                           const int32_t* cnt, int32_t* rcnt, const int64_t* roff, int32_t* rlist,
-                           int32_t P, cudaStream_t s) {
-  dp_recheck_set<<<P, kDpThreads, 0, s>>>(hi, lo, off, cnt, rcnt, roff, rlist);
+}  // namespace
+
+void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t* act_off,
+                          const int64_t* pcap, const uint32_t* pub, const int64_t* lb, int32_t P,
+                          int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
+                          uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
+                          cudaStream_t s) {
+  dp_bnb_expand<<<flat_grid(total), 256, 0, s>>>(plins, shared_lins ? 1 : 0, act_off, pcap, pub,
+                                                 lb, P, Bp, f, ccap, clins, ca, cb, ccnt);
 }
-void dp_launch_gather(const uint32_t* lins, const int64_t* off, const int64_t* roff,
-                      const int32_t* rcnt, const int32_t* rlist, uint32_t* rlins, int32_t P,
-                      cudaStream_t s) {
-  dp_gather<<<P, 128, 0, s>>>(lins, off, roff, rcnt, rlist, rlins);
+void dp_launch_final_max(const int64_t* act_off, const int64_t* cap, const uint32_t* lo, int32_t P,
+                         int64_t total, uint32_t* Lmax, cudaStream_t s) {
+  dp_final_max<<<flat_grid(total), 256, 0, s>>>(act_off, cap, lo, P, Lmax);
 }
-void dp_launch_finalize(const uint32_t* lins, const uint32_t* hi, const uint32_t* lo,
-                        const int64_t* off, const int32_t* cnt, const uint32_t* ex,
-                        const int64_t* roff, const int32_t* rcnt, const int32_t* rlist,
-                        int32_t* res, int32_t P, cudaStream_t s) {
-  dp_finalize<<<P, kDpThreads, 0, s>>>(lins, hi, lo, off, cnt, ex, roff, rcnt, rlist, res);
+void dp_launch_final_split(const int64_t* act_off, const int64_t* cap, const uint32_t* lins,
+                           const uint32_t* hi, const uint32_t* lo, const uint32_t* Lmax, int32_t P,
+                           int64_t total, unsigned long long* best, uint32_t* rlins, int32_t* rcnt,
+                           cudaStream_t s) {
+  dp_final_split<<<flat_grid(total), 256, 0, s>>>(act_off, cap, lins, hi, lo, Lmax, P, best, rlins,
+                                                  rcnt);
+}
+void dp_launch_final_rechecked(const int64_t* act_off, const int32_t* rcnt, const uint32_t* rlins,
+                               const uint32_t* ex, int32_t P, int64_t total,
+                               unsigned long long* best, cudaStream_t s) {
+  dp_final_rechecked<<<flat_grid(total), 256, 0, s>>>(act_off, rcnt, rlins, ex, P, best);
+}
+void dp_launch_final_ties(const int64_t* act_off, const int64_t* cap, const uint32_t* hi,
+                          const uint32_t* lo, const int32_t* rcnt, const uint32_t* ex, int32_t P,
+                          int64_t total, const unsigned long long* best, int32_t* ties,
+                          cudaStream_t s) {
+  dp_final_ties<<<flat_grid(2 * total), 256, 0, s>>>(act_off, cap, hi, lo, rcnt, ex, P, best, ties);
 }
 
 }  // namespace rv

@@ -20,24 +20,29 @@ void dp_launch_dive_pick(const uint32_t* lins, const uint32_t* a, const int64_t*
 // lb[p] = max cnt_b of the list
 void dp_launch_max_lo(const uint32_t* b, const int64_t* off, const int32_t* cnt, int64_t* lb,
                       int32_t P, cudaStream_t s);
-// BnB children of parents with UB >= lb[p] (count pass: out == nullptr -> ccnt; write pass
-// at out + coff[p]); shared_m > 0: every problem's parents are the shared list lins[0..m)
-// with UBs at ub + p*shared_m
-void dp_launch_bnb_children(const uint32_t* lins, const int64_t* poff, const uint32_t* ub,
-                            const int64_t* uoff, const int32_t* pcnt, int64_t shared_m,
-                            const int64_t* lb, int32_t Bp, int32_t f, uint32_t* out,
-                            const int64_t* coff, int32_t* ccnt, int32_t P, cudaStream_t s);
-// finest level: recheck set (count pass rlist == nullptr -> rcnt; write pass: positions)
-void dp_launch_recheck_set(const uint32_t* hi, const uint32_t* lo, const int64_t* off,
-                           const int32_t* cnt, int32_t* rcnt, const int64_t* roff, int32_t* rlist,
-                           int32_t P, cudaStream_t s);
-void dp_launch_gather(const uint32_t* lins, const int64_t* off, const int64_t* roff,
-                      const int32_t* rcnt, const int32_t* rlist, uint32_t* rlins, int32_t P,
-                      cudaStream_t s);
-// res[3p..3p+2] = {winner lin, votes, n_tied}
-void dp_launch_finalize(const uint32_t* lins, const uint32_t* hi, const uint32_t* lo,
-                        const int64_t* off, const int32_t* cnt, const uint32_t* ex,
-                        const int64_t* roff, const int32_t* rcnt, const int32_t* rlist,
-                        int32_t* res, int32_t P, cudaStream_t s);
+// Flat list kernels (one thread per entry; entries of problem p: act_off[p]..act_off[p+1]
+// stored from cap[p]).  BnB expand: candidate children of parents with UB >= lb[p] into the
+// child region ccap[p] (ccnt zeroed by the caller; the children's count slots are zeroed).
+void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t* act_off,
+                          const int64_t* pcap, const uint32_t* pub, const int64_t* lb, int32_t P,
+                          int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
+                          uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
+                          cudaStream_t s);
+// finest level: Lmax[p] = max lo; split into exact-known (offered to best[p], a packed
+// (count << 32 | ~lin) max) and recheck lists (rlins at act_off[p], rcnt[p]); after the
+// exact recheck (counts ex, same layout as rlins) the rechecked offer theirs; ties counted.
+void dp_launch_final_max(const int64_t* act_off, const int64_t* cap, const uint32_t* lo, int32_t P,
+                         int64_t total, uint32_t* Lmax, cudaStream_t s);
+void dp_launch_final_split(const int64_t* act_off, const int64_t* cap, const uint32_t* lins,
+                           const uint32_t* hi, const uint32_t* lo, const uint32_t* Lmax, int32_t P,
+                           int64_t total, unsigned long long* best, uint32_t* rlins, int32_t* rcnt,
+                           cudaStream_t s);
+void dp_launch_final_rechecked(const int64_t* act_off, const int32_t* rcnt, const uint32_t* rlins,
+                               const uint32_t* ex, int32_t P, int64_t total,
+                               unsigned long long* best, cudaStream_t s);
+void dp_launch_final_ties(const int64_t* act_off, const int64_t* cap, const uint32_t* hi,
+                          const uint32_t* lo, const int32_t* rcnt, const uint32_t* ex, int32_t P,
+                          int64_t total, const unsigned long long* best, int32_t* ties,
+                          cudaStream_t s);
 
 }  // namespace rv

@@ -61,8 +61,14 @@ struct VoteSeg {
 
 // One thread block of work: blocks [cell0, cell0+ncell) of segment seg against
 // correspondences [i0, i0+ni) of it (i0, ni multiples of 4; rows >= n are zero padding).
+// ablk (K3-TC only): the item's block of the A-operand table (launch_vote_tc).
 struct VoteItem {
-  int32_t seg, cell0, ncell, i0, ni;
+  int32_t seg, cell0, ncell, i0, ni, ablk;
+};
+
+// K3-TC A-operand block: rows of cells [cell0, cell0+ncell) of segment seg (8 KB in the table).
+struct ABlock {
+  int32_t seg, cell0, ncell, pad;
 };
 
 // One problem of a refinement launch.
@@ -96,11 +102,15 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
                      int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s);
 
 // K3-TC: BOUND-mode vote on tcgen05 (items: ncell <= kTcM, i0/ni multiples of kTcN, koff
-// in table rows); final_mode: RV_MODE_FINAL counts at tau -/+ guard (items: ncell <= kTcM/2).  dump != nullptr writes the raw scores S' = s - t instead of counting
-// (test hook): dump[cell * dump_ld + correspondence].
-void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* items,
-                    int32_t n_items, float guard, float* dump, int64_t dump_ld, cudaStream_t s,
-                    bool final_mode = false);
+// in table rows); final_mode: RV_MODE_FINAL counts at tau -/+ guard (items: ncell <= kTcM/2).
+// Two launches: K2-TC writes the A-operand table (8 KB per ABlock, kTcABlockBytes) into
+// atab, then the persistent vote kernel (item.ablk selects its A block).  dump != nullptr
+// writes the raw scores S' = s - t instead of counting (test hook):
+// dump[cell * dump_ld + correspondence].
+constexpr int64_t kTcABlockBytes = 128 * 64;
+void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, int32_t n_ablocks,
+                    const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
+                    float* dump, int64_t dump_ld, cudaStream_t s, bool final_mode = false);
 
 // K4 (batched): level-0 reductions, one CTA per problem.  argmax: the dive's start index per
 // problem (planner key, see rv_plan_feed_l0_start).  survivors: outc != nullptr counts the

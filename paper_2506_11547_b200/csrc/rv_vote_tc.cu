@@ -12,13 +12,17 @@
 // (tcgen05.ld 32x32b: TMEM lane = cell, column = correspondence), so the SM's integer pipes do
 // one instruction per pair instead of the FP32 pipe's 9-FMA contraction.
 //
-// CTA roles: warp 0 lane 0 = TMA producer (one 16 KB cp.async.bulk per tile into a ring of
-// kTcStages), warp 1 = TMEM allocator + single-thread MMA issuer (2 x tcgen05.mma K=16 per
-// tile, accumulators double-buffered in 2 x 256 TMEM columns), warps 2..9 = epilogue: warp w
-// reads TMEM lanes 32*(w%4).. (its cells) and half of the tile's columns; the count runs
-// as independent chains split between the ALU pipe (LEA.HI) and the FMA pipe (IMAD.HI).
-// Completion flows through mbarriers: full[s] (TMA tx), empty[s] (tcgen05.commit),
-// tfull[b] (tcgen05.commit), tempty[b] (the 8 epilogue warps).
+// Two kernels per vote: K2-TC writes the A operand of every distinct block of <= 128 cells
+// (8 KB each, fp64 cell rotation + threshold, one thread per row; a block shared by several
+// problems -- the level-0 grid of a batch -- is built once), then the persistent vote kernel,
+// one CTA per SM looping over work items.  CTA roles: warp 0 lane 0 = TMA producer (per item
+// its A block into one of two A buffers, then one 16 KB cp.async.bulk per correspondence tile
+// into a ring of kTcStages), warp 1 = TMEM allocator + single-thread MMA issuer
+// (2 x tcgen05.mma K=16 per tile, accumulators double-buffered in 2 x 256 TMEM columns),
+// warps 2..9 = epilogue (warp w reads TMEM lanes 32*(w%4).. (its cells) and half of the
+// tile's columns and counts sign bits).
+// Completion flows through mbarriers: full[s] / afull[a] (TMA tx), empty[s] / aempty[a]
+// (tcgen05.commit), tfull[b] (tcgen05.commit), tempty[b] (the 8 epilogue warps).
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_fp16.h>
@@ -213,34 +217,88 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 #endif
 constexpr int kTcEpiWarps = RV_TC_EPI_WARPS;  // multiple of 4 (one lane quarter per SMSP)
 constexpr int kTcSplit = kTcEpiWarps / 4;     // warps sharing a lane quarter (column split)
+constexpr int kTcEpi0 = 2;                    // first epilogue warp
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, epilogue warps
 constexpr int kTcAccCols = kTcAcc * kTcN;  // = 512: the whole TMEM
 constexpr uint32_t kTileBytes = kTcN * 64;  // 16 KB at N = 256
 
 struct __align__(1024) TcSmem {
   uint8_t b[kTcStages][kTileBytes];  // correspondence tiles
-  uint8_t a[128 * 64];               // 128 cells x 32 fp16
-  uint64_t full[kTcStages], empty[kTcStages], tfull[kTcAcc], tempty[kTcAcc];
+  uint8_t a[2][128 * 64];            // A operand (128 rows x 32 fp16), double-buffered
+  uint64_t full[kTcStages], empty[kTcStages], tfull[kTcAcc], tempty[kTcAcc], afull[2], aempty[2];
   uint32_t tmem_base;
 };
 
+// K2-TC: the A operand of every ABlock -- per row (cell, or cell x threshold in FIN mode)
+// [phi_hi | phi_lo | phi_hi | -t_hi, -t_lo, -1, 0, 0] in the interleaved K-major layout, one
+// thread per row.  Rows past the block's cells are zero (they score 0 and are not counted).
+template <bool FIN>
+__global__ void __launch_bounds__(128) rv_tc_atab_kernel(const VoteSeg* __restrict__ segs,
+                                                         const ABlock* __restrict__ ablocks,
+                                                         float guard, uint8_t* __restrict__ atab) {
+  const ABlock ab = ablocks[blockIdx.x];
+  const VoteSeg& sg = segs[ab.seg];
+  const int m = threadIdx.x;  // A row
+  const int cell = FIN ? (m >> 1) : m;
+  __half v[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) v[c] = __float2half_rn(0.0f);
+  if (cell < ab.ncell) {
+    const uint32_t lin = sg.lins[ab.cell0 + cell];
+    int32_t i, j, k;
+    lin_to_ijk(lin, sg.B, i, j, k);
+    double q[4], f[9];
+    cell_quat(sg.B, i, j, k, q);
+    phi9(q, f);
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const __half h = __double2half(f[t]);
+      const __half l = __double2half(f[t] - (double)__half2float(h));
+      v[t] = h;
+      v[9 + t] = l;
+      v[18 + t] = h;
+    }
+    const double thr = FIN ? cos(sg.eps) + ((m & 1) ? guard : -guard)
+                           : bound_threshold(sg.B, i, j, k, sg.eps) - guard;
+    const __half th = __double2half(-thr);
+    const __half tl = __double2half(-thr - (double)__half2float(th));
+    v[27] = th;
+    v[28] = tl;
+    v[29] = __float2half_rn(-1.0f);
+  }
+  uint8_t* blk = atab + (int64_t)blockIdx.x * kTcABlockBytes;
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint4 w;
+    __half* hw = reinterpret_cast<__half*>(&w);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) hw[e] = v[ch * 8 + e];
+    *reinterpret_cast<uint4*>(blk + il_off(m, ch * 8)) = w;
+  }
+}
+
+// Persistent: CTA b processes items b, b + gridDim.x, ...; every role walks the same item
+// sequence, and the tile / accumulator / A-buffer rings run on across item boundaries, so the
+// prologue (TMEM allocation, barriers) is paid once per SM instead of once per item.
+//   warp 0 lane 0   TMA producer: per item its 8 KB A block (K2-TC table) into the free A
+//                   buffer, then one 16 KB cp.async.bulk per correspondence tile
+//   warp 1 lane 0   MMA issuer: 2 x tcgen05.mma K=16 per tile into accumulator gt % 2
+//   warps 2..9      epilogue: tcgen05.ld the accumulator, count sign bits, one atomic per
+//                   (cell, item)
 // FIN: RV_MODE_FINAL -- two A rows per cell (TMEM lanes 2c, 2c+1) carry the thresholds
-//      tau - g' (cnt_a) and tau + g' (cnt_b), so a CTA covers kTcM/2 cells.
+//      tau - g' (cnt_a) and tau + g' (cnt_b), so an item covers kTcM/2 cells.
 // ABL (ablation, tuning only): bit0 skip the count, bit1 skip the MMAs, bit2 skip the TMA
 template <bool DUMP, int ABL = 0, bool FIN = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    rv_vote_tc_kernel(const uint8_t* __restrict__ tab, const VoteSeg* __restrict__ segs,
-                      const VoteItem* __restrict__ items, float guard, float* dump,
-                      int64_t dump_ld) {
+    rv_vote_tc_kernel(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ atab,
+                      const VoteSeg* __restrict__ segs, const VoteItem* __restrict__ items,
+                      int32_t n_items, float guard, float* dump, int64_t dump_ld) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   TcSmem& sm = *reinterpret_cast<TcSmem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  const VoteItem it = items[blockIdx.x];
-  const VoteSeg& sg = segs[it.seg];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = it.ni / kTcN;  // it.i0, it.ni are multiples of kTcN
 
-  // ---- prologue: TMEM, barriers, the A operand ----
+  // ---- prologue (once per CTA): TMEM, barriers ----
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(&sm.tmem_base)),
@@ -256,50 +314,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       bar_init(&sm.tfull[b], 1);
       bar_init(&sm.tempty[b], kTcEpiWarps);
     }
+    for (int b = 0; b < 2; ++b) {
+      bar_init(&sm.afull[b], 1);
+      bar_init(&sm.aempty[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  // epilogue thread <-> TMEM lane <-> cell of the CTA
-  const int m = 32 * (warp & 3) + lane;
-  float init_f = 0.0f;
-  const int cell = FIN ? (m >> 1) : m;  // cell of TMEM lane / A row m
-  if (warp >= 2 && warp < 6) {  // one writer per A row
-    __half v[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) v[c] = __float2half_rn(0.0f);
-    if (cell < it.ncell) {
-      const uint32_t lin = sg.lins[it.cell0 + cell];
-      int32_t i, j, k;
-      lin_to_ijk(lin, sg.B, i, j, k);
-      double q[4], f[9];
-      cell_quat(sg.B, i, j, k, q);
-      phi9(q, f);
-#pragma unroll
-      for (int t = 0; t < 9; ++t) {
-        const __half h = __double2half(f[t]);
-        const __half l = __double2half(f[t] - (double)__half2float(h));
-        v[t] = h;
-        v[9 + t] = l;
-        v[18 + t] = h;
-      }
-      const double thr = FIN ? cos(sg.eps) + ((m & 1) ? guard : -guard)
-                             : bound_threshold(sg.B, i, j, k, sg.eps) - guard;
-      const __half th = __double2half(-thr);
-      const __half tl = __double2half(-thr - (double)__half2float(th));
-      v[27] = th;
-      v[28] = tl;
-      v[29] = __float2half_rn(-1.0f);
-      init_f = (float)(-thr);
-    }
-#pragma unroll
-    for (int ch = 0; ch < 4; ++ch) {
-      uint4 w;
-      __half* hw = reinterpret_cast<__half*>(&w);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) hw[e] = v[ch * 8 + e];
-      *reinterpret_cast<uint4*>(&sm.a[il_off(m, ch * 8)]) = w;
-    }
-    // generic-proxy smem writes -> visible to the tensor core (async proxy)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -309,93 +328,117 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const uint8_t* src = tab + (sg.koff + it.i0) * 64;
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t % kTcStages;
-        if (t >= kTcStages) bar_wait(&sm.empty[s], (uint32_t)(((t / kTcStages) - 1) & 1));
-        if (ABL & 4) {
-          bar_arrive(&sm.full[s]);
-        } else {
-          bar_expect_tx(&sm.full[s], kTileBytes);
-          bulk_g2s(sm.b[s], src + (int64_t)t * kTileBytes, kTileBytes, &sm.full[s]);
+      uint32_t gt = 0, gi = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
+        const VoteItem it = items[idx];
+        const uint32_t ab = gi & 1;
+        if (gi >= 2) bar_wait(&sm.aempty[ab], ((gi >> 1) - 1) & 1);
+        bar_expect_tx(&sm.afull[ab], (uint32_t)kTcABlockBytes);
+        bulk_g2s(sm.a[ab], atab + (int64_t)it.ablk * kTcABlockBytes, (uint32_t)kTcABlockBytes,
+                 &sm.afull[ab]);
+        const uint8_t* src = tab + (segs[it.seg].koff + it.i0) * 64;
+        const int ntiles = it.ni / kTcN;  // it.i0, it.ni are multiples of kTcN
+        for (int t = 0; t < ntiles; ++t, ++gt) {
+          const uint32_t s = gt % kTcStages;
+          if (gt >= (uint32_t)kTcStages) bar_wait(&sm.empty[s], ((gt / kTcStages) - 1) & 1);
+          if (ABL & 4) {
+            bar_arrive(&sm.full[s]);
+          } else {
+            bar_expect_tx(&sm.full[s], kTileBytes);
+            bulk_g2s(sm.b[s], src + (int64_t)t * kTileBytes, kTileBytes, &sm.full[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      const uint32_t a0 = su32(sm.a);
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t % kTcStages, b = t % kTcAcc;
-        bar_wait(&sm.full[s], (uint32_t)((t / kTcStages) & 1));
-        if (t >= kTcAcc) bar_wait(&sm.tempty[b], (uint32_t)(((t / kTcAcc) - 1) & 1));
-        tc_fence_after();
-        const uint32_t b0 = su32(sm.b[s]);
-        if (!(ABL & 2)) {
+      uint32_t gt = 0, gi = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
+        const int ntiles = items[idx].ni / kTcN;
+        const uint32_t ab = gi & 1;
+        bar_wait(&sm.afull[ab], (gi >> 1) & 1);
+        const uint32_t a0 = su32(sm.a[ab]);
+        for (int t = 0; t < ntiles; ++t, ++gt) {
+          const uint32_t s = gt % kTcStages, b = gt % kTcAcc;
+          bar_wait(&sm.full[s], (gt / kTcStages) & 1);
+          if (gt >= (uint32_t)kTcAcc) bar_wait(&sm.tempty[b], ((gt / kTcAcc) - 1) & 1);
+          tc_fence_after();
+          const uint32_t b0 = su32(sm.b[s]);
+          if (!(ABL & 2)) {
 #pragma unroll
-          for (int k = 0; k < 2; ++k)
-            mma_f16(tmem + (uint32_t)(b * kTcN), smem_desc(a0 + 256 * k, 128, 512),
-                    smem_desc(b0 + 256 * k, 128, 512), (uint32_t)k);
+            for (int k = 0; k < 2; ++k)
+              mma_f16(tmem + b * kTcN, smem_desc(a0 + 256 * k, 128, 512),
+                      smem_desc(b0 + 256 * k, 128, 512), (uint32_t)k);
+          }
+          mma_commit(&sm.empty[s]);  // smem slot free once these MMAs completed
+          mma_commit(&sm.tfull[b]);  // accumulator b ready
         }
-        mma_commit(&sm.empty[s]);  // smem slot free once these MMAs completed
-        mma_commit(&sm.tfull[b]);  // accumulator b ready
+        mma_commit(&sm.aempty[ab]);  // A buffer free once the item's MMAs completed
       }
     }
   } else {
     // ---------------- epilogue: count sign bits (warps 2..9) ----------------
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-    const int half = (warp - 2) >> 2;          // which 1/kTcSplit of the tile's columns
+    const int half = (warp - kTcEpi0) >> 2;     // which 1/kTcSplit of the tile's columns
+    const int m = 32 * (warp & 3) + lane;       // TMEM lane = A row
+    const int cell = FIN ? (m >> 1) : m;
     const uint32_t two = guard > -1.0f ? 2u : 3u;  // a runtime 2 (keeps IMAD.HI)
-    uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, n4 = 0, n5 = 0, n6 = 0, n7 = 0;
     constexpr int kLd = kTcN / kTcSplit / 32;  // tcgen05.ld x32 per warp per tile
-    for (int t = 0; t < ntiles; ++t) {
-      const int b = t % kTcAcc;
-      bar_wait(&sm.tfull[b], (uint32_t)((t / kTcAcc) & 1));
-      tc_fence_after();
-      // this warp's half of accumulator b -> registers, then hand the buffer back to the MMA
-      // issuer before counting (the count overlaps the next MMAs)
-      const int col0 = half * (kTcN / kTcSplit);
-      uint32_t r[kLd][32];
+    const int col0 = half * (kTcN / kTcSplit);
+    uint32_t gt = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      const VoteItem it = items[idx];
+      const int ntiles = it.ni / kTcN;
+      uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, n4 = 0, n5 = 0, n6 = 0, n7 = 0;
+      for (int t = 0; t < ntiles; ++t, ++gt) {
+        const uint32_t b = gt % kTcAcc;
+        bar_wait(&sm.tfull[b], (gt / kTcAcc) & 1);
+        tc_fence_after();
+        // this warp's part of accumulator b -> registers, then hand the buffer back to the
+        // MMA issuer before counting (the count overlaps the next MMAs)
+        uint32_t r[kLd][32];
 #pragma unroll
-      for (int q = 0; q < kLd; ++q) RV_LD32(r[q], lane_addr + (uint32_t)(b * kTcN + col0 + 32 * q));
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) bar_arrive(&sm.tempty[b]);
-      if (ABL & 1) {
-        n0 += r[0][0] ^ r[kLd - 1][31];
-      } else if (DUMP) {
-        if (cell < it.ncell) {
-          float* drow = dump + (int64_t)(it.cell0 + cell) * dump_ld + it.i0 + (int64_t)t * kTcN + col0;
+        for (int q = 0; q < kLd; ++q) RV_LD32(r[q], lane_addr + (uint32_t)(b * kTcN + col0 + 32 * q));
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(&sm.tempty[b]);
+        if (ABL & 1) {
+          n0 += r[0][0] ^ r[kLd - 1][31];
+        } else if (DUMP) {
+          if (cell < it.ncell) {
+            float* drow = dump + (int64_t)(it.cell0 + cell) * dump_ld + it.i0 + (int64_t)t * kTcN + col0;
+#pragma unroll
+            for (int q = 0; q < kLd; ++q)
+#pragma unroll
+              for (int e = 0; e < 32; ++e) drow[32 * q + e] = __uint_as_float(r[q][e]);
+          }
+        } else {
 #pragma unroll
           for (int q = 0; q < kLd; ++q)
 #pragma unroll
-            for (int e = 0; e < 32; ++e) drow[32 * q + e] = __uint_as_float(r[q][e]);
+            for (int e = 0; e < 32; e += 8) {
+              add_sign_alu(n0, r[q][e]);
+              add_sign_fma(n1, r[q][e + 1], two);
+              add_sign_alu(n2, r[q][e + 2]);
+              add_sign_fma(n3, r[q][e + 3], two);
+              add_sign_alu(n4, r[q][e + 4]);
+              add_sign_fma(n5, r[q][e + 5], two);
+              add_sign_alu(n6, r[q][e + 6]);
+              add_sign_fma(n7, r[q][e + 7], two);
+            }
         }
-      } else {
-#pragma unroll
-        for (int q = 0; q < kLd; ++q)
-#pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            add_sign_alu(n0, r[q][e]);
-            add_sign_fma(n1, r[q][e + 1], two);
-            add_sign_alu(n2, r[q][e + 2]);
-            add_sign_fma(n3, r[q][e + 3], two);
-            add_sign_alu(n4, r[q][e + 4]);
-            add_sign_fma(n5, r[q][e + 5], two);
-            add_sign_alu(n6, r[q][e + 6]);
-            add_sign_fma(n7, r[q][e + 7], two);
-          }
+      }
+      if (!DUMP && cell < it.ncell) {
+        // rows of the chunk: real correspondences score phi.k - t; padding rows score -1
+        const VoteSeg& sg = segs[it.seg];
+        const uint32_t neg = (n0 + n1) + (n2 + n3) + (n4 + n5) + (n6 + n7);
+        const uint32_t cnt = (uint32_t)(it.ni / kTcSplit) - neg;  // its share of the columns
+        atomicAdd(FIN && (m & 1) ? &sg.cnt_b[it.cell0 + cell] : &sg.cnt_a[it.cell0 + cell], cnt);
       }
     }
-    if (!DUMP && cell < it.ncell) {
-      // rows of the chunk: real correspondences score phi.k - t; padding rows score -1
-      const uint32_t neg = (n0 + n1) + (n2 + n3) + (n4 + n5) + (n6 + n7);
-      const uint32_t cnt = (uint32_t)(it.ni / kTcSplit) - neg;  // its share of the columns
-      atomicAdd(FIN && (m & 1) ? &sg.cnt_b[it.cell0 + cell] : &sg.cnt_a[it.cell0 + cell], cnt);
-    }
   }
-  (void)init_f;
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -407,10 +450,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 size_t tc_smem_bytes() { return sizeof(TcSmem) + 1024; }
 
-void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* items,
-                    int32_t n_items, float guard, float* dump, int64_t dump_ld, cudaStream_t s,
-                    bool final_mode) {
-  if (n_items <= 0) return;
+void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, int32_t n_ablocks,
+                    const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
+                    float* dump, int64_t dump_ld, cudaStream_t s, bool final_mode) {
+  if (n_items <= 0 || n_ablocks <= 0) return;
+  if (final_mode)
+    rv_tc_atab_kernel<true><<<n_ablocks, 128, 0, s>>>(segs, ablocks, guard, atab);
+  else
+    rv_tc_atab_kernel<false><<<n_ablocks, 128, 0, s>>>(segs, ablocks, guard, atab);
+  static int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  const int grid = n_items < sms ? n_items : sms;  // persistent: one CTA per SM
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(rv_vote_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -422,8 +476,8 @@ void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* ite
     attr = true;
   }
   if (final_mode) {
-    rv_vote_tc_kernel<false, 0, true><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(
-        tab, segs, items, guard, nullptr, 0);
+    rv_vote_tc_kernel<false, 0, true><<<grid, kTcThreads, tc_smem_bytes(), s>>>(
+        tab, atab, segs, items, n_items, guard, nullptr, 0);
     return;
   }
   static const int abl = [] {
@@ -431,22 +485,22 @@ void launch_vote_tc(const uint8_t* tab, const VoteSeg* segs, const VoteItem* ite
     return e ? atoi(e) : 0;
   }();
   if (dump)
-    rv_vote_tc_kernel<true><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(tab, segs, items, guard,
-                                                                         dump, dump_ld);
+    rv_vote_tc_kernel<true><<<grid, kTcThreads, tc_smem_bytes(), s>>>(tab, atab, segs, items,
+                                                                         n_items, guard, dump, dump_ld);
   else if (abl != 0) {
 #define RV_ABL_CASE(A)                                                                           \
   case A:                                                                                        \
     cudaFuncSetAttribute(rv_vote_tc_kernel<false, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          (int)tc_smem_bytes());                                                  \
-    rv_vote_tc_kernel<false, A><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(tab, segs, items,   \
-                                                                             guard, nullptr, 0); \
+    rv_vote_tc_kernel<false, A><<<grid, kTcThreads, tc_smem_bytes(), s>>>(tab, atab, segs, items, \
+                                                                 n_items, guard, nullptr, 0);    \
     break;
     switch (abl) { RV_ABL_CASE(1) RV_ABL_CASE(2) RV_ABL_CASE(3) RV_ABL_CASE(4) RV_ABL_CASE(5)
                    RV_ABL_CASE(6) RV_ABL_CASE(7) default: break; }
 #undef RV_ABL_CASE
   } else
-    rv_vote_tc_kernel<false><<<n_items, kTcThreads, tc_smem_bytes(), s>>>(tab, segs, items,
-                                                                          guard, nullptr, 0);
+    rv_vote_tc_kernel<false><<<grid, kTcThreads, tc_smem_bytes(), s>>>(tab, atab, segs, items,
+                                                                          n_items, guard, nullptr, 0);
 }
 
 }  // namespace rv

@@ -257,7 +257,11 @@ class RotVote:
                                                    C.byref(r), mp))
         return Result.from_c(r)
 
-    def solve_batched(self, x, y, offsets, eps: float, levels: int = 0, masks=None) -> list:
+    def solve_batched(self, x, y, offsets, eps: float, levels: int = 0, masks=None,
+                      raw: bool = False):
+        """P independent problems (rows offsets[p]..offsets[p+1] of x / y).  Returns a list of
+        Result, or with raw=True the rv_result array itself as a numpy structured array
+        (fields as in include/rotvote.h; no per-problem Python objects)."""
         import torch
         offs = np.ascontiguousarray(offsets, np.int64)
         P = offs.size - 1
@@ -266,6 +270,8 @@ class RotVote:
         _check(self.ctx, lib().rot_vote_solve_batched(
             self.ctx, _dptr(x, torch.float32, "x"), _dptr(y, torch.float32, "y"),
             offs.ctypes.data, P, float(eps), int(levels), out, mp))
+        if raw:
+            return np.ctypeslib.as_array(out)
         return [Result.from_c(out[p]) for p in range(P)]
 
     # -- individual steps (parity tests) --
