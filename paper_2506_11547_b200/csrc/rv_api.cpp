@@ -201,6 +201,31 @@ struct rv_ctx {
   DevBuf<int32_t> dp_cnt[2], dp_rcnt, dp_ties;
   DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex, dp_lmax;
   DevBuf<unsigned long long> dp_best;
+  DevBuf<int64_t> dp_ioff, dp_aoff, dp_tot;
+  DevBuf<int32_t> dp_icnt, dp_phase;
+  // event pairs around the batched vote launches (read after the final sync)
+  std::vector<cudaEvent_t> evs;
+  size_t evn = 0;
+  void ev_reset() { evn = 0; }
+  cudaError_t ev_pair(cudaEvent_t* a, cudaEvent_t* b) {
+    while (evs.size() < evn + 2) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return r;
+      evs.push_back(e);
+    }
+    *a = evs[evn];
+    *b = evs[evn + 1];
+    evn += 2;
+    return cudaSuccess;
+  }
+  void ev_collect() {
+    for (size_t i = 0; i + 1 < evn; i += 2) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, evs[i], evs[i + 1]) == cudaSuccess) vote_ms += ms;
+    }
+    evn = 0;
+  }
   DevBuf<int32_t> l0surv;        // host-planner batched path: level-0 survivor indices
   DevBuf<uint8_t> atab;          // K3-TC A-operand blocks (K2-TC)
   DevBuf<rv::ABlock> ablk;
@@ -988,18 +1013,6 @@ int vote_lists(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   return RV_OK;
 }
 
-// D2H of PL per-problem counts through the pinned staging, then a stream sync.
-int read_counts(rv_ctx* ctx, const int32_t* dcnt, int32_t PL, std::vector<int32_t>& h) {
-  RV_CUDA(ctx->down.ensure((size_t)PL * 4 + 256), "allocating staging");
-  ctx->down.reset();
-  int32_t* hc = ctx->down.take<int32_t>(PL);
-  RV_CUDA(cudaMemcpyAsync(hc, dcnt, (size_t)PL * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-  RV_CUDA(cudaStreamSynchronize(ctx->stream), "batched level");
-  ctx->collect_vote_ms();
-  h.assign(hc, hc + PL);
-  return RV_OK;
-}
-
 // true when the device level loop applies: >= 2 levels and a cached level-0 background
 bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps) {
   if (levels_eff < 2) return false;
@@ -1009,8 +1022,59 @@ bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps) {
   return rv_plan_l0_background(B0, eps, &mbg) != nullptr && mbg > 0;
 }
 
+// Vote one level of per-problem device lists (rv::DpList).  K3-TC and K5: the items are
+// built on the device (dp_launch_items) and the kernels read their counts there -- no host
+// round trip.  FP32 K3 (tensor_vote = 0): the counts and bases are read back and the items
+// built on the host (vote_lists).  The caller has zeroed the count slots.
+int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
+               const std::vector<int64_t>& koff, double eps, int32_t mode, int32_t B,
+               const rv::DpList& Ld, int32_t PL, int64_t entries_bound, int64_t nmax) {
+  cudaStream_t s = ctx->stream;
+  if (ctx->tc_on || mode == RV_MODE_EXACT) {
+    const int im = mode == RV_MODE_EXACT ? 2 : mode == RV_MODE_FINAL ? 1 : 0;
+    int64_t mi = 0, ma = 0;
+    rv::dp_items_bound(im, entries_bound, PL, nmax, ctx->num_sms, &mi, &ma);
+    RV_CUDA(ctx->vsegs.ensure(PL), "allocating segments");
+    RV_CUDA(ctx->vitems.ensure(mi), "allocating items");
+    RV_CUDA(ctx->ablk.ensure(ma), "allocating A blocks");
+    if (im != 2) RV_CUDA(ctx->atab.ensure(ma * (size_t)rv::kTcABlockBytes), "allocating A table");
+    RV_CUDA(ctx->dp_ioff.ensure(PL + 1), "allocating");
+    RV_CUDA(ctx->dp_aoff.ensure(PL + 1), "allocating");
+    RV_CUDA(ctx->dp_icnt.ensure(4), "allocating");
+    rv::dp_launch_items(Ld, ctx->rows.p, im == 2 ? ctx->koffs.p : ctx->toffs.p, PL, B, eps, im,
+                        ctx->num_sms, ctx->vsegs.p, ctx->dp_ioff.p, ctx->dp_aoff.p, ctx->dp_icnt.p,
+                        ctx->vitems.p, ctx->ablk.p, s);
+    ctx->launches += 2;
+    if (im == 2) {
+      rv::launch_exact(ctx->k9.p, ctx->stride, x, y, ctx->vsegs.p, ctx->vitems.p, 0,
+                       ctx->cfg.guard, s, ctx->dp_icnt.p);
+      ctx->launches += 1;
+    } else {
+      cudaEvent_t e0, e1;
+      RV_CUDA(ctx->ev_pair(&e0, &e1), "event");
+      RV_CUDA(cudaEventRecord(e0, s), "event");
+      rv::launch_vote_tc(ctx->tctab.p, ctx->atab.p, ctx->ablk.p, 0, ctx->vsegs.p, ctx->vitems.p, 0,
+                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, im == 1, ctx->dp_icnt.p);
+      RV_CUDA(cudaEventRecord(e1, s), "event");
+      ctx->launches += 2;
+      ctx->vote_launches += 1;
+    }
+    RV_CUDA(cudaGetLastError(), "launching a batched vote");
+    return RV_OK;
+  }
+  // FP32 path: host-built items from the read-back counts
+  std::vector<int32_t> hcnt(PL);
+  std::vector<int64_t> hoff(PL + 1);
+  RV_CUDA(cudaMemcpyAsync(hcnt.data(), Ld.cnt, PL * 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hoff.data(), Ld.base, (PL + 1) * 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "batched level");
+  ctx->collect_vote_ms();
+  return vote_lists(ctx, x, y, rows, koff, eps, mode, B, Ld.lins, hoff, hcnt, 0, Ld.ca, Ld.cb);
+}
+
 // The certified search of rv_plan.cpp for PL problems at once, every decision on the device
-// (rv_dplan.cu); the host reads back one count array per level to size the next launch.
+// (rv_dplan.cu).  Host round trips: one per branch-and-bound level (the size of the next
+// child region) and one at the end; with K3-TC the items are built on the device.
 // ch = the `levels` resolutions searched (ch.size() >= 2).  Fills res[p].
 int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
                         const std::vector<int64_t>& rows, const std::vector<int64_t>& koff,
@@ -1018,7 +1082,19 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
                         std::vector<rv_plan_result>& res, Trace& tr) {
   const int L = (int)ch.size();
   cudaStream_t s = ctx->stream;
-  std::vector<std::vector<int32_t>> phases;  // per phase: blocks per problem
+  int64_t nmax = 0;
+  for (int32_t p = 0; p < PL; ++p) nmax = std::max<int64_t>(nmax, rows[p + 1] - rows[p]);
+  // per-phase block counts, kept on the device and read once at the end
+  const int max_ph = 2 * L + 1;
+  RV_CUDA(ctx->dp_phase.ensure((size_t)max_ph * PL), "allocating");
+  int nph = 0;
+  auto keep_phase = [&](const int32_t* dcnt) -> int {
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_phase.p + (size_t)nph * PL, dcnt, PL * 4,
+                            cudaMemcpyDeviceToDevice, s), "D2D");
+    ++nph;
+    return RV_OK;
+  };
+  ctx->ev_reset();
   // ---- level 0: every problem votes the full candidate grid; counts stay on the device
   const int32_t B0 = ch[0];
   const int64_t m0 = rv_grid_candidates(B0, nullptr, 0);
@@ -1038,7 +1114,19 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     ctx->l0bg_B = B0;
     ctx->l0bg_eps = eps;
   }
-  {
+  if (ctx->grid_list_B != B0 || ctx->grid_list_m != m0) {
+    RV_CUDA(ctx->grid_list.ensure(m0), "allocating grid list");
+    RV_CUDA(cudaMemcpy(ctx->grid_list.p, ctx->grid_host.data(), m0 * 4, cudaMemcpyHostToDevice),
+            "H2D grid");
+    ctx->grid_list_B = B0;
+    ctx->grid_list_m = m0;
+  }
+  if (ctx->tc_on) {
+    RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, (size_t)PL * m0 * 4, s), "memset");
+    const rv::DpList l0{ctx->grid_list.p, 1, m0, nullptr, nullptr, ctx->l0cnt.p, ctx->l0cnt.p};
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, PL * m0, nmax))
+      return rc;
+  } else {
     std::vector<BatchReq> g0(PL);
     for (int32_t p = 0; p < PL; ++p) g0[p] = {p, B0, RV_MODE_BOUND, m0, ctx->grid_host.data(), true};
     std::vector<std::vector<uint32_t>> unused;
@@ -1046,7 +1134,6 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
                             ctx->l0cnt.p))
       return rc;
   }
-  phases.emplace_back(PL, (int32_t)m0);
   RV_CUDA(ctx->l0idx.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_pick.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_lb.ensure(PL), "allocating");
@@ -1054,8 +1141,7 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
                        ctx->l0idx.p, s);
   ctx->launches += 1;
   tr.mark("  level 0");
-  std::vector<int32_t> hcnt;
-  std::vector<int64_t> hoff(PL + 1);
+  std::vector<int64_t> hbase(PL + 1);
   // ---- dive: the 27-neighbourhood of the pick, level by level; lb* at the finest level
   for (int l = 1; l < L; ++l) {
     const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1], cap = 27 * f * f * f;
@@ -1065,16 +1151,19 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     RV_CUDA(ctx->dp_cb[0].ensure(span), "allocating");
     RV_CUDA(ctx->dp_cnt[0].ensure(PL), "allocating");
     RV_CUDA(ctx->dp_off[0].ensure(PL + 1), "allocating");
+    for (int32_t p = 0; p <= PL; ++p) hbase[p] = (int64_t)p * cap;
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_off[0].p, hbase.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+            "H2D");
     rv::dp_launch_dive_children(ctx->dp_pick.p, ctx->l0idx.p, l == 1 ? ctx->grid_list.p : nullptr,
                                 Bp, f, ctx->dp_lins[0].p, cap, ctx->dp_cnt[0].p, PL, s);
-    ctx->launches += 1;
-    if (int rc = read_counts(ctx, ctx->dp_cnt[0].p, PL, hcnt)) return rc;
-    for (int32_t p = 0; p <= PL; ++p) hoff[p] = (int64_t)p * cap;
-    RV_CUDA(cudaMemcpyAsync(ctx->dp_off[0].p, hoff.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
-            "H2D");
     const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
-    if (int rc = vote_lists(ctx, x, y, rows, koff, eps, mode, ch[l], ctx->dp_lins[0].p, hoff, hcnt,
-                            (int64_t)span, ctx->dp_ca[0].p, ctx->dp_cb[0].p))
+    RV_CUDA(cudaMemsetAsync(ctx->dp_ca[0].p, 0, span * 4, s), "memset");
+    if (mode == RV_MODE_FINAL) RV_CUDA(cudaMemsetAsync(ctx->dp_cb[0].p, 0, span * 4, s), "memset");
+    ctx->launches += 1;
+    if (int rc = keep_phase(ctx->dp_cnt[0].p)) return rc;
+    const rv::DpList dl{ctx->dp_lins[0].p, 0, 0, ctx->dp_off[0].p, ctx->dp_cnt[0].p,
+                        ctx->dp_ca[0].p, ctx->dp_cb[0].p};
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], dl, PL, (int64_t)span, nmax))
       return rc;
     if (mode == RV_MODE_BOUND)
       rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, ctx->dp_off[0].p,
@@ -1082,50 +1171,70 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     else
       rv::dp_launch_max_lo(ctx->dp_cb[0].p, ctx->dp_off[0].p, ctx->dp_cnt[0].p, ctx->dp_lb.p, PL, s);
     ctx->launches += 1;
-    phases.push_back(hcnt);
     tr.mark("  dive level");
   }
-  // ---- branch and bound from the level-0 survivors (UB >= lb*).  A level's list of problem
-  // p has pact[p+1] - pact[p] entries stored from pcap[p]; its children get the capacity
-  // region (parents x f^3) starting at pact[p] * f^3.
-  std::vector<int64_t> pact(PL + 1);
-  for (int32_t p = 0; p <= PL; ++p) pact[p] = (int64_t)p * m0;  // the shared grid: act == cap
+  // ---- branch and bound from the level-0 survivors (UB >= lb*).  A list of problem p has
+  // act[p+1] - act[p] entries stored from base[p]; its children get the capacity region
+  // act[p] * f^3 .. act[p+1] * f^3 (parents x f^3).
+  RV_CUDA(ctx->dp_act.ensure(PL + 1), "allocating");
+  RV_CUDA(ctx->dp_tot.ensure(1), "allocating");
+  RV_CUDA(ctx->down.ensure(256), "allocating staging");
+  for (int32_t p = 0; p <= PL; ++p) hbase[p] = (int64_t)p * m0;  // level 0: act == base
+  RV_CUDA(cudaMemcpyAsync(ctx->dp_act.p, hbase.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+          "H2D");
+  int64_t ptotal = (int64_t)PL * m0;
   const uint32_t* plins = ctx->grid_list.p;
   const uint32_t* pub = ctx->l0cnt.p;
   bool shared = true;
   int cur = -1;
-  RV_CUDA(ctx->dp_act.ensure(PL + 1), "allocating");
+  {
+    // children base of BnB level 1: act * f^3
+    const int32_t f = ch[1] / ch[0];
+    const int64_t f3 = (int64_t)f * f * f;
+    RV_CUDA(ctx->dp_off[1].ensure(PL + 1), "allocating");
+    for (int32_t p = 0; p <= PL; ++p) hbase[p] = (int64_t)p * m0 * f3;
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_off[1].p, hbase.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+            "H2D");
+  }
   for (int l = 1; l < L; ++l) {
-    const int nb = cur == 0 ? 1 : 0;
+    const int nb = cur == 1 ? 0 : 1;  // level 1 -> set 1 (set 0 still holds the dive lists)
     const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1];
     const int64_t f3 = (int64_t)f * f * f;
-    std::vector<int64_t> ccap(PL + 1);
-    for (int32_t p = 0; p <= PL; ++p) ccap[p] = pact[p] * f3;
-    const int64_t cap_total = std::max<int64_t>(1, ccap[PL]);
+    const int64_t cap_total = std::max<int64_t>(1, ptotal * f3);
     RV_CUDA(ctx->dp_lins[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_ca[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_cb[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_cnt[nb].ensure(PL), "allocating");
-    RV_CUDA(ctx->dp_off[nb].ensure(PL + 1), "allocating");
-    RV_CUDA(cudaMemcpyAsync(ctx->dp_act.p, pact.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
-            "H2D");
-    RV_CUDA(cudaMemcpyAsync(ctx->dp_off[nb].p, ccap.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
-            "H2D");
     RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
+    // dp_off[nb] = the children's base (written by the previous scan, or above for level 1)
     rv::dp_launch_bnb_expand(plins, shared, ctx->dp_act.p, shared ? ctx->dp_act.p : ctx->dp_off[cur].p,
-                             pub, ctx->dp_lb.p, PL, pact[PL], Bp, f, ctx->dp_off[nb].p,
+                             pub, ctx->dp_lb.p, PL, ptotal, Bp, f, ctx->dp_off[nb].p,
                              ctx->dp_lins[nb].p, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p,
                              ctx->dp_cnt[nb].p, s);
-    ctx->launches += 1;
-    if (int rc = read_counts(ctx, ctx->dp_cnt[nb].p, PL, hcnt)) return rc;
+    if (int rc = keep_phase(ctx->dp_cnt[nb].p)) return rc;
+    // the children's act offsets, and the grandchildren's base (into the other set's dp_off)
+    const int other = nb == 0 ? 1 : 0;
+    int64_t nf3 = 1;
+    if (l + 1 < L) {
+      const int64_t nf = ch[l + 1] / ch[l];
+      nf3 = nf * nf * nf;
+    }
+    RV_CUDA(ctx->dp_off[other].ensure(PL + 1), "allocating");
+    rv::dp_launch_scan(ctx->dp_cnt[nb].p, PL, nf3, ctx->dp_act.p, ctx->dp_off[other].p,
+                       ctx->dp_tot.p, s);
+    ctx->launches += 2;
+    ctx->down.reset();
+    int64_t* ht = ctx->down.take<int64_t>(1);
+    RV_CUDA(cudaMemcpyAsync(ht, ctx->dp_tot.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    RV_CUDA(cudaStreamSynchronize(s), "batched level");
+    ctx->collect_vote_ms();
+    const int64_t ctotal = *ht;
     const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
-    // the expand kernel zeroed the count slots: no clear (span 0)
-    if (int rc = vote_lists(ctx, x, y, rows, koff, eps, mode, ch[l], ctx->dp_lins[nb].p, ccap, hcnt,
-                            0, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p))
+    const rv::DpList cl{ctx->dp_lins[nb].p, 0, 0, ctx->dp_off[nb].p, ctx->dp_cnt[nb].p,
+                        ctx->dp_ca[nb].p, ctx->dp_cb[nb].p};
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], cl, PL, ctotal, nmax))
       return rc;
-    phases.push_back(hcnt);
-    pact[0] = 0;
-    for (int32_t p = 0; p < PL; ++p) pact[p + 1] = pact[p] + hcnt[p];
+    ptotal = ctotal;
     plins = ctx->dp_lins[nb].p;
     pub = ctx->dp_ca[nb].p;
     shared = false;
@@ -1133,7 +1242,8 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     tr.mark("  bnb level");
   }
   // ---- finest level: max lo, exact-known blocks, recheck of hi >= max lo, hi != lo; winner
-  const int64_t ftotal = pact[PL];
+  // (dp_act holds the final list's act offsets from the last scan; its base is dp_off[cur])
+  const int64_t ftotal = ptotal;
   const uint32_t* flins = ctx->dp_lins[cur].p;
   const uint32_t* fhi = ctx->dp_ca[cur].p;
   const uint32_t* flo = ctx->dp_cb[cur].p;
@@ -1144,45 +1254,44 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   RV_CUDA(ctx->dp_ties.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_rlins.ensure(std::max<int64_t>(1, ftotal)), "allocating");
   RV_CUDA(ctx->dp_ex.ensure(std::max<int64_t>(1, ftotal)), "allocating");
-  RV_CUDA(cudaMemcpyAsync(ctx->dp_act.p, pact.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
-          "H2D");
   RV_CUDA(cudaMemsetAsync(ctx->dp_rcnt.p, 0, PL * 4, s), "memset");
   RV_CUDA(cudaMemsetAsync(ctx->dp_lmax.p, 0, PL * 4, s), "memset");
   RV_CUDA(cudaMemsetAsync(ctx->dp_best.p, 0, PL * 8, s), "memset");
   RV_CUDA(cudaMemsetAsync(ctx->dp_ties.p, 0, PL * 4, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_ex.p, 0, std::max<int64_t>(1, ftotal) * 4, s), "memset");
   rv::dp_launch_final_max(ctx->dp_act.p, fcap, flo, PL, ftotal, ctx->dp_lmax.p, s);
   rv::dp_launch_final_split(ctx->dp_act.p, fcap, flins, fhi, flo, ctx->dp_lmax.p, PL, ftotal,
                             ctx->dp_best.p, ctx->dp_rlins.p, ctx->dp_rcnt.p, s);
   ctx->launches += 2;
-  std::vector<int32_t> rcnt;
-  if (int rc = read_counts(ctx, ctx->dp_rcnt.p, PL, rcnt)) return rc;
-  int64_t rtotal = 0;
-  for (int32_t p = 0; p < PL; ++p) rtotal += rcnt[p];
-  if (rtotal > 0) {
-    if (int rc = vote_lists(ctx, x, y, rows, koff, eps, RV_MODE_EXACT, ch[L - 1], ctx->dp_rlins.p,
-                            pact, rcnt, std::max<int64_t>(1, ftotal), ctx->dp_ex.p, ctx->dp_ex.p))
-      return rc;
-    rv::dp_launch_final_rechecked(ctx->dp_act.p, ctx->dp_rcnt.p, ctx->dp_rlins.p, ctx->dp_ex.p, PL,
-                                  ftotal, ctx->dp_best.p, s);
-    ctx->launches += 1;
-    phases.push_back(rcnt);
-  }
+  if (int rc = keep_phase(ctx->dp_rcnt.p)) return rc;
+  const rv::DpList rl{ctx->dp_rlins.p, 0, 0, ctx->dp_act.p, ctx->dp_rcnt.p, ctx->dp_ex.p,
+                      ctx->dp_ex.p};
+  if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_EXACT, ch[L - 1], rl, PL, ftotal,
+                          nmax))
+    return rc;
+  rv::dp_launch_final_rechecked(ctx->dp_act.p, ctx->dp_rcnt.p, ctx->dp_rlins.p, ctx->dp_ex.p, PL,
+                                ftotal, ctx->dp_best.p, s);
   rv::dp_launch_final_ties(ctx->dp_act.p, fcap, fhi, flo, ctx->dp_rcnt.p, ctx->dp_ex.p, PL, ftotal,
                            ctx->dp_best.p, ctx->dp_ties.p, s);
-  ctx->launches += 1;
+  ctx->launches += 2;
   RV_CUDA(cudaGetLastError(), "launching the level loop");
-  RV_CUDA(ctx->down.ensure((size_t)PL * 24 + 512), "allocating staging");
+  RV_CUDA(ctx->down.ensure((size_t)PL * 24 + (size_t)nph * PL * 4 + 1024), "allocating staging");
   ctx->down.reset();
   unsigned long long* hbest = ctx->down.take<unsigned long long>(PL);
   int32_t* hties = ctx->down.take<int32_t>(PL);
   int64_t* hlb = ctx->down.take<int64_t>(PL);
+  int32_t* hph = ctx->down.take<int32_t>((size_t)nph * PL);
   RV_CUDA(cudaMemcpyAsync(hbest, ctx->dp_best.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hties, ctx->dp_ties.p, 4 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hlb, ctx->dp_lb.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hph, ctx->dp_phase.p, 4 * (size_t)nph * PL, cudaMemcpyDeviceToHost, s),
+          "D2H");
   RV_CUDA(cudaStreamSynchronize(s), "batched finalize");
   ctx->collect_vote_ms();
+  ctx->ev_collect();
   tr.mark("  finalize");
   res.assign(PL, rv_plan_result{});
+  uint64_t tc_pairs = 0;
   for (int32_t p = 0; p < PL; ++p) {
     rv_plan_result& r = res[p];
     const uint64_t n = (uint64_t)(rows[p + 1] - rows[p]);
@@ -1191,15 +1300,20 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     r.B = ch[L - 1];
     r.n_tied = hties[p];
     r.lb_star = (uint32_t)hlb[p];
-    r.n_rechecked = rcnt[p];
-    for (size_t ph = 0; ph < phases.size(); ++ph) {
-      const int64_t c = phases[ph][p];
-      if (ph + 1 == phases.size() && rtotal > 0 && rcnt[p] == 0) break;  // no recheck phase
+    const int32_t nre = hph[(size_t)(nph - 1) * PL + p];
+    r.n_rechecked = nre;
+    // phases: level 0, the dive, BnB, and the recheck when non-empty
+    auto add = [&](int64_t c) {
       r.pair_votes += (uint64_t)c * n;
       r.cells_evaluated += (uint64_t)c;
       if (r.n_phases < 16) r.cells_per_phase[r.n_phases++] = c;
-    }
+    };
+    add(m0);
+    for (int ph = 0; ph + 1 < nph; ++ph) add(hph[(size_t)ph * PL + p]);
+    if (nre > 0) add(nre);
+    tc_pairs += (r.pair_votes - (uint64_t)nre * n);
   }
+  if (ctx->tc_on) ctx->vote_pairs += tc_pairs;
   return RV_OK;
 }
 
@@ -1539,7 +1653,9 @@ void rot_vote_destroy(rv_ctx* ctx) {
   }
   ctx->dp_lb.release(); ctx->dp_act.release(); ctx->dp_rcnt.release(); ctx->dp_ties.release();
   ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release(); ctx->dp_lmax.release();
-  ctx->dp_best.release();
+  ctx->dp_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
+  ctx->dp_icnt.release(); ctx->dp_phase.release();
+  for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
   ctx->up.release(); ctx->down.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);

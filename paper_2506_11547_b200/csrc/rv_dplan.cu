@@ -14,6 +14,7 @@
 // The dive's lists are built per problem (one CTA, ordered compaction by warp ballots + a
 // CTA-wide scan); the BnB and final-level kernels are flat (one thread per list entry of all
 // problems, per-problem atomic slot allocation).
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -291,6 +292,205 @@ __global__ void dp_final_ties(const int64_t* __restrict__ act_off, const int64_t
   }
 }
 
+// ---- device-built vote decomposition ---------------------------------------------------------
+namespace {
+__host__ __device__ __forceinline__ int64_t i64min(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t i64max(int64_t a, int64_t b) { return a > b ? a : b; }
+constexpr int kPlanThreads = 1024;
+constexpr int64_t kExactChunk = 1 << 13;  // = build_exact_items
+
+__device__ __forceinline__ int64_t list_m(const DpList& L, int p) {
+  return L.cnt ? (int64_t)L.cnt[p] : L.shared_m;
+}
+
+// CTA-wide exclusive scan of one int64 per thread (kPlanThreads threads)
+__device__ int64_t cta_scan_excl(int64_t v, int64_t* sh, int64_t* total) {
+  const int t = threadIdx.x;
+  sh[t] = v;
+  __syncthreads();
+  for (int o = 1; o < kPlanThreads; o <<= 1) {
+    const int64_t add = t >= o ? sh[t - o] : 0;
+    __syncthreads();
+    sh[t] += add;
+    __syncthreads();
+  }
+  const int64_t incl = sh[t];
+  *total = sh[kPlanThreads - 1];
+  __syncthreads();
+  return incl - v;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
+    DpList L, const int64_t* __restrict__ rows, const int64_t* __restrict__ koffs, int32_t P,
+    int32_t B, double eps, int mode, int32_t slots, VoteSeg* segs, int64_t* item_off,
+    int64_t* ablk_off, int32_t* counts) {
+  __shared__ int64_t sh[kPlanThreads];
+  __shared__ int64_t s_cbs, s_tmax;
+  __shared__ int32_t s_nch;
+  const int t = threadIdx.x;
+  const int cpb = mode == 1 ? kTcM / 2 : kTcM;
+  // this thread's contiguous range of problems
+  const int p0 = (int)((int64_t)P * t / kPlanThreads), p1 = (int)((int64_t)P * (t + 1) / kPlanThreads);
+  int64_t cbs = 0, tmax = 0;
+  for (int p = p0; p < p1; ++p) {
+    const int64_t m = list_m(L, p), n = rows[p + 1] - rows[p];
+    if (m == 0 || n == 0) continue;
+    cbs += (m + cpb - 1) / cpb;
+    tmax = i64max(tmax, (n + kTcN - 1) / kTcN);
+  }
+  int64_t tot;
+  cta_scan_excl(cbs, sh, &tot);
+  if (t == 0) s_cbs = tot;
+  // max of tmax
+  sh[t] = tmax;
+  __syncthreads();
+  for (int o = kPlanThreads / 2; o > 0; o >>= 1) {
+    if (t < o) sh[t] = i64max(sh[t], sh[t + o]);
+    __syncthreads();
+  }
+  if (t == 0) {
+    s_tmax = sh[0];
+    // correspondence chunks per item: fill whole waves of the persistent kernel's CTAs
+    const int64_t cb_all = s_cbs, tm = s_tmax;
+    int64_t best_nch = 1;
+    if (mode != 2 && cb_all > 0) {
+      const int64_t min_tiles = i64min(tm, 8);
+      const int64_t max_nch = i64max(1, tm / i64max(1, min_tiles));
+      double best = -1;
+      for (int64_t nch = 1; nch <= max_nch; ++nch) {
+        const double waves = (double)(cb_all * nch) / slots;
+        if (waves > 64.0 && nch > 1) break;
+        const double eff = waves / ceil(waves);
+        const double score = eff - (waves < 4.0 ? 0.5 * (4.0 - waves) / 4.0 : 0.0);
+        if (score > best + 1e-9) { best = score; best_nch = nch; }
+      }
+    }
+    s_nch = (int32_t)best_nch;
+  }
+  __syncthreads();
+  const int64_t nch_all = s_nch;
+  // per-problem item / A-block counts, their offsets, and the segments
+  int64_t ni = 0, na = 0;
+  for (int p = p0; p < p1; ++p) {
+    const int64_t m = list_m(L, p), n = rows[p + 1] - rows[p];
+    if (m == 0 || n == 0) continue;
+    if (mode == 2) {
+      ni += m * ((n + kExactChunk - 1) / kExactChunk);
+    } else {
+      const int64_t cb = (m + cpb - 1) / cpb, nt = (n + kTcN - 1) / kTcN;
+      ni += cb * i64min(nch_all, nt);
+      if (!L.shared || p == 0) na += cb;
+    }
+  }
+  int64_t ti, ta;
+  int64_t ei = cta_scan_excl(ni, sh, &ti);
+  int64_t ea = cta_scan_excl(na, sh, &ta);
+  for (int p = p0; p < p1; ++p) {
+    item_off[p] = ei;
+    ablk_off[p] = L.shared ? 0 : ea;
+    const int64_t m = list_m(L, p), n = rows[p + 1] - rows[p];
+    if (m > 0 && n > 0) {
+      if (mode == 2) {
+        ei += m * ((n + kExactChunk - 1) / kExactChunk);
+      } else {
+        const int64_t cb = (m + cpb - 1) / cpb, nt = (n + kTcN - 1) / kTcN;
+        ei += cb * i64min(nch_all, nt);
+        if (!L.shared || p == 0) ea += cb;
+      }
+    }
+    VoteSeg sg;
+    const int64_t b = L.shared ? (int64_t)p * L.shared_m : L.base[p];
+    sg.lins = L.shared ? L.lins : L.lins + b;
+    sg.cnt_a = L.ca + b;
+    sg.cnt_b = L.cb + b;
+    sg.koff = koffs[p];
+    sg.row = rows[p];
+    sg.n = (int32_t)n;
+    sg.B = B;
+    sg.eps = eps;
+    segs[p] = sg;
+  }
+  if (t == 0) {
+    item_off[P] = ti;
+    ablk_off[P] = L.shared ? 0 : ta;
+    counts[0] = (int32_t)ti;
+    counts[1] = (int32_t)ta;
+    counts[2] = (int32_t)nch_all;
+  }
+}
+
+__global__ void dp_items_write(DpList L, const int64_t* __restrict__ rows, int32_t P, int mode,
+                               const int64_t* __restrict__ item_off,
+                               const int64_t* __restrict__ ablk_off,
+                               const int32_t* __restrict__ counts, VoteItem* items,
+                               ABlock* ablocks) {
+  const int64_t n_items = counts[0], n_ab = counts[1], nch_all = counts[2];
+  const int cpb = mode == 1 ? kTcM / 2 : kTcM;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_items; g += stride) {
+    const int p = find_problem(item_off, P, g);
+    const int64_t local = g - item_off[p];
+    const int64_t m = list_m(L, p), n = rows[p + 1] - rows[p];
+    VoteItem it;
+    it.seg = p;
+    if (mode == 2) {
+      const int64_t nc = (n + kExactChunk - 1) / kExactChunk;
+      const int64_t cell = local / nc, c = local % nc;
+      it.cell0 = (int32_t)cell;
+      it.ncell = 1;
+      it.i0 = (int32_t)(c * kExactChunk);
+      it.ni = (int32_t)i64min(kExactChunk, n - c * kExactChunk);
+      it.ablk = 0;
+    } else {
+      const int64_t cb = (m + cpb - 1) / cpb, per = (m + cb - 1) / cb;
+      const int64_t nt = (n + kTcN - 1) / kTcN, nch = i64min(nch_all, nt), ct = (nt + nch - 1) / nch;
+      const int64_t b = local / nch, c = local % nch;
+      const int64_t c0 = b * per, t0 = c * ct;
+      it.cell0 = (int32_t)c0;
+      it.ncell = (int32_t)i64max(0, i64min(per, m - c0));
+      it.i0 = (int32_t)(t0 * kTcN);
+      it.ni = (int32_t)(i64max(0, i64min(ct, nt - t0)) * kTcN);
+      it.ablk = (int32_t)(ablk_off[p] + b);
+    }
+    items[g] = it;
+  }
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_ab; g += stride) {
+    const int p = L.shared ? 0 : find_problem(ablk_off, P, g);
+    const int64_t local = g - (L.shared ? 0 : ablk_off[p]);
+    const int64_t m = list_m(L, p);
+    const int64_t cb = (m + cpb - 1) / cpb, per = (m + cb - 1) / cb;
+    ABlock a;
+    a.seg = p;
+    a.cell0 = (int32_t)(local * per);
+    a.ncell = (int32_t)i64max(0, i64min(per, m - local * per));
+    a.pad = 0;
+    ablocks[g] = a;
+  }
+}
+
+__global__ void __launch_bounds__(kPlanThreads) dp_scan(const int32_t* __restrict__ cnt, int32_t P,
+                                                        int64_t f3, int64_t* act,
+                                                        int64_t* next_base, int64_t* total) {
+  __shared__ int64_t sh[kPlanThreads];
+  const int t = threadIdx.x;
+  const int p0 = (int)((int64_t)P * t / kPlanThreads), p1 = (int)((int64_t)P * (t + 1) / kPlanThreads);
+  int64_t v = 0;
+  for (int p = p0; p < p1; ++p) v += cnt[p];
+  int64_t tot;
+  int64_t e = cta_scan_excl(v, sh, &tot);
+  for (int p = p0; p < p1; ++p) {
+    act[p] = e;
+    if (next_base) next_base[p] = e * f3;
+    e += cnt[p];
+  }
+  if (t == 0) {
+    act[P] = tot;
+    if (next_base) next_base[P] = tot * f3;
+    *total = tot;
+  }
+}
+
 // --- launchers ------------------------------------------------------------------------------
 void dp_launch_dive_children(const uint32_t* pick, const int32_t* pick_idx,
                              const uint32_t* idx_list, int32_t Bp, int32_t f, uint32_t* out,
@@ -306,6 +506,34 @@ void dp_launch_max_lo(const uint32_t* b, const int64_t* off, const int32_t* cnt,
                       int32_t P, cudaStream_t s) {
   dp_max_lo<<<P, kDpThreads, 0, s>>>(b, off, cnt, lb);
 }
+void dp_launch_items(const DpList& L, const int64_t* rows, const int64_t* koffs, int32_t P,
+                     int32_t B, double eps, int mode, int32_t slots, VoteSeg* segs,
+                     int64_t* item_off, int64_t* ablk_off, int32_t* counts, VoteItem* items,
+                     ABlock* ablocks, cudaStream_t s) {
+  dp_items_plan<<<1, kPlanThreads, 0, s>>>(L, rows, koffs, P, B, eps, mode, slots, segs, item_off,
+                                          ablk_off, counts);
+  dp_items_write<<<148 * 4, 256, 0, s>>>(L, rows, P, mode, item_off, ablk_off, counts, items,
+                                         ablocks);
+}
+
+void dp_items_bound(int mode, int64_t entries, int32_t P, int64_t nmax, int32_t slots,
+                    int64_t* max_items, int64_t* max_ablocks) {
+  if (mode == 2) {
+    *max_items = std::max<int64_t>(1, entries * ((nmax + kExactChunk - 1) / kExactChunk));
+    *max_ablocks = 1;
+    return;
+  }
+  const int cpb = mode == 1 ? kTcM / 2 : kTcM;
+  const int64_t cbs = entries / cpb + P + 1;  // sum of ceil(m_p / cpb)
+  *max_items = std::max<int64_t>(cbs, (int64_t)64 * slots + cbs);
+  *max_ablocks = cbs;
+}
+
+void dp_launch_scan(const int32_t* cnt, int32_t P, int64_t f3, int64_t* act, int64_t* next_base,
+                    int64_t* total, cudaStream_t s) {
+  dp_scan<<<1, kPlanThreads, 0, s>>>(cnt, P, f3, act, next_base, total);
+}
+
 namespace {
 inline unsigned flat_grid(int64_t n) {
   int64_t b = (n + 255) / 256;

@@ -6,7 +6,40 @@
 
 #include <cuda_runtime.h>
 
+#include "rv_kernels.h"
+
 namespace rv {
+
+// A level's per-problem block lists on the device: problem p's list is lins + base[p]
+// (shared: every problem's list is lins[0 .. shared_m)), cnt[p] entries (cnt == nullptr:
+// shared_m each); its counts live at ca / cb + base[p].
+struct DpList {
+  const uint32_t* lins;
+  int32_t shared;
+  int64_t shared_m;
+  const int64_t* base;
+  const int32_t* cnt;
+  uint32_t* ca;
+  uint32_t* cb;
+};
+
+// Device-built vote decomposition (same rules as build_tc_items / build_exact_items):
+// mode 0 = K3-TC bound (<= kTcM cells per item), 1 = K3-TC final (kTcM/2), 2 = K5 exact
+// (one cell per item, 8192-correspondence chunks).  Writes segs[P] (koffs: the TC table
+// offsets for modes 0/1, the K table offsets for mode 2), items, ablocks and
+// counts = {n_items, n_ablocks, chunks}; item_off / ablk_off: scratch [P+1].  The caller
+// sizes items / ablocks from a bound (dp_items_bound).
+void dp_launch_items(const DpList& L, const int64_t* rows, const int64_t* koffs, int32_t P,
+                     int32_t B, double eps, int mode, int32_t slots, VoteSeg* segs,
+                     int64_t* item_off, int64_t* ablk_off, int32_t* counts, VoteItem* items,
+                     ABlock* ablocks, cudaStream_t s);
+// items / ablocks needed for at most `entries` list entries over P problems of <= nmax rows
+void dp_items_bound(int mode, int64_t entries, int32_t P, int64_t nmax, int32_t slots,
+                    int64_t* max_items, int64_t* max_ablocks);
+// act[p] = exclusive prefix of cnt (act[P] = total, also written to *total); next_base[p] =
+// act[p] * f3 (optional)
+void dp_launch_scan(const int32_t* cnt, int32_t P, int64_t f3, int64_t* act, int64_t* next_base,
+                    int64_t* total, cudaStream_t s);
 
 // dive: candidate children (Bc = f*Bp) of the 27-neighbourhood of the pick (pick[p], or
 // idx_list[pick_idx[p]] if idx_list != nullptr), at out + p*cap

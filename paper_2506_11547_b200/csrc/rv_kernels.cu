@@ -345,8 +345,13 @@ __global__ void __launch_bounds__(256) rv_exact_kernel(const float* __restrict__
                                                        const float* __restrict__ y,
                                                        const VoteSeg* __restrict__ segs,
                                                        const VoteItem* __restrict__ items,
+                                                       int32_t n_items,
+                                                       const int32_t* __restrict__ n_dev,
                                                        float guard) {
-  const VoteItem it = items[blockIdx.x];
+  // n_dev: the item count lives on the device (device-built items; fixed grid)
+  const int32_t n = n_dev ? *n_dev : n_items;
+  for (int32_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
+  const VoteItem it = items[idx];
   const VoteSeg& sg = segs[it.seg];
   const uint32_t lin = sg.lins[it.cell0];
   int32_t ci, cj, ck;
@@ -396,13 +401,19 @@ __global__ void __launch_bounds__(256) rv_exact_kernel(const float* __restrict__
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
     atomicAdd(&sg.cnt_a[it.cell0], t);
   }
+  __syncthreads();  // ws is rewritten by the next item
+  }
 }
 
 void launch_exact(const float* k9, int64_t stride, const float* x, const float* y,
                   const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
-                  cudaStream_t s) {
+                  cudaStream_t s, const int32_t* n_dev) {
+  if (n_dev) {
+    rv_exact_kernel<<<148 * 8, 256, 0, s>>>(k9, stride, x, y, segs, items, 0, n_dev, guard);
+    return;
+  }
   if (n_items <= 0) return;
-  rv_exact_kernel<<<n_items, 256, 0, s>>>(k9, stride, x, y, segs, items, guard);
+  rv_exact_kernel<<<n_items, 256, 0, s>>>(k9, stride, x, y, segs, items, n_items, nullptr, guard);
 }
 
 // ------------------------------------------------------------------------------------------

@@ -108,9 +108,12 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 // writes the raw scores S' = s - t instead of counting (test hook):
 // dump[cell * dump_ld + correspondence].
 constexpr int64_t kTcABlockBytes = 128 * 64;
+// counts_dev != nullptr: {n_items, n_ablocks} are read on the device (device-built items;
+// the host arguments are ignored and the grids are fixed).
 void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, int32_t n_ablocks,
                     const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
-                    float* dump, int64_t dump_ld, cudaStream_t s, bool final_mode = false);
+                    float* dump, int64_t dump_ld, cudaStream_t s, bool final_mode = false,
+                    const int32_t* counts_dev = nullptr);
 
 // K4 (batched): level-0 reductions, one CTA per problem.  argmax: the dive's start index per
 // problem (planner key, see rv_plan_feed_l0_start).  survivors: outc != nullptr counts the
@@ -125,9 +128,10 @@ void launch_l0_survivors(const uint32_t* cnt, int64_t m0, const int32_t* problem
 
 // K5: exact counts (fp32 vote + fp64 recheck of |s32 - tau| < guard).  items: one block
 // per (block, correspondence chunk), ncell == 1.
+// n_dev != nullptr: the item count is read on the device (n_items ignored; fixed grid).
 void launch_exact(const float* k9, int64_t stride, const float* x, const float* y,
                   const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
-                  cudaStream_t s);
+                  cudaStream_t s, const int32_t* n_dev = nullptr);
 
 // K6: fp64 inlier test at qs[seg] + partial sums of K over inliers (+ mask words).
 void launch_inliers(const float* x, const float* y, const RefSeg* segs, const RefItem* items,

@@ -235,8 +235,12 @@ struct __align__(1024) TcSmem {
 template <bool FIN>
 __global__ void __launch_bounds__(128) rv_tc_atab_kernel(const VoteSeg* __restrict__ segs,
                                                          const ABlock* __restrict__ ablocks,
+                                                         int32_t n_ablocks,
+                                                         const int32_t* __restrict__ counts_dev,
                                                          float guard, uint8_t* __restrict__ atab) {
-  const ABlock ab = ablocks[blockIdx.x];
+  const int32_t nab = counts_dev ? counts_dev[1] : n_ablocks;
+  for (int32_t bi = blockIdx.x; bi < nab; bi += gridDim.x) {
+  const ABlock ab = ablocks[bi];
   const VoteSeg& sg = segs[ab.seg];
   const int m = threadIdx.x;  // A row
   const int cell = FIN ? (m >> 1) : m;
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(128) rv_tc_atab_kernel(const VoteSeg* __restri
     v[28] = tl;
     v[29] = __float2half_rn(-1.0f);
   }
-  uint8_t* blk = atab + (int64_t)blockIdx.x * kTcABlockBytes;
+  uint8_t* blk = atab + (int64_t)bi * kTcABlockBytes;
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
     uint4 w;
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(128) rv_tc_atab_kernel(const VoteSeg* __restri
 #pragma unroll
     for (int e = 0; e < 8; ++e) hw[e] = v[ch * 8 + e];
     *reinterpret_cast<uint4*>(blk + il_off(m, ch * 8)) = w;
+  }
   }
 }
 
@@ -292,8 +297,10 @@ template <bool DUMP, int ABL = 0, bool FIN = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
     rv_vote_tc_kernel(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ atab,
                       const VoteSeg* __restrict__ segs, const VoteItem* __restrict__ items,
-                      int32_t n_items, float guard, float* dump, int64_t dump_ld) {
+                      int32_t n_items_host, const int32_t* __restrict__ counts_dev, float guard,
+                      float* dump, int64_t dump_ld) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int32_t n_items = counts_dev ? counts_dev[0] : n_items_host;
   TcSmem& sm = *reinterpret_cast<TcSmem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -452,19 +459,22 @@ size_t tc_smem_bytes() { return sizeof(TcSmem) + 1024; }
 
 void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, int32_t n_ablocks,
                     const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
-                    float* dump, int64_t dump_ld, cudaStream_t s, bool final_mode) {
-  if (n_items <= 0 || n_ablocks <= 0) return;
-  if (final_mode)
-    rv_tc_atab_kernel<true><<<n_ablocks, 128, 0, s>>>(segs, ablocks, guard, atab);
-  else
-    rv_tc_atab_kernel<false><<<n_ablocks, 128, 0, s>>>(segs, ablocks, guard, atab);
+                    float* dump, int64_t dump_ld, cudaStream_t s, bool final_mode,
+                    const int32_t* counts_dev) {
+  if (!counts_dev && (n_items <= 0 || n_ablocks <= 0)) return;
   static int sms = [] {
     int dev = 0, v = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
-  const int grid = n_items < sms ? n_items : sms;  // persistent: one CTA per SM
+  const int agrid = counts_dev ? sms * 8 : n_ablocks;
+  if (final_mode)
+    rv_tc_atab_kernel<true><<<agrid, 128, 0, s>>>(segs, ablocks, n_ablocks, counts_dev, guard, atab);
+  else
+    rv_tc_atab_kernel<false><<<agrid, 128, 0, s>>>(segs, ablocks, n_ablocks, counts_dev, guard, atab);
+  // persistent: one CTA per SM
+  const int grid = counts_dev ? sms : (n_items < sms ? n_items : sms);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(rv_vote_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -477,7 +487,7 @@ void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, in
   }
   if (final_mode) {
     rv_vote_tc_kernel<false, 0, true><<<grid, kTcThreads, tc_smem_bytes(), s>>>(
-        tab, atab, segs, items, n_items, guard, nullptr, 0);
+        tab, atab, segs, items, n_items, counts_dev, guard, nullptr, 0);
     return;
   }
   static const int abl = [] {
@@ -486,21 +496,21 @@ void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, in
   }();
   if (dump)
     rv_vote_tc_kernel<true><<<grid, kTcThreads, tc_smem_bytes(), s>>>(tab, atab, segs, items,
-                                                                         n_items, guard, dump, dump_ld);
+                                                                         n_items, counts_dev, guard, dump, dump_ld);
   else if (abl != 0) {
 #define RV_ABL_CASE(A)                                                                           \
   case A:                                                                                        \
     cudaFuncSetAttribute(rv_vote_tc_kernel<false, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          (int)tc_smem_bytes());                                                  \
     rv_vote_tc_kernel<false, A><<<grid, kTcThreads, tc_smem_bytes(), s>>>(tab, atab, segs, items, \
-                                                                 n_items, guard, nullptr, 0);    \
+                                                                 n_items, counts_dev, guard, nullptr, 0);    \
     break;
     switch (abl) { RV_ABL_CASE(1) RV_ABL_CASE(2) RV_ABL_CASE(3) RV_ABL_CASE(4) RV_ABL_CASE(5)
                    RV_ABL_CASE(6) RV_ABL_CASE(7) default: break; }
 #undef RV_ABL_CASE
   } else
     rv_vote_tc_kernel<false><<<grid, kTcThreads, tc_smem_bytes(), s>>>(tab, atab, segs, items,
-                                                                          n_items, guard, nullptr, 0);
+                                                                          n_items, counts_dev, guard, nullptr, 0);
 }
 
 }  // namespace rv
