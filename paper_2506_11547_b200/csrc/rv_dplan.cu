@@ -218,14 +218,21 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
   }
 }
 
-// finest level, pass 1: Lmax[p] = max lo (zeroed by the caller)
+// finest level, pass 1: Lmax[p] = max lo (zeroed by the caller); one atomic per (warp, problem)
 __global__ void dp_final_max(const int64_t* __restrict__ act_off, const int64_t* __restrict__ cap,
                              const uint32_t* __restrict__ lo, int32_t P, uint32_t* Lmax) {
   const int64_t total = act_off[P];
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int p = find_problem(act_off, P, g);
-    atomicMax(&Lmax[p], lo[cap[p] + g - act_off[p]]);
+  const int lane = threadIdx.x & 31;
+  // warp-uniform loop: lanes past the end run with valid == false (whole-warp reductions)
+  for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); g0 < total;
+       g0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = g0 + lane;
+    const bool valid = g < total;
+    const int p = valid ? find_problem(act_off, P, g) : -1;
+    const uint32_t v = valid ? lo[cap[p] + g - act_off[p]] : 0u;
+    const uint32_t grp = __match_any_sync(0xffffffffu, p);
+    const uint32_t mx = __reduce_max_sync(grp, v);
+    if (valid && lane == __ffs(grp) - 1) atomicMax(&Lmax[p], mx);
   }
 }
 
@@ -233,25 +240,36 @@ __device__ __forceinline__ unsigned long long win_key(uint32_t votes, uint32_t l
   return ((unsigned long long)votes << 32) | (unsigned long long)(0xffffffffu - lin);
 }
 
-// finest level, pass 2: blocks with hi == lo offer their (exact) count to best[p]; blocks
-// with hi >= Lmax[p], hi != lo go to the recheck list of problem p (region act_off[p], count
-// rcnt[p]; both zeroed by the caller)
+// finest level, pass 2: blocks with hi == lo offer their (exact) count to best[p] (one
+// atomic per (warp, problem)); blocks with hi >= Lmax[p], hi != lo go to the recheck list of
+// problem p (region act_off[p], count rcnt[p]; both zeroed by the caller)
 __global__ void dp_final_split(const int64_t* __restrict__ act_off, const int64_t* __restrict__ cap,
                                const uint32_t* __restrict__ lins, const uint32_t* __restrict__ hi,
                                const uint32_t* __restrict__ lo, const uint32_t* __restrict__ Lmax,
                                int32_t P, unsigned long long* best, uint32_t* rlins,
                                int32_t* rcnt) {
   const int64_t total = act_off[P];
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int p = find_problem(act_off, P, g);
-    const int64_t idx = cap[p] + g - act_off[p];
-    const uint32_t h = hi[idx], l = lo[idx];
-    if (h == l) {
-      atomicMax(&best[p], win_key(l, lins[idx]));
-    } else if (h >= Lmax[p]) {
-      rlins[act_off[p] + atomicAdd(&rcnt[p], 1)] = lins[idx];
+  const int lane = threadIdx.x & 31;
+  // warp-uniform loop: lanes past the end run with valid == false (whole-warp reductions)
+  for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); g0 < total;
+       g0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = g0 + lane;
+    const bool valid = g < total;
+    const int p = valid ? find_problem(act_off, P, g) : -1;
+    uint32_t h = 0, l = 0, lin = 0;
+    if (valid) {
+      const int64_t idx = cap[p] + g - act_off[p];
+      h = hi[idx];
+      l = lo[idx];
+      lin = lins[idx];
     }
+    const bool exact = valid && h == l;
+    const uint32_t grp = __match_any_sync(0xffffffffu, p);
+    const uint32_t vmax = __reduce_max_sync(grp, exact ? l : 0u);
+    const uint32_t lmin = __reduce_min_sync(grp, (exact && l == vmax) ? lin : 0xffffffffu);
+    const uint32_t any = __ballot_sync(0xffffffffu, exact) & grp;
+    if (any && lane == __ffs(grp) - 1) atomicMax(&best[p], win_key(vmax, lmin));
+    if (valid && !exact && h >= Lmax[p]) rlins[act_off[p] + atomicAdd(&rcnt[p], 1)] = lin;
   }
 }
 

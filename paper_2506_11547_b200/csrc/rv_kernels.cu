@@ -533,38 +533,34 @@ __device__ void jacobi4(double A[4][4], double V[4][4]) {
   }
 }
 
-__global__ void __launch_bounds__(kRefThreads) rv_eig_kernel(const RefSeg* __restrict__ segs,
-                                                             const double* __restrict__ partials,
-                                                             double* qs, int32_t* flags,
-                                                             uint32_t* ninl, int mode) {
-  const RefSeg& sg = segs[blockIdx.x];
-  __shared__ double red[kRefThreads][10];
-  double acc[10];
+// One warp per problem (8 per CTA): the lanes sum the problem's K6 partials, lane 0 solves.
+__global__ void __launch_bounds__(256) rv_eig_kernel(const RefSeg* __restrict__ segs,
+                                                     const double* __restrict__ partials,
+                                                     double* qs, int32_t* flags, uint32_t* ninl,
+                                                     int mode, int32_t P) {
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (p >= P) return;
+  const RefSeg& sg = segs[p];
+  double S[10];
 #pragma unroll
-  for (int t = 0; t < 10; ++t) acc[t] = 0.0;
-  for (int itm = sg.item_begin + threadIdx.x; itm < sg.item_end; itm += kRefThreads)
+  for (int t = 0; t < 10; ++t) S[t] = 0.0;
+  for (int itm = sg.item_begin + lane; itm < sg.item_end; itm += 32)
 #pragma unroll
-    for (int t = 0; t < 10; ++t) acc[t] += partials[(int64_t)itm * 10 + t];
+    for (int t = 0; t < 10; ++t) S[t] += partials[(int64_t)itm * 10 + t];
 #pragma unroll
-  for (int t = 0; t < 10; ++t) red[threadIdx.x][t] = acc[t];
-  __syncthreads();
-  for (int w = kRefThreads / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w)
-#pragma unroll
-      for (int t = 0; t < 10; ++t) red[threadIdx.x][t] += red[threadIdx.x + w][t];
-    __syncthreads();
-  }
-  if (threadIdx.x != 0) return;
-  const double* S = red[0];
+  for (int t = 0; t < 10; ++t)
+    for (int o = 16; o > 0; o >>= 1) S[t] += __shfl_down_sync(0xffffffffu, S[t], o);
+  if (lane != 0) return;
   const double count = S[9];
   if (mode == 1) {
-    ninl[blockIdx.x] = (uint32_t)count;
+    ninl[p] = (uint32_t)count;
     return;
   }
-  int32_t fl = flags[blockIdx.x];
+  int32_t fl = flags[p];
   if (fl & kStop) return;
   if (count < 2.0) {
-    flags[blockIdx.x] = fl | RV_DEGENERATE | kStop;
+    flags[p] = fl | RV_DEGENERATE | kStop;
     return;
   }
   // S = sum K_i over inliers; K33 = -(K00 + K11 + K22) by tracelessness
@@ -582,7 +578,7 @@ __global__ void __launch_bounds__(kRefThreads) rv_eig_kernel(const RefSeg* __res
     if (r != i0 && A[r][r] > l2) l2 = A[r][r];
   const double l1 = A[i0][i0];
   if (l1 - l2 <= 1e-12 * fabs(l1)) {
-    flags[blockIdx.x] = fl | RV_DEGENERATE | kStop;
+    flags[p] = fl | RV_DEGENERATE | kStop;
     return;
   }
   double v[4] = {V[0][i0], V[1][i0], V[2][i0], V[3][i0]};
@@ -597,14 +593,14 @@ __global__ void __launch_bounds__(kRefThreads) rv_eig_kernel(const RefSeg* __res
       if (v[a] != 0.0) { flip = v[a] < 0.0; break; }
   }
   const double sgn = flip ? -nv : nv;
-  for (int a = 0; a < 4; ++a) qs[4 * blockIdx.x + a] = v[a] * sgn;
-  flags[blockIdx.x] = fl | RV_REFINED;
+  for (int a = 0; a < 4; ++a) qs[4 * p + a] = v[a] * sgn;
+  flags[p] = fl | RV_REFINED;
 }
 
 void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* qs, int32_t* flags,
                 uint32_t* ninl, int mode, cudaStream_t s) {
   if (P <= 0) return;
-  rv_eig_kernel<<<P, kRefThreads, 0, s>>>(segs, partials, qs, flags, ninl, mode);
+  rv_eig_kernel<<<(P + 7) / 8, 256, 0, s>>>(segs, partials, qs, flags, ninl, mode, P);
 }
 
 }  // namespace rv
