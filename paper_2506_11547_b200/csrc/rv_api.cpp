@@ -371,33 +371,43 @@ void build_tc_items(const std::vector<int64_t>& ncell, const std::vector<int64_t
   }
   int64_t last = -1;
   int32_t last_base = 0;
+  std::vector<int32_t> seg_base(ncell.size(), 0);
   for (size_t s = 0; s < ncell.size(); ++s) {
     if (ncell[s] == 0 || ncorr[s] == 0) continue;
-    const int64_t nt = (ncorr[s] + rv::kTcN - 1) / rv::kTcN;
     const int64_t cb = (ncell[s] + cpb - 1) / cpb;
     const int64_t per = (ncell[s] + cb - 1) / cb;
-    const int64_t nch = std::min<int64_t>(best_nch, nt);
-    const int64_t ct = (nt + nch - 1) / nch;  // tiles per chunk
-    int32_t base;
     if (seg_key && last >= 0 && (*seg_key)[s] == (*seg_key)[last] && ncell[s] == ncell[last]) {
-      base = last_base;
+      seg_base[s] = last_base;
     } else {
-      base = (int32_t)ablocks.size();
+      seg_base[s] = (int32_t)ablocks.size();
       for (int64_t b = 0; b < cb; ++b) {
         const int64_t c0 = b * per, nc = std::min(per, ncell[s] - c0);
         if (nc > 0) ablocks.push_back({(int32_t)s, (int32_t)c0, (int32_t)nc, 0});
       }
     }
     last = (int64_t)s;
-    last_base = base;
-    for (int64_t b = 0; b < cb; ++b) {
-      const int64_t c0 = b * per, nc = std::min(per, ncell[s] - c0);
-      if (nc <= 0) continue;
-      for (int64_t t0 = 0; t0 < nt; t0 += ct)
-        items.push_back({(int32_t)s, (int32_t)c0, (int32_t)nc, (int32_t)(t0 * rv::kTcN),
-                         (int32_t)(std::min(ct, nt - t0) * rv::kTcN), base + (int32_t)b});
-    }
+    last_base = seg_base[s];
   }
+  // chunk-major order: the CTAs running at the same time share one correspondence chunk,
+  // whose tiles then stay in L2 (block-major order spreads them over the whole table)
+  for (int64_t c = 0; c < best_nch; ++c)
+    for (size_t s = 0; s < ncell.size(); ++s) {
+      if (ncell[s] == 0 || ncorr[s] == 0) continue;
+      const int64_t nt = (ncorr[s] + rv::kTcN - 1) / rv::kTcN;
+      const int64_t nch = std::min<int64_t>(best_nch, nt);
+      if (c >= nch) continue;
+      const int64_t ct = (nt + nch - 1) / nch;  // tiles per chunk
+      const int64_t t0 = c * ct;
+      if (t0 >= nt) continue;
+      const int64_t cb = (ncell[s] + cpb - 1) / cpb;
+      const int64_t per = (ncell[s] + cb - 1) / cb;
+      for (int64_t b = 0; b < cb; ++b) {
+        const int64_t c0 = b * per, nc = std::min(per, ncell[s] - c0);
+        if (nc <= 0) continue;
+        items.push_back({(int32_t)s, (int32_t)c0, (int32_t)nc, (int32_t)(t0 * rv::kTcN),
+                         (int32_t)(std::min(ct, nt - t0) * rv::kTcN), seg_base[s] + (int32_t)b});
+      }
+    }
 }
 
 void build_exact_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
