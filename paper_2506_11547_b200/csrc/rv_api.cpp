@@ -202,7 +202,7 @@ struct rv_ctx {
   DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex, dp_lmax;
   DevBuf<unsigned long long> dp_best;
   DevBuf<int64_t> dp_ioff, dp_aoff, dp_tot;
-  DevBuf<int32_t> dp_icnt, dp_phase;
+  DevBuf<int32_t> dp_icnt, dp_phase, dp_err;
   // event pairs around the batched vote launches (read after the final sync)
   std::vector<cudaEvent_t> evs;
   size_t evn = 0;
@@ -1053,7 +1053,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     RV_CUDA(ctx->dp_icnt.ensure(4), "allocating");
     rv::dp_launch_items(Ld, ctx->rows.p, im == 2 ? ctx->koffs.p : ctx->toffs.p, PL, B, eps, im,
                         ctx->num_sms, ctx->vsegs.p, ctx->dp_ioff.p, ctx->dp_aoff.p, ctx->dp_icnt.p,
-                        ctx->vitems.p, ctx->ablk.p, s);
+                        ctx->vitems.p, ctx->ablk.p, mi, ma, ctx->dp_err.p, s);
     ctx->launches += 2;
     if (im == 2) {
       rv::launch_exact(ctx->k9.p, ctx->stride, x, y, ctx->vsegs.p, ctx->vitems.p, 0,
@@ -1105,6 +1105,8 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     return RV_OK;
   };
   ctx->ev_reset();
+  RV_CUDA(ctx->dp_err.ensure(1), "allocating");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_err.p, 0, 4, s), "memset");
   // ---- level 0: every problem votes the full candidate grid; counts stay on the device
   const int32_t B0 = ch[0];
   const int64_t m0 = rv_grid_candidates(B0, nullptr, 0);
@@ -1220,7 +1222,7 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     rv::dp_launch_bnb_expand(plins, shared, ctx->dp_act.p, shared ? ctx->dp_act.p : ctx->dp_off[cur].p,
                              pub, ctx->dp_lb.p, PL, ptotal, Bp, f, ctx->dp_off[nb].p,
                              ctx->dp_lins[nb].p, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p,
-                             ctx->dp_cnt[nb].p, s);
+                             ctx->dp_cnt[nb].p, ctx->dp_err.p, s);
     if (int rc = keep_phase(ctx->dp_cnt[nb].p)) return rc;
     // the children's act offsets, and the grandchildren's base (into the other set's dp_off)
     const int other = nb == 0 ? 1 : 0;
@@ -1291,6 +1293,8 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   int32_t* hties = ctx->down.take<int32_t>(PL);
   int64_t* hlb = ctx->down.take<int64_t>(PL);
   int32_t* hph = ctx->down.take<int32_t>((size_t)nph * PL);
+  int32_t* herr = ctx->down.take<int32_t>(1);
+  RV_CUDA(cudaMemcpyAsync(herr, ctx->dp_err.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hbest, ctx->dp_best.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hties, ctx->dp_ties.p, 4 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hlb, ctx->dp_lb.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
@@ -1299,6 +1303,8 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   RV_CUDA(cudaStreamSynchronize(s), "batched finalize");
   ctx->collect_vote_ms();
   ctx->ev_collect();
+  if (*herr != 0)
+    return ctx->fail(RV_ECUDA, "internal: device level-loop invariant violated (code %d)", *herr);
   tr.mark("  finalize");
   res.assign(PL, rv_plan_result{});
   uint64_t tc_pairs = 0;
@@ -1664,7 +1670,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->dp_lb.release(); ctx->dp_act.release(); ctx->dp_rcnt.release(); ctx->dp_ties.release();
   ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release(); ctx->dp_lmax.release();
   ctx->dp_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
-  ctx->dp_icnt.release(); ctx->dp_phase.release();
+  ctx->dp_icnt.release(); ctx->dp_phase.release(); ctx->dp_err.release();
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
   ctx->up.release(); ctx->down.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);

@@ -189,7 +189,8 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
                               const int64_t* __restrict__ act_off, const int64_t* __restrict__ pcap,
                               const uint32_t* __restrict__ pub, const int64_t* __restrict__ lb,
                               int32_t P, int32_t Bp, int32_t f, const int64_t* __restrict__ ccap,
-                              uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt) {
+                              uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
+                              int32_t* err) {
   const int64_t total = act_off[P];
   const int32_t Bc = Bp * f;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -205,6 +206,10 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
         for (int d = 0; d < f; ++d) c += is_candidate(Bc, f * i + a, f * j + b, f * k + d) ? 1 : 0;
     if (c == 0) continue;
     int64_t w = ccap[p] + atomicAdd(&ccnt[p], c);
+    if (w + c > ccap[p + 1]) {  // invariant: children <= parents x f^3 (never expected)
+      atomicOr(err, 1);
+      continue;
+    }
     for (int a = 0; a < f; ++a)
       for (int b = 0; b < f; ++b)
         for (int d = 0; d < f; ++d) {
@@ -442,9 +447,16 @@ __global__ void dp_items_write(DpList L, const int64_t* __restrict__ rows, int32
                                const int64_t* __restrict__ item_off,
                                const int64_t* __restrict__ ablk_off,
                                const int32_t* __restrict__ counts, VoteItem* items,
-                               ABlock* ablocks) {
-  const int64_t n_items = counts[0], n_ab = counts[1], nch_all = counts[2];
+                               ABlock* ablocks, int64_t max_items, int64_t max_ablocks,
+                               int32_t* err) {
+  int64_t n_items = counts[0], n_ab = counts[1];
+  const int64_t nch_all = counts[2];
   const int cpb = mode == 1 ? kTcM / 2 : kTcM;
+  if (n_items > max_items || n_ab > max_ablocks) {  // invariant: the host's bound holds
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(err, 2);
+    n_items = 0;
+    n_ab = 0;
+  }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_items; g += stride) {
     const int p = find_problem(item_off, P, g);
@@ -471,6 +483,7 @@ __global__ void dp_items_write(DpList L, const int64_t* __restrict__ rows, int32
       it.ni = (int32_t)(i64max(0, i64min(ct, nt - t0)) * kTcN);
       it.ablk = (int32_t)(ablk_off[p] + b);
     }
+    if (it.ncell < 1 || it.ncell > cpb || it.ni < 1) atomicOr(err, 4);  // invariant
     items[g] = it;
   }
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_ab; g += stride) {
@@ -527,11 +540,12 @@ void dp_launch_max_lo(const uint32_t* b, const int64_t* off, const int32_t* cnt,
 void dp_launch_items(const DpList& L, const int64_t* rows, const int64_t* koffs, int32_t P,
                      int32_t B, double eps, int mode, int32_t slots, VoteSeg* segs,
                      int64_t* item_off, int64_t* ablk_off, int32_t* counts, VoteItem* items,
-                     ABlock* ablocks, cudaStream_t s) {
+                     ABlock* ablocks, int64_t max_items, int64_t max_ablocks, int32_t* err,
+                     cudaStream_t s) {
   dp_items_plan<<<1, kPlanThreads, 0, s>>>(L, rows, koffs, P, B, eps, mode, slots, segs, item_off,
                                           ablk_off, counts);
   dp_items_write<<<148 * 4, 256, 0, s>>>(L, rows, P, mode, item_off, ablk_off, counts, items,
-                                         ablocks);
+                                         ablocks, max_items, max_ablocks, err);
 }
 
 void dp_items_bound(int mode, int64_t entries, int32_t P, int64_t nmax, int32_t slots,
@@ -564,9 +578,9 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           const int64_t* pcap, const uint32_t* pub, const int64_t* lb, int32_t P,
                           int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
                           uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
-                          cudaStream_t s) {
+                          int32_t* err, cudaStream_t s) {
   dp_bnb_expand<<<flat_grid(total), 256, 0, s>>>(plins, shared_lins ? 1 : 0, act_off, pcap, pub,
-                                                 lb, P, Bp, f, ccap, clins, ca, cb, ccnt);
+                                                 lb, P, Bp, f, ccap, clins, ca, cb, ccnt, err);
 }
 void dp_launch_final_max(const int64_t* act_off, const int64_t* cap, const uint32_t* lo, int32_t P,
                          int64_t total, uint32_t* Lmax, cudaStream_t s) {

@@ -29,10 +29,13 @@ struct DpList {
 // offsets for modes 0/1, the K table offsets for mode 2), items, ablocks and
 // counts = {n_items, n_ablocks, chunks}; item_off / ablk_off: scratch [P+1].  The caller
 // sizes items / ablocks from a bound (dp_items_bound).
+// err: invariant violations are OR-ed in (1 child capacity, 2 item bound, 4 item shape); the
+// host checks the word once at the end of the solve (there are no silent out-of-bounds writes).
 void dp_launch_items(const DpList& L, const int64_t* rows, const int64_t* koffs, int32_t P,
                      int32_t B, double eps, int mode, int32_t slots, VoteSeg* segs,
                      int64_t* item_off, int64_t* ablk_off, int32_t* counts, VoteItem* items,
-                     ABlock* ablocks, cudaStream_t s);
+                     ABlock* ablocks, int64_t max_items, int64_t max_ablocks, int32_t* err,
+                     cudaStream_t s);
 // items / ablocks needed for at most `entries` list entries over P problems of <= nmax rows
 void dp_items_bound(int mode, int64_t entries, int32_t P, int64_t nmax, int32_t slots,
                     int64_t* max_items, int64_t* max_ablocks);
@@ -60,7 +63,7 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           const int64_t* pcap, const uint32_t* pub, const int64_t* lb, int32_t P,
                           int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
                           uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
-                          cudaStream_t s);
+                          int32_t* err, cudaStream_t s);
 // finest level: Lmax[p] = max lo; split into exact-known (offered to best[p], a packed
 // (count << 32 | ~lin) max) and recheck lists (rlins at act_off[p], rcnt[p]); after the
 // exact recheck (counts ex, same layout as rlins) the rechecked offer theirs; ties counted.
