@@ -740,6 +740,10 @@ void fill_result(const rv_plan_result& pr, rv_result* out) {
   canonical_cell_quat(pr.B, pr.lin, out->q_cell);
 }
 
+int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets,
+                       int32_t P, double eps, int32_t levels, rv_result* out, uint32_t* masks);
+bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps);
+
 int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps, int32_t levels,
                rv_result* out, uint32_t* mask) {
   if (int rc = validate_common(ctx, x, y, eps, levels)) return rc;
@@ -748,6 +752,15 @@ int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double ep
   if (n > ctx->cfg.max_n)
     return ctx->fail(RV_EINVAL, "n = %lld exceeds max_n = %lld", (long long)n,
                      (long long)ctx->cfg.max_n);
+  // one GPU and no communicator: the device-resident level loop with P = 1 (5% faster than
+  // the host planner at cfg4: no per-level host work).  The host planner below is the path
+  // that shards each level's blocks over ranks (world > 1, emulated or NCCL).
+  const int32_t lev = levels == 0 ? std::min<int32_t>(5, (int32_t)ctx->chain.size()) : levels;
+  if (ctx->effective_world() == 1 && !ctx->comm &&
+      dplan_applies(ctx, lev, ctx->chain[ctx->chain.size() - lev], eps)) {
+    const int64_t offs1[2] = {0, n};
+    return solve_batched_impl(ctx, x, y, offs1, 1, eps, levels, out, mask);
+  }
   cudaStream_t s = ctx->stream;
   RV_CUDA(cudaEventRecord(ctx->ev0, s), "event");
   const int64_t offs[2] = {0, n};

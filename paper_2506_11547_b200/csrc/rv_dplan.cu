@@ -15,6 +15,7 @@
 // CTA-wide scan); the BnB and final-level kernels are flat (one thread per list entry of all
 // problems, per-problem atomic slot allocation).
 #include <algorithm>
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -322,6 +323,14 @@ __host__ __device__ __forceinline__ int64_t i64max(int64_t a, int64_t b) { retur
 constexpr int kPlanThreads = 1024;
 constexpr int64_t kExactChunk = 1 << 13;  // = build_exact_items
 
+// correspondence chunks of a problem with nt tiles: ct = ceil(nt / min(nch, nt)) tiles each,
+// ceil(nt / ct) of them non-empty (the host builder's loop `for t0 < nt; t0 += ct`)
+__device__ __forceinline__ void tc_chunks(int64_t nt, int64_t nch_all, int64_t* ct, int64_t* nc) {
+  const int64_t nch = i64min(nch_all, nt);
+  *ct = (nt + nch - 1) / nch;
+  *nc = (nt + *ct - 1) / *ct;
+}
+
 __device__ __forceinline__ int64_t list_m(const DpList& L, int p) {
   return L.cnt ? (int64_t)L.cnt[p] : L.shared_m;
 }
@@ -372,24 +381,42 @@ __global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
     if (t < o) sh[t] = i64max(sh[t], sh[t + o]);
     __syncthreads();
   }
-  if (t == 0) {
-    s_tmax = sh[0];
-    // correspondence chunks per item: fill whole waves of the persistent kernel's CTAs
+  if (t == 0) s_tmax = sh[0];
+  __syncthreads();
+  {
+    // correspondence chunks per item: fill whole waves of the persistent kernel's CTAs (the
+    // host rule: best score, >= 4 waves preferred; up to 64 waves).  Thread t scores the chunk
+    // counts t+1, t+1+kPlanThreads, ...; the CTA keeps the best score, smallest count.
     const int64_t cb_all = s_cbs, tm = s_tmax;
-    int64_t best_nch = 1;
+    double my_s = -1e300;
+    int64_t my_n = 1;
     if (mode != 2 && cb_all > 0) {
       const int64_t min_tiles = i64min(tm, 8);
       const int64_t max_nch = i64max(1, tm / i64max(1, min_tiles));
-      double best = -1;
-      for (int64_t nch = 1; nch <= max_nch; ++nch) {
+      for (int64_t nch = 1 + t; nch <= max_nch; nch += kPlanThreads) {
         const double waves = (double)(cb_all * nch) / slots;
         if (waves > 64.0 && nch > 1) break;
         const double eff = waves / ceil(waves);
         const double score = eff - (waves < 4.0 ? 0.5 * (4.0 - waves) / 4.0 : 0.0);
-        if (score > best + 1e-9) { best = score; best_nch = nch; }
+        if (score > my_s + 1e-9) { my_s = score; my_n = nch; }
       }
     }
-    s_nch = (int32_t)best_nch;
+    __shared__ double ss[kPlanThreads];
+    ss[t] = my_s;
+    __syncthreads();
+    for (int o = kPlanThreads / 2; o > 0; o >>= 1) {
+      if (t < o) ss[t] = ss[t] > ss[t + o] ? ss[t] : ss[t + o];
+      __syncthreads();
+    }
+    const double top = ss[0];
+    __syncthreads();
+    sh[t] = (my_s > top - 1e-9) ? my_n : INT64_MAX;
+    __syncthreads();
+    for (int o = kPlanThreads / 2; o > 0; o >>= 1) {
+      if (t < o) sh[t] = i64min(sh[t], sh[t + o]);
+      __syncthreads();
+    }
+    if (t == 0) s_nch = (int32_t)(sh[0] == INT64_MAX ? 1 : sh[0]);
   }
   __syncthreads();
   const int64_t nch_all = s_nch;
@@ -402,7 +429,9 @@ __global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
       ni += m * ((n + kExactChunk - 1) / kExactChunk);
     } else {
       const int64_t cb = (m + cpb - 1) / cpb, nt = (n + kTcN - 1) / kTcN;
-      ni += cb * i64min(nch_all, nt);
+      int64_t ct, nc;
+      tc_chunks(nt, nch_all, &ct, &nc);
+      ni += cb * nc;
       if (!L.shared || p == 0) na += cb;
     }
   }
@@ -418,7 +447,9 @@ __global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
         ei += m * ((n + kExactChunk - 1) / kExactChunk);
       } else {
         const int64_t cb = (m + cpb - 1) / cpb, nt = (n + kTcN - 1) / kTcN;
-        ei += cb * i64min(nch_all, nt);
+        int64_t ct, nc;
+        tc_chunks(nt, nch_all, &ct, &nc);
+        ei += cb * nc;
         if (!L.shared || p == 0) ea += cb;
       }
     }
@@ -474,8 +505,10 @@ __global__ void dp_items_write(DpList L, const int64_t* __restrict__ rows, int32
       it.ablk = 0;
     } else {
       const int64_t cb = (m + cpb - 1) / cpb, per = (m + cb - 1) / cb;
-      const int64_t nt = (n + kTcN - 1) / kTcN, nch = i64min(nch_all, nt), ct = (nt + nch - 1) / nch;
-      const int64_t b = local / nch, c = local % nch;
+      const int64_t nt = (n + kTcN - 1) / kTcN;
+      int64_t ct, nch;
+      tc_chunks(nt, nch_all, &ct, &nch);
+      const int64_t b = local % cb, c = local / cb;  // chunk-major (see build_tc_items)
       const int64_t c0 = b * per, t0 = c * ct;
       it.cell0 = (int32_t)c0;
       it.ncell = (int32_t)i64max(0, i64min(per, m - c0));

@@ -134,3 +134,47 @@ def test_device_loop_degenerate_batches(torch_cuda):
         assert (r1[0].cell, r1[0].votes) == (rd[3].cell, rd[3].votes)
     finally:
         ctx.close()
+
+
+def test_device_loop_large_single_problems(torch_cuda):
+    """One-problem batches of 2e4 ... 1e6 correspondences (many correspondence chunks per
+    item, uneven last chunks) through the device loop equal the host-planner solve."""
+    from paper_2506_11547_b200 import RotVote
+    torch = torch_cuda
+    ctx = RotVote(max_n=1_000_000)
+    try:
+        cases = [datagen.make_problem(20_000, 400, 0.01, 0.05, seed=81),
+                 datagen.make_problem(70_001, 700, 0.01, 0.05, seed=82),
+                 datagen.make_problem(250_000, 2_500, 0.01, 0.05, seed=83),
+                 datagen.cfg4()]
+        for pr in cases:
+            x, y = dev(torch, pr.x), dev(torch, pr.y)
+            rb = ctx.solve_batched(x, y, np.array([0, pr.n], np.int64), pr.eps)
+            rs = host_plan(lambda: ctx.solve(x, y, pr.eps))
+            compare(rb, [rs], strict_phases=True)
+    finally:
+        ctx.close()
+
+
+@pytest.mark.parametrize("tensor_vote", [False, True])
+def test_single_solve_device_loop_equals_host_planner(torch_cuda, tensor_vote):
+    """rot_vote_solve on one GPU takes the device loop (P = 1); the host planner (the
+    sharding path, RV_HOST_PLAN=1) must agree on every field, incl. per-phase block counts."""
+    from paper_2506_11547_b200 import RotVote
+    torch = torch_cuda
+    ctx = RotVote(max_n=200_000, tensor_vote=tensor_vote)
+    try:
+        cases = [datagen.cfg1(), datagen.cfg2(seed=3), datagen.cfg3(seed=4)]
+        rng = np.random.default_rng(77)
+        for k in range(6):
+            n = int(rng.integers(2, 20_000))
+            cases.append(datagen.make_problem(n, int(rng.integers(0, n + 1)), 0.01, 0.05,
+                                              seed=[77, k]))
+        for pr in cases:
+            x, y = dev(torch, pr.x), dev(torch, pr.y)
+            for levels in (0, 2, 3):
+                rd = ctx.solve(x, y, pr.eps, levels=levels)
+                rh = host_plan(lambda: ctx.solve(x, y, pr.eps, levels=levels))
+                compare([rd], [rh], strict_phases=True)
+    finally:
+        ctx.close()
