@@ -19,8 +19,9 @@
 // its A block into one of two A buffers, then one 16 KB cp.async.bulk per correspondence tile
 // into a ring of kTcStages), warp 1 = TMEM allocator + single-thread MMA issuer
 // (2 x tcgen05.mma K=16 per tile, accumulators double-buffered in 2 x 256 TMEM columns),
-// warps 2..9 = epilogue (warp w reads TMEM lanes 32*(w%4).. (its cells) and half of the
-// tile's columns and counts sign bits).
+// warps 2..9 = epilogue (warp w reads TMEM lanes 32*(w%4).. (its cells); the two warps of a
+// lane quarter take alternate tiles -- accumulator 0 / 1 -- so one warp's TMEM loads overlap
+// the other's count -- and counts sign bits).
 // Completion flows through mbarriers: full[s] / afull[a] (TMA tx), empty[s] / aempty[a]
 // (tcgen05.commit), tfull[b] (tcgen05.commit), tempty[b] (the 8 epilogue warps).
 #include <cstdint>
@@ -215,6 +216,9 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 #ifndef RV_TC_EPI_WARPS
 #define RV_TC_EPI_WARPS 8
 #endif
+#ifndef RV_TC_PINGPONG
+#define RV_TC_PINGPONG 1  // the two warps of a lane quarter take alternate tiles (0: split columns)
+#endif
 constexpr int kTcEpiWarps = RV_TC_EPI_WARPS;  // multiple of 4 (one lane quarter per SMSP)
 constexpr int kTcSplit = kTcEpiWarps / 4;     // warps sharing a lane quarter (column split)
 constexpr int kTcEpi0 = 2;                    // first epilogue warp
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     for (int b = 0; b < kTcAcc; ++b) {
       bar_init(&sm.tfull[b], 1);
-      bar_init(&sm.tempty[b], kTcEpiWarps);
+      bar_init(&sm.tempty[b], RV_TC_PINGPONG ? kTcEpiWarps / 2 : kTcEpiWarps);
     }
     for (int b = 0; b < 2; ++b) {
       bar_init(&sm.afull[b], 1);
@@ -387,13 +391,72 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else {
     // ---------------- epilogue: count sign bits (warps 2..9) ----------------
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-    const int half = (warp - kTcEpi0) >> 2;     // which 1/kTcSplit of the tile's columns
+    const int half = (warp - kTcEpi0) >> 2;     // accumulator (ping-pong) / column half
     const int m = 32 * (warp & 3) + lane;       // TMEM lane = A row
     const int cell = FIN ? (m >> 1) : m;
     const uint32_t two = guard > -1.0f ? 2u : 3u;  // a runtime 2 (keeps IMAD.HI)
+    uint32_t gt = 0;
+#if RV_TC_PINGPONG
+    // the warp pair (w, w + 4) of a lane quarter takes alternate tiles: warp half h counts the
+    // tiles in accumulator h (all 256 columns, two rounds of 128), so one warp's TMEM loads
+    // overlap the other warp's count
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      const VoteItem it = items[idx];
+      const int ntiles = it.ni / kTcN;
+      uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, n4 = 0, n5 = 0, n6 = 0, n7 = 0, mine = 0;
+      for (int t = 0; t < ntiles; ++t, ++gt) {
+        const uint32_t b = gt % kTcAcc;
+        if ((int)b != half) continue;
+        bar_wait(&sm.tfull[b], (gt / kTcAcc) & 1);
+        tc_fence_after();
+        ++mine;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          uint32_t r[4][32];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            RV_LD32(r[q], lane_addr + (uint32_t)(b * kTcN + rr * 128 + 32 * q));
+          tmem_wait_ld();
+          if (rr == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&sm.tempty[b]);
+          }
+          if (DUMP) {
+            if (cell < it.ncell) {
+              float* drow = dump + (int64_t)(it.cell0 + cell) * dump_ld + it.i0 + (int64_t)t * kTcN + rr * 128;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int e = 0; e < 32; ++e) drow[32 * q + e] = __uint_as_float(r[q][e]);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int e = 0; e < 32; e += 8) {
+                add_sign_alu(n0, r[q][e]);
+                add_sign_fma(n1, r[q][e + 1], two);
+                add_sign_alu(n2, r[q][e + 2]);
+                add_sign_fma(n3, r[q][e + 3], two);
+                add_sign_alu(n4, r[q][e + 4]);
+                add_sign_fma(n5, r[q][e + 5], two);
+                add_sign_alu(n6, r[q][e + 6]);
+                add_sign_fma(n7, r[q][e + 7], two);
+              }
+          }
+        }
+      }
+      if (!DUMP && cell < it.ncell && mine > 0) {
+        const VoteSeg& sg = segs[it.seg];
+        const uint32_t neg = (n0 + n1) + (n2 + n3) + (n4 + n5) + (n6 + n7);
+        const uint32_t cnt = mine * (uint32_t)kTcN - neg;  // its tiles' columns
+        atomicAdd(FIN && (m & 1) ? &sg.cnt_b[it.cell0 + cell] : &sg.cnt_a[it.cell0 + cell], cnt);
+      }
+    }
+#else
     constexpr int kLd = kTcN / kTcSplit / 32;  // tcgen05.ld x32 per warp per tile
     const int col0 = half * (kTcN / kTcSplit);
-    uint32_t gt = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const VoteItem it = items[idx];
       const int ntiles = it.ni / kTcN;
@@ -445,6 +508,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         atomicAdd(FIN && (m & 1) ? &sg.cnt_b[it.cell0 + cell] : &sg.cnt_a[it.cell0 + cell], cnt);
       }
     }
+#endif
   }
   tc_fence_before();
   __syncthreads();
