@@ -333,7 +333,9 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "result": {"cell": list(res.cell), "votes": res.votes, "n_inliers": res.n_inliers,
-                   "q": [float(v) for v in res.q]},
+                   "q": [float(v) for v in res.q],
+                   "rotation_error_deg": _rot_err_deg(pr.R, res.q)},
+        "ms_per_step_median": float(sorted(step_ms)[len(step_ms) // 2]),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cells, dt = oracle_sample(pr, args.cpu_seconds)
@@ -444,6 +446,15 @@ def run_batched(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _rot_err_deg(R_true, q):
+    """Geodesic angle between the ground truth and the returned rotation (stable form)."""
+    import numpy as np
+    M = R_true.T @ _quat_to_R(q)
+    c = (np.trace(M) - 1.0) / 2.0
+    s = np.linalg.norm([M[2, 1] - M[1, 2], M[0, 2] - M[2, 0], M[1, 0] - M[0, 1]]) / 2.0
+    return float(np.degrees(np.arctan2(s, c)))
 
 
 def _quat_to_R(q):

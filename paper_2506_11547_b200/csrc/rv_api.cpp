@@ -202,7 +202,8 @@ struct rv_ctx {
   DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex, dp_lmax;
   DevBuf<unsigned long long> dp_best;
   DevBuf<int64_t> dp_ioff, dp_aoff, dp_tot;
-  DevBuf<int32_t> dp_icnt, dp_phase, dp_err;
+  DevBuf<int32_t> dp_icnt, dp_phase, dp_err, dp_pcnt, dp_scnt;
+  DevBuf<int64_t> dp_poff, dp_sbase;
   // event pairs around the batched vote launches (read after the final sync)
   std::vector<cudaEvent_t> evs;
   size_t evn = 0;
@@ -752,12 +753,11 @@ int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double ep
   if (n > ctx->cfg.max_n)
     return ctx->fail(RV_EINVAL, "n = %lld exceeds max_n = %lld", (long long)n,
                      (long long)ctx->cfg.max_n);
-  // one GPU and no communicator: the device-resident level loop with P = 1 (5% faster than
-  // the host planner at cfg4: no per-level host work).  The host planner below is the path
-  // that shards each level's blocks over ranks (world > 1, emulated or NCCL).
+  // the device-resident level loop with P = 1 (no per-level host work; over several ranks each
+  // level's votes are sharded, see solve_batched_dplan).  The host planner below remains for
+  // RV_HOST_PLAN=1 and the configurations the device loop does not take (levels == 1).
   const int32_t lev = levels == 0 ? std::min<int32_t>(5, (int32_t)ctx->chain.size()) : levels;
-  if (ctx->effective_world() == 1 && !ctx->comm &&
-      dplan_applies(ctx, lev, ctx->chain[ctx->chain.size() - lev], eps)) {
+  if (dplan_applies(ctx, lev, ctx->chain[ctx->chain.size() - lev], eps)) {
     const int64_t offs1[2] = {0, n};
     return solve_batched_impl(ctx, x, y, offs1, 1, eps, levels, out, mask);
   }
@@ -1095,6 +1095,39 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   return vote_lists(ctx, x, y, rows, koff, eps, mode, B, Ld.lins, hoff, hcnt, 0, Ld.ca, Ld.cb);
 }
 
+// One level of a ONE-problem list sharded over ranks: rank r votes the entries
+// [r * chunk, (r + 1) * chunk) and one in-place ncclAllGather per count array assembles the
+// level (the count arrays hold >= W * chunk entries from 0).  The loopback emulation
+// (emulate_world) votes every rank's slice here, one launch sequence per slice.
+int vote_level_sharded(rv_ctx* ctx, const float* x, const float* y,
+                       const std::vector<int64_t>& rows, const std::vector<int64_t>& koff,
+                       double eps, int32_t mode, int32_t B, const rv::DpList& Ld, int64_t chunk,
+                       int64_t nmax) {
+  cudaStream_t s = ctx->stream;
+  const bool nccl_path = ctx->comm != nullptr;
+  const int W = ctx->effective_world();
+  const int r_lo = nccl_path ? ctx->cfg.rank : 0, r_hi = nccl_path ? r_lo + 1 : W;
+  RV_CUDA(ctx->dp_sbase.ensure(2), "allocating");
+  RV_CUDA(ctx->dp_scnt.ensure(1), "allocating");
+  for (int r = r_lo; r < r_hi; ++r) {
+    rv::dp_launch_slice(Ld.shared ? nullptr : Ld.base, Ld.cnt, Ld.shared_m, (int64_t)r * chunk, chunk,
+                        ctx->dp_sbase.p, ctx->dp_scnt.p, s);
+    ctx->launches += 1;
+    const rv::DpList Ls{Ld.lins, 0, 0, ctx->dp_sbase.p, ctx->dp_scnt.p, Ld.ca, Ld.cb};
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, B, Ls, 1, chunk, nmax)) return rc;
+  }
+  if (nccl_path) {
+    const size_t off = (size_t)ctx->cfg.rank * chunk;
+    for (int a = 0; a < (mode == RV_MODE_FINAL ? 2 : 1); ++a) {
+      uint32_t* buf = a == 0 ? Ld.ca : Ld.cb;
+      ncclResult_t nr = nccl().AllGather(buf + off, buf, (size_t)chunk, ncclUint32, ctx->comm, s);
+      if (nr != ncclSuccess)
+        return ctx->fail(RV_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(nr));
+    }
+  }
+  return RV_OK;
+}
+
 // The certified search of rv_plan.cpp for PL problems at once, every decision on the device
 // (rv_dplan.cu).  Host round trips: one per branch-and-bound level (the size of the next
 // child region) and one at the end; with K3-TC the items are built on the device.
@@ -1107,6 +1140,16 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   cudaStream_t s = ctx->stream;
   int64_t nmax = 0;
   for (int32_t p = 0; p < PL; ++p) nmax = std::max<int64_t>(nmax, rows[p + 1] - rows[p]);
+  // one problem on several ranks: every level's list is built identically on every rank
+  // (ordered expansion) and its votes are sharded (vote_level_sharded)
+  const int W = ctx->effective_world();
+  const bool shard = PL == 1 && W > 1;
+  const int64_t slack = shard ? W : 0;  // count arrays hold W * ceil(m / W) >= m entries
+  std::vector<int64_t> phase_chunk;       // per phase: the shard chunk (0: not sharded)
+  auto vote = [&](int32_t mode, int32_t B, const rv::DpList& Ld, int64_t entries) -> int {
+    if (!shard) return vote_level(ctx, x, y, rows, koff, eps, mode, B, Ld, PL, entries, nmax);
+    return vote_level_sharded(ctx, x, y, rows, koff, eps, mode, B, Ld, (entries + W - 1) / W, nmax);
+  };
   // per-phase block counts, kept on the device and read once at the end
   const int max_ph = 2 * L + 1;
   RV_CUDA(ctx->dp_phase.ensure((size_t)max_ph * PL), "allocating");
@@ -1131,7 +1174,7 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   int64_t mbg = 0;
   const double* bgh = rv_plan_l0_background(B0, eps, &mbg);
   if (!bgh || mbg != m0) return ctx->fail(RV_ECUDA, "internal: level-0 background unavailable");
-  RV_CUDA(ctx->l0cnt.ensure((size_t)PL * m0), "allocating level-0 counts");
+  RV_CUDA(ctx->l0cnt.ensure((size_t)PL * m0 + slack), "allocating level-0 counts");
   if (ctx->l0bg_B != B0 || ctx->l0bg_eps != eps || ctx->l0bg.cap < (size_t)m0) {
     RV_CUDA(ctx->l0bg.ensure(m0), "allocating");
     RV_CUDA(cudaMemcpy(ctx->l0bg.p, bgh, m0 * sizeof(double), cudaMemcpyHostToDevice),
@@ -1146,11 +1189,10 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     ctx->grid_list_B = B0;
     ctx->grid_list_m = m0;
   }
-  if (ctx->tc_on) {
-    RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, (size_t)PL * m0 * 4, s), "memset");
+  if (ctx->tc_on || shard) {
+    RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, ((size_t)PL * m0 + slack) * 4, s), "memset");
     const rv::DpList l0{ctx->grid_list.p, 1, m0, nullptr, nullptr, ctx->l0cnt.p, ctx->l0cnt.p};
-    if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, PL * m0, nmax))
-      return rc;
+    if (int rc = vote(RV_MODE_BOUND, B0, l0, PL * m0)) return rc;
   } else {
     std::vector<BatchReq> g0(PL);
     for (int32_t p = 0; p < PL; ++p) g0[p] = {p, B0, RV_MODE_BOUND, m0, ctx->grid_host.data(), true};
@@ -1170,7 +1212,7 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   // ---- dive: the 27-neighbourhood of the pick, level by level; lb* at the finest level
   for (int l = 1; l < L; ++l) {
     const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1], cap = 27 * f * f * f;
-    const size_t span = (size_t)PL * cap;
+    const size_t span = (size_t)PL * cap + slack;
     RV_CUDA(ctx->dp_lins[0].ensure(span), "allocating");
     RV_CUDA(ctx->dp_ca[0].ensure(span), "allocating");
     RV_CUDA(ctx->dp_cb[0].ensure(span), "allocating");
@@ -1188,8 +1230,8 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     if (int rc = keep_phase(ctx->dp_cnt[0].p)) return rc;
     const rv::DpList dl{ctx->dp_lins[0].p, 0, 0, ctx->dp_off[0].p, ctx->dp_cnt[0].p,
                         ctx->dp_ca[0].p, ctx->dp_cb[0].p};
-    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], dl, PL, (int64_t)span, nmax))
-      return rc;
+    if (int rc = vote(mode, ch[l], dl, (int64_t)PL * cap)) return rc;
+    phase_chunk.push_back(shard ? ((int64_t)cap + W - 1) / W : 0);
     if (mode == RV_MODE_BOUND)
       rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, ctx->dp_off[0].p,
                               ctx->dp_cnt[0].p, ch[l], eps, ctx->rows.p, ctx->dp_pick.p, PL, s);
@@ -1225,17 +1267,29 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     const int nb = cur == 1 ? 0 : 1;  // level 1 -> set 1 (set 0 still holds the dive lists)
     const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1];
     const int64_t f3 = (int64_t)f * f * f;
-    const int64_t cap_total = std::max<int64_t>(1, ptotal * f3);
+    const int64_t cap_total = std::max<int64_t>(1, ptotal * f3) + slack;
     RV_CUDA(ctx->dp_lins[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_ca[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_cb[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_cnt[nb].ensure(PL), "allocating");
     RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
     // dp_off[nb] = the children's base (written by the previous scan, or above for level 1)
-    rv::dp_launch_bnb_expand(plins, shared, ctx->dp_act.p, shared ? ctx->dp_act.p : ctx->dp_off[cur].p,
-                             pub, ctx->dp_lb.p, PL, ptotal, Bp, f, ctx->dp_off[nb].p,
-                             ctx->dp_lins[nb].p, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p,
-                             ctx->dp_cnt[nb].p, ctx->dp_err.p, s);
+    if (shard) {  // identical list on every rank: children placed by a prefix over parents
+      RV_CUDA(ctx->dp_pcnt.ensure(std::max<int64_t>(1, ptotal)), "allocating");
+      RV_CUDA(ctx->dp_poff.ensure(ptotal + 1), "allocating");
+      rv::dp_launch_expand_ordered(plins, shared, ctx->dp_act.p,
+                                   shared ? ctx->dp_act.p : ctx->dp_off[cur].p, pub, ctx->dp_lb.p,
+                                   PL, ptotal, Bp, f, ctx->dp_off[nb].p, ctx->dp_lins[nb].p,
+                                   ctx->dp_ca[nb].p, ctx->dp_cb[nb].p, ctx->dp_cnt[nb].p,
+                                   ctx->dp_pcnt.p, ctx->dp_poff.p, s);
+      ctx->launches += 2;
+    } else {
+      rv::dp_launch_bnb_expand(plins, shared, ctx->dp_act.p,
+                               shared ? ctx->dp_act.p : ctx->dp_off[cur].p, pub, ctx->dp_lb.p, PL,
+                               ptotal, Bp, f, ctx->dp_off[nb].p, ctx->dp_lins[nb].p,
+                               ctx->dp_ca[nb].p, ctx->dp_cb[nb].p, ctx->dp_cnt[nb].p,
+                               ctx->dp_err.p, s);
+    }
     if (int rc = keep_phase(ctx->dp_cnt[nb].p)) return rc;
     // the children's act offsets, and the grandchildren's base (into the other set's dp_off)
     const int other = nb == 0 ? 1 : 0;
@@ -1257,8 +1311,8 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
     const rv::DpList cl{ctx->dp_lins[nb].p, 0, 0, ctx->dp_off[nb].p, ctx->dp_cnt[nb].p,
                         ctx->dp_ca[nb].p, ctx->dp_cb[nb].p};
-    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], cl, PL, ctotal, nmax))
-      return rc;
+    if (int rc = vote(mode, ch[l], cl, ctotal)) return rc;
+    phase_chunk.push_back(shard ? (ctotal + W - 1) / W : 0);
     ptotal = ctotal;
     plins = ctx->dp_lins[nb].p;
     pub = ctx->dp_ca[nb].p;
@@ -1340,7 +1394,17 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     add(m0);
     for (int ph = 0; ph + 1 < nph; ++ph) add(hph[(size_t)ph * PL + p]);
     if (nre > 0) add(nre);
-    tc_pairs += (r.pair_votes - (uint64_t)nre * n);
+    if (!shard || !ctx->comm) {
+      tc_pairs += (r.pair_votes - (uint64_t)nre * n);
+    } else {  // this rank's slices only: level 0, then the dive and BnB phases
+      const int64_t c0 = (m0 + W - 1) / W;
+      auto mine = [&](int64_t m, int64_t c) {
+        return (uint64_t)std::max<int64_t>(0, std::min<int64_t>(c, m - (int64_t)ctx->cfg.rank * c));
+      };
+      tc_pairs += mine(m0, c0) * n;
+      for (int ph = 0; ph + 1 < nph; ++ph)
+        tc_pairs += mine(hph[(size_t)ph * PL + p], phase_chunk[ph]) * n;
+    }
   }
   if (ctx->tc_on) ctx->vote_pairs += tc_pairs;
   return RV_OK;
@@ -1362,6 +1426,12 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
   const int W = ctx->cfg.world;
   int64_t pb, pe;
   rv_shard_range(P, ctx->cfg.rank, W, &pb, &pe);
+  // one problem on several ranks: every rank runs it, each level's votes sharded over the
+  // ranks (solve_batched_dplan); no result gather
+  const int32_t lev_eff = levels == 0 ? std::min<int32_t>(5, (int32_t)ctx->chain.size()) : levels;
+  const bool one_sharded = P == 1 && W > 1 &&
+                           dplan_applies(ctx, lev_eff, ctx->chain[ctx->chain.size() - lev_eff], eps);
+  if (one_sharded) { pb = 0; pe = 1; }
   const int32_t PL = (int32_t)(pe - pb);
   std::vector<rv_result> local(PL);
   Trace tr;
@@ -1543,7 +1613,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
     r.launches = ctx->launches;
     r.vote_launches = ctx->vote_launches;
   }
-  if (!ctx->comm) {
+  if (!ctx->comm || one_sharded) {
     std::memcpy(out, local.data(), (size_t)P * sizeof(rv_result));
     return RV_OK;
   }
@@ -1684,6 +1754,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release(); ctx->dp_lmax.release();
   ctx->dp_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
   ctx->dp_icnt.release(); ctx->dp_phase.release(); ctx->dp_err.release();
+  ctx->dp_pcnt.release(); ctx->dp_scnt.release(); ctx->dp_poff.release(); ctx->dp_sbase.release();
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
   ctx->up.release(); ctx->down.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);

@@ -196,7 +196,8 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
   const int32_t Bc = Bp * f;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
-    const int p = find_problem(act_off, P, g);
+    // shared level-0 parents: every problem has act_off[1] of them (no search needed)
+    const int p = shared_lins ? (int)(g / act_off[1]) : find_problem(act_off, P, g);
     const int64_t e = g - act_off[p], idx = pcap[p] + e;
     if ((int64_t)pub[idx] < lb[p]) continue;
     int32_t i, j, k;
@@ -555,6 +556,97 @@ __global__ void __launch_bounds__(kPlanThreads) dp_scan(const int32_t* __restric
   }
 }
 
+// ---- one problem sharded over ranks: ordered (deterministic) lists -------------------------
+// Every rank must hold the identical list to vote a contiguous slice of it, so the children
+// are placed by a prefix over the parents instead of by atomics: count, scan, write.
+
+// pcnt[g] = candidate children of parent g if it survives (UB >= lb), else 0
+__global__ void dp_expand_count(const uint32_t* __restrict__ plins, int32_t shared_lins,
+                                const int64_t* __restrict__ act_off,
+                                const int64_t* __restrict__ pcap, const uint32_t* __restrict__ pub,
+                                const int64_t* __restrict__ lb, int32_t P, int32_t Bp, int32_t f,
+                                int32_t* pcnt) {
+  const int64_t total = act_off[P];
+  const int32_t Bc = Bp * f;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int p = find_problem(act_off, P, g);
+    const int64_t e = g - act_off[p], idx = pcap[p] + e;
+    int c = 0;
+    if ((int64_t)pub[idx] >= lb[p]) {
+      int32_t i, j, k;
+      lin_to_ijk(shared_lins ? plins[e] : plins[idx], Bp, i, j, k);
+      for (int a = 0; a < f; ++a)
+        for (int b = 0; b < f; ++b)
+          for (int d = 0; d < f; ++d) c += is_candidate(Bc, f * i + a, f * j + b, f * k + d) ? 1 : 0;
+    }
+    pcnt[g] = c;
+  }
+}
+
+// exclusive prefix of v[0..n) into off[0..n] (one CTA)
+__global__ void __launch_bounds__(kPlanThreads) dp_scan_i32(const int32_t* __restrict__ v,
+                                                            const int64_t* __restrict__ n_dev,
+                                                            int64_t* off) {
+  __shared__ int64_t sh[kPlanThreads];
+  const int64_t n = *n_dev;
+  const int t = threadIdx.x;
+  const int64_t i0 = n * t / kPlanThreads, i1 = n * (t + 1) / kPlanThreads;
+  int64_t sum = 0;
+  for (int64_t i = i0; i < i1; ++i) sum += v[i];
+  int64_t tot;
+  int64_t e = cta_scan_excl(sum, sh, &tot);
+  for (int64_t i = i0; i < i1; ++i) {
+    off[i] = e;
+    e += v[i];
+  }
+  if (t == 0) off[n] = tot;
+}
+
+// children of parent g at ccap[p] + (off[g] - off[act_off[p]]), (a,b,c) order; count slots
+// zeroed; ccnt[p] from the offsets
+__global__ void dp_expand_write(const uint32_t* __restrict__ plins, int32_t shared_lins,
+                                const int64_t* __restrict__ act_off,
+                                const int64_t* __restrict__ pcap, const int32_t* __restrict__ pcnt,
+                                const int64_t* __restrict__ off, int32_t P, int32_t Bp, int32_t f,
+                                const int64_t* __restrict__ ccap, uint32_t* clins, uint32_t* ca,
+                                uint32_t* cb, int32_t* ccnt) {
+  const int64_t total = act_off[P];
+  const int32_t Bc = Bp * f;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int p = find_problem(act_off, P, g);
+    if (g == act_off[p]) ccnt[p] = (int32_t)(off[act_off[p + 1]] - off[act_off[p]]);
+    if (pcnt[g] == 0) continue;
+    const int64_t e = g - act_off[p], idx = pcap[p] + e;
+    int32_t i, j, k;
+    lin_to_ijk(shared_lins ? plins[e] : plins[idx], Bp, i, j, k);
+    int64_t w = ccap[p] + off[g] - off[act_off[p]];
+    for (int a = 0; a < f; ++a)
+      for (int b = 0; b < f; ++b)
+        for (int d = 0; d < f; ++d) {
+          const int32_t ci = f * i + a, cj = f * j + b, ck = f * k + d;
+          if (!is_candidate(Bc, ci, cj, ck)) continue;
+          clins[w] = ijk_to_lin(ci, cj, ck, Bc);
+          ca[w] = 0;
+          cb[w] = 0;
+          ++w;
+        }
+  }
+}
+
+// the slice [r * chunk, min((r + 1) * chunk, cnt[0])) of a one-problem list: base_out[0],
+// cnt_out[0] (base_out[1] = base_out[0] + cnt_out[0] for the flat kernels' act layout)
+__global__ void dp_slice(const int64_t* __restrict__ base, const int32_t* __restrict__ cnt,
+                         int64_t shared_m, int64_t r0, int64_t chunk, int64_t* base_out,
+                         int32_t* cnt_out) {
+  const int64_t m = cnt ? (int64_t)cnt[0] : shared_m;
+  const int64_t c = i64max(0, i64min(chunk, m - r0));
+  base_out[0] = (base ? base[0] : 0) + r0;
+  base_out[1] = base_out[0] + c;
+  cnt_out[0] = (int32_t)c;
+}
+
 // --- launchers ------------------------------------------------------------------------------
 void dp_launch_dive_children(const uint32_t* pick, const int32_t* pick_idx,
                              const uint32_t* idx_list, int32_t Bp, int32_t f, uint32_t* out,
@@ -614,6 +706,21 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           int32_t* err, cudaStream_t s) {
   dp_bnb_expand<<<flat_grid(total), 256, 0, s>>>(plins, shared_lins ? 1 : 0, act_off, pcap, pub,
                                                  lb, P, Bp, f, ccap, clins, ca, cb, ccnt, err);
+}
+void dp_launch_expand_ordered(const uint32_t* plins, bool shared_lins, const int64_t* act_off,
+                              const int64_t* pcap, const uint32_t* pub, const int64_t* lb,
+                              int32_t P, int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
+                              uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
+                              int32_t* pcnt, int64_t* off, cudaStream_t s) {
+  dp_expand_count<<<flat_grid(total), 256, 0, s>>>(plins, shared_lins ? 1 : 0, act_off, pcap, pub,
+                                                   lb, P, Bp, f, pcnt);
+  dp_scan_i32<<<1, kPlanThreads, 0, s>>>(pcnt, act_off + P, off);
+  dp_expand_write<<<flat_grid(total), 256, 0, s>>>(plins, shared_lins ? 1 : 0, act_off, pcap,
+                                                   pcnt, off, P, Bp, f, ccap, clins, ca, cb, ccnt);
+}
+void dp_launch_slice(const int64_t* base, const int32_t* cnt, int64_t shared_m, int64_t r0,
+                     int64_t chunk, int64_t* base_out, int32_t* cnt_out, cudaStream_t s) {
+  dp_slice<<<1, 1, 0, s>>>(base, cnt, shared_m, r0, chunk, base_out, cnt_out);
 }
 void dp_launch_final_max(const int64_t* act_off, const int64_t* cap, const uint32_t* lo, int32_t P,
                          int64_t total, uint32_t* Lmax, cudaStream_t s) {

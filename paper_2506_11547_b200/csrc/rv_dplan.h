@@ -64,6 +64,18 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
                           uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
                           int32_t* err, cudaStream_t s);
+// Ordered BnB expansion (one problem sharded over ranks: every rank builds the identical
+// list): per-parent child counts into pcnt[total parents], their prefix into off[total + 1],
+// then the children in parent order.
+void dp_launch_expand_ordered(const uint32_t* plins, bool shared_lins, const int64_t* act_off,
+                              const int64_t* pcap, const uint32_t* pub, const int64_t* lb,
+                              int32_t P, int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
+                              uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
+                              int32_t* pcnt, int64_t* off, cudaStream_t s);
+// rank slice of a one-problem list: entries [r0, r0 + chunk) clipped to its length (cnt[0],
+// or shared_m when cnt == nullptr); base_out[2] = {start, end}, cnt_out[0] = length
+void dp_launch_slice(const int64_t* base, const int32_t* cnt, int64_t shared_m, int64_t r0,
+                     int64_t chunk, int64_t* base_out, int32_t* cnt_out, cudaStream_t s);
 // finest level: Lmax[p] = max lo; split into exact-known (offered to best[p], a packed
 // (count << 32 | ~lin) max) and recheck lists (rlins at act_off[p], rcnt[p]); after the
 // exact recheck (counts ex, same layout as rlins) the rechecked offer theirs; ties counted.

@@ -220,7 +220,7 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 #define RV_TC_PINGPONG 1  // the two warps of a lane quarter take alternate tiles (0: split columns)
 #endif
 constexpr int kTcEpiWarps = RV_TC_EPI_WARPS;  // multiple of 4 (one lane quarter per SMSP)
-constexpr int kTcSplit = kTcEpiWarps / 4;     // warps sharing a lane quarter (column split)
+[[maybe_unused]] constexpr int kTcSplit = kTcEpiWarps / 4;  // warps per lane quarter
 constexpr int kTcEpi0 = 2;                    // first epilogue warp
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, epilogue warps
 constexpr int kTcAccCols = kTcAcc * kTcN;  // = 512: the whole TMEM

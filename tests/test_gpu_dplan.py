@@ -178,3 +178,31 @@ def test_single_solve_device_loop_equals_host_planner(torch_cuda, tensor_vote):
                 compare([rd], [rh], strict_phases=True)
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("tensor_vote", [False, True])
+def test_sharded_single_solve_loopback(torch_cuda, tensor_vote):
+    """One problem over W emulated ranks (emulate_world): every level's list is built in
+    parent order and its votes are split into W slices -- the code path of the NCCL run with
+    the all-gather replaced by in-place writes.  Every field must equal the one-rank solve, and
+    the host planner's sharded path (RV_HOST_PLAN=1)."""
+    from paper_2506_11547_b200 import RotVote
+    torch = torch_cuda
+    cases = [datagen.cfg2(seed=5), datagen.cfg3(seed=6),
+             datagen.make_problem(3, 2, 0.0, 0.1, seed=7),
+             datagen.make_problem(40_000, 400, 0.01, 0.05, seed=8)]
+    for pr in cases:
+        x, y = dev(torch, pr.x), dev(torch, pr.y)
+        ref = None
+        for W in (1, 2, 3, 4, 8):
+            ctx = RotVote(max_n=1 << 17, emulate_world=W, tensor_vote=tensor_vote)
+            try:
+                r = ctx.solve(x, y, pr.eps)
+                rh = host_plan(lambda: ctx.solve(x, y, pr.eps))
+            finally:
+                ctx.close()
+            compare([r], [rh], strict_phases=True)
+            if ref is None:
+                ref = r
+            else:
+                compare([r], [ref], strict_phases=True)
