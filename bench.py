@@ -201,17 +201,26 @@ def _roofline(args, vote_pairs, vote_ms, ms_per_step):
     achieved = vote_pairs * FLOP_PER_PAIR / (vote_ms / 1e3) / 1e12 if vote_ms > 0 else None
     traffic, _ = _load_traffic(args.vote)
     if args.vote == "tc":
-        # the contraction runs on the tensor cores: fp16 dense peak (= the measured bf16 rate)
-        peak, src = measured_peak("bf16_tflops", 1590.0)
+        # The contraction runs on the tensor cores, but ncu shows the ALU pipe as the binding
+        # unit (88% busy against 40% for the tensor pipe, profiles/r01_tc_persistent_big_full):
+        # every pair's fp32 score leaves TMEM (tcgen05.ld, 64 B/clk/SMSP) and costs one ALU
+        # sign-count lane-op (16 lanes/clk/SMSP).  Bound = 148 SMs x 64 lane-ops/clk x 1965 MHz.
+        tpeak, src = measured_peak("bf16_tflops", 1590.0)
         pairs_s = vote_pairs / (vote_ms / 1e3)
+        alu_peak = TC_EPI_PEAK_PAIRS / 1e12
         return {
-            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": traffic,
+            "bound": "alu", "achieved": pairs_s / 1e12, "peak": alu_peak, "unit": "TOP/s",
+            "frac": pairs_s / TC_EPI_PEAK_PAIRS, "traffic": traffic,
             "kernel": "rv_vote_tc_kernel (K3-TC, tcgen05 kind::f16, fp16-split, fp32 TMEM accum)",
-            "peak_source": f"{src} dense bf16/fp16 tensor peak (MEASURED_PEAKS.json bf16_tflops)",
-            "flop_per_pair": FLOP_PER_PAIR,
-            "executed_mma_tflops": pairs_s * MMA_FLOP_PER_PAIR / 1e12,
-            "executed_mma_frac": pairs_s * MMA_FLOP_PER_PAIR / 1e12 / peak,
+            "ops_per_pair": 1,
+            "peak_source": "148 SMs x 4 SMSPs x 16 ALU lanes x 1965 MHz (B200_PROFILING.md unit "
+                           "counts); equals the TMEM readout bound (64 B/clk/SMSP at 4 B/pair)",
+            "tensor": {"peak_tflops": tpeak, "peak_source": f"{src} dense bf16/fp16 tensor peak "
+                       "(MEASURED_PEAKS.json bf16_tflops)",
+                       "algorithmic_tflops": achieved, "algorithmic_frac": achieved / tpeak,
+                       "flop_per_pair": FLOP_PER_PAIR,
+                       "executed_mma_tflops": pairs_s * MMA_FLOP_PER_PAIR / 1e12,
+                       "executed_mma_frac": pairs_s * MMA_FLOP_PER_PAIR / 1e12 / tpeak},
             "epilogue_bound": {
                 "what": "TMEM->RF readout (tcgen05.ld 64 B/clk/SMSP, 4 B/pair) and the ALU sign "
                         "count (16 lanes/clk/SMSP): 64 pairs/clk/SM at 1965 MHz",
