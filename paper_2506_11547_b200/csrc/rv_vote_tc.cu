@@ -226,6 +226,9 @@ constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, epilogue wa
 constexpr int kTcAccCols = kTcAcc * kTcN;  // = 512: the whole TMEM
 constexpr uint32_t kTileBytes = kTcN * 64;  // 16 KB at N = 256
 
+static_assert(!RV_TC_PINGPONG || (kTcAcc == 2 && kTcEpiWarps == 8),
+              "ping-pong epilogue: two accumulators, one warp pair per TMEM lane quarter");
+
 struct __align__(1024) TcSmem {
   uint8_t b[kTcStages][kTileBytes];  // correspondence tiles
   uint8_t a[2][128 * 64];            // A operand (128 rows x 32 fp16), double-buffered
@@ -404,23 +407,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const VoteItem it = items[idx];
       const int ntiles = it.ni / kTcN;
       uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, n4 = 0, n5 = 0, n6 = 0, n7 = 0, mine = 0;
-      for (int t = 0; t < ntiles; ++t, ++gt) {
-        const uint32_t b = gt % kTcAcc;
-        if ((int)b != half) continue;
-        bar_wait(&sm.tfull[b], (gt / kTcAcc) & 1);
+      // this warp's tiles of the item: global tile index g = gt + t with g % 2 == half
+      const uint32_t acc_addr = lane_addr + (uint32_t)(half * kTcN);
+      for (int t = (half - (int)(gt & 1)) & 1; t < ntiles; t += 2) {
+        const uint32_t g = gt + (uint32_t)t;
+        bar_wait(&sm.tfull[half], (g >> 1) & 1);
         tc_fence_after();
         ++mine;
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           uint32_t r[4][32];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            RV_LD32(r[q], lane_addr + (uint32_t)(b * kTcN + rr * 128 + 32 * q));
+          for (int q = 0; q < 4; ++q) RV_LD32(r[q], acc_addr + (uint32_t)(rr * 128 + 32 * q));
           tmem_wait_ld();
           if (rr == 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) bar_arrive(&sm.tempty[b]);
+            if (lane == 0) bar_arrive(&sm.tempty[half]);
           }
           if (DUMP) {
             if (cell < it.ncell) {
@@ -447,6 +450,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
         }
       }
+      gt += (uint32_t)ntiles;
       if (!DUMP && cell < it.ncell && mine > 0) {
         const VoteSeg& sg = segs[it.seg];
         const uint32_t neg = (n0 + n1) + (n2 + n3) + (n4 + n5) + (n6 + n7);
