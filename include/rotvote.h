@@ -209,6 +209,31 @@ int rot_vote_refine(rv_ctx* ctx, const float* x, const float* y, int64_t n, doub
                     const double* q0, int32_t rounds, double* q_out, int32_t* flags,
                     uint32_t* n_inliers, uint32_t* mask);
 
+/* ---- NEXT-4: the paper's Algorithm 1 as a same-box baseline ------------------
+ * Every correspondence's quaternion circle is sampled at J angles
+ * alpha_j = -pi + 2 pi j / J (Alg. 1 line 2), each sample taken to the half sphere q3 <= 0,
+ * projected and binned on the B^3 grid of [-1,1]^3 (Alg. 1 line 1; B = the chain's
+ * finest resolution, 360 by default); every sample adds one vote (Alg. 1 line 8).
+ * Result: the fullest bin (ties -> lowest lin), its votes and its centre's rotation (Alg. 1
+ * line 11; no refinement).  The bins are decided in fp64 with every operation rounded
+ * explicitly, so the accumulator equals the oracle's (or_alg1_bins) exactly.
+ * x, y: DEVICE [n][3] fp32.  acc_out: DEVICE u32 [B^3] copy of the accumulator (may be NULL).
+ * The context owns the accumulator (4 B^3 bytes, allocated on first use).
+ * Errors: RV_EINVAL (n < 1, J < 1, n > max_n), RV_EDATA (zero / non-finite vector),
+ * RV_ENOMEM, RV_ECUDA. */
+typedef struct {
+  double   q[4];        /* rotation of the winning block's centre (hemisphere-canonical) */
+  uint32_t votes;       /* its accumulator count (samples) */
+  int32_t  cell[3];     /* (i, j, k) at resolution B */
+  int32_t  B, J;
+  uint64_t samples;     /* n * J */
+  float    ms;          /* device time of the call (CUDA events) */
+  float    vote_ms;     /* device time of the sampling / scatter kernel */
+} rv_alg1_result;
+
+int rot_vote_alg1(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t J,
+                  rv_alg1_result* out, uint32_t* acc_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,12 @@ def lib():
         L.or_solve.restype = C.c_int32
         L.or_refine.argtypes = [fp, fp, C.c_int64, C.c_double, dp, C.c_int32, dp, i32p, u8p]
         L.or_refine.restype = C.c_int32
+        i64p = C.POINTER(C.c_int64)
+        L.or_alg1_basis.argtypes = [dp, dp, dp, dp]
+        L.or_alg1_bins.argtypes = [fp, fp, C.c_int64, C.c_int32, C.c_int32, i64p]
+        L.or_alg1_bins.restype = C.c_int64
+        L.or_alg1_solve.argtypes = [fp, fp, C.c_int64, C.c_int32, C.c_int32, i64p, u32p, dp]
+        L.or_alg1_solve.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -263,3 +269,36 @@ def rotation_angle_between(qa, qb) -> float:
     qa, qb = np.asarray(qa, float), np.asarray(qb, float)
     s = 1.0 if float(qa @ qb) >= 0 else -1.0
     return float(4.0 * np.arcsin(min(1.0, np.linalg.norm(qa - s * qb) / 2.0)))
+
+
+# ---- NEXT-4: the paper's Algorithm 1 ------------------------------
+
+def alg1_basis(a, b):
+    """(q_b1, q_b2) of the quaternion circle of a -> b (readings R13)."""
+    a, b = _f64(a), _f64(b)
+    q1, q2 = np.zeros(4), np.zeros(4)
+    lib().or_alg1_basis(_p(a, C.c_double), _p(b, C.c_double), _p(q1, C.c_double),
+                        _p(q2, C.c_double))
+    return q1, q2
+
+
+def alg1_bins(x, y, B=360, J=180) -> np.ndarray:
+    """The accumulator bin (lin) of every sample, [n, J] int64."""
+    x, y = _f32(x), _f32(y)
+    n = x.shape[0]
+    out = np.zeros((n, J), np.int64)
+    rc = lib().or_alg1_bins(_p(x, C.c_float), _p(y, C.c_float), n, B, J, _p(out, C.c_int64))
+    if rc != 0:
+        raise ValueError(f"or_alg1_bins: {rc}")
+    return out
+
+
+def alg1_solve(x, y, B=360, J=180):
+    """Algorithm 1 end to end: (lin of the max block, its votes, q of the block centre)."""
+    x, y = _f32(x), _f32(y)
+    lin = C.c_int64(); votes = C.c_uint32(); q = np.zeros(4)
+    rc = lib().or_alg1_solve(_p(x, C.c_float), _p(y, C.c_float), x.shape[0], B, J,
+                             C.byref(lin), C.byref(votes), _p(q, C.c_double))
+    if rc != 0:
+        raise ValueError(f"or_alg1_solve: {rc}")
+    return lin.value, votes.value, q

@@ -559,4 +559,102 @@ int32_t or_refine(const float* x, const float* y, int64_t n, double eps, const d
   return 0;
 }
 
+
+// ---- NEXT-4: the paper's Algorithm 1 (sampled voting), P:483-503 -------------------------
+// The quaternion circle of (a, b): q(alpha) = q_b1 cos(alpha/2) + q_b2 sin(alpha/2) with
+// q_b1 the quaternion of the minimal geodesic rotation a -> b, [cos(theta/2), sin(theta/2) c],
+// c = a x b / |a x b|, and q_b2 = [-b.q123, q0 b + b x q123].
+// Readings (R13-R15): cos/sin(theta/2) by the half-angle identities
+// sqrt((1 +- a.b)/2) (theta = arccos(a.b) in [0, pi]); when a x b = 0 (a = +-b, where the
+// paper leaves c open) c = normalize(a x e_k), e_k the axis of the smallest |a_k| (lowest k
+// on ties); alpha_j = -pi + 2 pi j / J, j = 0..J-1 ("discretizing [-pi, pi] uniformly",
+// Alg. 1 line 2; alpha = pi is the antipode of alpha = -pi, the same rotation, so it is not
+// sampled twice); each sample is taken to the half sphere q3 <= 0 (negated if q3 > 0),
+// projected by P and binned at step 2/B over [-1, 1]^3 (Alg. 1 line 1; B = 360,
+// P:635), index clamped to [0, B-1]; every sample adds 1 (Alg. 1 line 8).
+void or_alg1_basis(const double* a, const double* b, double* qb1, double* qb2) {
+  double d = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+  if (d > 1.0) d = 1.0;
+  if (d < -1.0) d = -1.0;
+  const double ch = std::sqrt((1.0 + d) / 2.0), sh = std::sqrt((1.0 - d) / 2.0);
+  double c[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+  double nc = std::sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+  if (nc == 0.0) {
+    int k = 0;
+    for (int t = 1; t < 3; ++t)
+      if (std::fabs(a[t]) < std::fabs(a[k])) k = t;
+    double e[3] = {0.0, 0.0, 0.0};
+    e[k] = 1.0;
+    c[0] = a[1] * e[2] - a[2] * e[1];
+    c[1] = a[2] * e[0] - a[0] * e[2];
+    c[2] = a[0] * e[1] - a[1] * e[0];
+    nc = std::sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+  }
+  qb1[0] = ch;
+  for (int t = 0; t < 3; ++t) qb1[1 + t] = sh * (c[t] / nc);
+  const double* v = qb1 + 1;  // q123
+  qb2[0] = -(b[0] * v[0] + b[1] * v[1] + b[2] * v[2]);
+  const double bxv[3] = {b[1] * v[2] - b[2] * v[1], b[2] * v[0] - b[0] * v[2],
+                         b[0] * v[1] - b[1] * v[0]};
+  for (int t = 0; t < 3; ++t) qb2[1 + t] = qb1[0] * b[t] + bxv[t];
+}
+
+// the bin of every sample: bins[i*J + j] = lin of sample j of correspondence i
+int64_t or_alg1_bins(const float* x, const float* y, int64_t n, int32_t B, int32_t J,
+                     int64_t* bins) {
+  if (B < 1 || J < 1) return -1;
+  const double pi = 3.14159265358979323846;
+  std::vector<double> cs(J), sn(J);
+  for (int32_t j = 0; j < J; ++j) {
+    const double half = (-pi + 2.0 * pi * (double)j / (double)J) / 2.0;
+    cs[j] = std::cos(half);
+    sn[j] = std::sin(half);
+  }
+  const double hb = (double)B / 2.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double a[3], b[3];
+    if (or_normalize(x + 3 * i, 1, a) != -1 || or_normalize(y + 3 * i, 1, b) != -1) return -2;
+    double qb1[4], qb2[4];
+    or_alg1_basis(a, b, qb1, qb2);
+    for (int32_t j = 0; j < J; ++j) {
+      double q[4];
+      for (int t = 0; t < 4; ++t) q[t] = qb1[t] * cs[j] + qb2[t] * sn[j];
+      if (q[3] > 0.0)
+        for (int t = 0; t < 4; ++t) q[t] = -q[t];
+      const double den = 1.0 - q[3];
+      int64_t idx[3];
+      for (int t = 0; t < 3; ++t) {
+        const double pt = q[t] / den;
+        int64_t v = (int64_t)std::floor((pt + 1.0) * hb);
+        if (v < 0) v = 0;
+        if (v > B - 1) v = B - 1;
+        idx[t] = v;
+      }
+      bins[i * J + j] = (idx[0] * B + idx[1]) * B + idx[2];
+    }
+  }
+  return 0;
+}
+
+// Algorithm 1 end to end: the dense B^3 accumulator, its maximum (ties -> lowest lin) and the
+// block centre's rotation (hemisphere representative).
+int64_t or_alg1_solve(const float* x, const float* y, int64_t n, int32_t B, int32_t J,
+                      int64_t* lin_out, uint32_t* votes_out, double* q_out) {
+  std::vector<int64_t> bins((size_t)n * J);
+  if (int64_t rc = or_alg1_bins(x, y, n, B, J, bins.data())) return rc;
+  std::vector<uint32_t> acc((size_t)B * B * B, 0u);
+  for (int64_t v : bins) ++acc[(size_t)v];
+  int64_t best = 0;
+  for (int64_t e = 1; e < (int64_t)acc.size(); ++e)
+    if (acc[(size_t)e] > acc[(size_t)best]) best = e;
+  *lin_out = best;
+  *votes_out = acc[(size_t)best];
+  const int64_t i = best / ((int64_t)B * B), j = (best / B) % B, k = best % B;
+  double p[3];
+  or_cell_center(B, i, j, k, p);
+  or_unproject(p, q_out);
+  or_canonicalize(q_out);
+  return 0;
+}
+
 }  // extern "C"

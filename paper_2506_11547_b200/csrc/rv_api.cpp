@@ -20,6 +20,7 @@
 #include "../../include/rotvote.h"
 #include "../../include/rotvote_plan.h"
 #include "rv_geom.h"
+#include "rv_alg1.h"
 #include "rv_dplan.h"
 #include "rv_kernels.h"
 
@@ -201,6 +202,10 @@ struct rv_ctx {
   DevBuf<int32_t> dp_cnt[2], dp_rcnt, dp_ties;
   DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex, dp_lmax;
   DevBuf<unsigned long long> dp_best;
+  DevBuf<uint32_t> a1_acc;          // NEXT-4: the Algorithm-1 accumulator (B^3)
+  DevBuf<double> a1_tab;            // cos / sin(alpha_j / 2)
+  DevBuf<unsigned long long> a1_best;
+  int32_t a1_J = 0;
   DevBuf<int64_t> dp_ioff, dp_aoff, dp_tot;
   DevBuf<int32_t> dp_icnt, dp_phase, dp_err, dp_pcnt, dp_scnt;
   DevBuf<int64_t> dp_poff, dp_sbase;
@@ -1752,7 +1757,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   }
   ctx->dp_lb.release(); ctx->dp_act.release(); ctx->dp_rcnt.release(); ctx->dp_ties.release();
   ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release(); ctx->dp_lmax.release();
-  ctx->dp_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
+  ctx->dp_best.release(); ctx->a1_acc.release(); ctx->a1_tab.release(); ctx->a1_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
   ctx->dp_icnt.release(); ctx->dp_phase.release(); ctx->dp_err.release();
   ctx->dp_pcnt.release(); ctx->dp_scnt.release(); ctx->dp_poff.release(); ctx->dp_sbase.release();
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
@@ -1888,6 +1893,73 @@ int rot_vote_debug_tc_scores(rv_ctx* ctx, const float* x, const float* y, int64_
   if (int rc = launch_tc(ctx, ablocks, (int32_t)items.size(), false, out, ld)) return rc;
   RV_CUDA(cudaGetLastError(), "launching K3-TC");
   RV_CUDA(cudaStreamSynchronize(ctx->stream), "K3-TC");
+  return RV_OK;
+}
+
+int rot_vote_alg1(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t J,
+                  rv_alg1_result* out, uint32_t* acc_out) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  if (!x || !y || !out) return ctx->fail(RV_EINVAL, "x, y and out must be non-null");
+  if (n < 1 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
+  if (J < 1 || J > (1 << 20)) return ctx->fail(RV_EINVAL, "J must lie in [1, 2^20]");
+  const int32_t B = ctx->chain.back();
+  const int64_t m = (int64_t)B * B * B;
+  cudaStream_t s = ctx->stream;
+  RV_CUDA(ctx->a1_acc.ensure(m), "allocating the Algorithm-1 accumulator");
+  RV_CUDA(ctx->a1_best.ensure(2), "allocating");
+  if (ctx->a1_J != J) {
+    // alpha_j = -pi + 2 pi j / J  (Alg. 1 line 2), the half angles' cos / sin in libm double
+    std::vector<double> tab(2 * (size_t)J);
+    const double pi = 3.14159265358979323846;
+    for (int32_t j = 0; j < J; ++j) {
+      const double half = (-pi + 2.0 * pi * (double)j / (double)J) / 2.0;
+      tab[j] = std::cos(half);
+      tab[J + j] = std::sin(half);
+    }
+    RV_CUDA(ctx->a1_tab.ensure(2 * (size_t)J), "allocating");
+    RV_CUDA(cudaMemcpy(ctx->a1_tab.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    ctx->a1_J = J;
+  }
+  cudaEvent_t e2, e3;
+  RV_CUDA(cudaEventCreate(&e2), "event");
+  RV_CUDA(cudaEventCreate(&e3), "event");
+  RV_CUDA(cudaEventRecord(ctx->ev0, s), "event");
+  RV_CUDA(cudaMemsetAsync(ctx->a1_acc.p, 0, m * 4, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->a1_best.p, 0, 8, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->a1_best.p + 1, 0xff, 8, s), "memset");
+  RV_CUDA(cudaEventRecord(e2, s), "event");
+  rv::launch_alg1(x, y, n, B, J, ctx->a1_tab.p, ctx->a1_tab.p + J, ctx->a1_acc.p,
+                  ctx->a1_best.p + 1, ctx->a1_best.p, s);
+  RV_CUDA(cudaGetLastError(), "launching Algorithm 1");
+  RV_CUDA(cudaEventRecord(e3, s), "event");
+  if (acc_out)
+    RV_CUDA(cudaMemcpyAsync(acc_out, ctx->a1_acc.p, m * 4, cudaMemcpyDeviceToDevice, s), "D2D");
+  unsigned long long hb[2];
+  RV_CUDA(cudaMemcpyAsync(hb, ctx->a1_best.p, 16, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
+  RV_CUDA(cudaStreamSynchronize(s), "Algorithm 1");
+  float ms = 0, vms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  cudaEventElapsedTime(&vms, e2, e3);
+  cudaEventDestroy(e2);
+  cudaEventDestroy(e3);
+  if (hb[1] != ~0ull)
+    return ctx->fail(RV_EDATA, "correspondence row %llu has a zero-length or non-finite vector",
+                     hb[1]);
+  std::memset(out, 0, sizeof(*out));
+  const uint32_t lin = 0xffffffffu - (uint32_t)(hb[0] & 0xffffffffu);
+  out->votes = (uint32_t)(hb[0] >> 32);
+  int32_t i, j, k;
+  rv::lin_to_ijk(lin, B, i, j, k);
+  out->cell[0] = i; out->cell[1] = j; out->cell[2] = k;
+  canonical_cell_quat(B, lin, out->q);
+  out->B = B;
+  out->J = J;
+  out->samples = (uint64_t)n * (uint64_t)J;
+  out->ms = ms;
+  out->vote_ms = vms;
   return RV_OK;
 }
 

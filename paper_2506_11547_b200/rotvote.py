@@ -53,6 +53,12 @@ class rv_result(C.Structure):
                 ("vote_pairs", C.c_uint64), ("vote_launches", C.c_int32), ("pad_", C.c_int32)]
 
 
+class rv_alg1_result(C.Structure):
+    _fields_ = [("q", C.c_double * 4), ("votes", C.c_uint32), ("cell", C.c_int32 * 3),
+                ("B", C.c_int32), ("J", C.c_int32), ("samples", C.c_uint64), ("ms", C.c_float),
+                ("vote_ms", C.c_float)]
+
+
 class rv_plan_result(C.Structure):
     _fields_ = [("lin", C.c_uint32), ("B", C.c_int32), ("votes", C.c_uint32), ("n_tied", C.c_int32),
                 ("lb_star", C.c_uint32), ("n_rechecked", C.c_int32), ("pair_votes", C.c_uint64),
@@ -87,6 +93,7 @@ def lib() -> C.CDLL:
     L.rot_vote_setup.argtypes = [vp, vp, vp, i64, vp]
     L.rot_vote_count_cells.argtypes = [vp, vp, vp, i64, i32, vp, i64, dbl, i32, vp, vp]
     L.rot_vote_refine.argtypes = [vp, vp, vp, i64, dbl, vp, i32, vp, vp, vp, vp]
+    L.rot_vote_alg1.argtypes = [vp, vp, vp, i64, i32, C.POINTER(rv_alg1_result), vp]
     L.rot_vote_debug_tc_scores.argtypes = [vp, vp, vp, i64, i32, vp, i64, dbl, vp]
     L.rv_plan_request_is_full_grid.argtypes = [vp]
     L.rv_plan_create.argtypes = [vp, i32, i32, i64, dbl, dbl, C.POINTER(vp)]
@@ -295,6 +302,20 @@ class RotVote:
         ca = a.cpu().numpy().view(np.uint32)
         cb = b.cpu().numpy().view(np.uint32)
         return (ca, cb) if mode in (RV_MODE_FINAL, RV_MODE_FINAL_TC) else ca
+
+    def alg1(self, x, y, J: int = 180, acc=None):
+        """NEXT-4: the paper's Algorithm 1 (J samples per circle, dense B^3 accumulator,
+        argmax) on the GPU.  acc: optional CUDA int32 tensor of B^3 entries receiving the
+        accumulator.  Returns the rv_alg1_result fields as a dict."""
+        import torch
+        r = rv_alg1_result()
+        ap = _dptr(acc, torch.int32, "acc") if acc is not None else None
+        _check(self.ctx, lib().rot_vote_alg1(self.ctx, _dptr(x, torch.float32, "x"),
+                                             _dptr(y, torch.float32, "y"), x.shape[0], int(J),
+                                             C.byref(r), ap))
+        return {"q": np.array(r.q[:]), "votes": r.votes, "cell": tuple(r.cell[:]), "B": r.B,
+                "J": r.J, "samples": r.samples, "ms": r.ms, "vote_ms": r.vote_ms,
+                "lin": (r.cell[0] * r.B + r.cell[1]) * r.B + r.cell[2]}
 
     def debug_tc_scores(self, x, y, B: int, lins, eps: float):
         """Raw K3-TC scores S' = s_tc - t (bound threshold), float32 [m, ceil(n/256)*256]."""
