@@ -60,8 +60,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--vote", default="tc", choices=["tc", "ffma2"],
                     help="bound levels on the tensor cores (K3-TC) or the FP32 pipe (K3)")
-    ap.add_argument("--method", default="certified", choices=["certified", "alg1"],
-                    help="alg1: the paper's Algorithm 1 (NEXT-4 baseline, extra line)")
+    ap.add_argument("--method", default="certified", choices=["certified", "alg1", "multi"],
+                    help="alg1: the paper's Algorithm 1 (NEXT-4 baseline, extra line); "
+                         "multi: two rotations of config 3 (NEXT-2, extra line)")
     ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg5"],
                     help="cfg5 (4096 x 1000 batched problems) is an extra measurement, "
                          "not the metric's bench line")
@@ -537,12 +538,57 @@ def run_alg1(args):
     return 0
 
 
+def run_multi(args):
+    """Extra line (NEXT-2): BASELINE config 3 (5% inliers to R, 3% to R2) -- both rotations
+    by rot_vote_solve_multi (K = 2, suppression 0.2 rad), beside the single solve."""
+    import numpy as np
+    import torch
+
+    import datagen
+    from paper_2506_11547_b200 import RotVote
+    pr = datagen.cfg3()
+    rv = RotVote(max_n=pr.n, stream=torch.cuda.current_stream())
+    x = torch.from_numpy(pr.x).cuda()
+    y = torch.from_numpy(pr.y).cuda()
+    K, rho = 2, 0.2
+    for _ in range(max(3, args.warmup)):
+        res = rv.solve_multi(x, y, pr.eps, K, rho)
+        one = rv.solve(x, y, pr.eps)
+    ms, ms1 = [], []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            res = rv.solve_multi(x, y, pr.eps, K, rho)
+            ms.append(res[0].ms)
+            one = rv.solve(x, y, pr.eps)
+            ms1.append(one.ms)
+    t, t1 = sum(ms) / len(ms), sum(ms1) / len(ms1)
+    line = {
+        "metric": "two rotations of BASELINE config 3 per second [NEXT-2]",
+        "value": 1e3 / t, "unit": "solves/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": t, "higher_is_better": True,
+        "dtype": "f16x3-split/f32", "data": "synthetic",
+        "config": {"workload": "cfg3: N=1e5, 5% inliers to R (sigma 0.02), 3% to R2, eps 0.08",
+                   "K": K, "rho_rad": rho, "path": "host planner, block counts reused across peaks"},
+        "peaks": [{"cell": list(r.cell), "votes": r.votes, "n_inliers": r.n_inliers,
+                   "rotation_error_deg": _rot_err_deg(R, r.q)}
+                  for r, R in zip(res, (pr.R, pr.R2))],
+        "single_solve_ms": t1,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    rv.close()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     if args.method == "alg1":
         return run_alg1(args)
+    if args.method == "multi":
+        return run_multi(args)
     if args.workload == "cfg5":
         return run_batched(args)
     return run_ours(args)

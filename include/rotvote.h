@@ -209,6 +209,20 @@ int rot_vote_refine(rv_ctx* ctx, const float* x, const float* y, int64_t n, doub
                     const double* q0, int32_t rounds, double* q_out, int32_t* flags,
                     uint32_t* n_inliers, uint32_t* mask);
 
+/* ---- NEXT-2: several rotations -----------------------------------------------
+ * Up to K peaks, greedily (reading R16): peak 1 is rot_vote_solve's winner; peak k is the
+ * fullest finest block whose centre rotation is more than rho (rotation angle, radians, in
+ * [0, pi]) from every earlier peak's centre (|q_c . q_j| < cos(rho/2)), ties -> lowest lin,
+ * found by the same certified search with the earlier peaks' balls excluded (blocks entirely
+ * inside a ball are skipped, finest blocks tested exactly).  Each peak is refined on its own
+ * inliers.  out: HOST rv_result[K]; *n_found peaks are written (fewer than K when every
+ * remaining block is suppressed).  Block counts voted for one peak are reused by the next.
+ * Runs the host planner (sharded over ranks like rot_vote_solve).  No masks.
+ * Errors: as rot_vote_solve; RV_EINVAL for K outside [1, 64] or rho outside [0, pi]. */
+int rot_vote_solve_multi(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                         int32_t levels, int32_t K, double rho, rv_result* out,
+                         int32_t* n_found);
+
 /* ---- NEXT-4: the paper's Algorithm 1 as a same-box baseline ------------------
  * Every correspondence's quaternion circle is sampled at J angles
  * alpha_j = -pi + 2 pi j / J (Alg. 1 line 2), each sample taken to the half sphere q3 <= 0,

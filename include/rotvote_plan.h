@@ -44,6 +44,15 @@ typedef struct {
  * guard >= 0.  Returns 0 or -1 (invalid) and sets *out. */
 int  rv_plan_create(const int32_t* chain, int32_t chain_len, int32_t levels, int64_t n,
                     double eps, double guard, rv_plan** out);
+/* NEXT-2 (several rotations): the same search restricted to the finest blocks whose centre
+ * rotation is more than rho (rotation angle, radians, in [0, pi]) from each of the n_excl
+ * rotations excl_q (HOST double[n_excl][4], scalar-first, normalised here): a finest block is
+ * excluded iff |q_c . q_e| >= cos(rho/2); a coarser block is skipped only when all of it is
+ * (angle(q_c, q_e) + r(c) <= rho).  With everything excluded the result has votes = 0 and
+ * n_tied = 0.  Returns 0 or -1. */
+int  rv_plan_create_ex(const int32_t* chain, int32_t chain_len, int32_t levels, int64_t n,
+                       double eps, double guard, const double* excl_q, int32_t n_excl,
+                       double rho, rv_plan** out);
 void rv_plan_destroy(rv_plan* p);
 
 /* 1 if a request is pending (outputs set; lins valid until the next feed), 0 when done. */

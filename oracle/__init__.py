@@ -302,3 +302,32 @@ def alg1_solve(x, y, B=360, J=180):
     if rc != 0:
         raise ValueError(f"or_alg1_solve: {rc}")
     return lin.value, votes.value, q
+
+
+# ---- NEXT-2: several rotations ------------------------------------
+
+def solve_multi(x, y, eps, B, K, rho):
+    """Top-K peaks with suppression, the plain definition (reading R16): exact counts of every
+    candidate block of the B grid (s >= cos(eps), double), then greedily: peak 1 = the fullest
+    block (ties -> lowest lin); peak k = the fullest block whose centre rotation is more than
+    rho (rotation angle) from every earlier peak's centre -- |q_c . q_j| < cos(rho/2).  Returns
+    a list of (lin, votes, n_tied, q_cell) with fewer than K entries when no block is left."""
+    lins = candidates(B)
+    cnt, _ = count_cells(x, y, B, lins, np.cos(eps))
+    cnt = cnt.astype(np.int64)
+    Q = np.array([cell_quat(B, int(l)) for l in lins])
+    alive = np.ones(lins.size, bool)
+    ch = np.cos(rho / 2.0)
+    out = []
+    for _ in range(K):
+        if not alive.any():
+            break
+        c = np.where(alive, cnt, -1)
+        best = c.max()
+        tied = np.flatnonzero(c == best)
+        e = tied[np.argmin(lins[tied])]
+        q = Q[e].copy()
+        canonicalize_q = q if q[3] <= 0 else -q
+        out.append((int(lins[e]), int(best), int(tied.size), canonicalize_q))
+        alive &= np.abs(Q @ Q[e]) < ch
+    return out

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -750,6 +751,61 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
                        int32_t P, double eps, int32_t levels, rv_result* out, uint32_t* masks);
 bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps);
 
+// Block counts already voted in this call, keyed by (mode, B, lin): a later search over the
+// same input (the next peak of rot_vote_solve_multi) votes only the blocks it has not seen.
+using CountCache = std::unordered_map<uint64_t, std::pair<uint32_t, uint32_t>>;
+
+// Drive a host planner to completion: every request voted (sharded over ranks) by
+// eval_request; with a cache only the uncached blocks are voted.
+int run_host_plan(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                  rv_plan* plan, rv_plan_result* pr, CountCache* cache) {
+  std::vector<uint32_t> ca, cb, ml, ma, mb;
+  std::vector<int64_t> mi;
+  int32_t B, mode;
+  int64_t m;
+  const uint32_t* lins;
+  while (rv_plan_request(plan, &B, &mode, &m, &lins)) {
+    ca.assign(m, 0);
+    cb.assign(m, 0);
+    if (!cache) {
+      if (int rc = eval_request(ctx, x, y, n, eps, B, mode, m, lins, ca.data(), cb.data()))
+        return rc;
+    } else {
+      ml.clear();
+      mi.clear();
+      for (int64_t e = 0; e < m; ++e) {
+        const uint64_t key = ((uint64_t)mode << 56) | ((uint64_t)B << 32) | lins[e];
+        auto it = cache->find(key);
+        if (it != cache->end()) {
+          ca[e] = it->second.first;
+          cb[e] = it->second.second;
+        } else {
+          ml.push_back(lins[e]);
+          mi.push_back(e);
+        }
+      }
+      if (!ml.empty()) {
+        ma.assign(ml.size(), 0);
+        mb.assign(ml.size(), 0);
+        if (int rc = eval_request(ctx, x, y, n, eps, B, mode, (int64_t)ml.size(), ml.data(),
+                                  ma.data(), mb.data()))
+          return rc;
+        for (size_t q = 0; q < ml.size(); ++q) {
+          ca[mi[q]] = ma[q];
+          cb[mi[q]] = mb[q];
+          cache->emplace(((uint64_t)mode << 56) | ((uint64_t)B << 32) | ml[q],
+                         std::make_pair(ma[q], mb[q]));
+        }
+      }
+    }
+    if (rv_plan_feed(plan, ca.data(), cb.data()) != 0)
+      return ctx->fail(RV_ECUDA, "internal: planner rejected counts");
+    ctx->mark("  fed");
+  }
+  rv_plan_get_result(plan, pr);
+  return RV_OK;
+}
+
 int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps, int32_t levels,
                rv_result* out, uint32_t* mask) {
   if (int rc = validate_common(ctx, x, y, eps, levels)) return rc;
@@ -781,24 +837,8 @@ int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double ep
                      (double)ctx->cfg.guard, &plan) != 0)
     return ctx->fail(RV_EINVAL, "invalid search plan");
   ctx->mark("plan");
-  std::vector<uint32_t> ca, cb;
-  int32_t B, mode;
-  int64_t m;
-  const uint32_t* lins;
-  int rc = RV_OK;
-  while (rv_plan_request(plan, &B, &mode, &m, &lins)) {
-    ca.assign(m, 0);
-    cb.assign(m, 0);
-    rc = eval_request(ctx, x, y, n, eps, B, mode, m, lins, ca.data(), cb.data());
-    if (rc) break;
-    if (rv_plan_feed(plan, ca.data(), cb.data()) != 0) {
-      rc = ctx->fail(RV_ECUDA, "internal: planner rejected counts");
-      break;
-    }
-    ctx->mark("  fed");
-  }
   rv_plan_result pr{};
-  if (!rc) rv_plan_get_result(plan, &pr);
+  int rc = run_host_plan(ctx, x, y, n, eps, plan, &pr, nullptr);
   rv_plan_destroy(plan);
   if (rc) return rc;
 
@@ -826,6 +866,64 @@ int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double ep
   return RV_OK;
 }
 
+
+// ---- NEXT-2: several rotations (greedy peaks with suppression, reading R16) --------------------
+int solve_multi_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                     int32_t levels, int32_t K, double rho, rv_result* out, int32_t* n_found) {
+  if (int rc = validate_common(ctx, x, y, eps, levels)) return rc;
+  if (!out || !n_found) return ctx->fail(RV_EINVAL, "out and n_found must be non-null");
+  if (K < 1 || K > 64) return ctx->fail(RV_EINVAL, "K must lie in [1, 64], got %d", K);
+  if (!(rho >= 0.0) || !(rho <= 3.141592653589793))
+    return ctx->fail(RV_EINVAL, "rho must lie in [0, pi], got %g", rho);
+  if (n < 2 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
+  *n_found = 0;
+  cudaStream_t s = ctx->stream;
+  RV_CUDA(cudaEventRecord(ctx->ev0, s), "event");
+  const int64_t offs[2] = {0, n};
+  std::vector<int64_t> koff;
+  if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
+  if (int rc = check_bad(ctx)) return rc;
+  CountCache cache;
+  std::vector<double> excl;  // earlier peaks' block-centre rotations
+  int32_t found = 0;
+  for (int32_t k = 0; k < K; ++k) {
+    rv_plan* plan = nullptr;
+    if (rv_plan_create_ex(ctx->chain.data(), (int32_t)ctx->chain.size(), levels, n, eps,
+                          (double)ctx->cfg.guard, excl.data(), k, rho, &plan) != 0)
+      return ctx->fail(RV_EINVAL, "invalid search plan");
+    rv_plan_result pr{};
+    int rc = run_host_plan(ctx, x, y, n, eps, plan, &pr, &cache);
+    rv_plan_destroy(plan);
+    if (rc) return rc;
+    if (pr.votes == 0 && pr.n_tied == 0) break;  // every block suppressed
+    rv_result& r = out[k];
+    fill_result(pr, &r);
+    int32_t fl = 0;
+    uint32_t ni = 0;
+    const int32_t pid = 0;
+    const int64_t mw = 0;
+    rc = run_refine(ctx, x, y, offs, 1, &pid, eps, r.q_cell, ctx->cfg.refine_rounds, &mw,
+                    nullptr, r.q, &fl, &ni);
+    if (rc) return rc;
+    r.flags |= fl;
+    r.n_inliers = ni;
+    excl.insert(excl.end(), r.q_cell, r.q_cell + 4);
+    ++found;
+  }
+  RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
+  RV_CUDA(cudaEventSynchronize(ctx->ev1), "event");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  for (int32_t k = 0; k < found; ++k) {
+    out[k].ms = ms;
+    out[k].vote_ms = ctx->vote_ms;
+    out[k].vote_pairs = ctx->vote_pairs;
+    out[k].launches = ctx->launches;
+    out[k].vote_launches = ctx->vote_launches;
+  }
+  *n_found = found;
+  return RV_OK;
+}
 
 // ---- batched: one launch per mode covers every active problem's request ----------------------
 struct BatchReq {
@@ -1894,6 +1992,16 @@ int rot_vote_debug_tc_scores(rv_ctx* ctx, const float* x, const float* y, int64_
   RV_CUDA(cudaGetLastError(), "launching K3-TC");
   RV_CUDA(cudaStreamSynchronize(ctx->stream), "K3-TC");
   return RV_OK;
+}
+
+int rot_vote_solve_multi(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                         int32_t levels, int32_t K, double rho, rv_result* out,
+                         int32_t* n_found) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  ctx->reset_counters();
+  return solve_multi_impl(ctx, x, y, n, eps, levels, K, rho, out, n_found);
 }
 
 int rot_vote_alg1(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t J,

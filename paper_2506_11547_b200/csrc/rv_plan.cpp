@@ -16,6 +16,7 @@
 //      winner = max exact count, ties -> lowest lin (R7).
 // The result equals the exhaustive scan of the finest grid for every chain and `levels`.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -95,6 +96,12 @@ struct rv_plan {
   std::vector<uint32_t> cells;  // pending request
 
   std::vector<uint32_t> l0_cells, l0_ub;
+  // NEXT-2 exclusion balls (earlier peaks' block-centre rotations, suppression angle rho):
+  // a finest block is excluded iff |q_c . q_e| >= cos(rho/2) (angle <= rho); a coarser block
+  // is dropped only when all of it is: angle(q_c, q_e) + r(c) <= rho (r(c) bounds the
+  // rotation angle from q_c to any rotation of the block, as in the certified bound)
+  std::vector<std::array<double, 4>> excl;
+  double rho = 0.0, cos_half_rho = 2.0;
   bool l0_ext = false;  // level 0 reduced by the caller (rv_plan_feed_l0_start / _survivors)
   int64_t lb_star = 0;
   // finest level
@@ -102,6 +109,33 @@ struct rv_plan {
   rv_plan_result res{};
 
   int last() const { return (int)chain.size() - 1; }
+
+  bool excluded(int l, uint32_t lin) const {
+    if (excl.empty()) return false;
+    const int32_t B = chain[l];
+    int32_t i, j, k;
+    rv::lin_to_ijk(lin, B, i, j, k);
+    double q[4];
+    rv::cell_quat(B, i, j, k, q);
+    const double r = l == last() ? 0.0 : rv::bound_radius(B, i, j, k);
+    for (const auto& e : excl) {
+      const double d = std::fabs(q[0] * e[0] + q[1] * e[1] + q[2] * e[2] + q[3] * e[3]);
+      if (l == last()) {
+        if (d >= cos_half_rho) return true;
+      } else {
+        const double ang = 2.0 * std::acos(std::min(1.0, d));
+        if (ang + r <= rho - 1e-9) return true;
+      }
+    }
+    return false;
+  }
+  void drop_excluded(int l, std::vector<uint32_t>& v) const {
+    if (excl.empty()) return;
+    size_t w = 0;
+    for (uint32_t c : v)
+      if (!excluded(l, c)) v[w++] = c;
+    v.resize(w);
+  }
   int32_t mode_for(int l) const { return l == last() ? RV_MODE_FINAL : RV_MODE_BOUND; }
 
   void note_request() {
@@ -117,18 +151,39 @@ struct rv_plan {
     return (double)ub - (double)n * (1.0 - t) * 0.5;
   }
 
-  // index of the max-excess block (blocks with their centre inside the ball first), ties ->
-  // lowest lin
-  size_t best_excess(int32_t B, const std::vector<uint32_t>& c, const uint32_t* ub,
+  // NEXT-2 dive preference of block lin at level l: 2 = entirely outside every exclusion
+  // ball (angle(q_c, q_e) - r(c) > rho), 1 = centre outside, 0 = centre inside a ball
+  int excl_rank(int l, uint32_t lin) const {
+    if (excl.empty()) return 2;
+    const int32_t B = chain[l];
+    int32_t i, j, k;
+    rv::lin_to_ijk(lin, B, i, j, k);
+    double q[4];
+    rv::cell_quat(B, i, j, k, q);
+    const double r = rv::bound_radius(B, i, j, k);
+    int rank = 2;
+    for (const auto& e : excl) {
+      const double d = std::fabs(q[0] * e[0] + q[1] * e[1] + q[2] * e[2] + q[3] * e[3]);
+      if (d >= cos_half_rho) return 0;
+      if (2.0 * std::acos(std::min(1.0, d)) - r <= rho) rank = 1;
+    }
+    return rank;
+  }
+
+  // index of the max-excess block, ties -> lowest lin; blocks whose centre lies inside the
+  // ball come first, and (NEXT-2) blocks away from the exclusion balls before those (excl_rank)
+  // -- a dive into or next to a suppressed region would end with a weak lb*
+  size_t best_excess(int l, const std::vector<uint32_t>& c, const uint32_t* ub,
                      const double* bg = nullptr) const {
+    const int32_t B = chain[l];
     size_t best = 0;
     double be = -1e300;
-    bool bin = false;
+    int bk = -1;  // rank: 2 * excl_rank + (centre inside the ball)
     for (size_t e = 0; e < c.size(); ++e) {
-      const bool in = centre_inside(B, c[e]);
-      if (bin && !in) continue;
+      const int kk = 2 * excl_rank(l, c[e]) + (centre_inside(B, c[e]) ? 1 : 0);
+      if (kk < bk) continue;
       const double x = bg ? (double)ub[e] - (double)n * bg[e] : excess(B, c[e], ub[e]);
-      if ((in && !bin) || x > be || (x == be && c[e] < c[best])) { be = x; best = e; bin = in; }
+      if (kk > bk || x > be || (x == be && c[e] < c[best])) { be = x; best = e; bk = kk; }
     }
     return best;
   }
@@ -159,6 +214,7 @@ struct rv_plan {
             if (inside || rv::is_candidate(Bc, ci, cj, ck)) out.push_back(rv::ijk_to_lin(ci, cj, ck, Bc));
           }
     }
+    drop_excluded(l + 1, out);
     return out;
   }
 
@@ -191,6 +247,18 @@ struct rv_plan {
     cells = children(0, surv);
     note_request();
   }
+  void start_dive_or_bnb(size_t s) {
+    if (l0_cells.empty()) {  // every level-0 block excluded: nothing left
+      lb_star = 0;
+      level = last();
+      mode = RV_MODE_FINAL;
+      cells.clear();
+      fin_cells.clear();
+      finalize();
+      return;
+    }
+    start_dive(s);
+  }
   void start_dive(size_t s) {
     phase = PH_DIVE;
     level = 1;
@@ -208,7 +276,7 @@ struct rv_plan {
     for (size_t r = 0; r < recheck_idx.size(); ++r) exact[recheck_idx[r]] = (int64_t)cells_exact[r];
     int64_t best = -1;
     uint32_t best_lin = 0;
-    int32_t tied = 0;
+    int32_t tied = 0;  // stays 0 (votes 0) when every block was excluded
     for (size_t e = 0; e < fin_cells.size(); ++e) {
       if (exact[e] < 0) continue;
       if (exact[e] > best) { best = exact[e]; best_lin = fin_cells[e]; tied = 1; }
@@ -245,21 +313,29 @@ struct rv_plan {
 
   int feed(const uint32_t* a, const uint32_t* b) {
     if (phase == PH_DONE) return -1;
-    if (mode == RV_MODE_FINAL && (b == nullptr || a == nullptr)) return -1;
+    if (mode == RV_MODE_FINAL && (b == nullptr || a == nullptr) && !cells.empty()) return -1;
     if (a == nullptr && !cells.empty()) return -1;
     switch (phase) {
       case PH_L0: {
         if (mode == RV_MODE_FINAL) { enter_final(a, b); return 0; }  // levels == 1
         l0_cells = cells;
         l0_ub.assign(a, a + cells.size());
-        const std::vector<double>* bg = grid_background(chain[0], eps);  // (1 - t_c)/2, cached
-        size_t s = best_excess(chain[0], l0_cells, l0_ub.data(), bg ? bg->data() : nullptr);
-        start_dive(s);
+        // (1 - t_c)/2 of the full grid, cached (not aligned with a filtered list)
+        const std::vector<double>* bg = excl.empty() ? grid_background(chain[0], eps) : nullptr;
+        size_t s = l0_cells.empty() ? 0 : best_excess(0, l0_cells, l0_ub.data(),
+                                                      bg ? bg->data() : nullptr);
+        start_dive_or_bnb(s);
         return 0;
       }
       case PH_DIVE: {
+        if (mode == RV_MODE_BOUND && cells.empty()) {
+          // every block of the neighbourhood excluded: no dive bound (lb* = 0)
+          lb_star = 0;
+          if (l0_ext) { phase = PH_NEED_SURV; cells.clear(); } else { start_bnb(); }
+          return 0;
+        }
         if (mode == RV_MODE_BOUND) {
-          size_t s = best_excess(chain[level], cells, a);
+          size_t s = best_excess(level, cells, a);
           uint32_t pick = cells[s];
           cells = children(level, neighbourhood(level, pick));
           ++level;
@@ -306,6 +382,12 @@ extern "C" {
 
 int rv_plan_create(const int32_t* chain, int32_t chain_len, int32_t levels, int64_t n, double eps,
                    double guard, rv_plan** out) {
+  return rv_plan_create_ex(chain, chain_len, levels, n, eps, guard, nullptr, 0, 0.0, out);
+}
+
+int rv_plan_create_ex(const int32_t* chain, int32_t chain_len, int32_t levels, int64_t n,
+                      double eps, double guard, const double* excl_q, int32_t n_excl, double rho,
+                      rv_plan** out) {
   if (!out) return -1;
   *out = nullptr;
   if (!chain || chain_len < 1 || chain_len > RV_MAX_CHAIN || n < 1) return -1;
@@ -324,7 +406,21 @@ int rv_plan_create(const int32_t* chain, int32_t chain_len, int32_t levels, int6
   p->phase = PH_L0;
   p->level = 0;
   p->mode = p->mode_for(0);
+  if (n_excl < 0 || (n_excl > 0 && (!excl_q || !(rho >= 0.0) || !(rho <= 3.141592653589793)))) {
+    delete p;
+    return -1;
+  }
+  for (int32_t e = 0; e < n_excl; ++e) {
+    std::array<double, 4> q{excl_q[4 * e], excl_q[4 * e + 1], excl_q[4 * e + 2], excl_q[4 * e + 3]};
+    const double nq = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (!(nq > 0.0)) { delete p; return -1; }
+    for (double& v : q) v /= nq;
+    p->excl.push_back(q);
+  }
+  p->rho = rho;
+  p->cos_half_rho = std::cos(rho / 2.0);
   p->cells = grid_cache(p->chain[0]).cand;
+  p->drop_excluded(0, p->cells);
   p->note_request();
   *out = p;
   return 0;
@@ -370,7 +466,7 @@ int rv_plan_feed_l0_survivors(rv_plan* p, const int32_t* idx, int64_t k) {
 }
 
 int rv_plan_request_is_full_grid(const rv_plan* p) {
-  return p && p->phase == PH_L0 ? 1 : 0;
+  return p && p->phase == PH_L0 && p->excl.empty() ? 1 : 0;
 }
 
 int rv_plan_feed(rv_plan* p, const uint32_t* cnt_a, const uint32_t* cnt_b) {

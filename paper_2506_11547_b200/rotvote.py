@@ -94,9 +94,12 @@ def lib() -> C.CDLL:
     L.rot_vote_count_cells.argtypes = [vp, vp, vp, i64, i32, vp, i64, dbl, i32, vp, vp]
     L.rot_vote_refine.argtypes = [vp, vp, vp, i64, dbl, vp, i32, vp, vp, vp, vp]
     L.rot_vote_alg1.argtypes = [vp, vp, vp, i64, i32, C.POINTER(rv_alg1_result), vp]
+    L.rot_vote_solve_multi.argtypes = [vp, vp, vp, i64, dbl, i32, i32, dbl, C.POINTER(rv_result),
+                                       C.POINTER(i32)]
     L.rot_vote_debug_tc_scores.argtypes = [vp, vp, vp, i64, i32, vp, i64, dbl, vp]
     L.rv_plan_request_is_full_grid.argtypes = [vp]
     L.rv_plan_create.argtypes = [vp, i32, i32, i64, dbl, dbl, C.POINTER(vp)]
+    L.rv_plan_create_ex.argtypes = [vp, i32, i32, i64, dbl, dbl, vp, i32, dbl, C.POINTER(vp)]
     L.rv_plan_destroy.argtypes = [vp]
     L.rv_plan_destroy.restype = None
     L.rv_plan_request.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64),
@@ -303,6 +306,16 @@ class RotVote:
         cb = b.cpu().numpy().view(np.uint32)
         return (ca, cb) if mode in (RV_MODE_FINAL, RV_MODE_FINAL_TC) else ca
 
+    def solve_multi(self, x, y, eps: float, K: int, rho: float, levels: int = 0) -> list:
+        """NEXT-2: up to K rotations, greedy peaks with suppression angle rho (radians)."""
+        import torch
+        out = (rv_result * K)()
+        nf = C.c_int32()
+        _check(self.ctx, lib().rot_vote_solve_multi(
+            self.ctx, _dptr(x, torch.float32, "x"), _dptr(y, torch.float32, "y"), x.shape[0],
+            float(eps), int(levels), int(K), float(rho), out, C.byref(nf)))
+        return [Result.from_c(out[k]) for k in range(nf.value)]
+
     def alg1(self, x, y, J: int = 180, acc=None):
         """NEXT-4: the paper's Algorithm 1 (J samples per circle, dense B^3 accumulator,
         argmax) on the GPU.  acc: optional CUDA int32 tensor of B^3 entries receiving the
@@ -347,11 +360,14 @@ class RotVote:
 class Plan:
     """The library's host-side level loop (include/rotvote_plan.h)."""
 
-    def __init__(self, chain, levels: int, n: int, eps: float, guard: float = 1e-5):
+    def __init__(self, chain, levels: int, n: int, eps: float, guard: float = 1e-5,
+                 excl=None, rho: float = 0.0):
         ch = np.ascontiguousarray(chain, np.int32)
         h = C.c_void_p()
-        rc = lib().rv_plan_create(ch.ctypes.data, ch.size, int(levels), int(n), float(eps),
-                                  float(guard), C.byref(h))
+        ex = np.ascontiguousarray(excl if excl is not None else np.zeros((0, 4)), np.float64)
+        rc = lib().rv_plan_create_ex(ch.ctypes.data, ch.size, int(levels), int(n), float(eps),
+                                     float(guard), ex.ctypes.data if ex.size else None,
+                                     ex.shape[0], float(rho), C.byref(h))
         if rc != 0:
             raise ValueError("invalid plan arguments")
         self.h = h.value

@@ -29,10 +29,11 @@ def oracle_counts(x, y, eps, B, mode, lins, guard=GUARD):
     return a, None
 
 
-def run_plan(x, y, eps, chain, levels, exchange=None, rank=0, world=1):
+def run_plan(x, y, eps, chain, levels, exchange=None, rank=0, world=1, excl=None, rho=0.0):
     """Run the planner to completion.  With world > 1 each rank counts its shard and
-    `exchange(local_counts) -> list of per-rank arrays` gathers them (gloo)."""
-    plan = rvmod.Plan(chain, levels, x.shape[0], eps)
+    `exchange(local_counts) -> list of per-rank arrays` gathers them (gloo).  excl / rho:
+    exclusion balls (NEXT-2, rv_plan_create_ex)."""
+    plan = rvmod.Plan(chain, levels, x.shape[0], eps, excl=excl, rho=rho)
     while True:
         req = plan.request()
         if req is None:
