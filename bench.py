@@ -60,9 +60,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--vote", default="tc", choices=["tc", "ffma2"],
                     help="bound levels on the tensor cores (K3-TC) or the FP32 pipe (K3)")
-    ap.add_argument("--method", default="certified", choices=["certified", "alg1", "multi"],
+    ap.add_argument("--method", default="certified", choices=["certified", "alg1", "multi", "rigid"],
                     help="alg1: the paper's Algorithm 1 (NEXT-4 baseline, extra line); "
-                         "multi: two rotations of config 3 (NEXT-2, extra line)")
+                         "multi: two rotations of config 3 (NEXT-2, extra line); "
+                         "rigid: rigid pose, the paper's synthetic setting (NEXT-3, extra line)")
     ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg5"],
                     help="cfg5 (4096 x 1000 batched problems) is an extra measurement, "
                          "not the metric's bench line")
@@ -581,6 +582,54 @@ def run_multi(args):
     return 0
 
 
+def run_rigid(args):
+    """Extra line (NEXT-3): rigid pose in the paper's synthetic setting (N = 5000
+    points in [-1,1]^3, 90% outliers, delta = 0.01): pairs + length check (mu_t = 0.05,
+    reading R17) -> rotation vote (eps = 0.05) -> translation vote ([-5,5]^3 at 0.025)."""
+    import numpy as np
+    import torch
+
+    import datagen
+    from paper_2506_11547_b200 import RotVote
+    lines = []
+    for rho in (0.9, 0.99):
+        pr = datagen.make_rigid(5000, rho, 0.01, seed=0)
+        rv = RotVote(max_n=4_000_000, stream=torch.cuda.current_stream())
+        x = torch.from_numpy(pr.x).cuda()
+        y = torch.from_numpy(pr.y).cuda()
+        for _ in range(max(3, args.warmup)):
+            r = rv.rigid(x, y, 0.05, 0.05)
+        rs = []
+        with ClockSampler(0) as clk:
+            for _ in range(args.steps):
+                torch.cuda.synchronize()
+                rs.append(rv.rigid(x, y, 0.05, 0.05))
+        t = sum(a["ms"] for a in rs) / len(rs)
+        r = rs[-1]
+        lines.append({
+            "metric": "rigid pose solves/s, paper's synthetic setting [NEXT-3]",
+            "value": 1e3 / t, "unit": "solves/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": t, "higher_is_better": True,
+            "dtype": "f16x3-split/f32 (rotation), f64 (pairs, translation)", "data": "synthetic",
+            "config": {"workload": f"N=5000 points in [-1,1]^3, {int(rho * 100)}% outliers, "
+                                   "delta=0.01, t in [-1,1]^3 (P:797-801)",
+                       "mu_t": 0.05, "eps": 0.05, "t_grid": "[-5,5]^3 at 0.025"},
+            "stages_ms": {"pairs": sum(a["pairs_ms"] for a in rs) / len(rs),
+                          "rotation": sum(a["rot_ms"] for a in rs) / len(rs),
+                          "translation": sum(a["trans_ms"] for a in rs) / len(rs)},
+            "pairs": {"total": r["pairs_total"], "kept": r["pairs_kept"]},
+            "result": {"rotation_error_deg": _rot_err_deg(pr.R, r["q"]),
+                       "translation_error": float(np.linalg.norm(r["t_mean"] - pr.t)),
+                       "translation_error_bin_centre": float(np.linalg.norm(r["t"] - pr.t)),
+                       "rot_votes": r["rot_votes"], "t_votes": r["t_votes"]},
+            "clocks": clk.summary(),
+        })
+        rv.close()
+    for l in lines:
+        print(json.dumps(l), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -589,6 +638,8 @@ def main():
         return run_alg1(args)
     if args.method == "multi":
         return run_multi(args)
+    if args.method == "rigid":
+        return run_rigid(args)
     if args.workload == "cfg5":
         return run_batched(args)
     return run_ours(args)

@@ -140,3 +140,38 @@ def batch_of(probs, eps: float) -> Batch:
 
 
 CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}
+
+
+# --- NEXT-3: rigid pose ----------------------------------------
+
+@dataclass
+class RigidProblem:
+    x: np.ndarray        # [n, 3] fp32 points in [-1, 1]^3
+    y: np.ndarray        # [n, 3] fp32: R x + t + delta N(0, I) for inliers
+    labels: np.ndarray   # 1 inlier, 0 outlier
+    R: np.ndarray
+    t: np.ndarray
+    delta: float
+    meta: dict
+
+
+def make_rigid(n: int, outlier_ratio: float, delta: float, seed=0) -> RigidProblem:
+    """The paper's synthetic rigid-motion setting: R Haar, t uniform in [-1,1]^3,
+    x uniform in [-1,1]^3, y = R x + t + delta N(0, I); outliers: x and y independent uniform
+    in [-1,1]^3; rows permuted."""
+    rng = np.random.default_rng(seed)
+    R = haar_rotation(rng)
+    t = rng.uniform(-1.0, 1.0, 3)
+    n_out = int(round(outlier_ratio * n))
+    n_in = n - n_out
+    x = rng.uniform(-1.0, 1.0, (n, 3))
+    y = np.empty_like(x)
+    y[:n_in] = x[:n_in] @ R.T + t + delta * rng.standard_normal((n_in, 3))
+    y[n_in:] = rng.uniform(-1.0, 1.0, (n_out, 3))
+    lab = np.zeros(n, np.uint8)
+    lab[:n_in] = 1
+    perm = rng.permutation(n)
+    return RigidProblem(x=np.ascontiguousarray(x[perm], np.float32),
+                        y=np.ascontiguousarray(y[perm], np.float32), labels=lab[perm], R=R,
+                        t=t, delta=float(delta),
+                        meta=dict(n=n, outlier_ratio=outlier_ratio, seed=seed))

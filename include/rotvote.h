@@ -223,6 +223,40 @@ int rot_vote_solve_multi(rv_ctx* ctx, const float* x, const float* y, int64_t n,
                          int32_t levels, int32_t K, double rho, rv_result* out,
                          int32_t* n_found);
 
+/* ---- NEXT-3: rigid pose front end ---------------------------------------------
+ * Points x, y (DEVICE [n][3] fp32, y = R x + t for inliers).  Pairs i < j give m = x_i - x_j,
+ * n = y_i - y_j, kept iff |‖m‖ - ‖n‖| <= mu_t (rotation-invariant length check, P:563-573;
+ * reading R17); the kept pairs are the correspondences of a rotation vote (rot_vote_solve at
+ * eps / levels), and with its rotation R* every point votes t_i = y_i - R* x_i on the grid
+ * [t_lo, t_hi)^3 at t_step ([-5,5]^3, 0.025); t = the fullest bin's centre (ties ->
+ * lowest lin), t_mean = the mean of its candidates.  The context needs max_n >= the number of
+ * kept pairs (RV_EINVAL otherwise, with the count in the message).  pair_ij: DEVICE int32
+ * [pair_cap][2] receiving the kept pairs' (i, j) in pair order (may be NULL). */
+typedef struct {
+  double   q[4];          /* rotation (rot_vote_solve on the pairs, refined) */
+  double   t[3];          /* translation: centre of the fullest bin */
+  double   t_mean[3];     /* mean of that bin's candidates */
+  uint32_t rot_votes;     /* the rotation's vote count (pairs) */
+  uint32_t rot_inliers;   /* pairs within eps of the refined rotation */
+  uint32_t t_votes;       /* candidates in the translation bin */
+  int32_t  t_cell[3];
+  int32_t  pad_;
+  int64_t  pairs_total;   /* n (n - 1) / 2 */
+  int64_t  pairs_kept;
+  float    ms, pairs_ms, rot_ms, trans_ms;  /* device times (CUDA events) */
+} rv_rigid_result;
+
+int rot_vote_rigid(rv_ctx* ctx, const float* x, const float* y, int64_t n, double mu_t,
+                   double eps, int32_t levels, double t_lo, double t_hi, double t_step,
+                   rv_rigid_result* out, int32_t* pair_ij, int64_t pair_cap);
+
+/* The translation vote alone, for a given rotation q (HOST double[4], scalar-first):
+ * lin / votes / t / t_mean as in rot_vote_rigid (HOST outputs).  RV_EDATA when no candidate
+ * falls inside the grid. */
+int rot_vote_translation(rv_ctx* ctx, const float* x, const float* y, int64_t n,
+                         const double* q, double t_lo, double t_hi, double t_step,
+                         int64_t* lin, uint32_t* votes, double* t, double* t_mean);
+
 /* ---- NEXT-4: the paper's Algorithm 1 as a same-box baseline ------------------
  * Every correspondence's quaternion circle is sampled at J angles
  * alpha_j = -pi + 2 pi j / J (Alg. 1 line 2), each sample taken to the half sphere q3 <= 0,

@@ -89,6 +89,11 @@ def lib():
         L.or_alg1_bins.restype = C.c_int64
         L.or_alg1_solve.argtypes = [fp, fp, C.c_int64, C.c_int32, C.c_int32, i64p, u32p, dp]
         L.or_alg1_solve.restype = C.c_int64
+        L.or_rigid_pairs.argtypes = [fp, fp, C.c_int64, C.c_double, C.c_int64, i64p, fp, fp]
+        L.or_rigid_pairs.restype = C.c_int64
+        L.or_translation_vote.argtypes = [fp, fp, C.c_int64, dp, C.c_double, C.c_double,
+                                          C.c_double, i64p, u32p, dp, dp]
+        L.or_translation_vote.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -331,3 +336,31 @@ def solve_multi(x, y, eps, B, K, rho):
         out.append((int(lins[e]), int(best), int(tied.size), canonicalize_q))
         alive &= np.abs(Q @ Q[e]) < ch
     return out
+
+
+# ---- NEXT-3: rigid pose front end ---------------------------------
+
+def rigid_pairs(x, y, mu_t):
+    """Kept pairs (i < j, lexicographic) of the length check: (ij [k,2], m [k,3], n [k,3])."""
+    x, y = _f32(x), _f32(y)
+    n = x.shape[0]
+    k = lib().or_rigid_pairs(_p(x, C.c_float), _p(y, C.c_float), n, float(mu_t), 0, None,
+                             None, None)
+    ij = np.zeros((k, 2), np.int64)
+    m = np.zeros((k, 3), np.float32)
+    d = np.zeros((k, 3), np.float32)
+    lib().or_rigid_pairs(_p(x, C.c_float), _p(y, C.c_float), n, float(mu_t), k,
+                         _p(ij, C.c_int64), _p(m, C.c_float), _p(d, C.c_float))
+    return ij, m, d
+
+
+def translation_vote(x, y, q, lo=-5.0, hi=5.0, step=0.025):
+    """(lin, votes, bin centre, mean of the bin's candidates) of the translation vote."""
+    x, y, q = _f32(x), _f32(y), _f64(q)
+    lin = C.c_int64(); votes = C.c_uint32(); t = np.zeros(3); tm = np.zeros(3)
+    rc = lib().or_translation_vote(_p(x, C.c_float), _p(y, C.c_float), x.shape[0],
+                                   _p(q, C.c_double), lo, hi, step, C.byref(lin),
+                                   C.byref(votes), _p(t, C.c_double), _p(tm, C.c_double))
+    if rc != 0:
+        return None
+    return lin.value, votes.value, t, tm

@@ -657,4 +657,89 @@ int64_t or_alg1_solve(const float* x, const float* y, int64_t n, int32_t B, int3
   return 0;
 }
 
+
+// ---- NEXT-3: rigid pose front end ------------------------------------------------
+// Pairs: for every i < j (lexicographic order) m = x_i - x_j, n = y_i - y_j,
+// computed in double (exact for fp32 inputs) and kept iff both are non-zero and the
+// rotation-invariant length check |‖m‖ - ‖n‖| <= mu_t holds (mu_t is a parameter,
+// the paper does not give it: reading R17).  Kept pairs are returned as fp32 (the rotation
+// vote's input format) with their (i, j).  Returns the number kept (writes up to cap).
+int64_t or_rigid_pairs(const float* x, const float* y, int64_t n, double mu_t, int64_t cap,
+                       int64_t* ij, float* m_out, float* n_out) {
+  int64_t k = 0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j) {
+      double m[3], d[3];
+      for (int t = 0; t < 3; ++t) {
+        m[t] = (double)x[3 * i + t] - (double)x[3 * j + t];
+        d[t] = (double)y[3 * i + t] - (double)y[3 * j + t];
+      }
+      const double lm = std::sqrt(m[0] * m[0] + m[1] * m[1] + m[2] * m[2]);
+      const double ld = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+      if (!(lm > 0.0) || !(ld > 0.0) || !(std::fabs(lm - ld) <= mu_t)) continue;
+      if (k < cap) {
+        ij[2 * k] = i;
+        ij[2 * k + 1] = j;
+        for (int t = 0; t < 3; ++t) {
+          m_out[3 * k + t] = (float)m[t];
+          n_out[3 * k + t] = (float)d[t];
+        }
+      }
+      ++k;
+    }
+  return k;
+}
+
+// Translation vote: t_i = y_i - R(q) x_i (double, R(q) of P:955-961) for every
+// correspondence, binned on [lo, hi)^3 at `step` ([-5,5]^3, 0.025) with
+// index floor((t - lo) * (1/step)); candidates outside the domain do not vote (R17).  Winner:
+// the fullest bin, ties -> lowest lin; t_out = its centre, t_mean = the mean of its
+// candidates.  Returns 0, or -1 when no candidate falls in the domain.
+int64_t or_translation_vote(const float* x, const float* y, int64_t n, const double* q,
+                            double lo, double hi, double step, int64_t* lin_out,
+                            uint32_t* votes_out, double* t_out, double* t_mean) {
+  double R[9];
+  or_quat_to_R(q, R);
+  const double inv = 1.0 / step;
+  const int64_t Bt = (int64_t)std::llround((hi - lo) * inv);
+  std::vector<int64_t> bins;
+  std::vector<double> ts;
+  for (int64_t i = 0; i < n; ++i) {
+    const double a[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
+    double t[3];
+    bool ok = true;
+    int64_t idx[3];
+    for (int r = 0; r < 3; ++r) {
+      const double ra = R[3 * r] * a[0] + R[3 * r + 1] * a[1] + R[3 * r + 2] * a[2];
+      t[r] = (double)y[3 * i + r] - ra;
+      const double f = std::floor((t[r] - lo) * inv);
+      if (!(f >= 0.0) || !(f < (double)Bt)) ok = false;
+      idx[r] = ok ? (int64_t)f : 0;
+    }
+    if (!ok) continue;
+    bins.push_back((idx[0] * Bt + idx[1]) * Bt + idx[2]);
+    ts.insert(ts.end(), t, t + 3);
+  }
+  if (bins.empty()) return -1;
+  std::vector<int64_t> sorted = bins;
+  std::sort(sorted.begin(), sorted.end());
+  int64_t best = sorted[0], bestc = 0;
+  for (size_t a = 0; a < sorted.size();) {
+    size_t b = a;
+    while (b < sorted.size() && sorted[b] == sorted[a]) ++b;
+    if ((int64_t)(b - a) > bestc) { bestc = (int64_t)(b - a); best = sorted[a]; }
+    a = b;
+  }
+  *lin_out = best;
+  *votes_out = (uint32_t)bestc;
+  const int64_t id[3] = {best / (Bt * Bt), (best / Bt) % Bt, best % Bt};
+  for (int r = 0; r < 3; ++r) t_out[r] = lo + ((double)id[r] + 0.5) * step;
+  double sm[3] = {0, 0, 0};
+  for (size_t e = 0; e < bins.size(); ++e)
+    if (bins[e] == best)
+      for (int r = 0; r < 3; ++r) sm[r] += ts[3 * e + r];
+  for (int r = 0; r < 3; ++r) t_mean[r] = sm[r] / (double)bestc;
+  return 0;
+}
+
 }  // extern "C"

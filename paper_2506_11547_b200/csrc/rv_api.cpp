@@ -23,6 +23,7 @@
 #include "rv_geom.h"
 #include "rv_alg1.h"
 #include "rv_dplan.h"
+#include "rv_rigid.h"
 #include "rv_kernels.h"
 
 namespace {
@@ -203,6 +204,13 @@ struct rv_ctx {
   DevBuf<int32_t> dp_cnt[2], dp_rcnt, dp_ties;
   DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex, dp_lmax;
   DevBuf<unsigned long long> dp_best;
+  DevBuf<float> rg_m, rg_n;         // NEXT-3: kept pairs
+  DevBuf<int32_t> rg_cnt;
+  DevBuf<int64_t> rg_off, rg_bins;
+  DevBuf<uint32_t> rg_acc;          // translation accumulator (zero between calls)
+  int64_t rg_acc_m = 0;
+  DevBuf<unsigned long long> rg_best;
+  DevBuf<double> rg_sums;
   DevBuf<uint32_t> a1_acc;          // NEXT-4: the Algorithm-1 accumulator (B^3)
   DevBuf<double> a1_tab;            // cos / sin(alpha_j / 2)
   DevBuf<unsigned long long> a1_best;
@@ -922,6 +930,125 @@ int solve_multi_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     out[k].vote_launches = ctx->vote_launches;
   }
   *n_found = found;
+  return RV_OK;
+}
+
+// ---- NEXT-3: rigid pose front end ----------------------------------------------------------
+// R(q) of P:955-961, row-major, each entry evaluated left to right (the translation bins are
+// integers decided on these values, so the order is part of the definition)
+void quat_to_R_rowmajor(const double* q, double* R) {
+  const double q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+  R[0] = q0 * q0 + q1 * q1 - q2 * q2 - q3 * q3;
+  R[1] = 2.0 * (q1 * q2 - q0 * q3);
+  R[2] = 2.0 * (q1 * q3 + q0 * q2);
+  R[3] = 2.0 * (q1 * q2 + q0 * q3);
+  R[4] = q0 * q0 - q1 * q1 + q2 * q2 - q3 * q3;
+  R[5] = 2.0 * (q2 * q3 - q0 * q1);
+  R[6] = 2.0 * (q1 * q3 - q0 * q2);
+  R[7] = 2.0 * (q2 * q3 + q0 * q1);
+  R[8] = q0 * q0 - q1 * q1 - q2 * q2 + q3 * q3;
+}
+
+int translation_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, const double* q,
+                     double lo, double hi, double step, int64_t* lin, uint32_t* votes, double* t,
+                     double* t_mean) {
+  if (!x || !y || !q || !lin || !votes || !t || !t_mean)
+    return ctx->fail(RV_EINVAL, "null argument");
+  if (n < 1 || !(step > 0.0) || !(hi > lo)) return ctx->fail(RV_EINVAL, "bad translation grid");
+  const double inv = 1.0 / step;
+  const int64_t Bt = (int64_t)std::llround((hi - lo) * inv);
+  if (Bt < 1 || Bt > 1024) return ctx->fail(RV_EINVAL, "translation grid of %lld bins per axis", (long long)Bt);
+  const int64_t m = Bt * Bt * Bt;
+  cudaStream_t s = ctx->stream;
+  if (ctx->rg_acc_m != m) {
+    RV_CUDA(ctx->rg_acc.ensure(m), "allocating the translation accumulator");
+    RV_CUDA(cudaMemsetAsync(ctx->rg_acc.p, 0, m * 4, s), "memset");  // kept zero afterwards
+    ctx->rg_acc_m = m;
+  }
+  RV_CUDA(ctx->rg_bins.ensure(n), "allocating");
+  RV_CUDA(ctx->rg_best.ensure(1), "allocating");
+  RV_CUDA(ctx->rg_sums.ensure(3), "allocating");
+  RV_CUDA(cudaMemsetAsync(ctx->rg_best.p, 0, 8, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->rg_sums.p, 0, 24, s), "memset");
+  double R[9];
+  quat_to_R_rowmajor(q, R);
+  rv::launch_translation(x, y, n, R, lo, inv, Bt, ctx->rg_acc.p, ctx->rg_bins.p, ctx->rg_best.p,
+                         ctx->rg_sums.p, s);
+  ctx->launches += 4;
+  RV_CUDA(cudaGetLastError(), "launching the translation vote");
+  unsigned long long hb = 0;
+  double hs[3];
+  RV_CUDA(cudaMemcpyAsync(&hb, ctx->rg_best.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hs, ctx->rg_sums.p, 24, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "translation vote");
+  if (hb == 0) return ctx->fail(RV_EDATA, "no translation candidate inside the grid");
+  const int64_t L = (int64_t)(0xffffffffu - (uint32_t)(hb & 0xffffffffu));
+  *lin = L;
+  *votes = (uint32_t)(hb >> 32);
+  const int64_t id[3] = {L / (Bt * Bt), (L / Bt) % Bt, L % Bt};
+  for (int r = 0; r < 3; ++r) {
+    t[r] = lo + ((double)id[r] + 0.5) * step;
+    t_mean[r] = hs[r] / (double)*votes;
+  }
+  return RV_OK;
+}
+
+int rigid_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double mu_t, double eps,
+               int32_t levels, double lo, double hi, double step, rv_rigid_result* out,
+               int32_t* pair_ij, int64_t pair_cap) {
+  if (!x || !y || !out) return ctx->fail(RV_EINVAL, "x, y and out must be non-null");
+  if (n < 2 || n > (1 << 20)) return ctx->fail(RV_EINVAL, "n must lie in [2, 2^20]");
+  if (!(mu_t >= 0.0)) return ctx->fail(RV_EINVAL, "mu_t must be >= 0");
+  cudaStream_t s = ctx->stream;
+  std::memset(out, 0, sizeof(*out));
+  cudaEvent_t e[4];
+  for (auto& v : e) RV_CUDA(cudaEventCreate(&v), "event");
+  struct Ev { cudaEvent_t* e; ~Ev() { for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]); } } guard_ev{e};
+  RV_CUDA(cudaEventRecord(e[0], s), "event");
+  // K9: the kept pairs, in pair order
+  const int64_t nb = rv::pairs_ctas(n);
+  RV_CUDA(ctx->rg_cnt.ensure(std::max<int64_t>(1, nb)), "allocating");
+  RV_CUDA(ctx->rg_off.ensure(nb + 1), "allocating");
+  rv::launch_pairs_count(x, y, n, mu_t, ctx->rg_cnt.p, ctx->rg_off.p, s);
+  int64_t kept = 0;
+  RV_CUDA(cudaMemcpyAsync(&kept, ctx->rg_off.p + nb, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "pair count");
+  out->pairs_total = n * (n - 1) / 2;
+  out->pairs_kept = kept;
+  if (kept < 2) return ctx->fail(RV_EDATA, "only %lld pairs pass the length check", (long long)kept);
+  if (kept > ctx->cfg.max_n)
+    return ctx->fail(RV_EINVAL, "%lld pairs pass the length check but max_n = %lld",
+                     (long long)kept, (long long)ctx->cfg.max_n);
+  RV_CUDA(ctx->rg_m.ensure(3 * kept), "allocating pairs");
+  RV_CUDA(ctx->rg_n.ensure(3 * kept), "allocating pairs");
+  rv::launch_pairs_write(x, y, n, mu_t, ctx->rg_off.p, ctx->rg_m.p, ctx->rg_n.p,
+                         (pair_ij && pair_cap >= kept) ? pair_ij : nullptr, s);
+  ctx->launches += 3;
+  RV_CUDA(cudaGetLastError(), "launching the pair kernels");
+  RV_CUDA(cudaEventRecord(e[1], s), "event");
+  // the rotation vote on the pairs
+  rv_result rot{};
+  if (int rc = solve_impl(ctx, ctx->rg_m.p, ctx->rg_n.p, kept, eps, levels, &rot, nullptr))
+    return rc;
+  RV_CUDA(cudaEventRecord(e[2], s), "event");
+  // K10: the translation vote with the refined rotation
+  int64_t lin = 0;
+  if (int rc = translation_impl(ctx, x, y, n, rot.q, lo, hi, step, &lin, &out->t_votes, out->t,
+                                out->t_mean))
+    return rc;
+  RV_CUDA(cudaEventRecord(e[3], s), "event");
+  RV_CUDA(cudaEventSynchronize(e[3]), "event");
+  const int64_t Bt = (int64_t)std::llround((hi - lo) / step);
+  out->t_cell[0] = (int32_t)(lin / (Bt * Bt));
+  out->t_cell[1] = (int32_t)((lin / Bt) % Bt);
+  out->t_cell[2] = (int32_t)(lin % Bt);
+  std::memcpy(out->q, rot.q, sizeof(out->q));
+  out->rot_votes = rot.votes;
+  out->rot_inliers = rot.n_inliers;
+  cudaEventElapsedTime(&out->ms, e[0], e[3]);
+  cudaEventElapsedTime(&out->pairs_ms, e[0], e[1]);
+  cudaEventElapsedTime(&out->rot_ms, e[1], e[2]);
+  cudaEventElapsedTime(&out->trans_ms, e[2], e[3]);
   return RV_OK;
 }
 
@@ -1855,6 +1982,8 @@ void rot_vote_destroy(rv_ctx* ctx) {
   }
   ctx->dp_lb.release(); ctx->dp_act.release(); ctx->dp_rcnt.release(); ctx->dp_ties.release();
   ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release(); ctx->dp_lmax.release();
+  ctx->rg_m.release(); ctx->rg_n.release(); ctx->rg_cnt.release(); ctx->rg_off.release();
+  ctx->rg_bins.release(); ctx->rg_acc.release(); ctx->rg_best.release(); ctx->rg_sums.release();
   ctx->dp_best.release(); ctx->a1_acc.release(); ctx->a1_tab.release(); ctx->a1_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
   ctx->dp_icnt.release(); ctx->dp_phase.release(); ctx->dp_err.release();
   ctx->dp_pcnt.release(); ctx->dp_scnt.release(); ctx->dp_poff.release(); ctx->dp_sbase.release();
@@ -2002,6 +2131,25 @@ int rot_vote_solve_multi(rv_ctx* ctx, const float* x, const float* y, int64_t n,
   cudaSetDevice(ctx->cfg.device);
   ctx->reset_counters();
   return solve_multi_impl(ctx, x, y, n, eps, levels, K, rho, out, n_found);
+}
+
+int rot_vote_rigid(rv_ctx* ctx, const float* x, const float* y, int64_t n, double mu_t,
+                   double eps, int32_t levels, double t_lo, double t_hi, double t_step,
+                   rv_rigid_result* out, int32_t* pair_ij, int64_t pair_cap) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  ctx->reset_counters();
+  return rigid_impl(ctx, x, y, n, mu_t, eps, levels, t_lo, t_hi, t_step, out, pair_ij, pair_cap);
+}
+
+int rot_vote_translation(rv_ctx* ctx, const float* x, const float* y, int64_t n,
+                         const double* q, double t_lo, double t_hi, double t_step,
+                         int64_t* lin, uint32_t* votes, double* t, double* t_mean) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  return translation_impl(ctx, x, y, n, q, t_lo, t_hi, t_step, lin, votes, t, t_mean);
 }
 
 int rot_vote_alg1(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t J,

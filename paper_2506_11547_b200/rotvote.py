@@ -59,6 +59,14 @@ class rv_alg1_result(C.Structure):
                 ("vote_ms", C.c_float)]
 
 
+class rv_rigid_result(C.Structure):
+    _fields_ = [("q", C.c_double * 4), ("t", C.c_double * 3), ("t_mean", C.c_double * 3),
+                ("rot_votes", C.c_uint32), ("rot_inliers", C.c_uint32), ("t_votes", C.c_uint32),
+                ("t_cell", C.c_int32 * 3), ("pad_", C.c_int32), ("pairs_total", C.c_int64),
+                ("pairs_kept", C.c_int64), ("ms", C.c_float), ("pairs_ms", C.c_float),
+                ("rot_ms", C.c_float), ("trans_ms", C.c_float)]
+
+
 class rv_plan_result(C.Structure):
     _fields_ = [("lin", C.c_uint32), ("B", C.c_int32), ("votes", C.c_uint32), ("n_tied", C.c_int32),
                 ("lb_star", C.c_uint32), ("n_rechecked", C.c_int32), ("pair_votes", C.c_uint64),
@@ -94,6 +102,10 @@ def lib() -> C.CDLL:
     L.rot_vote_count_cells.argtypes = [vp, vp, vp, i64, i32, vp, i64, dbl, i32, vp, vp]
     L.rot_vote_refine.argtypes = [vp, vp, vp, i64, dbl, vp, i32, vp, vp, vp, vp]
     L.rot_vote_alg1.argtypes = [vp, vp, vp, i64, i32, C.POINTER(rv_alg1_result), vp]
+    L.rot_vote_rigid.argtypes = [vp, vp, vp, i64, dbl, dbl, i32, dbl, dbl, dbl,
+                                 C.POINTER(rv_rigid_result), vp, i64]
+    L.rot_vote_translation.argtypes = [vp, vp, vp, i64, vp, dbl, dbl, dbl, C.POINTER(i64),
+                                       C.POINTER(C.c_uint32), vp, vp]
     L.rot_vote_solve_multi.argtypes = [vp, vp, vp, i64, dbl, i32, i32, dbl, C.POINTER(rv_result),
                                        C.POINTER(i32)]
     L.rot_vote_debug_tc_scores.argtypes = [vp, vp, vp, i64, i32, vp, i64, dbl, vp]
@@ -315,6 +327,37 @@ class RotVote:
             self.ctx, _dptr(x, torch.float32, "x"), _dptr(y, torch.float32, "y"), x.shape[0],
             float(eps), int(levels), int(K), float(rho), out, C.byref(nf)))
         return [Result.from_c(out[k]) for k in range(nf.value)]
+
+    def rigid(self, x, y, mu_t: float, eps: float, levels: int = 0, t_lo: float = -5.0,
+              t_hi: float = 5.0, t_step: float = 0.025, pair_ij=None) -> dict:
+        """NEXT-3: rigid pose from point correspondences (pairs + length check -> rotation
+        vote -> translation vote).  pair_ij: optional CUDA int32 tensor [cap, 2] receiving the
+        kept pairs' (i, j)."""
+        import torch
+        r = rv_rigid_result()
+        pp, cap = None, 0
+        if pair_ij is not None:
+            pp, cap = _dptr(pair_ij, torch.int32, "pair_ij"), pair_ij.shape[0]
+        _check(self.ctx, lib().rot_vote_rigid(
+            self.ctx, _dptr(x, torch.float32, "x"), _dptr(y, torch.float32, "y"), x.shape[0],
+            float(mu_t), float(eps), int(levels), float(t_lo), float(t_hi), float(t_step),
+            C.byref(r), pp, int(cap)))
+        return {f: (np.array(getattr(r, f)[:]) if f in ("q", "t", "t_mean") else
+                    tuple(getattr(r, f)[:]) if f == "t_cell" else getattr(r, f))
+                for f, _ in rv_rigid_result._fields_ if f != "pad_"}
+
+    def translation(self, x, y, q, t_lo: float = -5.0, t_hi: float = 5.0,
+                    t_step: float = 0.025):
+        """The translation vote alone for rotation q: (lin, votes, bin centre, mean)."""
+        import torch
+        qq = np.ascontiguousarray(q, np.float64)
+        lin, votes = C.c_int64(), C.c_uint32()
+        t, tm = np.zeros(3), np.zeros(3)
+        _check(self.ctx, lib().rot_vote_translation(
+            self.ctx, _dptr(x, torch.float32, "x"), _dptr(y, torch.float32, "y"), x.shape[0],
+            qq.ctypes.data, float(t_lo), float(t_hi), float(t_step), C.byref(lin),
+            C.byref(votes), t.ctypes.data, tm.ctypes.data))
+        return lin.value, votes.value, t, tm
 
     def alg1(self, x, y, J: int = 180, acc=None):
         """NEXT-4: the paper's Algorithm 1 (J samples per circle, dense B^3 accumulator,
