@@ -199,9 +199,10 @@ struct rv_ctx {
   int32_t grid_host_B = 0;
   // device-resident batched level loop (rv_dplan.cu): ping-pong block lists + counts, the
   // per-problem offsets/counts/picks/bounds, the recheck lists and the winners
-  DevBuf<uint32_t> dp_lins[2], dp_ca[2], dp_cb[2];
-  DevBuf<int64_t> dp_off[2], dp_lb, dp_act;
-  DevBuf<int32_t> dp_cnt[2], dp_rcnt, dp_ties;
+  // sets 0 / 1: ping-pong level lists; set 2: the re-dive's lists
+  DevBuf<uint32_t> dp_lins[3], dp_ca[3], dp_cb[3];
+  DevBuf<int64_t> dp_off[3], dp_lb, dp_lb2, dp_actr[2], dp_bring[3];
+  DevBuf<int32_t> dp_cnt[3], dp_rcnt, dp_ties, dp_rflag, dp_rany, dp_rdone;
   DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex, dp_lmax;
   DevBuf<unsigned long long> dp_best;
   DevBuf<float> rg_m, rg_n;         // NEXT-3: kept pairs
@@ -1381,13 +1382,15 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     return vote_level_sharded(ctx, x, y, rows, koff, eps, mode, B, Ld, (entries + W - 1) / W, nmax);
   };
   // per-phase block counts, kept on the device and read once at the end
-  const int max_ph = 2 * L + 1;
+  const int max_ph = 3 * L + 1;
   RV_CUDA(ctx->dp_phase.ensure((size_t)max_ph * PL), "allocating");
   int nph = 0;
-  auto keep_phase = [&](const int32_t* dcnt) -> int {
+  std::vector<char> ph_optional;  // re-dive phases: absent for problems that did not re-dive
+  auto keep_phase = [&](const int32_t* dcnt, bool optional = false) -> int {
     RV_CUDA(cudaMemcpyAsync(ctx->dp_phase.p + (size_t)nph * PL, dcnt, PL * 4,
                             cudaMemcpyDeviceToDevice, s), "D2D");
     ++nph;
+    ph_optional.push_back(optional ? 1 : 0);
     return RV_OK;
   };
   ctx->ev_reset();
@@ -1472,12 +1475,19 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   }
   // ---- branch and bound from the level-0 survivors (UB >= lb*).  A list of problem p has
   // act[p+1] - act[p] entries stored from base[p]; its children get the capacity region
-  // act[p] * f^3 .. act[p+1] * f^3 (parents x f^3).
-  RV_CUDA(ctx->dp_act.ensure(PL + 1), "allocating");
+  // act[p] * f^3 .. act[p+1] * f^3 (parents x f^3).  Lists alternate between sets 0 and 1;
+  // their offsets live in rings (act: 2, base: 3), so a level's parents' offsets survive the
+  // scan of its children -- the re-dive (R18) needs them.
+  //   parents' act of level l = dp_actr[l & 1]   (the scan writes the children's into the other)
+  //   children's base of level l = dp_bring[l % 3], parents' = dp_bring[(l - 1) % 3]
+  for (int r = 0; r < 2; ++r) RV_CUDA(ctx->dp_actr[r].ensure(PL + 1), "allocating");
+  for (int r = 0; r < 3; ++r) RV_CUDA(ctx->dp_bring[r].ensure(PL + 1), "allocating");
   RV_CUDA(ctx->dp_tot.ensure(1), "allocating");
   RV_CUDA(ctx->down.ensure(256), "allocating staging");
+  RV_CUDA(ctx->dp_rdone.ensure(PL), "allocating");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_rdone.p, 0, PL * 4, s), "memset");
   for (int32_t p = 0; p <= PL; ++p) hbase[p] = (int64_t)p * m0;  // level 0: act == base
-  RV_CUDA(cudaMemcpyAsync(ctx->dp_act.p, hbase.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
+  RV_CUDA(cudaMemcpyAsync(ctx->dp_actr[1].p, hbase.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
           "H2D");
   int64_t ptotal = (int64_t)PL * m0;
   const uint32_t* plins = ctx->grid_list.p;
@@ -1488,59 +1498,129 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     // children base of BnB level 1: act * f^3
     const int32_t f = ch[1] / ch[0];
     const int64_t f3 = (int64_t)f * f * f;
-    RV_CUDA(ctx->dp_off[1].ensure(PL + 1), "allocating");
     for (int32_t p = 0; p <= PL; ++p) hbase[p] = (int64_t)p * m0 * f3;
-    RV_CUDA(cudaMemcpyAsync(ctx->dp_off[1].p, hbase.data(), (PL + 1) * 8, cudaMemcpyHostToDevice, s),
-            "H2D");
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_bring[1].p, hbase.data(), (PL + 1) * 8, cudaMemcpyHostToDevice,
+                            s), "H2D");
   }
   for (int l = 1; l < L; ++l) {
     const int nb = cur == 1 ? 0 : 1;  // level 1 -> set 1 (set 0 still holds the dive lists)
     const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1];
     const int64_t f3 = (int64_t)f * f * f;
     const int64_t cap_total = std::max<int64_t>(1, ptotal * f3) + slack;
+    int64_t* pact = ctx->dp_actr[l & 1].p;          // parents' act
+    int64_t* cact = ctx->dp_actr[(l + 1) & 1].p;    // children's act (written by the scan)
+    int64_t* cbase = ctx->dp_bring[l % 3].p;        // children's base
+    int64_t* pbase = shared ? pact : ctx->dp_bring[(l + 2) % 3].p;  // parents' base
+    int64_t* nbase = ctx->dp_bring[(l + 1) % 3].p;  // grandchildren's base (scan output)
     RV_CUDA(ctx->dp_lins[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_ca[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_cb[nb].ensure(cap_total), "allocating");
     RV_CUDA(ctx->dp_cnt[nb].ensure(PL), "allocating");
-    RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
-    // dp_off[nb] = the children's base (written by the previous scan, or above for level 1)
-    if (shard) {  // identical list on every rank: children placed by a prefix over parents
+    if (shard) {
       RV_CUDA(ctx->dp_pcnt.ensure(std::max<int64_t>(1, ptotal)), "allocating");
       RV_CUDA(ctx->dp_poff.ensure(ptotal + 1), "allocating");
-      rv::dp_launch_expand_ordered(plins, shared, ctx->dp_act.p,
-                                   shared ? ctx->dp_act.p : ctx->dp_off[cur].p, pub, ctx->dp_lb.p,
-                                   PL, ptotal, Bp, f, ctx->dp_off[nb].p, ctx->dp_lins[nb].p,
-                                   ctx->dp_ca[nb].p, ctx->dp_cb[nb].p, ctx->dp_cnt[nb].p,
-                                   ctx->dp_pcnt.p, ctx->dp_poff.p, s);
-      ctx->launches += 2;
-    } else {
-      rv::dp_launch_bnb_expand(plins, shared, ctx->dp_act.p,
-                               shared ? ctx->dp_act.p : ctx->dp_off[cur].p, pub, ctx->dp_lb.p, PL,
-                               ptotal, Bp, f, ctx->dp_off[nb].p, ctx->dp_lins[nb].p,
-                               ctx->dp_ca[nb].p, ctx->dp_cb[nb].p, ctx->dp_cnt[nb].p,
-                               ctx->dp_err.p, s);
     }
-    if (int rc = keep_phase(ctx->dp_cnt[nb].p)) return rc;
-    // the children's act offsets, and the grandchildren's base (into the other set's dp_off)
-    const int other = nb == 0 ? 1 : 0;
+    auto expand = [&]() {
+      RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
+      if (shard) {  // identical list on every rank: children placed by a prefix over parents
+        rv::dp_launch_expand_ordered(plins, shared, pact, pbase, pub, ctx->dp_lb.p, PL, ptotal, Bp,
+                                     f, cbase, ctx->dp_lins[nb].p, ctx->dp_ca[nb].p,
+                                     ctx->dp_cb[nb].p, ctx->dp_cnt[nb].p, ctx->dp_pcnt.p,
+                                     ctx->dp_poff.p, s);
+        ctx->launches += 3;
+      } else {
+        rv::dp_launch_bnb_expand(plins, shared, pact, pbase, pub, ctx->dp_lb.p, PL, ptotal, Bp, f,
+                                 cbase, ctx->dp_lins[nb].p, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p,
+                                 ctx->dp_cnt[nb].p, ctx->dp_err.p, s);
+        ctx->launches += 1;
+      }
+      return RV_OK;
+    };
     int64_t nf3 = 1;
     if (l + 1 < L) {
       const int64_t nf = ch[l + 1] / ch[l];
       nf3 = nf * nf * nf;
     }
-    RV_CUDA(ctx->dp_off[other].ensure(PL + 1), "allocating");
-    rv::dp_launch_scan(ctx->dp_cnt[nb].p, PL, nf3, ctx->dp_act.p, ctx->dp_off[other].p,
-                       ctx->dp_tot.p, s);
-    ctx->launches += 2;
-    ctx->down.reset();
-    int64_t* ht = ctx->down.take<int64_t>(1);
-    RV_CUDA(cudaMemcpyAsync(ht, ctx->dp_tot.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
-    RV_CUDA(cudaStreamSynchronize(s), "batched level");
-    ctx->collect_vote_ms();
-    const int64_t ctotal = *ht;
+    // the children's act offsets and the grandchildren's base, and (level >= 2) the re-dive
+    // trigger (R18, as rv_plan.cpp: a problem whose level keeps >= 16384 blocks and more than
+    // half of all possible children dives again from its best-excess parent block, once per
+    // problem); then the total and the trigger on the host
+    RV_CUDA(ctx->dp_rflag.ensure(PL), "allocating");
+    RV_CUDA(ctx->dp_rany.ensure(1), "allocating");
+    auto scan_and_read = [&](int64_t* total, int32_t* any) -> int {
+      rv::RediveCheck chk{cur >= 0 ? ctx->dp_cnt[cur].p : nullptr, f3, ctx->dp_rdone.p,
+                          ctx->dp_rflag.p, ctx->dp_rany.p};
+      if (any) RV_CUDA(cudaMemsetAsync(ctx->dp_rany.p, 0, 4, s), "memset");
+      rv::dp_launch_scan(ctx->dp_cnt[nb].p, PL, nf3, cact, nbase, ctx->dp_tot.p, s,
+                         any ? &chk : nullptr);
+      ctx->launches += 1;
+      ctx->down.reset();
+      int64_t* ht = ctx->down.take<int64_t>(1);
+      int32_t* ha = ctx->down.take<int32_t>(1);
+      RV_CUDA(cudaMemcpyAsync(ht, ctx->dp_tot.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+      if (any) RV_CUDA(cudaMemcpyAsync(ha, ctx->dp_rany.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+      RV_CUDA(cudaStreamSynchronize(s), "batched level");
+      ctx->collect_vote_ms();
+      *total = *ht;
+      if (any) *any = *ha;
+      return RV_OK;
+    };
+    if (int rc = expand()) return rc;
+    int64_t ctotal = 0;
+    int32_t any = 0;
+    if (int rc = scan_and_read(&ctotal, l >= 2 ? &any : nullptr)) return rc;
+    {
+      if (any) {
+        RV_CUDA(ctx->dp_lb2.ensure(PL), "allocating");
+        rv::dp_launch_dive_pick(ctx->dp_lins[cur].p, ctx->dp_ca[cur].p, pbase, ctx->dp_cnt[cur].p,
+                                ch[l - 1], eps, ctx->rows.p, ctx->dp_pick.p, PL, s);
+        ctx->launches += 1;
+        for (int lv = l; lv < L; ++lv) {
+          const int32_t rf = ch[lv] / ch[lv - 1], rcap = 27 * rf * rf * rf;
+          const size_t rspan = (size_t)PL * rcap + slack;
+          RV_CUDA(ctx->dp_lins[2].ensure(rspan), "allocating");
+          RV_CUDA(ctx->dp_ca[2].ensure(rspan), "allocating");
+          RV_CUDA(ctx->dp_cb[2].ensure(rspan), "allocating");
+          RV_CUDA(ctx->dp_cnt[2].ensure(PL), "allocating");
+          RV_CUDA(ctx->dp_off[2].ensure(PL + 1), "allocating");
+          for (int32_t p = 0; p <= PL; ++p) hbase[p] = (int64_t)p * rcap;
+          RV_CUDA(cudaMemcpyAsync(ctx->dp_off[2].p, hbase.data(), (PL + 1) * 8,
+                                  cudaMemcpyHostToDevice, s), "H2D");
+          rv::dp_launch_dive_children(ctx->dp_pick.p, nullptr, nullptr, ch[lv - 1], rf,
+                                      ctx->dp_lins[2].p, rcap, ctx->dp_cnt[2].p, PL, s,
+                                      ctx->dp_rflag.p);
+          const int32_t rmode = lv == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
+          RV_CUDA(cudaMemsetAsync(ctx->dp_ca[2].p, 0, rspan * 4, s), "memset");
+          if (rmode == RV_MODE_FINAL)
+            RV_CUDA(cudaMemsetAsync(ctx->dp_cb[2].p, 0, rspan * 4, s), "memset");
+          ctx->launches += 1;
+          if (int rc = keep_phase(ctx->dp_cnt[2].p, true)) return rc;
+          const rv::DpList rl{ctx->dp_lins[2].p, 0, 0, ctx->dp_off[2].p, ctx->dp_cnt[2].p,
+                              ctx->dp_ca[2].p, ctx->dp_cb[2].p};
+          if (int rc = vote(rmode, ch[lv], rl, (int64_t)PL * rcap)) return rc;
+          phase_chunk.push_back(shard ? ((int64_t)rcap + W - 1) / W : 0);
+          if (rmode == RV_MODE_BOUND) {
+            rv::dp_launch_dive_pick(ctx->dp_lins[2].p, ctx->dp_ca[2].p, ctx->dp_off[2].p,
+                                    ctx->dp_cnt[2].p, ch[lv], eps, ctx->rows.p, ctx->dp_pick.p,
+                                    PL, s);
+          } else {
+            rv::dp_launch_max_lo(ctx->dp_cb[2].p, ctx->dp_off[2].p, ctx->dp_cnt[2].p,
+                                 ctx->dp_lb2.p, PL, s);
+            rv::dp_launch_lb_max(ctx->dp_lb.p, ctx->dp_lb2.p, PL, s);
+            ctx->launches += 1;
+          }
+          ctx->launches += 1;
+        }
+        // level l again, with the raised lb* (the parents' offsets are intact in the rings)
+        if (int rc = expand()) return rc;
+        if (int rc = scan_and_read(&ctotal, nullptr)) return rc;
+        tr.mark("  re-dive");
+      }
+    }
+    if (int rc = keep_phase(ctx->dp_cnt[nb].p)) return rc;
     const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
-    const rv::DpList cl{ctx->dp_lins[nb].p, 0, 0, ctx->dp_off[nb].p, ctx->dp_cnt[nb].p,
-                        ctx->dp_ca[nb].p, ctx->dp_cb[nb].p};
+    const rv::DpList cl{ctx->dp_lins[nb].p, 0, 0, cbase, ctx->dp_cnt[nb].p, ctx->dp_ca[nb].p,
+                        ctx->dp_cb[nb].p};
     if (int rc = vote(mode, ch[l], cl, ctotal)) return rc;
     phase_chunk.push_back(shard ? (ctotal + W - 1) / W : 0);
     ptotal = ctotal;
@@ -1551,12 +1631,14 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     tr.mark("  bnb level");
   }
   // ---- finest level: max lo, exact-known blocks, recheck of hi >= max lo, hi != lo; winner
-  // (dp_act holds the final list's act offsets from the last scan; its base is dp_off[cur])
+  // (the last scan, at level L-1, wrote the final list's act into dp_actr[L & 1]; its base is
+  // the ring's dp_bring[(L - 1) % 3])
   const int64_t ftotal = ptotal;
   const uint32_t* flins = ctx->dp_lins[cur].p;
   const uint32_t* fhi = ctx->dp_ca[cur].p;
   const uint32_t* flo = ctx->dp_cb[cur].p;
-  const int64_t* fcap = ctx->dp_off[cur].p;
+  const int64_t* fcap = ctx->dp_bring[(L - 1) % 3].p;
+  int64_t* fact = ctx->dp_actr[L & 1].p;
   RV_CUDA(ctx->dp_rcnt.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_lmax.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_best.ensure(PL), "allocating");
@@ -1568,19 +1650,19 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   RV_CUDA(cudaMemsetAsync(ctx->dp_best.p, 0, PL * 8, s), "memset");
   RV_CUDA(cudaMemsetAsync(ctx->dp_ties.p, 0, PL * 4, s), "memset");
   RV_CUDA(cudaMemsetAsync(ctx->dp_ex.p, 0, std::max<int64_t>(1, ftotal) * 4, s), "memset");
-  rv::dp_launch_final_max(ctx->dp_act.p, fcap, flo, PL, ftotal, ctx->dp_lmax.p, s);
-  rv::dp_launch_final_split(ctx->dp_act.p, fcap, flins, fhi, flo, ctx->dp_lmax.p, PL, ftotal,
+  rv::dp_launch_final_max(fact, fcap, flo, PL, ftotal, ctx->dp_lmax.p, s);
+  rv::dp_launch_final_split(fact, fcap, flins, fhi, flo, ctx->dp_lmax.p, PL, ftotal,
                             ctx->dp_best.p, ctx->dp_rlins.p, ctx->dp_rcnt.p, s);
   ctx->launches += 2;
   if (int rc = keep_phase(ctx->dp_rcnt.p)) return rc;
-  const rv::DpList rl{ctx->dp_rlins.p, 0, 0, ctx->dp_act.p, ctx->dp_rcnt.p, ctx->dp_ex.p,
+  const rv::DpList rl{ctx->dp_rlins.p, 0, 0, fact, ctx->dp_rcnt.p, ctx->dp_ex.p,
                       ctx->dp_ex.p};
   if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_EXACT, ch[L - 1], rl, PL, ftotal,
                           nmax))
     return rc;
-  rv::dp_launch_final_rechecked(ctx->dp_act.p, ctx->dp_rcnt.p, ctx->dp_rlins.p, ctx->dp_ex.p, PL,
+  rv::dp_launch_final_rechecked(fact, ctx->dp_rcnt.p, ctx->dp_rlins.p, ctx->dp_ex.p, PL,
                                 ftotal, ctx->dp_best.p, s);
-  rv::dp_launch_final_ties(ctx->dp_act.p, fcap, fhi, flo, ctx->dp_rcnt.p, ctx->dp_ex.p, PL, ftotal,
+  rv::dp_launch_final_ties(fact, fcap, fhi, flo, ctx->dp_rcnt.p, ctx->dp_ex.p, PL, ftotal,
                            ctx->dp_best.p, ctx->dp_ties.p, s);
   ctx->launches += 2;
   RV_CUDA(cudaGetLastError(), "launching the level loop");
@@ -1622,7 +1704,11 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
       if (r.n_phases < 16) r.cells_per_phase[r.n_phases++] = c;
     };
     add(m0);
-    for (int ph = 0; ph + 1 < nph; ++ph) add(hph[(size_t)ph * PL + p]);
+    for (int ph = 0; ph + 1 < nph; ++ph) {
+      const int64_t c = hph[(size_t)ph * PL + p];
+      if (ph_optional[ph] && c == 0) continue;  // this problem did not re-dive
+      add(c);
+    }
     if (nre > 0) add(nre);
     if (!shard || !ctx->comm) {
       tc_pairs += (r.pair_votes - (uint64_t)nre * n);
@@ -1976,11 +2062,15 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->hmask.release(); ctx->gather.release(); ctx->grid_list.release();
   ctx->l0cnt.release(); ctx->l0bg.release(); ctx->l0idx.release(); ctx->l0aux.release();
   ctx->l0surv.release(); ctx->atab.release(); ctx->ablk.release();
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < 3; ++b) {
     ctx->dp_lins[b].release(); ctx->dp_ca[b].release(); ctx->dp_cb[b].release();
     ctx->dp_off[b].release(); ctx->dp_cnt[b].release();
   }
-  ctx->dp_lb.release(); ctx->dp_act.release(); ctx->dp_rcnt.release(); ctx->dp_ties.release();
+  ctx->dp_lb2.release();
+  for (int b = 0; b < 2; ++b) ctx->dp_actr[b].release();
+  for (int b = 0; b < 3; ++b) ctx->dp_bring[b].release();
+  ctx->dp_rflag.release(); ctx->dp_rany.release(); ctx->dp_rdone.release();
+  ctx->dp_lb.release(); ctx->dp_rcnt.release(); ctx->dp_ties.release();
   ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release(); ctx->dp_lmax.release();
   ctx->rg_m.release(); ctx->rg_n.release(); ctx->rg_cnt.release(); ctx->rg_off.release();
   ctx->rg_bins.release(); ctx->rg_acc.release(); ctx->rg_best.release(); ctx->rg_sums.release();

@@ -72,8 +72,13 @@ __global__ void __launch_bounds__(kDpThreads) dp_dive_children(const uint32_t* _
                                                                const uint32_t* __restrict__ idx_list,
                                                                int32_t Bp, int32_t f,
                                                                uint32_t* out, int32_t cap,
-                                                               int32_t* cnt) {
+                                                               int32_t* cnt,
+                                                               const int32_t* __restrict__ active) {
   const int p = blockIdx.x;
+  if (active && !active[p]) {  // re-dive: this problem did not trigger it
+    if (threadIdx.x == 0) cnt[p] = 0;
+    return;
+  }
   __shared__ uint32_t par[27];
   __shared__ int npar, wsum[kDpThreads / 32];
   if (threadIdx.x == 0)
@@ -536,12 +541,24 @@ __global__ void dp_items_write(DpList L, const int64_t* __restrict__ rows, int32
 
 __global__ void __launch_bounds__(kPlanThreads) dp_scan(const int32_t* __restrict__ cnt, int32_t P,
                                                         int64_t f3, int64_t* act,
-                                                        int64_t* next_base, int64_t* total) {
+                                                        int64_t* next_base, int64_t* total,
+                                                        RediveCheck rc) {
   __shared__ int64_t sh[kPlanThreads];
   const int t = threadIdx.x;
   const int p0 = (int)((int64_t)P * t / kPlanThreads), p1 = (int)((int64_t)P * (t + 1) / kPlanThreads);
   int64_t v = 0;
-  for (int p = p0; p < p1; ++p) v += cnt[p];
+  for (int p = p0; p < p1; ++p) {
+    v += cnt[p];
+    if (rc.flags) {  // re-dive trigger (R18), once per problem
+      const int32_t fl = (!rc.done[p] && rc.pcnt[p] > 0 && cnt[p] >= 16384 &&
+                          2 * (int64_t)cnt[p] > (int64_t)rc.pcnt[p] * rc.f3) ? 1 : 0;
+      rc.flags[p] = fl;
+      if (fl) {
+        rc.done[p] = 1;
+        atomicOr(rc.any, 1);
+      }
+    }
+  }
   int64_t tot;
   int64_t e = cta_scan_excl(v, sh, &tot);
   for (int p = p0; p < p1; ++p) {
@@ -647,11 +664,22 @@ __global__ void dp_slice(const int64_t* __restrict__ base, const int32_t* __rest
   cnt_out[0] = (int32_t)c;
 }
 
+// lb[p] = max(lb[p], lb2[p])
+__global__ void dp_lb_max(int64_t* lb, const int64_t* __restrict__ lb2, int32_t P) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x)
+    if (lb2[p] > lb[p]) lb[p] = lb2[p];
+}
+
 // --- launchers ------------------------------------------------------------------------------
 void dp_launch_dive_children(const uint32_t* pick, const int32_t* pick_idx,
                              const uint32_t* idx_list, int32_t Bp, int32_t f, uint32_t* out,
-                             int32_t cap, int32_t* cnt, int32_t P, cudaStream_t s) {
-  dp_dive_children<<<P, kDpThreads, 0, s>>>(pick, pick_idx, idx_list, Bp, f, out, cap, cnt);
+                             int32_t cap, int32_t* cnt, int32_t P, cudaStream_t s,
+                             const int32_t* active) {
+  dp_dive_children<<<P, kDpThreads, 0, s>>>(pick, pick_idx, idx_list, Bp, f, out, cap, cnt,
+                                            active);
+}
+void dp_launch_lb_max(int64_t* lb, const int64_t* lb2, int32_t P, cudaStream_t s) {
+  dp_lb_max<<<(P + 255) / 256, 256, 0, s>>>(lb, lb2, P);
 }
 void dp_launch_dive_pick(const uint32_t* lins, const uint32_t* a, const int64_t* off,
                          const int32_t* cnt, int32_t B, double eps, const int64_t* rows,
@@ -687,8 +715,9 @@ void dp_items_bound(int mode, int64_t entries, int32_t P, int64_t nmax, int32_t 
 }
 
 void dp_launch_scan(const int32_t* cnt, int32_t P, int64_t f3, int64_t* act, int64_t* next_base,
-                    int64_t* total, cudaStream_t s) {
-  dp_scan<<<1, kPlanThreads, 0, s>>>(cnt, P, f3, act, next_base, total);
+                    int64_t* total, cudaStream_t s, const RediveCheck* rc) {
+  dp_scan<<<1, kPlanThreads, 0, s>>>(cnt, P, f3, act, next_base, total,
+                                    rc ? *rc : RediveCheck{nullptr, 0, nullptr, nullptr, nullptr});
 }
 
 namespace {

@@ -39,16 +39,29 @@ void dp_launch_items(const DpList& L, const int64_t* rows, const int64_t* koffs,
 // items / ablocks needed for at most `entries` list entries over P problems of <= nmax rows
 void dp_items_bound(int mode, int64_t entries, int32_t P, int64_t nmax, int32_t slots,
                     int64_t* max_items, int64_t* max_ablocks);
+// The re-dive trigger (R18) evaluated by the scan: flags[p] = !done[p] && pcnt[p] > 0 &&
+// cnt[p] >= 16384 && 2 cnt[p] > pcnt[p] * f3 (then done[p] = 1, *any |= 1)
+struct RediveCheck {
+  const int32_t* pcnt;
+  int64_t f3;
+  int32_t* done;
+  int32_t* flags;
+  int32_t* any;
+};
 // act[p] = exclusive prefix of cnt (act[P] = total, also written to *total); next_base[p] =
-// act[p] * f3 (optional)
+// act[p] * f3 (optional); rc: also evaluate the re-dive trigger
 void dp_launch_scan(const int32_t* cnt, int32_t P, int64_t f3, int64_t* act, int64_t* next_base,
-                    int64_t* total, cudaStream_t s);
+                    int64_t* total, cudaStream_t s, const RediveCheck* rc = nullptr);
 
 // dive: candidate children (Bc = f*Bp) of the 27-neighbourhood of the pick (pick[p], or
 // idx_list[pick_idx[p]] if idx_list != nullptr), at out + p*cap
+// (active != nullptr: problems with active[p] == 0 get an empty list -- the re-dive)
 void dp_launch_dive_children(const uint32_t* pick, const int32_t* pick_idx,
                              const uint32_t* idx_list, int32_t Bp, int32_t f, uint32_t* out,
-                             int32_t cap, int32_t* cnt, int32_t P, cudaStream_t s);
+                             int32_t cap, int32_t* cnt, int32_t P, cudaStream_t s,
+                             const int32_t* active = nullptr);
+// lb[p] = max(lb[p], lb2[p])
+void dp_launch_lb_max(int64_t* lb, const int64_t* lb2, int32_t P, cudaStream_t s);
 // dive: pick[p] = the list's max-excess block (planner key)
 void dp_launch_dive_pick(const uint32_t* lins, const uint32_t* a, const int64_t* off,
                          const int32_t* cnt, int32_t B, double eps, const int64_t* rows,

@@ -30,7 +30,7 @@
 
 namespace {
 
-enum Phase { PH_L0, PH_DIVE, PH_NEED_SURV, PH_BNB, PH_RECHECK, PH_DONE };
+enum Phase { PH_L0, PH_DIVE, PH_NEED_SURV, PH_BNB, PH_REDIVE, PH_RECHECK, PH_DONE };
 
 std::vector<uint32_t> candidates_of(int32_t B) {
   std::vector<uint32_t> out;
@@ -96,6 +96,15 @@ struct rv_plan {
   std::vector<uint32_t> cells;  // pending request
 
   std::vector<uint32_t> l0_cells, l0_ub;
+  // re-dive (reading R18): when a branch-and-bound level >= 2 would keep more than half of all
+  // possible children, the dive's lb* is too weak; dive once more from the best-excess block
+  // of the parent level, raise lb* to that dive's finest-level lower bound, and recompute
+  // the survivors
+  // (only for a level of at least kRediveMin blocks: a cheap level needs no stronger bound)
+  static constexpr int64_t kRediveMin = 16384;
+  bool redived = false;
+  int redive_parent = 0;
+  std::vector<uint32_t> redive_cells, redive_ub;
   // NEXT-2 exclusion balls (earlier peaks' block-centre rotations, suppression angle rho):
   // a finest block is excluded iff |q_c . q_e| >= cos(rho/2) (angle <= rho); a coarser block
   // is dropped only when all of it is: angle(q_c, q_e) + r(c) <= rho (r(c) bounds the
@@ -247,6 +256,18 @@ struct rv_plan {
     cells = children(0, surv);
     note_request();
   }
+  // back to branch and bound at the level whose children triggered the re-dive
+  void resume_bnb() {
+    std::vector<uint32_t> surv;
+    for (size_t e = 0; e < redive_cells.size(); ++e)
+      if ((int64_t)redive_ub[e] >= lb_star) surv.push_back(redive_cells[e]);
+    phase = PH_BNB;
+    level = redive_parent;
+    cells = children(level, surv);
+    ++level;
+    mode = mode_for(level);
+    note_request();
+  }
   void start_dive_or_bnb(size_t s) {
     if (l0_cells.empty()) {  // every level-0 block excluded: nothing left
       lb_star = 0;
@@ -358,12 +379,43 @@ struct rv_plan {
           std::vector<uint32_t> surv;
           for (size_t e = 0; e < cells.size(); ++e)
             if ((int64_t)a[e] >= lb_star) surv.push_back(cells[e]);
-          cells = children(level, surv);
+          std::vector<uint32_t> ch = children(level, surv);
+          const int64_t f = chain[level + 1] / chain[level];
+          if (!redived && level >= 1 && !cells.empty() && (int64_t)ch.size() >= kRediveMin &&
+              2 * (int64_t)ch.size() > (int64_t)cells.size() * f * f * f) {
+            redived = true;
+            redive_parent = level;
+            redive_cells = cells;
+            redive_ub.assign(a, a + cells.size());
+            const uint32_t pick = cells[best_excess(level, cells, a)];
+            phase = PH_REDIVE;
+            cells = children(level, neighbourhood(level, pick));
+            ++level;
+            mode = mode_for(level);
+            if (cells.empty()) { resume_bnb(); return 0; }
+            note_request();
+            return 0;
+          }
+          cells = std::move(ch);
           ++level;
           mode = mode_for(level);
           note_request();
         } else {
           enter_final(a, b);
+        }
+        return 0;
+      }
+      case PH_REDIVE: {
+        if (mode == RV_MODE_BOUND) {
+          const uint32_t pick = cells[best_excess(level, cells, a)];
+          cells = children(level, neighbourhood(level, pick));
+          ++level;
+          mode = mode_for(level);
+          if (cells.empty()) { resume_bnb(); return 0; }
+          note_request();
+        } else {
+          for (size_t e = 0; e < cells.size(); ++e) lb_star = std::max<int64_t>(lb_star, b[e]);
+          resume_bnb();
         }
         return 0;
       }
