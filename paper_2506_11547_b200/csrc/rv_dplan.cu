@@ -341,21 +341,45 @@ __device__ __forceinline__ int64_t list_m(const DpList& L, int p) {
   return L.cnt ? (int64_t)L.cnt[p] : L.shared_m;
 }
 
-// CTA-wide exclusive scan of one int64 per thread (kPlanThreads threads)
+// CTA-wide exclusive scan of one int64 per thread (kPlanThreads threads): warp shuffles,
+// then the warp totals scanned by warp 0 -- two barriers
 __device__ int64_t cta_scan_excl(int64_t v, int64_t* sh, int64_t* total) {
-  const int t = threadIdx.x;
-  sh[t] = v;
-  __syncthreads();
-  for (int o = 1; o < kPlanThreads; o <<= 1) {
-    const int64_t add = t >= o ? sh[t - o] : 0;
-    __syncthreads();
-    sh[t] += add;
-    __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
-  const int64_t incl = sh[t];
-  *total = sh[kPlanThreads - 1];
+  if (lane == 31) sh[warp] = x;  // warp inclusive total
   __syncthreads();
-  return incl - v;
+  if (warp == 0) {
+    int64_t w = lane < kPlanThreads / 32 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    sh[32 + lane] = w;  // inclusive prefix of the warp totals
+  }
+  __syncthreads();
+  const int64_t before = warp > 0 ? sh[32 + warp - 1] : 0;
+  *total = sh[32 + kPlanThreads / 32 - 1];
+  __syncthreads();  // sh is reused by the next call
+  return before + x - v;
+}
+
+// CTA-wide max of one int64 per thread
+__device__ int64_t cta_max(int64_t v, int64_t* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = i64max(v, __shfl_down_sync(0xffffffffu, v, o));
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  int64_t r = sh[0];
+  for (int w = 1; w < kPlanThreads / 32; ++w) r = i64max(r, sh[w]);
+  __syncthreads();
+  return r;
 }
 }  // namespace
 
@@ -380,14 +404,8 @@ __global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
   int64_t tot;
   cta_scan_excl(cbs, sh, &tot);
   if (t == 0) s_cbs = tot;
-  // max of tmax
-  sh[t] = tmax;
-  __syncthreads();
-  for (int o = kPlanThreads / 2; o > 0; o >>= 1) {
-    if (t < o) sh[t] = i64max(sh[t], sh[t + o]);
-    __syncthreads();
-  }
-  if (t == 0) s_tmax = sh[0];
+  const int64_t tmx = cta_max(tmax, sh);
+  if (t == 0) s_tmax = tmx;
   __syncthreads();
   {
     // correspondence chunks per item: fill whole waves of the persistent kernel's CTAs (the
@@ -407,22 +425,21 @@ __global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
         if (score > my_s + 1e-9) { my_s = score; my_n = nch; }
       }
     }
-    __shared__ double ss[kPlanThreads];
-    ss[t] = my_s;
-    __syncthreads();
-    for (int o = kPlanThreads / 2; o > 0; o >>= 1) {
-      if (t < o) ss[t] = ss[t] > ss[t + o] ? ss[t] : ss[t + o];
-      __syncthreads();
+    __shared__ double ss[kPlanThreads / 32];
+    double m = my_s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_down_sync(0xffffffffu, m, o);
+      m = y > m ? y : m;
     }
-    const double top = ss[0];
+    if ((t & 31) == 0) ss[t >> 5] = m;
     __syncthreads();
-    sh[t] = (my_s > top - 1e-9) ? my_n : INT64_MAX;
-    __syncthreads();
-    for (int o = kPlanThreads / 2; o > 0; o >>= 1) {
-      if (t < o) sh[t] = i64min(sh[t], sh[t + o]);
-      __syncthreads();
-    }
-    if (t == 0) s_nch = (int32_t)(sh[0] == INT64_MAX ? 1 : sh[0]);
+    double top = ss[0];
+    for (int w = 1; w < kPlanThreads / 32; ++w) top = ss[w] > top ? ss[w] : top;
+    // smallest chunk count whose score is within 1e-9 of the best
+    const int64_t cand = (my_s > top - 1e-9) ? my_n : INT64_MAX;
+    const int64_t best_n = -cta_max(-cand, sh);
+    if (t == 0) s_nch = (int32_t)(best_n == INT64_MAX ? 1 : best_n);
   }
   __syncthreads();
   const int64_t nch_all = s_nch;

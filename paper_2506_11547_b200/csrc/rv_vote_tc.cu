@@ -221,6 +221,10 @@ void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const 
 #endif
 constexpr int kTcEpiWarps = RV_TC_EPI_WARPS;  // multiple of 4 (one lane quarter per SMSP)
 [[maybe_unused]] constexpr int kTcSplit = kTcEpiWarps / 4;  // warps per lane quarter
+#ifndef RV_TC_ABUFS
+#define RV_TC_ABUFS 2
+#endif
+constexpr int kTcABufs = RV_TC_ABUFS;  // A-operand buffers (items of lookahead for its TMA)
 constexpr int kTcEpi0 = 2;                    // first epilogue warp
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // producer, MMA, epilogue warps
 constexpr int kTcAccCols = kTcAcc * kTcN;  // = 512: the whole TMEM
@@ -231,8 +235,9 @@ static_assert(!RV_TC_PINGPONG || (kTcAcc == 2 && kTcEpiWarps == 8),
 
 struct __align__(1024) TcSmem {
   uint8_t b[kTcStages][kTileBytes];  // correspondence tiles
-  uint8_t a[2][128 * 64];            // A operand (128 rows x 32 fp16), double-buffered
-  uint64_t full[kTcStages], empty[kTcStages], tfull[kTcAcc], tempty[kTcAcc], afull[2], aempty[2];
+  uint8_t a[kTcABufs][128 * 64];     // A operand (128 rows x 32 fp16), kTcABufs buffers
+  uint64_t full[kTcStages], empty[kTcStages], tfull[kTcAcc], tempty[kTcAcc], afull[kTcABufs],
+      aempty[kTcABufs];
   uint32_t tmem_base;
 };
 
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       bar_init(&sm.tfull[b], 1);
       bar_init(&sm.tempty[b], RV_TC_PINGPONG ? kTcEpiWarps / 2 : kTcEpiWarps);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kTcABufs; ++b) {
       bar_init(&sm.afull[b], 1);
       bar_init(&sm.aempty[b], 1);
     }
@@ -345,8 +350,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       uint32_t gt = 0, gi = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
         const VoteItem it = items[idx];
-        const uint32_t ab = gi & 1;
-        if (gi >= 2) bar_wait(&sm.aempty[ab], ((gi >> 1) - 1) & 1);
+        const uint32_t ab = gi % kTcABufs;
+        if (gi >= (uint32_t)kTcABufs) bar_wait(&sm.aempty[ab], ((gi / kTcABufs) - 1) & 1);
         bar_expect_tx(&sm.afull[ab], (uint32_t)kTcABlockBytes);
         bulk_g2s(sm.a[ab], atab + (int64_t)it.ablk * kTcABlockBytes, (uint32_t)kTcABlockBytes,
                  &sm.afull[ab]);
@@ -370,8 +375,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       uint32_t gt = 0, gi = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
         const int ntiles = items[idx].ni / kTcN;
-        const uint32_t ab = gi & 1;
-        bar_wait(&sm.afull[ab], (gi >> 1) & 1);
+        const uint32_t ab = gi % kTcABufs;
+        bar_wait(&sm.afull[ab], (gi / kTcABufs) & 1);
         const uint32_t a0 = su32(sm.a[ab]);
         for (int t = 0; t < ntiles; ++t, ++gt) {
           const uint32_t s = gt % kTcStages, b = gt % kTcAcc;
