@@ -84,6 +84,11 @@ typedef struct {
                             another on this GPU (loopback); 0/1 = off.  Requires world == 1. */
   int32_t tensor_vote;   /* 1: bound-level votes on the tensor cores (K3-TC, tcgen05, fp16-split
                             operands, fp32 accumulation); 0: FP32-pipe FFMA2 vote everywhere */
+  int32_t cull;          /* 1 (needs tensor_vote): ancestor culling -- level 0 writes each block's
+                            pass bitmask, every finer level votes its blocks only against the
+                            correspondences that passed their level-0 ancestor's bound test
+                            (K3-C; the certified argument is in DESIGN.md §6).  Same result; applies
+                            to the device level loop when the bitmasks fit (<= 4 GiB).  0: off */
 } rv_config;
 
 typedef struct {
@@ -95,7 +100,8 @@ typedef struct {
   int32_t  flags;         /* RV_REFINED | RV_DEGENERATE | RV_RECHECKED */
   int32_t  B;             /* finest resolution */
   int32_t  n_tied;        /* finest blocks sharing the winning count */
-  uint64_t pair_votes;    /* sum over every evaluated (correspondence, block) pair */
+  uint64_t pair_votes;    /* sum over levels of n x blocks: every (correspondence, block) pair the
+                             search decides (a culled pair is decided by its ancestor's test) */
   uint64_t cells_evaluated;
   uint32_t lb_star;       /* certified lower bound used for pruning */
   int32_t  n_phases;      /* entries used in cells_per_phase */
@@ -104,15 +110,19 @@ typedef struct {
   int32_t  n_rechecked;   /* blocks that needed the fp64 near-threshold recheck */
   float    vote_ms;       /* summed device time of the K3 vote launches (CUDA events on cfg.stream) */
   int32_t  launches;      /* kernels this call launched (all of librotvote's own) */
-  uint64_t vote_pairs;    /* (correspondence, block) pairs voted by K3 on this rank, padding excluded */
-  int32_t  vote_launches; /* K3 launches on this rank */
+  uint64_t vote_pairs;    /* (correspondence, block) pairs voted by K3 / K3-TC on this rank, padding
+                             excluded */
+  int32_t  vote_launches; /* K3 / K3-TC launches on this rank */
+  int32_t  cull_launches; /* K3-C (culled vote) launches on this rank */
+  uint64_t cull_pairs;    /* (correspondence, block) pairs K3-C evaluated on this rank */
+  float    cull_ms;       /* summed device time of the K3-C launches (CUDA events on cfg.stream) */
   int32_t  pad_;
 } rv_result;
 
 /* ---- lifetime ------------------------------------------------------------------ */
 
 /* Fill *cfg with the defaults: device 0, rank 0, world 1, max_n 1<<20, max_problems 1,
- * default chain, refine_rounds 2, guard 1e-5, stream NULL, tensor_vote 1. */
+ * default chain, refine_rounds 2, guard 1e-5, stream NULL, tensor_vote 1, cull 1. */
 void rot_vote_default_config(rv_config* cfg);
 
 /* Create a context.  Allocates all workspace for cfg->max_n correspondences on
@@ -192,6 +202,22 @@ int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n,
 /* rot_vote_count_cells maps modes to kernels literally (BOUND/FINAL: K3 on the FP32 pipe;
  * BOUND_TC/FINAL_TC: K3-TC).  The solve with tensor_vote = 1 sends its bound and final levels
  * to K3-TC: the planner only needs cnt_b <= exact <= cnt_a, which the wider band keeps. */
+
+/* Ancestor culling (K3-C), for parity tests: vote the full level-0 grid at
+ * resolution B0 with K3-TC (bound mode) writing the pass bitmasks, then count the m blocks
+ * `lins` (resolution B, B % B0 == 0, any order) against their level-0 ancestors'
+ * correspondences only:
+ *   BOUND: cnt_a = #{i in L(anc) : s32_i(q_c) >= cos(min(pi, eps + r(c))) - guard}
+ *   FINAL: cnt_a / cnt_b at cos(eps) -/+ guard (as RV_MODE_FINAL), over L(anc)
+ * with L(a) = {i : s_tc_i(q_a) >= cos(min(pi, eps + r(a))) - guard - 1.5e-5}.  Every exact voter
+ * of a block is in L(anc), so the counts stay within the guard band of the exact ones.
+ * bits_out: DEVICE uint32[m0][ceil(n/256)*8] copy of the level-0 bitmasks (row = the block's
+ * index in the ascending candidate list of B0, bit i%32 of word i/32 = i in L), or NULL.
+ * Needs tensor_vote = 1 and cull = 1; 1 <= B0 <= 90. */
+int rot_vote_count_cells_culled(rv_ctx* ctx, const float* x, const float* y, int64_t n,
+                                int32_t B0, int32_t B, const uint32_t* lins, int64_t m,
+                                double eps, int32_t mode, uint32_t* cnt_a, uint32_t* cnt_b,
+                                uint32_t* bits_out);
 
 /* Test hook for K3-TC's arithmetic: the raw tensor-core scores S' = s_tc - t of m blocks
  * (t = the RV_MODE_BOUND_TC threshold, guard included) against every correspondence.  out: DEVICE float

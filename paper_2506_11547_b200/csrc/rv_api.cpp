@@ -242,6 +242,48 @@ struct rv_ctx {
     }
     evn = 0;
   }
+  // ancestor culling (rv_cull.cu): level-0 pass bitmasks, the K3-C rows, the level-0 lin ->
+  // bitmask row table, the K3-C item planner's scratch, and its own event pairs
+  bool cull_on = false;          // cfg.cull (with tensor_vote)
+  bool cull_ready = false;       // this solve's level-0 bitmasks are written: levels >= 1 cull
+  int64_t cull_min_n = 0;        // cull only problems of >= this many correspondences (the
+                                 // largest of a batch); RV_CULL_MIN_N overrides
+  int32_t cull_B0 = 0;
+  int64_t cull_m0 = 0, cull_wpc_max = 0;
+  DevBuf<uint32_t> cbits;        // level-0 pass bitmasks (K3-TC)
+  DevBuf<int64_t> c_lofs;        // level-0 index lists: row offsets
+  DevBuf<uint32_t> c_lidx;       //   and the lists
+  DevBuf<int32_t> c_fill;        //   compaction fill counters
+  const uint32_t* cull_l0cnt = nullptr;  // the level-0 counts (= list lengths) of this solve
+  DevBuf<float> k12;
+  DevBuf<int32_t> lut0;
+  int32_t lut0_B = 0;
+  DevBuf<int64_t> c_act, c_aoff, c_ioff;
+  DevBuf<int32_t> c_acnt, c_tanc, c_tslot, c_cidx, c_icnt, c_work;
+  DevBuf<float> c_phi;
+  DevBuf<rv::CullItem> c_items;
+  DevBuf<unsigned long long> c_pairs;
+  std::vector<cudaEvent_t> cevs;
+  size_t cevn = 0;
+  cudaError_t cev_pair(cudaEvent_t* a, cudaEvent_t* b) {
+    while (cevs.size() < cevn + 2) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return r;
+      cevs.push_back(e);
+    }
+    *a = cevs[cevn];
+    *b = cevs[cevn + 1];
+    cevn += 2;
+    return cudaSuccess;
+  }
+  void cev_collect() {
+    for (size_t i = 0; i + 1 < cevn; i += 2) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, cevs[i], cevs[i + 1]) == cudaSuccess) cull_ms += ms;
+    }
+    cevn = 0;
+  }
   DevBuf<int32_t> l0surv;        // host-planner batched path: level-0 survivor indices
   DevBuf<uint8_t> atab;          // K3-TC A-operand blocks (K2-TC)
   DevBuf<rv::ABlock> ablk;
@@ -255,11 +297,22 @@ struct rv_ctx {
   Staging up, down;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evv0 = nullptr, evv1 = nullptr;
   // per-call counters reported in rv_result
-  float vote_ms = 0;
-  uint64_t vote_pairs = 0;
-  int32_t launches = 0, vote_launches = 0;
+  float vote_ms = 0, cull_ms = 0;
+  uint64_t vote_pairs = 0, cull_pairs = 0;
+  int32_t launches = 0, vote_launches = 0, cull_launches = 0;
   void reset_counters() {
     vote_ms = 0; vote_pairs = 0; launches = 0; vote_launches = 0; vote_pending = false;
+    cull_ms = 0; cull_pairs = 0; cull_launches = 0; cevn = 0;
+  }
+  template <class R>
+  void fill_counters(R& r) const {
+    r.vote_ms = vote_ms;
+    r.vote_pairs = vote_pairs;
+    r.launches = launches;
+    r.vote_launches = vote_launches;
+    r.cull_ms = cull_ms;
+    r.cull_pairs = cull_pairs;
+    r.cull_launches = cull_launches;
   }
   Trace* trace = nullptr;  // RV_TRACE=1: host phase timings
   void mark(const char* what) {
@@ -492,7 +545,9 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
     std::memcpy(ht, toff.data(), (P + 1) * sizeof(int64_t));
     RV_CUDA(cudaMemcpyAsync(ctx->toffs.p, ht, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
             "copying offsets");
-    rv::launch_setup_tc(x, y, ctx->rows.p, ctx->toffs.p, P, toff[P], ctx->tctab.p, ctx->stream);
+    if (ctx->cull_on) RV_CUDA(ctx->k12.ensure((size_t)toff[P] * 12), "allocating K3-C rows");
+    rv::launch_setup_tc(x, y, ctx->rows.p, ctx->toffs.p, P, toff[P], ctx->tctab.p, ctx->stream,
+                        ctx->cull_on ? ctx->k12.p : nullptr);
     ctx->launches += 1;
     ctx->tc_toff = toff;
   }
@@ -868,10 +923,7 @@ int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double ep
   float ms = 0;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   out->ms = ms;
-  out->vote_ms = ctx->vote_ms;
-  out->vote_pairs = ctx->vote_pairs;
-  out->launches = ctx->launches;
-  out->vote_launches = ctx->vote_launches;
+  ctx->fill_counters(*out);
   return RV_OK;
 }
 
@@ -925,10 +977,7 @@ int solve_multi_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   for (int32_t k = 0; k < found; ++k) {
     out[k].ms = ms;
-    out[k].vote_ms = ctx->vote_ms;
-    out[k].vote_pairs = ctx->vote_pairs;
-    out[k].launches = ctx->launches;
-    out[k].vote_launches = ctx->vote_launches;
+    ctx->fill_counters(out[k]);
   }
   *n_found = found;
   return RV_OK;
@@ -1267,6 +1316,57 @@ int vote_lists(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   return RV_OK;
 }
 
+// Culling state for a level 0 at B0 (grid_host holds its m0 candidates): the lin -> row table,
+// the pair counter (zeroed), the bitmask geometry.
+int cull_prepare(rv_ctx* ctx, int32_t B0, int64_t m0, int32_t PL) {
+  if (ctx->lut0_B != B0) {
+    std::vector<int32_t> lut((size_t)B0 * B0 * B0, -1);
+    for (int64_t a = 0; a < m0; ++a) lut[ctx->grid_host[a]] = (int32_t)a;
+    RV_CUDA(ctx->lut0.ensure(lut.size()), "allocating");
+    RV_CUDA(cudaMemcpy(ctx->lut0.p, lut.data(), lut.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
+    ctx->lut0_B = B0;
+  }
+  RV_CUDA(ctx->c_pairs.ensure(1), "allocating");
+  RV_CUDA(cudaMemsetAsync(ctx->c_pairs.p, 0, 8, ctx->stream), "memset");
+  RV_CUDA(ctx->dp_err.ensure(1), "allocating");
+  int64_t wmax = 0;
+  for (int32_t p = 0; p < PL; ++p)
+    wmax = std::max<int64_t>(wmax, (ctx->tc_toff[p + 1] - ctx->tc_toff[p]) / 32);
+  ctx->cull_B0 = B0;
+  ctx->cull_m0 = m0;
+  ctx->cull_wpc_max = wmax;
+  return RV_OK;
+}
+
+// After the level-0 vote wrote the bitmasks: the index lists L(a) (row offsets, one read of
+// their total, the compaction), and ctx->cull_ready.  Culling is skipped (the solve goes on
+// unculled) when the lists would exceed 2^29 entries or a quarter of the level-0 pairs (then
+// the ancestor lists cut too little for the gather to pay).
+int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
+                     bool force = false) {
+  cudaStream_t s = ctx->stream;
+  const int64_t NB = (int64_t)PL * m0;
+  RV_CUDA(ctx->c_lofs.ensure(NB + 1), "allocating");
+  rv::launch_cull_rows(l0cnt, PL, m0, ctx->c_lofs.p, s);
+  ctx->launches += 1;
+  ctx->down.reset();
+  int64_t* ht = ctx->down.take<int64_t>(1);
+  RV_CUDA(cudaMemcpyAsync(ht, ctx->c_lofs.p + NB, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "level-0 lists");
+  const int64_t total = *ht;
+  const double pairs0 = (double)m0 * (double)(ctx->tc_toff[PL] - ctx->tc_toff[0]);
+  ctx->cull_ready = false;
+  if (total > ((int64_t)1 << 29) || (!force && (double)total > 0.25 * pairs0)) return RV_OK;
+  RV_CUDA(ctx->c_lidx.ensure(total + 4), "allocating level-0 lists");
+  RV_CUDA(ctx->c_fill.ensure(NB), "allocating");
+  rv::launch_cull_compact(ctx->cbits.p, ctx->toffs.p, PL, m0, ctx->cull_wpc_max, ctx->c_lofs.p,
+                          ctx->c_fill.p, ctx->c_lidx.p, s);
+  ctx->launches += 1;
+  ctx->cull_l0cnt = l0cnt;
+  ctx->cull_ready = true;
+  return RV_OK;
+}
+
 // true when the device level loop applies: >= 2 levels and a cached level-0 background
 bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps) {
   if (levels_eff < 2) return false;
@@ -1280,10 +1380,50 @@ bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps) {
 // built on the device (dp_launch_items) and the kernels read their counts there -- no host
 // round trip.  FP32 K3 (tensor_vote = 0): the counts and bases are read back and the items
 // built on the host (vote_lists).  The caller has zeroed the count slots.
+// emit_bits (level 0 of a culled solve): K3-TC also writes the level-0 pass bitmasks.  Once
+// they exist (ctx->cull_ready), BOUND / FINAL levels go to K3-C (rv_cull.cu), items planned on
+// the device.
 int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
                const std::vector<int64_t>& koff, double eps, int32_t mode, int32_t B,
-               const rv::DpList& Ld, int32_t PL, int64_t entries_bound, int64_t nmax) {
+               const rv::DpList& Ld, int32_t PL, int64_t entries_bound, int64_t nmax,
+               bool emit_bits = false) {
   cudaStream_t s = ctx->stream;
+  if (ctx->cull_ready && mode != RV_MODE_EXACT) {
+    const int64_t eb = std::max<int64_t>(1, entries_bound);
+    const int64_t nb = (int64_t)PL * ctx->cull_m0;
+    const int64_t mi = rv::cull_items_bound(eb, ctx->num_sms);
+    RV_CUDA(ctx->c_act.ensure(PL + 1), "allocating");
+    RV_CUDA(ctx->c_acnt.ensure(nb), "allocating");
+    RV_CUDA(ctx->c_aoff.ensure(nb + 1), "allocating");
+    RV_CUDA(ctx->c_ioff.ensure(nb + 1), "allocating");
+    RV_CUDA(ctx->c_tanc.ensure(eb), "allocating");
+    RV_CUDA(ctx->c_tslot.ensure(eb), "allocating");
+    RV_CUDA(ctx->c_cidx.ensure(eb + 3 * nb + 4), "allocating");      // bucket positions are
+    RV_CUDA(ctx->c_phi.ensure((eb + 3 * nb + 4) * 12), "allocating");  // padded to quads
+    RV_CUDA(ctx->c_icnt.ensure(2), "allocating");
+    RV_CUDA(ctx->c_work.ensure(1), "allocating");
+    RV_CUDA(ctx->vsegs.ensure(PL), "allocating segments");
+    RV_CUDA(ctx->c_items.ensure(mi), "allocating K3-C items");
+    const rv::CullScratch cs{ctx->c_act.p, ctx->c_acnt.p, ctx->c_aoff.p, ctx->c_ioff.p,
+                             ctx->c_tanc.p, ctx->c_tslot.p, ctx->c_cidx.p, ctx->c_phi.p,
+                             ctx->c_icnt.p, ctx->c_work.p};
+    rv::launch_cull_items(Ld, ctx->rows.p, ctx->toffs.p, PL, B, ctx->cull_B0, ctx->lut0.p,
+                          ctx->cull_m0, ctx->cull_l0cnt, ctx->c_lofs.p, ctx->k12.p, eps, mode,
+                          ctx->cfg.guard,
+                          ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, mi, ctx->dp_err.p, s);
+    ctx->launches += 5;
+    cudaEvent_t e0, e1;
+    RV_CUDA(ctx->cev_pair(&e0, &e1), "event");
+    RV_CUDA(cudaEventRecord(e0, s), "event");
+    rv::launch_vote_cull(mode, ctx->vsegs.p, ctx->c_items.p, ctx->c_icnt.p, ctx->c_work.p,
+                         ctx->c_pairs.p, ctx->c_phi.p, ctx->c_cidx.p, ctx->c_lidx.p,
+                         ctx->cfg.guard, ctx->num_sms, s);
+    RV_CUDA(cudaEventRecord(e1, s), "event");
+    ctx->launches += 1;
+    ctx->cull_launches += 1;
+    RV_CUDA(cudaGetLastError(), "launching the culled vote");
+    return RV_OK;
+  }
   if (ctx->tc_on || mode == RV_MODE_EXACT) {
     const int im = mode == RV_MODE_EXACT ? 2 : mode == RV_MODE_FINAL ? 1 : 0;
     int64_t mi = 0, ma = 0;
@@ -1297,7 +1437,8 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     RV_CUDA(ctx->dp_icnt.ensure(4), "allocating");
     rv::dp_launch_items(Ld, ctx->rows.p, im == 2 ? ctx->koffs.p : ctx->toffs.p, PL, B, eps, im,
                         ctx->num_sms, ctx->vsegs.p, ctx->dp_ioff.p, ctx->dp_aoff.p, ctx->dp_icnt.p,
-                        ctx->vitems.p, ctx->ablk.p, mi, ma, ctx->dp_err.p, s);
+                        ctx->vitems.p, ctx->ablk.p, mi, ma, ctx->dp_err.p, s,
+                        emit_bits ? ctx->cbits.p : nullptr);
     ctx->launches += 2;
     if (im == 2) {
       rv::launch_exact(ctx->k9.p, ctx->stride, x, y, ctx->vsegs.p, ctx->vitems.p, 0,
@@ -1308,7 +1449,8 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
       RV_CUDA(ctx->ev_pair(&e0, &e1), "event");
       RV_CUDA(cudaEventRecord(e0, s), "event");
       rv::launch_vote_tc(ctx->tctab.p, ctx->atab.p, ctx->ablk.p, 0, ctx->vsegs.p, ctx->vitems.p, 0,
-                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, im == 1, ctx->dp_icnt.p);
+                         ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, im == 1, ctx->dp_icnt.p,
+                         emit_bits);
       RV_CUDA(cudaEventRecord(e1, s), "event");
       ctx->launches += 2;
       ctx->vote_launches += 1;
@@ -1422,7 +1564,27 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
     ctx->grid_list_B = B0;
     ctx->grid_list_m = m0;
   }
-  if (ctx->tc_on || shard) {
+  // ancestor culling: level 0 writes the pass bitmasks (every rank votes all of level 0, so
+  // every rank holds every ancestor's list); bitmasks capped at 4 GiB
+  ctx->cull_ready = false;
+  const int64_t tpad = ctx->tc_on ? ctx->tc_toff.back() : 0;
+  const bool cull = ctx->cull_on && (int64_t)ctx->tc_toff.size() == PL + 1 &&
+                    nmax >= ctx->cull_min_n && (int64_t)PL * m0 <= ((int64_t)1 << 22) &&
+                    (double)m0 * (double)(tpad / 32) * 4.0 <= 4294967296.0;
+  if (cull) {
+    RV_CUDA(ctx->cbits.ensure((size_t)m0 * (size_t)(tpad / 32)), "allocating level-0 bitmasks");
+    if (int rc = cull_prepare(ctx, B0, m0, PL)) return rc;
+  }
+  bool culled = false;  // the finer levels run K3-C (the lists were built)
+  if (cull) {
+    RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, ((size_t)PL * m0 + slack) * 4, s), "memset");
+    const rv::DpList l0{ctx->grid_list.p, 1, m0, nullptr, nullptr, ctx->l0cnt.p, ctx->l0cnt.p};
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, PL * m0, nmax,
+                            true))
+      return rc;
+    if (int rc = cull_build_lists(ctx, PL, m0, ctx->l0cnt.p)) return rc;
+    culled = ctx->cull_ready;
+  } else if (ctx->tc_on || shard) {
     RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, ((size_t)PL * m0 + slack) * 4, s), "memset");
     const rv::DpList l0{ctx->grid_list.p, 1, m0, nullptr, nullptr, ctx->l0cnt.p, ctx->l0cnt.p};
     if (int rc = vote(RV_MODE_BOUND, B0, l0, PL * m0)) return rc;
@@ -1666,14 +1828,16 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
                            ctx->dp_best.p, ctx->dp_ties.p, s);
   ctx->launches += 2;
   RV_CUDA(cudaGetLastError(), "launching the level loop");
-  RV_CUDA(ctx->down.ensure((size_t)PL * 24 + (size_t)nph * PL * 4 + 1024), "allocating staging");
+  RV_CUDA(ctx->down.ensure((size_t)PL * 24 + (size_t)nph * PL * 4 + 2048), "allocating staging");
   ctx->down.reset();
   unsigned long long* hbest = ctx->down.take<unsigned long long>(PL);
   int32_t* hties = ctx->down.take<int32_t>(PL);
   int64_t* hlb = ctx->down.take<int64_t>(PL);
   int32_t* hph = ctx->down.take<int32_t>((size_t)nph * PL);
   int32_t* herr = ctx->down.take<int32_t>(1);
+  unsigned long long* hcp = ctx->down.take<unsigned long long>(1);
   RV_CUDA(cudaMemcpyAsync(herr, ctx->dp_err.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  if (culled) RV_CUDA(cudaMemcpyAsync(hcp, ctx->c_pairs.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hbest, ctx->dp_best.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hties, ctx->dp_ties.p, 4 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hlb, ctx->dp_lb.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
@@ -1682,6 +1846,9 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   RV_CUDA(cudaStreamSynchronize(s), "batched finalize");
   ctx->collect_vote_ms();
   ctx->ev_collect();
+  ctx->cev_collect();
+  ctx->cull_ready = false;
+  if (culled) ctx->cull_pairs += *hcp;
   if (*herr != 0)
     return ctx->fail(RV_ECUDA, "internal: device level-loop invariant violated (code %d)", *herr);
   tr.mark("  finalize");
@@ -1710,7 +1877,17 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
       add(c);
     }
     if (nre > 0) add(nre);
-    if (!shard || !ctx->comm) {
+    if (culled) {  // K3-TC voted level 0 only (unsharded); K3-C counts its own pairs
+      tc_pairs += (uint64_t)m0 * n;
+    } else if (cull) {  // level 0 unsharded, the finer levels on K3-TC (sharded if W > 1)
+      tc_pairs += (uint64_t)m0 * n;
+      for (int ph = 0; ph + 1 < nph; ++ph) {
+        const int64_t c = hph[(size_t)ph * PL + p];
+        const int64_t mine = !shard || !ctx->comm ? c
+            : std::max<int64_t>(0, std::min<int64_t>(phase_chunk[ph], c - (int64_t)ctx->cfg.rank * phase_chunk[ph]));
+        tc_pairs += (uint64_t)mine * n;
+      }
+    } else if (!shard || !ctx->comm) {
       tc_pairs += (r.pair_votes - (uint64_t)nre * n);
     } else {  // this rank's slices only: level 0, then the dive and BnB phases
       const int64_t c0 = (m0 + W - 1) / W;
@@ -1924,10 +2101,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   for (rv_result& r : local) {
     r.ms = ms;
-    r.vote_ms = ctx->vote_ms;
-    r.vote_pairs = ctx->vote_pairs;
-    r.launches = ctx->launches;
-    r.vote_launches = ctx->vote_launches;
+    ctx->fill_counters(r);
   }
   if (!ctx->comm || one_sharded) {
     std::memcpy(out, local.data(), (size_t)P * sizeof(rv_result));
@@ -1979,6 +2153,7 @@ void rot_vote_default_config(rv_config* cfg) {
   cfg->stream = nullptr;
   cfg->emulate_world = 0;
   cfg->tensor_vote = 1;
+  cfg->cull = 1;
 }
 
 int rot_vote_get_unique_id(void* id_out) {
@@ -2014,6 +2189,8 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
   }
   ctx->stream = (cudaStream_t)cfg->stream;
   ctx->tc_on = cfg->tensor_vote != 0;
+  ctx->cull_on = ctx->tc_on && cfg->cull != 0;
+  if (const char* e = getenv("RV_CULL_MIN_N")) ctx->cull_min_n = atoll(e);
   if (const char* fg = getenv("RV_VOTE_GROUPS")) ctx->force_groups = atoi(fg);
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -2077,6 +2254,12 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->dp_best.release(); ctx->a1_acc.release(); ctx->a1_tab.release(); ctx->a1_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
   ctx->dp_icnt.release(); ctx->dp_phase.release(); ctx->dp_err.release();
   ctx->dp_pcnt.release(); ctx->dp_scnt.release(); ctx->dp_poff.release(); ctx->dp_sbase.release();
+  ctx->cbits.release(); ctx->k12.release(); ctx->lut0.release(); ctx->c_act.release();
+  ctx->c_lofs.release(); ctx->c_lidx.release(); ctx->c_fill.release();
+  ctx->c_ioff.release(); ctx->c_aoff.release(); ctx->c_acnt.release(); ctx->c_tanc.release();
+  ctx->c_tslot.release(); ctx->c_cidx.release(); ctx->c_phi.release(); ctx->c_icnt.release();
+  ctx->c_work.release(); ctx->c_items.release(); ctx->c_pairs.release();
+  for (cudaEvent_t e : ctx->cevs) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
   ctx->up.release(); ctx->down.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -2173,6 +2356,73 @@ int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n,
   if (mode == RV_MODE_FINAL || mode == RV_MODE_FINAL_TC)
     RV_CUDA(cudaMemcpyAsync(cnt_b, hb.data(), m * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
   RV_CUDA(cudaStreamSynchronize(ctx->stream), "H2D");
+  return RV_OK;
+}
+
+int rot_vote_count_cells_culled(rv_ctx* ctx, const float* x, const float* y, int64_t n, int32_t B0,
+                                int32_t B, const uint32_t* lins, int64_t m, double eps,
+                                int32_t mode, uint32_t* cnt_a, uint32_t* cnt_b, uint32_t* bits_out) {
+  if (!ctx) return RV_EINVAL;
+  ctx->err.clear();
+  cudaSetDevice(ctx->cfg.device);
+  if (int rc = validate_common(ctx, x, y, eps, 0)) return rc;
+  if (!ctx->cull_on) return ctx->fail(RV_EINVAL, "needs a context created with tensor_vote = 1, cull = 1");
+  if (!lins || !cnt_a || (mode == RV_MODE_FINAL && !cnt_b) || m < 0)
+    return ctx->fail(RV_EINVAL, "null pointer");
+  if (mode != RV_MODE_BOUND && mode != RV_MODE_FINAL) return ctx->fail(RV_EINVAL, "bad mode");
+  if (B0 < 1 || B0 > 90 || B < B0 || B > 1625 || B % B0 != 0) return ctx->fail(RV_EINVAL, "bad B0 / B");
+  if (n < 1 || n > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "n out of range");
+  cudaStream_t s = ctx->stream;
+  const int64_t offs[2] = {0, n};
+  std::vector<int64_t> koff;
+  ctx->reset_counters();
+  if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
+  if (int rc = check_bad(ctx)) return rc;
+  const int64_t m0 = rv_grid_candidates(B0, nullptr, 0);
+  if (ctx->grid_host_B != B0) {
+    ctx->grid_host.resize(m0);
+    rv_grid_candidates(B0, ctx->grid_host.data(), m0);
+    ctx->grid_host_B = B0;
+  }
+  RV_CUDA(ctx->grid_list.ensure(m0), "allocating grid list");
+  RV_CUDA(cudaMemcpy(ctx->grid_list.p, ctx->grid_host.data(), m0 * 4, cudaMemcpyHostToDevice), "H2D");
+  ctx->grid_list_B = B0;
+  ctx->grid_list_m = m0;
+  const int64_t wpc = ctx->tc_toff[1] / 32;
+  RV_CUDA(ctx->cbits.ensure((size_t)m0 * wpc), "allocating level-0 bitmasks");
+  RV_CUDA(ctx->l0cnt.ensure(m0), "allocating");
+  RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, m0 * 4, s), "memset");
+  if (int rc = cull_prepare(ctx, B0, m0, 1)) return rc;
+  RV_CUDA(cudaMemsetAsync(ctx->dp_err.p, 0, 4, s), "memset");
+  const std::vector<int64_t> rows{0, n};
+  ctx->cull_ready = false;
+  const rv::DpList l0{ctx->grid_list.p, 1, m0, nullptr, nullptr, ctx->l0cnt.p, ctx->l0cnt.p};
+  if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, 1, m0, n, true))
+    return rc;
+  if (int rc = cull_build_lists(ctx, 1, m0, ctx->l0cnt.p, true)) return rc;
+  if (m > 0 && !ctx->cull_ready) return ctx->fail(RV_ENOMEM, "level-0 lists exceed 2^29 entries");
+  if (m > 0) {
+    RV_CUDA(ctx->dp_sbase.ensure(2), "allocating");
+    RV_CUDA(ctx->dp_scnt.ensure(1), "allocating");
+    const int64_t hb[2] = {0, m};
+    const int32_t hc = (int32_t)m;
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_sbase.p, hb, 16, cudaMemcpyHostToDevice, s), "H2D");
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_scnt.p, &hc, 4, cudaMemcpyHostToDevice, s), "H2D");
+    RV_CUDA(cudaMemsetAsync(cnt_a, 0, m * 4, s), "memset");
+    if (mode == RV_MODE_FINAL) RV_CUDA(cudaMemsetAsync(cnt_b, 0, m * 4, s), "memset");
+    const rv::DpList Ld{lins, 0, 0, ctx->dp_sbase.p, ctx->dp_scnt.p, cnt_a,
+                        mode == RV_MODE_FINAL ? cnt_b : cnt_a};
+    int rc = vote_level(ctx, x, y, rows, koff, eps, mode, B, Ld, 1, m, n);
+    ctx->cull_ready = false;
+    if (rc) return rc;
+  }
+  if (bits_out)
+    RV_CUDA(cudaMemcpyAsync(bits_out, ctx->cbits.p, (size_t)m0 * wpc * 4, cudaMemcpyDeviceToDevice, s),
+            "D2D");
+  int32_t herr = 0;
+  RV_CUDA(cudaMemcpyAsync(&herr, ctx->dp_err.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaStreamSynchronize(s), "culled vote");
+  if (herr) return ctx->fail(RV_ECUDA, "internal: culled item planner invariant violated (code %d)", herr);
   return RV_OK;
 }
 

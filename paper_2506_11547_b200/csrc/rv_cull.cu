@@ -1,0 +1,634 @@
+// rv_cull.cu -- K3-C: the vote of a level's blocks against their level-0 ancestor's
+// correspondences only ("ancestor culling"), and its device item planner.
+//
+// Why it is exact.  Level 0 (resolution B0) is voted by K3-TC against every correspondence; its
+// epilogue also writes, per level-0 block a, the bitmask L(a) of the correspondences that
+// passed a's bound test  s_tc(q_a) >= cos(min(pi, eps + r(a))) - g'.  A block c at a finer level
+// lies inside its ancestor's box, so (R6's triangle inequality, with the half diagonal and the
+// conformal factor of the nested boxes: |p_c - p_a| + sqrt(3)/B_c <= sqrt(3)/B0 and
+// lambda(c) <= lambda(a))
+//     angle(R(q_a) x_i, y_i) <= angle(R(q_c) x_i, y_i) + r(a) - r(c),
+// hence every i with exact s_i(q_c) >= cos(eps + r(c)) (the bound level's true count) or
+// s_i(q_c) >= cos(eps) (the final level's) has exact s_i(q_a) >= cos(eps + r(a)) and is in L(a)
+// (the TC error 1.3e-5 < g' = g + 1.5e-5).  Correspondences outside L(a) therefore never vote for
+// c, and counting c over L(a) only, with the FP32 path's arithmetic and guard, gives
+//     cnt(c) = #{i in L(a) : s32_i(q_c) >= t_c - g}
+// which still contains every true voter (upper bounds stay certified, cnt_b <= exact <= cnt_a
+// at the final level) and differs from the unculled FP32 count only by pairs inside the guard
+// band -- the parity rule of SURVEY §8(c).
+//
+// Pipeline (all on the device; the host reads one total):
+//   K3-TC BITS   level 0 votes every correspondence and writes the pass bitmask of each block;
+//   cull_rows    row offsets (exclusive prefix of the level-0 counts, padded to multiples of 4);
+//   cull_compact the bitmasks -> per-block index lists L(a), ascending (one warp per row);
+//   per culled level: cull_act / cull_count / cull_scan / cull_scatter / cull_items bucket the
+//   level's blocks by (problem, ancestor), write each block's phi(q_c) and threshold once, and
+//   cut items of <= 32 blocks x a range of their ancestor's list (~8 items per resident warp);
+//   K3-C         one warp per item: 128-entry stages of K rows gathered by cp.async (double
+//                buffered) into shared memory; lane (quad q, group h) votes blocks 4q..4q+3
+//                (phi as FFMA2 register pairs) against entries h, h+4, ... of the stage (3
+//                LDS.128 per entry, 18 FFMA2 for 4 pairs; threshold folded into the chain's
+//                initial value and K3's operation order, so s32 is bit-identical); counts are
+//                sign bits, one atomicAdd per (block, item).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/rotvote.h"
+#include "rv_dplan.h"
+#include "rv_geom.h"
+#include "rv_kernels.h"
+
+namespace rv {
+
+namespace {
+
+constexpr int kCullWarpsPerCta = 4;
+constexpr int kCullThreads = 32 * kCullWarpsPerCta;
+#ifndef RV_CULL_CTAS
+#define RV_CULL_CTAS 4
+#endif
+constexpr int kCullCtasPerSm = RV_CULL_CTAS;
+constexpr int kCullChunk = 128;                 // correspondences per gathered stage
+
+__device__ __forceinline__ void add_sign(uint32_t& acc, float v) {
+  asm("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(__float_as_uint(v) >> 31));
+}
+
+__device__ __forceinline__ int64_t i64min(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ int64_t list_m(const DpList& L, int p) {
+  return L.cnt ? (int64_t)L.cnt[p] : L.shared_m;
+}
+
+// problem of flat index g: the last p with off[p] <= g (off ascending, off[P] = total)
+__device__ __forceinline__ int find_p(const int64_t* __restrict__ off, int32_t P, int64_t g) {
+  int lo = 0, hi = P;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// block-wide exclusive sum scan of one int64 per thread (blockDim.x <= 1024)
+__device__ int64_t blk_scan_sum(int64_t v, int64_t* sh, int64_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < nw ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    sh[32 + lane] = w;
+  }
+  __syncthreads();
+  const int64_t before = warp > 0 ? sh[32 + warp - 1] : 0;
+  *total = sh[32 + nw - 1];
+  __syncthreads();
+  return before + x - v;
+}
+// row of the level-0 ancestor of block lin (resolution B) in the bitmasks
+__device__ __forceinline__ int32_t ancestor(uint32_t lin, int32_t B, int32_t f, int32_t B0,
+                                            const int32_t* __restrict__ lut0) {
+  int32_t i, j, k;
+  lin_to_ijk(lin, B, i, j, k);
+  return lut0[ijk_to_lin(i / f, j / f, k / f, B0)];
+}
+
+}  // namespace
+
+// ---- item planner ---------------------------------------------------------------------------
+// The level's blocks are bucketed by (problem, level-0 ancestor) -- a counting sort: count,
+// scan, scatter -- so an item is up to 32 blocks of one bucket x a range of the ancestor's
+// bitmask words.  The scatter also writes each block's phi(q_c) and threshold (fp64 -> fp32,
+// K3's rounding) once per level, in bucket order, so the vote kernel loads them.
+
+// act[p] = exclusive prefix of the list lengths (one CTA)
+__global__ void __launch_bounds__(1024) cull_act(DpList L, int32_t P, int64_t* act) {
+  __shared__ int64_t sh[64];
+  const int t = threadIdx.x, T = blockDim.x;
+  const int p0 = (int)((int64_t)P * t / T), p1 = (int)((int64_t)P * (t + 1) / T);
+  int64_t v = 0;
+  for (int p = p0; p < p1; ++p) v += list_m(L, p);
+  int64_t tot;
+  int64_t e = blk_scan_sum(v, sh, &tot);
+  for (int p = p0; p < p1; ++p) {
+    act[p] = e;
+    e += list_m(L, p);
+  }
+  if (t == 0) act[P] = tot;
+}
+
+__device__ __forceinline__ const uint32_t* list_lins(const DpList& L, int p) {
+  return L.shared ? L.lins : L.lins + L.base[p];
+}
+
+// bucket sizes: acnt[p * m0 + a] (zeroed by the caller); each entry's ancestor and slot
+__global__ void cull_count(DpList L, int32_t P, int32_t B, int32_t B0,
+                           const int32_t* __restrict__ lut0, int64_t m0,
+                           const int64_t* __restrict__ act, int32_t* acnt, int32_t* tanc,
+                           int32_t* tslot, int32_t* err) {
+  const int64_t T = act[P];
+  const int32_t f = B / B0;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < T;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int p = find_p(act, P, g);
+    const int32_t a = ancestor(list_lins(L, p)[g - act[p]], B, f, B0, lut0);
+    if (a < 0) {
+      atomicOr(err, 4);
+      tanc[g] = 0;
+      tslot[g] = 0;
+      continue;
+    }
+    tanc[g] = a;
+    tslot[g] = atomicAdd(&acnt[(int64_t)p * m0 + a], 1);
+  }
+}
+
+// One CTA: lofs[b] = exclusive prefix of the level-0 counts rounded up to 4 (list row starts,
+// 16-byte aligned), lofs[NB] = their total
+__global__ void __launch_bounds__(1024) cull_rows(const uint32_t* __restrict__ l0cnt, int64_t NB,
+                                                  int64_t* lofs) {
+  __shared__ int64_t sh[64];
+  const int t = threadIdx.x, T = blockDim.x;
+  const int64_t b0 = NB * t / T, b1 = NB * (t + 1) / T;
+  int64_t v = 0;
+  for (int64_t b = b0; b < b1; ++b) v += ((int64_t)l0cnt[b] + 3) & ~(int64_t)3;
+  int64_t tot;
+  int64_t e = blk_scan_sum(v, sh, &tot);
+  for (int64_t b = b0; b < b1; ++b) {
+    lofs[b] = e;
+    e += ((int64_t)l0cnt[b] + 3) & ~(int64_t)3;
+  }
+  if (t == 0) lofs[NB] = tot;
+}
+
+// One warp per (level-0 row b = p * m0 + a, segment of 256 bitmask words): the set bits of
+// the segment, appended to the row's list idx[lofs[b] ..] at a position taken with one atomic
+// on fill[b] (zeroed by the caller).  A list's order is irrelevant (counts are sums), so the
+// rows' segments are compacted in parallel; each row ends with exactly l0cnt[b] entries
+// (K3-TC's count is the popcount of its words).
+constexpr int kCompactSeg = 256;
+__global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__ bits0,
+                                                    const int64_t* __restrict__ toffs, int64_t m0,
+                                                    int64_t NB, int64_t nseg,
+                                                    const int64_t* __restrict__ lofs,
+                                                    int32_t* fill, uint32_t* idx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       task < NB * nseg; task += nwarps) {
+    const int64_t b = task / nseg, sg = task % nseg;
+    const int64_t p = b / m0, a = b % m0;
+    const int64_t wpc = (toffs[p + 1] - toffs[p]) / 32;
+    const int64_t w0 = sg * kCompactSeg;
+    if (w0 >= wpc) continue;  // warp-uniform
+    const uint4* row = reinterpret_cast<const uint4*>(bits0 + m0 * (toffs[p] / 32) + a * wpc + w0);
+    const int64_t nq = (wpc - w0 < kCompactSeg ? wpc - w0 : kCompactSeg) / 4;
+    const uint4 v0 = lane < nq ? __ldg(row + lane) : make_uint4(0u, 0u, 0u, 0u);
+    const uint4 v1 = lane + 32 < nq ? __ldg(row + lane + 32) : make_uint4(0u, 0u, 0u, 0u);
+    const int c = __popc(v0.x) + __popc(v0.y) + __popc(v0.z) + __popc(v0.w) + __popc(v1.x) +
+                  __popc(v1.y) + __popc(v1.z) + __popc(v1.w);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&fill[b], total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    uint32_t* out = idx + lofs[b] + base + (incl - c);
+#pragma unroll
+    for (int s8 = 0; s8 < 8; ++s8) {
+      const uint4& v = s8 < 4 ? v0 : v1;
+      uint32_t w = (s8 & 3) == 0 ? v.x : (s8 & 3) == 1 ? v.y : (s8 & 3) == 2 ? v.z : v.w;
+      const uint32_t cb = (uint32_t)(w0 + 4 * (lane + 32 * (s8 >> 2)) + (s8 & 3)) * 32u;
+      while (w) {
+        *out++ = cb + (uint32_t)(__ffs(w) - 1);
+        w &= w - 1;
+      }
+    }
+  }
+}
+
+// One CTA: bucket offsets aoff (exclusive prefix of acnt rounded up to block quads), the entry
+// chunk CE (multiple of 128, ~`target` items in all), item offsets ioff per bucket
+// (ceil(cnt / 32) groups x ceil(|L(a)| / CE) chunks), the segments, counts = {n_items, CE};
+// zeroes the work counter.
+__global__ void __launch_bounds__(1024) cull_scan(DpList L, const int64_t* __restrict__ rows,
+                                                  const int64_t* __restrict__ toffs, int32_t P,
+                                                  int32_t B, double eps, int64_t m0,
+                                                  const uint32_t* __restrict__ l0cnt,
+                                                  const float* k12,
+                                                  const int32_t* __restrict__ acnt, int64_t* aoff,
+                                                  int64_t* ioff, VoteSeg* segs, int32_t* counts,
+                                                  int32_t* work, int64_t target, int64_t max_items,
+                                                  int32_t* err) {
+  __shared__ int64_t sh[64];
+  __shared__ int64_t s_ce;
+  const int t = threadIdx.x, T = blockDim.x;
+  const int64_t NB = (int64_t)P * m0;
+  const int64_t b0 = NB * t / T, b1 = NB * (t + 1) / T;
+  // pass 1: bucket positions and the vote work (groups x list entries)
+  int64_t ne = 0, work_e = 0;
+  for (int64_t bk = b0; bk < b1; ++bk) {
+    const int64_t c = acnt[bk];
+    ne += (c + 3) & ~(int64_t)3;
+    if (c) work_e += (c + 31) / 32 * (int64_t)l0cnt[bk];
+  }
+  int64_t tot_e, tot_w;
+  int64_t e = blk_scan_sum(ne, sh, &tot_e);
+  blk_scan_sum(work_e, sh, &tot_w);
+  if (t == 0) {
+    int64_t ce = (tot_w / (target > 0 ? target : 1) + 127) / 128 * 128;
+    s_ce = ce < 128 ? 128 : ce;
+  }
+  __syncthreads();
+  const int64_t CE = s_ce;
+  // pass 2: bucket and item offsets
+  auto items_of = [&](int64_t bk) -> int64_t {
+    const int64_t c = acnt[bk], l = l0cnt[bk];
+    return c && l ? (c + 31) / 32 * ((l + CE - 1) / CE) : 0;
+  };
+  int64_t ni = 0;
+  for (int64_t bk = b0; bk < b1; ++bk) ni += items_of(bk);
+  int64_t tot_i;
+  int64_t io = blk_scan_sum(ni, sh, &tot_i);
+  for (int64_t bk = b0; bk < b1; ++bk) {
+    aoff[bk] = e;
+    ioff[bk] = io;
+    e += (acnt[bk] + 3) & ~(int64_t)3;
+    io += items_of(bk);
+  }
+  for (int p = t; p < P; p += T) {
+    VoteSeg sg{};
+    const int64_t b = L.shared ? (int64_t)p * L.shared_m : L.base[p];
+    sg.lins = L.shared ? L.lins : L.lins + b;
+    sg.cnt_a = L.ca + b;
+    sg.cnt_b = L.cb + b;
+    sg.koff = toffs[p];
+    sg.row = rows[p];
+    sg.n = (int32_t)(rows[p + 1] - rows[p]);
+    sg.B = B;
+    sg.eps = eps;
+    sg.bits = nullptr;
+    sg.k12 = k12 + toffs[p] * 12;
+    sg.wpc = (int32_t)((toffs[p + 1] - toffs[p]) / 32);
+    segs[p] = sg;
+  }
+  if (t == 0) {
+    aoff[NB] = tot_e;
+    ioff[NB] = tot_i;
+    if (tot_i > max_items) {  // invariant: the host's bound holds
+      atomicOr(err, 2);
+      tot_i = 0;
+    }
+    counts[0] = (int32_t)tot_i;
+    counts[1] = (int32_t)CE;
+    *work = 0;
+  }
+}
+
+// entries into bucket order: cidx[pos] = the entry's index in its problem's list; phi: per
+// block quad (positions 4k .. 4k+3) 12 float4 rows, row j = (v_j of its 4 blocks) with
+// v = phi(q_c) (9), -(threshold) (the chain's initial value), 0, 0 -- so a lane loads its quad's
+// phi_j as one float4 whose halves are the aligned register pairs FFMA2 takes
+__global__ void cull_scatter(DpList L, int32_t P, int32_t B, double eps, int mode, float guard,
+                             int64_t m0, const int64_t* __restrict__ act,
+                             const int64_t* __restrict__ aoff, const int32_t* __restrict__ tanc,
+                             const int32_t* __restrict__ tslot, int32_t* cidx, float* phi) {
+  const int64_t T = act[P];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < T;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int p = find_p(act, P, g);
+    const int64_t e = g - act[p];
+    const int64_t pos = aoff[(int64_t)p * m0 + tanc[g]] + tslot[g];
+    cidx[pos] = (int32_t)e;
+    int32_t i, j, k;
+    lin_to_ijk(list_lins(L, p)[e], B, i, j, k);
+    double q[4], f[9];
+    cell_quat(B, i, j, k, q);
+    phi9(q, f);
+    const double thr = mode == RV_MODE_FINAL ? cos(eps) - guard
+                                             : bound_threshold(B, i, j, k, eps) - guard;
+    float* q4 = phi + (pos >> 2) * 48 + (pos & 3);
+#pragma unroll
+    for (int t = 0; t < 9; ++t) q4[4 * t] = (float)f[t];
+    q4[36] = (float)(-thr);
+  }
+}
+
+__global__ void cull_items(int32_t P, int64_t m0, const int32_t* __restrict__ acnt,
+                           const uint32_t* __restrict__ l0cnt, const int64_t* __restrict__ lofs,
+                           const int64_t* __restrict__ aoff, const int64_t* __restrict__ ioff,
+                           const int32_t* __restrict__ counts, CullItem* items, int32_t* err) {
+  const int64_t n_items = counts[0], CE = counts[1];
+  const int64_t NB = (int64_t)P * m0;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_items;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = NB;  // the last bucket with ioff <= g (empty buckets share offsets)
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ioff[mid] <= g) lo = mid; else hi = mid;
+    }
+    const int64_t bk = lo, local = g - ioff[bk];
+    const int64_t c = acnt[bk], ng = (c + 31) / 32, l = l0cnt[bk];
+    const int64_t grp = local % ng, ch = local / ng;  // chunk-major within the bucket
+    CullItem it;
+    it.seg = (int32_t)(bk / m0);
+    it.pos0 = (int32_t)(aoff[bk] + 32 * grp);
+    it.ncell = (int32_t)i64min(32, c - 32 * grp);
+    it.e0 = lofs[bk] + ch * CE;
+    it.ne = (int32_t)i64min(CE, l - ch * CE);
+    if (c < 1 || it.ncell < 1 || it.ne < 1) atomicOr(err, 4);
+    items[g] = it;
+  }
+}
+
+// ---- K3-C ------------------------------------------------------------------------------------
+// One warp per item.  Lane = (block quad q = lane / 4, entry group h = lane % 4): the lane holds
+// phi(q_c) and the thresholds of blocks 4q .. 4q+3 in registers (as two block pairs, the vector
+// operand of FFMA2) and votes the entries h, h+4, ... of each stage.  A stage is 128 gathered
+// 48-byte K rows in shared memory (AoS), filled by cp.async and double-buffered: the gather of
+// stage k+1 is in flight while stage k is voted.  Per entry a lane reads its row with 3
+// LDS.128 (the 8 lanes of a group read the same row: broadcast) and issues 18 FFMA2 (2 block
+// pairs x 9, the row's k_j the scalar operand) for 4 pairs.  The compaction of the ancestor's
+// bitmask words into entry indices happens between stages (one warp scan per 128 words when
+// the round has <= 512 set bits, per 16-lane half otherwise).
+template <int MODE>
+struct CullSmem {
+  static constexpr size_t stage = (size_t)kCullChunk * 48;  // 128 K rows (AoS, 12 floats)
+  static constexpr size_t per_warp = 2 * stage;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
+    rv_vote_cull_kernel(const VoteSeg* __restrict__ segs, const CullItem* __restrict__ items,
+                        const int32_t* __restrict__ counts_dev, int32_t* work,
+                        unsigned long long* pairs, const float* __restrict__ phi,
+                        const int32_t* __restrict__ cidx, const uint32_t* __restrict__ lidx,
+                        float guard) {
+  constexpr bool FIN = MODE == RV_MODE_FINAL;
+  extern __shared__ __align__(16) uint8_t cull_smem[];
+  float* sk0 = reinterpret_cast<float*>(cull_smem + (threadIdx.x >> 5) * CullSmem<MODE>::per_warp);
+  const int lane = threadIdx.x & 31, quad = lane >> 2, grp = lane & 3;
+  const int32_t n_items = counts_dev[0];
+  const float two_g = 2.0f * guard;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(work, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= n_items) break;
+    const CullItem it = items[idx];
+    const VoteSeg& sg = segs[it.seg];
+    const int ncell = it.ncell;
+    const float* __restrict__ k12 = sg.k12;
+    // this lane's four blocks 4q .. 4q+3 (a quad of the planner's phi table: row j holds
+    // phi_j of the four, row 9 the initial values); quads past ncell vote zeros, never stored
+    float2 pa[9], pb[9], ia, ib;
+    if (4 * quad < ncell) {
+      const float4* r = reinterpret_cast<const float4*>(phi + (int64_t)(it.pos0 + 4 * quad) * 12);
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const float4 v4 = __ldg(r + t);
+        pa[t] = make_float2(v4.x, v4.y);
+        pb[t] = make_float2(v4.z, v4.w);
+      }
+      const float4 v9 = __ldg(r + 9);
+      ia = make_float2(v9.x, v9.y);
+      ib = make_float2(v9.z, v9.w);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 9; ++t) pa[t] = pb[t] = make_float2(0.0f, 0.0f);
+      ia = ib = make_float2(0.0f, 0.0f);
+    }
+    uint32_t na0 = 0, na1 = 0, na2 = 0, na3 = 0, nb0 = 0, nb1 = 0, nb2 = 0, nb3 = 0;
+    uint32_t S = 0, V = 0;  // entry slots this lane voted / of which zero padding
+    auto count = [&](const float2 a, const float2 b) {
+      add_sign(na0, a.x);
+      add_sign(na1, a.y);
+      add_sign(na2, b.x);
+      add_sign(na3, b.y);
+      if (FIN) {
+        add_sign(nb0, a.x - two_g);
+        add_sign(nb1, a.y - two_g);
+        add_sign(nb2, b.x - two_g);
+        add_sign(nb3, b.y - two_g);
+      }
+    };
+    __syncwarp();    // the previous item's readers of the stages are done
+    const uint32_t* li = lidx + it.e0;
+    // a stage's four indices per lane are loaded one stage ahead of its gather, so the copies
+    // issue without waiting on the index loads
+    auto load_idx = [&](int k, uint32_t (&ix)[4]) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = k * kCullChunk + r * 32 + lane;
+        ix[r] = e < it.ne ? __ldg(li + e) : 0xffffffffu;
+      }
+    };
+    // gather of a stage: lane copies rows e = lane, lane + 32, ... (3 x 16 B each)
+    auto gather = [&](int stg, const uint32_t (&ix)[4]) {
+      float* sk = sk0 + stg * (kCullChunk * 12);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = r * 32 + lane;
+        if (ix[r] != 0xffffffffu) {
+          const float* src = k12 + (int64_t)ix[r] * 12;
+          cp_async16(sk + e * 12, src);
+          cp_async16(sk + e * 12 + 4, src + 4);
+          cp_async16(sk + e * 12 + 8, src + 8);
+        }
+      }
+      cp_async_commit();
+    };
+    const int nst = (it.ne + kCullChunk - 1) / kCullChunk;
+    int stg = 0;
+    uint32_t ixn[4];
+    load_idx(0, ixn);
+    gather(0, ixn);
+    if (nst > 1) load_idx(1, ixn);
+    for (int k = 0; k < nst; ++k) {
+      const int cur = min(kCullChunk, it.ne - k * kCullChunk);
+      if (k + 1 < nst) {
+        gather(stg ^ 1, ixn);
+        if (k + 2 < nst) load_idx(k + 2, ixn);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const float4* sk4 = reinterpret_cast<const float4*>(sk0 + stg * (kCullChunk * 12));
+      // two entries (e, e + 4) per step, four independent FFMA2 chains.  Two register sets
+      // ping-pong: the rows of the next step are read from shared memory while this step
+      // computes (no register rotation).  Rows past `cur` are stale stage data: computed,
+      // never counted.
+      struct Rows { float kv[9], mv[9]; };
+      auto ld = [&](int e, Rows& r) {
+        const int ee = e < kCullChunk - 4 ? e : grp;
+        const float4 k0 = sk4[3 * ee], k1 = sk4[3 * ee + 1], k2 = sk4[3 * ee + 2];
+        const float4 m0 = sk4[3 * ee + 12], m1 = sk4[3 * ee + 13], m2 = sk4[3 * ee + 14];
+        r.kv[0] = k0.x; r.kv[1] = k0.y; r.kv[2] = k0.z; r.kv[3] = k0.w;
+        r.kv[4] = k1.x; r.kv[5] = k1.y; r.kv[6] = k1.z; r.kv[7] = k1.w; r.kv[8] = k2.x;
+        r.mv[0] = m0.x; r.mv[1] = m0.y; r.mv[2] = m0.z; r.mv[3] = m0.w;
+        r.mv[4] = m1.x; r.mv[5] = m1.y; r.mv[6] = m1.z; r.mv[7] = m1.w; r.mv[8] = m2.x;
+      };
+      auto step = [&](const Rows& r, int e) {
+        float2 a = ia, b = ib, c = ia, d = ib;
+#pragma unroll
+        for (int jj = 0; jj < 9; ++jj) {
+          const float2 k2v = make_float2(r.kv[jj], r.kv[jj]);
+          const float2 m2v = make_float2(r.mv[jj], r.mv[jj]);
+          a = __ffma2_rn(pa[jj], k2v, a);
+          b = __ffma2_rn(pb[jj], k2v, b);
+          c = __ffma2_rn(pa[jj], m2v, c);
+          d = __ffma2_rn(pb[jj], m2v, d);
+        }
+        if (e < cur) { count(a, b); ++S; }
+        if (e + 4 < cur) { count(c, d); ++S; }
+      };
+      Rows r0, r1;
+      int e = grp;
+      ld(e, r0);
+#pragma unroll 1
+      for (; e < cur; e += 16) {
+        ld(e + 8, r1);
+        step(r0, e);
+        if (e + 8 >= cur) break;
+        ld(e + 16, r0);
+        step(r1, e + 8);
+      }
+      __syncwarp();  // stage stg is free for the gather after next
+      stg ^= 1;
+    }
+    // counts of this lane's entry group, summed over the quad's four groups
+    // processed slots - negatives - zero-padding slots that scored >= 0 (score = initial value)
+    auto pad = [&](float init) { return (__float_as_uint(init) >> 31) ? 0u : V; };
+    uint32_t c[4] = {S - na0 - pad(ia.x), S - na1 - pad(ia.y), S - na2 - pad(ib.x),
+                     S - na3 - pad(ib.y)};
+    uint32_t d[4] = {S - nb0 - pad(ia.x - two_g), S - nb1 - pad(ia.y - two_g),
+                     S - nb2 - pad(ib.x - two_g), S - nb3 - pad(ib.y - two_g)};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c[u] += __shfl_xor_sync(0xffffffffu, c[u], 1);
+      c[u] += __shfl_xor_sync(0xffffffffu, c[u], 2);
+      if (FIN) {
+        d[u] += __shfl_xor_sync(0xffffffffu, d[u], 1);
+        d[u] += __shfl_xor_sync(0xffffffffu, d[u], 2);
+      }
+    }
+    if (grp == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int cc = 4 * quad + u;
+        if (cc < ncell) {
+          const int32_t e = cidx[it.pos0 + cc];
+          if (c[u]) atomicAdd(&sg.cnt_a[e], c[u]);
+          if (FIN && d[u]) atomicAdd(&sg.cnt_b[e], d[u]);
+        }
+      }
+    }
+    if (lane == 0 && pairs) atomicAdd(pairs, (unsigned long long)it.ne * (unsigned long long)ncell);
+  }
+}
+
+namespace {
+template <int MODE>
+size_t cull_smem_bytes() {
+  return (size_t)kCullWarpsPerCta * CullSmem<MODE>::per_warp;
+}
+template <int MODE>
+void launch_cull_t(const VoteSeg* segs, const CullItem* items, const int32_t* counts_dev,
+                   int32_t* work, unsigned long long* pairs, const float* phi, const int32_t* cidx,
+                   const uint32_t* lidx, float guard, int num_sms, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rv_vote_cull_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)cull_smem_bytes<MODE>());
+    attr = true;
+  }
+  rv_vote_cull_kernel<MODE><<<num_sms * kCullCtasPerSm, kCullThreads, cull_smem_bytes<MODE>(), s>>>(
+      segs, items, counts_dev, work, pairs, phi, cidx, lidx, guard);
+}
+}  // namespace
+
+void launch_vote_cull(int mode, const VoteSeg* segs, const CullItem* items,
+                      const int32_t* counts_dev, int32_t* work, unsigned long long* pairs,
+                      const float* phi, const int32_t* cidx, const uint32_t* lidx, float guard,
+                      int num_sms, cudaStream_t s) {
+  if (mode == RV_MODE_FINAL)
+    launch_cull_t<RV_MODE_FINAL>(segs, items, counts_dev, work, pairs, phi, cidx, lidx, guard,
+                                 num_sms, s);
+  else
+    launch_cull_t<RV_MODE_BOUND>(segs, items, counts_dev, work, pairs, phi, cidx, lidx, guard,
+                                 num_sms, s);
+}
+
+void launch_cull_rows(const uint32_t* l0cnt, int32_t P, int64_t m0, int64_t* lofs,
+                      cudaStream_t s) {
+  cull_rows<<<1, 1024, 0, s>>>(l0cnt, (int64_t)P * m0, lofs);
+}
+
+void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P, int64_t m0,
+                         int64_t wpc_max, const int64_t* lofs, int32_t* fill, uint32_t* lidx,
+                         cudaStream_t s) {
+  const int64_t NB = (int64_t)P * m0, nseg = (wpc_max + kCompactSeg - 1) / kCompactSeg;
+  cudaMemsetAsync(fill, 0, (size_t)NB * 4, s);
+  int64_t blocks = (NB * nseg + 7) / 8;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  cull_compact<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(bits0, toffs, m0, NB, nseg, lofs,
+                                                                   fill, lidx);
+}
+
+void launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
+                       int32_t B, int32_t B0, const int32_t* lut0, int64_t m0,
+                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
+                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
+                       CullItem* items, int64_t max_items, int32_t* err, cudaStream_t s) {
+  cull_act<<<1, 1024, 0, s>>>(L, P, cs.act);
+  cudaMemsetAsync(cs.acnt, 0, (size_t)P * m0 * 4, s);
+  cull_count<<<148 * 8, 256, 0, s>>>(L, P, B, B0, lut0, m0, cs.act, cs.acnt, cs.tanc, cs.tslot, err);
+  const int64_t target = 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
+  cull_scan<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, eps, m0, l0cnt, k12, cs.acnt, cs.aoff, cs.ioff,
+                               segs, cs.counts, cs.work, target, max_items, err);
+  cull_scatter<<<148 * 8, 256, 0, s>>>(L, P, B, eps, mode, guard, m0, cs.act, cs.aoff, cs.tanc,
+                                       cs.tslot, cs.cidx, cs.phi);
+  cull_items<<<148 * 4, 256, 0, s>>>(P, m0, cs.acnt, l0cnt, lofs, cs.aoff, cs.ioff, cs.counts, items,
+                                     err);
+}
+
+int64_t cull_items_bound(int64_t entries, int num_sms) {
+  return 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta + entries + 1;
+}
+
+}  // namespace rv

@@ -28,14 +28,15 @@ struct DpList {
 // (one cell per item, 8192-correspondence chunks).  Writes segs[P] (koffs: the TC table
 // offsets for modes 0/1, the K table offsets for mode 2), items, ablocks and
 // counts = {n_items, n_ablocks, chunks}; item_off / ablk_off: scratch [P+1].  The caller
-// sizes items / ablocks from a bound (dp_items_bound).
+// sizes items / ablocks from a bound (dp_items_bound).  bits0 (mode 0 on the shared level-0
+// list only): the segments carry the level-0 pass bitmasks K3-TC writes (rv_cull.cu).
 // err: invariant violations are OR-ed in (1 child capacity, 2 item bound, 4 item shape); the
 // host checks the word once at the end of the solve (there are no silent out-of-bounds writes).
 void dp_launch_items(const DpList& L, const int64_t* rows, const int64_t* koffs, int32_t P,
                      int32_t B, double eps, int mode, int32_t slots, VoteSeg* segs,
                      int64_t* item_off, int64_t* ablk_off, int32_t* counts, VoteItem* items,
                      ABlock* ablocks, int64_t max_items, int64_t max_ablocks, int32_t* err,
-                     cudaStream_t s);
+                     cudaStream_t s, uint32_t* bits0 = nullptr);
 // items / ablocks needed for at most `entries` list entries over P problems of <= nmax rows
 void dp_items_bound(int mode, int64_t entries, int32_t P, int64_t nmax, int32_t slots,
                     int64_t* max_items, int64_t* max_ablocks);
@@ -105,5 +106,32 @@ void dp_launch_final_ties(const int64_t* act_off, const int64_t* cap, const uint
                           const uint32_t* lo, const int32_t* rcnt, const uint32_t* ex, int32_t P,
                           int64_t total, const unsigned long long* best, int32_t* ties,
                           cudaStream_t s);
+
+
+// Item planner of K3-C for a level's per-problem lists: the entries bucketed by (problem,
+// level-0 ancestor) (lut0: level-0 lin at resolution B0 -> bitmask row, -1 if not a
+// candidate), items of <= 32 blocks of a bucket x ranges of the ancestor's index list (l0cnt:
+// the list lengths = level-0 counts, lofs: their row offsets; ~8 items per resident warp);
+// segs[p] get the problem's k12 rows.  Scratch sizes: act P+1, acnt P*m0, aoff / ioff P*m0+1, tanc / tslot / cidx T,
+// phi 12 T floats, counts 2, work 1 (T = the level's total entries).
+struct CullScratch {
+  int64_t* act;
+  int32_t* acnt;
+  int64_t* aoff;
+  int64_t* ioff;
+  int32_t* tanc;
+  int32_t* tslot;
+  int32_t* cidx;
+  float* phi;
+  int32_t* counts;
+  int32_t* work;
+};
+void launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
+                       int32_t B, int32_t B0, const int32_t* lut0, int64_t m0,
+                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
+                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
+                       CullItem* items, int64_t max_items, int32_t* err, cudaStream_t s);
+// items needed for at most `entries` list entries
+int64_t cull_items_bound(int64_t entries, int num_sms);
 
 }  // namespace rv

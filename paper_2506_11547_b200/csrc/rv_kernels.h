@@ -57,7 +57,24 @@ struct VoteSeg {
   int32_t n;             // correspondences of the problem
   int32_t B;             // grid resolution of lins
   double eps;            // inlier angle
+  // ancestor culling (rv_cull.cu): the level-0 pass bitmasks of the problem (row r = level-0
+  // block r, wpc words per row, bit i%32 of word i/32 = correspondence i passed that block's
+  // bound test) and its 48-byte K rows; K3-TC with bits != nullptr writes the bitmasks
+  uint32_t* bits;
+  const float* k12;      // [n_pad][12] fp32: the 9 entries of K1, then 3 zeros
+  int32_t wpc;           // words per bitmask row (= the problem's padded rows / 32)
+  int32_t pad_;
 };
+
+// K3-C work item: the ncell (<= 32) blocks at bucket positions [pos0, pos0 + ncell) of the
+// level's bucket order (phi rows and list indices there), all of problem seg and one level-0
+// ancestor, against the entries [e0, e0 + ne) of that ancestor's index list (a range of
+// its row in the compacted level-0 lists).
+struct CullItem {
+  int32_t seg, pos0, ncell, ne;
+  int64_t e0;
+};
+constexpr int kCullMaxCells = 32;    // blocks per K3-C item
 
 // One thread block of work: blocks [cell0, cell0+ncell) of segment seg against
 // correspondences [i0, i0+ni) of it (i0, ni multiples of 4; rows >= n are zero padding).
@@ -98,8 +115,11 @@ void launch_vote(int mode, int groups, const float* k9, int64_t stride, const Vo
 
 // K1-TC: fp16-split correspondence table for the tensor-core vote (64 B per row,
 // interleaved K-major layout, each problem padded to a multiple of kTcN rows).
+// k12 != nullptr: also the 48-byte fp32 K rows of the culled vote ([toffs rows][12], the same
+// fp64 -> fp32 rounding as K1).
 void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const int64_t* toffs,
-                     int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s);
+                     int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s,
+                     float* k12 = nullptr);
 
 // K3-TC: BOUND-mode vote on tcgen05 (items: ncell <= kTcM, i0/ni multiples of kTcN, koff
 // in table rows); final_mode: RV_MODE_FINAL counts at tau -/+ guard (items: ncell <= kTcM/2).
@@ -113,7 +133,26 @@ constexpr int64_t kTcABlockBytes = 128 * 64;
 void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, int32_t n_ablocks,
                     const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
                     float* dump, int64_t dump_ld, cudaStream_t s, bool final_mode = false,
-                    const int32_t* counts_dev = nullptr);
+                    const int32_t* counts_dev = nullptr, bool emit_bits = false);
+
+// K3-C (rv_cull.cu): the culled vote.  mode RV_MODE_BOUND / RV_MODE_FINAL; counts_dev[0] =
+// item count (device); work counter: zeroed by the item planner; pairs: += evaluated pairs.
+// phi / cidx: the planner's bucket-order block rows and list indices; lidx: the level-0 index
+// lists (cull_compact).
+void launch_vote_cull(int mode, const VoteSeg* segs, const CullItem* items,
+                      const int32_t* counts_dev, int32_t* work, unsigned long long* pairs,
+                      const float* phi, const int32_t* cidx, const uint32_t* lidx, float guard,
+                      int num_sms, cudaStream_t s);
+// Level-0 index lists: row offsets lofs[P*m0 + 1] (exclusive prefix of the level-0 counts, each
+// padded to a multiple of 4; lofs[P*m0] = the total), then the compaction of the K3-TC bitmasks
+// (bits0: problem p's rows from m0 * toffs[p] / 32, (toffs[p+1] - toffs[p]) / 32 words each).
+void launch_cull_rows(const uint32_t* l0cnt, int32_t P, int64_t m0, int64_t* lofs,
+                      cudaStream_t s);
+// (any order within a row; fill: scratch [P*m0] int32)
+void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P, int64_t m0,
+                         int64_t wpc_max, const int64_t* lofs, int32_t* fill, uint32_t* lidx,
+                         cudaStream_t s);
+
 
 // K4 (batched): level-0 reductions, one CTA per problem.  argmax: the dive's start index per
 // problem (planner key, see rv_plan_feed_l0_start).  survivors: outc != nullptr counts the

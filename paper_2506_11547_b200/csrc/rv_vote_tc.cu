@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
                                                           const int64_t* __restrict__ rows,
                                                           const int64_t* __restrict__ toffs,
                                                           int32_t P, int64_t total_pad,
-                                                          uint8_t* __restrict__ tab) {
+                                                          uint8_t* __restrict__ tab,
+                                                          float* __restrict__ k12) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total_pad;
        g += (int64_t)gridDim.x * blockDim.x) {
     int32_t lo = 0, hi = P;
@@ -186,8 +187,18 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
       }
       v[27] = __float2half_rn(1.0f);
       v[28] = __float2half_rn(1.0f);
+      if (k12) {  // the culled vote's rows: K1's fp64 -> fp32 rounding
+        float4* kr = reinterpret_cast<float4*>(k12 + g * 12);
+        kr[0] = make_float4((float)k[0], (float)k[1], (float)k[2], (float)k[3]);
+        kr[1] = make_float4((float)k[4], (float)k[5], (float)k[6], (float)k[7]);
+        kr[2] = make_float4((float)k[8], 0.0f, 0.0f, 0.0f);
+      }
     } else {
       v[29] = __float2half_rn(1.0f);  // padding row: S' = -1
+      if (k12) {
+        float4* kr = reinterpret_cast<float4*>(k12 + g * 12);
+        kr[0] = kr[1] = kr[2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
     }
     // row g of the whole table: group g>>3, 4 chunks of 16 B
     uint8_t* rowp = tab + (g >> 3) * 512 + (g & 7) * 16;
@@ -203,11 +214,11 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
 }
 
 void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const int64_t* toffs,
-                     int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s) {
+                     int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s, float* k12) {
   int64_t blocks = (total_pad + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  rv_setup_tc_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, y, rows, toffs, P, total_pad, tab);
+  rv_setup_tc_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, y, rows, toffs, P, total_pad, tab, k12);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -232,6 +243,7 @@ constexpr uint32_t kTileBytes = kTcN * 64;  // 16 KB at N = 256
 
 static_assert(!RV_TC_PINGPONG || (kTcAcc == 2 && kTcEpiWarps == 8),
               "ping-pong epilogue: two accumulators, one warp pair per TMEM lane quarter");
+static_assert(RV_TC_PINGPONG || kTcN == 256, "bitmask emission needs the ping-pong epilogue");
 
 struct __align__(1024) TcSmem {
   uint8_t b[kTcStages][kTileBytes];  // correspondence tiles
@@ -305,7 +317,9 @@ __global__ void __launch_bounds__(128) rv_tc_atab_kernel(const VoteSeg* __restri
 // FIN: RV_MODE_FINAL -- two A rows per cell (TMEM lanes 2c, 2c+1) carry the thresholds
 //      tau - g' (cnt_a) and tau + g' (cnt_b), so an item covers kTcM/2 cells.
 // ABL (ablation, tuning only): bit0 skip the count, bit1 skip the MMAs, bit2 skip the TMA
-template <bool DUMP, int ABL = 0, bool FIN = false>
+// BITS: also write each cell's pass bitmask (seg.bits, ancestor culling, rv_cull.cu): bit e of
+//       word (i0 + 256 t) / 32 + 4 rr + q = score >= 0 for that column
+template <bool DUMP, int ABL = 0, bool FIN = false, bool BITS = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
     rv_vote_tc_kernel(const uint8_t* __restrict__ tab, const uint8_t* __restrict__ atab,
                       const VoteSeg* __restrict__ segs, const VoteItem* __restrict__ items,
@@ -430,7 +444,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             __syncwarp();
             if (lane == 0) bar_arrive(&sm.tempty[half]);
           }
-          if (DUMP) {
+          if (BITS) {
+            // sign bits -> one word per 32 columns (shf funnel: w = w << 1 | sign, column 31
+            // first, so bit e = column e); count = columns - negatives; store the pass words
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int e = 31; e >= 0; --e)
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w[q]) : "r"(r[q][e]));
+            n0 += __popc(w[0]);
+            n1 += __popc(w[1]);
+            n2 += __popc(w[2]);
+            n3 += __popc(w[3]);
+            if (cell < it.ncell) {
+              const VoteSeg& sg = segs[it.seg];
+              uint32_t* wp = sg.bits + (int64_t)(it.cell0 + cell) * sg.wpc +
+                             ((it.i0 + t * kTcN) >> 5) + rr * 4;
+              *reinterpret_cast<uint4*>(wp) = make_uint4(~w[0], ~w[1], ~w[2], ~w[3]);
+            }
+          } else if (DUMP) {
             if (cell < it.ncell) {
               float* drow = dump + (int64_t)(it.cell0 + cell) * dump_ld + it.i0 + (int64_t)t * kTcN + rr * 128;
 #pragma unroll
@@ -533,7 +566,7 @@ size_t tc_smem_bytes() { return sizeof(TcSmem) + 1024; }
 void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, int32_t n_ablocks,
                     const VoteSeg* segs, const VoteItem* items, int32_t n_items, float guard,
                     float* dump, int64_t dump_ld, cudaStream_t s, bool final_mode,
-                    const int32_t* counts_dev) {
+                    const int32_t* counts_dev, bool emit_bits) {
   if (!counts_dev && (n_items <= 0 || n_ablocks <= 0)) return;
   static int sms = [] {
     int dev = 0, v = 148;
@@ -556,7 +589,14 @@ void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, in
                          (int)tc_smem_bytes());
     cudaFuncSetAttribute(rv_vote_tc_kernel<false, 0, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes());
+    cudaFuncSetAttribute(rv_vote_tc_kernel<false, 0, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes());
     attr = true;
+  }
+  if (emit_bits && !final_mode && !dump) {
+    rv_vote_tc_kernel<false, 0, false, true><<<grid, kTcThreads, tc_smem_bytes(), s>>>(
+        tab, atab, segs, items, n_items, counts_dev, guard, nullptr, 0);
+    return;
   }
   if (final_mode) {
     rv_vote_tc_kernel<false, 0, true><<<grid, kTcThreads, tc_smem_bytes(), s>>>(

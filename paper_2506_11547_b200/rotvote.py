@@ -40,7 +40,7 @@ class rv_config(C.Structure):
                 ("nccl_id", C.c_void_p), ("max_n", C.c_int64), ("max_problems", C.c_int32),
                 ("chain_len", C.c_int32), ("chain", C.c_int32 * RV_MAX_CHAIN),
                 ("refine_rounds", C.c_int32), ("guard", C.c_float), ("stream", C.c_void_p),
-                ("emulate_world", C.c_int32), ("tensor_vote", C.c_int32)]
+                ("emulate_world", C.c_int32), ("tensor_vote", C.c_int32), ("cull", C.c_int32)]
 
 
 class rv_result(C.Structure):
@@ -50,7 +50,9 @@ class rv_result(C.Structure):
                 ("cells_evaluated", C.c_uint64), ("lb_star", C.c_uint32), ("n_phases", C.c_int32),
                 ("cells_per_phase", C.c_int64 * RV_MAX_PHASES), ("ms", C.c_float),
                 ("n_rechecked", C.c_int32), ("vote_ms", C.c_float), ("launches", C.c_int32),
-                ("vote_pairs", C.c_uint64), ("vote_launches", C.c_int32), ("pad_", C.c_int32)]
+                ("vote_pairs", C.c_uint64), ("vote_launches", C.c_int32),
+                ("cull_launches", C.c_int32), ("cull_pairs", C.c_uint64), ("cull_ms", C.c_float),
+                ("pad_", C.c_int32)]
 
 
 class rv_alg1_result(C.Structure):
@@ -109,6 +111,8 @@ def lib() -> C.CDLL:
     L.rot_vote_solve_multi.argtypes = [vp, vp, vp, i64, dbl, i32, i32, dbl, C.POINTER(rv_result),
                                        C.POINTER(i32)]
     L.rot_vote_debug_tc_scores.argtypes = [vp, vp, vp, i64, i32, vp, i64, dbl, vp]
+    L.rot_vote_count_cells_culled.argtypes = [vp, vp, vp, i64, i32, i32, vp, i64, dbl, i32, vp, vp,
+                                              vp]
     L.rv_plan_request_is_full_grid.argtypes = [vp]
     L.rv_plan_create.argtypes = [vp, i32, i32, i64, dbl, dbl, C.POINTER(vp)]
     L.rv_plan_create_ex.argtypes = [vp, i32, i32, i64, dbl, dbl, vp, i32, dbl, C.POINTER(vp)]
@@ -189,6 +193,9 @@ class Result:
     launches: int = 0
     vote_pairs: int = 0
     vote_launches: int = 0
+    cull_launches: int = 0
+    cull_pairs: int = 0
+    cull_ms: float = 0.0
 
     @property
     def lin(self) -> int:
@@ -203,7 +210,8 @@ class Result:
                       lb_star=r.lb_star, cells_per_phase=list(r.cells_per_phase[:r.n_phases]),
                       ms=r.ms, n_rechecked=r.n_rechecked, vote_ms=r.vote_ms,
                       launches=r.launches, vote_pairs=r.vote_pairs,
-                      vote_launches=r.vote_launches)
+                      vote_launches=r.vote_launches, cull_launches=r.cull_launches,
+                      cull_pairs=r.cull_pairs, cull_ms=r.cull_ms)
 
 
 class RotVote:
@@ -212,7 +220,7 @@ class RotVote:
     def __init__(self, device: int = 0, max_n: int = 1 << 20, max_problems: int = 1,
                  chain=None, refine_rounds: int = 2, guard: float = 1e-5, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 emulate_world: int = 0, tensor_vote: bool = True):
+                 emulate_world: int = 0, tensor_vote: bool = True, cull: bool = True):
         import torch
         cfg = rot_vote_default_config()
         cfg.device = device
@@ -235,6 +243,7 @@ class RotVote:
         cfg.stream = C.c_void_p(stream.cuda_stream)
         cfg.emulate_world = int(emulate_world)
         cfg.tensor_vote = int(bool(tensor_vote))
+        cfg.cull = int(bool(cull))
         self.cfg = cfg
         self.device = device
         self.chain = tuple(chain) if chain is not None else DEFAULT_CHAIN
@@ -317,6 +326,30 @@ class RotVote:
         ca = a.cpu().numpy().view(np.uint32)
         cb = b.cpu().numpy().view(np.uint32)
         return (ca, cb) if mode in (RV_MODE_FINAL, RV_MODE_FINAL_TC) else ca
+
+    def count_cells_culled(self, x, y, B0: int, B: int, lins, eps: float, mode: int,
+                           want_bits: bool = False):
+        """K3-C test hook: counts of `lins` (resolution B) over their level-0 (B0) ancestors'
+        pass lists; (cnt_a[, cnt_b][, bits]) with bits uint32 [m0, ceil(n/256)*8]."""
+        import torch
+        lins = torch.as_tensor(np.asarray(lins, np.uint32).view(np.int32), device=x.device)
+        m, n = lins.numel(), x.shape[0]
+        a = torch.zeros(max(m, 1), dtype=torch.int32, device=x.device)
+        b = torch.zeros(max(m, 1), dtype=torch.int32, device=x.device)
+        bits = None
+        if want_bits:
+            m0 = lib().rv_grid_candidates(int(B0), None, 0)
+            bits = torch.zeros((m0, (n + 255) // 256 * 8), dtype=torch.int32, device=x.device)
+        _check(self.ctx, lib().rot_vote_count_cells_culled(
+            self.ctx, _dptr(x, torch.float32, "x"), _dptr(y, torch.float32, "y"), n, int(B0),
+            int(B), lins.data_ptr() if m else a.data_ptr(), m, float(eps), int(mode),
+            a.data_ptr(), b.data_ptr(), bits.data_ptr() if bits is not None else None))
+        out = [a.cpu().numpy().view(np.uint32)[:m]]
+        if mode == RV_MODE_FINAL:
+            out.append(b.cpu().numpy().view(np.uint32)[:m])
+        if want_bits:
+            out.append(bits.cpu().numpy().view(np.uint32))
+        return out[0] if len(out) == 1 else tuple(out)
 
     def solve_multi(self, x, y, eps: float, K: int, rho: float, levels: int = 0) -> list:
         """NEXT-2: up to K rotations, greedy peaks with suppression angle rho (radians)."""

@@ -72,7 +72,7 @@ def test_device_loop_equals_host_planner(torch_cuda, tensor_vote, chain, levels)
     from paper_2506_11547_b200 import RotVote
     torch = torch_cuda
     bt = ragged_batch(5 + levels, 96, 3000, 0.1)
-    ctx = RotVote(max_n=int(bt.offsets[-1]) + 16, max_problems=96, chain=chain,
+    ctx = RotVote(max_n=int(bt.offsets[-1]) + 16, max_problems=96, chain=chain, cull=False,
                   tensor_vote=tensor_vote)
     try:
         x, y = dev(torch, bt.x), dev(torch, bt.y)
@@ -93,7 +93,7 @@ def test_device_loop_cfg5_equals_host_planner(torch_cuda):
     from paper_2506_11547_b200 import RotVote
     torch = torch_cuda
     bt = datagen.cfg5()
-    ctx = RotVote(max_n=int(bt.offsets[-1]) + 16, max_problems=4096, tensor_vote=True)
+    ctx = RotVote(max_n=int(bt.offsets[-1]) + 16, max_problems=4096, tensor_vote=True, cull=False)
     try:
         x, y = dev(torch, bt.x), dev(torch, bt.y)
         rd = ctx.solve_batched(x, y, bt.offsets, bt.eps)
@@ -120,7 +120,7 @@ def test_device_loop_degenerate_batches(torch_cuda):
     anti.y[:] = -anti.x
     probs.append(anti)
     bt = datagen.batch_of(probs, 0.2)
-    ctx = RotVote(max_n=4096, max_problems=8)
+    ctx = RotVote(max_n=4096, max_problems=8, cull=False)
     try:
         x, y = dev(torch, bt.x), dev(torch, bt.y)
         rd = ctx.solve_batched(x, y, bt.offsets, bt.eps)
@@ -141,7 +141,7 @@ def test_device_loop_large_single_problems(torch_cuda):
     item, uneven last chunks) through the device loop equal the host-planner solve."""
     from paper_2506_11547_b200 import RotVote
     torch = torch_cuda
-    ctx = RotVote(max_n=1_000_000)
+    ctx = RotVote(max_n=1_000_000, cull=False)
     try:
         cases = [datagen.make_problem(20_000, 400, 0.01, 0.05, seed=81),
                  datagen.make_problem(70_001, 700, 0.01, 0.05, seed=82),
@@ -162,7 +162,7 @@ def test_single_solve_device_loop_equals_host_planner(torch_cuda, tensor_vote):
     sharding path, RV_HOST_PLAN=1) must agree on every field, incl. per-phase block counts."""
     from paper_2506_11547_b200 import RotVote
     torch = torch_cuda
-    ctx = RotVote(max_n=200_000, tensor_vote=tensor_vote)
+    ctx = RotVote(max_n=200_000, tensor_vote=tensor_vote, cull=False)
     try:
         cases = [datagen.cfg1(), datagen.cfg2(seed=3), datagen.cfg3(seed=4)]
         rng = np.random.default_rng(77)
@@ -195,7 +195,7 @@ def test_sharded_single_solve_loopback(torch_cuda, tensor_vote):
         x, y = dev(torch, pr.x), dev(torch, pr.y)
         ref = None
         for W in (1, 2, 3, 4, 8):
-            ctx = RotVote(max_n=1 << 17, emulate_world=W, tensor_vote=tensor_vote)
+            ctx = RotVote(max_n=1 << 17, emulate_world=W, tensor_vote=tensor_vote, cull=False)
             try:
                 r = ctx.solve(x, y, pr.eps)
                 rh = host_plan(lambda: ctx.solve(x, y, pr.eps))
