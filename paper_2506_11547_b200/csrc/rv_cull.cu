@@ -370,7 +370,7 @@ __global__ void cull_items(int32_t P, int64_t m0, const int32_t* __restrict__ ac
 template <int MODE>
 struct CullSmem {
   static constexpr size_t stage = (size_t)kCullChunk * 48;  // 128 K rows (AoS, 12 floats)
-  static constexpr size_t per_warp = 2 * stage;
+  static constexpr size_t per_warp = 2 * stage + 2 * 32 * 4;  // + per-block count totals
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -401,7 +401,8 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
   constexpr bool FIN = MODE == RV_MODE_FINAL;
   extern __shared__ __align__(16) uint8_t cull_smem[];
   float* sk0 = reinterpret_cast<float*>(cull_smem + (threadIdx.x >> 5) * CullSmem<MODE>::per_warp);
-  const int lane = threadIdx.x & 31, quad = lane >> 2, grp = lane & 3;
+  uint32_t* tot = reinterpret_cast<uint32_t*>(sk0 + 2 * kCullChunk * 12);  // [2][32]
+  const int lane = threadIdx.x & 31;
   const int32_t n_items = counts_dev[0];
   const float two_g = 2.0f * guard;
   for (;;) {
@@ -413,10 +414,14 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
     const VoteSeg& sg = segs[it.seg];
     const int ncell = it.ncell;
     const float* __restrict__ k12 = sg.k12;
-    // this lane's four blocks 4q .. 4q+3 (a quad of the planner's phi table: row j holds
-    // phi_j of the four, row 9 the initial values); quads past ncell vote zeros, never stored
+    // lanes: nq = ceil(ncell / 4) block quads x G = 32 / nq entry groups (lanes past nq * G
+    // idle); lane l votes quad l % nq (blocks 4q .. 4q+3, a quad of the planner's phi table:
+    // row j holds phi_j of the four, row 9 the initial values) against entries g, g + G, ...
+    const int nq = (ncell + 3) >> 2, G = 32 / nq;
+    const int quad = lane % nq, grp = lane / nq;
+    const bool active = grp < G;
     float2 pa[9], pb[9], ia, ib;
-    if (4 * quad < ncell) {
+    {
       const float4* r = reinterpret_cast<const float4*>(phi + (int64_t)(it.pos0 + 4 * quad) * 12);
 #pragma unroll
       for (int t = 0; t < 9; ++t) {
@@ -427,11 +432,9 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
       const float4 v9 = __ldg(r + 9);
       ia = make_float2(v9.x, v9.y);
       ib = make_float2(v9.z, v9.w);
-    } else {
-#pragma unroll
-      for (int t = 0; t < 9; ++t) pa[t] = pb[t] = make_float2(0.0f, 0.0f);
-      ia = ib = make_float2(0.0f, 0.0f);
     }
+    tot[lane] = 0u;
+    tot[32 + lane] = 0u;
     uint32_t na0 = 0, na1 = 0, na2 = 0, na3 = 0, nb0 = 0, nb1 = 0, nb2 = 0, nb3 = 0;
     uint32_t S = 0, V = 0;  // entry slots this lane voted / of which zero padding
     auto count = [&](const float2 a, const float2 b) {
@@ -489,15 +492,16 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
       }
       __syncwarp();
       const float4* sk4 = reinterpret_cast<const float4*>(sk0 + stg * (kCullChunk * 12));
-      // two entries (e, e + 4) per step, four independent FFMA2 chains.  Two register sets
+      // two entries (e, e + G) per step, four independent FFMA2 chains.  Two register sets
       // ping-pong: the rows of the next step are read from shared memory while this step
       // computes (no register rotation).  Rows past `cur` are stale stage data: computed,
       // never counted.
       struct Rows { float kv[9], mv[9]; };
       auto ld = [&](int e, Rows& r) {
-        const int ee = e < kCullChunk - 4 ? e : grp;
-        const float4 k0 = sk4[3 * ee], k1 = sk4[3 * ee + 1], k2 = sk4[3 * ee + 2];
-        const float4 m0 = sk4[3 * ee + 12], m1 = sk4[3 * ee + 13], m2 = sk4[3 * ee + 14];
+        const int ek = e < kCullChunk ? e : kCullChunk - 1;  // rows past the stage: never
+        const int em = e + G < kCullChunk ? e + G : kCullChunk - 1;  // counted, kept in bounds
+        const float4 k0 = sk4[3 * ek], k1 = sk4[3 * ek + 1], k2 = sk4[3 * ek + 2];
+        const float4 m0 = sk4[3 * em], m1 = sk4[3 * em + 1], m2 = sk4[3 * em + 2];
         r.kv[0] = k0.x; r.kv[1] = k0.y; r.kv[2] = k0.z; r.kv[3] = k0.w;
         r.kv[4] = k1.x; r.kv[5] = k1.y; r.kv[6] = k1.z; r.kv[7] = k1.w; r.kv[8] = k2.x;
         r.mv[0] = m0.x; r.mv[1] = m0.y; r.mv[2] = m0.z; r.mv[3] = m0.w;
@@ -515,48 +519,44 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
           d = __ffma2_rn(pb[jj], m2v, d);
         }
         if (e < cur) { count(a, b); ++S; }
-        if (e + 4 < cur) { count(c, d); ++S; }
+        if (e + G < cur) { count(c, d); ++S; }
       };
-      Rows r0, r1;
-      int e = grp;
-      ld(e, r0);
+      if (active) {
+        Rows r0, r1;
+        int e = grp;
+        ld(e, r0);
 #pragma unroll 1
-      for (; e < cur; e += 16) {
-        ld(e + 8, r1);
-        step(r0, e);
-        if (e + 8 >= cur) break;
-        ld(e + 16, r0);
-        step(r1, e + 8);
+        for (; e < cur; e += 4 * G) {
+          ld(e + 2 * G, r1);
+          step(r0, e);
+          if (e + 2 * G >= cur) break;
+          ld(e + 4 * G, r0);
+          step(r1, e + 2 * G);
+        }
       }
       __syncwarp();  // stage stg is free for the gather after next
       stg ^= 1;
     }
-    // counts of this lane's entry group, summed over the quad's four groups
-    // processed slots - negatives - zero-padding slots that scored >= 0 (score = initial value)
+    // counts of this lane's entry group (processed slots - negatives - zero-padding slots that
+    // scored >= 0), summed over the quad's groups in shared memory, one global atomic per block
     auto pad = [&](float init) { return (__float_as_uint(init) >> 31) ? 0u : V; };
-    uint32_t c[4] = {S - na0 - pad(ia.x), S - na1 - pad(ia.y), S - na2 - pad(ib.x),
-                     S - na3 - pad(ib.y)};
-    uint32_t d[4] = {S - nb0 - pad(ia.x - two_g), S - nb1 - pad(ia.y - two_g),
-                     S - nb2 - pad(ib.x - two_g), S - nb3 - pad(ib.y - two_g)};
+    if (active && S) {
+      const uint32_t c[4] = {S - na0 - pad(ia.x), S - na1 - pad(ia.y), S - na2 - pad(ib.x),
+                             S - na3 - pad(ib.y)};
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      c[u] += __shfl_xor_sync(0xffffffffu, c[u], 1);
-      c[u] += __shfl_xor_sync(0xffffffffu, c[u], 2);
+      for (int u = 0; u < 4; ++u) atomicAdd(&tot[4 * quad + u], c[u]);
       if (FIN) {
-        d[u] += __shfl_xor_sync(0xffffffffu, d[u], 1);
-        d[u] += __shfl_xor_sync(0xffffffffu, d[u], 2);
+        const uint32_t d[4] = {S - nb0 - pad(ia.x - two_g), S - nb1 - pad(ia.y - two_g),
+                               S - nb2 - pad(ib.x - two_g), S - nb3 - pad(ib.y - two_g)};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) atomicAdd(&tot[32 + 4 * quad + u], d[u]);
       }
     }
-    if (grp == 0) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int cc = 4 * quad + u;
-        if (cc < ncell) {
-          const int32_t e = cidx[it.pos0 + cc];
-          if (c[u]) atomicAdd(&sg.cnt_a[e], c[u]);
-          if (FIN && d[u]) atomicAdd(&sg.cnt_b[e], d[u]);
-        }
-      }
+    __syncwarp();
+    if (lane < ncell) {
+      const int32_t e = cidx[it.pos0 + lane];
+      if (tot[lane]) atomicAdd(&sg.cnt_a[e], tot[lane]);
+      if (FIN && tot[32 + lane]) atomicAdd(&sg.cnt_b[e], tot[32 + lane]);
     }
     if (lane == 0 && pairs) atomicAdd(pairs, (unsigned long long)it.ne * (unsigned long long)ncell);
   }
