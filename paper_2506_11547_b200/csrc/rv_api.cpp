@@ -1411,7 +1411,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                           ctx->cull_m0, ctx->cull_l0cnt, ctx->c_lofs.p, ctx->k12.p, eps, mode,
                           ctx->cfg.guard,
                           ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, mi, ctx->dp_err.p, s);
-    ctx->launches += 5;
+    ctx->launches += 4;
     cudaEvent_t e0, e1;
     RV_CUDA(ctx->cev_pair(&e0, &e1), "event");
     RV_CUDA(cudaEventRecord(e0, s), "event");

@@ -112,10 +112,12 @@ __device__ __forceinline__ int32_t ancestor(uint32_t lin, int32_t B, int32_t f, 
 // bitmask words.  The scatter also writes each block's phi(q_c) and threshold (fp64 -> fp32,
 // K3's rounding) once per level, in bucket order, so the vote kernel loads them.
 
-// act[p] = exclusive prefix of the list lengths (one CTA)
-__global__ void __launch_bounds__(1024) cull_act(DpList L, int32_t P, int64_t* act) {
+// act[p] = exclusive prefix of the list lengths (one CTA); zeroes acnt[0 .. nzero)
+__global__ void __launch_bounds__(1024) cull_act(DpList L, int32_t P, int64_t* act, int32_t* acnt,
+                                                 int64_t nzero) {
   __shared__ int64_t sh[64];
   const int t = threadIdx.x, T = blockDim.x;
+  for (int64_t b = t; b < nzero; b += T) acnt[b] = 0;  // the bucket counters (small NB)
   const int p0 = (int)((int64_t)P * t / T), p1 = (int)((int64_t)P * (t + 1) / T);
   int64_t v = 0;
   for (int p = p0; p < p1; ++p) v += list_m(L, p);
@@ -178,11 +180,14 @@ __global__ void __launch_bounds__(1024) cull_rows(const uint32_t* __restrict__ l
 // rows' segments are compacted in parallel; each row ends with exactly l0cnt[b] entries
 // (K3-TC's count is the popcount of its words).
 constexpr int kCompactSeg = 256;
+constexpr int kCompactStage = 1024;  // entries staged in shared memory per warp
 __global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__ bits0,
                                                     const int64_t* __restrict__ toffs, int64_t m0,
                                                     int64_t NB, int64_t nseg,
                                                     const int64_t* __restrict__ lofs,
                                                     int32_t* fill, uint32_t* idx) {
+  __shared__ uint32_t sstage[8][kCompactStage];
+  uint32_t* stage = sstage[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -209,7 +214,10 @@ __global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__
     int base = 0;
     if (lane == 0) base = atomicAdd(&fill[b], total);
     base = __shfl_sync(0xffffffffu, base, 0);
-    uint32_t* out = idx + lofs[b] + base + (incl - c);
+    uint32_t* gout = idx + lofs[b] + base;
+    // sparse segments go through shared memory so the global writes are coalesced
+    const bool staged = total <= kCompactStage;
+    uint32_t* out = staged ? stage + (incl - c) : gout + (incl - c);
 #pragma unroll
     for (int s8 = 0; s8 < 8; ++s8) {
       const uint4& v = s8 < 4 ? v0 : v1;
@@ -219,6 +227,11 @@ __global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__
         *out++ = cb + (uint32_t)(__ffs(w) - 1);
         w &= w - 1;
       }
+    }
+    if (staged) {
+      __syncwarp();
+      for (int e = lane; e < total; e += 32) gout[e] = stage[e];
+      __syncwarp();
     }
   }
 }
@@ -305,7 +318,7 @@ __global__ void __launch_bounds__(1024) cull_scan(DpList L, const int64_t* __res
 // block quad (positions 4k .. 4k+3) 12 float4 rows, row j = (v_j of its 4 blocks) with
 // v = phi(q_c) (9), -(threshold) (the chain's initial value), 0, 0 -- so a lane loads its quad's
 // phi_j as one float4 whose halves are the aligned register pairs FFMA2 takes
-__global__ void cull_scatter(DpList L, int32_t P, int32_t B, double eps, int mode, float guard,
+__device__ __forceinline__ void cull_scatter_body(DpList L, int32_t P, int32_t B, double eps, int mode, float guard,
                              int64_t m0, const int64_t* __restrict__ act,
                              const int64_t* __restrict__ aoff, const int32_t* __restrict__ tanc,
                              const int32_t* __restrict__ tslot, int32_t* cidx, float* phi) {
@@ -330,7 +343,7 @@ __global__ void cull_scatter(DpList L, int32_t P, int32_t B, double eps, int mod
   }
 }
 
-__global__ void cull_items(int32_t P, int64_t m0, const int32_t* __restrict__ acnt,
+__device__ __forceinline__ void cull_items_body(int32_t P, int64_t m0, const int32_t* __restrict__ acnt,
                            const uint32_t* __restrict__ l0cnt, const int64_t* __restrict__ lofs,
                            const int64_t* __restrict__ aoff, const int64_t* __restrict__ ioff,
                            const int32_t* __restrict__ counts, CullItem* items, int32_t* err) {
@@ -355,6 +368,18 @@ __global__ void cull_items(int32_t P, int64_t m0, const int32_t* __restrict__ ac
     if (c < 1 || it.ncell < 1 || it.ne < 1) atomicOr(err, 4);
     items[g] = it;
   }
+}
+
+// the scatter and the item list in one launch
+__global__ void cull_fill(DpList L, int32_t P, int32_t B, double eps, int mode, float guard,
+                          int64_t m0, const int64_t* __restrict__ act,
+                          const int64_t* __restrict__ aoff, const int32_t* __restrict__ tanc,
+                          const int32_t* __restrict__ tslot, int32_t* cidx, float* phi,
+                          const int32_t* __restrict__ acnt, const uint32_t* __restrict__ l0cnt,
+                          const int64_t* __restrict__ lofs, const int64_t* __restrict__ ioff,
+                          const int32_t* __restrict__ counts, CullItem* items, int32_t* err) {
+  cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi);
+  cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err);
 }
 
 // ---- K3-C ------------------------------------------------------------------------------------
@@ -615,16 +640,17 @@ void launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toff
                        const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
                        int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
                        CullItem* items, int64_t max_items, int32_t* err, cudaStream_t s) {
-  cull_act<<<1, 1024, 0, s>>>(L, P, cs.act);
-  cudaMemsetAsync(cs.acnt, 0, (size_t)P * m0 * 4, s);
+  const int64_t NB = (int64_t)P * m0;
+  const bool small = NB <= (1 << 16);
+  if (!small) cudaMemsetAsync(cs.acnt, 0, (size_t)NB * 4, s);
+  cull_act<<<1, 1024, 0, s>>>(L, P, cs.act, cs.acnt, small ? NB : 0);
   cull_count<<<148 * 8, 256, 0, s>>>(L, P, B, B0, lut0, m0, cs.act, cs.acnt, cs.tanc, cs.tslot, err);
   const int64_t target = 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
   cull_scan<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, eps, m0, l0cnt, k12, cs.acnt, cs.aoff, cs.ioff,
                                segs, cs.counts, cs.work, target, max_items, err);
-  cull_scatter<<<148 * 8, 256, 0, s>>>(L, P, B, eps, mode, guard, m0, cs.act, cs.aoff, cs.tanc,
-                                       cs.tslot, cs.cidx, cs.phi);
-  cull_items<<<148 * 4, 256, 0, s>>>(P, m0, cs.acnt, l0cnt, lofs, cs.aoff, cs.ioff, cs.counts, items,
-                                     err);
+  cull_fill<<<148 * 8, 256, 0, s>>>(L, P, B, eps, mode, guard, m0, cs.act, cs.aoff, cs.tanc, cs.tslot,
+                                    cs.cidx, cs.phi, cs.acnt, l0cnt, lofs, cs.ioff, cs.counts, items,
+                                    err);
 }
 
 int64_t cull_items_bound(int64_t entries, int num_sms) {
