@@ -44,11 +44,25 @@ namespace {
 
 constexpr int kCullWarpsPerCta = 4;
 constexpr int kCullThreads = 32 * kCullWarpsPerCta;
+#ifndef RV_CULL_ABL
+#define RV_CULL_ABL 0  // tuning only: 1 no FFMA2, 2 no gather (wrong counts)
+#endif
+#ifndef RV_CULL_VARIANT
+#define RV_CULL_VARIANT 0
+#endif
 #ifndef RV_CULL_CTAS
 #define RV_CULL_CTAS 4
 #endif
 constexpr int kCullCtasPerSm = RV_CULL_CTAS;
-constexpr int kCullChunk = 128;                 // correspondences per gathered stage
+#ifndef RV_CULL_CHUNK
+#define RV_CULL_CHUNK 128
+#endif
+#ifndef RV_CULL_STAGES
+#define RV_CULL_STAGES 2
+#endif
+constexpr int kCullChunk = RV_CULL_CHUNK;       // correspondences per gathered stage
+constexpr int kCullStages = RV_CULL_STAGES;     // stages in flight (ring)
+constexpr int kCullPerLane = kCullChunk / 32;   // rows each lane gathers per stage
 
 __device__ __forceinline__ void add_sign(uint32_t& acc, float v) {
   asm("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(__float_as_uint(v) >> 31));
@@ -394,8 +408,8 @@ __global__ void cull_fill(DpList L, int32_t P, int32_t B, double eps, int mode, 
 // the round has <= 512 set bits, per 16-lane half otherwise).
 template <int MODE>
 struct CullSmem {
-  static constexpr size_t stage = (size_t)kCullChunk * 48;  // 128 K rows (AoS, 12 floats)
-  static constexpr size_t per_warp = 2 * stage + 2 * 32 * 4;  // + per-block count totals
+  static constexpr size_t stage = (size_t)kCullChunk * 48;  // K rows (AoS, 12 floats)
+  static constexpr size_t per_warp = kCullStages * stage + 2 * 32 * 4;  // + per-block totals
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -426,7 +440,7 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
   constexpr bool FIN = MODE == RV_MODE_FINAL;
   extern __shared__ __align__(16) uint8_t cull_smem[];
   float* sk0 = reinterpret_cast<float*>(cull_smem + (threadIdx.x >> 5) * CullSmem<MODE>::per_warp);
-  uint32_t* tot = reinterpret_cast<uint32_t*>(sk0 + 2 * kCullChunk * 12);  // [2][32]
+  uint32_t* tot = reinterpret_cast<uint32_t*>(sk0 + kCullStages * kCullChunk * 12);  // [2][32]
   const int lane = threadIdx.x & 31;
   const int32_t n_items = counts_dev[0];
   const float two_g = 2.0f * guard;
@@ -478,20 +492,21 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
     const uint32_t* li = lidx + it.e0;
     // a stage's four indices per lane are loaded one stage ahead of its gather, so the copies
     // issue without waiting on the index loads
-    auto load_idx = [&](int k, uint32_t (&ix)[4]) {
+    auto load_idx = [&](int k, uint32_t (&ix)[kCullPerLane]) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < kCullPerLane; ++r) {
         const int e = k * kCullChunk + r * 32 + lane;
         ix[r] = e < it.ne ? __ldg(li + e) : 0xffffffffu;
       }
     };
-    // gather of a stage: lane copies rows e = lane, lane + 32, ... (3 x 16 B each)
-    auto gather = [&](int stg, const uint32_t (&ix)[4]) {
+    // gather of a stage: lane copies rows e = lane, lane + 32, ... (3 x 16 B each); one
+    // commit group per stage (also when empty, so the group count stays uniform)
+    auto gather = [&](int stg, const uint32_t (&ix)[kCullPerLane]) {
       float* sk = sk0 + stg * (kCullChunk * 12);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < kCullPerLane; ++r) {
         const int e = r * 32 + lane;
-        if (ix[r] != 0xffffffffu) {
+        if (!(RV_CULL_ABL & 2) && ix[r] != 0xffffffffu) {
           const float* src = k12 + (int64_t)ix[r] * 12;
           cp_async16(sk + e * 12, src);
           cp_async16(sk + e * 12 + 4, src + 4);
@@ -500,21 +515,22 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
       }
       cp_async_commit();
     };
+    // ring of kCullStages stages: the gathers of stages k+1 .. k+S-1 are in flight while stage
+    // k is voted; the indices of the next gather are loaded a stage ahead of it
     const int nst = (it.ne + kCullChunk - 1) / kCullChunk;
-    int stg = 0;
-    uint32_t ixn[4];
+    uint32_t ixn[kCullPerLane];
     load_idx(0, ixn);
-    gather(0, ixn);
-    if (nst > 1) load_idx(1, ixn);
+#pragma unroll
+    for (int k = 0; k < kCullStages - 1; ++k) {
+      gather(k, ixn);  // stages past nst gather nothing (empty groups)
+      load_idx(k + 1, ixn);
+    }
+    int stg = 0;
     for (int k = 0; k < nst; ++k) {
       const int cur = min(kCullChunk, it.ne - k * kCullChunk);
-      if (k + 1 < nst) {
-        gather(stg ^ 1, ixn);
-        if (k + 2 < nst) load_idx(k + 2, ixn);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
+      gather((k + kCullStages - 1) % kCullStages, ixn);
+      load_idx(k + kCullStages, ixn);
+      cp_async_wait<kCullStages - 1>();
       __syncwarp();
       const float4* sk4 = reinterpret_cast<const float4*>(sk0 + stg * (kCullChunk * 12));
       // two entries (e, e + G) per step, four independent FFMA2 chains.  Two register sets
@@ -534,6 +550,9 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
       };
       auto step = [&](const Rows& r, int e) {
         float2 a = ia, b = ib, c = ia, d = ib;
+#if RV_CULL_ABL & 1
+        a.x += r.kv[0]; b.y += r.mv[8]; c.x += r.kv[4]; d.y += r.mv[2];  // ablation: no FFMA2
+#else
 #pragma unroll
         for (int jj = 0; jj < 9; ++jj) {
           const float2 k2v = make_float2(r.kv[jj], r.kv[jj]);
@@ -543,9 +562,41 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
           c = __ffma2_rn(pa[jj], m2v, c);
           d = __ffma2_rn(pb[jj], m2v, d);
         }
+#endif
         if (e < cur) { count(a, b); ++S; }
         if (e + G < cur) { count(c, d); ++S; }
       };
+#if RV_CULL_VARIANT == 1
+      // variant 1: four entries per step, eight chains, rows loaded at the step's start
+      if (active) {
+#pragma unroll 1
+        for (int e = grp; e < cur; e += 4 * G) {
+          Rows r0, r1;
+          ld(e, r0);
+          ld(e + 2 * G, r1);
+          float2 a0 = ia, b0 = ib, c0 = ia, d0 = ib, a1 = ia, b1 = ib, c1 = ia, d1 = ib;
+#pragma unroll
+          for (int jj = 0; jj < 9; ++jj) {
+            const float2 k0 = make_float2(r0.kv[jj], r0.kv[jj]);
+            const float2 m0 = make_float2(r0.mv[jj], r0.mv[jj]);
+            const float2 k1 = make_float2(r1.kv[jj], r1.kv[jj]);
+            const float2 m1 = make_float2(r1.mv[jj], r1.mv[jj]);
+            a0 = __ffma2_rn(pa[jj], k0, a0);
+            b0 = __ffma2_rn(pb[jj], k0, b0);
+            c0 = __ffma2_rn(pa[jj], m0, c0);
+            d0 = __ffma2_rn(pb[jj], m0, d0);
+            a1 = __ffma2_rn(pa[jj], k1, a1);
+            b1 = __ffma2_rn(pb[jj], k1, b1);
+            c1 = __ffma2_rn(pa[jj], m1, c1);
+            d1 = __ffma2_rn(pb[jj], m1, d1);
+          }
+          if (e < cur) { count(a0, b0); ++S; }
+          if (e + G < cur) { count(c0, d0); ++S; }
+          if (e + 2 * G < cur) { count(a1, b1); ++S; }
+          if (e + 3 * G < cur) { count(c1, d1); ++S; }
+        }
+      }
+#else
       if (active) {
         Rows r0, r1;
         int e = grp;
@@ -559,9 +610,11 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
           step(r1, e + 2 * G);
         }
       }
-      __syncwarp();  // stage stg is free for the gather after next
-      stg ^= 1;
+#endif
+      __syncwarp();  // stage stg is free for the next gather into it
+      stg = stg + 1 == kCullStages ? 0 : stg + 1;
     }
+    cp_async_wait<0>();  // no copy may still target the stages when the next item starts
     // counts of this lane's entry group (processed slots - negatives - zero-padding slots that
     // scored >= 0), summed over the quad's groups in shared memory, one global atomic per block
     auto pad = [&](float init) { return (__float_as_uint(init) >> 31) ? 0u : V; };
