@@ -1398,8 +1398,8 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     RV_CUDA(ctx->c_ioff.ensure(nb + 1), "allocating");
     RV_CUDA(ctx->c_tanc.ensure(eb), "allocating");
     RV_CUDA(ctx->c_tslot.ensure(eb), "allocating");
-    RV_CUDA(ctx->c_cidx.ensure(eb + 3 * nb + 4), "allocating");      // bucket positions are
-    RV_CUDA(ctx->c_phi.ensure((eb + 3 * nb + 4) * 12), "allocating");  // padded to quads
+    RV_CUDA(ctx->c_cidx.ensure(eb + 3 * nb + 8), "allocating");      // bucket positions are
+    RV_CUDA(ctx->c_phi.ensure((eb + 3 * nb + 8) * 12), "allocating");  // padded to quads
     RV_CUDA(ctx->c_icnt.ensure(2), "allocating");
     RV_CUDA(ctx->c_work.ensure(1), "allocating");
     RV_CUDA(ctx->vsegs.ensure(PL), "allocating segments");
@@ -1407,11 +1407,11 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     const rv::CullScratch cs{ctx->c_act.p, ctx->c_acnt.p, ctx->c_aoff.p, ctx->c_ioff.p,
                              ctx->c_tanc.p, ctx->c_tslot.p, ctx->c_cidx.p, ctx->c_phi.p,
                              ctx->c_icnt.p, ctx->c_work.p};
-    rv::launch_cull_items(Ld, ctx->rows.p, ctx->toffs.p, PL, B, ctx->cull_B0, ctx->lut0.p,
-                          ctx->cull_m0, ctx->cull_l0cnt, ctx->c_lofs.p, ctx->k12.p, eps, mode,
-                          ctx->cfg.guard,
-                          ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, mi, ctx->dp_err.p, s);
-    ctx->launches += 4;
+    ctx->launches += rv::launch_cull_items(Ld, ctx->rows.p, ctx->toffs.p, PL, B, ctx->cull_B0,
+                                           ctx->lut0.p, ctx->cull_m0, ctx->cull_l0cnt,
+                                           ctx->c_lofs.p, ctx->k12.p, eps, mode, ctx->cfg.guard,
+                                           ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, eb, mi,
+                                           ctx->dp_err.p, s);
     cudaEvent_t e0, e1;
     RV_CUDA(ctx->cev_pair(&e0, &e1), "event");
     RV_CUDA(cudaEventRecord(e0, s), "event");

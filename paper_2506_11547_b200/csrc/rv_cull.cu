@@ -50,10 +50,14 @@ constexpr int kCullThreads = 32 * kCullWarpsPerCta;
 #ifndef RV_CULL_VARIANT
 #define RV_CULL_VARIANT 0
 #endif
+#ifndef RV_CULL_CPL
+#define RV_CULL_CPL 8  // blocks per lane (4: quads, 8: octets)
+#endif
 #ifndef RV_CULL_CTAS
-#define RV_CULL_CTAS 4
+#define RV_CULL_CTAS (RV_CULL_CPL == 8 ? 3 : 4)
 #endif
 constexpr int kCullCtasPerSm = RV_CULL_CTAS;
+constexpr int kCullCellsPerLane = RV_CULL_CPL;
 #ifndef RV_CULL_CHUNK
 #define RV_CULL_CHUNK 128
 #endif
@@ -127,8 +131,8 @@ __device__ __forceinline__ int32_t ancestor(uint32_t lin, int32_t B, int32_t f, 
 // K3's rounding) once per level, in bucket order, so the vote kernel loads them.
 
 // act[p] = exclusive prefix of the list lengths (one CTA); zeroes acnt[0 .. nzero)
-__global__ void __launch_bounds__(1024) cull_act(DpList L, int32_t P, int64_t* act, int32_t* acnt,
-                                                 int64_t nzero) {
+__device__ __forceinline__ void cull_act_body(DpList L, int32_t P, int64_t* act, int32_t* acnt,
+                                              int64_t nzero) {
   __shared__ int64_t sh[64];
   const int t = threadIdx.x, T = blockDim.x;
   for (int64_t b = t; b < nzero; b += T) acnt[b] = 0;  // the bucket counters (small NB)
@@ -148,8 +152,13 @@ __device__ __forceinline__ const uint32_t* list_lins(const DpList& L, int p) {
   return L.shared ? L.lins : L.lins + L.base[p];
 }
 
+__global__ void __launch_bounds__(1024) cull_act(DpList L, int32_t P, int64_t* act, int32_t* acnt,
+                                                 int64_t nzero) {
+  cull_act_body(L, P, act, acnt, nzero);
+}
+
 // bucket sizes: acnt[p * m0 + a] (zeroed by the caller); each entry's ancestor and slot
-__global__ void cull_count(DpList L, int32_t P, int32_t B, int32_t B0,
+__device__ __forceinline__ void cull_count_body(DpList L, int32_t P, int32_t B, int32_t B0,
                            const int32_t* __restrict__ lut0, int64_t m0,
                            const int64_t* __restrict__ act, int32_t* acnt, int32_t* tanc,
                            int32_t* tslot, int32_t* err) {
@@ -168,6 +177,12 @@ __global__ void cull_count(DpList L, int32_t P, int32_t B, int32_t B0,
     tanc[g] = a;
     tslot[g] = atomicAdd(&acnt[(int64_t)p * m0 + a], 1);
   }
+}
+__global__ void cull_count(DpList L, int32_t P, int32_t B, int32_t B0,
+                           const int32_t* __restrict__ lut0, int64_t m0,
+                           const int64_t* __restrict__ act, int32_t* acnt, int32_t* tanc,
+                           int32_t* tslot, int32_t* err) {
+  cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err);
 }
 
 // One CTA: lofs[b] = exclusive prefix of the level-0 counts rounded up to 4 (list row starts,
@@ -254,7 +269,7 @@ __global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__
 // chunk CE (multiple of 128, ~`target` items in all), item offsets ioff per bucket
 // (ceil(cnt / 32) groups x ceil(|L(a)| / CE) chunks), the segments, counts = {n_items, CE};
 // zeroes the work counter.
-__global__ void __launch_bounds__(1024) cull_scan(DpList L, const int64_t* __restrict__ rows,
+__device__ __forceinline__ void cull_scan_body(DpList L, const int64_t* __restrict__ rows,
                                                   const int64_t* __restrict__ toffs, int32_t P,
                                                   int32_t B, double eps, int64_t m0,
                                                   const uint32_t* __restrict__ l0cnt,
@@ -327,6 +342,18 @@ __global__ void __launch_bounds__(1024) cull_scan(DpList L, const int64_t* __res
     *work = 0;
   }
 }
+__global__ void __launch_bounds__(1024) cull_scan(DpList L, const int64_t* __restrict__ rows,
+                                                  const int64_t* __restrict__ toffs, int32_t P,
+                                                  int32_t B, double eps, int64_t m0,
+                                                  const uint32_t* __restrict__ l0cnt,
+                                                  const float* k12,
+                                                  const int32_t* __restrict__ acnt, int64_t* aoff,
+                                                  int64_t* ioff, VoteSeg* segs, int32_t* counts,
+                                                  int32_t* work, int64_t target, int64_t max_items,
+                                                  int32_t* err) {
+  cull_scan_body(L, rows, toffs, P, B, eps, m0, l0cnt, k12, acnt, aoff, ioff, segs, counts, work,
+                 target, max_items, err);
+}
 
 // entries into bucket order: cidx[pos] = the entry's index in its problem's list; phi: per
 // block quad (positions 4k .. 4k+3) 12 float4 rows, row j = (v_j of its 4 blocks) with
@@ -396,6 +423,26 @@ __global__ void cull_fill(DpList L, int32_t P, int32_t B, double eps, int mode, 
   cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err);
 }
 
+// All of a small level's planning in one CTA (the four steps above, block barriers between):
+// one launch instead of four for the dive and the levels past the big one.
+__global__ void __launch_bounds__(1024) cull_plan_small(
+    DpList L, const int64_t* __restrict__ rows, const int64_t* __restrict__ toffs, int32_t P,
+    int32_t B, int32_t B0, const int32_t* __restrict__ lut0, int64_t m0, double eps, int mode,
+    float guard, const uint32_t* __restrict__ l0cnt, const int64_t* __restrict__ lofs,
+    const float* k12, int64_t* act, int32_t* acnt, int32_t* tanc, int32_t* tslot, int64_t* aoff,
+    int64_t* ioff, int32_t* cidx, float* phi, VoteSeg* segs, int32_t* counts, int32_t* work,
+    CullItem* items, int64_t target, int64_t max_items, int32_t* err) {
+  cull_act_body(L, P, act, acnt, (int64_t)P * m0);
+  __syncthreads();
+  cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err);
+  __syncthreads();
+  cull_scan_body(L, rows, toffs, P, B, eps, m0, l0cnt, k12, acnt, aoff, ioff, segs, counts, work,
+                 target, max_items, err);
+  __syncthreads();
+  cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi);
+  cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err);
+}
+
 // ---- K3-C ------------------------------------------------------------------------------------
 // One warp per item.  Lane = (block quad q = lane / 4, entry group h = lane % 4): the lane holds
 // phi(q_c) and the thresholds of blocks 4q .. 4q+3 in registers (as two block pairs, the vector
@@ -408,7 +455,8 @@ __global__ void cull_fill(DpList L, int32_t P, int32_t B, double eps, int mode, 
 // the round has <= 512 set bits, per 16-lane half otherwise).
 template <int MODE>
 struct CullSmem {
-  static constexpr size_t stage = (size_t)kCullChunk * 48;  // K rows (AoS, 12 floats)
+  static constexpr size_t stage = (size_t)(kCullChunk + 1) * 48;  // K rows (AoS, 12 floats) +
+                                                                  // a zero row
   static constexpr size_t per_warp = kCullStages * stage + 2 * 32 * 4;  // + per-block totals
 };
 
@@ -438,9 +486,12 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
                         const int32_t* __restrict__ cidx, const uint32_t* __restrict__ lidx,
                         float guard) {
   constexpr bool FIN = MODE == RV_MODE_FINAL;
+  constexpr int CPL = kCullCellsPerLane, NP = CPL / 2;
   extern __shared__ __align__(16) uint8_t cull_smem[];
   float* sk0 = reinterpret_cast<float*>(cull_smem + (threadIdx.x >> 5) * CullSmem<MODE>::per_warp);
-  uint32_t* tot = reinterpret_cast<uint32_t*>(sk0 + kCullStages * kCullChunk * 12);  // [2][32]
+  uint32_t* tot = reinterpret_cast<uint32_t*>(sk0 + kCullStages * (kCullChunk + 1) * 12);  // [2][32]
+  for (int z = threadIdx.x & 31; z < kCullStages * 12; z += 32)  // the stages' zero rows
+    sk0[(z / 12) * (kCullChunk + 1) * 12 + kCullChunk * 12 + z % 12] = 0.0f;
   const int lane = threadIdx.x & 31;
   const int32_t n_items = counts_dev[0];
   const float two_g = 2.0f * guard;
@@ -453,39 +504,43 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
     const VoteSeg& sg = segs[it.seg];
     const int ncell = it.ncell;
     const float* __restrict__ k12 = sg.k12;
-    // lanes: nq = ceil(ncell / 4) block quads x G = 32 / nq entry groups (lanes past nq * G
-    // idle); lane l votes quad l % nq (blocks 4q .. 4q+3, a quad of the planner's phi table:
-    // row j holds phi_j of the four, row 9 the initial values) against entries g, g + G, ...
-    const int nq = (ncell + 3) >> 2, G = 32 / nq;
-    const int quad = lane % nq, grp = lane / nq;
+    // lanes: no = ceil(ncell / CPL) block groups x G = 32 / no entry groups (lanes past no * G
+    // idle); lane l votes block group l % no (blocks CPL o .. CPL o + CPL - 1, i.e. quads of
+    // the planner's phi table: row j holds phi_j of the four, row 9 the initial values) against
+    // entries g, g + G, ...
+    const int no = (ncell + CPL - 1) / CPL, G = 32 / no;
+    const int oct = lane % no, grp = lane / no;
     const bool active = grp < G;
-    float2 pa[9], pb[9], ia, ib;
-    {
-      const float4* r = reinterpret_cast<const float4*>(phi + (int64_t)(it.pos0 + 4 * quad) * 12);
+    float2 pp[NP][9], ini[NP];
+#pragma unroll
+    for (int h = 0; h < CPL / 4; ++h) {
+      const float4* r =
+          reinterpret_cast<const float4*>(phi + (int64_t)(it.pos0 + CPL * oct + 4 * h) * 12);
 #pragma unroll
       for (int t = 0; t < 9; ++t) {
         const float4 v4 = __ldg(r + t);
-        pa[t] = make_float2(v4.x, v4.y);
-        pb[t] = make_float2(v4.z, v4.w);
+        pp[2 * h][t] = make_float2(v4.x, v4.y);
+        pp[2 * h + 1][t] = make_float2(v4.z, v4.w);
       }
       const float4 v9 = __ldg(r + 9);
-      ia = make_float2(v9.x, v9.y);
-      ib = make_float2(v9.z, v9.w);
+      ini[2 * h] = make_float2(v9.x, v9.y);
+      ini[2 * h + 1] = make_float2(v9.z, v9.w);
     }
     tot[lane] = 0u;
     tot[32 + lane] = 0u;
-    uint32_t na0 = 0, na1 = 0, na2 = 0, na3 = 0, nb0 = 0, nb1 = 0, nb2 = 0, nb3 = 0;
+    uint32_t na[CPL], nb[CPL];
+#pragma unroll
+    for (int u = 0; u < CPL; ++u) na[u] = nb[u] = 0u;
     uint32_t S = 0, V = 0;  // entry slots this lane voted / of which zero padding
-    auto count = [&](const float2 a, const float2 b) {
-      add_sign(na0, a.x);
-      add_sign(na1, a.y);
-      add_sign(na2, b.x);
-      add_sign(na3, b.y);
-      if (FIN) {
-        add_sign(nb0, a.x - two_g);
-        add_sign(nb1, a.y - two_g);
-        add_sign(nb2, b.x - two_g);
-        add_sign(nb3, b.y - two_g);
+    auto count = [&](const float2 (&acc)[NP]) {
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        add_sign(na[2 * u], acc[u].x);
+        add_sign(na[2 * u + 1], acc[u].y);
+        if (FIN) {
+          add_sign(nb[2 * u], acc[u].x - two_g);
+          add_sign(nb[2 * u + 1], acc[u].y - two_g);
+        }
       }
     };
     __syncwarp();    // the previous item's readers of the stages are done
@@ -502,7 +557,7 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
     // gather of a stage: lane copies rows e = lane, lane + 32, ... (3 x 16 B each); one
     // commit group per stage (also when empty, so the group count stays uniform)
     auto gather = [&](int stg, const uint32_t (&ix)[kCullPerLane]) {
-      float* sk = sk0 + stg * (kCullChunk * 12);
+      float* sk = sk0 + stg * ((kCullChunk + 1) * 12);
 #pragma unroll
       for (int r = 0; r < kCullPerLane; ++r) {
         const int e = r * 32 + lane;
@@ -532,15 +587,27 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
       load_idx(k + kCullStages, ixn);
       cp_async_wait<kCullStages - 1>();
       __syncwarp();
-      const float4* sk4 = reinterpret_cast<const float4*>(sk0 + stg * (kCullChunk * 12));
+      const float4* sk4 = reinterpret_cast<const float4*>(sk0 + stg * ((kCullChunk + 1) * 12));
       // two entries (e, e + G) per step, four independent FFMA2 chains.  Two register sets
       // ping-pong: the rows of the next step are read from shared memory while this step
       // computes (no register rotation).  Rows past `cur` are stale stage data: computed,
       // never counted.
+      // Lane slots: entries grp, grp + G, ... in steps of two (e, e + G); every lane runs
+      // the same number of steps T, slots past `cur` read the stage's zero row (score = the
+      // initial value, corrected for in the count through V) -- no per-entry predicates.
+      // Two register sets ping-pong: the next step's rows are read while this step computes.
       struct Rows { float kv[9], mv[9]; };
       auto ld = [&](int e, Rows& r) {
-        const int ek = e < kCullChunk ? e : kCullChunk - 1;  // rows past the stage: never
-        const int em = e + G < kCullChunk ? e + G : kCullChunk - 1;  // counted, kept in bounds
+#if RV_CULL_ABL & 4  // ablation: no shared-memory reads (rows from the lane's own registers)
+#pragma unroll
+        for (int jj = 0; jj < 9; ++jj) {
+          r.kv[jj] = pp[0][jj].x + (float)e;
+          r.mv[jj] = pp[NP - 1][jj].y;
+        }
+        return;
+#endif
+        const int ek = e < cur ? e : kCullChunk;
+        const int em = e + G < cur ? e + G : kCullChunk;
         const float4 k0 = sk4[3 * ek], k1 = sk4[3 * ek + 1], k2 = sk4[3 * ek + 2];
         const float4 m0 = sk4[3 * em], m1 = sk4[3 * em + 1], m2 = sk4[3 * em + 2];
         r.kv[0] = k0.x; r.kv[1] = k0.y; r.kv[2] = k0.z; r.kv[3] = k0.w;
@@ -548,86 +615,62 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
         r.mv[0] = m0.x; r.mv[1] = m0.y; r.mv[2] = m0.z; r.mv[3] = m0.w;
         r.mv[4] = m1.x; r.mv[5] = m1.y; r.mv[6] = m1.z; r.mv[7] = m1.w; r.mv[8] = m2.x;
       };
-      auto step = [&](const Rows& r, int e) {
-        float2 a = ia, b = ib, c = ia, d = ib;
+      auto step = [&](const Rows& r) {
+        float2 a[NP], c[NP];
+#pragma unroll
+        for (int u = 0; u < NP; ++u) a[u] = c[u] = ini[u];
 #if RV_CULL_ABL & 1
-        a.x += r.kv[0]; b.y += r.mv[8]; c.x += r.kv[4]; d.y += r.mv[2];  // ablation: no FFMA2
+        a[0].x += r.kv[0]; c[NP - 1].y += r.mv[8];  // ablation: no FFMA2
 #else
 #pragma unroll
         for (int jj = 0; jj < 9; ++jj) {
           const float2 k2v = make_float2(r.kv[jj], r.kv[jj]);
           const float2 m2v = make_float2(r.mv[jj], r.mv[jj]);
-          a = __ffma2_rn(pa[jj], k2v, a);
-          b = __ffma2_rn(pb[jj], k2v, b);
-          c = __ffma2_rn(pa[jj], m2v, c);
-          d = __ffma2_rn(pb[jj], m2v, d);
+#pragma unroll
+          for (int u = 0; u < NP; ++u) {
+            a[u] = __ffma2_rn(pp[u][jj], k2v, a[u]);
+            c[u] = __ffma2_rn(pp[u][jj], m2v, c[u]);
+          }
         }
 #endif
-        if (e < cur) { count(a, b); ++S; }
-        if (e + G < cur) { count(c, d); ++S; }
+        count(a);
+        count(c);
       };
-#if RV_CULL_VARIANT == 1
-      // variant 1: four entries per step, eight chains, rows loaded at the step's start
       if (active) {
-#pragma unroll 1
-        for (int e = grp; e < cur; e += 4 * G) {
-          Rows r0, r1;
-          ld(e, r0);
-          ld(e + 2 * G, r1);
-          float2 a0 = ia, b0 = ib, c0 = ia, d0 = ib, a1 = ia, b1 = ib, c1 = ia, d1 = ib;
-#pragma unroll
-          for (int jj = 0; jj < 9; ++jj) {
-            const float2 k0 = make_float2(r0.kv[jj], r0.kv[jj]);
-            const float2 m0 = make_float2(r0.mv[jj], r0.mv[jj]);
-            const float2 k1 = make_float2(r1.kv[jj], r1.kv[jj]);
-            const float2 m1 = make_float2(r1.mv[jj], r1.mv[jj]);
-            a0 = __ffma2_rn(pa[jj], k0, a0);
-            b0 = __ffma2_rn(pb[jj], k0, b0);
-            c0 = __ffma2_rn(pa[jj], m0, c0);
-            d0 = __ffma2_rn(pb[jj], m0, d0);
-            a1 = __ffma2_rn(pa[jj], k1, a1);
-            b1 = __ffma2_rn(pb[jj], k1, b1);
-            c1 = __ffma2_rn(pa[jj], m1, c1);
-            d1 = __ffma2_rn(pb[jj], m1, d1);
-          }
-          if (e < cur) { count(a0, b0); ++S; }
-          if (e + G < cur) { count(c0, d0); ++S; }
-          if (e + 2 * G < cur) { count(a1, b1); ++S; }
-          if (e + 3 * G < cur) { count(c1, d1); ++S; }
-        }
-      }
-#else
-      if (active) {
+        const int T = ((cur + G - 1) / G + 1) >> 1;          // steps (warp-uniform)
+        const int nv = cur > grp ? (cur - grp + G - 1) / G : 0;  // this lane's real entries
+        S += (uint32_t)(2 * T);
+        V += (uint32_t)(2 * T - nv);
         Rows r0, r1;
         int e = grp;
         ld(e, r0);
 #pragma unroll 1
-        for (; e < cur; e += 4 * G) {
+        for (int t = 0; t < T; t += 2) {
           ld(e + 2 * G, r1);
-          step(r0, e);
-          if (e + 2 * G >= cur) break;
+          step(r0);
+          if (t + 1 >= T) break;
           ld(e + 4 * G, r0);
-          step(r1, e + 2 * G);
+          step(r1);
+          e += 4 * G;
         }
       }
-#endif
       __syncwarp();  // stage stg is free for the next gather into it
       stg = stg + 1 == kCullStages ? 0 : stg + 1;
     }
     cp_async_wait<0>();  // no copy may still target the stages when the next item starts
     // counts of this lane's entry group (processed slots - negatives - zero-padding slots that
-    // scored >= 0), summed over the quad's groups in shared memory, one global atomic per block
+    // scored >= 0), summed over the block group's lanes in shared memory, one global atomic per
+    // block
     auto pad = [&](float init) { return (__float_as_uint(init) >> 31) ? 0u : V; };
     if (active && S) {
-      const uint32_t c[4] = {S - na0 - pad(ia.x), S - na1 - pad(ia.y), S - na2 - pad(ib.x),
-                             S - na3 - pad(ib.y)};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) atomicAdd(&tot[4 * quad + u], c[u]);
-      if (FIN) {
-        const uint32_t d[4] = {S - nb0 - pad(ia.x - two_g), S - nb1 - pad(ia.y - two_g),
-                               S - nb2 - pad(ib.x - two_g), S - nb3 - pad(ib.y - two_g)};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) atomicAdd(&tot[32 + 4 * quad + u], d[u]);
+      for (int u = 0; u < NP; ++u) {
+        atomicAdd(&tot[CPL * oct + 2 * u], S - na[2 * u] - pad(ini[u].x));
+        atomicAdd(&tot[CPL * oct + 2 * u + 1], S - na[2 * u + 1] - pad(ini[u].y));
+        if (FIN) {
+          atomicAdd(&tot[32 + CPL * oct + 2 * u], S - nb[2 * u] - pad(ini[u].x - two_g));
+          atomicAdd(&tot[32 + CPL * oct + 2 * u + 1], S - nb[2 * u + 1] - pad(ini[u].y - two_g));
+        }
       }
     }
     __syncwarp();
@@ -688,22 +731,31 @@ void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P,
                                                                    fill, lidx);
 }
 
-void launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
-                       int32_t B, int32_t B0, const int32_t* lut0, int64_t m0,
-                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
-                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
-                       CullItem* items, int64_t max_items, int32_t* err, cudaStream_t s) {
+int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
+                      int32_t B, int32_t B0, const int32_t* lut0, int64_t m0,
+                      const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
+                      int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
+                      CullItem* items, int64_t entries_bound, int64_t max_items, int32_t* err,
+                      cudaStream_t s) {
   const int64_t NB = (int64_t)P * m0;
+  const int64_t target = 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
+  if (entries_bound <= 8192 && NB <= (1 << 14)) {
+    cull_plan_small<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, B0, lut0, m0, eps, mode, guard, l0cnt,
+                                       lofs, k12, cs.act, cs.acnt, cs.tanc, cs.tslot, cs.aoff,
+                                       cs.ioff, cs.cidx, cs.phi, segs, cs.counts, cs.work, items,
+                                       target, max_items, err);
+    return 1;
+  }
   const bool small = NB <= (1 << 16);
   if (!small) cudaMemsetAsync(cs.acnt, 0, (size_t)NB * 4, s);
   cull_act<<<1, 1024, 0, s>>>(L, P, cs.act, cs.acnt, small ? NB : 0);
   cull_count<<<148 * 8, 256, 0, s>>>(L, P, B, B0, lut0, m0, cs.act, cs.acnt, cs.tanc, cs.tslot, err);
-  const int64_t target = 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
   cull_scan<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, eps, m0, l0cnt, k12, cs.acnt, cs.aoff, cs.ioff,
                                segs, cs.counts, cs.work, target, max_items, err);
   cull_fill<<<148 * 8, 256, 0, s>>>(L, P, B, eps, mode, guard, m0, cs.act, cs.aoff, cs.tanc, cs.tslot,
                                     cs.cidx, cs.phi, cs.acnt, l0cnt, lofs, cs.ioff, cs.counts, items,
                                     err);
+  return 4;
 }
 
 int64_t cull_items_bound(int64_t entries, int num_sms) {

@@ -126,11 +126,13 @@ struct CullScratch {
   int32_t* counts;
   int32_t* work;
 };
-void launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
-                       int32_t B, int32_t B0, const int32_t* lut0, int64_t m0,
-                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
-                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
-                       CullItem* items, int64_t max_items, int32_t* err, cudaStream_t s);
+// returns the number of kernels it launched (one CTA does everything for small levels)
+int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
+                      int32_t B, int32_t B0, const int32_t* lut0, int64_t m0,
+                      const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
+                      int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
+                      CullItem* items, int64_t entries_bound, int64_t max_items, int32_t* err,
+                      cudaStream_t s);
 // items needed for at most `entries` list entries
 int64_t cull_items_bound(int64_t entries, int num_sms);
 
