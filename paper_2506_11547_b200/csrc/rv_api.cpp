@@ -42,6 +42,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -58,9 +60,11 @@ NcclApi& nccl() {
     a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
     a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
     a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+    a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
     a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
     a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
-    a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.CommDestroy && a.GetErrorString;
+    a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.AllReduce && a.CommDestroy &&
+           a.GetErrorString;
     if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
     return a;
   }();
@@ -255,6 +259,7 @@ struct rv_ctx {
   DevBuf<uint32_t> c_lidx;       //   and the lists
   DevBuf<int32_t> c_fill;        //   compaction fill counters
   const uint32_t* cull_l0cnt = nullptr;  // the level-0 counts (= list lengths) of this solve
+  int64_t cull_own_lo = 0, cull_own_hi = INT64_MAX;  // level-0 rows a K3-C launch votes
   DevBuf<float> k12;
   DevBuf<int32_t> lut0;
   int32_t lut0_B = 0;
@@ -1359,8 +1364,14 @@ int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
   if (total > ((int64_t)1 << 29) || (!force && (double)total > 0.25 * pairs0)) return RV_OK;
   RV_CUDA(ctx->c_lidx.ensure(total + 4), "allocating level-0 lists");
   RV_CUDA(ctx->c_fill.ensure(NB), "allocating");
+  int64_t row_lo = 0, row_hi = NB;
+  if (ctx->comm && PL == 1 && ctx->cfg.world > 1) {  // this rank's level-0 slice
+    const int64_t c0 = (m0 + ctx->cfg.world - 1) / ctx->cfg.world;
+    row_lo = (int64_t)ctx->cfg.rank * c0;
+    row_hi = std::min<int64_t>(m0, row_lo + c0);
+  }
   rv::launch_cull_compact(ctx->cbits.p, ctx->toffs.p, PL, m0, ctx->cull_wpc_max, ctx->c_lofs.p,
-                          ctx->c_fill.p, ctx->c_lidx.p, s);
+                          ctx->c_fill.p, ctx->c_lidx.p, s, row_lo, row_hi);
   ctx->launches += 1;
   ctx->cull_l0cnt = l0cnt;
   ctx->cull_ready = true;
@@ -1411,7 +1422,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                                            ctx->lut0.p, ctx->cull_m0, ctx->cull_l0cnt,
                                            ctx->c_lofs.p, ctx->k12.p, eps, mode, ctx->cfg.guard,
                                            ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, eb, mi,
-                                           ctx->dp_err.p, s);
+                                           ctx->dp_err.p, s, ctx->cull_own_lo, ctx->cull_own_hi);
     cudaEvent_t e0, e1;
     RV_CUDA(ctx->cev_pair(&e0, &e1), "event");
     RV_CUDA(cudaEventRecord(e0, s), "event");
@@ -1438,7 +1449,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     rv::dp_launch_items(Ld, ctx->rows.p, im == 2 ? ctx->koffs.p : ctx->toffs.p, PL, B, eps, im,
                         ctx->num_sms, ctx->vsegs.p, ctx->dp_ioff.p, ctx->dp_aoff.p, ctx->dp_icnt.p,
                         ctx->vitems.p, ctx->ablk.p, mi, ma, ctx->dp_err.p, s,
-                        emit_bits ? ctx->cbits.p : nullptr);
+                        emit_bits ? ctx->cbits.p : nullptr, ctx->cull_m0);
     ctx->launches += 2;
     if (im == 2) {
       rv::launch_exact(ctx->k9.p, ctx->stride, x, y, ctx->vsegs.p, ctx->vitems.p, 0,
@@ -1475,7 +1486,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
 int vote_level_sharded(rv_ctx* ctx, const float* x, const float* y,
                        const std::vector<int64_t>& rows, const std::vector<int64_t>& koff,
                        double eps, int32_t mode, int32_t B, const rv::DpList& Ld, int64_t chunk,
-                       int64_t nmax) {
+                       int64_t nmax, bool emit_bits = false) {
   cudaStream_t s = ctx->stream;
   const bool nccl_path = ctx->comm != nullptr;
   const int W = ctx->effective_world();
@@ -1487,7 +1498,8 @@ int vote_level_sharded(rv_ctx* ctx, const float* x, const float* y,
                         ctx->dp_sbase.p, ctx->dp_scnt.p, s);
     ctx->launches += 1;
     const rv::DpList Ls{Ld.lins, 0, 0, ctx->dp_sbase.p, ctx->dp_scnt.p, Ld.ca, Ld.cb};
-    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, B, Ls, 1, chunk, nmax)) return rc;
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, B, Ls, 1, chunk, nmax, emit_bits))
+      return rc;
   }
   if (nccl_path) {
     const size_t off = (size_t)ctx->cfg.rank * chunk;
@@ -1496,6 +1508,37 @@ int vote_level_sharded(rv_ctx* ctx, const float* x, const float* y,
       ncclResult_t nr = nccl().AllGather(buf + off, buf, (size_t)chunk, ncclUint32, ctx->comm, s);
       if (nr != ncclSuccess)
         return ctx->fail(RV_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(nr));
+    }
+  }
+  return RV_OK;
+}
+
+// A culled level of a ONE-problem list over ranks: rank r votes the blocks whose level-0
+// ancestor is one of the rows it voted (and compacted) at level 0, [r c0, (r+1) c0); the other
+// blocks' counts stay zero and one in-place ncclAllReduce(sum) per count array assembles the
+// level (each block is voted by exactly one rank).  Loopback: every rank's share in turn.
+int vote_level_owned(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
+                     const std::vector<int64_t>& koff, double eps, int32_t mode, int32_t B,
+                     const rv::DpList& Ld, int64_t entries, int64_t nmax) {
+  const bool nccl_path = ctx->comm != nullptr;
+  const int W = ctx->effective_world();
+  const int r_lo = nccl_path ? ctx->cfg.rank : 0, r_hi = nccl_path ? r_lo + 1 : W;
+  const int64_t c0 = (ctx->cull_m0 + W - 1) / W;
+  for (int r = r_lo; r < r_hi; ++r) {
+    ctx->cull_own_lo = (int64_t)r * c0;
+    ctx->cull_own_hi = std::min<int64_t>(ctx->cull_m0, (int64_t)(r + 1) * c0);
+    int rc = vote_level(ctx, x, y, rows, koff, eps, mode, B, Ld, 1, entries, nmax);
+    ctx->cull_own_lo = 0;
+    ctx->cull_own_hi = INT64_MAX;
+    if (rc) return rc;
+  }
+  if (nccl_path) {
+    for (int a = 0; a < (mode == RV_MODE_FINAL ? 2 : 1); ++a) {
+      uint32_t* buf = a == 0 ? Ld.ca : Ld.cb;
+      ncclResult_t nr = nccl().AllReduce(buf, buf, (size_t)entries, ncclUint32, ncclSum, ctx->comm,
+                                         ctx->stream);
+      if (nr != ncclSuccess)
+        return ctx->fail(RV_ENCCL, "ncclAllReduce: %s", nccl().GetErrorString(nr));
     }
   }
   return RV_OK;
@@ -1521,6 +1564,8 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   std::vector<int64_t> phase_chunk;       // per phase: the shard chunk (0: not sharded)
   auto vote = [&](int32_t mode, int32_t B, const rv::DpList& Ld, int64_t entries) -> int {
     if (!shard) return vote_level(ctx, x, y, rows, koff, eps, mode, B, Ld, PL, entries, nmax);
+    if (ctx->cull_ready)  // culled levels: sharded by ancestor ownership
+      return vote_level_owned(ctx, x, y, rows, koff, eps, mode, B, Ld, entries, nmax);
     return vote_level_sharded(ctx, x, y, rows, koff, eps, mode, B, Ld, (entries + W - 1) / W, nmax);
   };
   // per-phase block counts, kept on the device and read once at the end
@@ -1579,9 +1624,14 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   if (cull) {
     RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, ((size_t)PL * m0 + slack) * 4, s), "memset");
     const rv::DpList l0{ctx->grid_list.p, 1, m0, nullptr, nullptr, ctx->l0cnt.p, ctx->l0cnt.p};
-    if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, PL * m0, nmax,
-                            true))
+    if (shard) {  // each rank votes (and later compacts) its slice of level 0
+      if (int rc = vote_level_sharded(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0,
+                                      (m0 + W - 1) / W, nmax, true))
+        return rc;
+    } else if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, PL * m0,
+                                   nmax, true)) {
       return rc;
+    }
     if (int rc = cull_build_lists(ctx, PL, m0, ctx->l0cnt.p)) return rc;
     culled = ctx->cull_ready;
   } else if (ctx->tc_on || shard) {
@@ -1877,8 +1927,13 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
       add(c);
     }
     if (nre > 0) add(nre);
-    if (culled) {  // K3-TC voted level 0 only (unsharded); K3-C counts its own pairs
-      tc_pairs += (uint64_t)m0 * n;
+    if (culled) {  // K3-TC voted level 0 only (this rank's slice); K3-C counts its own pairs
+      if (shard && ctx->comm) {
+        const int64_t c0 = (m0 + W - 1) / W;
+        tc_pairs += (uint64_t)std::max<int64_t>(0, std::min<int64_t>(c0, m0 - (int64_t)ctx->cfg.rank * c0)) * n;
+      } else {
+        tc_pairs += (uint64_t)m0 * n;
+      }
     } else if (cull) {  // level 0 unsharded, the finer levels on K3-TC (sharded if W > 1)
       tc_pairs += (uint64_t)m0 * n;
       for (int ph = 0; ph + 1 < nph; ++ph) {

@@ -161,16 +161,16 @@ __global__ void __launch_bounds__(1024) cull_act(DpList L, int32_t P, int64_t* a
 __device__ __forceinline__ void cull_count_body(DpList L, int32_t P, int32_t B, int32_t B0,
                            const int32_t* __restrict__ lut0, int64_t m0,
                            const int64_t* __restrict__ act, int32_t* acnt, int32_t* tanc,
-                           int32_t* tslot, int32_t* err) {
+                           int32_t* tslot, int32_t* err, int64_t own_lo, int64_t own_hi) {
   const int64_t T = act[P];
   const int32_t f = B / B0;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < T;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int p = find_p(act, P, g);
     const int32_t a = ancestor(list_lins(L, p)[g - act[p]], B, f, B0, lut0);
-    if (a < 0) {
-      atomicOr(err, 4);
-      tanc[g] = 0;
+    if (a < 0) atomicOr(err, 4);
+    if (a < own_lo || a >= own_hi) {  // another rank's ancestor (or the error above)
+      tanc[g] = -1;
       tslot[g] = 0;
       continue;
     }
@@ -181,8 +181,8 @@ __device__ __forceinline__ void cull_count_body(DpList L, int32_t P, int32_t B, 
 __global__ void cull_count(DpList L, int32_t P, int32_t B, int32_t B0,
                            const int32_t* __restrict__ lut0, int64_t m0,
                            const int64_t* __restrict__ act, int32_t* acnt, int32_t* tanc,
-                           int32_t* tslot, int32_t* err) {
-  cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err);
+                           int32_t* tslot, int32_t* err, int64_t own_lo, int64_t own_hi) {
+  cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err, own_lo, own_hi);
 }
 
 // One CTA: lofs[b] = exclusive prefix of the level-0 counts rounded up to 4 (list row starts,
@@ -212,7 +212,7 @@ constexpr int kCompactSeg = 256;
 constexpr int kCompactStage = 1024;  // entries staged in shared memory per warp
 __global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__ bits0,
                                                     const int64_t* __restrict__ toffs, int64_t m0,
-                                                    int64_t NB, int64_t nseg,
+                                                    int64_t row_lo, int64_t NR, int64_t nseg,
                                                     const int64_t* __restrict__ lofs,
                                                     int32_t* fill, uint32_t* idx) {
   __shared__ uint32_t sstage[8][kCompactStage];
@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       task < NB * nseg; task += nwarps) {
-    const int64_t b = task / nseg, sg = task % nseg;
+       task < NR * nseg; task += nwarps) {
+    const int64_t b = row_lo + task / nseg, sg = task % nseg;
     const int64_t p = b / m0, a = b % m0;
     const int64_t wpc = (toffs[p + 1] - toffs[p]) / 32;
     const int64_t w0 = sg * kCompactSeg;
@@ -366,6 +366,7 @@ __device__ __forceinline__ void cull_scatter_body(DpList L, int32_t P, int32_t B
   const int64_t T = act[P];
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < T;
        g += (int64_t)gridDim.x * blockDim.x) {
+    if (tanc[g] < 0) continue;  // not this rank's
     const int p = find_p(act, P, g);
     const int64_t e = g - act[p];
     const int64_t pos = aoff[(int64_t)p * m0 + tanc[g]] + tslot[g];
@@ -431,10 +432,11 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
     float guard, const uint32_t* __restrict__ l0cnt, const int64_t* __restrict__ lofs,
     const float* k12, int64_t* act, int32_t* acnt, int32_t* tanc, int32_t* tslot, int64_t* aoff,
     int64_t* ioff, int32_t* cidx, float* phi, VoteSeg* segs, int32_t* counts, int32_t* work,
-    CullItem* items, int64_t target, int64_t max_items, int32_t* err) {
+    CullItem* items, int64_t target, int64_t max_items, int32_t* err, int64_t own_lo,
+    int64_t own_hi) {
   cull_act_body(L, P, act, acnt, (int64_t)P * m0);
   __syncthreads();
-  cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err);
+  cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err, own_lo, own_hi);
   __syncthreads();
   cull_scan_body(L, rows, toffs, P, B, eps, m0, l0cnt, k12, acnt, aoff, ioff, segs, counts, work,
                  target, max_items, err);
@@ -722,13 +724,16 @@ void launch_cull_rows(const uint32_t* l0cnt, int32_t P, int64_t m0, int64_t* lof
 
 void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P, int64_t m0,
                          int64_t wpc_max, const int64_t* lofs, int32_t* fill, uint32_t* lidx,
-                         cudaStream_t s) {
+                         cudaStream_t s, int64_t row_lo, int64_t row_hi) {
   const int64_t NB = (int64_t)P * m0, nseg = (wpc_max + kCompactSeg - 1) / kCompactSeg;
+  if (row_hi > NB) row_hi = NB;
+  if (row_lo >= row_hi) return;
+  const int64_t NR = row_hi - row_lo;
   cudaMemsetAsync(fill, 0, (size_t)NB * 4, s);
-  int64_t blocks = (NB * nseg + 7) / 8;
+  int64_t blocks = (NR * nseg + 7) / 8;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  cull_compact<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(bits0, toffs, m0, NB, nseg, lofs,
-                                                                   fill, lidx);
+  cull_compact<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(bits0, toffs, m0, row_lo, NR, nseg,
+                                                                   lofs, fill, lidx);
 }
 
 int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
@@ -736,20 +741,21 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
                       CullItem* items, int64_t entries_bound, int64_t max_items, int32_t* err,
-                      cudaStream_t s) {
+                      cudaStream_t s, int64_t own_lo, int64_t own_hi) {
   const int64_t NB = (int64_t)P * m0;
   const int64_t target = 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
   if (entries_bound <= 8192 && NB <= (1 << 14)) {
     cull_plan_small<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, B0, lut0, m0, eps, mode, guard, l0cnt,
                                        lofs, k12, cs.act, cs.acnt, cs.tanc, cs.tslot, cs.aoff,
                                        cs.ioff, cs.cidx, cs.phi, segs, cs.counts, cs.work, items,
-                                       target, max_items, err);
+                                       target, max_items, err, own_lo, own_hi);
     return 1;
   }
   const bool small = NB <= (1 << 16);
   if (!small) cudaMemsetAsync(cs.acnt, 0, (size_t)NB * 4, s);
   cull_act<<<1, 1024, 0, s>>>(L, P, cs.act, cs.acnt, small ? NB : 0);
-  cull_count<<<148 * 8, 256, 0, s>>>(L, P, B, B0, lut0, m0, cs.act, cs.acnt, cs.tanc, cs.tslot, err);
+  cull_count<<<148 * 8, 256, 0, s>>>(L, P, B, B0, lut0, m0, cs.act, cs.acnt, cs.tanc, cs.tslot, err,
+                                     own_lo, own_hi);
   cull_scan<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, eps, m0, l0cnt, k12, cs.acnt, cs.aoff, cs.ioff,
                                segs, cs.counts, cs.work, target, max_items, err);
   cull_fill<<<148 * 8, 256, 0, s>>>(L, P, B, eps, mode, guard, m0, cs.act, cs.aoff, cs.tanc, cs.tslot,

@@ -386,7 +386,7 @@ __device__ int64_t cta_max(int64_t v, int64_t* sh) {
 __global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
     DpList L, const int64_t* __restrict__ rows, const int64_t* __restrict__ koffs, int32_t P,
     int32_t B, double eps, int mode, int32_t slots, VoteSeg* segs, int64_t* item_off,
-    int64_t* ablk_off, int32_t* counts, uint32_t* bits0) {
+    int64_t* ablk_off, int32_t* counts, uint32_t* bits0, int64_t bits_m0) {
   __shared__ int64_t sh[kPlanThreads];
   __shared__ int64_t s_cbs, s_tmax;
   __shared__ int32_t s_nch;
@@ -489,7 +489,8 @@ __global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
     // level-0 pass bitmasks (K3-TC BITS; the list is the shared level-0 grid): rows of m0
     // blocks x wpc words, problem p from m0 * toffs[p] / 32
     sg.wpc = (int32_t)((koffs[p + 1] - koffs[p]) / 32);
-    sg.bits = bits0 ? bits0 + L.shared_m * (koffs[p] / 32) : nullptr;
+    // (a rank's slice of a one-problem grid starts at row base[0] of the grid)
+    sg.bits = bits0 ? bits0 + bits_m0 * (koffs[p] / 32) + (L.shared ? 0 : b) * sg.wpc : nullptr;
     sg.k12 = nullptr;
     sg.pad_ = 0;
     segs[p] = sg;
@@ -717,9 +718,9 @@ void dp_launch_items(const DpList& L, const int64_t* rows, const int64_t* koffs,
                      int32_t B, double eps, int mode, int32_t slots, VoteSeg* segs,
                      int64_t* item_off, int64_t* ablk_off, int32_t* counts, VoteItem* items,
                      ABlock* ablocks, int64_t max_items, int64_t max_ablocks, int32_t* err,
-                     cudaStream_t s, uint32_t* bits0) {
+                     cudaStream_t s, uint32_t* bits0, int64_t bits_m0) {
   dp_items_plan<<<1, kPlanThreads, 0, s>>>(L, rows, koffs, P, B, eps, mode, slots, segs, item_off,
-                                          ablk_off, counts, bits0);
+                                          ablk_off, counts, bits0, bits_m0);
   dp_items_write<<<148 * 4, 256, 0, s>>>(L, rows, P, mode, item_off, ablk_off, counts, items,
                                          ablocks, max_items, max_ablocks, err);
 }

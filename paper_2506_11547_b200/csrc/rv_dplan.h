@@ -28,15 +28,16 @@ struct DpList {
 // (one cell per item, 8192-correspondence chunks).  Writes segs[P] (koffs: the TC table
 // offsets for modes 0/1, the K table offsets for mode 2), items, ablocks and
 // counts = {n_items, n_ablocks, chunks}; item_off / ablk_off: scratch [P+1].  The caller
-// sizes items / ablocks from a bound (dp_items_bound).  bits0 (mode 0 on the shared level-0
-// list only): the segments carry the level-0 pass bitmasks K3-TC writes (rv_cull.cu).
+// sizes items / ablocks from a bound (dp_items_bound).  bits0 (mode 0 on the level-0 grid, or
+// a rank's slice of a one-problem grid): the segments carry the level-0 pass bitmasks K3-TC
+// writes (rv_cull.cu), bits_m0 rows per problem.
 // err: invariant violations are OR-ed in (1 child capacity, 2 item bound, 4 item shape); the
 // host checks the word once at the end of the solve (there are no silent out-of-bounds writes).
 void dp_launch_items(const DpList& L, const int64_t* rows, const int64_t* koffs, int32_t P,
                      int32_t B, double eps, int mode, int32_t slots, VoteSeg* segs,
                      int64_t* item_off, int64_t* ablk_off, int32_t* counts, VoteItem* items,
                      ABlock* ablocks, int64_t max_items, int64_t max_ablocks, int32_t* err,
-                     cudaStream_t s, uint32_t* bits0 = nullptr);
+                     cudaStream_t s, uint32_t* bits0 = nullptr, int64_t bits_m0 = 0);
 // items / ablocks needed for at most `entries` list entries over P problems of <= nmax rows
 void dp_items_bound(int mode, int64_t entries, int32_t P, int64_t nmax, int32_t slots,
                     int64_t* max_items, int64_t* max_ablocks);
@@ -127,12 +128,14 @@ struct CullScratch {
   int32_t* work;
 };
 // returns the number of kernels it launched (one CTA does everything for small levels)
+// own_lo .. own_hi: the level-0 rows (ancestors) this rank votes (blocks of other ancestors
+// are left at zero for the count all-reduce)
 int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
                       int32_t B, int32_t B0, const int32_t* lut0, int64_t m0,
                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
                       CullItem* items, int64_t entries_bound, int64_t max_items, int32_t* err,
-                      cudaStream_t s);
+                      cudaStream_t s, int64_t own_lo = 0, int64_t own_hi = INT64_MAX);
 // items needed for at most `entries` list entries
 int64_t cull_items_bound(int64_t entries, int num_sms);
 

@@ -148,10 +148,11 @@ void launch_vote_cull(int mode, const VoteSeg* segs, const CullItem* items,
 // (bits0: problem p's rows from m0 * toffs[p] / 32, (toffs[p+1] - toffs[p]) / 32 words each).
 void launch_cull_rows(const uint32_t* l0cnt, int32_t P, int64_t m0, int64_t* lofs,
                       cudaStream_t s);
-// (any order within a row; fill: scratch [P*m0] int32)
+// (any order within a row; fill: scratch [P*m0] int32; rows [row_lo, row_hi) only: the rows
+// this rank voted at level 0)
 void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P, int64_t m0,
                          int64_t wpc_max, const int64_t* lofs, int32_t* fill, uint32_t* lidx,
-                         cudaStream_t s);
+                         cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = INT64_MAX);
 
 
 // K4 (batched): level-0 reductions, one CTA per problem.  argmax: the dive's start index per
