@@ -44,6 +44,9 @@ namespace {
 
 constexpr int kCullWarpsPerCta = 4;
 constexpr int kCullThreads = 32 * kCullWarpsPerCta;
+#ifndef RV_CULL_MIN_CE
+#define RV_CULL_MIN_CE 128  // entries per K3-C item at least (multiple of 128)
+#endif
 #ifndef RV_CULL_ABL
 #define RV_CULL_ABL 0  // tuning only: 1 no FFMA2, 2 no gather (wrong counts)
 #endif
@@ -295,7 +298,7 @@ __device__ __forceinline__ void cull_scan_body(DpList L, const int64_t* __restri
   blk_scan_sum(work_e, sh, &tot_w);
   if (t == 0) {
     int64_t ce = (tot_w / (target > 0 ? target : 1) + 127) / 128 * 128;
-    s_ce = ce < 128 ? 128 : ce;
+    s_ce = ce < RV_CULL_MIN_CE ? RV_CULL_MIN_CE : ce;
   }
   __syncthreads();
   const int64_t CE = s_ce;

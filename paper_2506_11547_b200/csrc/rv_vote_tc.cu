@@ -426,6 +426,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const VoteItem it = items[idx];
       const int ntiles = it.ni / kTcN;
       uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, n4 = 0, n5 = 0, n6 = 0, n7 = 0, mine = 0;
+      // BITS: this cell's bitmask row for the item's columns (hoisted out of the tile loop)
+      uint32_t* brow = nullptr;
+      if (BITS && cell < it.ncell) {
+        const VoteSeg& sg = segs[it.seg];
+        brow = sg.bits + (int64_t)(it.cell0 + cell) * sg.wpc + (it.i0 >> 5);
+      }
       // this warp's tiles of the item: global tile index g = gt + t with g % 2 == half
       const uint32_t acc_addr = lane_addr + (uint32_t)(half * kTcN);
       for (int t = (half - (int)(gt & 1)) & 1; t < ntiles; t += 2) {
@@ -457,12 +463,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             n1 += __popc(w[1]);
             n2 += __popc(w[2]);
             n3 += __popc(w[3]);
-            if (cell < it.ncell) {
-              const VoteSeg& sg = segs[it.seg];
-              uint32_t* wp = sg.bits + (int64_t)(it.cell0 + cell) * sg.wpc +
-                             ((it.i0 + t * kTcN) >> 5) + rr * 4;
-              *reinterpret_cast<uint4*>(wp) = make_uint4(~w[0], ~w[1], ~w[2], ~w[3]);
-            }
+            if (brow)
+              *reinterpret_cast<uint4*>(brow + t * (kTcN >> 5) + rr * 4) =
+                  make_uint4(~w[0], ~w[1], ~w[2], ~w[3]);
           } else if (DUMP) {
             if (cell < it.ncell) {
               float* drow = dump + (int64_t)(it.cell0 + cell) * dump_ld + it.i0 + (int64_t)t * kTcN + rr * 128;
