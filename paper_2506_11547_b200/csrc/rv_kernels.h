@@ -45,7 +45,10 @@ constexpr int kTcAcc = 512 / kTcN;                 // K3-TC: TMEM accumulator bu
 constexpr int kTcM = 128;                          // K3-TC: cells per CTA (MMA M, TMEM lanes)
 constexpr int kTcStages = 7;                       // K3-TC: 16 KB tiles in flight (also pins 1 CTA/SM)
 constexpr int kRefThreads = 256;                   // K6/K7 block
-constexpr int kRefRowsPerItem = 2048;              // K6 rows per block (multiple of 32)
+#ifndef RV_REF_ROWS
+#define RV_REF_ROWS 2048
+#endif
+constexpr int kRefRowsPerItem = RV_REF_ROWS;       // K6 rows per block (multiple of 32)
 
 // One problem's block list for a vote launch.
 struct VoteSeg {
