@@ -174,6 +174,7 @@ struct rv_ctx {
   DevBuf<float> k9;              // [9][stride]
   int64_t stride = 0;
   DevBuf<uint8_t> tctab;         // K3-TC table, 64 B per (padded) row
+  DevBuf<uint8_t> tctab_rm;      // its rows row-major (K3-CT's gather source)
   DevBuf<int64_t> toffs;         // per-problem row offsets in tctab
   bool tc_on = false;            // cfg.tensor_vote: BOUND levels on tcgen05
   std::vector<int64_t> tc_toff;  // host copy of toffs for the current setup
@@ -266,6 +267,8 @@ struct rv_ctx {
   DevBuf<int64_t> c_act, c_aoff, c_ioff;
   DevBuf<int32_t> c_acnt, c_tanc, c_tslot, c_cidx, c_icnt, c_work;
   DevBuf<float> c_phi;
+  DevBuf<uint8_t> c_tphi;        // K3-CT block rows (fp16 split)
+  bool cull_tc = false;          // culled levels on K3-C (FP32); RV_CULL_TC=1: tensor cores (K3-CT)
   DevBuf<rv::CullItem> c_items;
   DevBuf<unsigned long long> c_pairs;
   std::vector<cudaEvent_t> cevs;
@@ -544,15 +547,19 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
       const int64_t np = offsets[p + 1] - offsets[p];
       toff[p + 1] = toff[p] + (np + rv::kTcN - 1) / rv::kTcN * rv::kTcN;
     }
-    RV_CUDA(ctx->tctab.ensure((size_t)toff[P] * 64), "allocating K3-TC table");
+    // + one group of 8 padding rows after the last problem (K3-CT gathers it for padding)
+    RV_CUDA(ctx->tctab.ensure((size_t)(toff[P] + 8) * 64), "allocating K3-TC table");
     RV_CUDA(ctx->toffs.ensure(P + 1), "allocating offsets");
     int64_t* ht = ctx->up.take<int64_t>(P + 1);  // staging sized for it above
     std::memcpy(ht, toff.data(), (P + 1) * sizeof(int64_t));
     RV_CUDA(cudaMemcpyAsync(ctx->toffs.p, ht, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
             "copying offsets");
-    if (ctx->cull_on) RV_CUDA(ctx->k12.ensure((size_t)toff[P] * 12), "allocating K3-C rows");
-    rv::launch_setup_tc(x, y, ctx->rows.p, ctx->toffs.p, P, toff[P], ctx->tctab.p, ctx->stream,
-                        ctx->cull_on ? ctx->k12.p : nullptr);
+    if (ctx->cull_on) RV_CUDA(ctx->k12.ensure((size_t)(toff[P] + 8) * 12), "allocating K3-C rows");
+    if (ctx->cull_on && ctx->cull_tc)
+      RV_CUDA(ctx->tctab_rm.ensure((size_t)(toff[P] + 8) * 64), "allocating K3-CT rows");
+    rv::launch_setup_tc(x, y, ctx->rows.p, ctx->toffs.p, P, toff[P] + 8, ctx->tctab.p, ctx->stream,
+                        ctx->cull_on ? ctx->k12.p : nullptr,
+                        ctx->cull_on && ctx->cull_tc ? ctx->tctab_rm.p : nullptr);
     ctx->launches += 1;
     ctx->tc_toff = toff;
   }
@@ -1409,15 +1416,19 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     RV_CUDA(ctx->c_ioff.ensure(nb + 1), "allocating");
     RV_CUDA(ctx->c_tanc.ensure(eb), "allocating");
     RV_CUDA(ctx->c_tslot.ensure(eb), "allocating");
-    RV_CUDA(ctx->c_cidx.ensure(eb + 3 * nb + 8), "allocating");      // bucket positions are
-    RV_CUDA(ctx->c_phi.ensure((eb + 3 * nb + 8) * 12), "allocating");  // padded to quads
+    const int64_t npos = eb + 7 * nb + 16;  // bucket positions are padded to multiples of 8
+    RV_CUDA(ctx->c_cidx.ensure(npos), "allocating");
+    RV_CUDA(ctx->c_phi.ensure(npos * 12), "allocating");
+    if (ctx->cull_tc) RV_CUDA(ctx->c_tphi.ensure(npos * 2 * 64), "allocating");
     RV_CUDA(ctx->c_icnt.ensure(2), "allocating");
     RV_CUDA(ctx->c_work.ensure(1), "allocating");
     RV_CUDA(ctx->vsegs.ensure(PL), "allocating segments");
     RV_CUDA(ctx->c_items.ensure(mi), "allocating K3-C items");
     const rv::CullScratch cs{ctx->c_act.p, ctx->c_acnt.p, ctx->c_aoff.p, ctx->c_ioff.p,
                              ctx->c_tanc.p, ctx->c_tslot.p, ctx->c_cidx.p, ctx->c_phi.p,
-                             ctx->c_icnt.p, ctx->c_work.p};
+                             ctx->c_icnt.p, ctx->c_work.p,
+                             ctx->cull_tc ? ctx->c_tphi.p : nullptr,
+                             ctx->cfg.guard + kTcExtraGuard};
     ctx->launches += rv::launch_cull_items(Ld, ctx->rows.p, ctx->toffs.p, PL, B, ctx->cull_B0,
                                            ctx->lut0.p, ctx->cull_m0, ctx->cull_l0cnt,
                                            ctx->c_lofs.p, ctx->k12.p, eps, mode, ctx->cfg.guard,
@@ -1426,9 +1437,14 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     cudaEvent_t e0, e1;
     RV_CUDA(ctx->cev_pair(&e0, &e1), "event");
     RV_CUDA(cudaEventRecord(e0, s), "event");
-    rv::launch_vote_cull(mode, ctx->vsegs.p, ctx->c_items.p, ctx->c_icnt.p, ctx->c_work.p,
-                         ctx->c_pairs.p, ctx->c_phi.p, ctx->c_cidx.p, ctx->c_lidx.p,
-                         ctx->cfg.guard, ctx->num_sms, s);
+    if (ctx->cull_tc)
+      rv::launch_vote_cull_tc(mode, ctx->vsegs.p, ctx->c_items.p, ctx->c_icnt.p, ctx->tctab_rm.p,
+                              ctx->tc_toff.back(), ctx->c_tphi.p, ctx->c_cidx.p, ctx->c_lidx.p,
+                              ctx->c_pairs.p, ctx->num_sms, s);
+    else
+      rv::launch_vote_cull(mode, ctx->vsegs.p, ctx->c_items.p, ctx->c_icnt.p, ctx->c_work.p,
+                           ctx->c_pairs.p, ctx->c_phi.p, ctx->c_cidx.p, ctx->c_lidx.p,
+                           ctx->cfg.guard, ctx->num_sms, s);
     RV_CUDA(cudaEventRecord(e1, s), "event");
     ctx->launches += 1;
     ctx->cull_launches += 1;
@@ -2246,6 +2262,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
   ctx->tc_on = cfg->tensor_vote != 0;
   ctx->cull_on = ctx->tc_on && cfg->cull != 0;
   if (const char* e = getenv("RV_CULL_MIN_N")) ctx->cull_min_n = atoll(e);
+  if (const char* e = getenv("RV_CULL_TC")) ctx->cull_tc = atoi(e) != 0;
   if (const char* fg = getenv("RV_VOTE_GROUPS")) ctx->force_groups = atoi(fg);
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -2286,7 +2303,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
 void rot_vote_destroy(rv_ctx* ctx) {
   if (!ctx) return;
   if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
-  ctx->tctab.release(); ctx->toffs.release();
+  ctx->tctab.release(); ctx->tctab_rm.release(); ctx->toffs.release();
   ctx->k9.release(); ctx->lins.release(); ctx->cnt.release(); ctx->vsegs.release();
   ctx->vitems.release(); ctx->rsegs.release(); ctx->ritems.release(); ctx->partials.release();
   ctx->qs.release(); ctx->flags.release(); ctx->ninl.release(); ctx->rows.release();
@@ -2313,6 +2330,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->c_lofs.release(); ctx->c_lidx.release(); ctx->c_fill.release();
   ctx->c_ioff.release(); ctx->c_aoff.release(); ctx->c_acnt.release(); ctx->c_tanc.release();
   ctx->c_tslot.release(); ctx->c_cidx.release(); ctx->c_phi.release(); ctx->c_icnt.release();
+  ctx->c_tphi.release();
   ctx->c_work.release(); ctx->c_items.release(); ctx->c_pairs.release();
   for (cudaEvent_t e : ctx->cevs) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);

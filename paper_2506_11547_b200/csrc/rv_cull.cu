@@ -31,12 +31,15 @@
 //                initial value and K3's operation order, so s32 is bit-identical); counts are
 //                sign bits, one atomicAdd per (block, item).
 #include <cstdint>
+#include <cstdio>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "../../include/rotvote.h"
 #include "rv_dplan.h"
 #include "rv_geom.h"
 #include "rv_kernels.h"
+#include "rv_tc_ptx.h"
 
 namespace rv {
 
@@ -290,7 +293,7 @@ __device__ __forceinline__ void cull_scan_body(DpList L, const int64_t* __restri
   int64_t ne = 0, work_e = 0;
   for (int64_t bk = b0; bk < b1; ++bk) {
     const int64_t c = acnt[bk];
-    ne += (c + 3) & ~(int64_t)3;
+    ne += (c + 7) & ~(int64_t)7;  // bucket positions padded to 8 (K3-CT 8-row groups)
     if (c) work_e += (c + 31) / 32 * (int64_t)l0cnt[bk];
   }
   int64_t tot_e, tot_w;
@@ -314,7 +317,7 @@ __device__ __forceinline__ void cull_scan_body(DpList L, const int64_t* __restri
   for (int64_t bk = b0; bk < b1; ++bk) {
     aoff[bk] = e;
     ioff[bk] = io;
-    e += (acnt[bk] + 3) & ~(int64_t)3;
+    e += (acnt[bk] + 7) & ~(int64_t)7;
     io += items_of(bk);
   }
   for (int p = t; p < P; p += T) {
@@ -365,7 +368,8 @@ __global__ void __launch_bounds__(1024) cull_scan(DpList L, const int64_t* __res
 __device__ __forceinline__ void cull_scatter_body(DpList L, int32_t P, int32_t B, double eps, int mode, float guard,
                              int64_t m0, const int64_t* __restrict__ act,
                              const int64_t* __restrict__ aoff, const int32_t* __restrict__ tanc,
-                             const int32_t* __restrict__ tslot, int32_t* cidx, float* phi) {
+                             const int32_t* __restrict__ tslot, int32_t* cidx, float* phi,
+                             uint8_t* tphi, float tc_guard) {
   const int64_t T = act[P];
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < T;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -385,6 +389,39 @@ __device__ __forceinline__ void cull_scatter_body(DpList L, int32_t P, int32_t B
 #pragma unroll
     for (int t = 0; t < 9; ++t) q4[4 * t] = (float)f[t];
     q4[36] = (float)(-thr);
+    if (tphi) {  // K3-CT's B operand: K2-TC rows [phi_hi | phi_lo | phi_hi | -t_hi, -t_lo, -1, 0, 0]
+      const bool fin = mode == RV_MODE_FINAL;
+      for (int h = 0; h < (fin ? 2 : 1); ++h) {
+        const double tt = fin ? cos(eps) + (h ? tc_guard : -tc_guard)
+                              : bound_threshold(B, i, j, k, eps) - tc_guard;
+        __half v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = __float2half_rn(0.0f);
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          const __half hi = __double2half(f[t]);
+          const __half lo = __double2half(f[t] - (double)__half2float(hi));
+          v[t] = hi;
+          v[9 + t] = lo;
+          v[18 + t] = hi;
+        }
+        const __half th = __double2half(-tt);
+        const __half tl = __double2half(-tt - (double)__half2float(th));
+        v[27] = th;
+        v[28] = tl;
+        v[29] = __float2half_rn(-1.0f);
+        const int64_t row = fin ? 2 * pos + h : pos;
+        uint8_t* rp = tphi + (row >> 3) * 512 + (row & 7) * 16;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint4 w;
+          __half* hw = reinterpret_cast<__half*>(&w);
+#pragma unroll
+          for (int e2 = 0; e2 < 8; ++e2) hw[e2] = v[ch * 8 + e2];
+          *reinterpret_cast<uint4*>(rp + ch * 128) = w;
+        }
+      }
+    }
   }
 }
 
@@ -420,10 +457,12 @@ __global__ void cull_fill(DpList L, int32_t P, int32_t B, double eps, int mode, 
                           int64_t m0, const int64_t* __restrict__ act,
                           const int64_t* __restrict__ aoff, const int32_t* __restrict__ tanc,
                           const int32_t* __restrict__ tslot, int32_t* cidx, float* phi,
+                          uint8_t* tphi, float tc_guard,
                           const int32_t* __restrict__ acnt, const uint32_t* __restrict__ l0cnt,
                           const int64_t* __restrict__ lofs, const int64_t* __restrict__ ioff,
                           const int32_t* __restrict__ counts, CullItem* items, int32_t* err) {
-  cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi);
+  cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi, tphi,
+                    tc_guard);
   cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err);
 }
 
@@ -434,9 +473,9 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
     int32_t B, int32_t B0, const int32_t* __restrict__ lut0, int64_t m0, double eps, int mode,
     float guard, const uint32_t* __restrict__ l0cnt, const int64_t* __restrict__ lofs,
     const float* k12, int64_t* act, int32_t* acnt, int32_t* tanc, int32_t* tslot, int64_t* aoff,
-    int64_t* ioff, int32_t* cidx, float* phi, VoteSeg* segs, int32_t* counts, int32_t* work,
-    CullItem* items, int64_t target, int64_t max_items, int32_t* err, int64_t own_lo,
-    int64_t own_hi) {
+    int64_t* ioff, int32_t* cidx, float* phi, uint8_t* tphi, float tc_guard, VoteSeg* segs,
+    int32_t* counts, int32_t* work, CullItem* items, int64_t target, int64_t max_items,
+    int32_t* err, int64_t own_lo, int64_t own_hi) {
   cull_act_body(L, P, act, acnt, (int64_t)P * m0);
   __syncthreads();
   cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err, own_lo, own_hi);
@@ -444,7 +483,8 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
   cull_scan_body(L, rows, toffs, P, B, eps, m0, l0cnt, k12, acnt, aoff, ioff, segs, counts, work,
                  target, max_items, err);
   __syncthreads();
-  cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi);
+  cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi, tphi,
+                    tc_guard);
   cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err);
 }
 
@@ -688,6 +728,256 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
   }
 }
 
+// ---- K3-CT: the culled vote on the tensor cores ------------------------------------------------
+// The same items as K3-C, with the roles of K3-TC transposed: A (M = 128) = a stage of 128
+// gathered correspondences (their 64-byte fp16-split rows of the K1-TC table, copied by cp.async
+// into the UMMA interleaved layout), B (N = 32, FIN: 64) = the item's blocks (the planner's
+// K2-TC-format rows; FIN: two rows per block, tau -/+ g'), D = 128 x N scores in TMEM.  One
+// CTA per SM, persistent over items (static stride); roles: warp 0 gathers (all lanes, four
+// 16-byte cp.async per row, completion on an mbarrier via cp.async.mbarrier.arrive.noinc), warp 1
+// allocates TMEM and issues 2 tcgen05.mma (K = 16 each) per stage into a ring of 512 / N
+// accumulators, warps 2-5 read their 32 TMEM lanes (= 32 correspondences of the stage) with one
+// tcgen05.ld.32x32b.x32 per 32 columns and count sign bits per column (block) in registers.
+// Padding correspondences gather the table's padding row (score -1: never counted).  Error bound
+// and guard: K3-TC's.
+#ifndef RV_CT_EG
+#define RV_CT_EG 2  // K3-CT epilogue: accumulators read per round (bound mode)
+#endif
+#ifndef RV_CT_ABL
+#define RV_CT_ABL 0  // tuning only: 1 no gather copies, 2 no MMAs (wrong counts)
+#endif
+#ifndef RV_CT_FENCE
+#define RV_CT_FENCE 1
+#endif
+#ifndef RV_CT_LOOK
+#define RV_CT_LOOK 12  // stages of entry indices the K3-CT producer loads ahead
+#endif
+#ifndef RV_CT_STAGES
+#define RV_CT_STAGES 16
+#endif
+constexpr int kCtStages = RV_CT_STAGES;  // 8 KB gathered stages in flight
+#ifndef RV_CT_PROD
+#define RV_CT_PROD 4  // gathering warps (stage gs goes to warp gs % RV_CT_PROD)
+#endif
+constexpr int kCtProd = RV_CT_PROD;
+constexpr int kCtThreads = (kCtProd + 5) * 32;
+
+#ifndef RV_CT_TILES
+#define RV_CT_TILES 1  // 128-entry tiles per K3-CT stage (amortises the per-stage barrier work)
+#endif
+constexpr int kCtTiles = RV_CT_TILES;
+
+template <bool FIN>
+struct CtSmem {
+  static constexpr int N = FIN ? 64 : 32;
+  static constexpr int NACC = 512 / N;
+  uint8_t a[kCtStages][kCtTiles][128 * 64];
+  uint8_t b[2][64 * 64];
+  uint64_t full[kCtStages], empty[kCtStages], bfull[2], bempty[2], tfull[NACC], tempty[NACC];
+  uint32_t tot[2][64];
+  uint32_t tmem_base;
+};
+
+template <bool FIN>
+__global__ void __launch_bounds__(kCtThreads, 1)
+    rv_vote_cull_tc_kernel(const VoteSeg* __restrict__ segs, const CullItem* __restrict__ items,
+                           const int32_t* __restrict__ counts_dev, const uint8_t* __restrict__ tab,
+                           int64_t pad_row, const uint8_t* __restrict__ tphi,
+                           const int32_t* __restrict__ cidx, const uint32_t* __restrict__ lidx,
+                           unsigned long long* pairs) {
+  using namespace tcx;
+  using SM = CtSmem<FIN>;
+  constexpr int N = SM::N, NACC = SM::NACC, T = kCtTiles, SE = 128 * T;  // entries per stage
+  static_assert(NACC % T == 0, "a stage's accumulators are consecutive in the ring");
+  extern __shared__ __align__(1024) uint8_t ct_raw[];
+  SM& sm = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(ct_raw) + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t n_items = counts_dev[0];
+  if (warp == kCtProd) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(&sm.tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kCtStages; ++i) {
+      bar_init(&sm.full[i], 32);  // one cp.async arrive per lane of the stage's gathering warp
+      bar_init(&sm.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&sm.bfull[i], 1);
+      bar_init(&sm.bempty[i], 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      bar_init(&sm.tfull[i], 1);
+      bar_init(&sm.tempty[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp < kCtProd) {
+    // ---------------- gather (kCtProd warps; stage gs goes to warp gs % kCtProd) ----------------
+    const int pw = warp;
+    uint32_t gs = 0, gi = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
+      const CullItem it = items[idx];
+      const VoteSeg& sg = segs[it.seg];
+      const int64_t toff = sg.koff;
+      const uint32_t bb = gi & 1;
+      if (pw == 0 && lane == 0) {
+        if (gi >= 2) bar_wait(&sm.bempty[bb], ((gi >> 1) - 1) & 1);
+        const uint32_t bytes = (uint32_t)N * 64;
+        const int64_t row0 = FIN ? 2 * (int64_t)it.pos0 : it.pos0;  // multiple of 8
+        bar_expect_tx(&sm.bfull[bb], bytes);
+        bulk_g2s(sm.b[bb], tphi + (row0 >> 3) * 512, bytes, &sm.bfull[bb]);
+      }
+      const uint32_t* li = lidx + it.e0;
+      const int ns = (it.ne + SE - 1) / SE;
+      // a stage's SE indices (4 T per lane: entry r*32 + lane) are loaded kCtLook of this warp's
+      // stages ahead into a register ring whose slots are reused in place
+      constexpr int kCtLook = RV_CT_LOOK;
+      uint32_t ring[kCtLook][4 * T];
+      auto load_idx = [&](int k, uint32_t (&ix)[4 * T]) {
+#pragma unroll
+        for (int r = 0; r < 4 * T; ++r) {
+          const int ge = k * SE + r * 32 + lane;
+          ix[r] = ge < it.ne ? __ldcs(li + ge) : 0xffffffffu;  // streamed once: evict first
+        }
+      };
+      const int k0 = (int)((pw - (int)(gs % kCtProd) + kCtProd) % kCtProd);
+#pragma unroll
+      for (int d = 0; d < kCtLook; ++d) load_idx(k0 + d * kCtProd, ring[d]);
+      for (int kb = k0; kb < ns; kb += kCtLook * kCtProd) {
+#pragma unroll
+        for (int d = 0; d < kCtLook; ++d) {
+          const int k = kb + d * kCtProd;
+          if (k >= ns) break;
+          const uint32_t gk = gs + (uint32_t)k, st = gk % kCtStages;
+          uint32_t cur[4 * T];
+#pragma unroll
+          for (int r = 0; r < 4 * T; ++r) cur[r] = ring[d][r];
+          load_idx(k + kCtLook * kCtProd, ring[d]);
+          if (gk >= (uint32_t)kCtStages) bar_wait(&sm.empty[st], ((gk / kCtStages) - 1) & 1);
+          // four lanes per row, one 16-byte chunk each: a copy instruction covers 8 whole rows
+#pragma unroll
+          for (int j = 0; j < 16 * T; ++j) {
+            const int e = 8 * j + (lane >> 2), c = lane & 3;  // stage row, chunk
+            const uint32_t ix = __shfl_sync(0xffffffffu, cur[j >> 2], e & 31);
+            const int64_t g = ix != 0xffffffffu ? toff + (int64_t)ix : pad_row;
+            uint8_t* dst = sm.a[st][e >> 7] + ((e & 127) >> 3) * 512 + (e & 7) * 16 + c * 128;
+            if (!(RV_CT_ABL & 1))
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)),
+                           "l"(tab + g * 64 + c * 16)
+                           : "memory");
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                           su32(&sm.full[st]))
+                       : "memory");
+        }
+      }
+      gs += (uint32_t)ns;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == kCtProd) {
+    // ---------------- MMA issuer: T tiles per stage into T consecutive accumulators ----------
+    if (lane == 0) {
+      uint32_t gs = 0, gi = 0, ga = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
+        const int ns = (items[idx].ne + SE - 1) / SE;
+        const uint32_t bb = gi & 1;
+        bar_wait(&sm.bfull[bb], (gi >> 1) & 1);
+        const uint32_t b0 = su32(sm.b[bb]);
+        for (int k = 0; k < ns; ++k, ++gs, ga += T) {
+          const uint32_t st = gs % kCtStages, acc0 = ga % NACC;
+          bar_wait(&sm.full[st], (gs / kCtStages) & 1);
+#if RV_CT_FENCE
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+          if (ga >= (uint32_t)NACC) bar_wait(&sm.tempty[acc0], ((ga / NACC) - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            const uint32_t a0 = su32(sm.a[st][t]);
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+              if (!(RV_CT_ABL & 2))
+                mma_f16_n<N>(tmem + (acc0 + t) * N, smem_desc(a0 + 256 * kk, 128, 512),
+                             smem_desc(b0 + 256 * kk, 128, 512), (uint32_t)kk);
+          }
+          mma_commit(&sm.empty[st]);
+          mma_commit(&sm.tfull[acc0]);  // one barrier per stage (the group's first accumulator)
+        }
+        mma_commit(&sm.bempty[bb]);
+      }
+    }
+  } else {
+    // ---------------- epilogue (4 warps: TMEM lane quarter warp % 4) ----------------
+    const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    const int ew = warp - kCtProd - 1;  // 0..3
+    uint32_t ga = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      const CullItem it = items[idx];
+      const int ns = (it.ne + SE - 1) / SE;
+      uint32_t neg[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) neg[j] = 0u;
+      for (int k = 0; k < ns; ++k, ga += T) {
+        const uint32_t acc0 = ga % NACC;
+        bar_wait(&sm.tfull[acc0], (ga / NACC) & 1);
+        tc_fence_after();
+        uint32_t r[T][N];
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          RV_TCX_LD32(r[t], lane_addr + (acc0 + t) * N);
+          if (N == 64) RV_TCX_LD32((r[t] + 32), lane_addr + (acc0 + t) * N + 32);
+        }
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(&sm.tempty[acc0]);
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+#pragma unroll
+          for (int j = 0; j < N; ++j)
+            asm volatile("add.u32 %0, %0, %1;" : "+r"(neg[j]) : "r"(r[t][j] >> 31));
+      }
+      // column totals: slots - negatives, summed over the 32 lanes and the 4 epilogue warps
+      // (padding rows score -1: negatives, so the slots need no correction)
+      if (ew == 0 && lane < N / 2) sm.tot[0][lane] = 0u, sm.tot[0][lane + N / 2] = 0u;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const uint32_t v = __reduce_add_sync(0xffffffffu, (uint32_t)(ns * T) - neg[j]);
+        if (lane == 0) atomicAdd(&sm.tot[0][j], v);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (ew == 0 && lane < it.ncell) {
+        const VoteSeg& sg = segs[it.seg];
+        const int32_t e = cidx[it.pos0 + lane];
+        if (FIN) {
+          if (sm.tot[0][2 * lane]) atomicAdd(&sg.cnt_a[e], sm.tot[0][2 * lane]);
+          if (sm.tot[0][2 * lane + 1]) atomicAdd(&sg.cnt_b[e], sm.tot[0][2 * lane + 1]);
+        } else if (sm.tot[0][lane]) {
+          atomicAdd(&sg.cnt_a[e], sm.tot[0][lane]);
+        }
+      }
+      if (ew == 0 && lane == 0 && pairs)
+        atomicAdd(pairs, (unsigned long long)it.ne * (unsigned long long)it.ncell);
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // tot is reused by the next item
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kCtProd) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 namespace {
 template <int MODE>
 size_t cull_smem_bytes() {
@@ -707,6 +997,27 @@ void launch_cull_t(const VoteSeg* segs, const CullItem* items, const int32_t* co
       segs, items, counts_dev, work, pairs, phi, cidx, lidx, guard);
 }
 }  // namespace
+
+void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
+                         const int32_t* counts_dev, const uint8_t* tab, int64_t pad_row,
+                         const uint8_t* tphi, const int32_t* cidx, const uint32_t* lidx,
+                         unsigned long long* pairs, int num_sms, cudaStream_t s) {
+  static bool attr = false;
+  const size_t b0 = sizeof(CtSmem<false>) + 1024, b1 = sizeof(CtSmem<true>) + 1024;
+  if (!attr) {
+    cudaFuncSetAttribute(rv_vote_cull_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)b0);
+    cudaFuncSetAttribute(rv_vote_cull_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)b1);
+    attr = true;
+  }
+  if (mode == RV_MODE_FINAL)
+    rv_vote_cull_tc_kernel<true><<<num_sms, kCtThreads, b1, s>>>(segs, items, counts_dev, tab, pad_row,
+                                                                tphi, cidx, lidx, pairs);
+  else
+    rv_vote_cull_tc_kernel<false><<<num_sms, kCtThreads, b0, s>>>(segs, items, counts_dev, tab, pad_row,
+                                                                 tphi, cidx, lidx, pairs);
+}
 
 void launch_vote_cull(int mode, const VoteSeg* segs, const CullItem* items,
                       const int32_t* counts_dev, int32_t* work, unsigned long long* pairs,
@@ -746,12 +1057,15 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
                       CullItem* items, int64_t entries_bound, int64_t max_items, int32_t* err,
                       cudaStream_t s, int64_t own_lo, int64_t own_hi) {
   const int64_t NB = (int64_t)P * m0;
-  const int64_t target = 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
+  // items: ~8 per resident K3-C warp; K3-CT (one CTA per SM, tphi set) ~4 per CTA, since its
+  // per-item cost (the block rows, the column reduction) is larger
+  const int64_t target = cs.tphi ? 4LL * num_sms : 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
   if (entries_bound <= 8192 && NB <= (1 << 14)) {
     cull_plan_small<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, B0, lut0, m0, eps, mode, guard, l0cnt,
                                        lofs, k12, cs.act, cs.acnt, cs.tanc, cs.tslot, cs.aoff,
-                                       cs.ioff, cs.cidx, cs.phi, segs, cs.counts, cs.work, items,
-                                       target, max_items, err, own_lo, own_hi);
+                                       cs.ioff, cs.cidx, cs.phi, cs.tphi, cs.tc_guard, segs,
+                                       cs.counts, cs.work, items, target, max_items, err, own_lo,
+                                       own_hi);
     return 1;
   }
   const bool small = NB <= (1 << 16);
@@ -762,8 +1076,8 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
   cull_scan<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, eps, m0, l0cnt, k12, cs.acnt, cs.aoff, cs.ioff,
                                segs, cs.counts, cs.work, target, max_items, err);
   cull_fill<<<148 * 8, 256, 0, s>>>(L, P, B, eps, mode, guard, m0, cs.act, cs.aoff, cs.tanc, cs.tslot,
-                                    cs.cidx, cs.phi, cs.acnt, l0cnt, lofs, cs.ioff, cs.counts, items,
-                                    err);
+                                    cs.cidx, cs.phi, cs.tphi, cs.tc_guard, cs.acnt, l0cnt, lofs,
+                                    cs.ioff, cs.counts, items, err);
   return 4;
 }
 

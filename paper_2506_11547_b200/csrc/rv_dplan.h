@@ -126,6 +126,8 @@ struct CullScratch {
   float* phi;
   int32_t* counts;
   int32_t* work;
+  uint8_t* tphi;    // K3-CT: the blocks' 64-byte fp16-split rows (nullptr: FP32 K3-C only)
+  float tc_guard;   // the guard of those rows' thresholds (guard + the TC error margin)
 };
 // returns the number of kernels it launched (one CTA does everything for small levels)
 // own_lo .. own_hi: the level-0 rows (ancestors) this rank votes (blocks of other ancestors

@@ -119,10 +119,11 @@ void launch_vote(int mode, int groups, const float* k9, int64_t stride, const Vo
 // K1-TC: fp16-split correspondence table for the tensor-core vote (64 B per row,
 // interleaved K-major layout, each problem padded to a multiple of kTcN rows).
 // k12 != nullptr: also the 48-byte fp32 K rows of the culled vote ([toffs rows][12], the same
-// fp64 -> fp32 rounding as K1).
+// fp64 -> fp32 rounding as K1); tab_rm != nullptr: the table's rows again, row-major (64 B each,
+// contiguous: K3-CT's gather source).
 void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const int64_t* toffs,
                      int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s,
-                     float* k12 = nullptr);
+                     float* k12 = nullptr, uint8_t* tab_rm = nullptr);
 
 // K3-TC: BOUND-mode vote on tcgen05 (items: ncell <= kTcM, i0/ni multiples of kTcN, koff
 // in table rows); final_mode: RV_MODE_FINAL counts at tau -/+ guard (items: ncell <= kTcM/2).
@@ -146,6 +147,13 @@ void launch_vote_cull(int mode, const VoteSeg* segs, const CullItem* items,
                       const int32_t* counts_dev, int32_t* work, unsigned long long* pairs,
                       const float* phi, const int32_t* cidx, const uint32_t* lidx, float guard,
                       int num_sms, cudaStream_t s);
+// K3-CT (rv_cull.cu): the culled vote on the tensor cores (same items and planner as K3-C;
+// needs the planner's fp16-split block rows tphi).  tab: the K1-TC table, pad_row: a padding
+// row of it (score -1).
+void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
+                         const int32_t* counts_dev, const uint8_t* tab, int64_t pad_row,
+                         const uint8_t* tphi, const int32_t* cidx, const uint32_t* lidx,
+                         unsigned long long* pairs, int num_sms, cudaStream_t s);
 // Level-0 index lists: row offsets lofs[P*m0 + 1] (exclusive prefix of the level-0 counts, each
 // padded to a multiple of 4; lofs[P*m0] = the total), then the compaction of the K3-TC bitmasks
 // (bits0: problem p's rows from m0 * toffs[p] / 32, (toffs[p+1] - toffs[p]) / 32 words each).

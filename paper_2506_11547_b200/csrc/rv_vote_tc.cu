@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
                                                           const int64_t* __restrict__ toffs,
                                                           int32_t P, int64_t total_pad,
                                                           uint8_t* __restrict__ tab,
-                                                          float* __restrict__ k12) {
+                                                          float* __restrict__ k12,
+                                                          uint8_t* __restrict__ tab_rm) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total_pad;
        g += (int64_t)gridDim.x * blockDim.x) {
     int32_t lo = 0, hi = P;
@@ -200,7 +201,8 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
         kr[0] = kr[1] = kr[2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
     }
-    // row g of the whole table: group g>>3, 4 chunks of 16 B
+    // row g of the whole table: group g>>3, 4 chunks of 16 B (+ the row-major copy K3-CT
+    // gathers: a row's 64 B contiguous, two whole 32-byte sectors)
     uint8_t* rowp = tab + (g >> 3) * 512 + (g & 7) * 16;
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) {
@@ -209,16 +211,19 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
 #pragma unroll
       for (int e = 0; e < 8; ++e) hw[e] = v[ch * 8 + e];
       *reinterpret_cast<uint4*>(rowp + ch * 128) = w;
+      if (tab_rm) *reinterpret_cast<uint4*>(tab_rm + g * 64 + ch * 16) = w;
     }
   }
 }
 
 void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const int64_t* toffs,
-                     int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s, float* k12) {
+                     int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s, float* k12,
+                     uint8_t* tab_rm) {
   int64_t blocks = (total_pad + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  rv_setup_tc_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, y, rows, toffs, P, total_pad, tab, k12);
+  rv_setup_tc_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, y, rows, toffs, P, total_pad, tab, k12,
+                                                       tab_rm);
 }
 
 // ------------------------------------------------------------------------------------------

@@ -35,14 +35,36 @@ def torch_cuda():
     return torch
 
 
-@pytest.fixture(scope="module")
-def rvc(torch_cuda):
-    from paper_2506_11547_b200 import RotVote, build
+def _ctx(path, **kw):
+    """A culling context on the FP32 K3-C path ("fp32", default) or the tensor-core K3-CT path
+    ("tc": RV_CULL_TC=1 at creation)."""
+    import os
+    from paper_2506_11547_b200 import RotVote
+    old = os.environ.get("RV_CULL_TC")
+    os.environ["RV_CULL_TC"] = "1" if path == "tc" else "0"
+    try:
+        return RotVote(tensor_vote=True, cull=True, **kw)
+    finally:
+        if old is None:
+            del os.environ["RV_CULL_TC"]
+        else:
+            os.environ["RV_CULL_TC"] = old
+
+
+@pytest.fixture(scope="module", params=["tc", "fp32"])
+def rvc(request, torch_cuda):
+    from paper_2506_11547_b200 import build
     build.build()
     oracle.build()
-    ctx = RotVote(max_n=1 << 20, max_problems=512, tensor_vote=True, cull=True)
+    ctx = _ctx(request.param, max_n=1 << 20, max_problems=512)
+    ctx.path = request.param
     yield ctx
     ctx.close()
+
+
+def guard_of(ctx):
+    """the guard of a culled count's threshold: K3-CT = K3-TC's, K3-C = K3's"""
+    return GUARD_TC if ctx.path == "tc" else GUARD
 
 
 def dev(torch, a):
@@ -96,17 +118,20 @@ def test_culled_counts_in_band(rvc, torch_cuda, n, eps):
             c = oracle.candidates(B)
             lins = rng.choice(c, 300, replace=True).astype(np.uint32)
             lins = np.concatenate([lins, lins[:7]])  # repeats
+            g = guard_of(rvc)
             got = rvc.count_cells_culled(x, y, 15, B, lins, eps, RV_MODE_BOUND)
-            thr = np.array([oracle.cell_bound_threshold(B, int(l), eps) - GUARD for l in lins])
+            thr = np.array([oracle.cell_bound_threshold(B, int(l), eps) - g for l in lins])
             assert np.all(in_band(got, pr.x, pr.y, B, lins, thr)), B
-            ref = fp32.count_cells(x, y, B, lins, eps, RV_MODE_BOUND)
-            assert np.all(got <= ref), B          # a subset evaluated with K3's arithmetic
+            if rvc.path == "fp32":  # a subset evaluated with K3's exact arithmetic
+                ref = fp32.count_cells(x, y, B, lins, eps, RV_MODE_BOUND)
+                assert np.all(got <= ref), B
             ga, gb = rvc.count_cells_culled(x, y, 15, B, lins, eps, RV_MODE_FINAL)
             tau = math.cos(eps)
-            assert np.all(in_band(ga, pr.x, pr.y, B, lins, tau - GUARD)), B
-            assert np.all(in_band(gb, pr.x, pr.y, B, lins, tau + GUARD)), B
-            ra, rb = fp32.count_cells(x, y, B, lins, eps, RV_MODE_FINAL)
-            assert np.all(ga <= ra) and np.all(gb <= rb), B
+            assert np.all(in_band(ga, pr.x, pr.y, B, lins, tau - g)), B
+            assert np.all(in_band(gb, pr.x, pr.y, B, lins, tau + g)), B
+            if rvc.path == "fp32":
+                ra, rb = fp32.count_cells(x, y, B, lins, eps, RV_MODE_FINAL)
+                assert np.all(ga <= ra) and np.all(gb <= rb), B
             ex, _ = oracle.count_cells(pr.x, pr.y, B, lins, tau, 0.0)
             assert np.all(gb <= ex) and np.all(ex <= ga), B  # cnt_b <= exact <= cnt_a
     finally:
@@ -131,7 +156,8 @@ def test_culled_counts_near_the_peak(rvc, torch_cuda):
                         lins.append(oracle.lin_of(B, u, v, w))
         lins = np.array(sorted(lins), np.uint32)
         got = rvc.count_cells_culled(x, y, 15, B, lins, pr.eps, RV_MODE_BOUND)
-        thr = np.array([oracle.cell_bound_threshold(B, int(l), pr.eps) - GUARD for l in lins])
+        thr = np.array([oracle.cell_bound_threshold(B, int(l), pr.eps) - guard_of(rvc)
+                        for l in lins])
         assert np.all(in_band(got, pr.x, pr.y, B, lins, thr)), B
         assert got.max() >= 2_000 * 0.9, (B, got.max())
 
@@ -204,7 +230,7 @@ def test_culled_loopback_shards(torch_cuda):
         x, y = dev(torch, pr.x), dev(torch, pr.y)
         ref = None
         for W in (1, 2, 3, 8):
-            ctx = RotVote(max_n=1 << 17, emulate_world=W, cull=True)
+            ctx = _ctx("tc", max_n=1 << 17, emulate_world=W)
             try:
                 r = ctx.solve(x, y, pr.eps)
             finally:
