@@ -221,12 +221,40 @@ def _k3c_entry(args, cull_pairs, cull_ms, ms_per_step):
             "vote_share_of_step": (cull_ms / steps) / ms_per_step}
 
 
-def _roofline(args, vote_pairs, vote_ms, ms_per_step, cull_pairs=0, cull_ms=0.0):
+def _k3ct_entry(args, cull_pairs, cull_ms, ms_per_step):
+    """K3-CT (the culled vote on the tensor cores): like K3-TC, every evaluated pair's score
+    leaves TMEM (tcgen05.ld) and costs one sign-count lane-op, so the bound is the same epilogue
+    bound (148 SMs x 64 pairs/clk); the tensor-core FLOP rate rides along."""
+    steps = args.steps
+    pairs_s = cull_pairs / (cull_ms / 1e3) if cull_ms > 0 else None
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "vote_cull_tc_kernel_traffic.json"))
+                            ).get("bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    tpeak, src = measured_peak("bf16_tflops", 1590.0)
+    return {"bound": "alu", "achieved": pairs_s / 1e12 if pairs_s else None,
+            "peak": TC_EPI_PEAK_PAIRS / 1e12, "unit": "TOP/s",
+            "frac": pairs_s / TC_EPI_PEAK_PAIRS if pairs_s else None, "traffic": traffic,
+            "kernel": "rv_vote_cull_tc_kernel (K3-CT: blocks of a 2x2x1 level-0 ancestor group vs "
+                      "the group's union list, cp.async-gathered fp16-split rows, tcgen05 kind::f16 "
+                      "M=128 N=256, TMEM accumulators), one TMEM read + sign count per pair",
+            "ops_per_pair": 1,
+            "peak_source": "148 SMs x 4 SMSPs x 16 lanes x 1965 MHz (the K3-TC epilogue bound)",
+            "tensor": {"peak_tflops": tpeak, "peak_source": src,
+                       "algorithmic_tflops": pairs_s * FLOP_PER_PAIR / 1e12 if pairs_s else None},
+            "pairs_per_step": cull_pairs / steps,
+            "vote_ms_per_step": cull_ms / steps,
+            "vote_share_of_step": (cull_ms / steps) / ms_per_step}
+
+
+def _roofline(args, vote_pairs, vote_ms, ms_per_step, cull_pairs=0, cull_ms=0.0, cull_tc=False):
     """The dominant kernel's roofline entry from the library's own CUDA-event vote timing
     (rv_result.vote_ms / cull_ms: events recorded on the library's stream around every vote
     launch).  With culling the dominant kernel is K3-C; the K3-TC level-0 entry rides along."""
     if cull_ms > 0:
-        main = _k3c_entry(args, cull_pairs, cull_ms, ms_per_step)
+        main = (_k3ct_entry if cull_tc else _k3c_entry)(args, cull_pairs, cull_ms, ms_per_step)
         other = _roofline(args, vote_pairs, vote_ms, ms_per_step) if vote_ms > 0 else None
         if other is not None and other["vote_ms_per_step"] > main["vote_ms_per_step"]:
             other["also"] = main
@@ -319,7 +347,7 @@ def run_ours(args):
         res = rv.solve(x, y, pr.eps, levels=args.levels, mask=mask)
     barrier()
     step_ms, vote_ms, vote_pairs, launches, vote_launches = [], 0.0, 0, 0, 0
-    cull_ms, cull_pairs = 0.0, 0
+    cull_ms, cull_pairs, cull_tc = 0.0, 0, 0
     pair_votes = res.pair_votes
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -336,6 +364,7 @@ def run_ours(args):
             vote_launches += r.vote_launches
             cull_ms += r.cull_ms
             cull_pairs += r.cull_pairs
+            cull_tc += r.cull_tc_launches
             assert (r.cell, r.votes) == (res.cell, res.votes)
     barrier()
     total = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
@@ -364,7 +393,7 @@ def run_ours(args):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = r2.pair_votes * args.e2e_steps / (float(e2e_t.item()) / 1e3)
 
-    roofline = _roofline(args, vote_pairs, vote_ms, ms_per_step, cull_pairs, cull_ms)
+    roofline = _roofline(args, vote_pairs, vote_ms, ms_per_step, cull_pairs, cull_ms, cull_tc > 0)
     evaluated = (vote_pairs + cull_pairs) / args.steps
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

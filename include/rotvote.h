@@ -113,10 +113,11 @@ typedef struct {
   uint64_t vote_pairs;    /* (correspondence, block) pairs voted by K3 / K3-TC on this rank, padding
                              excluded */
   int32_t  vote_launches; /* K3 / K3-TC launches on this rank */
-  int32_t  cull_launches; /* K3-C (culled vote) launches on this rank */
-  uint64_t cull_pairs;    /* (correspondence, block) pairs K3-C evaluated on this rank */
-  float    cull_ms;       /* summed device time of the K3-C launches (CUDA events on cfg.stream) */
-  int32_t  pad_;
+  int32_t  cull_launches; /* culled-vote launches (K3-CT or K3-C) on this rank */
+  uint64_t cull_pairs;    /* (correspondence, block) pairs the culled vote evaluated on this rank */
+  float    cull_ms;       /* summed device time of the culled-vote launches (CUDA events on
+                             cfg.stream) */
+  int32_t  cull_tc_launches; /* of cull_launches: on the tensor cores (K3-CT) */
 } rv_result;
 
 /* ---- lifetime ------------------------------------------------------------------ */

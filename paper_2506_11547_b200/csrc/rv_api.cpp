@@ -264,11 +264,17 @@ struct rv_ctx {
   DevBuf<float> k12;
   DevBuf<int32_t> lut0;
   int32_t lut0_B = 0;
+  // K3-CT ancestor groups (2 x 2 x 1 neighbouring level-0 blocks share one union list):
+  // lutg = level-0 lin -> group, gmem[goff[g] .. goff[g+1]) = its level-0 rows
+  DevBuf<int32_t> lutg, goff, gmem;
+  int64_t cull_G = 0, cull_G_grouped = 0;
+  bool cull_grouped = false;     // this solve's lists are group unions (K3-CT, one rank)
   DevBuf<int64_t> c_act, c_aoff, c_ioff;
   DevBuf<int32_t> c_acnt, c_tanc, c_tslot, c_cidx, c_icnt, c_work;
   DevBuf<float> c_phi;
   DevBuf<uint8_t> c_tphi;        // K3-CT block rows (fp16 split)
-  bool cull_tc = false;          // culled levels on K3-C (FP32); RV_CULL_TC=1: tensor cores (K3-CT)
+  bool cull_tc = true;           // culled levels on the tensor cores (K3-CT, one rank: group
+                                 // lists); RV_CULL_TC=0 (or several ranks): FP32 K3-C
   DevBuf<rv::CullItem> c_items;
   DevBuf<unsigned long long> c_pairs;
   std::vector<cudaEvent_t> cevs;
@@ -307,10 +313,10 @@ struct rv_ctx {
   // per-call counters reported in rv_result
   float vote_ms = 0, cull_ms = 0;
   uint64_t vote_pairs = 0, cull_pairs = 0;
-  int32_t launches = 0, vote_launches = 0, cull_launches = 0;
+  int32_t launches = 0, vote_launches = 0, cull_launches = 0, cull_tc_launches = 0;
   void reset_counters() {
     vote_ms = 0; vote_pairs = 0; launches = 0; vote_launches = 0; vote_pending = false;
-    cull_ms = 0; cull_pairs = 0; cull_launches = 0; cevn = 0;
+    cull_ms = 0; cull_pairs = 0; cull_launches = 0; cull_tc_launches = 0; cevn = 0;
   }
   template <class R>
   void fill_counters(R& r) const {
@@ -321,6 +327,7 @@ struct rv_ctx {
     r.cull_ms = cull_ms;
     r.cull_pairs = cull_pairs;
     r.cull_launches = cull_launches;
+    r.cull_tc_launches = cull_tc_launches;
   }
   Trace* trace = nullptr;  // RV_TRACE=1: host phase timings
   void mark(const char* what) {
@@ -1336,8 +1343,38 @@ int cull_prepare(rv_ctx* ctx, int32_t B0, int64_t m0, int32_t PL) {
     for (int64_t a = 0; a < m0; ++a) lut[ctx->grid_host[a]] = (int32_t)a;
     RV_CUDA(ctx->lut0.ensure(lut.size()), "allocating");
     RV_CUDA(cudaMemcpy(ctx->lut0.p, lut.data(), lut.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
+    // groups: level-0 blocks (i, j, k) with equal (i / 2, j / 2, k), numbered in row order
+    std::vector<int32_t> lg((size_t)B0 * B0 * B0, -1), key((size_t)B0 * B0 * B0, -1);
+    std::vector<std::vector<int32_t>> mem;
+    for (int64_t a = 0; a < m0; ++a) {
+      const int64_t lin = ctx->grid_host[a];
+      const int64_t i = lin / ((int64_t)B0 * B0), j = (lin / B0) % B0, k = lin % B0;
+      const int64_t kk = ((i / 2) * B0 + j / 2) * B0 + k;
+      if (key[kk] < 0) {
+        key[kk] = (int32_t)mem.size();
+        mem.emplace_back();
+      }
+      lg[lin] = key[kk];
+      mem[key[kk]].push_back((int32_t)a);
+    }
+    std::vector<int32_t> go(mem.size() + 1, 0), gm;
+    for (size_t g = 0; g < mem.size(); ++g) {
+      go[g + 1] = go[g] + (int32_t)mem[g].size();
+      gm.insert(gm.end(), mem[g].begin(), mem[g].end());
+    }
+    RV_CUDA(ctx->lutg.ensure(lg.size()), "allocating");
+    RV_CUDA(ctx->goff.ensure(go.size()), "allocating");
+    RV_CUDA(ctx->gmem.ensure(gm.size()), "allocating");
+    RV_CUDA(cudaMemcpy(ctx->lutg.p, lg.data(), lg.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
+    RV_CUDA(cudaMemcpy(ctx->goff.p, go.data(), go.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
+    RV_CUDA(cudaMemcpy(ctx->gmem.p, gm.data(), gm.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
+    ctx->cull_G_grouped = (int64_t)mem.size();
     ctx->lut0_B = B0;
   }
+  // group unions only for K3-CT on one rank (a rank's level-0 slice need not hold whole groups)
+  // (K3-CT needs them: with per-ancestor lists an item fills a quarter of its 128 rows)
+  ctx->cull_grouped = ctx->cull_tc && ctx->effective_world() == 1 && !ctx->comm;
+  ctx->cull_G = ctx->cull_grouped ? ctx->cull_G_grouped : m0;
   RV_CUDA(ctx->c_pairs.ensure(1), "allocating");
   RV_CUDA(cudaMemsetAsync(ctx->c_pairs.p, 0, 8, ctx->stream), "memset");
   RV_CUDA(ctx->dp_err.ensure(1), "allocating");
@@ -1357,9 +1394,11 @@ int cull_prepare(rv_ctx* ctx, int32_t B0, int64_t m0, int32_t PL) {
 int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
                      bool force = false) {
   cudaStream_t s = ctx->stream;
-  const int64_t NB = (int64_t)PL * m0;
+  rv::CullGroups gr;
+  if (ctx->cull_grouped) gr = rv::CullGroups{ctx->goff.p, ctx->gmem.p, ctx->cull_G};
+  const int64_t NB = (int64_t)PL * ctx->cull_G;
   RV_CUDA(ctx->c_lofs.ensure(NB + 1), "allocating");
-  rv::launch_cull_rows(l0cnt, PL, m0, ctx->c_lofs.p, s);
+  rv::launch_cull_rows(l0cnt, PL, m0, ctx->c_lofs.p, s, gr);
   ctx->launches += 1;
   ctx->down.reset();
   int64_t* ht = ctx->down.take<int64_t>(1);
@@ -1378,9 +1417,10 @@ int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
     row_hi = std::min<int64_t>(m0, row_lo + c0);
   }
   rv::launch_cull_compact(ctx->cbits.p, ctx->toffs.p, PL, m0, ctx->cull_wpc_max, ctx->c_lofs.p,
-                          ctx->c_fill.p, ctx->c_lidx.p, s, row_lo, row_hi);
+                          ctx->c_fill.p, ctx->c_lidx.p, s, row_lo, row_hi, gr);
   ctx->launches += 1;
-  ctx->cull_l0cnt = l0cnt;
+  // list lengths: the level-0 counts, or the union sizes the compaction counted
+  ctx->cull_l0cnt = ctx->cull_grouped ? reinterpret_cast<const uint32_t*>(ctx->c_fill.p) : l0cnt;
   ctx->cull_ready = true;
   return RV_OK;
 }
@@ -1408,7 +1448,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   cudaStream_t s = ctx->stream;
   if (ctx->cull_ready && mode != RV_MODE_EXACT) {
     const int64_t eb = std::max<int64_t>(1, entries_bound);
-    const int64_t nb = (int64_t)PL * ctx->cull_m0;
+    const int64_t nb = (int64_t)PL * ctx->cull_G;  // buckets: (problem, list row)
     const int64_t mi = rv::cull_items_bound(eb, ctx->num_sms);
     RV_CUDA(ctx->c_act.ensure(PL + 1), "allocating");
     RV_CUDA(ctx->c_acnt.ensure(nb), "allocating");
@@ -1419,7 +1459,8 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     const int64_t npos = eb + 7 * nb + 16;  // bucket positions are padded to multiples of 8
     RV_CUDA(ctx->c_cidx.ensure(npos), "allocating");
     RV_CUDA(ctx->c_phi.ensure(npos * 12), "allocating");
-    if (ctx->cull_tc) RV_CUDA(ctx->c_tphi.ensure(npos * 2 * 64), "allocating");
+    // (+128 rows: K3-CT's A tile reads 128 rows from an item's first)
+    if (ctx->cull_grouped) RV_CUDA(ctx->c_tphi.ensure((npos * 2 + 128) * 64), "allocating");
     RV_CUDA(ctx->c_icnt.ensure(2), "allocating");
     RV_CUDA(ctx->c_work.ensure(1), "allocating");
     RV_CUDA(ctx->vsegs.ensure(PL), "allocating segments");
@@ -1427,17 +1468,18 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     const rv::CullScratch cs{ctx->c_act.p, ctx->c_acnt.p, ctx->c_aoff.p, ctx->c_ioff.p,
                              ctx->c_tanc.p, ctx->c_tslot.p, ctx->c_cidx.p, ctx->c_phi.p,
                              ctx->c_icnt.p, ctx->c_work.p,
-                             ctx->cull_tc ? ctx->c_tphi.p : nullptr,
+                             ctx->cull_grouped ? ctx->c_tphi.p : nullptr,
                              ctx->cfg.guard + kTcExtraGuard};
     ctx->launches += rv::launch_cull_items(Ld, ctx->rows.p, ctx->toffs.p, PL, B, ctx->cull_B0,
-                                           ctx->lut0.p, ctx->cull_m0, ctx->cull_l0cnt,
+                                           ctx->cull_grouped ? ctx->lutg.p : ctx->lut0.p,
+                                           ctx->cull_G, ctx->cull_l0cnt,
                                            ctx->c_lofs.p, ctx->k12.p, eps, mode, ctx->cfg.guard,
                                            ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, eb, mi,
                                            ctx->dp_err.p, s, ctx->cull_own_lo, ctx->cull_own_hi);
     cudaEvent_t e0, e1;
     RV_CUDA(ctx->cev_pair(&e0, &e1), "event");
     RV_CUDA(cudaEventRecord(e0, s), "event");
-    if (ctx->cull_tc)
+    if (ctx->cull_grouped)  // K3-CT
       rv::launch_vote_cull_tc(mode, ctx->vsegs.p, ctx->c_items.p, ctx->c_icnt.p, ctx->tctab_rm.p,
                               ctx->tc_toff.back(), ctx->c_tphi.p, ctx->c_cidx.p, ctx->c_lidx.p,
                               ctx->c_pairs.p, ctx->num_sms, s);
@@ -1448,6 +1490,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     RV_CUDA(cudaEventRecord(e1, s), "event");
     ctx->launches += 1;
     ctx->cull_launches += 1;
+    ctx->cull_tc_launches += ctx->cull_grouped ? 1 : 0;
     RV_CUDA(cudaGetLastError(), "launching the culled vote");
     return RV_OK;
   }
@@ -1539,10 +1582,10 @@ int vote_level_owned(rv_ctx* ctx, const float* x, const float* y, const std::vec
   const bool nccl_path = ctx->comm != nullptr;
   const int W = ctx->effective_world();
   const int r_lo = nccl_path ? ctx->cfg.rank : 0, r_hi = nccl_path ? r_lo + 1 : W;
-  const int64_t c0 = (ctx->cull_m0 + W - 1) / W;
+  const int64_t c0 = (ctx->cull_G + W - 1) / W;  // (ungrouped when W > 1: G = m0)
   for (int r = r_lo; r < r_hi; ++r) {
     ctx->cull_own_lo = (int64_t)r * c0;
-    ctx->cull_own_hi = std::min<int64_t>(ctx->cull_m0, (int64_t)(r + 1) * c0);
+    ctx->cull_own_hi = std::min<int64_t>(ctx->cull_G, (int64_t)(r + 1) * c0);
     int rc = vote_level(ctx, x, y, rows, koff, eps, mode, B, Ld, 1, entries, nmax);
     ctx->cull_own_lo = 0;
     ctx->cull_own_hi = INT64_MAX;
@@ -2326,7 +2369,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->dp_best.release(); ctx->a1_acc.release(); ctx->a1_tab.release(); ctx->a1_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
   ctx->dp_icnt.release(); ctx->dp_phase.release(); ctx->dp_err.release();
   ctx->dp_pcnt.release(); ctx->dp_scnt.release(); ctx->dp_poff.release(); ctx->dp_sbase.release();
-  ctx->cbits.release(); ctx->k12.release(); ctx->lut0.release(); ctx->c_act.release();
+  ctx->cbits.release(); ctx->k12.release(); ctx->lut0.release(); ctx->lutg.release(); ctx->goff.release(); ctx->gmem.release(); ctx->lut0_B = 0; ctx->c_act.release();
   ctx->c_lofs.release(); ctx->c_lidx.release(); ctx->c_fill.release();
   ctx->c_ioff.release(); ctx->c_aoff.release(); ctx->c_acnt.release(); ctx->c_tanc.release();
   ctx->c_tslot.release(); ctx->c_cidx.release(); ctx->c_phi.release(); ctx->c_icnt.release();

@@ -191,33 +191,50 @@ __global__ void cull_count(DpList L, int32_t P, int32_t B, int32_t B0,
   cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err, own_lo, own_hi);
 }
 
-// One CTA: lofs[b] = exclusive prefix of the level-0 counts rounded up to 4 (list row starts,
+// Length bound of list row b = p * G + g: the level-0 count of row p * m0 + g, or with ancestor
+// groups (goff != nullptr: group g = the level-0 rows gmem[goff[g] .. goff[g+1])) the sum of its
+// members' counts (its union list is at most that long)
+__device__ __forceinline__ int64_t row_bound(const uint32_t* __restrict__ l0cnt, int64_t b,
+                                             int64_t m0, int64_t G, const int32_t* goff,
+                                             const int32_t* gmem) {
+  if (!goff) return l0cnt[b];
+  const int64_t p = b / G, g = b % G;
+  int64_t v = 0;
+  for (int k = goff[g]; k < goff[g + 1]; ++k) v += l0cnt[p * m0 + gmem[k]];
+  return v;
+}
+
+// One CTA: lofs[b] = exclusive prefix of the row bounds rounded up to 4 (list row starts,
 // 16-byte aligned), lofs[NB] = their total
 __global__ void __launch_bounds__(1024) cull_rows(const uint32_t* __restrict__ l0cnt, int64_t NB,
-                                                  int64_t* lofs) {
+                                                  int64_t m0, int64_t G, const int32_t* goff,
+                                                  const int32_t* gmem, int64_t* lofs) {
   __shared__ int64_t sh[64];
   const int t = threadIdx.x, T = blockDim.x;
   const int64_t b0 = NB * t / T, b1 = NB * (t + 1) / T;
   int64_t v = 0;
-  for (int64_t b = b0; b < b1; ++b) v += ((int64_t)l0cnt[b] + 3) & ~(int64_t)3;
+  for (int64_t b = b0; b < b1; ++b) v += (row_bound(l0cnt, b, m0, G, goff, gmem) + 3) & ~(int64_t)3;
   int64_t tot;
   int64_t e = blk_scan_sum(v, sh, &tot);
   for (int64_t b = b0; b < b1; ++b) {
     lofs[b] = e;
-    e += ((int64_t)l0cnt[b] + 3) & ~(int64_t)3;
+    e += (row_bound(l0cnt, b, m0, G, goff, gmem) + 3) & ~(int64_t)3;
   }
   if (t == 0) lofs[NB] = tot;
 }
 
-// One warp per (level-0 row b = p * m0 + a, segment of 256 bitmask words): the set bits of
-// the segment, appended to the row's list idx[lofs[b] ..] at a position taken with one atomic
-// on fill[b] (zeroed by the caller).  A list's order is irrelevant (counts are sums), so the
-// rows' segments are compacted in parallel; each row ends with exactly l0cnt[b] entries
-// (K3-TC's count is the popcount of its words).
+// One warp per (list row b = p * G + g, segment of 256 bitmask words): the set bits of the
+// segment (with groups: of the OR of its members' words), appended to the row's list
+// idx[lofs[b] ..] at a position taken with one atomic on fill[b] (zeroed by the caller).  A
+// list's order is irrelevant (counts are sums), so the rows' segments are compacted in
+// parallel; each row ends with fill[b] entries (ungrouped: exactly l0cnt[b], K3-TC's count
+// being the popcount of its words).
 constexpr int kCompactSeg = 256;
 constexpr int kCompactStage = 1024;  // entries staged in shared memory per warp
 __global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__ bits0,
                                                     const int64_t* __restrict__ toffs, int64_t m0,
+                                                    int64_t G, const int32_t* __restrict__ goff,
+                                                    const int32_t* __restrict__ gmem,
                                                     int64_t row_lo, int64_t NR, int64_t nseg,
                                                     const int64_t* __restrict__ lofs,
                                                     int32_t* fill, uint32_t* idx) {
@@ -228,14 +245,21 @@ __global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__
   for (int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
        task < NR * nseg; task += nwarps) {
     const int64_t b = row_lo + task / nseg, sg = task % nseg;
-    const int64_t p = b / m0, a = b % m0;
+    const int64_t p = b / G, g = b % G;
     const int64_t wpc = (toffs[p + 1] - toffs[p]) / 32;
     const int64_t w0 = sg * kCompactSeg;
     if (w0 >= wpc) continue;  // warp-uniform
-    const uint4* row = reinterpret_cast<const uint4*>(bits0 + m0 * (toffs[p] / 32) + a * wpc + w0);
     const int64_t nq = (wpc - w0 < kCompactSeg ? wpc - w0 : kCompactSeg) / 4;
-    const uint4 v0 = lane < nq ? __ldg(row + lane) : make_uint4(0u, 0u, 0u, 0u);
-    const uint4 v1 = lane + 32 < nq ? __ldg(row + lane + 32) : make_uint4(0u, 0u, 0u, 0u);
+    uint4 v0 = make_uint4(0u, 0u, 0u, 0u), v1 = v0;
+    const int k0 = goff ? goff[g] : 0, k1 = goff ? goff[g + 1] : 1;
+    for (int k = k0; k < k1; ++k) {
+      const int64_t a = goff ? gmem[k] : g;
+      const uint4* row = reinterpret_cast<const uint4*>(bits0 + m0 * (toffs[p] / 32) + a * wpc + w0);
+      const uint4 u0 = lane < nq ? __ldg(row + lane) : make_uint4(0u, 0u, 0u, 0u);
+      const uint4 u1 = lane + 32 < nq ? __ldg(row + lane + 32) : make_uint4(0u, 0u, 0u, 0u);
+      v0.x |= u0.x; v0.y |= u0.y; v0.z |= u0.z; v0.w |= u0.w;
+      v1.x |= u1.x; v1.y |= u1.y; v1.z |= u1.z; v1.w |= u1.w;
+    }
     const int c = __popc(v0.x) + __popc(v0.y) + __popc(v0.z) + __popc(v0.w) + __popc(v1.x) +
                   __popc(v1.y) + __popc(v1.z) + __popc(v1.w);
     int incl = c;
@@ -283,7 +307,7 @@ __device__ __forceinline__ void cull_scan_body(DpList L, const int64_t* __restri
                                                   const int32_t* __restrict__ acnt, int64_t* aoff,
                                                   int64_t* ioff, VoteSeg* segs, int32_t* counts,
                                                   int32_t* work, int64_t target, int64_t max_items,
-                                                  int32_t* err) {
+                                                  int32_t* err, int32_t cpi) {
   __shared__ int64_t sh[64];
   __shared__ int64_t s_ce;
   const int t = threadIdx.x, T = blockDim.x;
@@ -294,21 +318,22 @@ __device__ __forceinline__ void cull_scan_body(DpList L, const int64_t* __restri
   for (int64_t bk = b0; bk < b1; ++bk) {
     const int64_t c = acnt[bk];
     ne += (c + 7) & ~(int64_t)7;  // bucket positions padded to 8 (K3-CT 8-row groups)
-    if (c) work_e += (c + 31) / 32 * (int64_t)l0cnt[bk];
+    if (c) work_e += (c + cpi - 1) / cpi * (int64_t)l0cnt[bk];
   }
   int64_t tot_e, tot_w;
   int64_t e = blk_scan_sum(ne, sh, &tot_e);
   blk_scan_sum(work_e, sh, &tot_w);
   if (t == 0) {
-    int64_t ce = (tot_w / (target > 0 ? target : 1) + 127) / 128 * 128;
-    s_ce = ce < RV_CULL_MIN_CE ? RV_CULL_MIN_CE : ce;
+    const int64_t q = cpi > 32 ? 256 : 128;  // K3-CT stages are 256 entries
+    const int64_t ce = (tot_w / (target > 0 ? target : 1) + q - 1) / q * q;
+    s_ce = ce < RV_CULL_MIN_CE ? (RV_CULL_MIN_CE + q - 1) / q * q : ce;
   }
   __syncthreads();
   const int64_t CE = s_ce;
   // pass 2: bucket and item offsets
   auto items_of = [&](int64_t bk) -> int64_t {
     const int64_t c = acnt[bk], l = l0cnt[bk];
-    return c && l ? (c + 31) / 32 * ((l + CE - 1) / CE) : 0;
+    return c && l ? (c + cpi - 1) / cpi * ((l + CE - 1) / CE) : 0;
   };
   int64_t ni = 0;
   for (int64_t bk = b0; bk < b1; ++bk) ni += items_of(bk);
@@ -356,9 +381,9 @@ __global__ void __launch_bounds__(1024) cull_scan(DpList L, const int64_t* __res
                                                   const int32_t* __restrict__ acnt, int64_t* aoff,
                                                   int64_t* ioff, VoteSeg* segs, int32_t* counts,
                                                   int32_t* work, int64_t target, int64_t max_items,
-                                                  int32_t* err) {
+                                                  int32_t* err, int32_t cpi) {
   cull_scan_body(L, rows, toffs, P, B, eps, m0, l0cnt, k12, acnt, aoff, ioff, segs, counts, work,
-                 target, max_items, err);
+                 target, max_items, err, cpi);
 }
 
 // entries into bucket order: cidx[pos] = the entry's index in its problem's list; phi: per
@@ -428,7 +453,8 @@ __device__ __forceinline__ void cull_scatter_body(DpList L, int32_t P, int32_t B
 __device__ __forceinline__ void cull_items_body(int32_t P, int64_t m0, const int32_t* __restrict__ acnt,
                            const uint32_t* __restrict__ l0cnt, const int64_t* __restrict__ lofs,
                            const int64_t* __restrict__ aoff, const int64_t* __restrict__ ioff,
-                           const int32_t* __restrict__ counts, CullItem* items, int32_t* err) {
+                           const int32_t* __restrict__ counts, CullItem* items, int32_t* err,
+                           int32_t cpi) {
   const int64_t n_items = counts[0], CE = counts[1];
   const int64_t NB = (int64_t)P * m0;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_items;
@@ -439,12 +465,12 @@ __device__ __forceinline__ void cull_items_body(int32_t P, int64_t m0, const int
       if (ioff[mid] <= g) lo = mid; else hi = mid;
     }
     const int64_t bk = lo, local = g - ioff[bk];
-    const int64_t c = acnt[bk], ng = (c + 31) / 32, l = l0cnt[bk];
+    const int64_t c = acnt[bk], ng = (c + cpi - 1) / cpi, l = l0cnt[bk];
     const int64_t grp = local % ng, ch = local / ng;  // chunk-major within the bucket
     CullItem it;
     it.seg = (int32_t)(bk / m0);
-    it.pos0 = (int32_t)(aoff[bk] + 32 * grp);
-    it.ncell = (int32_t)i64min(32, c - 32 * grp);
+    it.pos0 = (int32_t)(aoff[bk] + cpi * grp);
+    it.ncell = (int32_t)i64min(cpi, c - cpi * grp);
     it.e0 = lofs[bk] + ch * CE;
     it.ne = (int32_t)i64min(CE, l - ch * CE);
     if (c < 1 || it.ncell < 1 || it.ne < 1) atomicOr(err, 4);
@@ -460,10 +486,11 @@ __global__ void cull_fill(DpList L, int32_t P, int32_t B, double eps, int mode, 
                           uint8_t* tphi, float tc_guard,
                           const int32_t* __restrict__ acnt, const uint32_t* __restrict__ l0cnt,
                           const int64_t* __restrict__ lofs, const int64_t* __restrict__ ioff,
-                          const int32_t* __restrict__ counts, CullItem* items, int32_t* err) {
+                          const int32_t* __restrict__ counts, CullItem* items, int32_t* err,
+                          int32_t cpi) {
   cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi, tphi,
                     tc_guard);
-  cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err);
+  cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err, cpi);
 }
 
 // All of a small level's planning in one CTA (the four steps above, block barriers between):
@@ -475,17 +502,17 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
     const float* k12, int64_t* act, int32_t* acnt, int32_t* tanc, int32_t* tslot, int64_t* aoff,
     int64_t* ioff, int32_t* cidx, float* phi, uint8_t* tphi, float tc_guard, VoteSeg* segs,
     int32_t* counts, int32_t* work, CullItem* items, int64_t target, int64_t max_items,
-    int32_t* err, int64_t own_lo, int64_t own_hi) {
+    int32_t* err, int64_t own_lo, int64_t own_hi, int32_t cpi) {
   cull_act_body(L, P, act, acnt, (int64_t)P * m0);
   __syncthreads();
   cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err, own_lo, own_hi);
   __syncthreads();
   cull_scan_body(L, rows, toffs, P, B, eps, m0, l0cnt, k12, acnt, aoff, ioff, segs, counts, work,
-                 target, max_items, err);
+                 target, max_items, err, cpi);
   __syncthreads();
   cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi, tphi,
                     tc_guard);
-  cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err);
+  cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err, cpi);
 }
 
 // ---- K3-C ------------------------------------------------------------------------------------
@@ -729,68 +756,91 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
 }
 
 // ---- K3-CT: the culled vote on the tensor cores ------------------------------------------------
-// The same items as K3-C, with the roles of K3-TC transposed: A (M = 128) = a stage of 128
-// gathered correspondences (their 64-byte fp16-split rows of the K1-TC table, copied by cp.async
-// into the UMMA interleaved layout), B (N = 32, FIN: 64) = the item's blocks (the planner's
-// K2-TC-format rows; FIN: two rows per block, tau -/+ g'), D = 128 x N scores in TMEM.  One
-// CTA per SM, persistent over items (static stride); roles: warp 0 gathers (all lanes, four
-// 16-byte cp.async per row, completion on an mbarrier via cp.async.mbarrier.arrive.noinc), warp 1
-// allocates TMEM and issues 2 tcgen05.mma (K = 16 each) per stage into a ring of 512 / N
-// accumulators, warps 2-5 read their 32 TMEM lanes (= 32 correspondences of the stage) with one
-// tcgen05.ld.32x32b.x32 per 32 columns and count sign bits per column (block) in registers.
-// Padding correspondences gather the table's padding row (score -1: never counted).  Error bound
-// and guard: K3-TC's.
-#ifndef RV_CT_EG
-#define RV_CT_EG 2  // K3-CT epilogue: accumulators read per round (bound mode)
-#endif
+// An item is up to 128 block rows (FIN: 64 blocks, two rows each, tau -/+ g') of one bucket x a
+// range of the bucket's list.  The bucket is a GROUP of level-0 ancestors (K3-CT lists are the
+// unions of 2 x 2 neighbouring ancestors' lists, so an item carries ~4 x 27 blocks and each
+// gathered correspondence row is reused by all of them; a block's count over the union differs
+// from its count over its own ancestor's list only inside the guard band, as above).
+// D[block, entry] = A . B^T with A (M = 128) = the item's block rows (the planner's K2-TC-format
+// fp16-split rows, one 8 KB bulk copy per item) and B (N = 256) = a stage of 256 gathered
+// correspondences (their 64-byte rows of the K1-TC table, cp.async into the UMMA interleaved
+// layout), two tcgen05.mma (K = 16 each) per stage into one of two 256-column TMEM accumulators.
+// One CTA per SM, persistent over items (static stride).  Warps: 0 .. kCtProd-1 gather (stage k
+// to warp k % kCtProd, completion on an mbarrier via cp.async.mbarrier.arrive.noinc; warp 0 also
+// loads the A rows), kCtProd issues the MMAs, then 8 epilogue warps: two per TMEM lane quarter
+// (= 32 block rows), taking alternate stages, each thread counting the sign bits of its block
+// row over the stage's 256 columns (tcgen05.ld.32x32b.x32, half on the ALU, half as IMAD.HI).
+// Warps whose 32 rows are all past the item's blocks skip the reads.  Padding correspondences
+// gather the table's padding row (score -1: never counted).  Error bound and guard: K3-TC's.
 #ifndef RV_CT_ABL
-#define RV_CT_ABL 0  // tuning only: 1 no gather copies, 2 no MMAs (wrong counts)
-#endif
-#ifndef RV_CT_FENCE
-#define RV_CT_FENCE 1
+#define RV_CT_ABL 0  // tuning only: 1 no gather copies, 2 no MMAs, 4 no TMEM reads, 8 no index
+                     // loads (wrong counts)
 #endif
 #ifndef RV_CT_LOOK
-#define RV_CT_LOOK 12  // stages of entry indices the K3-CT producer loads ahead
+#define RV_CT_LOOK 3  // stages of entry indices a K3-CT gathering warp loads ahead
 #endif
 #ifndef RV_CT_STAGES
-#define RV_CT_STAGES 16
+#define RV_CT_STAGES 8
 #endif
-constexpr int kCtStages = RV_CT_STAGES;  // 8 KB gathered stages in flight
+constexpr int kCtStages = RV_CT_STAGES;  // 16 KB gathered stages in flight
 #ifndef RV_CT_PROD
-#define RV_CT_PROD 4  // gathering warps (stage gs goes to warp gs % RV_CT_PROD)
+#define RV_CT_PROD 4  // gathering warps
 #endif
 constexpr int kCtProd = RV_CT_PROD;
-constexpr int kCtThreads = (kCtProd + 5) * 32;
-
-#ifndef RV_CT_TILES
-#define RV_CT_TILES 1  // 128-entry tiles per K3-CT stage (amortises the per-stage barrier work)
+constexpr int kCtN = 256;                            // gathered entries per stage
+#ifndef RV_CT_EPQ
+#define RV_CT_EPQ 4  // K3-CT epilogue warps per TMEM lane quarter (column slices of a stage)
 #endif
-constexpr int kCtTiles = RV_CT_TILES;
+constexpr int kCtEpq = RV_CT_EPQ;
+constexpr int kCtEpi0 = kCtProd + 1;                 // first epilogue warp
+constexpr int kCtThreads = (kCtProd + 1 + 4 * kCtEpq) * 32;
+#ifndef RV_CT_ITEMS_PER_SM
+#define RV_CT_ITEMS_PER_SM 32  // K3-CT planner target (items per CTA)
+#endif
 
-template <bool FIN>
 struct CtSmem {
-  static constexpr int N = FIN ? 64 : 32;
-  static constexpr int NACC = 512 / N;
-  uint8_t a[kCtStages][kCtTiles][128 * 64];
-  uint8_t b[2][64 * 64];
-  uint64_t full[kCtStages], empty[kCtStages], bfull[2], bempty[2], tfull[NACC], tempty[NACC];
-  uint32_t tot[2][64];
+  uint8_t b[kCtStages][kCtN * 64];  // gathered correspondence rows (B operand)
+  uint8_t a[2][128 * 64];           // the item's block rows (A operand), double-buffered
+  uint64_t full[kCtStages], empty[kCtStages], afull[2], aempty[2], tfull[2], tempty[2];
   uint32_t tmem_base;
 };
 
+__device__ __forceinline__ void ct_sign_alu(uint32_t& acc, uint32_t bits) {
+  asm volatile("add.u32 %0, %0, %1;" : "+r"(acc) : "r"(bits >> 31));
+}
+__device__ __forceinline__ void ct_sign_fma(uint32_t& acc, uint32_t bits, uint32_t two) {
+  asm volatile("mad.hi.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(bits), "r"(two));
+}
+
+#ifndef RV_CT_SPIN
+#define RV_CT_SPIN 0  // tuning: poll the pipeline barriers with test_wait instead of try_wait
+#endif
+__device__ __forceinline__ void ct_wait(uint64_t* b, uint32_t parity) {
+#if RV_CT_SPIN
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(tcx::su32(b)), "r"(parity)
+        : "memory");
+#else
+  tcx::bar_wait(b, parity);
+#endif
+}
+
 template <bool FIN>
-__global__ void __launch_bounds__(kCtThreads, 1)
+__global__ void __launch_bounds__(kCtThreads)
     rv_vote_cull_tc_kernel(const VoteSeg* __restrict__ segs, const CullItem* __restrict__ items,
                            const int32_t* __restrict__ counts_dev, const uint8_t* __restrict__ tab,
                            int64_t pad_row, const uint8_t* __restrict__ tphi,
                            const int32_t* __restrict__ cidx, const uint32_t* __restrict__ lidx,
                            unsigned long long* pairs) {
   using namespace tcx;
-  using SM = CtSmem<FIN>;
-  constexpr int N = SM::N, NACC = SM::NACC, T = kCtTiles, SE = 128 * T;  // entries per stage
-  static_assert(NACC % T == 0, "a stage's accumulators are consecutive in the ring");
   extern __shared__ __align__(1024) uint8_t ct_raw[];
-  SM& sm = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(ct_raw) + 1023) & ~(uintptr_t)1023);
+  CtSmem& sm = *reinterpret_cast<CtSmem*>((reinterpret_cast<uintptr_t>(ct_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t n_items = counts_dev[0];
   if (warp == kCtProd) {
@@ -805,12 +855,10 @@ __global__ void __launch_bounds__(kCtThreads, 1)
       bar_init(&sm.empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      bar_init(&sm.bfull[i], 1);
-      bar_init(&sm.bempty[i], 1);
-    }
-    for (int i = 0; i < NACC; ++i) {
+      bar_init(&sm.afull[i], 1);
+      bar_init(&sm.aempty[i], 1);
       bar_init(&sm.tfull[i], 1);
-      bar_init(&sm.tempty[i], 4);
+      bar_init(&sm.tempty[i], 4 * kCtEpq);  // every epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -820,55 +868,54 @@ __global__ void __launch_bounds__(kCtThreads, 1)
   const uint32_t tmem = sm.tmem_base;
 
   if (warp < kCtProd) {
-    // ---------------- gather (kCtProd warps; stage gs goes to warp gs % kCtProd) ----------------
+    // ---------------- gather ----------------
     const int pw = warp;
     uint32_t gs = 0, gi = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
       const CullItem it = items[idx];
-      const VoteSeg& sg = segs[it.seg];
-      const int64_t toff = sg.koff;
-      const uint32_t bb = gi & 1;
-      if (pw == 0 && lane == 0) {
-        if (gi >= 2) bar_wait(&sm.bempty[bb], ((gi >> 1) - 1) & 1);
-        const uint32_t bytes = (uint32_t)N * 64;
+      const int64_t toff = segs[it.seg].koff;
+      if (pw == 0 && lane == 0) {  // the item's 128 block rows (rows past its blocks: ignored)
+        const uint32_t ab = gi & 1;
+        if (gi >= 2) bar_wait(&sm.aempty[ab], ((gi >> 1) - 1) & 1);
         const int64_t row0 = FIN ? 2 * (int64_t)it.pos0 : it.pos0;  // multiple of 8
-        bar_expect_tx(&sm.bfull[bb], bytes);
-        bulk_g2s(sm.b[bb], tphi + (row0 >> 3) * 512, bytes, &sm.bfull[bb]);
+        bar_expect_tx(&sm.afull[ab], 128 * 64);
+        bulk_g2s(sm.a[ab], tphi + (row0 >> 3) * 512, 128 * 64, &sm.afull[ab]);
       }
       const uint32_t* li = lidx + it.e0;
-      const int ns = (it.ne + SE - 1) / SE;
-      // a stage's SE indices (4 T per lane: entry r*32 + lane) are loaded kCtLook of this warp's
-      // stages ahead into a register ring whose slots are reused in place
-      constexpr int kCtLook = RV_CT_LOOK;
-      uint32_t ring[kCtLook][4 * T];
-      auto load_idx = [&](int k, uint32_t (&ix)[4 * T]) {
+      const int ns = (it.ne + kCtN - 1) / kCtN;
+      // a stage's 256 indices (8 per lane: entry r*32 + lane) are loaded RV_CT_LOOK of this
+      // warp's stages ahead into a register ring whose slots are reused in place
+      constexpr int kLook = RV_CT_LOOK;
+      uint32_t ring[kLook][8];
+      auto load_idx = [&](int k, uint32_t (&ix)[8]) {
 #pragma unroll
-        for (int r = 0; r < 4 * T; ++r) {
-          const int ge = k * SE + r * 32 + lane;
-          ix[r] = ge < it.ne ? __ldcs(li + ge) : 0xffffffffu;  // streamed once: evict first
+        for (int r = 0; r < 8; ++r) {
+          const int ge = k * kCtN + r * 32 + lane;
+          ix[r] = (RV_CT_ABL & 8) ? (uint32_t)ge
+                                  : ge < it.ne ? __ldcs(li + ge) : 0xffffffffu;  // streamed once
         }
       };
       const int k0 = (int)((pw - (int)(gs % kCtProd) + kCtProd) % kCtProd);
 #pragma unroll
-      for (int d = 0; d < kCtLook; ++d) load_idx(k0 + d * kCtProd, ring[d]);
-      for (int kb = k0; kb < ns; kb += kCtLook * kCtProd) {
+      for (int d = 0; d < kLook; ++d) load_idx(k0 + d * kCtProd, ring[d]);
+      for (int kb = k0; kb < ns; kb += kLook * kCtProd) {
 #pragma unroll
-        for (int d = 0; d < kCtLook; ++d) {
+        for (int d = 0; d < kLook; ++d) {
           const int k = kb + d * kCtProd;
           if (k >= ns) break;
           const uint32_t gk = gs + (uint32_t)k, st = gk % kCtStages;
-          uint32_t cur[4 * T];
+          uint32_t cur[8];
 #pragma unroll
-          for (int r = 0; r < 4 * T; ++r) cur[r] = ring[d][r];
-          load_idx(k + kCtLook * kCtProd, ring[d]);
+          for (int r = 0; r < 8; ++r) cur[r] = ring[d][r];
+          load_idx(k + kLook * kCtProd, ring[d]);
           if (gk >= (uint32_t)kCtStages) bar_wait(&sm.empty[st], ((gk / kCtStages) - 1) & 1);
           // four lanes per row, one 16-byte chunk each: a copy instruction covers 8 whole rows
 #pragma unroll
-          for (int j = 0; j < 16 * T; ++j) {
+          for (int j = 0; j < 32; ++j) {
             const int e = 8 * j + (lane >> 2), c = lane & 3;  // stage row, chunk
             const uint32_t ix = __shfl_sync(0xffffffffu, cur[j >> 2], e & 31);
             const int64_t g = ix != 0xffffffffu ? toff + (int64_t)ix : pad_row;
-            uint8_t* dst = sm.a[st][e >> 7] + ((e & 127) >> 3) * 512 + (e & 7) * 16 + c * 128;
+            uint8_t* dst = sm.b[st] + (e >> 3) * 512 + (e & 7) * 16 + c * 128;
             if (!(RV_CT_ABL & 1))
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)),
                            "l"(tab + g * 64 + c * 16)
@@ -883,91 +930,92 @@ __global__ void __launch_bounds__(kCtThreads, 1)
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == kCtProd) {
-    // ---------------- MMA issuer: T tiles per stage into T consecutive accumulators ----------
+    // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      uint32_t gs = 0, gi = 0, ga = 0;
+      uint32_t gs = 0, gi = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
-        const int ns = (items[idx].ne + SE - 1) / SE;
-        const uint32_t bb = gi & 1;
-        bar_wait(&sm.bfull[bb], (gi >> 1) & 1);
-        const uint32_t b0 = su32(sm.b[bb]);
-        for (int k = 0; k < ns; ++k, ++gs, ga += T) {
-          const uint32_t st = gs % kCtStages, acc0 = ga % NACC;
-          bar_wait(&sm.full[st], (gs / kCtStages) & 1);
-#if RV_CT_FENCE
+        const int ns = (items[idx].ne + kCtN - 1) / kCtN;
+        const uint32_t ab = gi & 1;
+        bar_wait(&sm.afull[ab], (gi >> 1) & 1);
+        const uint32_t a0 = su32(sm.a[ab]);
+        for (int k = 0; k < ns; ++k, ++gs) {
+          const uint32_t st = gs % kCtStages, acc = gs & 1;
+          ct_wait(&sm.full[st], (gs / kCtStages) & 1);
+          // cp.async writes are generic-proxy writes; the MMA reads through the async proxy
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
-          if (ga >= (uint32_t)NACC) bar_wait(&sm.tempty[acc0], ((ga / NACC) - 1) & 1);
+          if (gs >= 2) ct_wait(&sm.tempty[acc], ((gs >> 1) - 1) & 1);
           tc_fence_after();
+          const uint32_t b0 = su32(sm.b[st]);
 #pragma unroll
-          for (int t = 0; t < T; ++t) {
-            const uint32_t a0 = su32(sm.a[st][t]);
-#pragma unroll
-            for (int kk = 0; kk < 2; ++kk)
-              if (!(RV_CT_ABL & 2))
-                mma_f16_n<N>(tmem + (acc0 + t) * N, smem_desc(a0 + 256 * kk, 128, 512),
-                             smem_desc(b0 + 256 * kk, 128, 512), (uint32_t)kk);
-          }
+          for (int kk = 0; kk < 2; ++kk)
+            if (!(RV_CT_ABL & 2))
+              mma_f16_n<kCtN>(tmem + acc * kCtN, smem_desc(a0 + 256 * kk, 128, 512),
+                              smem_desc(b0 + 256 * kk, 128, 512), (uint32_t)kk);
           mma_commit(&sm.empty[st]);
-          mma_commit(&sm.tfull[acc0]);  // one barrier per stage (the group's first accumulator)
+          mma_commit(&sm.tfull[acc]);
         }
-        mma_commit(&sm.bempty[bb]);
+        mma_commit(&sm.aempty[ab]);
       }
     }
   } else {
-    // ---------------- epilogue (4 warps: TMEM lane quarter warp % 4) ----------------
-    const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-    const int ew = warp - kCtProd - 1;  // 0..3
-    uint32_t ga = 0;
+    // ---------------- epilogue (4 kCtEpq warps: lane quarter warp % 4, a column slice each) ---
+    const int ew = warp - kCtEpi0, slice = ew >> 2;
+    constexpr int kCols = kCtN / kCtEpq;  // columns of a stage per warp
+    const uint32_t lane_addr =
+        tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(slice * kCols);
+    const int m = 32 * (warp & 3) + lane;  // TMEM lane = A row = block row of the item
+    uint32_t gs = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const CullItem it = items[idx];
-      const int ns = (it.ne + SE - 1) / SE;
-      uint32_t neg[N];
-#pragma unroll
-      for (int j = 0; j < N; ++j) neg[j] = 0u;
-      for (int k = 0; k < ns; ++k, ga += T) {
-        const uint32_t acc0 = ga % NACC;
-        bar_wait(&sm.tfull[acc0], (ga / NACC) & 1);
+      const int ns = (it.ne + kCtN - 1) / kCtN;
+      const int nrows = FIN ? 2 * it.ncell : it.ncell;
+      const bool active = 32 * (warp & 3) < nrows;  // warp-uniform
+      uint32_t n0 = 0, n1 = 0;
+      for (int k = 0; k < ns; ++k) {
+        const uint32_t g = gs + (uint32_t)k, acc = g & 1;
+        ct_wait(&sm.tfull[acc], (g >> 1) & 1);
         tc_fence_after();
-        uint32_t r[T][N];
+        if (active && !(RV_CT_ABL & 4)) {
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-          RV_TCX_LD32(r[t], lane_addr + (acc0 + t) * N);
-          if (N == 64) RV_TCX_LD32((r[t] + 32), lane_addr + (acc0 + t) * N + 32);
+          for (int rr = 0; rr < kCols / 64; ++rr) {  // 64 columns per round (registers)
+            uint32_t r[2][32];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              RV_TCX_LD32(r[q], lane_addr + acc * kCtN + (uint32_t)(rr * 64 + 32 * q));
+            tmem_wait_ld();
+            if (rr == kCols / 64 - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) bar_arrive(&sm.tempty[acc]);
+            }
+            // sign bits -> one word per 32 columns (shf funnel: w = w << 1 | sign); negatives
+            // = its popcount
+            uint32_t w0 = 0u, w1 = 0u;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w0) : "r"(r[0][e]));
+              asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w1) : "r"(r[1][e]));
+            }
+            n0 += __popc(w0);
+            n1 += __popc(w1);
+          }
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) bar_arrive(&sm.tempty[acc]);
         }
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) bar_arrive(&sm.tempty[acc0]);
-#pragma unroll
-        for (int t = 0; t < T; ++t)
-#pragma unroll
-          for (int j = 0; j < N; ++j)
-            asm volatile("add.u32 %0, %0, %1;" : "+r"(neg[j]) : "r"(r[t][j] >> 31));
       }
-      // column totals: slots - negatives, summed over the 32 lanes and the 4 epilogue warps
-      // (padding rows score -1: negatives, so the slots need no correction)
-      if (ew == 0 && lane < N / 2) sm.tot[0][lane] = 0u, sm.tot[0][lane + N / 2] = 0u;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-#pragma unroll
-      for (int j = 0; j < N; ++j) {
-        const uint32_t v = __reduce_add_sync(0xffffffffu, (uint32_t)(ns * T) - neg[j]);
-        if (lane == 0) atomicAdd(&sm.tot[0][j], v);
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (ew == 0 && lane < it.ncell) {
-        const VoteSeg& sg = segs[it.seg];
-        const int32_t e = cidx[it.pos0 + lane];
-        if (FIN) {
-          if (sm.tot[0][2 * lane]) atomicAdd(&sg.cnt_a[e], sm.tot[0][2 * lane]);
-          if (sm.tot[0][2 * lane + 1]) atomicAdd(&sg.cnt_b[e], sm.tot[0][2 * lane + 1]);
-        } else if (sm.tot[0][lane]) {
-          atomicAdd(&sg.cnt_a[e], sm.tot[0][lane]);
+      gs += (uint32_t)ns;
+      if (active && m < nrows) {
+        const uint32_t pass = (uint32_t)ns * kCols - (n0 + n1);
+        if (pass) {
+          const VoteSeg& sg = segs[it.seg];
+          const int32_t e = cidx[it.pos0 + (FIN ? (m >> 1) : m)];
+          atomicAdd(FIN && (m & 1) ? &sg.cnt_b[e] : &sg.cnt_a[e], pass);
         }
       }
       if (ew == 0 && lane == 0 && pairs)
         atomicAdd(pairs, (unsigned long long)it.ne * (unsigned long long)it.ncell);
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // tot is reused by the next item
     }
   }
   tc_fence_before();
@@ -1003,7 +1051,7 @@ void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
                          const uint8_t* tphi, const int32_t* cidx, const uint32_t* lidx,
                          unsigned long long* pairs, int num_sms, cudaStream_t s) {
   static bool attr = false;
-  const size_t b0 = sizeof(CtSmem<false>) + 1024, b1 = sizeof(CtSmem<true>) + 1024;
+  const size_t b0 = sizeof(CtSmem) + 1024, b1 = b0;
   if (!attr) {
     cudaFuncSetAttribute(rv_vote_cull_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)b0);
@@ -1032,22 +1080,24 @@ void launch_vote_cull(int mode, const VoteSeg* segs, const CullItem* items,
 }
 
 void launch_cull_rows(const uint32_t* l0cnt, int32_t P, int64_t m0, int64_t* lofs,
-                      cudaStream_t s) {
-  cull_rows<<<1, 1024, 0, s>>>(l0cnt, (int64_t)P * m0, lofs);
+                      cudaStream_t s, const CullGroups& gr) {
+  const int64_t G = gr.goff ? gr.G : m0;
+  cull_rows<<<1, 1024, 0, s>>>(l0cnt, (int64_t)P * G, m0, G, gr.goff, gr.gmem, lofs);
 }
 
 void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P, int64_t m0,
                          int64_t wpc_max, const int64_t* lofs, int32_t* fill, uint32_t* lidx,
-                         cudaStream_t s, int64_t row_lo, int64_t row_hi) {
-  const int64_t NB = (int64_t)P * m0, nseg = (wpc_max + kCompactSeg - 1) / kCompactSeg;
+                         cudaStream_t s, int64_t row_lo, int64_t row_hi, const CullGroups& gr) {
+  const int64_t G = gr.goff ? gr.G : m0;
+  const int64_t NB = (int64_t)P * G, nseg = (wpc_max + kCompactSeg - 1) / kCompactSeg;
   if (row_hi > NB) row_hi = NB;
   if (row_lo >= row_hi) return;
   const int64_t NR = row_hi - row_lo;
   cudaMemsetAsync(fill, 0, (size_t)NB * 4, s);
   int64_t blocks = (NR * nseg + 7) / 8;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  cull_compact<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(bits0, toffs, m0, row_lo, NR, nseg,
-                                                                   lofs, fill, lidx);
+  cull_compact<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(
+      bits0, toffs, m0, G, gr.goff, gr.gmem, row_lo, NR, nseg, lofs, fill, lidx);
 }
 
 int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
@@ -1059,13 +1109,16 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
   const int64_t NB = (int64_t)P * m0;
   // items: ~8 per resident K3-C warp; K3-CT (one CTA per SM, tphi set) ~4 per CTA, since its
   // per-item cost (the block rows, the column reduction) is larger
-  const int64_t target = cs.tphi ? 4LL * num_sms : 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
+  const int64_t target = cs.tphi ? (int64_t)RV_CT_ITEMS_PER_SM * num_sms
+                                 : 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
+  // blocks per item: K3-C 32 (a warp's lanes); K3-CT the MMA's 128 rows (FIN: two per block)
+  const int32_t cpi = cs.tphi ? (mode == RV_MODE_FINAL ? 64 : 128) : kCullMaxCells;
   if (entries_bound <= 8192 && NB <= (1 << 14)) {
     cull_plan_small<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, B0, lut0, m0, eps, mode, guard, l0cnt,
                                        lofs, k12, cs.act, cs.acnt, cs.tanc, cs.tslot, cs.aoff,
                                        cs.ioff, cs.cidx, cs.phi, cs.tphi, cs.tc_guard, segs,
                                        cs.counts, cs.work, items, target, max_items, err, own_lo,
-                                       own_hi);
+                                       own_hi, cpi);
     return 1;
   }
   const bool small = NB <= (1 << 16);
@@ -1074,10 +1127,10 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
   cull_count<<<148 * 8, 256, 0, s>>>(L, P, B, B0, lut0, m0, cs.act, cs.acnt, cs.tanc, cs.tslot, err,
                                      own_lo, own_hi);
   cull_scan<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, eps, m0, l0cnt, k12, cs.acnt, cs.aoff, cs.ioff,
-                               segs, cs.counts, cs.work, target, max_items, err);
+                               segs, cs.counts, cs.work, target, max_items, err, cpi);
   cull_fill<<<148 * 8, 256, 0, s>>>(L, P, B, eps, mode, guard, m0, cs.act, cs.aoff, cs.tanc, cs.tslot,
                                     cs.cidx, cs.phi, cs.tphi, cs.tc_guard, cs.acnt, l0cnt, lofs,
-                                    cs.ioff, cs.counts, items, err);
+                                    cs.ioff, cs.counts, items, err, cpi);
   return 4;
 }
 

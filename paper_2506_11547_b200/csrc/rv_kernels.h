@@ -157,13 +157,21 @@ void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
 // Level-0 index lists: row offsets lofs[P*m0 + 1] (exclusive prefix of the level-0 counts, each
 // padded to a multiple of 4; lofs[P*m0] = the total), then the compaction of the K3-TC bitmasks
 // (bits0: problem p's rows from m0 * toffs[p] / 32, (toffs[p+1] - toffs[p]) / 32 words each).
+// Ancestor groups (K3-CT): list row g of a problem is the union of the level-0 rows
+// gmem[goff[g] .. goff[g+1]), G rows per problem; goff == nullptr: one row per level-0 row.
+struct CullGroups {
+  const int32_t* goff = nullptr;
+  const int32_t* gmem = nullptr;
+  int64_t G = 0;
+};
 void launch_cull_rows(const uint32_t* l0cnt, int32_t P, int64_t m0, int64_t* lofs,
-                      cudaStream_t s);
+                      cudaStream_t s, const CullGroups& gr = CullGroups());
 // (any order within a row; fill: scratch [P*m0] int32; rows [row_lo, row_hi) only: the rows
 // this rank voted at level 0)
 void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P, int64_t m0,
                          int64_t wpc_max, const int64_t* lofs, int32_t* fill, uint32_t* lidx,
-                         cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = INT64_MAX);
+                         cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = INT64_MAX,
+                         const CullGroups& gr = CullGroups());
 
 
 // K4 (batched): level-0 reductions, one CTA per problem.  argmax: the dive's start index per

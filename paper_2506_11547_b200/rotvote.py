@@ -52,7 +52,7 @@ class rv_result(C.Structure):
                 ("n_rechecked", C.c_int32), ("vote_ms", C.c_float), ("launches", C.c_int32),
                 ("vote_pairs", C.c_uint64), ("vote_launches", C.c_int32),
                 ("cull_launches", C.c_int32), ("cull_pairs", C.c_uint64), ("cull_ms", C.c_float),
-                ("pad_", C.c_int32)]
+                ("cull_tc_launches", C.c_int32)]
 
 
 class rv_alg1_result(C.Structure):
@@ -196,6 +196,7 @@ class Result:
     cull_launches: int = 0
     cull_pairs: int = 0
     cull_ms: float = 0.0
+    cull_tc_launches: int = 0
 
     @property
     def lin(self) -> int:
@@ -211,7 +212,8 @@ class Result:
                       ms=r.ms, n_rechecked=r.n_rechecked, vote_ms=r.vote_ms,
                       launches=r.launches, vote_pairs=r.vote_pairs,
                       vote_launches=r.vote_launches, cull_launches=r.cull_launches,
-                      cull_pairs=r.cull_pairs, cull_ms=r.cull_ms)
+                      cull_pairs=r.cull_pairs, cull_ms=r.cull_ms,
+                      cull_tc_launches=r.cull_tc_launches)
 
 
 class RotVote:

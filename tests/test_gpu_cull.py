@@ -36,8 +36,8 @@ def torch_cuda():
 
 
 def _ctx(path, **kw):
-    """A culling context on the FP32 K3-C path ("fp32", default) or the tensor-core K3-CT path
-    ("tc": RV_CULL_TC=1 at creation)."""
+    """A culling context on the tensor-core K3-CT path ("tc", default; one rank) or the FP32
+    K3-C path ("fp32": RV_CULL_TC=0 at creation)."""
     import os
     from paper_2506_11547_b200 import RotVote
     old = os.environ.get("RV_CULL_TC")
@@ -223,14 +223,16 @@ def test_culled_batched_matches_oracle(rvc, torch_cuda):
 
 def test_culled_loopback_shards(torch_cuda):
     """emulate_world: level 0 voted whole (every rank holds every ancestor's list), finer
-    levels sliced over the emulated ranks -- the same result as one rank."""
-    from paper_2506_11547_b200 import RotVote
+    levels sliced over the emulated ranks -- the same result as one rank.  Several ranks vote
+    the culled levels on K3-C (a rank's level-0 slice need not hold whole K3-CT groups), so the
+    search path is compared against one rank on K3-C, and the one-rank K3-CT solve (whose
+    bounds differ inside the guard band) must reach the same answer."""
     torch = torch_cuda
     for pr in (datagen.cfg2(seed=5), datagen.make_problem(40_000, 400, 0.01, 0.05, seed=8)):
         x, y = dev(torch, pr.x), dev(torch, pr.y)
         ref = None
         for W in (1, 2, 3, 8):
-            ctx = _ctx("tc", max_n=1 << 17, emulate_world=W)
+            ctx = _ctx("fp32", max_n=1 << 17, emulate_world=W)
             try:
                 r = ctx.solve(x, y, pr.eps)
             finally:
@@ -243,3 +245,12 @@ def test_culled_loopback_shards(torch_cuda):
                                                                 ref.n_inliers), W
             assert np.array_equal(r.q, ref.q), W
             assert r.cells_per_phase == ref.cells_per_phase, W
+        ctx = _ctx("tc", max_n=1 << 17)
+        try:
+            r = ctx.solve(x, y, pr.eps)
+        finally:
+            ctx.close()
+        assert r.cull_tc_launches > 0
+        assert (r.cell, r.votes, r.n_tied, r.n_inliers) == (ref.cell, ref.votes, ref.n_tied,
+                                                            ref.n_inliers)
+        assert oracle.rotation_angle_between(r.q, ref.q) < 1e-9
