@@ -776,6 +776,12 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
 #define RV_CT_ABL 0  // tuning only: 1 no gather copies, 2 no MMAs, 4 no TMEM reads, 8 no index
                      // loads (wrong counts)
 #endif
+#ifndef RV_CT_FENCE
+// no proxy fence between the cp.async gathers and the MMA reads: the gathers complete on the
+// stage's mbarrier (cp.async.mbarrier.arrive) and the MMA thread acquires it -- the protocol of
+// CUTLASS's sm100 cp.async UMMA mainloop (PipelineUmmaConsumerAsync); 1 adds the fence
+#define RV_CT_FENCE 0
+#endif
 #ifndef RV_CT_LOOK
 #define RV_CT_LOOK 3  // stages of entry indices a K3-CT gathering warp loads ahead
 #endif
@@ -941,8 +947,9 @@ __global__ void __launch_bounds__(kCtThreads)
         for (int k = 0; k < ns; ++k, ++gs) {
           const uint32_t st = gs % kCtStages, acc = gs & 1;
           ct_wait(&sm.full[st], (gs / kCtStages) & 1);
-          // cp.async writes are generic-proxy writes; the MMA reads through the async proxy
+#if RV_CT_FENCE
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
           if (gs >= 2) ct_wait(&sm.tempty[acc], ((gs >> 1) - 1) & 1);
           tc_fence_after();
           const uint32_t b0 = su32(sm.b[st]);
