@@ -50,6 +50,10 @@ constexpr int kCullThreads = 32 * kCullWarpsPerCta;
 #ifndef RV_CULL_MIN_CE
 #define RV_CULL_MIN_CE 128  // entries per K3-C item at least (multiple of 128)
 #endif
+#ifndef RV_CT_MIN_CE
+#define RV_CT_MIN_CE 2048  // entries per K3-CT item at least (measured: 256 -> 2048 halves the
+                           // small levels' vote time)
+#endif
 #ifndef RV_CULL_ABL
 #define RV_CULL_ABL 0  // tuning only: 1 no FFMA2, 2 no gather (wrong counts)
 #endif
@@ -326,7 +330,10 @@ __device__ __forceinline__ void cull_scan_body(DpList L, const int64_t* __restri
   if (t == 0) {
     const int64_t q = cpi > 32 ? 256 : 128;  // K3-CT stages are 256 entries
     const int64_t ce = (tot_w / (target > 0 ? target : 1) + q - 1) / q * q;
-    s_ce = ce < RV_CULL_MIN_CE ? (RV_CULL_MIN_CE + q - 1) / q * q : ce;
+    // K3-CT: at least 2048 entries (8 stages) per item -- small levels otherwise cut
+    // thousands of one-stage items, each paying its block-row load and pipeline fill
+    const int64_t mce = cpi > 32 ? RV_CT_MIN_CE : RV_CULL_MIN_CE;
+    s_ce = ce < mce ? (mce + q - 1) / q * q : ce;
   }
   __syncthreads();
   const int64_t CE = s_ce;
