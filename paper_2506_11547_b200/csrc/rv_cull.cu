@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(1024) cull_scan(DpList L, const int64_t* __res
                  target, max_items, err, cpi);
 }
 
-// entries into bucket order: cidx[pos] = the entry's index in its problem's list; phi: per
-// block quad (positions 4k .. 4k+3) 12 float4 rows, row j = (v_j of its 4 blocks) with
+// entries into bucket order: cidx[pos] = the entry's index in its problem's list; K3-CT
+// (tphi set): the blocks' fp16-split rows only; K3-C: phi, per block quad (positions 4k .. 4k+3) 12 float4 rows, row j = (v_j of its 4 blocks) with
 // v = phi(q_c) (9), -(threshold) (the chain's initial value), 0, 0 -- so a lane loads its quad's
 // phi_j as one float4 whose halves are the aligned register pairs FFMA2 takes
 __device__ __forceinline__ void cull_scatter_body(DpList L, int32_t P, int32_t B, double eps, int mode, float guard,
@@ -403,6 +403,57 @@ __device__ __forceinline__ void cull_scatter_body(DpList L, int32_t P, int32_t B
                              const int32_t* __restrict__ tslot, int32_t* cidx, float* phi,
                              uint8_t* tphi, float tc_guard) {
   const int64_t T = act[P];
+  const bool fin = mode == RV_MODE_FINAL;
+  if (tphi) {
+    // K3-CT reads only the fp16-split rows and cidx: one thread per row (FIN: two per block),
+    // no FP32 phi table
+    const int64_t R = fin ? 2 * T : T;
+    for (int64_t gr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gr < R;
+         gr += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t g = fin ? gr >> 1 : gr;
+      const int h = fin ? (int)(gr & 1) : 0;
+      if (tanc[g] < 0) continue;  // not this rank's
+      const int p = find_p(act, P, g);
+      const int64_t e = g - act[p];
+      const int64_t pos = aoff[(int64_t)p * m0 + tanc[g]] + tslot[g];
+      if (h == 0) cidx[pos] = (int32_t)e;
+      int32_t i, j, k;
+      lin_to_ijk(list_lins(L, p)[e], B, i, j, k);
+      double q[4], f[9];
+      cell_quat(B, i, j, k, q);
+      phi9(q, f);
+      // K2-TC rows [phi_hi | phi_lo | phi_hi | -t_hi, -t_lo, -1, 0, 0]
+      const double tt = fin ? cos(eps) + (h ? tc_guard : -tc_guard)
+                            : bound_threshold(B, i, j, k, eps) - tc_guard;
+      __half v[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = __float2half_rn(0.0f);
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const __half hi = __double2half(f[t]);
+        const __half lo = __double2half(f[t] - (double)__half2float(hi));
+        v[t] = hi;
+        v[9 + t] = lo;
+        v[18 + t] = hi;
+      }
+      const __half th = __double2half(-tt);
+      const __half tl = __double2half(-tt - (double)__half2float(th));
+      v[27] = th;
+      v[28] = tl;
+      v[29] = __float2half_rn(-1.0f);
+      const int64_t row = fin ? 2 * pos + h : pos;
+      uint8_t* rp = tphi + (row >> 3) * 512 + (row & 7) * 16;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint4 w;
+        __half* hw = reinterpret_cast<__half*>(&w);
+#pragma unroll
+        for (int e2 = 0; e2 < 8; ++e2) hw[e2] = v[ch * 8 + e2];
+        *reinterpret_cast<uint4*>(rp + ch * 128) = w;
+      }
+    }
+    return;
+  }
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < T;
        g += (int64_t)gridDim.x * blockDim.x) {
     if (tanc[g] < 0) continue;  // not this rank's
@@ -415,45 +466,11 @@ __device__ __forceinline__ void cull_scatter_body(DpList L, int32_t P, int32_t B
     double q[4], f[9];
     cell_quat(B, i, j, k, q);
     phi9(q, f);
-    const double thr = mode == RV_MODE_FINAL ? cos(eps) - guard
-                                             : bound_threshold(B, i, j, k, eps) - guard;
+    const double thr = fin ? cos(eps) - guard : bound_threshold(B, i, j, k, eps) - guard;
     float* q4 = phi + (pos >> 2) * 48 + (pos & 3);
 #pragma unroll
     for (int t = 0; t < 9; ++t) q4[4 * t] = (float)f[t];
     q4[36] = (float)(-thr);
-    if (tphi) {  // K3-CT's B operand: K2-TC rows [phi_hi | phi_lo | phi_hi | -t_hi, -t_lo, -1, 0, 0]
-      const bool fin = mode == RV_MODE_FINAL;
-      for (int h = 0; h < (fin ? 2 : 1); ++h) {
-        const double tt = fin ? cos(eps) + (h ? tc_guard : -tc_guard)
-                              : bound_threshold(B, i, j, k, eps) - tc_guard;
-        __half v[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = __float2half_rn(0.0f);
-#pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          const __half hi = __double2half(f[t]);
-          const __half lo = __double2half(f[t] - (double)__half2float(hi));
-          v[t] = hi;
-          v[9 + t] = lo;
-          v[18 + t] = hi;
-        }
-        const __half th = __double2half(-tt);
-        const __half tl = __double2half(-tt - (double)__half2float(th));
-        v[27] = th;
-        v[28] = tl;
-        v[29] = __float2half_rn(-1.0f);
-        const int64_t row = fin ? 2 * pos + h : pos;
-        uint8_t* rp = tphi + (row >> 3) * 512 + (row & 7) * 16;
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint4 w;
-          __half* hw = reinterpret_cast<__half*>(&w);
-#pragma unroll
-          for (int e2 = 0; e2 < 8; ++e2) hw[e2] = v[ch * 8 + e2];
-          *reinterpret_cast<uint4*>(rp + ch * 128) = w;
-        }
-      }
-    }
   }
 }
 
