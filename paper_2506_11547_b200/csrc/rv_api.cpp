@@ -497,11 +497,12 @@ void build_tc_items(const std::vector<int64_t>& ncell, const std::vector<int64_t
 void build_exact_items(const std::vector<int64_t>& ncell, const std::vector<int64_t>& ncorr,
                        std::vector<rv::VoteItem>& items) {
   items.clear();
-  const int64_t chunk = 1 << 13;  // >= 1 wave of CTAs even for a single block at N = 1e6
+  const int64_t chunk = 1 << 12;  // ~250 items per block group at N = 1e6: one wave
   for (size_t s = 0; s < ncell.size(); ++s)
-    for (int64_t c = 0; c < ncell[s]; ++c)
+    for (int64_t c = 0; c < ncell[s]; c += rv::kExactCells)
       for (int64_t i0 = 0; i0 < ncorr[s]; i0 += chunk)
-        items.push_back({(int32_t)s, (int32_t)c, 1, (int32_t)i0,
+        items.push_back({(int32_t)s, (int32_t)c,
+                         (int32_t)std::min<int64_t>(rv::kExactCells, ncell[s] - c), (int32_t)i0,
                          (int32_t)std::min(chunk, ncorr[s] - i0)});
 }
 

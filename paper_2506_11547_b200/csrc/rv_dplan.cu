@@ -327,7 +327,7 @@ namespace {
 __host__ __device__ __forceinline__ int64_t i64min(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t i64max(int64_t a, int64_t b) { return a > b ? a : b; }
 constexpr int kPlanThreads = 1024;
-constexpr int64_t kExactChunk = 1 << 13;  // = build_exact_items
+constexpr int64_t kExactChunk = 1 << 12;  // = build_exact_items (the final level has few blocks: the CTAs come from the correspondences)
 
 // correspondence chunks of a problem with nt tiles: ct = ceil(nt / min(nch, nt)) tiles each,
 // ceil(nt / ct) of them non-empty (the host builder's loop `for t0 < nt; t0 += ct`)
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
     const int64_t m = list_m(L, p), n = rows[p + 1] - rows[p];
     if (m == 0 || n == 0) continue;
     if (mode == 2) {
-      ni += m * ((n + kExactChunk - 1) / kExactChunk);
+      ni += (m + kExactCells - 1) / kExactCells * ((n + kExactChunk - 1) / kExactChunk);
     } else {
       const int64_t cb = (m + cpb - 1) / cpb, nt = (n + kTcN - 1) / kTcN;
       int64_t ct, nc;
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kPlanThreads) dp_items_plan(
     const int64_t m = list_m(L, p), n = rows[p + 1] - rows[p];
     if (m > 0 && n > 0) {
       if (mode == 2) {
-        ei += m * ((n + kExactChunk - 1) / kExactChunk);
+        ei += (m + kExactCells - 1) / kExactCells * ((n + kExactChunk - 1) / kExactChunk);
       } else {
         const int64_t cb = (m + cpb - 1) / cpb, nt = (n + kTcN - 1) / kTcN;
         int64_t ct, nc;
@@ -527,9 +527,9 @@ __global__ void dp_items_write(DpList L, const int64_t* __restrict__ rows, int32
     it.seg = p;
     if (mode == 2) {
       const int64_t nc = (n + kExactChunk - 1) / kExactChunk;
-      const int64_t cell = local / nc, c = local % nc;
-      it.cell0 = (int32_t)cell;
-      it.ncell = 1;
+      const int64_t cg = local / nc, c = local % nc;
+      it.cell0 = (int32_t)(cg * kExactCells);
+      it.ncell = (int32_t)i64min(kExactCells, m - cg * kExactCells);
       it.i0 = (int32_t)(c * kExactChunk);
       it.ni = (int32_t)i64min(kExactChunk, n - c * kExactChunk);
       it.ablk = 0;

@@ -339,7 +339,7 @@ void launch_vote(int mode, int groups, const float* k9, int64_t stride, const Vo
 // ------------------------------------------------------------------------------------------
 // K5 exact count
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) rv_exact_kernel(const float* __restrict__ k9,
+__global__ void __launch_bounds__(256, 2) rv_exact_kernel(const float* __restrict__ k9,
                                                        int64_t stride,
                                                        const float* __restrict__ x,
                                                        const float* __restrict__ y,
@@ -349,59 +349,92 @@ __global__ void __launch_bounds__(256) rv_exact_kernel(const float* __restrict__
                                                        const int32_t* __restrict__ n_dev,
                                                        float guard) {
   // n_dev: the item count lives on the device (device-built items; fixed grid)
+  // An item is up to kExactCells blocks x a range of correspondences: each correspondence's K
+  // row is read once for all of them (the final level's few blocks used to re-stream the table
+  // once per block).
   const int32_t n = n_dev ? *n_dev : n_items;
+  __shared__ float sf32[kExactCells][9];
+  __shared__ double sf64[kExactCells][9];
+  __shared__ uint32_t ws[kExactCells][8];
+  __shared__ double s_tau;
   for (int32_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
   const VoteItem it = items[idx];
   const VoteSeg& sg = segs[it.seg];
-  const uint32_t lin = sg.lins[it.cell0];
-  int32_t ci, cj, ck;
-  lin_to_ijk(lin, sg.B, ci, cj, ck);
-  double q[4], f64[9];
-  cell_quat(sg.B, ci, cj, ck, q);
-  phi9(q, f64);
-  float f32[9];
+  const int nc = it.ncell < 1 ? 1 : (it.ncell > kExactCells ? kExactCells : it.ncell);
+  if (threadIdx.x == 32) s_tau = cos(sg.eps);
+  if ((int)threadIdx.x < nc) {
+    const uint32_t lin = sg.lins[it.cell0 + threadIdx.x];
+    int32_t ci, cj, ck;
+    lin_to_ijk(lin, sg.B, ci, cj, ck);
+    double q[4], f64[9];
+    cell_quat(sg.B, ci, cj, ck, q);
+    phi9(q, f64);
 #pragma unroll
-  for (int t = 0; t < 9; ++t) f32[t] = (float)f64[t];
-  const double tau = cos(sg.eps);
-  const float init = (float)(-tau);
+    for (int t = 0; t < 9; ++t) {
+      sf64[threadIdx.x][t] = f64[t];
+      sf32[threadIdx.x][t] = (float)f64[t];
+    }
+  }
+  __syncthreads();
+  const double tau_it = s_tau;
+  const float init = (float)(-tau_it);
 
-  uint32_t cnt = 0;
+  uint32_t cnt[kExactCells];
+#pragma unroll
+  for (int c = 0; c < kExactCells; ++c) cnt[c] = 0u;
   const int end = min(it.i0 + it.ni, sg.n);
   for (int i = it.i0 + threadIdx.x; i < end; i += blockDim.x) {
-    float s = init;
+    float kv[9];
 #pragma unroll
-    for (int t = 0; t < 9; ++t) s = fmaf(f32[t], k9[t * stride + sg.koff + i], s);
-    bool in;
-    if (fabsf(s) < guard) {  // near the threshold: decide in fp64 from the raw inputs
+    for (int t = 0; t < 9; ++t) kv[t] = k9[t * stride + sg.koff + i];
+    uint32_t near = 0u;  // blocks whose fp32 score is inside the guard band
+#pragma unroll
+    for (int c = 0; c < kExactCells; ++c) {
+      if (c < nc) {
+        float s = init;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) s = fmaf(sf32[c][t], kv[t], s);
+        if (fabsf(s) < guard) near |= 1u << c;
+        else cnt[c] += s >= 0.0f ? 1u : 0u;
+      }
+    }
+    if (near) {  // decide those in fp64 from the raw inputs
       const int64_t r = sg.row + i;
       double a[3] = {x[3 * r], x[3 * r + 1], x[3 * r + 2]};
       double b[3] = {y[3 * r], y[3 * r + 1], y[3 * r + 2]};
       const double ia = 1.0 / sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
       const double ib = 1.0 / sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { a[c] *= ia; b[c] *= ib; }
+      for (int u = 0; u < 3; ++u) { a[u] *= ia; b[u] *= ib; }
       double k[9];
       k9_of(a, b, k);
-      double s64 = 0.0;
+      uint32_t pass = 0u;
+#pragma unroll 1
+      for (int c = 0; c < kExactCells; ++c) {
+        if (!(near >> c & 1u)) continue;
+        double s64 = 0.0;
 #pragma unroll
-      for (int t = 0; t < 9; ++t) s64 = fma(f64[t], k[t], s64);
-      in = s64 >= tau;
-    } else {
-      in = s >= 0.0f;
+        for (int t = 0; t < 9; ++t) s64 = fma(sf64[c][t], k[t], s64);
+        pass |= (s64 >= tau_it ? 1u : 0u) << c;
+      }
+#pragma unroll
+      for (int c = 0; c < kExactCells; ++c) cnt[c] += pass >> c & 1u;  // (cnt stays in registers)
     }
-    cnt += in ? 1u : 0u;
   }
-  // block reduction
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
-  __shared__ uint32_t ws[32];
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
+  // block reduction per block of the item
+#pragma unroll
+  for (int c = 0; c < kExactCells; ++c) {
+    uint32_t v = cnt[c];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) ws[c][threadIdx.x >> 5] = v;
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if ((int)threadIdx.x < nc) {
     uint32_t t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
-    atomicAdd(&sg.cnt_a[it.cell0], t);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[threadIdx.x][w];
+    atomicAdd(&sg.cnt_a[it.cell0 + threadIdx.x], t);
   }
-  __syncthreads();  // ws is rewritten by the next item
+  __syncthreads();  // ws / sf* are rewritten by the next item
   }
 }
 

@@ -85,6 +85,7 @@ constexpr int kCullMaxCells = 32;    // blocks per K3-C item
 struct VoteItem {
   int32_t seg, cell0, ncell, i0, ni, ablk;
 };
+constexpr int kExactCells = 8;  // blocks per K5 item (each K row read once for all of them)
 
 // K3-TC A-operand block: rows of cells [cell0, cell0+ncell) of segment seg (8 KB in the table).
 struct ABlock {
