@@ -566,25 +566,43 @@ __device__ void jacobi4(double A[4][4], double V[4][4]) {
   }
 }
 
-// One warp per problem (8 per CTA): the lanes sum the problem's K6 partials, lane 0 solves.
+// One warp per problem (8 per CTA; per_cta: one CTA per problem, for small batches, so the
+// partials of a 1e6-row problem are summed by 256 threads): the lanes sum the problem's K6
+// partials in a fixed order, lane 0 solves.
 __global__ void __launch_bounds__(256) rv_eig_kernel(const RefSeg* __restrict__ segs,
                                                      const double* __restrict__ partials,
                                                      double* qs, int32_t* flags, uint32_t* ninl,
-                                                     int mode, int32_t P) {
+                                                     int mode, int32_t P, int per_cta) {
   const int lane = threadIdx.x & 31;
-  const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int p = per_cta ? blockIdx.x : blockIdx.x * 8 + (threadIdx.x >> 5);
   if (p >= P) return;
   const RefSeg& sg = segs[p];
   double S[10];
 #pragma unroll
   for (int t = 0; t < 10; ++t) S[t] = 0.0;
-  for (int itm = sg.item_begin + lane; itm < sg.item_end; itm += 32)
+  const int t0 = per_cta ? (int)threadIdx.x : lane, tn = per_cta ? (int)blockDim.x : 32;
+  for (int itm = sg.item_begin + t0; itm < sg.item_end; itm += tn)
 #pragma unroll
     for (int t = 0; t < 10; ++t) S[t] += partials[(int64_t)itm * 10 + t];
 #pragma unroll
   for (int t = 0; t < 10; ++t)
     for (int o = 16; o > 0; o >>= 1) S[t] += __shfl_down_sync(0xffffffffu, S[t], o);
-  if (lane != 0) return;
+  if (per_cta) {  // the warps' sums in warp order
+    __shared__ double ws[8][10];
+    if (lane == 0)
+#pragma unroll
+      for (int t = 0; t < 10; ++t) ws[threadIdx.x >> 5][t] = S[t];
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+#pragma unroll
+    for (int t = 0; t < 10; ++t) {
+      double v = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += ws[w][t];
+      S[t] = v;
+    }
+  } else if (lane != 0) {
+    return;
+  }
   const double count = S[9];
   if (mode == 1) {
     ninl[p] = (uint32_t)count;
@@ -603,18 +621,28 @@ __global__ void __launch_bounds__(256) rv_eig_kernel(const RefSeg* __restrict__ 
                     {S[5], S[7], S[8], -(S[0] + S[1] + S[2])}};
   double V[4][4];
   jacobi4(A, V);
+  // the largest eigenvalue and its column, selected with constant indices only (a dynamic
+  // index would put A and V in local memory for the whole solve)
+  double d[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) d[r] = A[r][r];
   int i0 = 0;
+  double l1 = d[0];
+#pragma unroll
   for (int r = 1; r < 4; ++r)
-    if (A[r][r] > A[i0][i0]) i0 = r;
+    if (d[r] > l1) { l1 = d[r]; i0 = r; }
   double l2 = -1e300;
+#pragma unroll
   for (int r = 0; r < 4; ++r)
-    if (r != i0 && A[r][r] > l2) l2 = A[r][r];
-  const double l1 = A[i0][i0];
+    if (r != i0 && d[r] > l2) l2 = d[r];
   if (l1 - l2 <= 1e-12 * fabs(l1)) {
     flags[p] = fl | RV_DEGENERATE | kStop;
     return;
   }
-  double v[4] = {V[0][i0], V[1][i0], V[2][i0], V[3][i0]};
+  double v[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+    v[a] = i0 == 0 ? V[a][0] : i0 == 1 ? V[a][1] : i0 == 2 ? V[a][2] : V[a][3];
   const double nv = rsqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3]);
   // hemisphere representative: q3 < 0; |q3| <= 1e-15 -> first nonzero of q0..q2 positive
   bool flip;
@@ -633,7 +661,10 @@ __global__ void __launch_bounds__(256) rv_eig_kernel(const RefSeg* __restrict__ 
 void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* qs, int32_t* flags,
                 uint32_t* ninl, int mode, cudaStream_t s) {
   if (P <= 0) return;
-  rv_eig_kernel<<<(P + 7) / 8, 256, 0, s>>>(segs, partials, qs, flags, ninl, mode, P);
+  if (P <= 148)
+    rv_eig_kernel<<<P, 256, 0, s>>>(segs, partials, qs, flags, ninl, mode, P, 1);
+  else
+    rv_eig_kernel<<<(P + 7) / 8, 256, 0, s>>>(segs, partials, qs, flags, ninl, mode, P, 0);
 }
 
 }  // namespace rv
