@@ -519,6 +519,9 @@ __global__ void cull_fill(DpList L, int32_t P, int32_t B, double eps, int mode, 
 
 // All of a small level's planning in one CTA (the four steps above, block barriers between):
 // one launch instead of four for the dive and the levels past the big one.
+#ifndef RV_PS_THREADS
+#define RV_PS_THREADS 1024
+#endif
 __global__ void __launch_bounds__(1024) cull_plan_small(
     DpList L, const int64_t* __restrict__ rows, const int64_t* __restrict__ toffs, int32_t P,
     int32_t B, int32_t B0, const int32_t* __restrict__ lut0, int64_t m0, double eps, int mode,
@@ -534,9 +537,14 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
   cull_scan_body(L, rows, toffs, P, B, eps, m0, l0cnt, k12, acnt, aoff, ioff, segs, counts, work,
                  target, max_items, err, cpi);
   __syncthreads();
-  cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi, tphi,
-                    tc_guard);
-  cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err, cpi);
+#ifndef RV_PS_ABL
+#define RV_PS_ABL 0  // tuning only: 1 skip the scatter, 2 skip the items (wrong results)
+#endif
+  if (!(RV_PS_ABL & 1))
+    cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi, tphi,
+                      tc_guard);
+  if (!(RV_PS_ABL & 2))
+    cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err, cpi);
 }
 
 // ---- K3-C ------------------------------------------------------------------------------------
@@ -1145,7 +1153,7 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
   // blocks per item: K3-C 32 (a warp's lanes); K3-CT the MMA's 128 rows (FIN: two per block)
   const int32_t cpi = cs.tphi ? (mode == RV_MODE_FINAL ? 64 : 128) : kCullMaxCells;
   if (entries_bound <= 8192 && NB <= (1 << 14)) {
-    cull_plan_small<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, B0, lut0, m0, eps, mode, guard, l0cnt,
+    cull_plan_small<<<1, RV_PS_THREADS, 0, s>>>(L, rows, toffs, P, B, B0, lut0, m0, eps, mode, guard, l0cnt,
                                        lofs, k12, cs.act, cs.acnt, cs.tanc, cs.tslot, cs.aoff,
                                        cs.ioff, cs.cidx, cs.phi, cs.tphi, cs.tc_guard, segs,
                                        cs.counts, cs.work, items, target, max_items, err, own_lo,
