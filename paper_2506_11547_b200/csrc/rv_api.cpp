@@ -268,7 +268,11 @@ struct rv_ctx {
   // lutg = level-0 lin -> group, gmem[goff[g] .. goff[g+1]) = its level-0 rows
   DevBuf<int32_t> lutg, goff, gmem;
   int64_t cull_G = 0, cull_G_grouped = 0;
-  bool cull_grouped = false;     // this solve's lists are group unions (K3-CT, one rank)
+  bool cull_grouped = false;     // this solve's lists are group unions (K3-CT)
+  // several ranks: level 0 is sliced at i-slab boundaries (a group never straddles two
+  // slices); rank r votes level-0 rows [cull_s[r], cull_s[r+1]) and owns the groups
+  // [cull_g[r], cull_g[r+1]) (those whose first member is in its slice)
+  std::vector<int64_t> cull_s, cull_g;
   DevBuf<int64_t> c_act, c_aoff, c_ioff;
   DevBuf<int32_t> c_acnt, c_tanc, c_tslot, c_cidx, c_icnt, c_work;
   DevBuf<float> c_phi;
@@ -1344,13 +1348,14 @@ int cull_prepare(rv_ctx* ctx, int32_t B0, int64_t m0, int32_t PL) {
     for (int64_t a = 0; a < m0; ++a) lut[ctx->grid_host[a]] = (int32_t)a;
     RV_CUDA(ctx->lut0.ensure(lut.size()), "allocating");
     RV_CUDA(cudaMemcpy(ctx->lut0.p, lut.data(), lut.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
-    // groups: level-0 blocks (i, j, k) with equal (i / 2, j / 2, k), numbered in row order
+    // groups: level-0 blocks (i, j, k) with equal (i, j / 2, k / 2), numbered in row order:
+    // a group lies inside one i-slab of the (lin-sorted) level-0 list
     std::vector<int32_t> lg((size_t)B0 * B0 * B0, -1), key((size_t)B0 * B0 * B0, -1);
     std::vector<std::vector<int32_t>> mem;
     for (int64_t a = 0; a < m0; ++a) {
       const int64_t lin = ctx->grid_host[a];
       const int64_t i = lin / ((int64_t)B0 * B0), j = (lin / B0) % B0, k = lin % B0;
-      const int64_t kk = ((i / 2) * B0 + j / 2) * B0 + k;
+      const int64_t kk = (i * B0 + j / 2) * B0 + k / 2;
       if (key[kk] < 0) {
         key[kk] = (int32_t)mem.size();
         mem.emplace_back();
@@ -1371,10 +1376,36 @@ int cull_prepare(rv_ctx* ctx, int32_t B0, int64_t m0, int32_t PL) {
     RV_CUDA(cudaMemcpy(ctx->gmem.p, gm.data(), gm.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
     ctx->cull_G_grouped = (int64_t)mem.size();
     ctx->lut0_B = B0;
+    ctx->cull_s.clear();  // recomputed below for this B0
   }
-  // group unions only for K3-CT on one rank (a rank's level-0 slice need not hold whole groups)
-  // (K3-CT needs them: with per-ancestor lists an item fills a quarter of its 128 rows)
-  ctx->cull_grouped = ctx->cull_tc && ctx->effective_world() == 1 && !ctx->comm;
+  {
+    const int W = ctx->effective_world();
+    if ((int64_t)ctx->cull_s.size() != W + 1) {
+      // slice boundaries at i-slab starts (the first slab start at or after r m0 / W) and
+      // the groups whose first member falls in each slice
+      ctx->cull_s.assign(W + 1, m0);
+      ctx->cull_g.assign(W + 1, ctx->cull_G_grouped);
+      auto slab = [&](int64_t a) { return (int64_t)ctx->grid_host[a] / ((int64_t)B0 * B0); };
+      ctx->cull_s[0] = 0;
+      for (int r = 1; r < W; ++r) {
+        int64_t a = std::max<int64_t>(ctx->cull_s[r - 1], (m0 * r + W - 1) / W);
+        while (a < m0 && a > 0 && slab(a) == slab(a - 1)) ++a;
+        ctx->cull_s[r] = std::min<int64_t>(a, m0);
+      }
+      std::vector<int32_t> go(ctx->cull_G_grouped + 1), gm(m0);
+      cudaMemcpy(go.data(), ctx->goff.p, go.size() * 4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(gm.data(), ctx->gmem.p, gm.size() * 4, cudaMemcpyDeviceToHost);
+      ctx->cull_g[0] = 0;
+      for (int r = 1; r <= W; ++r) {
+        int64_t g = ctx->cull_g[r - 1];
+        while (g < ctx->cull_G_grouped && gm[go[g]] < ctx->cull_s[r]) ++g;
+        ctx->cull_g[r] = g;
+      }
+    }
+  }
+  // group unions for K3-CT (with per-ancestor lists an item would fill a quarter of its 128
+  // rows); several ranks: one problem only (the sharded path), slab-aligned slices above
+  ctx->cull_grouped = ctx->cull_tc && (ctx->effective_world() == 1 || PL == 1);
   ctx->cull_G = ctx->cull_grouped ? ctx->cull_G_grouped : m0;
   RV_CUDA(ctx->c_pairs.ensure(1), "allocating");
   RV_CUDA(cudaMemsetAsync(ctx->c_pairs.p, 0, 8, ctx->stream), "memset");
@@ -1412,10 +1443,15 @@ int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
   RV_CUDA(ctx->c_lidx.ensure(total + 4), "allocating level-0 lists");
   RV_CUDA(ctx->c_fill.ensure(NB), "allocating");
   int64_t row_lo = 0, row_hi = NB;
-  if (ctx->comm && PL == 1 && ctx->cfg.world > 1) {  // this rank's level-0 slice
-    const int64_t c0 = (m0 + ctx->cfg.world - 1) / ctx->cfg.world;
-    row_lo = (int64_t)ctx->cfg.rank * c0;
-    row_hi = std::min<int64_t>(m0, row_lo + c0);
+  if (ctx->comm && PL == 1 && ctx->cfg.world > 1) {  // this rank's level-0 slice / groups
+    if (ctx->cull_grouped) {
+      row_lo = ctx->cull_g[ctx->cfg.rank];
+      row_hi = ctx->cull_g[ctx->cfg.rank + 1];
+    } else {
+      const int64_t c0 = (m0 + ctx->cfg.world - 1) / ctx->cfg.world;
+      row_lo = (int64_t)ctx->cfg.rank * c0;
+      row_hi = std::min<int64_t>(m0, row_lo + c0);
+    }
   }
   rv::launch_cull_compact(ctx->cbits.p, ctx->toffs.p, PL, m0, ctx->cull_wpc_max, ctx->c_lofs.p,
                           ctx->c_fill.p, ctx->c_lidx.p, s, row_lo, row_hi, gr);
@@ -1573,6 +1609,36 @@ int vote_level_sharded(rv_ctx* ctx, const float* x, const float* y,
   return RV_OK;
 }
 
+// Level 0 of a culled ONE-problem solve over ranks: rank r votes (with the pass bitmasks) the
+// i-slab-aligned rows [cull_s[r], cull_s[r+1]) of the shared level-0 list, so every group of
+// the rank's culled levels has all its members' bitmasks here; one in-place ncclAllReduce(sum)
+// assembles the counts (the slices are disjoint and the array was zeroed).  Loopback: every
+// rank's slice in turn.
+int vote_level0_slabs(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
+                      const std::vector<int64_t>& koff, double eps, int32_t B0, const rv::DpList& Ld,
+                      int64_t m0, int64_t nmax) {
+  cudaStream_t s = ctx->stream;
+  const bool nccl_path = ctx->comm != nullptr;
+  const int W = ctx->effective_world();
+  const int r_lo = nccl_path ? ctx->cfg.rank : 0, r_hi = nccl_path ? r_lo + 1 : W;
+  RV_CUDA(ctx->dp_sbase.ensure(2), "allocating");
+  RV_CUDA(ctx->dp_scnt.ensure(1), "allocating");
+  for (int r = r_lo; r < r_hi; ++r) {
+    const int64_t r0 = ctx->cull_s[r], len = ctx->cull_s[r + 1] - r0;
+    if (len <= 0) continue;
+    rv::dp_launch_slice(nullptr, Ld.cnt, Ld.shared_m, r0, len, ctx->dp_sbase.p, ctx->dp_scnt.p, s);
+    ctx->launches += 1;
+    const rv::DpList Ls{Ld.lins, 0, 0, ctx->dp_sbase.p, ctx->dp_scnt.p, Ld.ca, Ld.cb};
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, Ls, 1, len, nmax, true))
+      return rc;
+  }
+  if (nccl_path) {
+    ncclResult_t nr = nccl().AllReduce(Ld.ca, Ld.ca, (size_t)m0, ncclUint32, ncclSum, ctx->comm, s);
+    if (nr != ncclSuccess) return ctx->fail(RV_ENCCL, "ncclAllReduce: %s", nccl().GetErrorString(nr));
+  }
+  return RV_OK;
+}
+
 // A culled level of a ONE-problem list over ranks: rank r votes the blocks whose level-0
 // ancestor is one of the rows it voted (and compacted) at level 0, [r c0, (r+1) c0); the other
 // blocks' counts stay zero and one in-place ncclAllReduce(sum) per count array assembles the
@@ -1583,10 +1649,15 @@ int vote_level_owned(rv_ctx* ctx, const float* x, const float* y, const std::vec
   const bool nccl_path = ctx->comm != nullptr;
   const int W = ctx->effective_world();
   const int r_lo = nccl_path ? ctx->cfg.rank : 0, r_hi = nccl_path ? r_lo + 1 : W;
-  const int64_t c0 = (ctx->cull_G + W - 1) / W;  // (ungrouped when W > 1: G = m0)
+  const int64_t c0 = (ctx->cull_G + W - 1) / W;
   for (int r = r_lo; r < r_hi; ++r) {
-    ctx->cull_own_lo = (int64_t)r * c0;
-    ctx->cull_own_hi = std::min<int64_t>(ctx->cull_G, (int64_t)(r + 1) * c0);
+    if (ctx->cull_grouped) {  // the groups whose members this rank voted at level 0
+      ctx->cull_own_lo = ctx->cull_g[r];
+      ctx->cull_own_hi = ctx->cull_g[r + 1];
+    } else {
+      ctx->cull_own_lo = (int64_t)r * c0;
+      ctx->cull_own_hi = std::min<int64_t>(ctx->cull_G, (int64_t)(r + 1) * c0);
+    }
     int rc = vote_level(ctx, x, y, rows, koff, eps, mode, B, Ld, 1, entries, nmax);
     ctx->cull_own_lo = 0;
     ctx->cull_own_hi = INT64_MAX;
@@ -1684,7 +1755,9 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   if (cull) {
     RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, ((size_t)PL * m0 + slack) * 4, s), "memset");
     const rv::DpList l0{ctx->grid_list.p, 1, m0, nullptr, nullptr, ctx->l0cnt.p, ctx->l0cnt.p};
-    if (shard) {  // each rank votes (and later compacts) its slice of level 0
+    if (shard && ctx->cull_grouped) {  // slab-aligned slices (whole groups per rank)
+      if (int rc = vote_level0_slabs(ctx, x, y, rows, koff, eps, B0, l0, m0, nmax)) return rc;
+    } else if (shard) {  // each rank votes (and later compacts) its slice of level 0
       if (int rc = vote_level_sharded(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0,
                                       (m0 + W - 1) / W, nmax, true))
         return rc;

@@ -222,35 +222,33 @@ def test_culled_batched_matches_oracle(rvc, torch_cuda):
 
 
 def test_culled_loopback_shards(torch_cuda):
-    """emulate_world: level 0 voted whole (every rank holds every ancestor's list), finer
-    levels sliced over the emulated ranks -- the same result as one rank.  Several ranks vote
-    the culled levels on K3-C (a rank's level-0 slice need not hold whole K3-CT groups), so the
-    search path is compared against one rank on K3-C, and the one-rank K3-CT solve (whose
-    bounds differ inside the guard band) must reach the same answer."""
+    """emulate_world: level 0 sliced over the emulated ranks with its bitmasks (K3-CT: slices
+    at i-slab boundaries, so a rank holds every member of the ancestor groups it owns; K3-C:
+    uniform slices), finer levels voted by the owning rank -- the same result and per-phase
+    block counts as one rank, on both culled vote paths; the two paths reach the same answer."""
     torch = torch_cuda
     for pr in (datagen.cfg2(seed=5), datagen.make_problem(40_000, 400, 0.01, 0.05, seed=8)):
         x, y = dev(torch, pr.x), dev(torch, pr.y)
-        ref = None
-        for W in (1, 2, 3, 8):
-            ctx = _ctx("fp32", max_n=1 << 17, emulate_world=W)
-            try:
-                r = ctx.solve(x, y, pr.eps)
-            finally:
-                ctx.close()
-            if ref is None:
-                ref = r
-                o = oracle.solve(pr.x, pr.y, pr.eps)
-                assert (r.cell, r.votes, r.n_tied) == (o.cell, o.votes, o.n_tied)
-            assert (r.cell, r.votes, r.n_tied, r.n_inliers) == (ref.cell, ref.votes, ref.n_tied,
-                                                                ref.n_inliers), W
-            assert np.array_equal(r.q, ref.q), W
-            assert r.cells_per_phase == ref.cells_per_phase, W
-        ctx = _ctx("tc", max_n=1 << 17)
-        try:
-            r = ctx.solve(x, y, pr.eps)
-        finally:
-            ctx.close()
-        assert r.cull_tc_launches > 0
-        assert (r.cell, r.votes, r.n_tied, r.n_inliers) == (ref.cell, ref.votes, ref.n_tied,
-                                                            ref.n_inliers)
-        assert oracle.rotation_angle_between(r.q, ref.q) < 1e-9
+        o = oracle.solve(pr.x, pr.y, pr.eps)
+        refs = {}
+        for path in ("tc", "fp32"):
+            ref = None
+            for W in (1, 2, 3, 8):
+                ctx = _ctx(path, max_n=1 << 17, emulate_world=W)
+                try:
+                    r = ctx.solve(x, y, pr.eps)
+                finally:
+                    ctx.close()
+                if path == "tc":
+                    assert r.cull_tc_launches > 0, W
+                if ref is None:
+                    ref = r
+                    assert (r.cell, r.votes, r.n_tied) == (o.cell, o.votes, o.n_tied)
+                assert (r.cell, r.votes, r.n_tied, r.n_inliers) == (ref.cell, ref.votes,
+                                                                    ref.n_tied, ref.n_inliers), W
+                assert np.array_equal(r.q, ref.q), W
+                assert r.cells_per_phase == ref.cells_per_phase, (path, W)
+            refs[path] = ref
+        a, b = refs["tc"], refs["fp32"]
+        assert (a.cell, a.votes, a.n_tied, a.n_inliers) == (b.cell, b.votes, b.n_tied, b.n_inliers)
+        assert oracle.rotation_angle_between(a.q, b.q) < 1e-9
