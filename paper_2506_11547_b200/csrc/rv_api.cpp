@@ -269,8 +269,8 @@ struct rv_ctx {
   DevBuf<int32_t> lutg, goff, gmem;
   int64_t cull_G = 0, cull_G_grouped = 0;
   bool cull_grouped = false;     // this solve's lists are group unions (K3-CT)
-  // several ranks: level 0 is sliced at i-slab boundaries (a group never straddles two
-  // slices); rank r votes level-0 rows [cull_s[r], cull_s[r+1]) and owns the groups
+  // several ranks: level 0 is sliced at (i, j/2) row-pair boundaries (a group never straddles
+  // two slices); rank r votes level-0 rows [cull_s[r], cull_s[r+1]) and owns the groups
   // [cull_g[r], cull_g[r+1]) (those whose first member is in its slice)
   std::vector<int64_t> cull_s, cull_g;
   DevBuf<int64_t> c_act, c_aoff, c_ioff;
@@ -1381,11 +1381,15 @@ int cull_prepare(rv_ctx* ctx, int32_t B0, int64_t m0, int32_t PL) {
   {
     const int W = ctx->effective_world();
     if ((int64_t)ctx->cull_s.size() != W + 1) {
-      // slice boundaries at i-slab starts (the first slab start at or after r m0 / W) and
-      // the groups whose first member falls in each slice
+      // slice boundaries where a new (i, j / 2) row pair starts (no group straddles one: a
+      // group's members are (i, j..j+1, k..k+1), j even) -- the first at or after r m0 / W --
+      // and the groups whose first member falls in each slice
       ctx->cull_s.assign(W + 1, m0);
       ctx->cull_g.assign(W + 1, ctx->cull_G_grouped);
-      auto slab = [&](int64_t a) { return (int64_t)ctx->grid_host[a] / ((int64_t)B0 * B0); };
+      auto slab = [&](int64_t a) {
+        const int64_t lin = ctx->grid_host[a], i = lin / ((int64_t)B0 * B0), j = (lin / B0) % B0;
+        return i * B0 + j / 2;
+      };
       ctx->cull_s[0] = 0;
       for (int r = 1; r < W; ++r) {
         int64_t a = std::max<int64_t>(ctx->cull_s[r - 1], (m0 * r + W - 1) / W);
