@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--levels", type=int, default=0)
+    ap.add_argument("--chain", default="15,45,180,360",
+                    help="nested resolution chain of the certified search (result chain-independent; "
+                         "with culling 15,45,180,360 measured fastest, profiles/r01_chain_sweep_cull.log)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -331,8 +334,10 @@ def run_ours(args):
     world, rank, local, nccl_id = _dist_setup(args)
     pr = datagen.cfg4()
     stream = torch.cuda.current_stream()
+    chain = tuple(int(c) for c in args.chain.split(","))
     rv = RotVote(device=local, max_n=pr.n, rank=rank, world=world, nccl_id=nccl_id,
-                 stream=stream, tensor_vote=(args.vote == "tc"), cull=(args.cull == "on"))
+                 stream=stream, tensor_vote=(args.vote == "tc"), cull=(args.cull == "on"),
+                 chain=chain)
     x = torch.from_numpy(pr.x).cuda()
     y = torch.from_numpy(pr.y).cuda()
     mask = torch.zeros((pr.n + 31) // 32, dtype=torch.int32, device="cuda")
@@ -400,9 +405,10 @@ def run_ours(args):
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
         "dtype": "f16x3-split/f32" if args.vote == "tc" else "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "levels": args.levels or 5,
+        "config": {"workload": WORKLOAD, "levels": args.levels or min(5, len(chain)),
                    "vote_path": args.vote + ("+cull" if cull_ms > 0 else ""),
-                   "chain": [15, 45, 90, 180, 360], "l2": "flushed between steps (512 MB write)",
+                   "chain": list(chain[-(args.levels or min(5, len(chain))):]),
+                   "l2": "flushed between steps (512 MB write)",
                    "parallelism": f"cells sharded over {world} GPU(s)" if world > 1 else "1 GPU",
                    "pair_votes_per_solve": pair_votes, "cells_per_phase": res.cells_per_phase,
                    "value_counts": "corr x cell pairs the certified search decides per second "
