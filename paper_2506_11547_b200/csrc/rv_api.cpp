@@ -566,12 +566,14 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
     std::memcpy(ht, toff.data(), (P + 1) * sizeof(int64_t));
     RV_CUDA(cudaMemcpyAsync(ctx->toffs.p, ht, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
             "copying offsets");
-    if (ctx->cull_on) RV_CUDA(ctx->k12.ensure((size_t)(toff[P] + 8) * 12), "allocating K3-C rows");
-    if (ctx->cull_on && ctx->cull_tc)
-      RV_CUDA(ctx->tctab_rm.ensure((size_t)(toff[P] + 8) * 64), "allocating K3-CT rows");
+    // the culled levels' rows: K3-CT's fp16-split row-major copy, or K3-C's fp32 rows (the
+    // culled path cull_prepare will pick: K3-CT unless RV_CULL_TC=0 or a multi-rank batch)
+    const bool ct = ctx->cull_on && ctx->cull_tc && (ctx->effective_world() == 1 || P == 1);
+    const bool k3c = ctx->cull_on && !ct;
+    if (k3c) RV_CUDA(ctx->k12.ensure((size_t)(toff[P] + 8) * 12), "allocating K3-C rows");
+    if (ct) RV_CUDA(ctx->tctab_rm.ensure((size_t)(toff[P] + 8) * 64), "allocating K3-CT rows");
     rv::launch_setup_tc(x, y, ctx->rows.p, ctx->toffs.p, P, toff[P] + 8, ctx->tctab.p, ctx->stream,
-                        ctx->cull_on ? ctx->k12.p : nullptr,
-                        ctx->cull_on && ctx->cull_tc ? ctx->tctab_rm.p : nullptr);
+                        k3c ? ctx->k12.p : nullptr, ct ? ctx->tctab_rm.p : nullptr);
     ctx->launches += 1;
     ctx->tc_toff = toff;
   }
