@@ -519,6 +519,9 @@ __global__ void cull_fill(DpList L, int32_t P, int32_t B, double eps, int mode, 
 
 // All of a small level's planning in one CTA (the four steps above, block barriers between):
 // one launch instead of four for the dive and the levels past the big one.
+#ifndef RV_PS_TIMING
+#define RV_PS_TIMING 0  // tuning only: print the one-CTA planner's phase cycles
+#endif
 #ifndef RV_PS_THREADS
 #define RV_PS_THREADS 1024
 #endif
@@ -530,13 +533,28 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
     int64_t* ioff, int32_t* cidx, float* phi, uint8_t* tphi, float tc_guard, VoteSeg* segs,
     int32_t* counts, int32_t* work, CullItem* items, int64_t target, int64_t max_items,
     int32_t* err, int64_t own_lo, int64_t own_hi, int32_t cpi) {
+#if RV_PS_TIMING
+  long long t0 = clock64();
+#endif
   cull_act_body(L, P, act, acnt, (int64_t)P * m0);
   __syncthreads();
+#if RV_PS_TIMING
+  long long t1 = clock64();
+#endif
   cull_count_body(L, P, B, B0, lut0, m0, act, acnt, tanc, tslot, err, own_lo, own_hi);
   __syncthreads();
+#if RV_PS_TIMING
+  long long t2 = clock64();
+#endif
   cull_scan_body(L, rows, toffs, P, B, eps, m0, l0cnt, k12, acnt, aoff, ioff, segs, counts, work,
                  target, max_items, err, cpi);
   __syncthreads();
+#if RV_PS_TIMING
+  long long t3 = clock64();
+  if (threadIdx.x == 0)
+    printf("plan_small cycles: act %lld count %lld scan %lld (NB %lld, T %lld)\n", t1 - t0, t2 - t1,
+           t3 - t2, (long long)P * m0, (long long)act[P]);
+#endif
 #ifndef RV_PS_ABL
 #define RV_PS_ABL 0  // tuning only: 1 skip the scatter, 2 skip the items (wrong results)
 #endif
