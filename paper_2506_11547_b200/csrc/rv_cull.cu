@@ -1,5 +1,6 @@
-// rv_cull.cu -- K3-C: the vote of a level's blocks against their level-0 ancestor's
-// correspondences only ("ancestor culling"), and its device item planner.
+// rv_cull.cu -- the culled vote: a level's blocks voted against their level-0 ancestor
+// group's correspondences only ("ancestor culling"), on the tensor cores (K3-CT,
+// default) or the FP32 pipe (K3-C), and its device item planner.
 //
 // Why it is exact.  Level 0 (resolution B0) is voted by K3-TC against every correspondence; its
 // epilogue also writes, per level-0 block a, the bitmask L(a) of the correspondences that
@@ -11,25 +12,28 @@
 // hence every i with exact s_i(q_c) >= cos(eps + r(c)) (the bound level's true count) or
 // s_i(q_c) >= cos(eps) (the final level's) has exact s_i(q_a) >= cos(eps + r(a)) and is in L(a)
 // (the TC error 1.3e-5 < g' = g + 1.5e-5).  Correspondences outside L(a) therefore never vote for
-// c, and counting c over L(a) only, with the FP32 path's arithmetic and guard, gives
-//     cnt(c) = #{i in L(a) : s32_i(q_c) >= t_c - g}
+// c, and counting c over any superset U of L(a) (K3-CT: the union over the ancestor's group of
+// 1 x 2 x 2 level-0 blocks; K3-C: L(a) itself) with the guarded test gives
+//     cnt(c) = #{i in U : s_i(q_c) >= t_c - g}
 // which still contains every true voter (upper bounds stay certified, cnt_b <= exact <= cnt_a
-// at the final level) and differs from the unculled FP32 count only by pairs inside the guard
+// at the final level) and differs from the unculled count only by pairs inside the guard
 // band -- the parity rule of SURVEY §8(c).
 //
 // Pipeline (all on the device; the host reads one total):
 //   K3-TC BITS   level 0 votes every correspondence and writes the pass bitmask of each block;
-//   cull_rows    row offsets (exclusive prefix of the level-0 counts, padded to multiples of 4);
-//   cull_compact the bitmasks -> per-block index lists L(a), ascending (one warp per row);
+//   cull_rows    row offsets (exclusive prefix of the lists' length bounds, padded to 4);
+//   cull_compact the bitmasks (OR over a group's members) -> index lists, one warp per row segment;
 //   per culled level: cull_act / cull_count / cull_scan / cull_scatter / cull_items bucket the
-//   level's blocks by (problem, ancestor), write each block's phi(q_c) and threshold once, and
-//   cut items of <= 32 blocks x a range of their ancestor's list (~8 items per resident warp);
+//   level's blocks by (problem, list row), write each block's K3-CT fp16-split row (or K3-C's
+//   phi(q_c) and threshold) once, and cut items of <= 128 (K3-C: 32) blocks x a range of the
+//   row's list;
+//   K3-CT        tcgen05 MMA of an item's block rows against 256-entry stages of gathered
+//                correspondence rows, sign counts from TMEM (see its kernel);
 //   K3-C         one warp per item: 128-entry stages of K rows gathered by cp.async (double
-//                buffered) into shared memory; lane (quad q, group h) votes blocks 4q..4q+3
-//                (phi as FFMA2 register pairs) against entries h, h+4, ... of the stage (3
-//                LDS.128 per entry, 18 FFMA2 for 4 pairs; threshold folded into the chain's
-//                initial value and K3's operation order, so s32 is bit-identical); counts are
-//                sign bits, one atomicAdd per (block, item).
+//                buffered) into shared memory; lanes hold octets of blocks (phi as FFMA2 register
+//                pairs) against the stage's entries (threshold folded into the chain's initial
+//                value and K3's operation order, so s32 is bit-identical); counts are sign bits,
+//                one atomicAdd per (block, item).
 #include <cstdint>
 #include <cstdio>
 #include <cuda_fp16.h>
