@@ -86,9 +86,11 @@ typedef struct {
                             operands, fp32 accumulation); 0: FP32-pipe FFMA2 vote everywhere */
   int32_t cull;          /* 1 (needs tensor_vote): ancestor culling -- level 0 writes each block's
                             pass bitmask, every finer level votes its blocks only against the
-                            correspondences that passed their level-0 ancestor's bound test
-                            (K3-C; the certified argument is in DESIGN.md §6).  Same result; applies
-                            to the device level loop when the bitmasks fit (<= 4 GiB).  0: off */
+                            correspondences that passed the bound test of a level-0 block of
+                            their ancestor's group (K3-CT on the tensor cores; K3-C on the FP32
+                            pipe with the environment RV_CULL_TC=0; the certified argument is in
+                            DESIGN.md §5).  Same result; applies to the device level loop when
+                            the bitmasks fit (<= 4 GiB).  0: off */
 } rv_config;
 
 typedef struct {
@@ -204,14 +206,16 @@ int rot_vote_count_cells(rv_ctx* ctx, const float* x, const float* y, int64_t n,
  * BOUND_TC/FINAL_TC: K3-TC).  The solve with tensor_vote = 1 sends its bound and final levels
  * to K3-TC: the planner only needs cnt_b <= exact <= cnt_a, which the wider band keeps. */
 
-/* Ancestor culling (K3-C), for parity tests: vote the full level-0 grid at
- * resolution B0 with K3-TC (bound mode) writing the pass bitmasks, then count the m blocks
+/* Ancestor culling (K3-CT / K3-C), for parity tests: vote the full level-0 grid
+ * at resolution B0 with K3-TC (bound mode) writing the pass bitmasks, then count the m blocks
  * `lins` (resolution B, B % B0 == 0, any order) against their level-0 ancestors'
- * correspondences only:
- *   BOUND: cnt_a = #{i in L(anc) : s32_i(q_c) >= cos(min(pi, eps + r(c))) - guard}
- *   FINAL: cnt_a / cnt_b at cos(eps) -/+ guard (as RV_MODE_FINAL), over L(anc)
- * with L(a) = {i : s_tc_i(q_a) >= cos(min(pi, eps + r(a))) - guard - 1.5e-5}.  Every exact voter
- * of a block is in L(anc), so the counts stay within the guard band of the exact ones.
+ * correspondences only (K3-CT: the union U over the ancestor's group; K3-C: L(anc)):
+ *   BOUND: cnt_a = #{i in U : s_i(q_c) >= cos(min(pi, eps + r(c))) - guard'}
+ *   FINAL: cnt_a / cnt_b at cos(eps) -/+ guard' (as RV_MODE_FINAL), over U
+ * with L(a) = {i : s_tc_i(q_a) >= cos(min(pi, eps + r(a))) - guard - 1.5e-5}; guard' = the
+ * vote's own guard (K3-CT: guard + 1.5e-5, fp16-split scores; K3-C: guard, FP32 scores).
+ * Every exact voter of a block is in L(anc) ⊆ U, so the counts stay within the guard band of
+ * the exact ones.
  * bits_out: DEVICE uint32[m0][ceil(n/256)*8] copy of the level-0 bitmasks (row = the block's
  * index in the ascending candidate list of B0, bit i%32 of word i/32 = i in L), or NULL.
  * Needs tensor_vote = 1 and cull = 1; 1 <= B0 <= 90. */
