@@ -252,3 +252,25 @@ def test_culled_loopback_shards(torch_cuda):
         a, b = refs["tc"], refs["fp32"]
         assert (a.cell, a.votes, a.n_tied, a.n_inliers) == (b.cell, b.votes, b.n_tied, b.n_inliers)
         assert oracle.rotation_angle_between(a.q, b.q) < 1e-9
+
+
+def test_culled_chains_agree(torch_cuda):
+    """The certified result does not depend on the resolution chain: the bench's chain
+    15-45-180-360 and the library's default 15-45-90-180-360 give the oracle's answer on the
+    culled tensor-core path."""
+    from paper_2506_11547_b200 import RotVote
+    torch = torch_cuda
+    pr = datagen.make_problem(60_000, 600, 0.01, 0.05, seed=11)
+    x, y = dev(torch, pr.x), dev(torch, pr.y)
+    o = oracle.solve(pr.x, pr.y, pr.eps)
+    res = []
+    for chain in ((15, 45, 180, 360), None):
+        ctx = RotVote(max_n=1 << 17, chain=chain) if chain else RotVote(max_n=1 << 17)
+        try:
+            r = ctx.solve(x, y, pr.eps, levels=len(chain) if chain else 0)
+        finally:
+            ctx.close()
+        assert r.cull_tc_launches > 0
+        assert (r.cell, r.votes, r.n_tied) == (o.cell, o.votes, o.n_tied), chain
+        res.append(r)
+    assert np.array_equal(res[0].q, res[1].q)
