@@ -79,3 +79,34 @@ def test_full_oracle_search_agrees(setup):
     ref = oracle.solve(pr.x, pr.y, pr.eps)
     assert (res.cell, res.votes, res.n_tied) == (ref.cell, ref.votes, ref.n_tied)
     assert oracle.rotation_angle_between(res.q, ref.q) < 1e-4
+
+
+def test_culled_vote_full_size(setup):
+    """The default culled vote (K3-CT over the level-0 ancestor-group lists, the launch
+    configuration the bench times) at cfg4's full size: sampled B = 45 blocks (the dominant
+    level) and the 3x3x3 B = 360 blocks around the winner, every count inside the guard band of
+    the oracle's fp64 count; cnt_b <= exact <= cnt_a at the final level."""
+    from paper_2506_11547_b200 import RV_MODE_BOUND, RV_MODE_FINAL
+    pr, rv, x, y, res = setup
+    g = GUARD + 1.5e-5  # K3-CT's guard (K3-TC's: the fp16-split error margin added)
+    rng = np.random.default_rng(4)
+
+    def in_band(got, B, lins, thr):
+        ge, near = oracle.count_cells(pr.x, pr.y, B, lins, thr, BAND)
+        ge, near, got = ge.astype(np.int64), near.astype(np.int64), np.asarray(got, np.int64)
+        return (got >= ge - near) & (got <= ge + near)
+
+    lins = rng.choice(oracle.candidates(45), 24, replace=False).astype(np.uint32)
+    i, j, k = res.cell
+    lins = np.concatenate([lins, [oracle.lin_of(45, i // 8, j // 8, k // 8)]]).astype(np.uint32)
+    got = rv.count_cells_culled(x, y, 15, 45, lins, pr.eps, RV_MODE_BOUND)
+    thr = np.array([oracle.cell_bound_threshold(45, int(l), pr.eps) - g for l in lins])
+    assert np.all(in_band(got, 45, lins, thr))
+    near = np.array(sorted({oracle.lin_of(360, i + a, j + b, k + c) for a in (-1, 0, 1)
+                            for b in (-1, 0, 1) for c in (-1, 0, 1)}), np.uint32)
+    ga, gb = rv.count_cells_culled(x, y, 15, 360, near, pr.eps, RV_MODE_FINAL)
+    tau = math.cos(pr.eps)
+    assert np.all(in_band(ga, 360, near, tau - g)) and np.all(in_band(gb, 360, near, tau + g))
+    ex, _ = oracle.count_cells(pr.x, pr.y, 360, near, tau, 0.0)
+    assert np.all(gb <= ex) and np.all(ex <= ga)
+    assert ga.max() >= res.votes >= gb.max()
