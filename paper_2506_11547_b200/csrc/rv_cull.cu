@@ -853,7 +853,12 @@ constexpr int kCtN = 256;                            // gathered entries per sta
 #endif
 constexpr int kCtEpq = RV_CT_EPQ;
 constexpr int kCtEpi0 = kCtProd + 1;                 // first epilogue warp
-constexpr int kCtThreads = (kCtProd + 1 + 4 * kCtEpq) * 32;
+#ifndef RV_CT_DYN
+#define RV_CT_DYN 1  // items handed out dynamically (a scheduler warp + a work counter)
+#endif
+constexpr int kCtIR = 8;  // item ring (dynamic scheduling)
+constexpr int kCtSched = kCtEpi0 + 4 * kCtEpq;  // the scheduler warp
+constexpr int kCtThreads = (kCtProd + 1 + 4 * kCtEpq + RV_CT_DYN) * 32;
 #ifndef RV_CT_ITEMS_PER_SM
 #define RV_CT_ITEMS_PER_SM 32  // K3-CT planner target (items per CTA)
 #endif
@@ -862,6 +867,8 @@ struct CtSmem {
   uint8_t b[kCtStages][kCtN * 64];  // gathered correspondence rows (B operand)
   uint8_t a[2][128 * 64];           // the item's block rows (A operand), double-buffered
   uint64_t full[kCtStages], empty[kCtStages], afull[2], aempty[2], tfull[2], tempty[2];
+  uint64_t ifull[kCtIR], iempty[kCtIR];
+  int32_t iring[kCtIR];
   uint32_t tmem_base;
 };
 
@@ -897,7 +904,7 @@ __global__ void __launch_bounds__(kCtThreads)
                            const int32_t* __restrict__ counts_dev, const uint8_t* __restrict__ tab,
                            int64_t pad_row, const uint8_t* __restrict__ tphi,
                            const int32_t* __restrict__ cidx, const uint32_t* __restrict__ lidx,
-                           unsigned long long* pairs) {
+                           unsigned long long* pairs, int32_t* work) {
   using namespace tcx;
   extern __shared__ __align__(1024) uint8_t ct_raw[];
   CtSmem& sm = *reinterpret_cast<CtSmem*>((reinterpret_cast<uintptr_t>(ct_raw) + 1023) & ~(uintptr_t)1023);
@@ -920,18 +927,50 @@ __global__ void __launch_bounds__(kCtThreads)
       bar_init(&sm.tfull[i], 1);
       bar_init(&sm.tempty[i], 4 * kCtEpq);  // every epilogue warp
     }
+    for (int i = 0; i < kCtIR; ++i) {
+      bar_init(&sm.ifull[i], 1);                         // the scheduler
+      bar_init(&sm.iempty[i], kCtProd + 1 + 4 * kCtEpq);  // every consuming warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  // the item sequence every role walks: static (b, b + grid, ...) or, RV_CT_DYN, the scheduler
+  // warp's atomically fetched indices through a ring (each consuming warp reads a slot, then
+  // one lane releases it); -1 ends the sequence
+  uint32_t kq = 0;
+  int sidx = (int)blockIdx.x - (int)gridDim.x;
+  // dynamic only for big levels (many items per CTA): small levels keep the static order
+  const bool dyn = RV_CT_DYN && n_items >= 8 * (int)gridDim.x;
+  auto next_item = [&](bool warp_wide) -> int {
+#if RV_CT_DYN
+    if (!dyn) {
+      sidx += (int)gridDim.x;
+      return sidx < n_items ? sidx : -1;
+    }
+    const uint32_t slot = kq % kCtIR;
+    ct_wait(&sm.ifull[slot], (kq / kCtIR) & 1);
+    const int idx = *reinterpret_cast<volatile int32_t*>(&sm.iring[slot]);
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || lane == 0) bar_arrive(&sm.iempty[slot]);
+    ++kq;
+    return idx;
+#else
+    (void)warp_wide;
+    sidx += (int)gridDim.x;
+    return sidx < n_items ? sidx : -1;
+#endif
+  };
 
   if (warp < kCtProd) {
     // ---------------- gather ----------------
     const int pw = warp;
     uint32_t gs = 0, gi = 0;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
+    for (;; ++gi) {
+      const int idx = next_item(true);
+      if (idx < 0) break;
       const CullItem it = items[idx];
       const int64_t toff = segs[it.seg].koff;
       if (pw == 0 && lane == 0) {  // the item's 128 block rows (rows past its blocks: ignored)
@@ -993,7 +1032,9 @@ __global__ void __launch_bounds__(kCtThreads)
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       uint32_t gs = 0, gi = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
+      for (;; ++gi) {
+        const int idx = next_item(false);
+        if (idx < 0) break;
         const int ns = (items[idx].ne + kCtN - 1) / kCtN;
         const uint32_t ab = gi & 1;
         bar_wait(&sm.afull[ab], (gi >> 1) & 1);
@@ -1018,7 +1059,7 @@ __global__ void __launch_bounds__(kCtThreads)
         mma_commit(&sm.aempty[ab]);
       }
     }
-  } else {
+  } else if (warp < kCtSched) {
     // ---------------- epilogue (4 kCtEpq warps: lane quarter warp % 4, a column slice each) ---
     const int ew = warp - kCtEpi0, slice = ew >> 2;
     constexpr int kCols = kCtN / kCtEpq;  // columns of a stage per warp
@@ -1026,7 +1067,9 @@ __global__ void __launch_bounds__(kCtThreads)
         tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(slice * kCols);
     const int m = 32 * (warp & 3) + lane;  // TMEM lane = A row = block row of the item
     uint32_t gs = 0;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    for (;;) {
+      const int idx = next_item(true);
+      if (idx < 0) break;
       const CullItem it = items[idx];
       const int ns = (it.ne + kCtN - 1) / kCtN;
       const int nrows = FIN ? 2 * it.ncell : it.ncell;
@@ -1079,6 +1122,20 @@ __global__ void __launch_bounds__(kCtThreads)
         atomicAdd(pairs, (unsigned long long)it.ne * (unsigned long long)it.ncell);
     }
   }
+#if RV_CT_DYN
+  else if (lane == 0 && dyn) {
+    // ---------------- scheduler: the next item index per ring slot (-1: done) ----------------
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t slot = k % kCtIR;
+      if (k >= (uint32_t)kCtIR) ct_wait(&sm.iempty[slot], ((k / kCtIR) - 1) & 1);
+      int idx = atomicAdd(work, 1);
+      if (idx >= n_items) idx = -1;
+      *reinterpret_cast<volatile int32_t*>(&sm.iring[slot]) = idx;
+      bar_arrive(&sm.ifull[slot]);
+      if (idx < 0) break;
+    }
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == kCtProd) {
@@ -1110,7 +1167,8 @@ void launch_cull_t(const VoteSeg* segs, const CullItem* items, const int32_t* co
 void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
                          const int32_t* counts_dev, const uint8_t* tab, int64_t pad_row,
                          const uint8_t* tphi, const int32_t* cidx, const uint32_t* lidx,
-                         unsigned long long* pairs, int num_sms, cudaStream_t s) {
+                         unsigned long long* pairs, int num_sms, cudaStream_t s,
+                         int32_t* work) {
   static bool attr = false;
   const size_t b0 = sizeof(CtSmem) + 1024, b1 = b0;
   if (!attr) {
@@ -1122,10 +1180,10 @@ void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
   }
   if (mode == RV_MODE_FINAL)
     rv_vote_cull_tc_kernel<true><<<num_sms, kCtThreads, b1, s>>>(segs, items, counts_dev, tab, pad_row,
-                                                                tphi, cidx, lidx, pairs);
+                                                                tphi, cidx, lidx, pairs, work);
   else
     rv_vote_cull_tc_kernel<false><<<num_sms, kCtThreads, b0, s>>>(segs, items, counts_dev, tab, pad_row,
-                                                                 tphi, cidx, lidx, pairs);
+                                                                 tphi, cidx, lidx, pairs, work);
 }
 
 void launch_vote_cull(int mode, const VoteSeg* segs, const CullItem* items,
