@@ -824,7 +824,9 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
 // loads the A rows), kCtProd issues the MMAs, then 8 epilogue warps: two per TMEM lane quarter
 // (= 32 block rows), taking alternate stages, each thread counting the sign bits of its block
 // row over the stage's 256 columns (tcgen05.ld.32x32b.x32, half on the ALU, half as IMAD.HI).
-// Warps whose 32 rows are all past the item's blocks skip the reads.  Padding correspondences
+// Warps whose 32 rows are all past the item's blocks skip the reads.  Big levels (>= 8 items per
+// CTA) take their items dynamically: a scheduler warp fetches indices from the planner's work
+// counter into a ring every role reads.  Padding correspondences
 // gather the table's padding row (score -1: never counted).  Error bound and guard: K3-TC's.
 #ifndef RV_CT_ABL
 #define RV_CT_ABL 0  // tuning only: 1 no gather copies, 2 no MMAs, 4 no TMEM reads, 8 no index
