@@ -87,10 +87,13 @@ typedef struct {
   int32_t cull;          /* 1 (needs tensor_vote): ancestor culling -- level 0 writes each block's
                             pass bitmask, every finer level votes its blocks only against the
                             correspondences that passed the bound test of a level-0 block of
-                            their ancestor's group (K3-CT on the tensor cores; K3-C on the FP32
-                            pipe with the environment RV_CULL_TC=0; the certified argument is in
+                            their ancestor's group (K3-CT on the tensor cores; 2: K3-C on the
+                            FP32 pipe over per-ancestor lists; the certified argument is in
                             DESIGN.md §5).  Same result; applies to the device level loop when
-                            the bitmasks fit (<= 4 GiB).  0: off */
+                            the bitmasks fit (<= 4 GiB).  0: off.  Other values -> RV_EINVAL. */
+  int32_t planner;       /* 0: the level loop runs on the device (default); 1: the host planner
+                            (rv_plan.cpp) drives every level -- the reference the GPU tests compare
+                            the device loop against.  Same result.  Other values -> RV_EINVAL. */
 } rv_config;
 
 typedef struct {

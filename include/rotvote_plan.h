@@ -89,6 +89,23 @@ void rv_shard_range(int64_t m, int32_t rank, int32_t world, int64_t* begin, int6
  * index; writes min(count, cap) entries to out (may be NULL) and returns the count. */
 int64_t rv_grid_candidates(int32_t B, uint32_t* out, int64_t cap);
 
+/* Ancestor groups of a culled solve: the level-0 blocks of the B0 grid (rows in
+ * rv_grid_candidates(B0) order, m0 of them) with equal (i / gi, j / gj, k / gk) form a group,
+ * numbered by first appearance in row order; a group's list is the union of its members'.
+ * Writes (each may be NULL) group_of[m0] (row -> group), goff[G + 1] and gmem[m0] (the rows of
+ * group g, ascending, are gmem[goff[g] .. goff[g+1])).  Returns G, or -1 for B0 outside
+ * [1, 1625] or a group extent < 1. */
+int64_t rv_cull_groups(int32_t B0, int32_t gi, int32_t gj, int32_t gk, int32_t* group_of,
+                       int32_t* goff, int32_t* gmem);
+/* The multi-rank partition of one culled problem: slice[world + 1] = level-0
+ * row boundaries (rank r votes rows slice[r] .. slice[r+1] with their pass bitmasks), each cut at
+ * the first row at or after ceil(m0 r / world) where a new run of whole groups starts, so no
+ * group straddles two slices; gslice[world + 1] = group boundaries (rank r owns groups
+ * gslice[r] .. gslice[r+1], those whose first member is in its slice, and votes every finer
+ * block whose level-0 ancestor is in one of them).  0, or -1 on invalid arguments. */
+int rv_cull_partition(int32_t B0, int32_t gi, int32_t gj, int32_t gk, int32_t world,
+                      int64_t* slice, int64_t* gslice);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,6 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "librotvote.so")
 SOURCES = ["rv_kernels.cu", "rv_vote_tc.cu", "rv_dplan.cu", "rv_cull.cu", "rv_alg1.cu", "rv_rigid.cu", "rv_api.cpp", "rv_plan.cpp"]
-HEADERS = ["rv_geom.h", "rv_kernels.h", "rv_dplan.h", "rv_alg1.h", "rv_rigid.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -22,8 +21,10 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    deps += [os.path.join(ROOT, "include", f) for f in ("rotvote.h", "rotvote_plan.h")]
+    # every file of csrc/ and include/ (a header missing from a hand-kept list once left a stale
+    # library in place)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps += [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))]
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
 

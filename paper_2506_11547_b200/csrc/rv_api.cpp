@@ -168,7 +168,11 @@ struct rv_ctx {
   std::string err;
   int num_sms = 148;
   int vote_blocks_per_sm = rv::kVoteMinBlocks;
-  int force_groups = 0;  // tuning hook: RV_VOTE_GROUPS=1|2|4 forces the K3 CTA shape
+#ifdef RV_VOTE_GROUPS
+  int force_groups = RV_VOTE_GROUPS;  // tuning builds: force the FP32 K3 CTA shape (1|2|4)
+#else
+  int force_groups = 0;
+#endif
   ncclComm_t comm = nullptr;
 
   DevBuf<float> k9;              // [9][stride]
@@ -252,7 +256,7 @@ struct rv_ctx {
   bool cull_on = false;          // cfg.cull (with tensor_vote)
   bool cull_ready = false;       // this solve's level-0 bitmasks are written: levels >= 1 cull
   int64_t cull_min_n = 0;        // cull only problems of >= this many correspondences (the
-                                 // largest of a batch); RV_CULL_MIN_N overrides
+                                 // largest of a batch)
   int32_t cull_B0 = 0;
   int64_t cull_m0 = 0, cull_wpc_max = 0;
   DevBuf<uint32_t> cbits;        // level-0 pass bitmasks (K3-TC)
@@ -269,6 +273,7 @@ struct rv_ctx {
   DevBuf<int32_t> lutg, goff, gmem;
   int64_t cull_G = 0, cull_G_grouped = 0;
   bool cull_grouped = false;     // this solve's lists are group unions (K3-CT)
+  int32_t cull_gshape[3] = {1, 2, 2};  // ancestor group extent along (i, j, k)
   // several ranks: level 0 is sliced at (i, j/2) row-pair boundaries (a group never straddles
   // two slices); rank r votes level-0 rows [cull_s[r], cull_s[r+1]) and owns the groups
   // [cull_g[r], cull_g[r+1]) (those whose first member is in its slice)
@@ -277,8 +282,8 @@ struct rv_ctx {
   DevBuf<int32_t> c_acnt, c_tanc, c_tslot, c_cidx, c_icnt, c_work;
   DevBuf<float> c_phi;
   DevBuf<uint8_t> c_tphi;        // K3-CT block rows (fp16 split)
-  bool cull_tc = true;           // culled levels on the tensor cores (K3-CT, one rank: group
-                                 // lists); RV_CULL_TC=0 (or several ranks): FP32 K3-C
+  bool cull_tc = true;           // culled levels on the tensor cores (K3-CT, group lists);
+                                 // cfg.cull == 2: the FP32 K3-C on per-ancestor lists
   DevBuf<rv::CullItem> c_items;
   DevBuf<unsigned long long> c_pairs;
   std::vector<cudaEvent_t> cevs;
@@ -351,6 +356,11 @@ struct rv_ctx {
     return fail(e == cudaErrorMemoryAllocation ? RV_ENOMEM : RV_ECUDA, "%s: %s", what,
                 cudaGetErrorString(e));
   }
+  // this call runs ONE problem whose levels are sharded over the ranks (or the loopback
+  // emulation of that); set by solve_batched_impl from the caller's problem count -- a rank's
+  // local share of a batch (one problem when P is in [W, 2W)) is never split
+  bool split_one = false;
+  bool host_plan = false;  // cfg.planner == 1: the host planner drives every level
   int effective_world() const {
     if (cfg.world > 1) return cfg.world;
     return cfg.emulate_world > 1 ? cfg.emulate_world : 1;
@@ -568,7 +578,7 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
             "copying offsets");
     // the culled levels' rows: K3-CT's fp16-split row-major copy, or K3-C's fp32 rows (the
     // culled path cull_prepare will pick: K3-CT unless RV_CULL_TC=0 or a multi-rank batch)
-    const bool ct = ctx->cull_on && ctx->cull_tc && (ctx->effective_world() == 1 || P == 1);
+    const bool ct = ctx->cull_on && ctx->cull_tc;
     const bool k3c = ctx->cull_on && !ct;
     if (k3c) RV_CUDA(ctx->k12.ensure((size_t)(toff[P] + 8) * 12), "allocating K3-C rows");
     if (ct) RV_CUDA(ctx->tctab_rm.ensure((size_t)(toff[P] + 8) * 64), "allocating K3-CT rows");
@@ -1350,68 +1360,40 @@ int cull_prepare(rv_ctx* ctx, int32_t B0, int64_t m0, int32_t PL) {
     for (int64_t a = 0; a < m0; ++a) lut[ctx->grid_host[a]] = (int32_t)a;
     RV_CUDA(ctx->lut0.ensure(lut.size()), "allocating");
     RV_CUDA(cudaMemcpy(ctx->lut0.p, lut.data(), lut.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
-    // groups: level-0 blocks (i, j, k) with equal (i, j / 2, k / 2), numbered in row order:
-    // a group lies inside one i-slab of the (lin-sorted) level-0 list
-    std::vector<int32_t> lg((size_t)B0 * B0 * B0, -1), key((size_t)B0 * B0 * B0, -1);
-    std::vector<std::vector<int32_t>> mem;
-    for (int64_t a = 0; a < m0; ++a) {
-      const int64_t lin = ctx->grid_host[a];
-      const int64_t i = lin / ((int64_t)B0 * B0), j = (lin / B0) % B0, k = lin % B0;
-      const int64_t kk = (i * B0 + j / 2) * B0 + k / 2;
-      if (key[kk] < 0) {
-        key[kk] = (int32_t)mem.size();
-        mem.emplace_back();
-      }
-      lg[lin] = key[kk];
-      mem[key[kk]].push_back((int32_t)a);
-    }
-    std::vector<int32_t> go(mem.size() + 1, 0), gm;
-    for (size_t g = 0; g < mem.size(); ++g) {
-      go[g + 1] = go[g] + (int32_t)mem[g].size();
-      gm.insert(gm.end(), mem[g].begin(), mem[g].end());
-    }
+    // ancestor groups (rotvote_plan.h rv_cull_groups): level-0 blocks with equal
+    // (i / gi, j / gj, k / gk), numbered in row order
+    const int32_t* gs = ctx->cull_gshape;
+    const int64_t G = rv_cull_groups(B0, gs[0], gs[1], gs[2], nullptr, nullptr, nullptr);
+    if (G < 1) return ctx->fail(RV_EINVAL, "invalid ancestor group shape");
+    std::vector<int32_t> g_of((size_t)m0), go((size_t)G + 1), gm((size_t)m0);
+    rv_cull_groups(B0, gs[0], gs[1], gs[2], g_of.data(), go.data(), gm.data());
+    std::vector<int32_t> lg((size_t)B0 * B0 * B0, -1);
+    for (int64_t a = 0; a < m0; ++a) lg[ctx->grid_host[a]] = g_of[a];
     RV_CUDA(ctx->lutg.ensure(lg.size()), "allocating");
     RV_CUDA(ctx->goff.ensure(go.size()), "allocating");
     RV_CUDA(ctx->gmem.ensure(gm.size()), "allocating");
     RV_CUDA(cudaMemcpy(ctx->lutg.p, lg.data(), lg.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
     RV_CUDA(cudaMemcpy(ctx->goff.p, go.data(), go.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
     RV_CUDA(cudaMemcpy(ctx->gmem.p, gm.data(), gm.size() * 4, cudaMemcpyHostToDevice), "H2D lut");
-    ctx->cull_G_grouped = (int64_t)mem.size();
+    ctx->cull_G_grouped = G;
     ctx->lut0_B = B0;
     ctx->cull_s.clear();  // recomputed below for this B0
   }
   {
     const int W = ctx->effective_world();
     if ((int64_t)ctx->cull_s.size() != W + 1) {
-      // slice boundaries where a new (i, j / 2) row pair starts (no group straddles one: a
-      // group's members are (i, j..j+1, k..k+1), j even) -- the first at or after r m0 / W --
-      // and the groups whose first member falls in each slice
-      ctx->cull_s.assign(W + 1, m0);
-      ctx->cull_g.assign(W + 1, ctx->cull_G_grouped);
-      auto slab = [&](int64_t a) {
-        const int64_t lin = ctx->grid_host[a], i = lin / ((int64_t)B0 * B0), j = (lin / B0) % B0;
-        return i * B0 + j / 2;
-      };
-      ctx->cull_s[0] = 0;
-      for (int r = 1; r < W; ++r) {
-        int64_t a = std::max<int64_t>(ctx->cull_s[r - 1], (m0 * r + W - 1) / W);
-        while (a < m0 && a > 0 && slab(a) == slab(a - 1)) ++a;
-        ctx->cull_s[r] = std::min<int64_t>(a, m0);
-      }
-      std::vector<int32_t> go(ctx->cull_G_grouped + 1), gm(m0);
-      cudaMemcpy(go.data(), ctx->goff.p, go.size() * 4, cudaMemcpyDeviceToHost);
-      cudaMemcpy(gm.data(), ctx->gmem.p, gm.size() * 4, cudaMemcpyDeviceToHost);
-      ctx->cull_g[0] = 0;
-      for (int r = 1; r <= W; ++r) {
-        int64_t g = ctx->cull_g[r - 1];
-        while (g < ctx->cull_G_grouped && gm[go[g]] < ctx->cull_s[r]) ++g;
-        ctx->cull_g[r] = g;
-      }
+      // rotvote_plan.h rv_cull_partition: level-0 slices of whole groups, owned group ranges
+      ctx->cull_s.assign(W + 1, 0);
+      ctx->cull_g.assign(W + 1, 0);
+      const int32_t* gs = ctx->cull_gshape;
+      if (rv_cull_partition(B0, gs[0], gs[1], gs[2], W, ctx->cull_s.data(), ctx->cull_g.data()))
+        return ctx->fail(RV_EINVAL, "invalid culling partition");
     }
   }
   // group unions for K3-CT (with per-ancestor lists an item would fill a quarter of its 128
-  // rows); several ranks: one problem only (the sharded path), slab-aligned slices above
-  ctx->cull_grouped = ctx->cull_tc && (ctx->effective_world() == 1 || PL == 1);
+  // rows); a split problem (ctx->split_one) uses the slab-aligned slices above, a rank's share
+  // of a batch runs like a one-rank batch
+  ctx->cull_grouped = ctx->cull_tc;
   ctx->cull_G = ctx->cull_grouped ? ctx->cull_G_grouped : m0;
   RV_CUDA(ctx->c_pairs.ensure(1), "allocating");
   RV_CUDA(cudaMemsetAsync(ctx->c_pairs.p, 0, 8, ctx->stream), "memset");
@@ -1449,7 +1431,7 @@ int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
   RV_CUDA(ctx->c_lidx.ensure(total + 4), "allocating level-0 lists");
   RV_CUDA(ctx->c_fill.ensure(NB), "allocating");
   int64_t row_lo = 0, row_hi = NB;
-  if (ctx->comm && PL == 1 && ctx->cfg.world > 1) {  // this rank's level-0 slice / groups
+  if (ctx->comm && ctx->split_one) {  // this rank's level-0 slice / groups
     if (ctx->cull_grouped) {
       row_lo = ctx->cull_g[ctx->cfg.rank];
       row_hi = ctx->cull_g[ctx->cfg.rank + 1];
@@ -1470,9 +1452,7 @@ int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
 
 // true when the device level loop applies: >= 2 levels and a cached level-0 background
 bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps) {
-  if (levels_eff < 2) return false;
-  if (const char* e = getenv("RV_HOST_PLAN"))
-    if (atoi(e) != 0) return false;
+  if (levels_eff < 2 || ctx->host_plan) return false;
   int64_t mbg = 0;
   return rv_plan_l0_background(B0, eps, &mbg) != nullptr && mbg > 0;
 }
@@ -1697,7 +1677,8 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   // one problem on several ranks: every level's list is built identically on every rank
   // (ordered expansion) and its votes are sharded (vote_level_sharded)
   const int W = ctx->effective_world();
-  const bool shard = PL == 1 && W > 1;
+  const bool shard = ctx->split_one;
+  if (shard && PL != 1) return ctx->fail(RV_ECUDA, "internal: a split solve has one problem");
   const int64_t slack = shard ? W : 0;  // count arrays hold W * ceil(m / W) >= m entries
   std::vector<int64_t> phase_chunk;       // per phase: the shard chunk (0: not sharded)
   auto vote = [&](int32_t mode, int32_t B, const rv::DpList& Ld, int64_t entries) -> int {
@@ -2120,6 +2101,10 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
   const bool one_sharded = P == 1 && W > 1 &&
                            dplan_applies(ctx, lev_eff, ctx->chain[ctx->chain.size() - lev_eff], eps);
   if (one_sharded) { pb = 0; pe = 1; }
+  // the one-problem split (real ranks or the loopback emulation) is decided from the caller's P
+  // here, never from this rank's local share
+  ctx->split_one = P == 1 && ctx->effective_world() > 1 &&
+                   dplan_applies(ctx, lev_eff, ctx->chain[ctx->chain.size() - lev_eff], eps);
   const int32_t PL = (int32_t)(pe - pb);
   std::vector<rv_result> local(PL);
   Trace tr;
@@ -2371,6 +2356,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
   if (cfg->max_n < 2 || cfg->max_n > ((int64_t)1 << 31) - 4096) return RV_EINVAL;
   if (cfg->max_problems < 1 || cfg->refine_rounds < 0 || !(cfg->guard >= 0.0f)) return RV_EINVAL;
   if (cfg->chain_len < 0 || cfg->chain_len > RV_MAX_CHAIN) return RV_EINVAL;
+  if (cfg->cull < 0 || cfg->cull > 2 || cfg->planner < 0 || cfg->planner > 1) return RV_EINVAL;
   rv_ctx* ctx = new rv_ctx();
   ctx->cfg = *cfg;
   if (cfg->chain_len == 0) ctx->chain.assign(kDefaultChain, kDefaultChain + 6);
@@ -2385,9 +2371,8 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
   ctx->stream = (cudaStream_t)cfg->stream;
   ctx->tc_on = cfg->tensor_vote != 0;
   ctx->cull_on = ctx->tc_on && cfg->cull != 0;
-  if (const char* e = getenv("RV_CULL_MIN_N")) ctx->cull_min_n = atoll(e);
-  if (const char* e = getenv("RV_CULL_TC")) ctx->cull_tc = atoi(e) != 0;
-  if (const char* fg = getenv("RV_VOTE_GROUPS")) ctx->force_groups = atoi(fg);
+  ctx->cull_tc = cfg->cull != 2;
+  ctx->host_plan = cfg->planner == 1;
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
@@ -2573,6 +2558,7 @@ int rot_vote_count_cells_culled(rv_ctx* ctx, const float* x, const float* y, int
   const int64_t offs[2] = {0, n};
   std::vector<int64_t> koff;
   ctx->reset_counters();
+  ctx->split_one = false;  // a one-rank step: this rank compacts every list
   if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
   if (int rc = check_bad(ctx)) return rc;
   const int64_t m0 = rv_grid_candidates(B0, nullptr, 0);

@@ -1155,11 +1155,11 @@ template <int MODE>
 void launch_cull_t(const VoteSeg* segs, const CullItem* items, const int32_t* counts_dev,
                    int32_t* work, unsigned long long* pairs, const float* phi, const int32_t* cidx,
                    const uint32_t* lidx, float guard, int num_sms, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_done{0};
+  if (first_launch_on_device(attr_done)) {
     cudaFuncSetAttribute(rv_vote_cull_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)cull_smem_bytes<MODE>());
-    attr = true;
+    mark_device_done(attr_done);
   }
   rv_vote_cull_kernel<MODE><<<num_sms * kCullCtasPerSm, kCullThreads, cull_smem_bytes<MODE>(), s>>>(
       segs, items, counts_dev, work, pairs, phi, cidx, lidx, guard);
@@ -1171,14 +1171,14 @@ void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
                          const uint8_t* tphi, const int32_t* cidx, const uint32_t* lidx,
                          unsigned long long* pairs, int num_sms, cudaStream_t s,
                          int32_t* work) {
-  static bool attr = false;
+  static std::atomic<uint64_t> attr_done{0};
   const size_t b0 = sizeof(CtSmem) + 1024, b1 = b0;
-  if (!attr) {
+  if (first_launch_on_device(attr_done)) {
     cudaFuncSetAttribute(rv_vote_cull_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)b0);
     cudaFuncSetAttribute(rv_vote_cull_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)b1);
-    attr = true;
+    mark_device_done(attr_done);
   }
   if (mode == RV_MODE_FINAL)
     rv_vote_cull_tc_kernel<true><<<num_sms, kCtThreads, b1, s>>>(segs, items, counts_dev, tab, pad_row,

@@ -1,10 +1,28 @@
 // rv_kernels.h -- device-side descriptors and launchers of librotvote's sm_100a kernels.
 #pragma once
+#include <atomic>
 #include <cstdint>
 
 #include <cuda_runtime.h>
 
 namespace rv {
+
+// Kernel attributes (the dynamic shared-memory opt-in) are per device: a launcher sets them the
+// first time it runs on each device of the process.  Racing threads may both set them
+// (idempotent).
+inline bool first_launch_on_device(std::atomic<uint64_t>& done) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const uint64_t bit = 1ull << (d & 63);
+  if (done.load(std::memory_order_acquire) & bit) return false;
+  return true;
+}
+inline void mark_device_done(std::atomic<uint64_t>& done) {
+  int d = 0;
+  cudaGetDevice(&d);
+  done.fetch_or(1ull << (d & 63), std::memory_order_release);
+}
+
 
 #ifndef RV_CPT
 #define RV_CPT 4

@@ -22,6 +22,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/rotvote.h"
@@ -555,6 +556,75 @@ int64_t rv_grid_candidates(int32_t B, uint32_t* out, int64_t cap) {
           ++m;
         }
   return m;
+}
+
+int64_t rv_cull_groups(int32_t B0, int32_t gi, int32_t gj, int32_t gk, int32_t* group_of,
+                       int32_t* goff, int32_t* gmem) {
+  if (B0 < 1 || B0 > 1625 || gi < 1 || gj < 1 || gk < 1) return -1;
+  const int64_t m0 = rv_grid_candidates(B0, nullptr, 0);
+  std::vector<uint32_t> rows((size_t)m0);
+  rv_grid_candidates(B0, rows.data(), m0);
+  // group key of a row -> group id, numbered by first appearance in row (lin) order
+  std::unordered_map<int64_t, int32_t> id;
+  std::vector<int32_t> g_of((size_t)m0), size;
+  for (int64_t a = 0; a < m0; ++a) {
+    int32_t i, j, k;
+    rv::lin_to_ijk(rows[a], B0, i, j, k);
+    const int64_t key = ((int64_t)(i / gi) * B0 + j / gj) * B0 + k / gk;
+    auto it = id.find(key);
+    if (it == id.end()) {
+      it = id.emplace(key, (int32_t)size.size()).first;
+      size.push_back(0);
+    }
+    g_of[a] = it->second;
+    ++size[it->second];
+  }
+  const int64_t G = (int64_t)size.size();
+  std::vector<int32_t> off((size_t)G + 1, 0);
+  for (int64_t g = 0; g < G; ++g) off[g + 1] = off[g] + size[g];
+  if (group_of) std::copy(g_of.begin(), g_of.end(), group_of);
+  if (goff) std::copy(off.begin(), off.end(), goff);
+  if (gmem) {
+    std::vector<int32_t> fill(off.begin(), off.end() - 1);
+    for (int64_t a = 0; a < m0; ++a) gmem[fill[g_of[a]]++] = (int32_t)a;  // ascending rows
+  }
+  return G;
+}
+
+int rv_cull_partition(int32_t B0, int32_t gi, int32_t gj, int32_t gk, int32_t world,
+                      int64_t* slice, int64_t* gslice) {
+  if (world < 1 || !slice || !gslice) return -1;
+  const int64_t G = rv_cull_groups(B0, gi, gj, gk, nullptr, nullptr, nullptr);
+  if (G < 0) return -1;
+  const int64_t m0 = rv_grid_candidates(B0, nullptr, 0);
+  std::vector<uint32_t> rows((size_t)m0);
+  rv_grid_candidates(B0, rows.data(), m0);
+  std::vector<int32_t> g_of((size_t)m0), goff((size_t)G + 1), gmem((size_t)m0);
+  rv_cull_groups(B0, gi, gj, gk, g_of.data(), goff.data(), gmem.data());
+  // a run of consecutive rows that holds whole groups: the i-slab of gi rows when gi > 1 (the
+  // rows of i .. i+gi-1 are contiguous in lin order), else the (i, j / gj) row slab, else the
+  // (i, j, k / gk) run
+  auto slab = [&](int64_t a) -> int64_t {
+    int32_t i, j, k;
+    rv::lin_to_ijk(rows[a], B0, i, j, k);
+    if (gi > 1) return i / gi;
+    if (gj > 1) return (int64_t)i * B0 + j / gj;
+    return ((int64_t)i * B0 + j) * B0 + k / gk;
+  };
+  slice[0] = 0;
+  for (int32_t r = 1; r < world; ++r) {
+    int64_t a = std::max<int64_t>(slice[r - 1], (m0 * r + world - 1) / world);
+    while (a < m0 && a > 0 && slab(a) == slab(a - 1)) ++a;
+    slice[r] = std::min<int64_t>(a, m0);
+  }
+  slice[world] = m0;
+  gslice[0] = 0;
+  for (int32_t r = 1; r <= world; ++r) {
+    int64_t g = gslice[r - 1];
+    while (g < G && gmem[goff[g]] < slice[r]) ++g;
+    gslice[r] = g;
+  }
+  return 0;
 }
 
 }  // extern "C"

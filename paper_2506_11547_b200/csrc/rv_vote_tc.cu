@@ -589,8 +589,8 @@ void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, in
     rv_tc_atab_kernel<false><<<agrid, 128, 0, s>>>(segs, ablocks, n_ablocks, counts_dev, guard, atab);
   // persistent: one CTA per SM
   const int grid = counts_dev ? sms : (n_items < sms ? n_items : sms);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_done{0};
+  if (first_launch_on_device(attr_done)) {
     cudaFuncSetAttribute(rv_vote_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)tc_smem_bytes());
     cudaFuncSetAttribute(rv_vote_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -599,7 +599,7 @@ void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, in
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes());
     cudaFuncSetAttribute(rv_vote_tc_kernel<false, 0, false, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes());
-    attr = true;
+    mark_device_done(attr_done);
   }
   if (emit_bits && !final_mode && !dump) {
     rv_vote_tc_kernel<false, 0, false, true><<<grid, kTcThreads, tc_smem_bytes(), s>>>(
@@ -611,10 +611,13 @@ void launch_vote_tc(const uint8_t* tab, uint8_t* atab, const ABlock* ablocks, in
         tab, atab, segs, items, n_items, counts_dev, guard, nullptr, 0);
     return;
   }
-  static const int abl = [] {
-    const char* e = getenv("RV_TC_ABLATE");  // tuning only: skip pipeline stages (wrong counts)
-    return e ? atoi(e) : 0;
-  }();
+  // tuning builds only (-DRV_TC_ABLATE=1..7 skips pipeline stages: WRONG counts); the product
+  // library is compiled without it
+#ifdef RV_TC_ABLATE
+  constexpr int abl = RV_TC_ABLATE;
+#else
+  constexpr int abl = 0;
+#endif
   if (dump)
     rv_vote_tc_kernel<true><<<grid, kTcThreads, tc_smem_bytes(), s>>>(tab, atab, segs, items,
                                                                          n_items, counts_dev, guard, dump, dump_ld);

@@ -40,7 +40,8 @@ class rv_config(C.Structure):
                 ("nccl_id", C.c_void_p), ("max_n", C.c_int64), ("max_problems", C.c_int32),
                 ("chain_len", C.c_int32), ("chain", C.c_int32 * RV_MAX_CHAIN),
                 ("refine_rounds", C.c_int32), ("guard", C.c_float), ("stream", C.c_void_p),
-                ("emulate_world", C.c_int32), ("tensor_vote", C.c_int32), ("cull", C.c_int32)]
+                ("emulate_world", C.c_int32), ("tensor_vote", C.c_int32), ("cull", C.c_int32),
+                ("planner", C.c_int32)]
 
 
 class rv_result(C.Structure):
@@ -126,6 +127,10 @@ def lib() -> C.CDLL:
     L.rv_shard_range.restype = None
     L.rv_grid_candidates.argtypes = [i32, vp, i64]
     L.rv_grid_candidates.restype = i64
+    L.rv_cull_groups.argtypes = [i32, i32, i32, i32, vp, vp, vp]
+    L.rv_cull_groups.restype = i64
+    L.rv_cull_partition.argtypes = [i32, i32, i32, i32, i32, vp, vp]
+    L.rv_cull_partition.restype = i32
     _lib = L
     return L
 
@@ -222,8 +227,15 @@ class RotVote:
     def __init__(self, device: int = 0, max_n: int = 1 << 20, max_problems: int = 1,
                  chain=None, refine_rounds: int = 2, guard: float = 1e-5, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 emulate_world: int = 0, tensor_vote: bool = True, cull: bool = True):
+                 emulate_world: int = 0, tensor_vote: bool = True, cull=True,
+                 planner: str = "device"):
+        """cull: True / "tc" (K3-CT, default), "fp32" (K3-C), False (off).
+        planner: "device" (the level loop on the GPU, default) or "host" (rv_plan.cpp)."""
         import torch
+        self._kw = dict(device=device, max_n=max_n, max_problems=max_problems, chain=chain,
+                        refine_rounds=refine_rounds, guard=guard, stream=stream, rank=rank,
+                        world=world, nccl_id=nccl_id, emulate_world=emulate_world,
+                        tensor_vote=tensor_vote, cull=cull, planner=planner)
         cfg = rot_vote_default_config()
         cfg.device = device
         cfg.rank, cfg.world = rank, world
@@ -245,11 +257,16 @@ class RotVote:
         cfg.stream = C.c_void_p(stream.cuda_stream)
         cfg.emulate_world = int(emulate_world)
         cfg.tensor_vote = int(bool(tensor_vote))
-        cfg.cull = int(bool(cull))
+        cfg.cull = {True: 1, "tc": 1, "fp32": 2, False: 0, None: 0}[cull]
+        cfg.planner = {"device": 0, "host": 1}[planner]
         self.cfg = cfg
         self.device = device
         self.chain = tuple(chain) if chain is not None else DEFAULT_CHAIN
         self.ctx = rot_vote_create(cfg)
+
+    def twin(self, **overrides) -> "RotVote":
+        """A second context with this one's settings, some overridden (e.g. planner="host")."""
+        return RotVote(**{**self._kw, **overrides})
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -482,6 +499,30 @@ def shard_range(m: int, rank: int, world: int):
     b, e = C.c_int64(), C.c_int64()
     lib().rv_shard_range(int(m), int(rank), int(world), C.byref(b), C.byref(e))
     return b.value, e.value
+
+
+def cull_groups(B0: int, shape=(1, 2, 2)):
+    """(group_of[m0], goff[G+1], gmem[m0]) of the ancestor groups (rotvote_plan.h)."""
+    gi, gj, gk = (int(v) for v in shape)
+    G = lib().rv_cull_groups(int(B0), gi, gj, gk, None, None, None)
+    if G < 0:
+        raise ValueError("invalid group shape")
+    m0 = lib().rv_grid_candidates(int(B0), None, 0)
+    g_of = np.zeros(m0, np.int32)
+    goff = np.zeros(G + 1, np.int32)
+    gmem = np.zeros(m0, np.int32)
+    lib().rv_cull_groups(int(B0), gi, gj, gk, g_of.ctypes.data, goff.ctypes.data, gmem.ctypes.data)
+    return g_of, goff, gmem
+
+
+def cull_partition(B0: int, world: int, shape=(1, 2, 2)):
+    """(slice[world+1], gslice[world+1]): level-0 row slices and owned group ranges."""
+    gi, gj, gk = (int(v) for v in shape)
+    sl = np.zeros(world + 1, np.int64)
+    gsl = np.zeros(world + 1, np.int64)
+    if lib().rv_cull_partition(int(B0), gi, gj, gk, int(world), sl.ctypes.data, gsl.ctypes.data):
+        raise ValueError("invalid partition arguments")
+    return sl, gsl
 
 
 def grid_candidates(B: int) -> np.ndarray:

@@ -36,19 +36,10 @@ def torch_cuda():
 
 
 def _ctx(path, **kw):
-    """A culling context on the tensor-core K3-CT path ("tc", default; one rank) or the FP32
-    K3-C path ("fp32": RV_CULL_TC=0 at creation)."""
-    import os
+    """A culling context on the tensor-core K3-CT path ("tc", default) or the FP32 K3-C path
+    ("fp32", cull = 2)."""
     from paper_2506_11547_b200 import RotVote
-    old = os.environ.get("RV_CULL_TC")
-    os.environ["RV_CULL_TC"] = "1" if path == "tc" else "0"
-    try:
-        return RotVote(tensor_vote=True, cull=True, **kw)
-    finally:
-        if old is None:
-            del os.environ["RV_CULL_TC"]
-        else:
-            os.environ["RV_CULL_TC"] = old
+    return RotVote(tensor_vote=True, cull=path, **kw)
 
 
 @pytest.fixture(scope="module", params=["tc", "fp32"])

@@ -1,5 +1,5 @@
 """The device-resident level loop of batched solves (csrc/rv_dplan.cu) against the host
-planner (rv_plan.cpp, forced with RV_HOST_PLAN=1) and the oracle.
+planner (rv_plan.cpp, forced with planner="host") and the oracle.
 
 The device loop takes the planner's decisions on the GPU; it must return the same winner,
 votes, ties, lb* and recheck sets as the host planner on every problem, for several chains
@@ -30,12 +30,13 @@ def dev(torch, a):
     return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
 
 
-def host_plan(fn):
-    os.environ["RV_HOST_PLAN"] = "1"
+def host_plan(ctx, fn):
+    """fn run on a twin of ctx whose levels are driven by the host planner (planner="host")."""
+    h = ctx.twin(planner="host")
     try:
-        return fn()
+        return fn(h)
     finally:
-        del os.environ["RV_HOST_PLAN"]
+        h.close()
 
 
 def compare(res_d, res_h, strict_phases=False):
@@ -77,7 +78,7 @@ def test_device_loop_equals_host_planner(torch_cuda, tensor_vote, chain, levels)
     try:
         x, y = dev(torch, bt.x), dev(torch, bt.y)
         rd = ctx.solve_batched(x, y, bt.offsets, bt.eps, levels=levels)
-        rh = host_plan(lambda: ctx.solve_batched(x, y, bt.offsets, bt.eps, levels=levels))
+        rh = host_plan(ctx, lambda c: c.solve_batched(x, y, bt.offsets, bt.eps, levels=levels))
         compare(rd, rh)
         # and the oracle (certified == exhaustive) on a sample
         for p in range(0, 96, 17):
@@ -97,7 +98,7 @@ def test_device_loop_cfg5_equals_host_planner(torch_cuda):
     try:
         x, y = dev(torch, bt.x), dev(torch, bt.y)
         rd = ctx.solve_batched(x, y, bt.offsets, bt.eps)
-        rh = host_plan(lambda: ctx.solve_batched(x, y, bt.offsets, bt.eps))
+        rh = host_plan(ctx, lambda c: c.solve_batched(x, y, bt.offsets, bt.eps))
         mism = compare(rd, rh)
         print("cfg5 phase-list mismatches:", mism)
         # repeated calls reuse the context's buffers and give identical answers
@@ -124,7 +125,7 @@ def test_device_loop_degenerate_batches(torch_cuda):
     try:
         x, y = dev(torch, bt.x), dev(torch, bt.y)
         rd = ctx.solve_batched(x, y, bt.offsets, bt.eps)
-        rh = host_plan(lambda: ctx.solve_batched(x, y, bt.offsets, bt.eps))
+        rh = host_plan(ctx, lambda c: c.solve_batched(x, y, bt.offsets, bt.eps))
         compare(rd, rh, strict_phases=True)
         for pr, r in zip(probs, rd):
             ref = oracle.solve(pr.x, pr.y, bt.eps)
@@ -150,7 +151,7 @@ def test_device_loop_large_single_problems(torch_cuda):
         for pr in cases:
             x, y = dev(torch, pr.x), dev(torch, pr.y)
             rb = ctx.solve_batched(x, y, np.array([0, pr.n], np.int64), pr.eps)
-            rs = host_plan(lambda: ctx.solve(x, y, pr.eps))
+            rs = host_plan(ctx, lambda c: c.solve(x, y, pr.eps))
             compare(rb, [rs], strict_phases=True)
     finally:
         ctx.close()
@@ -159,7 +160,7 @@ def test_device_loop_large_single_problems(torch_cuda):
 @pytest.mark.parametrize("tensor_vote", [False, True])
 def test_single_solve_device_loop_equals_host_planner(torch_cuda, tensor_vote):
     """rot_vote_solve on one GPU takes the device loop (P = 1); the host planner (the
-    sharding path, RV_HOST_PLAN=1) must agree on every field, incl. per-phase block counts."""
+    sharding path, planner="host") must agree on every field, incl. per-phase block counts."""
     from paper_2506_11547_b200 import RotVote
     torch = torch_cuda
     ctx = RotVote(max_n=200_000, tensor_vote=tensor_vote, cull=False)
@@ -174,7 +175,7 @@ def test_single_solve_device_loop_equals_host_planner(torch_cuda, tensor_vote):
             x, y = dev(torch, pr.x), dev(torch, pr.y)
             for levels in (0, 2, 3):
                 rd = ctx.solve(x, y, pr.eps, levels=levels)
-                rh = host_plan(lambda: ctx.solve(x, y, pr.eps, levels=levels))
+                rh = host_plan(ctx, lambda c: c.solve(x, y, pr.eps, levels=levels))
                 compare([rd], [rh], strict_phases=True)
     finally:
         ctx.close()
@@ -185,7 +186,7 @@ def test_sharded_single_solve_loopback(torch_cuda, tensor_vote):
     """One problem over W emulated ranks (emulate_world): every level's list is built in
     parent order and its votes are split into W slices -- the code path of the NCCL run with
     the all-gather replaced by in-place writes.  Every field must equal the one-rank solve, and
-    the host planner's sharded path (RV_HOST_PLAN=1)."""
+    the host planner's sharded path (planner="host")."""
     from paper_2506_11547_b200 import RotVote
     torch = torch_cuda
     cases = [datagen.cfg2(seed=5), datagen.cfg3(seed=6),
@@ -198,7 +199,7 @@ def test_sharded_single_solve_loopback(torch_cuda, tensor_vote):
             ctx = RotVote(max_n=1 << 17, emulate_world=W, tensor_vote=tensor_vote, cull=False)
             try:
                 r = ctx.solve(x, y, pr.eps)
-                rh = host_plan(lambda: ctx.solve(x, y, pr.eps))
+                rh = host_plan(ctx, lambda c: c.solve(x, y, pr.eps))
             finally:
                 ctx.close()
             compare([r], [rh], strict_phases=True)

@@ -86,7 +86,11 @@ def test_count_cells_bound_mode(rv, torch_cuda, cfg):
         thr = np.array([oracle.cell_bound_threshold(B, int(l), pr.eps) for l in lins]) - GUARD
         lo, hi = in_band_bounds(pr.x, pr.y, B, lins, thr)
         assert np.all(got >= lo) and np.all(got <= hi), B
-        assert np.mean(lo == hi) > 0.5
+        # non-vacuity: most cells have an empty near band.  Outlier scores are uniform on
+        # [-1, 1] (Archimedes), so P(|s - t| < g) = g per pair and a cell's band
+        # is empty with probability ~exp(-n g): 0.999 at cfg1, 0.905 at cfg2 (5 sigma of
+        # 700 cells below that is 0.056)
+        assert np.mean(lo == hi) >= math.exp(-pr.n * GUARD) - 0.06
 
 
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])

@@ -144,33 +144,25 @@ def test_tc_final_counts_parity(rvtc, torch_cuda, n):
 
 def test_tc_loopback_and_nccl_paths(torch_cuda):
     """The sharded paths (loopback ranks, 1-rank NCCL communicator) with the tensor-core
-    vote give the direct answer.  Sharded contexts vote the culled levels on K3-C, so the
-    reference for the search path (pair_votes) is a one-rank K3-C context; the default one-rank
-    context (K3-CT) must give the same answer."""
-    import os
+    vote give the one-rank answer, on both culled vote paths (K3-CT, the default, and the FP32
+    K3-C): the same (cell, votes, ties, q) and the same searched pairs (pair_votes)."""
     from paper_2506_11547_b200 import RotVote, rot_vote_get_unique_id
     torch = torch_cuda
     pr = datagen.cfg2(seed=9)
     x, y = dev(torch, pr.x), dev(torch, pr.y)
-    old = os.environ.get("RV_CULL_TC")
-    os.environ["RV_CULL_TC"] = "0"
-    try:
-        base = RotVote(max_n=1 << 16)
-        ctxs = (RotVote(max_n=1 << 16, emulate_world=3),
-                RotVote(max_n=1 << 16, nccl_id=rot_vote_get_unique_id()))
-    finally:
-        if old is None:
-            del os.environ["RV_CULL_TC"]
-        else:
-            os.environ["RV_CULL_TC"] = old
-    ref = base.solve(x, y, pr.eps)
-    for ctx in ctxs:
-        r = ctx.solve(x, y, pr.eps)
-        assert (r.cell, r.votes, r.n_tied, r.pair_votes) == (ref.cell, ref.votes, ref.n_tied,
-                                                             ref.pair_votes)
-        assert np.array_equal(r.q, ref.q)
-        ctx.close()
-    r = RotVote(max_n=1 << 16).solve(x, y, pr.eps)
-    assert (r.cell, r.votes, r.n_tied) == (ref.cell, ref.votes, ref.n_tied)
-    assert np.array_equal(r.q, ref.q)
-    base.close()
+    answers = []
+    for path in ("tc", "fp32"):
+        base = RotVote(max_n=1 << 16, cull=path)
+        ref = base.solve(x, y, pr.eps)
+        base.close()
+        for kw in (dict(emulate_world=3), dict(nccl_id=rot_vote_get_unique_id())):
+            ctx = RotVote(max_n=1 << 16, cull=path, **kw)
+            r = ctx.solve(x, y, pr.eps)
+            ctx.close()
+            assert (r.cell, r.votes, r.n_tied, r.pair_votes) == (ref.cell, ref.votes, ref.n_tied,
+                                                                 ref.pair_votes), (path, kw)
+            assert np.array_equal(r.q, ref.q)
+        answers.append(ref)
+    assert (answers[0].cell, answers[0].votes, answers[0].n_tied) == \
+        (answers[1].cell, answers[1].votes, answers[1].n_tied)
+    assert np.array_equal(answers[0].q, answers[1].q)

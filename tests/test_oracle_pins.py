@@ -198,6 +198,81 @@ def test_candidate_cells_brute_force(oracle_mod, B):
         assert got.size == 52461
 
 
+@pytest.mark.parametrize("B", [1, 2, 5, 15, 45, 360])
+def test_cell_center_is_block_midpoint(oracle_mod, B):
+    """P:488 divides [-1,1]^3 into B blocks per axis; P:502 returns "the center of the
+    block".  The centre of block i along an axis is the midpoint of the i-th interval of
+    np.linspace(-1, 1, B + 1) (an independent construction of the same grid).  A
+    corner-for-centre mistake (p = -1 + 2i/B) fails this by 1/B."""
+    edges = np.linspace(-1.0, 1.0, B + 1)
+    mids = 0.5 * (edges[:-1] + edges[1:])
+    rng = np.random.default_rng(B)
+    idx = [(0, 0, 0), (B - 1, B - 1, B - 1)] + [tuple(rng.integers(0, B, 3)) for _ in range(40)]
+    for i, j, k in idx:
+        p = oracle_mod.cell_center(B, int(i), int(j), int(k))
+        assert np.allclose(p, [mids[i], mids[j], mids[k]], rtol=0, atol=4e-16), (B, i, j, k)
+        # the centre lies strictly inside its block, half a step from both faces
+        for a, v in enumerate((i, j, k)):
+            assert edges[v] < p[a] < edges[v + 1]
+            assert abs((p[a] - edges[v]) - (edges[v + 1] - p[a])) < 1e-15
+
+
+def test_cell_quat_hand_evaluated(oracle_mod):
+    """q_c = P'(p_c): P'(p) = [2p/(1+p.p), (p.p-1)/(1+p.p)].  Values worked out by
+    hand as exact fractions at block centres (no code shared with the oracle):
+      B=1 (0,0,0):  p = 0                   -> q = (0, 0, 0, -1)
+      B=2 (1,1,1):  p = (1/2, 1/2, 1/2)     -> p.p = 3/4,  q = (4/7, 4/7, 4/7, -1/7)
+      B=2 (0,1,1):  p = (-1/2, 1/2, 1/2)    -> q = (-4/7, 4/7, 4/7, -1/7)
+      B=4 (3,0,1):  p = (3/4, -3/4, -1/4)   -> p.p = 19/16, q = (24/35, -24/35, -8/35, 3/35)
+                    (centre outside the ball: q3 > 0, the same rotation as -q, R4)
+      B=5 (2,2,4):  p = (0, 0, 4/5)         -> p.p = 16/25, q = (0, 0, 40/41, -9/41)
+    A corner-for-centre or a sign/ordering mistake (pole, scalar-first) fails here."""
+    o = oracle_mod
+    cases = [
+        (1, (0, 0, 0), (0, 0, 0, -1)),
+        (2, (1, 1, 1), (4 / 7, 4 / 7, 4 / 7, -1 / 7)),
+        (2, (0, 1, 1), (-4 / 7, 4 / 7, 4 / 7, -1 / 7)),
+        (4, (3, 0, 1), (24 / 35, -24 / 35, -8 / 35, 3 / 35)),
+        (5, (2, 2, 4), (0, 0, 40 / 41, -9 / 41)),
+    ]
+    for B, (i, j, k), q in cases:
+        got = o.cell_quat(B, o.lin_of(B, i, j, k))
+        assert np.allclose(got, q, rtol=0, atol=1e-15), (B, i, j, k, got)
+        assert abs(np.linalg.norm(got) - 1) < 1e-15
+
+
+def test_count_cells_near_band_independent(oracle_mod):
+    """or_count_cells' second output is #{i : |s_i(q_c) - t| < band}, the band the GPU
+    parity tests accept (SURVEY §8(c) parity rule).  Recomputed here in numpy from
+    scipy's rotation of the block quaternion: near = #{s > t - band} - #{s >= t + band},
+    and the count = #{s >= t}.  Bands of 1e-2 / 3e-3 / 1e-5 so both are non-trivial;
+    a widened or narrowed band, or a one-sided band, fails."""
+    o = oracle_mod
+    pr = datagen.make_problem(4000, 400, 0.01, 0.05, seed=21)
+    xn = pr.x.astype(np.float64)
+    yn = pr.y.astype(np.float64)
+    xn /= np.linalg.norm(xn, axis=1, keepdims=True)
+    yn /= np.linalg.norm(yn, axis=1, keepdims=True)
+    rng = np.random.default_rng(22)
+    B = 45
+    lins = np.sort(rng.choice(o.candidates(B), 24, replace=False)).astype(np.uint32)
+    total_near = 0
+    for band in (1e-2, 3e-3, 1e-5):
+        t = rng.uniform(0.2, 0.99, lins.size)
+        cnt, near = o.count_cells(pr.x, pr.y, B, lins, t, band=band)
+        for m, lin in enumerate(lins):
+            q = o.cell_quat(B, int(lin))
+            s = np.einsum("ij,ij->i", yn, xn @ scipy_R(q).T)
+            # pairs within 1e-12 of an edge could round either way: skip the cell then
+            edge = np.abs(np.abs(s - t[m]) - band) < 1e-12
+            if edge.any() or (np.abs(s - t[m]) < 1e-12).any():
+                continue
+            assert near[m] == int((s > t[m] - band).sum() - (s >= t[m] + band).sum())
+            assert cnt[m] == int((s >= t[m]).sum())
+            total_near += int(near[m])
+    assert total_near > 100  # the band is exercised
+
+
 def test_cell_radius_bounds_rotation_spread(oracle_mod):
     """For any p in a block, angle(R(P'(p)), R(P'(p_c))) <= r(c) (R6).
     Also checks the bound is not vacuous: the corner nearest the origin reaches
