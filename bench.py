@@ -33,6 +33,9 @@ METRIC = "corr×cell votes/s and ms/solve at N=1e6, 99% outliers, 1/2/4/8 B200"
 UNIT = "corr×cell votes/s"
 WORKLOAD = "cfg4: N=1e6 fp32 correspondences, 1% inliers (sigma=0.01), 99% uniform-S2 outliers, eps=0.05"
 FLOP_PER_PAIR = 18          # 9 FMA per (correspondence, cell) pair in the traceless 9-entry form
+SURVEY_FLOP_PER_PAIR = 20   # 10 FMA per pair (the 10-entry form) -- the roofline unit
+PAPER_CONTEXT = ("< 0.5 s per solve at N = 1e6, 99% outliers on a GeForce RTX 4080 + i7 CPU, "
+                 "Python/CuPy (PAPER.md P:33, P:634-635); another machine -- context, not a target")
 SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0   # B200_PROFILING.md nominal table
 FP32_PEAK_TFLOPS = SM_COUNT * FP32_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 74.4 TFLOP/s
 # K3-TC epilogue bound: every pair's fp32 score leaves TMEM through tcgen05.ld (64 B/clk per
@@ -60,6 +63,9 @@ def parse():
                          "with culling 15,45,180,360 measured fastest, profiles/r01_chain_sweep_cull.log)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-full", type=int, default=1,
+                    help="1: cpu_baseline = one complete oracle solve of cfg4 pinned to one core; "
+                         "0: a --cpu-seconds sample of the oracle's count loop")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--vote", default="tc", choices=["tc", "ffma2"],
                     help="bound levels on the tensor cores (K3-TC) or the FP32 pipe (K3)")
@@ -83,7 +89,7 @@ _REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_
 
 
 class ClockSampler:
-    def __init__(self, device: int, period: float = 0.02):
+    def __init__(self, device: int, period: float = 0.002):
         self.samples, self.reasons, self.ok = [], set(), False
         self.period, self._stop = period, threading.Event()
         try:
@@ -149,6 +155,52 @@ def oracle_sample(pr, seconds: float):
         done += sub.size
     dt = time.perf_counter() - t0
     return done * pr.n / dt, done, dt
+
+
+_ORACLE_SOLVE = r"""
+import json, os, sys, time
+sys.path.insert(0, sys.argv[1])
+import datagen, oracle
+oracle.build()
+pr = getattr(datagen, sys.argv[2])()
+t0 = time.perf_counter()
+r = oracle.solve(pr.x, pr.y, pr.eps)
+dt = time.perf_counter() - t0
+print(json.dumps({"s": dt, "lin": int(r.lin), "votes": int(r.votes), "n_tied": int(r.n_tied),
+                  "cells": int(r.cells_evaluated), "pairs": int(r.cells_evaluated) * pr.n,
+                  "affinity": sorted(os.sched_getaffinity(0))}))
+"""
+
+
+def oracle_full_solve(cfg="cfg4", core=0):
+    """One complete certified solve by the oracle (oracle/, as it stands: plain single-threaded
+    C++, depth-first certified branch and bound, exact fp64 counts), pinned to one host core
+    (taskset -c <core>).  Returns its record or None."""
+    import subprocess
+    cmd = [sys.executable, "-c", _ORACLE_SOLVE, ROOT, cfg]
+    try:
+        import shutil
+        if shutil.which("taskset"):
+            cmd = ["taskset", "-c", str(core)] + cmd
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=1800).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception:
+        return None
+
+
+def _host_info():
+    info = {"nproc": os.cpu_count(), "cpu": _cpu_name()}
+    try:
+        import subprocess
+        ls = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=20).stdout
+        keep = ("Model name", "CPU(s)", "Thread(s) per core", "Core(s) per socket", "Socket(s)",
+                "CPU max MHz", "L3 cache")
+        info["lscpu"] = {k.strip(): v.strip() for k, v in
+                         (ln.split(":", 1) for ln in ls.splitlines() if ":" in ln)
+                         if k.strip() in keep}
+    except Exception:
+        pass
+    return info
 
 
 def run_reference(args):
@@ -237,16 +289,22 @@ def _k3ct_entry(args, cull_pairs, cull_ms, ms_per_step):
     except (OSError, ValueError):
         pass
     tpeak, src = measured_peak("bf16_tflops", 1590.0)
-    return {"bound": "alu", "achieved": pairs_s / 1e12 if pairs_s else None,
-            "peak": TC_EPI_PEAK_PAIRS / 1e12, "unit": "TOP/s",
-            "frac": pairs_s / TC_EPI_PEAK_PAIRS if pairs_s else None, "traffic": traffic,
-            "kernel": "rv_vote_cull_tc_kernel (K3-CT: blocks of a 2x2x1 level-0 ancestor group vs "
+    alg = pairs_s * SURVEY_FLOP_PER_PAIR / 1e12 if pairs_s else None
+    return {"bound": "tensor", "achieved": alg, "peak": tpeak, "unit": "TFLOP/s",
+            "frac": alg / tpeak if alg else None, "traffic": traffic,
+            "kernel": "rv_vote_cull_tc_kernel (K3-CT: blocks of a 1x2x2 level-0 ancestor group vs "
                       "the group's union list, cp.async-gathered fp16-split rows, tcgen05 kind::f16 "
                       "M=128 N=256, TMEM accumulators), one TMEM read + sign count per pair",
-            "ops_per_pair": 1,
-            "peak_source": "148 SMs x 4 SMSPs x 16 lanes x 1965 MHz (the K3-TC epilogue bound)",
-            "tensor": {"peak_tflops": tpeak, "peak_source": src,
-                       "algorithmic_tflops": pairs_s * FLOP_PER_PAIR / 1e12 if pairs_s else None},
+            "flop_per_pair": SURVEY_FLOP_PER_PAIR,
+            "peak_source": f"{src} dense bf16/fp16 tensor peak (MEASURED_PEAKS.json bf16_tflops); "
+                           "SURVEY §8(d): the tensor path is reported against the tensor-pipe "
+                           "peak at the algorithmic 20 flop per evaluated (corr, cell) pair",
+            "epilogue_bound": {
+                "what": "every evaluated pair's fp32 score leaves TMEM (tcgen05.ld, 64 B/clk/SMSP) "
+                        "and costs one ALU sign-count lane-op (16 lanes/clk/SMSP): 64 pairs/clk/SM "
+                        "= 148 SMs x 4 SMSPs x 16 lanes x 1965 MHz",
+                "peak_pairs_per_s": TC_EPI_PEAK_PAIRS, "achieved_pairs_per_s": pairs_s,
+                "frac": pairs_s / TC_EPI_PEAK_PAIRS if pairs_s else None},
             "pairs_per_step": cull_pairs / steps,
             "vote_ms_per_step": cull_ms / steps,
             "vote_share_of_step": (cull_ms / steps) / ms_per_step}
@@ -275,19 +333,16 @@ def _roofline(args, vote_pairs, vote_ms, ms_per_step, cull_pairs=0, cull_ms=0.0,
         tpeak, src = measured_peak("bf16_tflops", 1590.0)
         pairs_s = vote_pairs / (vote_ms / 1e3)
         alu_peak = TC_EPI_PEAK_PAIRS / 1e12
+        alg = pairs_s * SURVEY_FLOP_PER_PAIR / 1e12
         return {
-            "bound": "alu", "achieved": pairs_s / 1e12, "peak": alu_peak, "unit": "TOP/s",
-            "frac": pairs_s / TC_EPI_PEAK_PAIRS, "traffic": traffic,
+            "bound": "tensor", "achieved": alg, "peak": tpeak, "unit": "TFLOP/s",
+            "frac": alg / tpeak, "traffic": traffic,
             "kernel": "rv_vote_tc_kernel (K3-TC, tcgen05 kind::f16, fp16-split, fp32 TMEM accum)",
-            "ops_per_pair": 1,
-            "peak_source": "148 SMs x 4 SMSPs x 16 ALU lanes x 1965 MHz (B200_PROFILING.md unit "
-                           "counts); equals the TMEM readout bound (64 B/clk/SMSP at 4 B/pair)",
-            "tensor": {"peak_tflops": tpeak, "peak_source": f"{src} dense bf16/fp16 tensor peak "
-                       "(MEASURED_PEAKS.json bf16_tflops)",
-                       "algorithmic_tflops": achieved, "algorithmic_frac": achieved / tpeak,
-                       "flop_per_pair": FLOP_PER_PAIR,
-                       "executed_mma_tflops": pairs_s * MMA_FLOP_PER_PAIR / 1e12,
-                       "executed_mma_frac": pairs_s * MMA_FLOP_PER_PAIR / 1e12 / tpeak},
+            "flop_per_pair": SURVEY_FLOP_PER_PAIR,
+            "peak_source": f"{src} dense bf16/fp16 tensor peak (MEASURED_PEAKS.json bf16_tflops)",
+            "executed_mma": {"flop_per_pair": MMA_FLOP_PER_PAIR,
+                             "tflops": pairs_s * MMA_FLOP_PER_PAIR / 1e12,
+                             "frac": pairs_s * MMA_FLOP_PER_PAIR / 1e12 / tpeak},
             "epilogue_bound": {
                 "what": "TMEM->RF readout (tcgen05.ld 64 B/clk/SMSP, 4 B/pair) and the ALU sign "
                         "count (16 lanes/clk/SMSP): 64 pairs/clk/SM at 1965 MHz",
@@ -423,18 +478,36 @@ def run_ours(args):
                 "ms_per_step": sum(e2e_ms) / len(e2e_ms)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "evaluated_votes_per_s": evaluated / (ms_per_step / 1e3),
+        "paper_context": PAPER_CONTEXT,
         "result": {"cell": list(res.cell), "votes": res.votes, "n_inliers": res.n_inliers,
                    "q": [float(v) for v in res.q],
                    "rotation_error_deg": _rot_err_deg(pr.R, res.q)},
         "ms_per_step_median": float(sorted(step_ms)[len(step_ms) // 2]),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cells, dt = oracle_sample(pr, args.cpu_seconds)
-        line["cpu_baseline"] = {
-            "value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{cells} B=45 blocks x 1e6 correspondences ({cells * pr.n:.3g} pair votes, "
-                      f"{dt:.1f} s, one thread): the oracle's count loop on the solve's dominant "
-                      f"level", "cpu": _cpu_name()}
+        host = _host_info()
+        full = oracle_full_solve("cfg4") if args.cpu_full else None
+        if full is not None:
+            r0 = res
+            B = r0.B
+            lin = (r0.cell[0] * B + r0.cell[1]) * B + r0.cell[2]
+            line["cpu_baseline"] = {
+                "value": full["pairs"] / full["s"], "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"one complete certified solve of cfg4 by the oracle, pinned to core "
+                          f"{full['affinity']} (taskset): {full['cells']} blocks x 1e6 "
+                          f"correspondences, exact fp64 counts",
+                "ms_per_solve": 1e3 * full["s"],
+                "same_answer_as_gpu": (full["lin"], full["votes"], full["n_tied"]) ==
+                                      (lin, r0.votes, r0.n_tied),
+                **host}
+        else:
+            v, cells, dt = oracle_sample(pr, args.cpu_seconds)
+            line["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"{cells} B=45 blocks x 1e6 correspondences ({cells * pr.n:.3g} pair "
+                          f"votes, {dt:.1f} s, one thread): the oracle's count loop on the "
+                          f"solve's dominant level", **host}
     if rank == 0:
         print(json.dumps(line), flush=True)
     rv.close()

@@ -255,6 +255,7 @@ struct rv_ctx {
   // bitmask row table, the K3-C item planner's scratch, and its own event pairs
   bool cull_on = false;          // cfg.cull (with tensor_vote)
   bool cull_ready = false;       // this solve's level-0 bitmasks are written: levels >= 1 cull
+  bool ct_prefetched = false;    // K3-CT's gather table was prefetched into L2 this solve
   int64_t cull_min_n = 0;        // cull only problems of >= this many correspondences (the
                                  // largest of a batch)
   int32_t cull_B0 = 0;
@@ -1447,6 +1448,7 @@ int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
   // list lengths: the level-0 counts, or the union sizes the compaction counted
   ctx->cull_l0cnt = ctx->cull_grouped ? reinterpret_cast<const uint32_t*>(ctx->c_fill.p) : l0cnt;
   ctx->cull_ready = true;
+  ctx->ct_prefetched = false;
   return RV_OK;
 }
 
@@ -1499,6 +1501,14 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                                            ctx->c_lofs.p, ctx->k12.p, eps, mode, ctx->cfg.guard,
                                            ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, eb, mi,
                                            ctx->dp_err.p, s, ctx->cull_own_lo, ctx->cull_own_hi);
+#ifndef RV_CT_PREFETCH
+#define RV_CT_PREFETCH 1
+#endif
+    if (RV_CT_PREFETCH && ctx->cull_grouped && !ctx->ct_prefetched) {  // first culled level
+      rv::launch_l2_prefetch(ctx->tctab_rm.p, (ctx->tc_toff.back() + 8) * 64, s);
+      ctx->launches += 1;
+      ctx->ct_prefetched = true;
+    }
     cudaEvent_t e0, e1;
     RV_CUDA(ctx->cev_pair(&e0, &e1), "event");
     RV_CUDA(cudaEventRecord(e0, s), "event");

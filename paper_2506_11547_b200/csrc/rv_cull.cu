@@ -37,6 +37,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_fp16.h>
+#include <algorithm>
+
 #include <cuda_runtime.h>
 
 #include "../../include/rotvote.h"
@@ -1144,6 +1146,27 @@ __global__ void __launch_bounds__(kCtThreads)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
+}
+
+// Bring K3-CT's gather source (the row-major fp16-split table) into L2 ahead of the first culled
+// level: the level-0 bitmasks and the compaction's lists stream ~0.5 GB through L2 after K1-TC
+// wrote the table, so without this the first gathers of each row miss to DRAM and every stage
+// waits for its slowest row.  One cp.async.bulk.prefetch.L2 per 16 KB.
+__global__ void l2_prefetch_kernel(const uint8_t* __restrict__ p, int64_t bytes) {
+  constexpr int64_t kChunk = 16384;
+  for (int64_t off = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kChunk; off < bytes;
+       off += (int64_t)gridDim.x * blockDim.x * kChunk) {
+    const uint32_t n = (uint32_t)(bytes - off < kChunk ? bytes - off : kChunk) & ~15u;
+    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(n) : "memory");
+  }
+}
+
+void launch_l2_prefetch(const void* p, int64_t bytes, cudaStream_t s) {
+  if (!p || bytes <= 0) return;
+  const int64_t chunks = (bytes + 16383) / 16384;
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>(148, (chunks + threads - 1) / threads);
+  l2_prefetch_kernel<<<blocks, threads, 0, s>>>(static_cast<const uint8_t*>(p), bytes);
 }
 
 namespace {

@@ -192,6 +192,8 @@ void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P,
                          int64_t wpc_max, const int64_t* lofs, int32_t* fill, uint32_t* lidx,
                          cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = INT64_MAX,
                          const CullGroups& gr = CullGroups());
+// L2 prefetch of [p, p + bytes) (cp.async.bulk.prefetch.L2, 16 KB per request)
+void launch_l2_prefetch(const void* p, int64_t bytes, cudaStream_t s);
 
 
 // K4 (batched): level-0 reductions, one CTA per problem.  argmax: the dive's start index per
