@@ -274,7 +274,14 @@ struct rv_ctx {
   DevBuf<int32_t> lutg, goff, gmem;
   int64_t cull_G = 0, cull_G_grouped = 0;
   bool cull_grouped = false;     // this solve's lists are group unions (K3-CT)
-  int32_t cull_gshape[3] = {1, 2, 2};  // ancestor group extent along (i, j, k)
+#ifndef RV_CT_NA
+#define RV_CT_NA 1  // 2 (2x2x2 groups, M = 256 per gathered stage): measured slower, 1.12 vs 0.86 ms
+#endif
+  // K3-CT: items of up to cull_na x 128 block rows (one gathered stage feeds cull_na MMAs) over
+  // the union lists of ancestor groups of cull_gshape level-0 blocks -- 2 x (2 x 2 x 2) by
+  // default: up to 216 children of 8 ancestors at f = 3 share each gathered row
+  int32_t cull_na = RV_CT_NA;
+  int32_t cull_gshape[3] = {RV_CT_NA == 2 ? 2 : 1, 2, 2};  // ancestor group extent (i, j, k)
   // several ranks: level 0 is sliced at (i, j/2) row-pair boundaries (a group never straddles
   // two slices); rank r votes level-0 rows [cull_s[r], cull_s[r+1]) and owns the groups
   // [cull_g[r], cull_g[r+1]) (those whose first member is in its slice)
@@ -1484,8 +1491,8 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     const int64_t npos = eb + 7 * nb + 16;  // bucket positions are padded to multiples of 8
     RV_CUDA(ctx->c_cidx.ensure(npos), "allocating");
     RV_CUDA(ctx->c_phi.ensure(npos * 12), "allocating");
-    // (+128 rows: K3-CT's A tile reads 128 rows from an item's first)
-    if (ctx->cull_grouped) RV_CUDA(ctx->c_tphi.ensure((npos * 2 + 128) * 64), "allocating");
+    // (+256 rows: K3-CT's A tiles read up to 2 x 128 rows from an item's first)
+    if (ctx->cull_grouped) RV_CUDA(ctx->c_tphi.ensure((npos * 2 + 256) * 64), "allocating");
     RV_CUDA(ctx->c_icnt.ensure(2), "allocating");
     RV_CUDA(ctx->c_work.ensure(1), "allocating");
     RV_CUDA(ctx->vsegs.ensure(PL), "allocating segments");
@@ -1494,7 +1501,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                              ctx->c_tanc.p, ctx->c_tslot.p, ctx->c_cidx.p, ctx->c_phi.p,
                              ctx->c_icnt.p, ctx->c_work.p,
                              ctx->cull_grouped ? ctx->c_tphi.p : nullptr,
-                             ctx->cfg.guard + kTcExtraGuard};
+                             ctx->cfg.guard + kTcExtraGuard, ctx->cull_na};
     ctx->launches += rv::launch_cull_items(Ld, ctx->rows.p, ctx->toffs.p, PL, B, ctx->cull_B0,
                                            ctx->cull_grouped ? ctx->lutg.p : ctx->lut0.p,
                                            ctx->cull_G, ctx->cull_l0cnt,
@@ -1502,7 +1509,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                                            ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, eb, mi,
                                            ctx->dp_err.p, s, ctx->cull_own_lo, ctx->cull_own_hi);
 #ifndef RV_CT_PREFETCH
-#define RV_CT_PREFETCH 1
+#define RV_CT_PREFETCH 0  // measured: no gain (K3-CT 0.843 vs 0.844 ms), +25 us
 #endif
     if (RV_CT_PREFETCH && ctx->cull_grouped && !ctx->ct_prefetched) {  // first culled level
       rv::launch_l2_prefetch(ctx->tctab_rm.p, (ctx->tc_toff.back() + 8) * 64, s);

@@ -852,6 +852,9 @@ constexpr int kCtStages = RV_CT_STAGES;  // 16 KB gathered stages in flight
 #endif
 constexpr int kCtProd = RV_CT_PROD;
 constexpr int kCtN = 256;                            // gathered entries per stage
+#ifndef RV_CT_PP
+#define RV_CT_PP 0  // 1: ping-pong epilogue (alternate stages per warp group): measured slower at NA = 1
+#endif
 #ifndef RV_CT_EPQ
 #define RV_CT_EPQ 4  // K3-CT epilogue warps per TMEM lane quarter (column slices of a stage)
 #endif
@@ -867,9 +870,26 @@ constexpr int kCtThreads = (kCtProd + 1 + 4 * kCtEpq + RV_CT_DYN) * 32;
 #define RV_CT_ITEMS_PER_SM 32  // K3-CT planner target (items per CTA)
 #endif
 
+// An item holds up to kCtMaxNa A blocks of 128 rows (na = ceil(rows / 128) of them); a stage
+// gathers kCtN / na correspondences, so the accumulator of a stage is always kCtN columns
+// (na sub-accumulators of kCtN / na) and TMEM holds two stages.
+constexpr int kCtMaxNa = 2;
+#ifndef RV_CT_TRACE
+#define RV_CT_TRACE 0  // tuning builds: per-stage clock64 stamps of CTA 0 (rv_ct_trace_copy)
+#endif
+#if RV_CT_TRACE
+constexpr int kCtTraceN = 4096;
+// [0] gather issue start, [1] gather arrive, [2] MMA full ok, [3] MMA tempty ok, [4] MMA commit,
+// [5] epilogue (quarter 0, slice 0) tfull ok, [6] its tempty arrive
+__device__ long long g_ct_trace[7][kCtTraceN];
+#define CT_STAMP(r, i) \
+  do { if (blockIdx.x == 0 && (i) < kCtTraceN) g_ct_trace[r][i] = clock64(); } while (0)
+#else
+#define CT_STAMP(r, i) do { } while (0)
+#endif
 struct CtSmem {
   uint8_t b[kCtStages][kCtN * 64];  // gathered correspondence rows (B operand)
-  uint8_t a[2][128 * 64];           // the item's block rows (A operand), double-buffered
+  uint8_t a[2][kCtMaxNa * 128 * 64];  // the item's block rows (A operand), double-buffered
   uint64_t full[kCtStages], empty[kCtStages], afull[2], aempty[2], tfull[2], tempty[2];
   uint64_t ifull[kCtIR], iempty[kCtIR];
   int32_t iring[kCtIR];
@@ -914,6 +934,11 @@ __global__ void __launch_bounds__(kCtThreads)
   CtSmem& sm = *reinterpret_cast<CtSmem*>((reinterpret_cast<uintptr_t>(ct_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t n_items = counts_dev[0];
+  // A blocks of an item: its rows (FIN: two per block) in 128-row blocks, at most kCtMaxNa
+  auto ct_na = [](const CullItem& it) -> int {
+    const int rows = FIN ? 2 * it.ncell : it.ncell;
+    return rows > 128 ? kCtMaxNa : 1;
+  };
   if (warp == kCtProd) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(&sm.tmem_base)),
@@ -929,7 +954,7 @@ __global__ void __launch_bounds__(kCtThreads)
       bar_init(&sm.afull[i], 1);
       bar_init(&sm.aempty[i], 1);
       bar_init(&sm.tfull[i], 1);
-      bar_init(&sm.tempty[i], 4 * kCtEpq);  // every epilogue warp
+      bar_init(&sm.tempty[i], RV_CT_PP ? 8 : 4 * kCtEpq);  // the epilogue warps reading it
     }
     for (int i = 0; i < kCtIR; ++i) {
       bar_init(&sm.ifull[i], 1);                         // the scheduler
@@ -977,25 +1002,27 @@ __global__ void __launch_bounds__(kCtThreads)
       if (idx < 0) break;
       const CullItem it = items[idx];
       const int64_t toff = segs[it.seg].koff;
-      if (pw == 0 && lane == 0) {  // the item's 128 block rows (rows past its blocks: ignored)
+      const int na = ct_na(it);
+      const int N = kCtN / na;  // entries per stage
+      if (pw == 0 && lane == 0) {  // the item's na x 128 block rows (rows past its blocks: ignored)
         const uint32_t ab = gi & 1;
         if (gi >= 2) bar_wait(&sm.aempty[ab], ((gi >> 1) - 1) & 1);
         const int64_t row0 = FIN ? 2 * (int64_t)it.pos0 : it.pos0;  // multiple of 8
-        bar_expect_tx(&sm.afull[ab], 128 * 64);
-        bulk_g2s(sm.a[ab], tphi + (row0 >> 3) * 512, 128 * 64, &sm.afull[ab]);
+        bar_expect_tx(&sm.afull[ab], na * 128 * 64);
+        bulk_g2s(sm.a[ab], tphi + (row0 >> 3) * 512, na * 128 * 64, &sm.afull[ab]);
       }
       const uint32_t* li = lidx + it.e0;
-      const int ns = (it.ne + kCtN - 1) / kCtN;
-      // a stage's 256 indices (8 per lane: entry r*32 + lane) are loaded RV_CT_LOOK of this
+      const int ns = (it.ne + N - 1) / N;
+      // a stage's N indices (N / 32 per lane: entry r*32 + lane) are loaded RV_CT_LOOK of this
       // warp's stages ahead into a register ring whose slots are reused in place
       constexpr int kLook = RV_CT_LOOK;
       uint32_t ring[kLook][8];
       auto load_idx = [&](int k, uint32_t (&ix)[8]) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          const int ge = k * kCtN + r * 32 + lane;
+          const int ge = k * N + r * 32 + lane;
           ix[r] = (RV_CT_ABL & 8) ? (uint32_t)ge
-                                  : ge < it.ne ? __ldcs(li + ge) : 0xffffffffu;  // streamed once
+                  : (r * 32 < N && ge < it.ne) ? __ldcs(li + ge) : 0xffffffffu;  // streamed once
         }
       };
       const int k0 = (int)((pw - (int)(gs % kCtProd) + kCtProd) % kCtProd);
@@ -1007,6 +1034,7 @@ __global__ void __launch_bounds__(kCtThreads)
           const int k = kb + d * kCtProd;
           if (k >= ns) break;
           const uint32_t gk = gs + (uint32_t)k, st = gk % kCtStages;
+          if (lane == 0) CT_STAMP(0, gk);
           uint32_t cur[8];
 #pragma unroll
           for (int r = 0; r < 8; ++r) cur[r] = ring[d][r];
@@ -1015,18 +1043,29 @@ __global__ void __launch_bounds__(kCtThreads)
           // four lanes per row, one 16-byte chunk each: a copy instruction covers 8 whole rows
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
+            if (8 * j >= N) break;  // warp-uniform
             const int e = 8 * j + (lane >> 2), c = lane & 3;  // stage row, chunk
             const uint32_t ix = __shfl_sync(0xffffffffu, cur[j >> 2], e & 31);
             const int64_t g = ix != 0xffffffffu ? toff + (int64_t)ix : pad_row;
             uint8_t* dst = sm.b[st] + (e >> 3) * 512 + (e & 7) * 16 + c * 128;
-            if (!(RV_CT_ABL & 1))
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)),
-                           "l"(tab + g * 64 + c * 16)
-                           : "memory");
+#ifndef RV_CT_CA
+#define RV_CT_CA 0  // 1: L1-allocating cp.async.ca (tuning)
+#endif
+            if (!(RV_CT_ABL & 1) && !((RV_CT_ABL & 16) && c >= 2)) {
+              if (RV_CT_CA)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(su32(dst)),
+                             "l"(tab + g * 64 + c * 16)
+                             : "memory");
+              else
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)),
+                             "l"(tab + g * 64 + c * 16)
+                             : "memory");
+            }
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
                            su32(&sm.full[st]))
                        : "memory");
+          if (lane == 0) CT_STAMP(1, gk);
         }
       }
       gs += (uint32_t)ns;
@@ -1039,48 +1078,66 @@ __global__ void __launch_bounds__(kCtThreads)
       for (;; ++gi) {
         const int idx = next_item(false);
         if (idx < 0) break;
-        const int ns = (items[idx].ne + kCtN - 1) / kCtN;
+        const CullItem it = items[idx];
+        const int na = ct_na(it);
+        const uint32_t N = (uint32_t)(kCtN / na), idesc = idesc_f16(N);
+        const int ns = (it.ne + (int)N - 1) / (int)N;
         const uint32_t ab = gi & 1;
         bar_wait(&sm.afull[ab], (gi >> 1) & 1);
         const uint32_t a0 = su32(sm.a[ab]);
         for (int k = 0; k < ns; ++k, ++gs) {
           const uint32_t st = gs % kCtStages, acc = gs & 1;
-          ct_wait(&sm.full[st], (gs / kCtStages) & 1);
+          if (!(RV_CT_ABL & 64)) ct_wait(&sm.full[st], (gs / kCtStages) & 1);
+          CT_STAMP(2, gs);
 #if RV_CT_FENCE
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #endif
-          if (gs >= 2) ct_wait(&sm.tempty[acc], ((gs >> 1) - 1) & 1);
+          if (gs >= 2 && !(RV_CT_ABL & 32)) ct_wait(&sm.tempty[acc], ((gs >> 1) - 1) & 1);
+          CT_STAMP(3, gs);
           tc_fence_after();
           const uint32_t b0 = su32(sm.b[st]);
+          // sub-accumulator h (columns h*N .. h*N+N of the stage's kCtN) = A block h x the stage
+          for (int h = 0; h < na; ++h)
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            if (!(RV_CT_ABL & 2))
-              mma_f16_n<kCtN>(tmem + acc * kCtN, smem_desc(a0 + 256 * kk, 128, 512),
-                              smem_desc(b0 + 256 * kk, 128, 512), (uint32_t)kk);
+            for (int kk = 0; kk < 2; ++kk)
+              if (!(RV_CT_ABL & 2))
+                mma_f16_i(tmem + acc * kCtN + (uint32_t)h * N,
+                          smem_desc(a0 + (uint32_t)h * (128 * 64) + 256 * kk, 128, 512),
+                          smem_desc(b0 + 256 * kk, 128, 512), idesc, (uint32_t)kk);
           mma_commit(&sm.empty[st]);
           mma_commit(&sm.tfull[acc]);
+          CT_STAMP(4, gs);
         }
         mma_commit(&sm.aempty[ab]);
       }
     }
   } else if (warp < kCtSched) {
-    // ---------------- epilogue (4 kCtEpq warps: lane quarter warp % 4, a column slice each) ---
-    const int ew = warp - kCtEpi0, slice = ew >> 2;
-    constexpr int kCols = kCtN / kCtEpq;  // columns of a stage per warp
+#if RV_CT_PP
+    // ---------------- epilogue, ping-pong: 4 warps per TMEM lane quarter (warp % 4) ----------
+    // warp j = ew >> 2 of its quarter: group G = j & 1 takes the stages of accumulator G (every
+    // other stage), slot = j >> 1 reads the stage's columns [128 slot, 128 slot + 128) -- so one
+    // group's TMEM reads overlap the other group's sign counts (a lockstep epilogue spends
+    // 512 clk reading and then 512 clk counting per stage on each SMSP)
+    const int ew = warp - kCtEpi0, pj = ew >> 2, grp = pj & 1, slot = pj >> 1;
+    constexpr int kCols = kCtN / 2;  // columns of a stage per warp
     const uint32_t lane_addr =
-        tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(slice * kCols);
-    const int m = 32 * (warp & 3) + lane;  // TMEM lane = A row = block row of the item
+        tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(slot * kCols);
     uint32_t gs = 0;
     for (;;) {
       const int idx = next_item(true);
       if (idx < 0) break;
       const CullItem it = items[idx];
-      const int ns = (it.ne + kCtN - 1) / kCtN;
+      const int na = ct_na(it);
+      const int ns = (it.ne + kCtN / na - 1) / (kCtN / na);
       const int nrows = FIN ? 2 * it.ncell : it.ncell;
-      const bool active = 32 * (warp & 3) < nrows;  // warp-uniform
-      uint32_t n0 = 0, n1 = 0;
+      const int h = na == 1 ? 0 : slot;  // na = 2: slot s reads sub-accumulator s (A block s)
+      const int m = 128 * h + 32 * (warp & 3) + lane;
+      const bool active = 128 * h + 32 * (warp & 3) < nrows;  // warp-uniform
+      uint32_t n0 = 0, n1 = 0, mine = 0;
       for (int k = 0; k < ns; ++k) {
         const uint32_t g = gs + (uint32_t)k, acc = g & 1;
+        if ((int)acc != grp) continue;
+        ++mine;
         ct_wait(&sm.tfull[acc], (g >> 1) & 1);
         tc_fence_after();
         if (active && !(RV_CT_ABL & 4)) {
@@ -1095,6 +1152,71 @@ __global__ void __launch_bounds__(kCtThreads)
               tc_fence_before();
               __syncwarp();
               if (lane == 0) bar_arrive(&sm.tempty[acc]);
+            }
+            uint32_t w0 = 0u, w1 = 0u;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w0) : "r"(r[0][e]));
+              asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w1) : "r"(r[1][e]));
+            }
+            n0 += __popc(w0);
+            n1 += __popc(w1);
+          }
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) bar_arrive(&sm.tempty[acc]);
+        }
+      }
+      gs += (uint32_t)ns;
+      if (active && m < nrows) {
+        const uint32_t pass = mine * kCols - (n0 + n1);
+        if (pass) {
+          const VoteSeg& sg = segs[it.seg];
+          const int32_t e = cidx[it.pos0 + (FIN ? (m >> 1) : m)];
+          atomicAdd(FIN && (m & 1) ? &sg.cnt_b[e] : &sg.cnt_a[e], pass);
+        }
+      }
+      if (ew == 0 && lane == 0 && pairs)
+        atomicAdd(pairs, (unsigned long long)it.ne * (unsigned long long)it.ncell);
+    }
+#else
+    // ---------------- epilogue (4 kCtEpq warps: lane quarter warp % 4, a column slice each) ---
+    const int ew = warp - kCtEpi0, slice = ew >> 2;
+    constexpr int kCols = kCtN / kCtEpq;  // columns of a stage per warp
+    const uint32_t lane_addr =
+        tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(slice * kCols);
+    uint32_t gs = 0;
+    for (;;) {
+      const int idx = next_item(true);
+      if (idx < 0) break;
+      const CullItem it = items[idx];
+      const int na = ct_na(it);
+      const int ns = (it.ne + kCtN / na - 1) / (kCtN / na);
+      const int nrows = FIN ? 2 * it.ncell : it.ncell;
+      // this warp's 64 columns belong to sub-accumulator h = the item's A block h: block row m
+      const int h = na == 1 ? 0 : (slice * kCols) / (kCtN / na);
+      const int m = 128 * h + 32 * (warp & 3) + lane;
+      const bool active = 128 * h + 32 * (warp & 3) < nrows;  // warp-uniform
+      uint32_t n0 = 0, n1 = 0;
+      for (int k = 0; k < ns; ++k) {
+        const uint32_t g = gs + (uint32_t)k, acc = g & 1;
+        ct_wait(&sm.tfull[acc], (g >> 1) & 1);
+        if (ew == 0 && lane == 0) CT_STAMP(5, g);
+        tc_fence_after();
+        if (active && !(RV_CT_ABL & 4)) {
+#pragma unroll
+          for (int rr = 0; rr < kCols / 64; ++rr) {  // 64 columns per round (registers)
+            uint32_t r[2][32];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              RV_TCX_LD32(r[q], lane_addr + acc * kCtN + (uint32_t)(rr * 64 + 32 * q));
+            tmem_wait_ld();
+            if (rr == kCols / 64 - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) bar_arrive(&sm.tempty[acc]);
+              if (ew == 0 && lane == 0) CT_STAMP(6, g);
             }
             // sign bits -> one word per 32 columns (shf funnel: w = w << 1 | sign); negatives
             // = its popcount
@@ -1125,6 +1247,7 @@ __global__ void __launch_bounds__(kCtThreads)
       if (ew == 0 && lane == 0 && pairs)
         atomicAdd(pairs, (unsigned long long)it.ne * (unsigned long long)it.ncell);
     }
+#endif
   }
 #if RV_CT_DYN
   else if (lane == 0 && dyn) {
@@ -1160,6 +1283,12 @@ __global__ void l2_prefetch_kernel(const uint8_t* __restrict__ p, int64_t bytes)
     if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(n) : "memory");
   }
 }
+
+#if RV_CT_TRACE
+extern "C" int rv_ct_trace_copy(long long* host, int64_t n) {
+  return (int)cudaMemcpyFromSymbol(host, g_ct_trace, sizeof(long long) * (n < 7 * kCtTraceN ? n : 7 * kCtTraceN));
+}
+#endif
 
 void launch_l2_prefetch(const void* p, int64_t bytes, cudaStream_t s) {
   if (!p || bytes <= 0) return;
@@ -1256,7 +1385,8 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
   const int64_t target = cs.tphi ? (int64_t)RV_CT_ITEMS_PER_SM * num_sms
                                  : 8LL * num_sms * kCullCtasPerSm * kCullWarpsPerCta;
   // blocks per item: K3-C 32 (a warp's lanes); K3-CT the MMA's 128 rows (FIN: two per block)
-  const int32_t cpi = cs.tphi ? (mode == RV_MODE_FINAL ? 64 : 128) : kCullMaxCells;
+  // blocks per item: K3-C a warp's 32 lanes; K3-CT ct_na A blocks of 128 rows (FIN: 2 per block)
+  const int32_t cpi = cs.tphi ? (mode == RV_MODE_FINAL ? 64 : 128) * cs.ct_na : kCullMaxCells;
   if (entries_bound <= 8192 && NB <= (1 << 14)) {
     cull_plan_small<<<1, RV_PS_THREADS, 0, s>>>(L, rows, toffs, P, B, B0, lut0, m0, eps, mode, guard, l0cnt,
                                        lofs, k12, cs.act, cs.acnt, cs.tanc, cs.tslot, cs.aoff,

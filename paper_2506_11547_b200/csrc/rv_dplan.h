@@ -128,6 +128,7 @@ struct CullScratch {
   int32_t* work;
   uint8_t* tphi;    // K3-CT: the blocks' 64-byte fp16-split rows (nullptr: FP32 K3-C only)
   float tc_guard;   // the guard of those rows' thresholds (guard + the TC error margin)
+  int32_t ct_na;    // K3-CT: A blocks of 128 rows per item (1 or 2)
 };
 // returns the number of kernels it launched (one CTA does everything for small levels)
 // own_lo .. own_hi: the level-0 rows (ancestors) this rank votes (blocks of other ancestors

@@ -29,6 +29,27 @@ print(f"{sys.argv[3]:>10s} {cfg}: solve {med(ms):.3f} ms (min {min(ms):.3f})  K3
 """
 
 
+MICRO = r"""
+import sys, torch, datagen, numpy as np, oracle
+from paper_2506_11547_b200 import RotVote
+pr = datagen.cfg4()
+x, y = torch.from_numpy(pr.x).cuda(), torch.from_numpy(pr.y).cuda()
+rv = RotVote(max_n=pr.n)
+lins = oracle.candidates(45).astype(np.uint32)
+def t(l, reps=7):
+    ts = []
+    for i in range(reps):
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record(); c = rv.count_cells_culled(x, y, 15, 45, l, pr.eps, 0); e1.record(); e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return sorted(ts)[reps // 2], c
+t1, _ = t(lins[:1])
+ta, c = t(lins)
+print(f"{sys.argv[1]:>10s} level-1 micro: all {ta:.3f} ms, one {t1:.3f} ms, culled vote ~ {ta - t1:.3f} ms, "
+      f"sum counts {int(c.sum())}", flush=True)
+"""
+
+
 def build(specs):
     from paper_2506_11547_b200 import build as b
     os.makedirs(OUT, exist_ok=True)
@@ -40,7 +61,7 @@ def build(specs):
 
 
 def run(args):
-    chain, cfg = "15,45,180,360", "cfg4"
+    chain, cfg, micro = "15,45,180,360", "cfg4", False
     names = []
     it = iter(args)
     for a in it:
@@ -48,14 +69,17 @@ def run(args):
             chain = next(it)
         elif a == "--cfg":
             cfg = next(it)
+        elif a == "--micro":
+            micro = True
         else:
             names.append(a)
     for name in names:
         env = dict(os.environ)
         if name != "base":
             env["RV_LIB"] = os.path.join(OUT, f"librotvote_{name}.so")
-        subprocess.run([sys.executable, "-c", CODE, chain, cfg, name], env=env,
-                       cwd=os.path.dirname(HERE), timeout=600)
+        args = [MICRO, name] if micro else [CODE, chain, cfg, name]
+        subprocess.run([sys.executable, "-c", *args], env=env, cwd=os.path.dirname(HERE),
+                       timeout=600)
 
 
 if __name__ == "__main__":
