@@ -12,7 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "librotvote.so")
-SOURCES = ["rv_kernels.cu", "rv_vote_tc.cu", "rv_dplan.cu", "rv_cull.cu", "rv_alg1.cu", "rv_rigid.cu", "rv_api.cpp", "rv_plan.cpp"]
+SOURCES = ["rv_kernels.cu", "rv_vote_tc.cu", "rv_dplan.cu", "rv_cull.cu", "rv_alg1.cu", "rv_rigid.cu",
+           "rv_api.cpp", "rv_setup.cpp", "rv_host_plan.cpp", "rv_level_loop.cpp", "rv_plan.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -247,8 +247,15 @@ __global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__
                                                     const int32_t* __restrict__ gmem,
                                                     int64_t row_lo, int64_t NR, int64_t nseg,
                                                     const int64_t* __restrict__ lofs,
-                                                    int32_t* fill, uint32_t* idx) {
+                                                    int32_t* fill, uint32_t* idx, int64_t NB,
+                                                    int64_t cap, int32_t* err) {
   __shared__ uint32_t sstage[8][kCompactStage];
+  // one-pass solves size the lists by a fixed capacity: longer lists raise the error word (the
+  // solve is then redone with the total read back) and nothing is written
+  if (cap > 0 && lofs[NB] > cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(err, 16);
+    return;
+  }
   uint32_t* stage = sstage[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -1360,7 +1367,8 @@ void launch_cull_rows(const uint32_t* l0cnt, int32_t P, int64_t m0, int64_t* lof
 
 void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P, int64_t m0,
                          int64_t wpc_max, const int64_t* lofs, int32_t* fill, uint32_t* lidx,
-                         cudaStream_t s, int64_t row_lo, int64_t row_hi, const CullGroups& gr) {
+                         cudaStream_t s, int64_t row_lo, int64_t row_hi, const CullGroups& gr,
+                         int64_t cap, int32_t* err) {
   const int64_t G = gr.goff ? gr.G : m0;
   const int64_t NB = (int64_t)P * G, nseg = (wpc_max + kCompactSeg - 1) / kCompactSeg;
   if (row_hi > NB) row_hi = NB;
@@ -1370,7 +1378,7 @@ void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P,
   int64_t blocks = (NR * nseg + 7) / 8;
   if (blocks > 148 * 32) blocks = 148 * 32;
   cull_compact<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(
-      bits0, toffs, m0, G, gr.goff, gr.gmem, row_lo, NR, nseg, lofs, fill, lidx);
+      bits0, toffs, m0, G, gr.goff, gr.gmem, row_lo, NR, nseg, lofs, fill, lidx, NB, cap, err);
 }
 
 int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,

@@ -563,36 +563,46 @@ __global__ void dp_items_write(DpList L, const int64_t* __restrict__ rows, int32
   }
 }
 
-__global__ void __launch_bounds__(kPlanThreads) dp_scan(const int32_t* __restrict__ cnt, int32_t P,
+__global__ void __launch_bounds__(kPlanThreads) dp_scan(int32_t* cnt, int32_t P,
                                                         int64_t f3, int64_t* act,
                                                         int64_t* next_base, int64_t* total,
-                                                        RediveCheck rc) {
+                                                        RediveCheck rc, OnePass op) {
   __shared__ int64_t sh[kPlanThreads];
+  __shared__ int32_t s_abort;
   const int t = threadIdx.x;
   const int p0 = (int)((int64_t)P * t / kPlanThreads), p1 = (int)((int64_t)P * (t + 1) / kPlanThreads);
-  int64_t v = 0;
   for (int p = p0; p < p1; ++p) {
-    v += cnt[p];
     if (rc.flags) {  // re-dive trigger (R18), once per problem
       const int32_t fl = (!rc.done[p] && rc.pcnt[p] > 0 && cnt[p] >= 16384 &&
                           2 * (int64_t)cnt[p] > (int64_t)rc.pcnt[p] * rc.f3) ? 1 : 0;
       rc.flags[p] = fl;
       if (fl) {
         rc.done[p] = 1;
-        atomicOr(rc.any, 1);
+        atomicOr(rc.any, rc.any_bit);
       }
     }
   }
+  // one-pass solve: a raised error word (capacity, or the re-dive the one-pass loop does not
+  // take) empties this level, so every later launch has nothing to do; the host redoes the solve
+  if (t == 0) s_abort = op.err ? *reinterpret_cast<volatile int32_t*>(op.err) : 0;
+  __syncthreads();
+  const bool abort = s_abort != 0;
+  int64_t v = 0;
+  for (int p = p0; p < p1; ++p) {
+    if (abort) cnt[p] = 0;
+    v += cnt[p];
+  }
   int64_t tot;
   int64_t e = cta_scan_excl(v, sh, &tot);
+  auto clamp = [&](int64_t b) { return op.cap_lim > 0 && b > op.cap_lim ? op.cap_lim : b; };
   for (int p = p0; p < p1; ++p) {
     act[p] = e;
-    if (next_base) next_base[p] = e * f3;
+    if (next_base) next_base[p] = clamp(e * f3);
     e += cnt[p];
   }
   if (t == 0) {
     act[P] = tot;
-    if (next_base) next_base[P] = tot * f3;
+    if (next_base) next_base[P] = clamp(tot * f3);
     *total = tot;
   }
 }
@@ -738,10 +748,11 @@ void dp_items_bound(int mode, int64_t entries, int32_t P, int64_t nmax, int32_t 
   *max_ablocks = cbs;
 }
 
-void dp_launch_scan(const int32_t* cnt, int32_t P, int64_t f3, int64_t* act, int64_t* next_base,
-                    int64_t* total, cudaStream_t s, const RediveCheck* rc) {
+void dp_launch_scan(int32_t* cnt, int32_t P, int64_t f3, int64_t* act, int64_t* next_base,
+                    int64_t* total, cudaStream_t s, const RediveCheck* rc, const OnePass* op) {
   dp_scan<<<1, kPlanThreads, 0, s>>>(cnt, P, f3, act, next_base, total,
-                                    rc ? *rc : RediveCheck{nullptr, 0, nullptr, nullptr, nullptr});
+                                    rc ? *rc : RediveCheck{nullptr, 0, nullptr, nullptr, nullptr, 1},
+                                    op ? *op : OnePass{nullptr, 0});
 }
 
 namespace {

@@ -49,11 +49,21 @@ struct RediveCheck {
   int32_t* done;
   int32_t* flags;
   int32_t* any;
+  int32_t any_bit;  // OR-ed into *any when a problem triggers
+};
+// One-pass single solve (no host round trip per level): err = the solve's error word -- when it
+// is nonzero the scan empties the level (counts and offsets 0), so the rest of the solve does
+// nothing and the host redoes it with per-level round trips; cap_lim > 0 clamps next_base to
+// the fixed capacity of the next level's arrays (one problem: its region is [0, cap_lim)).
+struct OnePass {
+  int32_t* err;
+  int64_t cap_lim;
 };
 // act[p] = exclusive prefix of cnt (act[P] = total, also written to *total); next_base[p] =
 // act[p] * f3 (optional); rc: also evaluate the re-dive trigger
-void dp_launch_scan(const int32_t* cnt, int32_t P, int64_t f3, int64_t* act, int64_t* next_base,
-                    int64_t* total, cudaStream_t s, const RediveCheck* rc = nullptr);
+void dp_launch_scan(int32_t* cnt, int32_t P, int64_t f3, int64_t* act, int64_t* next_base,
+                    int64_t* total, cudaStream_t s, const RediveCheck* rc = nullptr,
+                    const OnePass* op = nullptr);
 
 // dive: candidate children (Bc = f*Bp) of the 27-neighbourhood of the pick (pick[p], or
 // idx_list[pick_idx[p]] if idx_list != nullptr), at out + p*cap

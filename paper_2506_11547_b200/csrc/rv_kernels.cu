@@ -12,6 +12,7 @@
 // (Appendix A) with K_i traceless, so 9 numbers per correspondence suffice:
 //   s = phi(q) . k,  phi = [q0²-q3², q1²-q3², q2²-q3², 2q0q1, 2q0q2, 2q0q3, 2q1q2, 2q1q3, 2q2q3].
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "../../include/rotvote.h"
@@ -566,6 +567,54 @@ __device__ void jacobi4(double A[4][4], double V[4][4]) {
   }
 }
 
+// One refinement step from the inlier sums S (9 entries of sum K_i, count): flags | RV_REFINED and
+// q <- the hemisphere-canonical top eigenvector, or flags | RV_DEGENERATE | kStop (fewer than 2
+// inliers, or eigengap <= 1e-12 |lambda1|: q kept, later rounds skipped, reading R8)
+__device__ int32_t eig_update(const double S[10], int32_t fl, double* q) {
+  const double count = S[9];
+  if (fl & kStop) return fl;
+  if (count < 2.0) return fl | RV_DEGENERATE | kStop;
+  // S = sum K_i over inliers; K33 = -(K00 + K11 + K22) by tracelessness
+  double A[4][4] = {{S[0], S[3], S[4], S[5]},
+                    {S[3], S[1], S[6], S[7]},
+                    {S[4], S[6], S[2], S[8]},
+                    {S[5], S[7], S[8], -(S[0] + S[1] + S[2])}};
+  double V[4][4];
+  jacobi4(A, V);
+  // the largest eigenvalue and its column, selected with constant indices only (a dynamic
+  // index would put A and V in local memory for the whole solve)
+  double d[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) d[r] = A[r][r];
+  int i0 = 0;
+  double l1 = d[0];
+#pragma unroll
+  for (int r = 1; r < 4; ++r)
+    if (d[r] > l1) { l1 = d[r]; i0 = r; }
+  double l2 = -1e300;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    if (r != i0 && d[r] > l2) l2 = d[r];
+  if (l1 - l2 <= 1e-12 * fabs(l1)) return fl | RV_DEGENERATE | kStop;
+  double v[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+    v[a] = i0 == 0 ? V[a][0] : i0 == 1 ? V[a][1] : i0 == 2 ? V[a][2] : V[a][3];
+  const double nv = rsqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3]);
+  // hemisphere representative: q3 < 0; |q3| <= 1e-15 -> first nonzero of q0..q2 positive
+  bool flip;
+  if (v[3] * nv < -1e-15) flip = false;
+  else if (v[3] * nv > 1e-15) flip = true;
+  else {
+    flip = false;
+    for (int a = 0; a < 3; ++a)
+      if (v[a] != 0.0) { flip = v[a] < 0.0; break; }
+  }
+  const double sgn = flip ? -nv : nv;
+  for (int a = 0; a < 4; ++a) q[a] = v[a] * sgn;
+  return fl | RV_REFINED;
+}
+
 // One warp per problem (8 per CTA; per_cta: one CTA per problem, for small batches, so the
 // partials of a 1e6-row problem are summed by 256 threads): the lanes sum the problem's K6
 // partials in a fixed order, lane 0 solves.
@@ -608,54 +657,7 @@ __global__ void __launch_bounds__(256) rv_eig_kernel(const RefSeg* __restrict__ 
     ninl[p] = (uint32_t)count;
     return;
   }
-  int32_t fl = flags[p];
-  if (fl & kStop) return;
-  if (count < 2.0) {
-    flags[p] = fl | RV_DEGENERATE | kStop;
-    return;
-  }
-  // S = sum K_i over inliers; K33 = -(K00 + K11 + K22) by tracelessness
-  double A[4][4] = {{S[0], S[3], S[4], S[5]},
-                    {S[3], S[1], S[6], S[7]},
-                    {S[4], S[6], S[2], S[8]},
-                    {S[5], S[7], S[8], -(S[0] + S[1] + S[2])}};
-  double V[4][4];
-  jacobi4(A, V);
-  // the largest eigenvalue and its column, selected with constant indices only (a dynamic
-  // index would put A and V in local memory for the whole solve)
-  double d[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) d[r] = A[r][r];
-  int i0 = 0;
-  double l1 = d[0];
-#pragma unroll
-  for (int r = 1; r < 4; ++r)
-    if (d[r] > l1) { l1 = d[r]; i0 = r; }
-  double l2 = -1e300;
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-    if (r != i0 && d[r] > l2) l2 = d[r];
-  if (l1 - l2 <= 1e-12 * fabs(l1)) {
-    flags[p] = fl | RV_DEGENERATE | kStop;
-    return;
-  }
-  double v[4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-    v[a] = i0 == 0 ? V[a][0] : i0 == 1 ? V[a][1] : i0 == 2 ? V[a][2] : V[a][3];
-  const double nv = rsqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3]);
-  // hemisphere representative: q3 < 0; |q3| <= 1e-15 -> first nonzero of q0..q2 positive
-  bool flip;
-  if (v[3] * nv < -1e-15) flip = false;
-  else if (v[3] * nv > 1e-15) flip = true;
-  else {
-    flip = false;
-    for (int a = 0; a < 3; ++a)
-      if (v[a] != 0.0) { flip = v[a] < 0.0; break; }
-  }
-  const double sgn = flip ? -nv : nv;
-  for (int a = 0; a < 4; ++a) qs[4 * p + a] = v[a] * sgn;
-  flags[p] = fl | RV_REFINED;
+  flags[p] = eig_update(S, flags[p], qs + 4 * p);
 }
 
 void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* qs, int32_t* flags,
@@ -667,6 +669,149 @@ void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* q
     rv_eig_kernel<<<(P + 7) / 8, 256, 0, s>>>(segs, partials, qs, flags, ninl, mode, P, 0);
 }
 
+
+// ------------------------------------------------------------------------------------------
+// K6+K7 fused for ONE problem (the one-pass single solve): the rounds of R8 and the final mask in
+// one cooperative launch (grid-wide barriers instead of launch boundaries).  q0 is the winner's
+// block centre decoded on the device from the winner key (count << 32 | ~lin), so the solve needs
+// no host round trip between the vote and the refinement.  The inlier test screens every row
+// with the fp32 K table of K1 against cos(eps) -/+ guard (|s32 - s| <= 2.7e-6 < guard, DESIGN R10)
+// and decides the rows inside the band in fp64 from x, y exactly as K6 does; the inliers' fp64
+// K_i are summed in a fixed order (warp butterflies, CTA partials in block order).
+// ------------------------------------------------------------------------------------------
+constexpr int kR1Threads = 256;
+
+__global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double ws[kR1Threads / 32][10];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double q[4] = {0.0, 0.0, 0.0, -1.0};
+    if (a.q0) {
+      const double nq = sqrt(a.q0[0] * a.q0[0] + a.q0[1] * a.q0[1] + a.q0[2] * a.q0[2] +
+                             a.q0[3] * a.q0[3]);
+      for (int c = 0; c < 4; ++c) q[c] = a.q0[c] / nq;
+    } else {
+      const unsigned long long key = *a.best;
+      if (key) {  // (no winner only when the solve was abandoned; the host redoes it)
+        const uint32_t lin = 0xffffffffu - (uint32_t)(key & 0xffffffffull);
+        int32_t i, j, k;
+        lin_to_ijk(lin, a.B, i, j, k);
+        cell_quat(a.B, i, j, k, q);
+      }
+    }
+    bool flip;  // hemisphere representative (R9), as the host's canonicalize
+    if (q[3] < -1e-15) flip = false;
+    else if (q[3] > 1e-15) flip = true;
+    else {
+      flip = false;
+      for (int c = 0; c < 3; ++c)
+        if (q[c] != 0.0) { flip = q[c] < 0.0; break; }
+    }
+    for (int c = 0; c < 4; ++c) a.q[c] = flip ? -q[c] : q[c];
+    *a.flags = 0;
+  }
+  grid.sync();
+  const float t_hi = (float)(a.tau + (double)a.guard), t_lo = (float)(a.tau - (double)a.guard);
+  const int64_t gthreads = (int64_t)gridDim.x * kR1Threads;
+  for (int r = 0; r <= a.rounds; ++r) {
+    const bool last = r == a.rounds;
+    double q[4];
+    for (int c = 0; c < 4; ++c) q[c] = reinterpret_cast<volatile double*>(a.q)[c];
+    double f[9];
+    phi9(q, f);
+    float f32[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) f32[t] = (float)f[t];
+    double acc[10];
+#pragma unroll
+    for (int t = 0; t < 10; ++t) acc[t] = 0.0;
+    for (int64_t base = ((int64_t)blockIdx.x * kR1Threads + warp * 32); base < a.n; base += gthreads) {
+      const int64_t i = base + lane;
+      bool in = false, band = false;
+      if (i < a.n) {
+        float s32 = 0.0f;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) s32 = fmaf(f32[t], __ldg(a.k9 + t * a.stride + i), s32);
+        in = s32 >= t_hi;
+        band = !in && s32 >= t_lo;
+      }
+      double k[9];
+      if (in || band) {  // fp64 K_i from the raw row (the sums, and the band's exact decision)
+        double xa[3] = {a.x[3 * i], a.x[3 * i + 1], a.x[3 * i + 2]};
+        double yb[3] = {a.y[3 * i], a.y[3 * i + 1], a.y[3 * i + 2]};
+        const double ia = 1.0 / sqrt(xa[0] * xa[0] + xa[1] * xa[1] + xa[2] * xa[2]);
+        const double ib = 1.0 / sqrt(yb[0] * yb[0] + yb[1] * yb[1] + yb[2] * yb[2]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { xa[c] *= ia; yb[c] *= ib; }
+        k9_of(xa, yb, k);
+        if (band) {
+          double s = 0.0;
+#pragma unroll
+          for (int t = 0; t < 9; ++t) s = fma(f[t], k[t], s);
+          in = s >= a.tau;
+        }
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, in);
+      if (last && a.mask && lane == 0) a.mask[base >> 5] = bal;
+      if (in) {
+#pragma unroll
+        for (int t = 0; t < 9; ++t) acc[t] += k[t];
+        acc[9] += 1.0;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 10; ++t)
+      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_down_sync(0xffffffffu, acc[t], o);
+    if (lane == 0)
+#pragma unroll
+      for (int t = 0; t < 10; ++t) ws[warp][t] = acc[t];
+    __syncthreads();
+    if (threadIdx.x < 10) {
+      double v = 0.0;
+      for (int w = 0; w < kR1Threads / 32; ++w) v += ws[w][threadIdx.x];
+      a.partials[(int64_t)blockIdx.x * 10 + threadIdx.x] = v;
+    }
+    grid.sync();
+    if (blockIdx.x == 0 && warp == 0) {
+      double S[10];
+#pragma unroll
+      for (int t = 0; t < 10; ++t) S[t] = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32)
+#pragma unroll
+        for (int t = 0; t < 10; ++t) S[t] += a.partials[(int64_t)b * 10 + t];
+#pragma unroll
+      for (int t = 0; t < 10; ++t)
+        for (int o = 16; o > 0; o >>= 1) S[t] += __shfl_down_sync(0xffffffffu, S[t], o);
+      if (lane == 0) {
+        if (last) *a.ninl = (uint32_t)S[9];
+        else *a.flags = eig_update(S, *a.flags, a.q);
+      }
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.flags &= (RV_REFINED | RV_DEGENERATE);
+}
+
+cudaError_t launch_refine1(const Refine1Args& a, int num_sms, cudaStream_t s) {
+  static int per_sm[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (per_sm[dev] == 0) {
+    int b = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rv_refine1_kernel, kR1Threads, 0);
+    if (e != cudaSuccess) return e;
+    per_sm[dev] = b < 1 ? 1 : (b > 4 ? 4 : b);
+  }
+  const int grid = num_sms * per_sm[dev];
+  if (grid > kRefine1MaxCtas) return cudaErrorInvalidConfiguration;
+  Refine1Args args = a;
+  void* kargs[] = {&args};
+  return cudaLaunchCooperativeKernel((const void*)rv_refine1_kernel, dim3(grid), dim3(kR1Threads),
+                                     kargs, 0, s);
+}
 }  // namespace rv
 
 namespace rv {

@@ -191,7 +191,9 @@ void launch_cull_rows(const uint32_t* l0cnt, int32_t P, int64_t m0, int64_t* lof
 void launch_cull_compact(const uint32_t* bits0, const int64_t* toffs, int32_t P, int64_t m0,
                          int64_t wpc_max, const int64_t* lofs, int32_t* fill, uint32_t* lidx,
                          cudaStream_t s, int64_t row_lo = 0, int64_t row_hi = INT64_MAX,
-                         const CullGroups& gr = CullGroups());
+                         const CullGroups& gr = CullGroups(), int64_t cap = 0,
+                         int32_t* err = nullptr);
+// (cap > 0: lists longer than cap entries in total raise bit 16 of *err and write nothing)
 // L2 prefetch of [p, p + bytes) (cp.async.bulk.prefetch.L2, 16 KB per request)
 void launch_l2_prefetch(const void* p, int64_t bytes, cudaStream_t s);
 
@@ -223,5 +225,31 @@ void launch_inliers(const float* x, const float* y, const RefSeg* segs, const Re
 // step (cyclic Jacobi, fp64) updating qs/flags; mode 1: write the inlier count only.
 void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* qs,
                 int32_t* flags, uint32_t* ninl, int mode, cudaStream_t s);
+
+// K6+K7 fused for one problem (cooperative launch, grid-wide barriers between the passes):
+// `rounds` refinement rounds from q0 (HOST-independent: q0 != nullptr DEVICE double[4], else the
+// centre of the winner decoded from *best at resolution B), then the final mask / count.
+// Writes q[4], *flags (RV_REFINED | RV_DEGENERATE), *ninl, mask (DEVICE, may be null).
+// partials: DEVICE double [kRefine1MaxCtas * 10].
+constexpr int kRefine1MaxCtas = 148 * 8;
+struct Refine1Args {
+  const float* x;
+  const float* y;
+  int64_t n;
+  const float* k9;       // K1's fp32 table [9][stride] of this problem
+  int64_t stride;
+  double tau;            // cos(eps)
+  float guard;           // fp32 screening band (>= 2.7e-6, R10)
+  int32_t rounds;
+  const unsigned long long* best;
+  int32_t B;
+  const double* q0;
+  double* partials;
+  double* q;
+  int32_t* flags;
+  uint32_t* ninl;
+  uint32_t* mask;
+};
+cudaError_t launch_refine1(const Refine1Args& a, int num_sms, cudaStream_t s);
 
 }  // namespace rv
