@@ -56,6 +56,8 @@ extern "C" {
 #define RV_DEGENERATE  2  /* a round had < 2 inliers or eigengap <= 1e-12*|lambda1|;
                              q is the last good estimate (q_c* if round 1 failed) */
 #define RV_RECHECKED   4  /* the final level needed the fp64 near-threshold recheck */
+#define RV_RETRIED     8  /* the one-pass solve hit a fixed capacity or the re-dive trigger (R18)
+                             and was redone by the per-level loop (same result, slower) */
 
 #define RV_MAX_CHAIN   8
 #define RV_MAX_PHASES 16
@@ -91,9 +93,12 @@ typedef struct {
                             FP32 pipe over per-ancestor lists; the certified argument is in
                             DESIGN.md §5).  Same result; applies to the device level loop when
                             the bitmasks fit (<= 4 GiB).  0: off.  Other values -> RV_EINVAL. */
-  int32_t planner;       /* 0: the level loop runs on the device (default); 1: the host planner
-                            (rv_plan.cpp) drives every level -- the reference the GPU tests compare
-                            the device loop against.  Same result.  Other values -> RV_EINVAL. */
+  int32_t planner;       /* 0: the level loop runs on the device (default; a single problem on one
+                            GPU runs it in one pass: one host round trip per solve); 1: the host
+                            planner (rv_plan.cpp) drives every level -- the reference the GPU tests
+                            compare the device loop against; 2: the device loop with one host round
+                            trip per branch-and-bound level (the one-pass solve's fallback).  Same
+                            result.  Other values -> RV_EINVAL. */
 } rv_config;
 
 typedef struct {
@@ -123,6 +128,11 @@ typedef struct {
   float    cull_ms;       /* summed device time of the culled-vote launches (CUDA events on
                              cfg.stream) */
   int32_t  cull_tc_launches; /* of cull_launches: on the tensor cores (K3-CT) */
+  int32_t  host_syncs;    /* host waits on the device inside the call (one-pass solve: 1) */
+  /* device time per phase (CUDA events on cfg.stream; one-pass single solves, else 0):
+   * a1 setup, level 0 (vote + culling lists + dive start), the dive, the branch-and-bound
+   * levels, the finest level (a5 recheck + winner), a6 refinement */
+  float    t_setup_ms, t_level0_ms, t_dive_ms, t_bnb_ms, t_final_ms, t_refine_ms;
 } rv_result;
 
 /* ---- lifetime ------------------------------------------------------------------ */

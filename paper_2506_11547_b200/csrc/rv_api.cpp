@@ -98,7 +98,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
   if (cfg->max_n < 2 || cfg->max_n > ((int64_t)1 << 31) - 4096) return RV_EINVAL;
   if (cfg->max_problems < 1 || cfg->refine_rounds < 0 || !(cfg->guard >= 0.0f)) return RV_EINVAL;
   if (cfg->chain_len < 0 || cfg->chain_len > RV_MAX_CHAIN) return RV_EINVAL;
-  if (cfg->cull < 0 || cfg->cull > 2 || cfg->planner < 0 || cfg->planner > 1) return RV_EINVAL;
+  if (cfg->cull < 0 || cfg->cull > 2 || cfg->planner < 0 || cfg->planner > 2) return RV_EINVAL;
   rv_ctx* ctx = new rv_ctx();
   ctx->cfg = *cfg;
   if (cfg->chain_len == 0) ctx->chain.assign(kDefaultChain, kDefaultChain + 6);
@@ -121,6 +121,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->evv0);
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->evv1);
+  for (int k = 0; k < 8 && e == cudaSuccess; ++k) e = cudaEventCreate(&ctx->ph[k]);
   if (e == cudaSuccess) {
     ctx->stride = pad4(cfg->max_n) + 64;
     e = ctx->k9.ensure((size_t)9 * ctx->stride);
@@ -190,6 +191,8 @@ void rot_vote_destroy(rv_ctx* ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evv0) cudaEventDestroy(ctx->evv0);
   if (ctx->evv1) cudaEventDestroy(ctx->evv1);
+  for (cudaEvent_t e : ctx->ph)
+    if (e) cudaEventDestroy(e);
   delete ctx;
 }
 

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges per phase (Nsight Systems timelines)
 #include <nccl.h>  // types only; the library is dlopen'ed (libnccl.so.2) when world > 1
 
 #include "../../include/rotvote.h"
@@ -336,11 +337,16 @@ struct rv_ctx {
   }
   Staging up, down;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evv0 = nullptr, evv1 = nullptr;
+  cudaEvent_t ph[8] = {};       // phase boundaries of a one-pass solve (rv_result.t_*_ms)
+  int32_t host_syncs = 0;       // host waits on the device in this call
+  bool retried = false;         // a one-pass solve was redone by the per-level loop
+  int32_t redo_reason = 0;      // its error word
   // per-call counters reported in rv_result
   float vote_ms = 0, cull_ms = 0;
   uint64_t vote_pairs = 0, cull_pairs = 0;
   int32_t launches = 0, vote_launches = 0, cull_launches = 0, cull_tc_launches = 0;
   void reset_counters() {
+    host_syncs = 0; retried = false; redo_reason = 0;
     vote_ms = 0; vote_pairs = 0; launches = 0; vote_launches = 0; vote_pending = false;
     cull_ms = 0; cull_pairs = 0; cull_launches = 0; cull_tc_launches = 0; cevn = 0;
   }
@@ -354,6 +360,8 @@ struct rv_ctx {
     r.cull_pairs = cull_pairs;
     r.cull_launches = cull_launches;
     r.cull_tc_launches = cull_tc_launches;
+    r.host_syncs = host_syncs;
+    if (retried) r.flags |= RV_RETRIED;
   }
   Trace* trace = nullptr;  // RV_TRACE=1: host phase timings
   void mark(const char* what) {
@@ -384,6 +392,13 @@ struct rv_ctx {
   }
 };
 
+// a host wait on the device inside a call (counted in rv_result.host_syncs)
+#define RV_SYNC(call, what)                               \
+  do {                                                    \
+    ctx->host_syncs += 1;                                 \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return ctx->cuda_fail(e_, what); \
+  } while (0)
 #define RV_CUDA(call, what)                               \
   do {                                                    \
     cudaError_t e_ = (call);                              \

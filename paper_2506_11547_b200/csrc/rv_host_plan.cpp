@@ -280,7 +280,7 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
   uint32_t* hc = ctx->down.take<uint32_t>(per_rank * W);
   RV_CUDA(cudaMemcpyAsync(hc, gathered, per_rank * W * 4, cudaMemcpyDeviceToHost, s), "D2H");
   ctx->mark("  launched");
-  RV_CUDA(cudaStreamSynchronize(s), "vote");
+  RV_SYNC(cudaStreamSynchronize(s), "vote");
   ctx->mark("  synced");
   if (mode != RV_MODE_EXACT && !items.empty()) {
     float ms = 0;
@@ -400,7 +400,7 @@ int solve_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double ep
   out->flags |= fl;
   out->n_inliers = ni;
   RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
-  RV_CUDA(cudaEventSynchronize(ctx->ev1), "event");
+  RV_SYNC(cudaEventSynchronize(ctx->ev1), "event");
   float ms = 0;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   out->ms = ms;
@@ -453,7 +453,7 @@ int solve_multi_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     ++found;
   }
   RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
-  RV_CUDA(cudaEventSynchronize(ctx->ev1), "event");
+  RV_SYNC(cudaEventSynchronize(ctx->ev1), "event");
   float ms = 0;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   for (int32_t k = 0; k < found; ++k) {
@@ -511,7 +511,7 @@ int translation_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, con
   double hs[3];
   RV_CUDA(cudaMemcpyAsync(&hb, ctx->rg_best.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hs, ctx->rg_sums.p, 24, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaStreamSynchronize(s), "translation vote");
+  RV_SYNC(cudaStreamSynchronize(s), "translation vote");
   if (hb == 0) return ctx->fail(RV_EDATA, "no translation candidate inside the grid");
   const int64_t L = (int64_t)(0xffffffffu - (uint32_t)(hb & 0xffffffffu));
   *lin = L;
@@ -543,7 +543,7 @@ int rigid_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double mu
   rv::launch_pairs_count(x, y, n, mu_t, ctx->rg_cnt.p, ctx->rg_off.p, s);
   int64_t kept = 0;
   RV_CUDA(cudaMemcpyAsync(&kept, ctx->rg_off.p + nb, 8, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaStreamSynchronize(s), "pair count");
+  RV_SYNC(cudaStreamSynchronize(s), "pair count");
   out->pairs_total = n * (n - 1) / 2;
   out->pairs_kept = kept;
   if (kept < 2) return ctx->fail(RV_EDATA, "only %lld pairs pass the length check", (long long)kept);
@@ -568,7 +568,7 @@ int rigid_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, double mu
                                 out->t_mean))
     return rc;
   RV_CUDA(cudaEventRecord(e[3], s), "event");
-  RV_CUDA(cudaEventSynchronize(e[3]), "event");
+  RV_SYNC(cudaEventSynchronize(e[3]), "event");
   const int64_t Bt = (int64_t)std::llround((hi - lo) / step);
   out->t_cell[0] = (int32_t)(lin / (Bt * Bt));
   out->t_cell[1] = (int32_t)((lin / Bt) % Bt);
@@ -690,7 +690,7 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   RV_CUDA(cudaGetLastError(), "launching the vote kernel");
   if (keep_dev) {
     RV_CUDA(cudaMemcpyAsync(keep_dev, ctx->cnt.p, total * 4, cudaMemcpyDeviceToDevice, s), "D2D");
-    RV_CUDA(cudaStreamSynchronize(s), "batched vote");
+    RV_SYNC(cudaStreamSynchronize(s), "batched vote");
     if (mode != RV_MODE_EXACT && !items.empty()) {
       float ms = 0;
       cudaEventElapsedTime(&ms, ctx->evv0, ctx->evv1);
@@ -701,7 +701,7 @@ int eval_batch(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   ctx->down.reset();
   uint32_t* hc = ctx->down.take<uint32_t>(2 * total);
   RV_CUDA(cudaMemcpyAsync(hc, ctx->cnt.p, ncnt * 4, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaStreamSynchronize(s), "batched vote");
+  RV_SYNC(cudaStreamSynchronize(s), "batched vote");
   if (mode != RV_MODE_EXACT && !items.empty()) {
     float ms = 0;
     cudaEventElapsedTime(&ms, ctx->evv0, ctx->evv1);

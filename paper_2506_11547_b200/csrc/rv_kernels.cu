@@ -453,6 +453,19 @@ void launch_exact(const float* k9, int64_t stride, const float* x, const float* 
 // ------------------------------------------------------------------------------------------
 // K6 inliers + partial sums
 // ------------------------------------------------------------------------------------------
+// K_i of row r in fp64 from the raw fp32 row (normalised in fp64), one compiled copy shared by
+// K6 and the fused refinement so both produce the same bits
+__device__ __noinline__ void ref_row_k(const float* __restrict__ x, const float* __restrict__ y,
+                                       int64_t r, double k[9]) {
+  double a[3] = {x[3 * r], x[3 * r + 1], x[3 * r + 2]};
+  double b[3] = {y[3 * r], y[3 * r + 1], y[3 * r + 2]};
+  const double ia = 1.0 / sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+  const double ib = 1.0 / sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) { a[c] *= ia; b[c] *= ib; }
+  k9_of(a, b, k);
+}
+
 __global__ void __launch_bounds__(kRefThreads) rv_inliers_kernel(
     const float* __restrict__ x, const float* __restrict__ y, const RefSeg* __restrict__ segs,
     const RefItem* __restrict__ items, const double* __restrict__ qs, uint32_t* masks,
@@ -472,14 +485,7 @@ __global__ void __launch_bounds__(kRefThreads) rv_inliers_kernel(
     bool in = false;
     double k[9];
     if (i < end && i < sg.n) {
-      const int64_t r = sg.row + i;
-      double a[3] = {x[3 * r], x[3 * r + 1], x[3 * r + 2]};
-      double b[3] = {y[3 * r], y[3 * r + 1], y[3 * r + 2]};
-      const double ia = 1.0 / sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
-      const double ib = 1.0 / sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) { a[c] *= ia; b[c] *= ib; }
-      k9_of(a, b, k);
+      ref_row_k(x, y, sg.row + i, k);
       double s = 0.0;
 #pragma unroll
       for (int t = 0; t < 9; ++t) s = fma(f[t], k[t], s);
@@ -570,7 +576,7 @@ __device__ void jacobi4(double A[4][4], double V[4][4]) {
 // One refinement step from the inlier sums S (9 entries of sum K_i, count): flags | RV_REFINED and
 // q <- the hemisphere-canonical top eigenvector, or flags | RV_DEGENERATE | kStop (fewer than 2
 // inliers, or eigengap <= 1e-12 |lambda1|: q kept, later rounds skipped, reading R8)
-__device__ int32_t eig_update(const double S[10], int32_t fl, double* q) {
+__device__ __noinline__ int32_t eig_update(const double S[10], int32_t fl, double* q) {
   const double count = S[9];
   if (fl & kStop) return fl;
   if (count < 2.0) return fl | RV_DEGENERATE | kStop;
@@ -679,7 +685,24 @@ void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* q
 // and decides the rows inside the band in fp64 from x, y exactly as K6 does; the inliers' fp64
 // K_i are summed in a fixed order (warp butterflies, CTA partials in block order).
 // ------------------------------------------------------------------------------------------
-constexpr int kR1Threads = 256;
+#ifndef RV_R1_TRACE
+#define RV_R1_TRACE 0  // tuning builds: %globaltimer stamps of CTA 0 (rv_r1_trace_copy)
+#endif
+#if RV_R1_TRACE
+__device__ unsigned long long g_r1_trace[32];
+__device__ __forceinline__ void r1_stamp(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x == 0 && threadIdx.x == 0 && k < 32) g_r1_trace[k] = t;
+}
+extern "C" int rv_r1_trace_copy(unsigned long long* h) {
+  return (int)cudaMemcpyFromSymbol(h, g_r1_trace, sizeof(g_r1_trace));
+}
+#else
+__device__ __forceinline__ void r1_stamp(int) {}
+#endif
+constexpr int kR1Threads = kRefThreads;  // K6's decomposition (see below)
+static_assert(kRefRowsPerItem % kRefThreads == 0, "K6 items are whole rounds of rows");
 
 __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
   namespace cg = cooperative_groups;
@@ -712,9 +735,14 @@ __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
     for (int c = 0; c < 4; ++c) a.q[c] = flip ? -q[c] : q[c];
     *a.flags = 0;
   }
+  r1_stamp(0);
   grid.sync();
+  r1_stamp(1);
   const float t_hi = (float)(a.tau + (double)a.guard), t_lo = (float)(a.tau - (double)a.guard);
-  const int64_t gthreads = (int64_t)gridDim.x * kR1Threads;
+  // K6's decomposition exactly (items of kRefRowsPerItem rows, warp w takes rows w*32 + lane +
+  // 256 j of an item, per-item partials reduced as K6 does, summed as K7 does), so q, the mask
+  // and the count are bit-identical to the K6 / K7 launches
+  const int64_t n_items = (a.n + kRefRowsPerItem - 1) / kRefRowsPerItem;
   for (int r = 0; r <= a.rounds; ++r) {
     const bool last = r == a.rounds;
     double q[4];
@@ -724,72 +752,99 @@ __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
     float f32[9];
 #pragma unroll
     for (int t = 0; t < 9; ++t) f32[t] = (float)f[t];
-    double acc[10];
+    for (int64_t itm = blockIdx.x; itm < n_items; itm += gridDim.x) {
+      const int64_t r0 = itm * kRefRowsPerItem;
+      const int64_t end = r0 + kRefRowsPerItem < a.n ? r0 + kRefRowsPerItem : a.n;
+      double acc[10];
 #pragma unroll
-    for (int t = 0; t < 10; ++t) acc[t] = 0.0;
-    for (int64_t base = ((int64_t)blockIdx.x * kR1Threads + warp * 32); base < a.n; base += gthreads) {
-      const int64_t i = base + lane;
-      bool in = false, band = false;
-      if (i < a.n) {
-        float s32 = 0.0f;
+      for (int t = 0; t < 10; ++t) acc[t] = 0.0;
+      // pass A: the fp32 screen of the thread's kRowsPT rows (rows r0 + warp*32 + lane + 256 j),
+      // every K-table load issued up front; pass B: the decisions and the sums in K6's order
+      constexpr int kRowsPT = kRefRowsPerItem / kR1Threads;
+      float s32[kRowsPT];
 #pragma unroll
-        for (int t = 0; t < 9; ++t) s32 = fmaf(f32[t], __ldg(a.k9 + t * a.stride + i), s32);
-        in = s32 >= t_hi;
-        band = !in && s32 >= t_lo;
+      for (int jr = 0; jr < kRowsPT; ++jr) {
+        const int64_t i = r0 + warp * 32 + lane + (int64_t)jr * kR1Threads;
+        float v = 0.0f;
+        if (i < end) {
+#pragma unroll
+          for (int t = 0; t < 9; ++t) v = fmaf(f32[t], __ldg(a.k9 + t * a.stride + i), v);
+        }
+        s32[jr] = v;
       }
-      double k[9];
-      if (in || band) {  // fp64 K_i from the raw row (the sums, and the band's exact decision)
-        double xa[3] = {a.x[3 * i], a.x[3 * i + 1], a.x[3 * i + 2]};
-        double yb[3] = {a.y[3 * i], a.y[3 * i + 1], a.y[3 * i + 2]};
-        const double ia = 1.0 / sqrt(xa[0] * xa[0] + xa[1] * xa[1] + xa[2] * xa[2]);
-        const double ib = 1.0 / sqrt(yb[0] * yb[0] + yb[1] * yb[1] + yb[2] * yb[2]);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) { xa[c] *= ia; yb[c] *= ib; }
-        k9_of(xa, yb, k);
-        if (band) {
-          double s = 0.0;
+      for (int jr = 0; jr < kRowsPT; ++jr) {
+        const int64_t base = r0 + warp * 32 + (int64_t)jr * kR1Threads;
+        if (base >= end) break;  // warp-uniform
+        const int64_t i = base + lane;
+        bool in = false, band = false;
+        if (i < end) {
+          in = s32[jr] >= t_hi;
+          band = !in && s32[jr] >= t_lo;
+        }
+        double k[9];
+        if (in || band) {  // fp64 K_i from the raw row (the sums, and the band's decision), as K6
+          ref_row_k(a.x, a.y, i, k);
+          if (band) {
+            double sd = 0.0;
 #pragma unroll
-          for (int t = 0; t < 9; ++t) s = fma(f[t], k[t], s);
-          in = s >= a.tau;
+            for (int t = 0; t < 9; ++t) sd = fma(f[t], k[t], sd);
+            in = sd >= a.tau;
+          }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        if (last && a.mask && lane == 0) a.mask[base >> 5] = bal;
+        if (in) {
+#pragma unroll
+          for (int t = 0; t < 9; ++t) acc[t] += k[t];
+          acc[9] += 1.0;
         }
       }
-      const uint32_t bal = __ballot_sync(0xffffffffu, in);
-      if (last && a.mask && lane == 0) a.mask[base >> 5] = bal;
-      if (in) {
 #pragma unroll
-        for (int t = 0; t < 9; ++t) acc[t] += k[t];
-        acc[9] += 1.0;
+      for (int t = 0; t < 10; ++t)
+        for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_down_sync(0xffffffffu, acc[t], o);
+      if (lane == 0)
+#pragma unroll
+        for (int t = 0; t < 10; ++t) ws[warp][t] = acc[t];
+      __syncthreads();
+      if (threadIdx.x < 10) {
+        double v = 0.0;
+        for (int w = 0; w < kR1Threads / 32; ++w) v += ws[w][threadIdx.x];
+        a.partials[itm * 10 + threadIdx.x] = v;
       }
+      __syncthreads();
     }
-#pragma unroll
-    for (int t = 0; t < 10; ++t)
-      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_down_sync(0xffffffffu, acc[t], o);
-    if (lane == 0)
-#pragma unroll
-      for (int t = 0; t < 10; ++t) ws[warp][t] = acc[t];
-    __syncthreads();
-    if (threadIdx.x < 10) {
-      double v = 0.0;
-      for (int w = 0; w < kR1Threads / 32; ++w) v += ws[w][threadIdx.x];
-      a.partials[(int64_t)blockIdx.x * 10 + threadIdx.x] = v;
-    }
+    r1_stamp(2 + 4 * r);
     grid.sync();
-    if (blockIdx.x == 0 && warp == 0) {
+    r1_stamp(3 + 4 * r);
+    if (blockIdx.x == 0) {  // K7's per-CTA sum: thread t takes items t, t + 256, ...
       double S[10];
 #pragma unroll
       for (int t = 0; t < 10; ++t) S[t] = 0.0;
-      for (int b = lane; b < (int)gridDim.x; b += 32)
+      for (int64_t b = threadIdx.x; b < n_items; b += kR1Threads)
 #pragma unroll
-        for (int t = 0; t < 10; ++t) S[t] += a.partials[(int64_t)b * 10 + t];
+        for (int t = 0; t < 10; ++t) S[t] += a.partials[b * 10 + t];
 #pragma unroll
       for (int t = 0; t < 10; ++t)
         for (int o = 16; o > 0; o >>= 1) S[t] += __shfl_down_sync(0xffffffffu, S[t], o);
-      if (lane == 0) {
+      if (lane == 0)
+#pragma unroll
+        for (int t = 0; t < 10; ++t) ws[warp][t] = S[t];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int t = 0; t < 10; ++t) {
+          double v = 0.0;
+          for (int w = 0; w < kR1Threads / 32; ++w) v += ws[w][t];
+          S[t] = v;
+        }
         if (last) *a.ninl = (uint32_t)S[9];
         else *a.flags = eig_update(S, *a.flags, a.q);
       }
     }
+    r1_stamp(4 + 4 * r);
     grid.sync();
+    r1_stamp(5 + 4 * r);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.flags &= (RV_REFINED | RV_DEGENERATE);
 }

@@ -64,7 +64,7 @@ constexpr int kTcM = 128;                          // K3-TC: cells per CTA (MMA 
 constexpr int kTcStages = 7;                       // K3-TC: 16 KB tiles in flight (also pins 1 CTA/SM)
 constexpr int kRefThreads = 256;                   // K6/K7 block
 #ifndef RV_REF_ROWS
-#define RV_REF_ROWS 2048
+#define RV_REF_ROWS 4096
 #endif
 constexpr int kRefRowsPerItem = RV_REF_ROWS;       // K6 rows per block (multiple of 32)
 
@@ -230,7 +230,7 @@ void launch_eig(const RefSeg* segs, int32_t P, const double* partials, double* q
 // `rounds` refinement rounds from q0 (HOST-independent: q0 != nullptr DEVICE double[4], else the
 // centre of the winner decoded from *best at resolution B), then the final mask / count.
 // Writes q[4], *flags (RV_REFINED | RV_DEGENERATE), *ninl, mask (DEVICE, may be null).
-// partials: DEVICE double [kRefine1MaxCtas * 10].
+// partials: DEVICE double [ceil(n / kRefRowsPerItem) * 10].
 constexpr int kRefine1MaxCtas = 148 * 8;
 struct Refine1Args {
   const float* x;

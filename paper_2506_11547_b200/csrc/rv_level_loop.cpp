@@ -75,7 +75,7 @@ int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
   ctx->down.reset();
   int64_t* ht = ctx->down.take<int64_t>(1);
   RV_CUDA(cudaMemcpyAsync(ht, ctx->c_lofs.p + NB, 8, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaStreamSynchronize(s), "level-0 lists");
+  RV_SYNC(cudaStreamSynchronize(s), "level-0 lists");
   const int64_t total = *ht;
   const double pairs0 = (double)m0 * (double)(ctx->tc_toff[PL] - ctx->tc_toff[0]);
   ctx->cull_ready = false;
@@ -134,7 +134,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     RV_CUDA(ctx->c_tslot.ensure(eb), "allocating");
     const int64_t npos = eb + 7 * nb + 16;  // bucket positions are padded to multiples of 8
     RV_CUDA(ctx->c_cidx.ensure(npos), "allocating");
-    RV_CUDA(ctx->c_phi.ensure(npos * 12), "allocating");
+    if (!ctx->cull_grouped) RV_CUDA(ctx->c_phi.ensure(npos * 12), "allocating");  // K3-C only
     // (+256 rows: K3-CT's A tiles read up to 2 x 128 rows from an item's first)
     if (ctx->cull_grouped) RV_CUDA(ctx->c_tphi.ensure((npos * 2 + 256) * 64), "allocating");
     RV_CUDA(ctx->c_icnt.ensure(2), "allocating");
@@ -218,7 +218,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
   std::vector<int64_t> hoff(PL + 1);
   RV_CUDA(cudaMemcpyAsync(hcnt.data(), Ld.cnt, PL * 4, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hoff.data(), Ld.base, (PL + 1) * 8, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaStreamSynchronize(s), "batched level");
+  RV_SYNC(cudaStreamSynchronize(s), "batched level");
   ctx->collect_vote_ms();
   return vote_lists(ctx, x, y, rows, koff, eps, mode, B, Ld.lins, hoff, hcnt, 0, Ld.ca, Ld.cb);
 }
@@ -553,7 +553,7 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
       int32_t* ha = ctx->down.take<int32_t>(1);
       RV_CUDA(cudaMemcpyAsync(ht, ctx->dp_tot.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
       if (any) RV_CUDA(cudaMemcpyAsync(ha, ctx->dp_rany.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
-      RV_CUDA(cudaStreamSynchronize(s), "batched level");
+      RV_SYNC(cudaStreamSynchronize(s), "batched level");
       ctx->collect_vote_ms();
       *total = *ht;
       if (any) *any = *ha;
@@ -675,7 +675,7 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   RV_CUDA(cudaMemcpyAsync(hlb, ctx->dp_lb.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hph, ctx->dp_phase.p, 4 * (size_t)nph * PL, cudaMemcpyDeviceToHost, s),
           "D2H");
-  RV_CUDA(cudaStreamSynchronize(s), "batched finalize");
+  RV_SYNC(cudaStreamSynchronize(s), "batched finalize");
   ctx->collect_vote_ms();
   ctx->ev_collect();
   ctx->cev_collect();
@@ -740,6 +740,354 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
   return RV_OK;
 }
 
+// ---- the one-pass single solve ------------------------------------------------------------------
+// One problem on one GPU: the whole certified search -- setup, level 0 with its culling lists,
+// the dive, every branch-and-bound level, the finest level with its exact recheck, and the
+// refinement -- is enqueued without a single host round trip; the host reads everything back
+// once at the end.  What the per-level loop (solve_batched_dplan) learns from its round trips is
+// replaced by fixed, data-independent capacities: the level lists hold up to kOnePassCap blocks
+// (min with the grid's candidate count), the culling lists up to a quarter of the level-0 pairs
+// (the per-level loop's own culling limit), the exact recheck up to kOnePassRecheck blocks.  A
+// device-side violation (a longer list, or the re-dive trigger R18, which this loop does not
+// take) raises the solve's error word; the level scans then empty every later level, and the
+// host redoes the solve with the per-level loop (rv_result.flags |= RV_RETRIED).  Every decision
+// is the per-level loop's, so both give the same result.
+constexpr int64_t kOnePassCap = (int64_t)1 << 22;
+constexpr int64_t kOnePassRecheck = 4096;
+
+bool one_pass_applies(rv_ctx* ctx, int32_t P) {
+  return P == 1 && ctx->cfg.planner == 0 && ctx->tc_on && !ctx->comm &&
+         ctx->effective_world() == 1;
+}
+
+int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                   const std::vector<int32_t>& ch, rv_result* out, uint32_t* mask, bool* redo) {
+  *redo = false;
+  const int L = (int)ch.size();
+  // the flat kernels loop over the device's own totals; their grids only need to fill the GPU
+  auto flat_hint = [&](int64_t m) { return std::min<int64_t>(m, (int64_t)ctx->num_sms * 2 * 256); };
+  cudaStream_t s = ctx->stream;
+  const int32_t PL = 1;
+  const int64_t offs[2] = {0, n};
+  std::vector<int64_t> rows(offs, offs + 2), koff;
+  cudaEvent_t* ph = ctx->ph;
+  const int32_t B0 = ch[0];
+  const int64_t m0 = rv_grid_candidates(B0, nullptr, 0);
+  // pinned staging for every host-built upload of the solve (it is not reused before the final
+  // sync): run_setup's offsets, the level-0 background, the dive / BnB offsets
+  RV_CUDA(ctx->up.ensure((size_t)m0 * 8 + 65536), "allocating staging");
+  RV_CUDA(cudaEventRecord(ph[0], s), "event");
+  nvtxRangePushA("rv.setup");
+  if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;  // resets ctx->up, then takes
+  nvtxRangePop();
+  RV_CUDA(cudaEventRecord(ph[1], s), "event");
+  auto upload_i64 = [&](int64_t* dst, std::initializer_list<int64_t> v) -> int {
+    int64_t* h = ctx->up.take<int64_t>(v.size());
+    std::copy(v.begin(), v.end(), h);
+    RV_CUDA(cudaMemcpyAsync(dst, h, v.size() * 8, cudaMemcpyHostToDevice, s), "H2D");
+    return RV_OK;
+  };
+  int64_t nmax = n;
+  RV_CUDA(ctx->dp_phase.ensure((size_t)(3 * L + 1)), "allocating");
+  int nph = 0;
+  auto keep_phase = [&](const int32_t* dcnt) -> int {
+    RV_CUDA(cudaMemcpyAsync(ctx->dp_phase.p + nph, dcnt, 4, cudaMemcpyDeviceToDevice, s), "D2D");
+    ++nph;
+    return RV_OK;
+  };
+  ctx->ev_reset();
+  RV_CUDA(ctx->dp_err.ensure(1), "allocating");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_err.p, 0, 4, s), "memset");
+  // ---- level 0 (every block of the grid), with the culling lists
+  nvtxRangePushA("rv.level0");
+  if (ctx->grid_host_B != B0) {
+    ctx->grid_host.resize(m0);
+    rv_grid_candidates(B0, ctx->grid_host.data(), m0);
+    ctx->grid_host_B = B0;
+  }
+  int64_t mbg = 0;
+  const double* bgh = rv_plan_l0_background(B0, eps, &mbg);
+  if (!bgh || mbg != m0) return ctx->fail(RV_ECUDA, "internal: level-0 background unavailable");
+  RV_CUDA(ctx->l0cnt.ensure((size_t)m0), "allocating level-0 counts");
+  if (ctx->l0bg_B != B0 || ctx->l0bg_eps != eps || ctx->l0bg.cap < (size_t)m0) {
+    RV_CUDA(ctx->l0bg.ensure(m0), "allocating");
+    double* h = ctx->up.take<double>(m0);
+    std::memcpy(h, bgh, m0 * sizeof(double));
+    RV_CUDA(cudaMemcpyAsync(ctx->l0bg.p, h, m0 * sizeof(double), cudaMemcpyHostToDevice, s),
+            "H2D background");
+    ctx->l0bg_B = B0;
+    ctx->l0bg_eps = eps;
+  }
+  if (ctx->grid_list_B != B0 || ctx->grid_list_m != m0) {
+    RV_CUDA(ctx->grid_list.ensure(m0), "allocating grid list");
+    RV_CUDA(cudaMemcpy(ctx->grid_list.p, ctx->grid_host.data(), m0 * 4, cudaMemcpyHostToDevice),
+            "H2D grid");
+    ctx->grid_list_B = B0;
+    ctx->grid_list_m = m0;
+  }
+  ctx->cull_ready = false;
+  const int64_t tpad = ctx->tc_toff.back();
+  const bool cull = ctx->cull_on && (double)m0 * (double)(tpad / 32) * 4.0 <= 4294967296.0;
+  RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, (size_t)m0 * 4, s), "memset");
+  const rv::DpList l0{ctx->grid_list.p, 1, m0, nullptr, nullptr, ctx->l0cnt.p, ctx->l0cnt.p};
+  if (cull) {
+    RV_CUDA(ctx->cbits.ensure((size_t)m0 * (size_t)(tpad / 32)), "allocating level-0 bitmasks");
+    if (int rc = cull_prepare(ctx, B0, m0, PL)) return rc;
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, m0, nmax, true))
+      return rc;
+    // the lists: row offsets, then the compaction into a fixed capacity (an eighth of the
+    // level-0 pairs; cfg4's lists fill 3%: longer lists raise the error word and the per-level
+    // loop, which reads their length back, redoes the solve)
+    rv::CullGroups gr;
+    if (ctx->cull_grouped) gr = rv::CullGroups{ctx->goff.p, ctx->gmem.p, ctx->cull_G};
+    const int64_t NB = ctx->cull_G;
+    const int64_t lcap = std::min<int64_t>((int64_t)1 << 29, m0 * tpad / 8) + 4 * NB;
+    RV_CUDA(ctx->c_lofs.ensure(NB + 1), "allocating");
+    RV_CUDA(ctx->c_lidx.ensure(lcap + 4), "allocating level-0 lists");
+    RV_CUDA(ctx->c_fill.ensure(NB), "allocating");
+    rv::launch_cull_rows(ctx->l0cnt.p, PL, m0, ctx->c_lofs.p, s, gr);
+    rv::launch_cull_compact(ctx->cbits.p, ctx->toffs.p, PL, m0, ctx->cull_wpc_max, ctx->c_lofs.p,
+                            ctx->c_fill.p, ctx->c_lidx.p, s, 0, NB, gr, lcap, ctx->dp_err.p);
+    ctx->launches += 2;
+    // list lengths = the compaction's fill counters (also per ancestor, where they equal the
+    // level-0 counts): a compaction that overflowed wrote nothing and leaves them 0, so no
+    // later vote reads an unwritten list before the error word ends the solve
+    ctx->cull_l0cnt = reinterpret_cast<const uint32_t*>(ctx->c_fill.p);
+    ctx->cull_ready = true;
+  } else {
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, m0, nmax))
+      return rc;
+  }
+  RV_CUDA(ctx->l0idx.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_pick.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_lb.ensure(PL), "allocating");
+  rv::launch_l0_argmax(ctx->l0cnt.p, m0, ctx->grid_list.p, B0, ctx->l0bg.p, ctx->rows.p, PL,
+                       ctx->l0idx.p, s);
+  ctx->launches += 1;
+  nvtxRangePop();
+  RV_CUDA(cudaEventRecord(ph[2], s), "event");
+  // ---- dive (fixed sizes: the 27-neighbourhood's children)
+  nvtxRangePushA("rv.dive");
+  for (int l = 1; l < L; ++l) {
+    const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1], cap = 27 * f * f * f;
+    RV_CUDA(ctx->dp_lins[0].ensure(cap), "allocating");
+    RV_CUDA(ctx->dp_ca[0].ensure(cap), "allocating");
+    RV_CUDA(ctx->dp_cb[0].ensure(cap), "allocating");
+    RV_CUDA(ctx->dp_cnt[0].ensure(PL), "allocating");
+    RV_CUDA(ctx->dp_off[0].ensure(PL + 1), "allocating");
+    if (int rc = upload_i64(ctx->dp_off[0].p, {0, cap})) return rc;
+    rv::dp_launch_dive_children(ctx->dp_pick.p, ctx->l0idx.p, l == 1 ? ctx->grid_list.p : nullptr,
+                                Bp, f, ctx->dp_lins[0].p, cap, ctx->dp_cnt[0].p, PL, s);
+    const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
+    RV_CUDA(cudaMemsetAsync(ctx->dp_ca[0].p, 0, (size_t)cap * 4, s), "memset");
+    if (mode == RV_MODE_FINAL) RV_CUDA(cudaMemsetAsync(ctx->dp_cb[0].p, 0, (size_t)cap * 4, s), "memset");
+    ctx->launches += 1;
+    if (int rc = keep_phase(ctx->dp_cnt[0].p)) return rc;
+    const rv::DpList dl{ctx->dp_lins[0].p, 0, 0, ctx->dp_off[0].p, ctx->dp_cnt[0].p,
+                        ctx->dp_ca[0].p, ctx->dp_cb[0].p};
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], dl, PL, cap, nmax)) return rc;
+    if (mode == RV_MODE_BOUND)
+      rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, ctx->dp_off[0].p,
+                              ctx->dp_cnt[0].p, ch[l], eps, ctx->rows.p, ctx->dp_pick.p, PL, s);
+    else
+      rv::dp_launch_max_lo(ctx->dp_cb[0].p, ctx->dp_off[0].p, ctx->dp_cnt[0].p, ctx->dp_lb.p, PL, s);
+    ctx->launches += 1;
+  }
+  nvtxRangePop();
+  RV_CUDA(cudaEventRecord(ph[3], s), "event");
+  // ---- branch and bound from the level-0 survivors: lists alternate between sets 0 and 1 at
+  // fixed capacities; offsets in the rings as in the per-level loop
+  nvtxRangePushA("rv.bnb");
+  std::vector<int64_t> capl(L, 0);
+  for (int l = 1; l < L; ++l)
+    capl[l] = std::min<int64_t>(kOnePassCap, (int64_t)ch[l] * ch[l] * ch[l]);  // (B^3 >= candidates;
+                                                                              // counting them costs ms)
+  for (int r = 0; r < 2; ++r) RV_CUDA(ctx->dp_actr[r].ensure(PL + 1), "allocating");
+  for (int r = 0; r < 3; ++r) RV_CUDA(ctx->dp_bring[r].ensure(PL + 1), "allocating");
+  RV_CUDA(ctx->dp_tot.ensure(1), "allocating");
+  RV_CUDA(ctx->dp_rdone.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_rflag.ensure(PL), "allocating");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_rdone.p, 0, PL * 4, s), "memset");
+  if (int rc = upload_i64(ctx->dp_actr[1].p, {0, m0})) return rc;
+  {
+    const int64_t f = ch[1] / ch[0];
+    if (int rc = upload_i64(ctx->dp_bring[1].p, {0, std::min<int64_t>(m0 * f * f * f, capl[1])}))
+      return rc;
+  }
+  const uint32_t* plins = ctx->grid_list.p;
+  const uint32_t* pub = ctx->l0cnt.p;
+  bool shared = true;
+  int cur = -1;
+  for (int l = 1; l < L; ++l) {
+    const int nb = cur == 1 ? 0 : 1;
+    const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1];
+    const int64_t f3 = (int64_t)f * f * f;
+    int64_t* pact = ctx->dp_actr[l & 1].p;
+    int64_t* cact = ctx->dp_actr[(l + 1) & 1].p;
+    int64_t* cbase = ctx->dp_bring[l % 3].p;
+    int64_t* pbase = shared ? pact : ctx->dp_bring[(l + 2) % 3].p;
+    int64_t* nbase = ctx->dp_bring[(l + 1) % 3].p;
+    RV_CUDA(ctx->dp_lins[nb].ensure(capl[l]), "allocating");
+    RV_CUDA(ctx->dp_ca[nb].ensure(capl[l]), "allocating");
+    RV_CUDA(ctx->dp_cb[nb].ensure(capl[l]), "allocating");
+    RV_CUDA(ctx->dp_cnt[nb].ensure(PL), "allocating");
+    RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
+    rv::dp_launch_bnb_expand(plins, shared, pact, pbase, pub, ctx->dp_lb.p, PL,
+                             flat_hint(shared ? m0 : capl[l - 1]), Bp, f, cbase, ctx->dp_lins[nb].p,
+                             ctx->dp_ca[nb].p, ctx->dp_cb[nb].p, ctx->dp_cnt[nb].p, ctx->dp_err.p, s);
+    int64_t nf3 = 1;
+    if (l + 1 < L) {
+      const int64_t nf = ch[l + 1] / ch[l];
+      nf3 = nf * nf * nf;
+    }
+    // re-dive trigger (R18): not taken here -- it raises the error word (bit 8) and the solve
+    // is redone by the per-level loop, which takes it
+    rv::RediveCheck chk{cur >= 0 ? ctx->dp_cnt[cur].p : nullptr, f3, ctx->dp_rdone.p,
+                        ctx->dp_rflag.p, ctx->dp_err.p, 8};
+    const rv::OnePass op{ctx->dp_err.p, l + 1 < L ? capl[l + 1] : 0};
+    rv::dp_launch_scan(ctx->dp_cnt[nb].p, PL, nf3, cact, nbase, ctx->dp_tot.p, s,
+                       l >= 2 ? &chk : nullptr, &op);
+    ctx->launches += 2;
+    if (int rc = keep_phase(ctx->dp_cnt[nb].p)) return rc;
+    const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
+    const rv::DpList cl{ctx->dp_lins[nb].p, 0, 0, cbase, ctx->dp_cnt[nb].p, ctx->dp_ca[nb].p,
+                        ctx->dp_cb[nb].p};
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], cl, PL, capl[l], nmax))
+      return rc;
+    plins = ctx->dp_lins[nb].p;
+    pub = ctx->dp_ca[nb].p;
+    shared = false;
+    cur = nb;
+  }
+  nvtxRangePop();
+  RV_CUDA(cudaEventRecord(ph[4], s), "event");
+  // ---- finest level: max lo, exact-known blocks, the fp64 recheck, winner, ties
+  nvtxRangePushA("rv.final");
+  const int64_t fcapn = capl[L - 1];
+  const uint32_t* flins = ctx->dp_lins[cur].p;
+  const uint32_t* fhi = ctx->dp_ca[cur].p;
+  const uint32_t* flo = ctx->dp_cb[cur].p;
+  const int64_t* fcap = ctx->dp_bring[(L - 1) % 3].p;
+  int64_t* fact = ctx->dp_actr[L & 1].p;
+  RV_CUDA(ctx->dp_rcnt.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_lmax.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_best.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_ties.ensure(PL), "allocating");
+  RV_CUDA(ctx->dp_rlins.ensure(fcapn), "allocating");
+  RV_CUDA(ctx->dp_ex.ensure(fcapn), "allocating");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_rcnt.p, 0, PL * 4, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_lmax.p, 0, PL * 4, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_best.p, 0, PL * 8, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_ties.p, 0, PL * 4, s), "memset");
+  RV_CUDA(cudaMemsetAsync(ctx->dp_ex.p, 0, (size_t)kOnePassRecheck * 4, s), "memset");
+  rv::dp_launch_final_max(fact, fcap, flo, PL, flat_hint(fcapn), ctx->dp_lmax.p, s);
+  rv::dp_launch_final_split(fact, fcap, flins, fhi, flo, ctx->dp_lmax.p, PL, flat_hint(fcapn),
+                            ctx->dp_best.p, ctx->dp_rlins.p, ctx->dp_rcnt.p, s);
+  ctx->launches += 2;
+  if (int rc = keep_phase(ctx->dp_rcnt.p)) return rc;
+  // (a recheck list longer than kOnePassRecheck blocks exceeds the items' bound: error word)
+  const rv::DpList rl{ctx->dp_rlins.p, 0, 0, fact, ctx->dp_rcnt.p, ctx->dp_ex.p, ctx->dp_ex.p};
+  if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_EXACT, ch[L - 1], rl, PL,
+                          kOnePassRecheck, nmax))
+    return rc;
+  rv::dp_launch_final_rechecked(fact, ctx->dp_rcnt.p, ctx->dp_rlins.p, ctx->dp_ex.p, PL,
+                                kOnePassRecheck, ctx->dp_best.p, s);
+  rv::dp_launch_final_ties(fact, fcap, fhi, flo, ctx->dp_rcnt.p, ctx->dp_ex.p, PL, flat_hint(fcapn),
+                           ctx->dp_best.p, ctx->dp_ties.p, s);
+  ctx->launches += 2;
+  nvtxRangePop();
+  RV_CUDA(cudaEventRecord(ph[5], s), "event");
+  // ---- refinement from the winner (decoded on the device), K6 + K7 in one cooperative launch
+  nvtxRangePushA("rv.refine");
+  RV_CUDA(ctx->partials.ensure((size_t)((n + rv::kRefRowsPerItem - 1) / rv::kRefRowsPerItem) * 10),
+          "allocating");
+  RV_CUDA(ctx->qs.ensure(4), "allocating");
+  RV_CUDA(ctx->flags.ensure(1), "allocating");
+  RV_CUDA(ctx->ninl.ensure(1), "allocating");
+  rv::Refine1Args ra{x, y, n, ctx->k9.p, ctx->stride, std::cos(eps), ctx->cfg.guard,
+                     ctx->cfg.refine_rounds, ctx->dp_best.p, ch[L - 1], nullptr,
+                     ctx->partials.p, ctx->qs.p, ctx->flags.p, ctx->ninl.p, mask};
+  RV_CUDA(rv::launch_refine1(ra, ctx->num_sms, s), "launching the refinement");
+  ctx->launches += 1;
+  nvtxRangePop();
+  RV_CUDA(cudaEventRecord(ph[6], s), "event");
+  // ---- the one read-back
+  RV_CUDA(ctx->down.ensure(4096), "allocating staging");
+  ctx->down.reset();
+  unsigned long long* hbest = ctx->down.take<unsigned long long>(1);
+  int32_t* hties = ctx->down.take<int32_t>(1);
+  int64_t* hlb = ctx->down.take<int64_t>(1);
+  int32_t* hph = ctx->down.take<int32_t>(nph);
+  int32_t* herr = ctx->down.take<int32_t>(1);
+  unsigned long long* hcp = ctx->down.take<unsigned long long>(1);
+  unsigned long long* hbad = ctx->down.take<unsigned long long>(1);
+  double* hq = ctx->down.take<double>(4);
+  int32_t* hfl = ctx->down.take<int32_t>(1);
+  uint32_t* hni = ctx->down.take<uint32_t>(1);
+  *hcp = 0;
+  RV_CUDA(cudaMemcpyAsync(herr, ctx->dp_err.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hbad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  if (cull) RV_CUDA(cudaMemcpyAsync(hcp, ctx->c_pairs.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hbest, ctx->dp_best.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hties, ctx->dp_ties.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hlb, ctx->dp_lb.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hph, ctx->dp_phase.p, 4 * (size_t)nph, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hq, ctx->qs.p, 32, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hfl, ctx->flags.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hni, ctx->ninl.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
+  RV_SYNC(cudaEventSynchronize(ctx->ev1), "one-pass solve");
+  ctx->collect_vote_ms();
+  ctx->ev_collect();
+  ctx->cev_collect();
+  ctx->cull_ready = false;
+  if (*hbad != ~0ull)
+    return ctx->fail(RV_EDATA, "correspondence row %llu has a zero-length or non-finite vector",
+                     *hbad);
+  if (*herr != 0) {  // a capacity or the re-dive: the per-level loop redoes the solve
+    *redo = true;
+    ctx->redo_reason = *herr;
+    return RV_OK;
+  }
+  // ---- the result (as solve_batched_dplan + fill_result + run_refine)
+  rv_plan_result r{};
+  r.votes = (uint32_t)(*hbest >> 32);
+  r.lin = *hbest ? 0xffffffffu - (uint32_t)(*hbest & 0xffffffffu) : 0u;
+  r.B = ch[L - 1];
+  r.n_tied = *hties;
+  r.lb_star = (uint32_t)*hlb;
+  const int32_t nre = hph[nph - 1];
+  r.n_rechecked = nre;
+  auto add = [&](int64_t c) {
+    r.pair_votes += (uint64_t)c * (uint64_t)n;
+    r.cells_evaluated += (uint64_t)c;
+    if (r.n_phases < 16) r.cells_per_phase[r.n_phases++] = c;
+  };
+  add(m0);
+  for (int p = 0; p + 1 < nph; ++p) add(hph[p]);
+  if (nre > 0) add(nre);
+  fill_result(r, out);
+  // no successful round keeps q0: the host's block centre (as the per-level loop returns it;
+  // the device-decoded copy can differ in the last bit)
+  if (*hfl & RV_REFINED) std::memcpy(out->q, hq, 32);
+  else std::memcpy(out->q, out->q_cell, 32);
+  out->flags |= *hfl;
+  out->n_inliers = *hni;
+  if (cull) {
+    ctx->cull_pairs += *hcp;
+    ctx->vote_pairs += (uint64_t)m0 * (uint64_t)n;
+  } else {
+    ctx->vote_pairs += r.pair_votes - (uint64_t)nre * (uint64_t)n;
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ph[0], ctx->ev1);
+  out->ms = ms;
+  float* tp[6] = {&out->t_setup_ms, &out->t_level0_ms, &out->t_dive_ms, &out->t_bnb_ms,
+                  &out->t_final_ms, &out->t_refine_ms};
+  for (int k = 0; k < 6; ++k) cudaEventElapsedTime(tp[k], ph[k], ph[k + 1]);
+  return RV_OK;
+}
+
 int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets,
                        int32_t P, double eps, int32_t levels, rv_result* out, uint32_t* masks) {
   if (int rc = validate_common(ctx, x, y, eps, levels)) return rc;
@@ -752,6 +1100,23 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
       return ctx->fail(RV_EINVAL, "problem %d has fewer than 2 correspondences", p);
   if (offsets[P] > ctx->cfg.max_n) return ctx->fail(RV_EINVAL, "total rows exceed max_n");
   cudaStream_t s = ctx->stream;
+  {
+    const int32_t lev = levels == 0 ? std::min<int32_t>(5, (int32_t)ctx->chain.size()) : levels;
+    const std::vector<int32_t> ch(ctx->chain.end() - lev, ctx->chain.end());
+    if (one_pass_applies(ctx, P) && dplan_applies(ctx, lev, ch[0], eps)) {
+      bool redo = false;
+      if (int rc = solve_one_pass(ctx, x, y, offsets[1], eps, ch, out, masks, &redo)) return rc;
+      if (!redo) {
+        out->launches = ctx->launches;
+        ctx->fill_counters(*out);
+        return RV_OK;
+      }
+      const int32_t hs = ctx->host_syncs;
+      ctx->reset_counters();  // the per-level loop below redoes the solve
+      ctx->host_syncs = hs;
+      ctx->retried = true;
+    }
+  }
   RV_CUDA(cudaEventRecord(ctx->ev0, s), "event");
   const int W = ctx->cfg.world;
   int64_t pb, pe;
@@ -835,7 +1200,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
             std::vector<int32_t> start(PL);
             RV_CUDA(cudaMemcpyAsync(start.data(), ctx->l0idx.p, PL * 4, cudaMemcpyDeviceToHost,
                                     ctx->stream), "D2H");
-            RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 argmax");
+            RV_SYNC(cudaStreamSynchronize(ctx->stream), "level-0 argmax");
             std::vector<int> bad(PL, 0);
             parallel_for(PL, [&](int64_t p) { bad[p] = rv_plan_feed_l0_start(plans[p], start[p]); });
             for (int b : bad)
@@ -884,7 +1249,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
         rv::launch_l0_survivors(ctx->l0cnt.p, m0, dprob, dlb, nullptr, J, dcnt, nullptr, ctx->stream);
         std::vector<int32_t> k(J);
         RV_CUDA(cudaMemcpyAsync(k.data(), dcnt, J * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-        RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
+        RV_SYNC(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
         std::vector<int64_t> offv(J + 1, 0);
         for (int32_t j = 0; j < J; ++j) offv[j + 1] = offv[j] + k[j];
         DevBuf<int32_t>& surv = ctx->l0surv;
@@ -895,7 +1260,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
         std::vector<int32_t> idx(std::max<int64_t>(1, offv[J]));
         RV_CUDA(cudaMemcpyAsync(idx.data(), surv.p, offv[J] * 4, cudaMemcpyDeviceToHost, ctx->stream),
                 "D2H");
-        RV_CUDA(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
+        RV_SYNC(cudaStreamSynchronize(ctx->stream), "level-0 survivors");
         std::vector<int> bad(J, 0);
         parallel_for(J, [&](int64_t j) {
           bad[j] = rv_plan_feed_l0_survivors(plans[need[j]], idx.data() + offv[j], k[j]);
@@ -937,7 +1302,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
     }
   }
   RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
-  RV_CUDA(cudaEventSynchronize(ctx->ev1), "event");
+  RV_SYNC(cudaEventSynchronize(ctx->ev1), "event");
   float ms = 0;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   for (rv_result& r : local) {
@@ -965,7 +1330,7 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
   ctx->down.reset();
   char* hd = ctx->down.take<char>(slot * W);
   RV_CUDA(cudaMemcpyAsync(hd, ctx->gather.p, slot * W, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaStreamSynchronize(s), "gather");
+  RV_SYNC(cudaStreamSynchronize(s), "gather");
   for (int r = 0; r < W; ++r) {
     int64_t b, e;
     rv_shard_range(P, r, W, &b, &e);

@@ -63,7 +63,7 @@ int check_bad(rv_ctx* ctx) {
   unsigned long long b = 0;
   RV_CUDA(cudaMemcpyAsync(&b, ctx->bad.p, sizeof(b), cudaMemcpyDeviceToHost, ctx->stream),
           "reading data flag");
-  RV_CUDA(cudaStreamSynchronize(ctx->stream), "rv_setup");
+  RV_SYNC(cudaStreamSynchronize(ctx->stream), "rv_setup");
   if (b != ~0ull)
     return ctx->fail(RV_EDATA, "correspondence row %llu has a zero-length or non-finite vector", b);
   return RV_OK;
@@ -130,7 +130,7 @@ int run_refine(rv_ctx* ctx, const float* x, const float* y, const int64_t* offse
   RV_CUDA(cudaMemcpyAsync(dq, ctx->qs.p, (size_t)P * 32, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(df, ctx->flags.p, P * 4, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(dn, ctx->ninl.p, P * 4, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaStreamSynchronize(s), "refinement");
+  RV_SYNC(cudaStreamSynchronize(s), "refinement");
   std::memcpy(q_out, dq, (size_t)P * 32);
   for (int32_t p = 0; p < P; ++p) flags_out[p] = df[p] & (RV_REFINED | RV_DEGENERATE);
   std::memcpy(ninl_out, dn, P * 4);

@@ -53,7 +53,9 @@ class rv_result(C.Structure):
                 ("n_rechecked", C.c_int32), ("vote_ms", C.c_float), ("launches", C.c_int32),
                 ("vote_pairs", C.c_uint64), ("vote_launches", C.c_int32),
                 ("cull_launches", C.c_int32), ("cull_pairs", C.c_uint64), ("cull_ms", C.c_float),
-                ("cull_tc_launches", C.c_int32)]
+                ("cull_tc_launches", C.c_int32), ("host_syncs", C.c_int32),
+                ("t_setup_ms", C.c_float), ("t_level0_ms", C.c_float), ("t_dive_ms", C.c_float),
+                ("t_bnb_ms", C.c_float), ("t_final_ms", C.c_float), ("t_refine_ms", C.c_float)]
 
 
 class rv_alg1_result(C.Structure):
@@ -178,6 +180,10 @@ def _dptr(t, dtype, name):
     return t.data_ptr()
 
 
+PHASES = ("setup", "level0", "dive", "bnb", "final", "refine")
+RV_RETRIED = 8
+
+
 @dataclass
 class Result:
     q: np.ndarray
@@ -202,6 +208,8 @@ class Result:
     cull_pairs: int = 0
     cull_ms: float = 0.0
     cull_tc_launches: int = 0
+    host_syncs: int = 0
+    phase_ms: dict = None   # one-pass solves: device time per phase (CUDA events)
 
     @property
     def lin(self) -> int:
@@ -218,7 +226,8 @@ class Result:
                       launches=r.launches, vote_pairs=r.vote_pairs,
                       vote_launches=r.vote_launches, cull_launches=r.cull_launches,
                       cull_pairs=r.cull_pairs, cull_ms=r.cull_ms,
-                      cull_tc_launches=r.cull_tc_launches)
+                      cull_tc_launches=r.cull_tc_launches, host_syncs=r.host_syncs,
+                      phase_ms={k: getattr(r, f"t_{k}_ms") for k in PHASES})
 
 
 class RotVote:
@@ -230,7 +239,9 @@ class RotVote:
                  emulate_world: int = 0, tensor_vote: bool = True, cull=True,
                  planner: str = "device"):
         """cull: True / "tc" (K3-CT, default), "fp32" (K3-C), False (off).
-        planner: "device" (the level loop on the GPU, default) or "host" (rv_plan.cpp)."""
+        planner: "device" (the level loop on the GPU, one host round trip per single solve;
+        default), "device_sync" (the device loop with a round trip per level, the one-pass
+        solve's fallback) or "host" (rv_plan.cpp)."""
         import torch
         self._kw = dict(device=device, max_n=max_n, max_problems=max_problems, chain=chain,
                         refine_rounds=refine_rounds, guard=guard, stream=stream, rank=rank,
@@ -258,7 +269,7 @@ class RotVote:
         cfg.emulate_world = int(emulate_world)
         cfg.tensor_vote = int(bool(tensor_vote))
         cfg.cull = {True: 1, "tc": 1, "fp32": 2, False: 0, None: 0}[cull]
-        cfg.planner = {"device": 0, "host": 1}[planner]
+        cfg.planner = {"device": 0, "host": 1, "device_sync": 2}[planner]
         self.cfg = cfg
         self.device = device
         self.chain = tuple(chain) if chain is not None else DEFAULT_CHAIN

@@ -1,0 +1,139 @@
+"""The one-pass single solve (csrc/rv_level_loop.cpp solve_one_pass: the whole certified search
+and the refinement enqueued with no host round trip, one read-back per solve) against the
+device loop with per-level round trips (planner="device_sync", its fallback), the host planner
+(planner="host") and the oracle.
+
+Every decision of the one-pass loop is the per-level loop's, and its fused refinement
+(rv_refine1_kernel) keeps K6/K7's decomposition and summation order, so the results must be
+bit-identical: winner, votes, ties, lb*, per-phase block counts, refined q, flags and the mask.
+A solve that outgrows the fixed capacities or meets the re-dive trigger (R18) is redone by the
+per-level loop (flag RV_RETRIED) and must still be identical."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+RV_RETRIED = 8
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+
+
+def solve_all(torch, rv, pr, levels=0):
+    """(result, mask) of one solve on a context."""
+    x, y = dev(torch, pr.x), dev(torch, pr.y)
+    mask = torch.zeros((pr.n + 31) // 32, dtype=torch.int32, device="cuda")
+    r = rv.solve(x, y, pr.eps, levels=levels, mask=mask)
+    return r, mask.cpu().numpy()
+
+
+def same(a, b, ma, mb, phases=True):
+    assert (a.cell, a.votes, a.n_tied, a.lb_star) == (b.cell, b.votes, b.n_tied, b.lb_star)
+    assert np.array_equal(a.q, b.q), (a.q, b.q)
+    assert (a.n_inliers, a.flags & ~RV_RETRIED) == (b.n_inliers, b.flags & ~RV_RETRIED)
+    assert np.array_equal(ma, mb)
+    if phases:
+        assert a.cells_per_phase == b.cells_per_phase
+        assert (a.n_rechecked, a.pair_votes) == (b.n_rechecked, b.pair_votes)
+
+
+PROBLEMS = [
+    ("cfg1", lambda: datagen.cfg1()),
+    ("n2", lambda: datagen.make_problem(2, 2, 0.0, 0.05, seed=3)),
+    ("n37", lambda: datagen.make_problem(37, 20, 0.01, 0.05, seed=4)),
+    ("n4000", lambda: datagen.make_problem(4000, 400, 0.01, 0.05, seed=1)),
+    ("n20k_99", lambda: datagen.make_problem(20000, 200, 0.01, 0.05, seed=2)),
+    ("cfg2", lambda: datagen.cfg2()),
+]
+
+
+@pytest.mark.parametrize("name,mk", PROBLEMS)
+@pytest.mark.parametrize("cull", [True, False])
+def test_one_pass_equals_per_level_loop(torch_cuda, name, mk, cull):
+    from paper_2506_11547_b200 import RotVote
+    pr = mk()
+    rv = RotVote(max_n=max(pr.n, 64), cull=cull)
+    sync = rv.twin(planner="device_sync")
+    try:
+        a, ma = solve_all(torch_cuda, rv, pr)
+        b, mb = solve_all(torch_cuda, sync, pr)
+        same(a, b, ma, mb)
+        if not a.flags & RV_RETRIED:
+            assert a.host_syncs == 1, a.host_syncs
+            assert b.host_syncs > a.host_syncs
+            # phase times: every phase measured, their sum is the solve
+            t = a.phase_ms
+            assert all(v >= 0.0 for v in t.values()), t
+            assert abs(sum(t.values()) - a.ms) <= 0.05 * a.ms + 0.05, (t, a.ms)
+        ref = oracle.solve(pr.x, pr.y, pr.eps)
+        assert (a.cell, a.votes, a.n_tied) == (ref.cell, ref.votes, ref.n_tied)
+    finally:
+        rv.close()
+        sync.close()
+
+
+@pytest.mark.parametrize("levels", [2, 3, 4, 5])
+def test_one_pass_levels_and_host_planner(torch_cuda, levels):
+    from paper_2506_11547_b200 import RotVote
+    pr = datagen.make_problem(6000, 300, 0.01, 0.05, seed=10 + levels)
+    rv = RotVote(max_n=pr.n)
+    host = rv.twin(planner="host")
+    try:
+        a, ma = solve_all(torch_cuda, rv, pr, levels)
+        b, mb = solve_all(torch_cuda, host, pr, levels)
+        same(a, b, ma, mb, phases=False)
+        assert a.host_syncs == 1 or a.flags & RV_RETRIED
+    finally:
+        rv.close()
+        host.close()
+
+
+def test_one_pass_retry_path(torch_cuda):
+    """A wide inlier angle (eps = 0.6 rad): a correspondence passes the bound test of ~25% of
+    the level-0 blocks, so the culling lists outgrow the one-pass capacity (an eighth of the
+    level-0 pairs); the one-pass solve must hand the problem to the per-level loop and still
+    return its exact result."""
+    from paper_2506_11547_b200 import RotVote
+    pr = datagen.make_problem(3000, 900, 0.01, 0.6, seed=7)
+    n = pr.n
+    rv = RotVote(max_n=n, chain=(15, 45, 90, 180, 360))
+    sync = rv.twin(planner="device_sync")
+    try:
+        a, ma = solve_all(torch_cuda, rv, pr)
+        b, mb = solve_all(torch_cuda, sync, pr)
+        same(a, b, ma, mb)
+        assert a.flags & RV_RETRIED, "expected the one-pass solve to be redone"
+        assert a.host_syncs > 1
+    finally:
+        rv.close()
+        sync.close()
+
+
+def test_one_pass_full_size_cfg4(torch_cuda):
+    """The bench's workload (cfg4, chain 15-45-180-360): one pass, identical to the per-level
+    loop, and the oracle's winner (the full oracle solve is in test_gpu_fullsize.py)."""
+    from paper_2506_11547_b200 import RotVote
+    pr = datagen.cfg4()
+    rv = RotVote(max_n=pr.n, chain=(15, 45, 180, 360))
+    sync = rv.twin(planner="device_sync")
+    try:
+        a, ma = solve_all(torch_cuda, rv, pr)
+        b, mb = solve_all(torch_cuda, sync, pr)
+        same(a, b, ma, mb)
+        assert a.host_syncs == 1 and not a.flags & RV_RETRIED
+        assert a.votes == 10605
+    finally:
+        rv.close()
+        sync.close()

@@ -44,9 +44,9 @@ def test_struct_sizes_match_header(L):
 #include <stddef.h>
 #include "rotvote.h"
 #include "rotvote_plan.h"
-int main(){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(rv_config), sizeof(rv_result),
+int main(){printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(rv_config), sizeof(rv_result),
  sizeof(rv_plan_result), offsetof(rv_result, ms), offsetof(rv_config, stream),
- offsetof(rv_result, cells_per_phase));return 0;}
+ offsetof(rv_result, cells_per_phase), offsetof(rv_result, t_refine_ms));return 0;}
 '''
     with tempfile.TemporaryDirectory() as d:
         c = os.path.join(d, "t.c")
@@ -55,7 +55,8 @@ int main(){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(rv_config), sizeof(rv_resu
         subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
         got = [int(v) for v in subprocess.check_output([exe]).split()]
     want = [C.sizeof(rv.rv_config), C.sizeof(rv.rv_result), C.sizeof(rv.rv_plan_result),
-            rv.rv_result.ms.offset, rv.rv_config.stream.offset, rv.rv_result.cells_per_phase.offset]
+            rv.rv_result.ms.offset, rv.rv_config.stream.offset, rv.rv_result.cells_per_phase.offset,
+            rv.rv_result.t_refine_ms.offset]
     assert got == want
 
 
