@@ -408,6 +408,7 @@ def run_ours(args):
     barrier()
     step_ms, vote_ms, vote_pairs, launches, vote_launches = [], 0.0, 0, 0, 0
     cull_ms, cull_pairs, cull_tc = 0.0, 0, 0
+    phases, syncs = [], []
     pair_votes = res.pair_votes
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -425,6 +426,8 @@ def run_ours(args):
             cull_ms += r.cull_ms
             cull_pairs += r.cull_pairs
             cull_tc += r.cull_tc_launches
+            phases.append(r.phase_ms or {})
+            syncs.append(r.host_syncs)
             assert (r.cell, r.votes) == (res.cell, res.votes)
     barrier()
     total = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
@@ -484,6 +487,11 @@ def run_ours(args):
                    "q": [float(v) for v in res.q],
                    "rotation_error_deg": _rot_err_deg(pr.R, res.q)},
         "ms_per_step_median": float(sorted(step_ms)[len(step_ms) // 2]),
+        # device time per phase of the one-pass solve (CUDA events inside the library; median
+        # over the timed steps) and the host waits per solve
+        "phase_ms": {k: statistics.median(p.get(k, 0.0) for p in phases)
+                     for k in ("setup", "level0", "dive", "bnb", "final", "refine")},
+        "host_syncs_per_solve": max(syncs) if syncs else None,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         host = _host_info()

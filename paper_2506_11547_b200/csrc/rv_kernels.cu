@@ -527,6 +527,42 @@ void launch_inliers(const float* x, const float* y, const RefSeg* segs, const Re
 // ------------------------------------------------------------------------------------------
 constexpr int32_t kStop = 1 << 8;  // internal: a round failed, later rounds keep q
 
+// Jacobi rotation (p, q) of A (similarity) and V (accumulated), given c, s
+__device__ __forceinline__ void jrot(double A[4][4], double V[4][4], int p, int q, double c,
+                                     double s) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double akp = A[k][p], akq = A[k][q];
+    A[k][p] = c * akp - s * akq;
+    A[k][q] = s * akp + c * akq;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double apk = A[p][k], aqk = A[q][k];
+    A[p][k] = c * apk - s * aqk;
+    A[q][k] = s * apk + c * aqk;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double vkp = V[k][p], vkq = V[k][q];
+    V[k][p] = c * vkp - s * vkq;
+    V[k][q] = s * vkp + c * vkq;
+  }
+}
+// rotation zeroing A[p][q]: tan(2 phi) = 2 apq / (aqq - app), t = tan phi in the stable form
+// sign(d) apq / (|d| + sqrt(d^2 + apq^2)), d = (aqq - app) / 2 (one sqrt, one division)
+__device__ __forceinline__ void jparams(double app, double aqq, double apq, double& c, double& s) {
+  const double d = 0.5 * (aqq - app);
+  const double t = copysign(1.0, d) * apq / (fabs(d) + sqrt(d * d + apq * apq));
+  c = rsqrt(1.0 + t * t);
+  s = t * c;
+}
+
+// 4x4 symmetric eigen-decomposition by Jacobi sweeps in the parallel (round-robin) order: each
+// sweep is three rounds of two disjoint rotations, (0,1)(2,3), (0,2)(1,3), (0,3)(1,2), whose
+// parameters are computed side by side (the serial solve's latency is the point: it runs on one
+// thread between two grid-wide passes).  Stops when the off-diagonal mass is below 1e-32 of the
+// diagonal's (relative 1e-16).
 __device__ void jacobi4(double A[4][4], double V[4][4]) {
 #pragma unroll
   for (int r = 0; r < 4; ++r)
@@ -540,36 +576,18 @@ __device__ void jacobi4(double A[4][4], double V[4][4]) {
 #pragma unroll
       for (int c = r + 1; c < 4; ++c) off += A[r][c] * A[r][c];
     }
-    if (off == 0.0 || off <= 1e-36 * diag) break;
+    if (off == 0.0 || off <= 1e-32 * diag) break;
 #pragma unroll
-    for (int p = 0; p < 3; ++p)
-#pragma unroll
-      for (int qq = p + 1; qq < 4; ++qq) {
-        const double apq = A[p][qq];
-        if (apq == 0.0) continue;
-        // rotation zeroing A[p][qq]: tan(2 phi) = 2 apq / (aqq - app)
-        const double zeta = (A[qq][qq] - A[p][p]) / (2.0 * apq);
-        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = rsqrt(1.0 + t * t), s = t * c;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double akp = A[k][p], akq = A[k][qq];
-          A[k][p] = c * akp - s * akq;
-          A[k][qq] = s * akp + c * akq;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double apk = A[p][k], aqk = A[qq][k];
-          A[p][k] = c * apk - s * aqk;
-          A[qq][k] = s * apk + c * aqk;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double vkp = V[k][p], vkq = V[k][qq];
-          V[k][p] = c * vkp - s * vkq;
-          V[k][qq] = s * vkp + c * vkq;
-        }
-      }
+    for (int rd = 0; rd < 3; ++rd) {
+      const int p1 = 0, q1 = rd + 1;                        // (0,1) (0,2) (0,3)
+      const int p2 = rd == 0 ? 2 : 1, q2 = rd == 2 ? 2 : 3;  // (2,3) (1,3) (1,2)
+      double c1 = 1.0, s1 = 0.0, c2 = 1.0, s2 = 0.0;
+      const bool r1 = A[p1][q1] != 0.0, r2 = A[p2][q2] != 0.0;
+      if (r1) jparams(A[p1][p1], A[q1][q1], A[p1][q1], c1, s1);
+      if (r2) jparams(A[p2][p2], A[q2][q2], A[p2][q2], c2, s2);
+      if (r1) jrot(A, V, p1, q1, c1, s1);
+      if (r2) jrot(A, V, p2, q2, c2, s2);
+    }
   }
 }
 
@@ -704,9 +722,29 @@ __device__ __forceinline__ void r1_stamp(int) {}
 constexpr int kR1Threads = kRefThreads;  // K6's decomposition (see below)
 static_assert(kRefRowsPerItem % kRefThreads == 0, "K6 items are whole rounds of rows");
 
+// Grid-wide barrier of a cooperative launch (all CTAs co-resident): thread 0 of each CTA
+// arrives on a counter and polls it with relaxed loads and a short sleep; one fence after.  (The
+// cooperative-groups barrier polls with L1-invalidating acquire loads, and a CTA sharing its SM
+// with the one doing the serial eigen step slowed that step ~5x.)
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++gen;
+    __threadfence();
+    atomicAdd(bar, 1u);
+    const uint32_t target = gen * gridDim.x;
+    uint32_t v;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v < target) __nanosleep(32);
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
+  uint32_t gen = 0;  // grid barriers passed (a.bar counts arrivals; zeroed before the launch)
   __shared__ double ws[kR1Threads / 32][10];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -736,7 +774,7 @@ __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
     *a.flags = 0;
   }
   r1_stamp(0);
-  grid.sync();
+  grid_barrier(a.bar, gen);
   r1_stamp(1);
   const float t_hi = (float)(a.tau + (double)a.guard), t_lo = (float)(a.tau - (double)a.guard);
   // K6's decomposition exactly (items of kRefRowsPerItem rows, warp w takes rows w*32 + lane +
@@ -810,12 +848,12 @@ __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
       if (threadIdx.x < 10) {
         double v = 0.0;
         for (int w = 0; w < kR1Threads / 32; ++w) v += ws[w][threadIdx.x];
-        a.partials[itm * 10 + threadIdx.x] = v;
+        __stcg(a.partials + itm * 10 + threadIdx.x, v);
       }
       __syncthreads();
     }
     r1_stamp(2 + 4 * r);
-    grid.sync();
+    grid_barrier(a.bar, gen);
     r1_stamp(3 + 4 * r);
     if (blockIdx.x == 0) {  // K7's per-CTA sum: thread t takes items t, t + 256, ...
       double S[10];
@@ -823,14 +861,17 @@ __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
       for (int t = 0; t < 10; ++t) S[t] = 0.0;
       for (int64_t b = threadIdx.x; b < n_items; b += kR1Threads)
 #pragma unroll
-        for (int t = 0; t < 10; ++t) S[t] += a.partials[b * 10 + t];
+        for (int t = 0; t < 10; ++t) S[t] += __ldcg(a.partials + b * 10 + t);
+      r1_stamp(16 + 4 * r);
 #pragma unroll
       for (int t = 0; t < 10; ++t)
         for (int o = 16; o > 0; o >>= 1) S[t] += __shfl_down_sync(0xffffffffu, S[t], o);
       if (lane == 0)
 #pragma unroll
         for (int t = 0; t < 10; ++t) ws[warp][t] = S[t];
+      r1_stamp(17 + 4 * r);
       __syncthreads();
+      r1_stamp(18 + 4 * r);
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int t = 0; t < 10; ++t) {
@@ -843,7 +884,7 @@ __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
       }
     }
     r1_stamp(4 + 4 * r);
-    grid.sync();
+    grid_barrier(a.bar, gen);
     r1_stamp(5 + 4 * r);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.flags &= (RV_REFINED | RV_DEGENERATE);
@@ -863,6 +904,8 @@ cudaError_t launch_refine1(const Refine1Args& a, int num_sms, cudaStream_t s) {
   const int grid = num_sms * per_sm[dev];
   if (grid > kRefine1MaxCtas) return cudaErrorInvalidConfiguration;
   Refine1Args args = a;
+  cudaError_t e = cudaMemsetAsync(args.bar, 0, 4, s);
+  if (e != cudaSuccess) return e;
   void* kargs[] = {&args};
   return cudaLaunchCooperativeKernel((const void*)rv_refine1_kernel, dim3(grid), dim3(kR1Threads),
                                      kargs, 0, s);

@@ -249,6 +249,7 @@ struct Refine1Args {
   int32_t* flags;
   uint32_t* ninl;
   uint32_t* mask;
+  uint32_t* bar;         // DEVICE grid-barrier counter, zeroed by launch_refine1
 };
 cudaError_t launch_refine1(const Refine1Args& a, int num_sms, cudaStream_t s);
 

@@ -1003,10 +1003,11 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
           "allocating");
   RV_CUDA(ctx->qs.ensure(4), "allocating");
   RV_CUDA(ctx->flags.ensure(1), "allocating");
-  RV_CUDA(ctx->ninl.ensure(1), "allocating");
+  RV_CUDA(ctx->ninl.ensure(2), "allocating");  // [1]: the refinement's grid-barrier counter
   rv::Refine1Args ra{x, y, n, ctx->k9.p, ctx->stride, std::cos(eps), ctx->cfg.guard,
                      ctx->cfg.refine_rounds, ctx->dp_best.p, ch[L - 1], nullptr,
-                     ctx->partials.p, ctx->qs.p, ctx->flags.p, ctx->ninl.p, mask};
+                     ctx->partials.p, ctx->qs.p, ctx->flags.p, ctx->ninl.p, mask,
+                     reinterpret_cast<uint32_t*>(ctx->ninl.p + 1)};
   RV_CUDA(rv::launch_refine1(ra, ctx->num_sms, s), "launching the refinement");
   ctx->launches += 1;
   nvtxRangePop();

@@ -16,4 +16,8 @@ t0 = buf[0]
 names = ["q0", "q0 sync"] + [f"r{r} {w}" for r in range(3) for w in ("pass", "sync1", "eig", "sync2")]
 for k in range(14):
     print(f"{names[k]:>10s} {(buf[k] - t0) / 1000:8.2f} us")
+for r_ in range(3):
+    print(f"  round {r_}: after sync1 -> loads {(buf[16+4*r_]-buf[3+4*r_])/1000:.2f} us, -> shuffles "
+          f"{(buf[17+4*r_]-buf[16+4*r_])/1000:.2f}, -> syncthreads {(buf[18+4*r_]-buf[17+4*r_])/1000:.2f}, "
+          f"-> eig done {(buf[4+4*r_]-buf[18+4*r_])/1000:.2f}")
 print("refine phase ms", r.phase_ms["refine"])
