@@ -122,6 +122,10 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->evv0);
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->evv1);
   for (int k = 0; k < 8 && e == cudaSuccess; ++k) e = cudaEventCreate(&ctx->ph[k]);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->gfork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->gjoin, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&ctx->grb), 4096);
   if (e == cudaSuccess) {
     ctx->stride = pad4(cfg->max_n) + 64;
     e = ctx->k9.ensure((size_t)9 * ctx->stride);
@@ -193,6 +197,11 @@ void rot_vote_destroy(rv_ctx* ctx) {
   if (ctx->evv1) cudaEventDestroy(ctx->evv1);
   for (cudaEvent_t e : ctx->ph)
     if (e) cudaEventDestroy(e);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->gfork) cudaEventDestroy(ctx->gfork);
+  if (ctx->gjoin) cudaEventDestroy(ctx->gjoin);
+  if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
+  if (ctx->grb) cudaFreeHost(ctx->grb);
   delete ctx;
 }
 

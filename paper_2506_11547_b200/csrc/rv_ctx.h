@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -76,12 +77,17 @@ inline NcclApi& nccl() {
 }
 
 // ---- growable buffers ------------------------------------------------------------------------
+// Bumped by every workspace (re)allocation: a captured one-pass graph holds raw device pointers,
+// so it is replayed only while this is unchanged since its capture.
+inline std::atomic<uint64_t> g_realloc_epoch{0};
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t cap = 0;
   cudaError_t ensure(size_t n) {
     if (n <= cap) return cudaSuccess;
+    g_realloc_epoch.fetch_add(1);
     size_t want = std::max<size_t>(n, cap * 3 / 2 + 64);
     if (p) cudaFree(p);
     p = nullptr;
@@ -259,6 +265,7 @@ struct rv_ctx {
       float ms = 0;
       if (cudaEventElapsedTime(&ms, evs[i], evs[i + 1]) == cudaSuccess) vote_ms += ms;
     }
+    cudaGetLastError();
     evn = 0;
   }
   // ancestor culling (rv_cull.cu): level-0 pass bitmasks, the K3-C rows, the level-0 lin ->
@@ -323,6 +330,7 @@ struct rv_ctx {
       float ms = 0;
       if (cudaEventElapsedTime(&ms, cevs[i], cevs[i + 1]) == cudaSuccess) cull_ms += ms;
     }
+    cudaGetLastError();
     cevn = 0;
   }
   DevBuf<int32_t> l0surv;        // host-planner batched path: level-0 survivor indices
@@ -338,6 +346,31 @@ struct rv_ctx {
   Staging up, down;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evv0 = nullptr, evv1 = nullptr;
   cudaEvent_t ph[8] = {};       // phase boundaries of a one-pass solve (rv_result.t_*_ms)
+  // one-pass solves as a CUDA graph: the enqueue sequence of a single solve depends only on
+  // (x, y, n, eps, levels, mask) and the context, so the second consecutive solve with the same
+  // key is captured (on gstream, forked from / joined to the caller's stream) and later ones
+  // replay it; grb is the graph's pinned read-back block (never reallocated)
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gfork = nullptr, gjoin = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  bool graphs_on = true;        // cleared for good if a capture fails
+  uint64_t gepoch = 0;          // g_realloc_epoch at the capture
+  uint64_t gkey[8] = {}, lastkey[8] = {};
+  bool gkey_ok = false, lastkey_ok = false;
+  char* grb = nullptr;          // pinned, 4 KB
+  bool capturing = false;
+  // an event record that becomes an event node of a captured graph (timing inside the graph)
+  cudaError_t record(cudaEvent_t e, cudaStream_t s) const {
+    return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                     : cudaEventRecord(e, s);
+  }
+  struct OnePassHost {          // host values of the captured enqueue (same on every replay)
+    int64_t m0 = 0;
+    int nph = 0;
+    bool cull = false;
+    int32_t launches = 0, vote_launches = 0, cull_launches = 0, cull_tc_launches = 0;
+    size_t evn = 0, cevn = 0;
+  } ghost;
   int32_t host_syncs = 0;       // host waits on the device in this call
   bool retried = false;         // a one-pass solve was redone by the per-level loop
   int32_t redo_reason = 0;      // its error word
@@ -418,8 +451,10 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
                  int32_t mode, int64_t m, const uint32_t* lins, uint32_t* cnt_a, uint32_t* cnt_b,
                  bool auto_tc = true);
 // rv_setup.cpp
+// dev_offsets (P == 1 only): the offset tables are written by a kernel from its arguments instead
+// of copied from pinned staging (a captured graph must not point at reusable host memory)
 int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
-              std::vector<int64_t>& koff_out);
+              std::vector<int64_t>& koff_out, bool dev_offsets = false);
 int check_bad(rv_ctx* ctx);
 int run_refine(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
                const int32_t* prob_ids, double eps, const double* qs0, int32_t rounds,

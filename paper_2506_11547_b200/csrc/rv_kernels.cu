@@ -890,6 +890,16 @@ __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.flags &= (RV_REFINED | RV_DEGENERATE);
 }
 
+// two int64 constants into device memory as a kernel (a one-pass solve's offsets: a captured
+// graph then carries them in its kernel arguments instead of pointing at host staging)
+__global__ void rv_set_i64x2_kernel(int64_t* d, int64_t v0, int64_t v1) {
+  d[0] = v0;
+  d[1] = v1;
+}
+void launch_set_i64x2(int64_t* d, int64_t v0, int64_t v1, cudaStream_t s) {
+  rv_set_i64x2_kernel<<<1, 1, 0, s>>>(d, v0, v1);
+}
+
 cudaError_t launch_refine1(const Refine1Args& a, int num_sms, cudaStream_t s) {
   static int per_sm[64] = {0};
   int dev = 0;

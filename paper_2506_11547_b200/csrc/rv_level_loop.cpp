@@ -162,7 +162,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     }
     cudaEvent_t e0, e1;
     RV_CUDA(ctx->cev_pair(&e0, &e1), "event");
-    RV_CUDA(cudaEventRecord(e0, s), "event");
+    RV_CUDA(ctx->record(e0, s), "event");
     if (ctx->cull_grouped)  // K3-CT
       rv::launch_vote_cull_tc(mode, ctx->vsegs.p, ctx->c_items.p, ctx->c_icnt.p, ctx->tctab_rm.p,
                               ctx->tc_toff.back(), ctx->c_tphi.p, ctx->c_cidx.p, ctx->c_lidx.p,
@@ -172,7 +172,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
       rv::launch_vote_cull(mode, ctx->vsegs.p, ctx->c_items.p, ctx->c_icnt.p, ctx->c_work.p,
                            ctx->c_pairs.p, ctx->c_phi.p, ctx->c_cidx.p, ctx->c_lidx.p,
                            ctx->cfg.guard, ctx->num_sms, s);
-    RV_CUDA(cudaEventRecord(e1, s), "event");
+    RV_CUDA(ctx->record(e1, s), "event");
     ctx->launches += 1;
     ctx->cull_launches += 1;
     ctx->cull_tc_launches += ctx->cull_grouped ? 1 : 0;
@@ -202,11 +202,11 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
     } else {
       cudaEvent_t e0, e1;
       RV_CUDA(ctx->ev_pair(&e0, &e1), "event");
-      RV_CUDA(cudaEventRecord(e0, s), "event");
+      RV_CUDA(ctx->record(e0, s), "event");
       rv::launch_vote_tc(ctx->tctab.p, ctx->atab.p, ctx->ablk.p, 0, ctx->vsegs.p, ctx->vitems.p, 0,
                          ctx->cfg.guard + kTcExtraGuard, nullptr, 0, s, im == 1, ctx->dp_icnt.p,
                          emit_bits);
-      RV_CUDA(cudaEventRecord(e1, s), "event");
+      RV_CUDA(ctx->record(e1, s), "event");
       ctx->launches += 2;
       ctx->vote_launches += 1;
     }
@@ -760,9 +760,32 @@ bool one_pass_applies(rv_ctx* ctx, int32_t P) {
          ctx->effective_world() == 1;
 }
 
-int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
-                   const std::vector<int32_t>& ch, rv_result* out, uint32_t* mask, bool* redo) {
-  *redo = false;
+// The read-back slots of a one-pass solve in ctx->grb (pinned)
+struct OnePassRB {
+  unsigned long long *best, *cp, *bad;
+  int32_t *ties, *err, *fl, *ph;
+  int64_t* lb;
+  double* q;
+  uint32_t* ni;
+  explicit OnePassRB(char* g) {
+    best = reinterpret_cast<unsigned long long*>(g);
+    cp = best + 1;
+    bad = best + 2;
+    lb = reinterpret_cast<int64_t*>(g + 24);
+    q = reinterpret_cast<double*>(g + 32);
+    ties = reinterpret_cast<int32_t*>(g + 64);
+    err = ties + 1;
+    fl = ties + 2;
+    ni = reinterpret_cast<uint32_t*>(ties + 3);
+    ph = ties + 4;  // up to 3 L + 1 phase counts
+  }
+};
+
+// Enqueue the whole solve on ctx->stream (no host wait), read-backs into ctx->grb; fills the
+// host values the result needs (hv).  Every size and launch shape is a function of (n, eps, ch)
+// and the context only, which is what makes the sequence graph-capturable.
+int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                     const std::vector<int32_t>& ch, uint32_t* mask, rv_ctx::OnePassHost& hv) {
   const int L = (int)ch.size();
   // the flat kernels loop over the device's own totals; their grids only need to fill the GPU
   auto flat_hint = [&](int64_t m) { return std::min<int64_t>(m, (int64_t)ctx->num_sms * 2 * 256); };
@@ -776,15 +799,14 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
   // pinned staging for every host-built upload of the solve (it is not reused before the final
   // sync): run_setup's offsets, the level-0 background, the dive / BnB offsets
   RV_CUDA(ctx->up.ensure((size_t)m0 * 8 + 65536), "allocating staging");
-  RV_CUDA(cudaEventRecord(ph[0], s), "event");
+  RV_CUDA(ctx->record(ph[0], s), "event");
   nvtxRangePushA("rv.setup");
-  if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;  // resets ctx->up, then takes
+  if (int rc = run_setup(ctx, x, y, offs, 1, koff, true)) return rc;
   nvtxRangePop();
-  RV_CUDA(cudaEventRecord(ph[1], s), "event");
+  RV_CUDA(ctx->record(ph[1], s), "event");
   auto upload_i64 = [&](int64_t* dst, std::initializer_list<int64_t> v) -> int {
-    int64_t* h = ctx->up.take<int64_t>(v.size());
-    std::copy(v.begin(), v.end(), h);
-    RV_CUDA(cudaMemcpyAsync(dst, h, v.size() * 8, cudaMemcpyHostToDevice, s), "H2D");
+    rv::launch_set_i64x2(dst, *v.begin(), *(v.begin() + 1), s);  // kernel arguments, see run_setup
+    ctx->launches += 1;
     return RV_OK;
   };
   int64_t nmax = n;
@@ -865,7 +887,7 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
                        ctx->l0idx.p, s);
   ctx->launches += 1;
   nvtxRangePop();
-  RV_CUDA(cudaEventRecord(ph[2], s), "event");
+  RV_CUDA(ctx->record(ph[2], s), "event");
   // ---- dive (fixed sizes: the 27-neighbourhood's children)
   nvtxRangePushA("rv.dive");
   for (int l = 1; l < L; ++l) {
@@ -894,7 +916,7 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
     ctx->launches += 1;
   }
   nvtxRangePop();
-  RV_CUDA(cudaEventRecord(ph[3], s), "event");
+  RV_CUDA(ctx->record(ph[3], s), "event");
   // ---- branch and bound from the level-0 survivors: lists alternate between sets 0 and 1 at
   // fixed capacities; offsets in the rings as in the per-level loop
   nvtxRangePushA("rv.bnb");
@@ -960,7 +982,7 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
     cur = nb;
   }
   nvtxRangePop();
-  RV_CUDA(cudaEventRecord(ph[4], s), "event");
+  RV_CUDA(ctx->record(ph[4], s), "event");
   // ---- finest level: max lo, exact-known blocks, the fp64 recheck, winner, ties
   nvtxRangePushA("rv.final");
   const int64_t fcapn = capl[L - 1];
@@ -996,7 +1018,7 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
                            ctx->dp_best.p, ctx->dp_ties.p, s);
   ctx->launches += 2;
   nvtxRangePop();
-  RV_CUDA(cudaEventRecord(ph[5], s), "event");
+  RV_CUDA(ctx->record(ph[5], s), "event");
   // ---- refinement from the winner (decoded on the device), K6 + K7 in one cooperative launch
   nvtxRangePushA("rv.refine");
   RV_CUDA(ctx->partials.ensure((size_t)((n + rv::kRefRowsPerItem - 1) / rv::kRefRowsPerItem) * 10),
@@ -1011,53 +1033,152 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
   RV_CUDA(rv::launch_refine1(ra, ctx->num_sms, s), "launching the refinement");
   ctx->launches += 1;
   nvtxRangePop();
-  RV_CUDA(cudaEventRecord(ph[6], s), "event");
-  // ---- the one read-back
-  RV_CUDA(ctx->down.ensure(4096), "allocating staging");
-  ctx->down.reset();
-  unsigned long long* hbest = ctx->down.take<unsigned long long>(1);
-  int32_t* hties = ctx->down.take<int32_t>(1);
-  int64_t* hlb = ctx->down.take<int64_t>(1);
-  int32_t* hph = ctx->down.take<int32_t>(nph);
-  int32_t* herr = ctx->down.take<int32_t>(1);
-  unsigned long long* hcp = ctx->down.take<unsigned long long>(1);
-  unsigned long long* hbad = ctx->down.take<unsigned long long>(1);
-  double* hq = ctx->down.take<double>(4);
-  int32_t* hfl = ctx->down.take<int32_t>(1);
-  uint32_t* hni = ctx->down.take<uint32_t>(1);
-  *hcp = 0;
-  RV_CUDA(cudaMemcpyAsync(herr, ctx->dp_err.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaMemcpyAsync(hbad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
-  if (cull) RV_CUDA(cudaMemcpyAsync(hcp, ctx->c_pairs.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaMemcpyAsync(hbest, ctx->dp_best.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaMemcpyAsync(hties, ctx->dp_ties.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaMemcpyAsync(hlb, ctx->dp_lb.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaMemcpyAsync(hph, ctx->dp_phase.p, 4 * (size_t)nph, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaMemcpyAsync(hq, ctx->qs.p, 32, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaMemcpyAsync(hfl, ctx->flags.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaMemcpyAsync(hni, ctx->ninl.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
-  RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
+  RV_CUDA(ctx->record(ph[6], s), "event");
+  // ---- the one read-back (into the pinned block; the host reads it after one wait)
+  OnePassRB rb(ctx->grb);
+  if (nph > 3 * L + 1) return ctx->fail(RV_ECUDA, "internal: phase slots");
+  RV_CUDA(cudaMemcpyAsync(rb.err, ctx->dp_err.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(rb.bad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  if (cull) RV_CUDA(cudaMemcpyAsync(rb.cp, ctx->c_pairs.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(rb.best, ctx->dp_best.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(rb.ties, ctx->dp_ties.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(rb.lb, ctx->dp_lb.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(rb.ph, ctx->dp_phase.p, 4 * (size_t)nph, cudaMemcpyDeviceToHost, s),
+          "D2H");
+  RV_CUDA(cudaMemcpyAsync(rb.q, ctx->qs.p, 32, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(rb.fl, ctx->flags.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(rb.ni, ctx->ninl.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  hv.m0 = m0;
+  hv.nph = nph;
+  hv.cull = cull;
+  return RV_OK;
+}
+
+// Key of a one-pass enqueue: everything its launch sequence depends on
+static void one_pass_key(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                         const std::vector<int32_t>& ch, const uint32_t* mask, uint64_t k[8]) {
+  uint64_t e;
+  std::memcpy(&e, &eps, 8);
+  k[0] = (uint64_t)(uintptr_t)x;
+  k[1] = (uint64_t)(uintptr_t)y;
+  k[2] = (uint64_t)n;
+  k[3] = e;
+  k[4] = (uint64_t)(uintptr_t)mask;
+  k[5] = ((uint64_t)ch.size() << 32) | (uint64_t)(uint32_t)ch[0];
+  k[6] = (uint64_t)(uintptr_t)ctx->stream;
+  k[7] = 0;
+  for (int32_t b : ch) k[7] = k[7] * 1009u + (uint64_t)b;
+}
+
+int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                   const std::vector<int32_t>& ch, rv_result* out, uint32_t* mask, bool* redo) {
+  *redo = false;
+  cudaStream_t s = ctx->stream;
+  uint64_t key[8];
+  one_pass_key(ctx, x, y, n, eps, ch, mask, key);
+  const bool same_as_last = ctx->lastkey_ok && std::memcmp(key, ctx->lastkey, sizeof(key)) == 0;
+  const bool replay = ctx->graphs_on && ctx->gexec && ctx->gkey_ok &&
+                      std::memcmp(key, ctx->gkey, sizeof(key)) == 0 &&
+                      ctx->gepoch == g_realloc_epoch.load();
+  rv_ctx::OnePassHost hv;
+  ctx->ev_reset();
+  ctx->cevn = 0;
+  if (replay) {
+    RV_CUDA(cudaEventRecord(ctx->gfork, s), "event");
+    RV_CUDA(cudaStreamWaitEvent(ctx->gstream, ctx->gfork, 0), "fork");
+    RV_CUDA(cudaGraphLaunch(ctx->gexec, ctx->gstream), "launching the solve graph");
+    RV_CUDA(cudaEventRecord(ctx->ev1, ctx->gstream), "event");
+    RV_CUDA(cudaEventRecord(ctx->gjoin, ctx->gstream), "event");
+    RV_CUDA(cudaStreamWaitEvent(s, ctx->gjoin, 0), "join");
+    hv = ctx->ghost;
+    ctx->launches = hv.launches;
+    ctx->vote_launches = hv.vote_launches;
+    ctx->cull_launches = hv.cull_launches;
+    ctx->cull_tc_launches = hv.cull_tc_launches;
+    ctx->evn = hv.evn;
+    ctx->cevn = hv.cevn;
+  } else if (ctx->graphs_on && same_as_last && ctx->gstream) {
+    // capture this enqueue (the previous solve with the same key ran it directly, so the
+    // workspace is sized and every one-time kernel attribute is set)
+    if (ctx->gexec) {
+      cudaGraphExecDestroy(ctx->gexec);
+      ctx->gexec = nullptr;
+      ctx->gkey_ok = false;
+    }
+    RV_CUDA(cudaEventRecord(ctx->gfork, s), "event");
+    RV_CUDA(cudaStreamWaitEvent(ctx->gstream, ctx->gfork, 0), "fork");
+    ctx->stream = ctx->gstream;
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeRelaxed);
+    int rc = RV_OK;
+    if (ce == cudaSuccess) {
+      ctx->capturing = true;
+      rc = enqueue_one_pass(ctx, x, y, n, eps, ch, mask, hv);
+      ctx->capturing = false;
+      cudaError_t ee = cudaStreamEndCapture(ctx->gstream, &g);
+      if (ce == cudaSuccess) ce = ee;
+    }
+    ctx->stream = s;
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    cudaGraphExec_t ge = nullptr;
+    if (ce == cudaSuccess) ce = cudaGraphInstantiateWithFlags(&ge, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (ce != cudaSuccess) {  // not capturable here: run directly from now on
+      cudaGetLastError();
+      ctx->graphs_on = false;
+      ctx->stream = s;
+      return solve_one_pass(ctx, x, y, n, eps, ch, out, mask, redo);
+    }
+    ctx->gexec = ge;
+    std::memcpy(ctx->gkey, key, sizeof(key));
+    ctx->gkey_ok = true;
+    ctx->gepoch = g_realloc_epoch.load();
+    hv.launches = ctx->launches;
+    hv.vote_launches = ctx->vote_launches;
+    hv.cull_launches = ctx->cull_launches;
+    hv.cull_tc_launches = ctx->cull_tc_launches;
+    hv.evn = ctx->evn;
+    hv.cevn = ctx->cevn;
+    ctx->ghost = hv;
+    RV_CUDA(cudaGraphLaunch(ctx->gexec, ctx->gstream), "launching the solve graph");
+    RV_CUDA(cudaEventRecord(ctx->ev1, ctx->gstream), "event");
+    RV_CUDA(cudaEventRecord(ctx->gjoin, ctx->gstream), "event");
+    RV_CUDA(cudaStreamWaitEvent(s, ctx->gjoin, 0), "join");
+  } else {
+    if (int rc = enqueue_one_pass(ctx, x, y, n, eps, ch, mask, hv)) return rc;
+    RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
+  }
+  std::memcpy(ctx->lastkey, key, sizeof(key));
+  ctx->lastkey_ok = true;
   RV_SYNC(cudaEventSynchronize(ctx->ev1), "one-pass solve");
   ctx->collect_vote_ms();
   ctx->ev_collect();
   ctx->cev_collect();
   ctx->cull_ready = false;
-  if (*hbad != ~0ull)
+  OnePassRB rb(ctx->grb);
+  const int64_t m0 = hv.m0;
+  const int nph = hv.nph;
+  const int L = (int)ch.size();
+  cudaEvent_t* ph = ctx->ph;
+  if (*rb.bad != ~0ull)
     return ctx->fail(RV_EDATA, "correspondence row %llu has a zero-length or non-finite vector",
-                     *hbad);
-  if (*herr != 0) {  // a capacity or the re-dive: the per-level loop redoes the solve
+                     *rb.bad);
+  if (*rb.err != 0) {  // a capacity or the re-dive: the per-level loop redoes the solve
     *redo = true;
-    ctx->redo_reason = *herr;
+    ctx->redo_reason = *rb.err;
     return RV_OK;
   }
   // ---- the result (as solve_batched_dplan + fill_result + run_refine)
   rv_plan_result r{};
-  r.votes = (uint32_t)(*hbest >> 32);
-  r.lin = *hbest ? 0xffffffffu - (uint32_t)(*hbest & 0xffffffffu) : 0u;
+  r.votes = (uint32_t)(*rb.best >> 32);
+  r.lin = *rb.best ? 0xffffffffu - (uint32_t)(*rb.best & 0xffffffffu) : 0u;
   r.B = ch[L - 1];
-  r.n_tied = *hties;
-  r.lb_star = (uint32_t)*hlb;
-  const int32_t nre = hph[nph - 1];
+  r.n_tied = *rb.ties;
+  r.lb_star = (uint32_t)*rb.lb;
+  const int32_t nre = rb.ph[nph - 1];
   r.n_rechecked = nre;
   auto add = [&](int64_t c) {
     r.pair_votes += (uint64_t)c * (uint64_t)n;
@@ -1065,17 +1186,17 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
     if (r.n_phases < 16) r.cells_per_phase[r.n_phases++] = c;
   };
   add(m0);
-  for (int p = 0; p + 1 < nph; ++p) add(hph[p]);
+  for (int p = 0; p + 1 < nph; ++p) add(rb.ph[p]);
   if (nre > 0) add(nre);
   fill_result(r, out);
   // no successful round keeps q0: the host's block centre (as the per-level loop returns it;
   // the device-decoded copy can differ in the last bit)
-  if (*hfl & RV_REFINED) std::memcpy(out->q, hq, 32);
+  if (*rb.fl & RV_REFINED) std::memcpy(out->q, rb.q, 32);
   else std::memcpy(out->q, out->q_cell, 32);
-  out->flags |= *hfl;
-  out->n_inliers = *hni;
-  if (cull) {
-    ctx->cull_pairs += *hcp;
+  out->flags |= *rb.fl;
+  out->n_inliers = *rb.ni;
+  if (hv.cull) {
+    ctx->cull_pairs += *rb.cp;
     ctx->vote_pairs += (uint64_t)m0 * (uint64_t)n;
   } else {
     ctx->vote_pairs += r.pair_votes - (uint64_t)nre * (uint64_t)n;
@@ -1086,6 +1207,7 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
   float* tp[6] = {&out->t_setup_ms, &out->t_level0_ms, &out->t_dive_ms, &out->t_bnb_ms,
                   &out->t_final_ms, &out->t_refine_ms};
   for (int k = 0; k < 6; ++k) cudaEventElapsedTime(tp[k], ph[k], ph[k + 1]);
+  cudaGetLastError();  // (a failed timing query must not surface in a later launch check)
   return RV_OK;
 }
 

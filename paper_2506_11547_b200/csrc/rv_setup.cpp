@@ -6,7 +6,7 @@ namespace rvi {
 
 // ---- K1 for P problems ----------------------------------------------------------------------
 int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
-              std::vector<int64_t>& koff_out) {
+              std::vector<int64_t>& koff_out, bool dev_offsets) {
   koff_out.assign(P + 1, 0);
   for (int32_t p = 0; p < P; ++p) koff_out[p + 1] = koff_out[p] + pad4(offsets[p + 1] - offsets[p]);
   const int64_t total = koff_out[P];
@@ -19,14 +19,20 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
   RV_CUDA(ctx->bad.ensure(1), "allocating flag");
   RV_CUDA(ctx->up.ensure(3 * (P + 1) * sizeof(int64_t) + 2048), "allocating staging");
   ctx->up.reset();
-  int64_t* hrows = ctx->up.take<int64_t>(P + 1);
-  int64_t* hk = ctx->up.take<int64_t>(P + 1);
-  std::memcpy(hrows, offsets, (P + 1) * sizeof(int64_t));
-  std::memcpy(hk, koff_out.data(), (P + 1) * sizeof(int64_t));
-  RV_CUDA(cudaMemcpyAsync(ctx->rows.p, hrows, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
-          "copying offsets");
-  RV_CUDA(cudaMemcpyAsync(ctx->koffs.p, hk, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
-          "copying offsets");
+  if (dev_offsets) {  // one problem: the offsets as kernel arguments (graph-capturable)
+    rv::launch_set_i64x2(ctx->rows.p, offsets[0], offsets[1], ctx->stream);
+    rv::launch_set_i64x2(ctx->koffs.p, koff_out[0], koff_out[1], ctx->stream);
+    ctx->launches += 2;
+  } else {
+    int64_t* hrows = ctx->up.take<int64_t>(P + 1);
+    int64_t* hk = ctx->up.take<int64_t>(P + 1);
+    std::memcpy(hrows, offsets, (P + 1) * sizeof(int64_t));
+    std::memcpy(hk, koff_out.data(), (P + 1) * sizeof(int64_t));
+    RV_CUDA(cudaMemcpyAsync(ctx->rows.p, hrows, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
+            "copying offsets");
+    RV_CUDA(cudaMemcpyAsync(ctx->koffs.p, hk, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
+            "copying offsets");
+  }
   RV_CUDA(cudaMemsetAsync(ctx->bad.p, 0xff, sizeof(unsigned long long), ctx->stream), "memset");
   rv::launch_setup(x, y, ctx->rows.p, ctx->koffs.p, P, total, ctx->k9.p, ctx->stride, ctx->bad.p,
                    ctx->stream);
@@ -40,10 +46,15 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
     // + one group of 8 padding rows after the last problem (K3-CT gathers it for padding)
     RV_CUDA(ctx->tctab.ensure((size_t)(toff[P] + 8) * 64), "allocating K3-TC table");
     RV_CUDA(ctx->toffs.ensure(P + 1), "allocating offsets");
-    int64_t* ht = ctx->up.take<int64_t>(P + 1);  // staging sized for it above
-    std::memcpy(ht, toff.data(), (P + 1) * sizeof(int64_t));
-    RV_CUDA(cudaMemcpyAsync(ctx->toffs.p, ht, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
-            "copying offsets");
+    if (dev_offsets) {
+      rv::launch_set_i64x2(ctx->toffs.p, toff[0], toff[1], ctx->stream);
+      ctx->launches += 1;
+    } else {
+      int64_t* ht = ctx->up.take<int64_t>(P + 1);  // staging sized for it above
+      std::memcpy(ht, toff.data(), (P + 1) * sizeof(int64_t));
+      RV_CUDA(cudaMemcpyAsync(ctx->toffs.p, ht, (P + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
+              "copying offsets");
+    }
     // the culled levels' rows: K3-CT's fp16-split row-major copy, or K3-C's fp32 rows (the
     // culled path cull_prepare will pick: K3-CT unless RV_CULL_TC=0 or a multi-rank batch)
     const bool ct = ctx->cull_on && ctx->cull_tc;

@@ -137,3 +137,33 @@ def test_one_pass_full_size_cfg4(torch_cuda):
     finally:
         rv.close()
         sync.close()
+
+
+def test_graph_replay_equals_direct(torch_cuda):
+    """The second solve with the same (x, y, n, eps, levels, mask) is captured as a CUDA graph
+    and later ones replay it: every solve must return the first (directly enqueued) result bit
+    for bit; a new mask buffer or eps starts over (direct, capture, replay)."""
+    from paper_2506_11547_b200 import RotVote
+    pr = datagen.make_problem(20000, 400, 0.01, 0.05, seed=21)
+    rv = RotVote(max_n=pr.n)
+    try:
+        x, y = dev(torch_cuda, pr.x), dev(torch_cuda, pr.y)
+        mask = torch_cuda.zeros((pr.n + 31) // 32, dtype=torch_cuda.int32, device="cuda")
+        ref = rv.solve(x, y, pr.eps, mask=mask)
+        m_ref = mask.cpu().numpy()
+        for k in range(4):
+            mask.zero_()
+            r = rv.solve(x, y, pr.eps, mask=mask)
+            same(r, ref, mask.cpu().numpy(), m_ref)
+            assert r.host_syncs == 1 and r.launches == ref.launches, (k, r.host_syncs, r.launches)
+            assert abs(sum(r.phase_ms.values()) - r.ms) <= 0.05 * r.ms + 0.05
+        mask2 = torch_cuda.zeros_like(mask)
+        for k in range(3):
+            r = rv.solve(x, y, pr.eps, mask=mask2)
+            same(r, ref, mask2.cpu().numpy(), m_ref)
+        r = rv.solve(x, y, pr.eps * 1.2, mask=mask2)  # another key: direct again
+        ref2 = rv.twin(planner="device_sync").solve(x, y, pr.eps * 1.2)
+        assert (r.cell, r.votes, r.n_tied) == (ref2.cell, ref2.votes, ref2.n_tied)
+        assert np.array_equal(r.q, ref2.q)
+    finally:
+        rv.close()
