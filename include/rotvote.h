@@ -99,6 +99,11 @@ typedef struct {
                             compare the device loop against; 2: the device loop with one host round
                             trip per branch-and-bound level (the one-pass solve's fallback).  Same
                             result.  Other values -> RV_EINVAL. */
+  int32_t ct_sched;      /* K3-CT item scheduling: 0 (default) = big levels take their items
+                            dynamically from a work counter (a scheduler warp per CTA), small ones
+                            in the static order b, b + grid, ...; 1 = always the static order.
+                            Same counts (integer sums); 1 exists so the tests can compare the
+                            two orders.  Other values -> RV_EINVAL. */
 } rv_config;
 
 typedef struct {

@@ -99,6 +99,7 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
   if (cfg->max_problems < 1 || cfg->refine_rounds < 0 || !(cfg->guard >= 0.0f)) return RV_EINVAL;
   if (cfg->chain_len < 0 || cfg->chain_len > RV_MAX_CHAIN) return RV_EINVAL;
   if (cfg->cull < 0 || cfg->cull > 2 || cfg->planner < 0 || cfg->planner > 2) return RV_EINVAL;
+  if (cfg->ct_sched < 0 || cfg->ct_sched > 1) return RV_EINVAL;
   rv_ctx* ctx = new rv_ctx();
   ctx->cfg = *cfg;
   if (cfg->chain_len == 0) ctx->chain.assign(kDefaultChain, kDefaultChain + 6);

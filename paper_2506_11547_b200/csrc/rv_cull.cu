@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(kCtThreads)
                            const int32_t* __restrict__ counts_dev, const uint8_t* __restrict__ tab,
                            int64_t pad_row, const uint8_t* __restrict__ tphi,
                            const int32_t* __restrict__ cidx, const uint32_t* __restrict__ lidx,
-                           unsigned long long* pairs, int32_t* work) {
+                           unsigned long long* pairs, int32_t* work, int32_t static_order) {
   using namespace tcx;
   extern __shared__ __align__(1024) uint8_t ct_raw[];
   CtSmem& sm = *reinterpret_cast<CtSmem*>((reinterpret_cast<uintptr_t>(ct_raw) + 1023) & ~(uintptr_t)1023);
@@ -979,7 +979,7 @@ __global__ void __launch_bounds__(kCtThreads)
   uint32_t kq = 0;
   int sidx = (int)blockIdx.x - (int)gridDim.x;
   // dynamic only for big levels (many items per CTA): small levels keep the static order
-  const bool dyn = RV_CT_DYN && n_items >= 8 * (int)gridDim.x;
+  const bool dyn = RV_CT_DYN && !static_order && n_items >= 8 * (int)gridDim.x;
   auto next_item = [&](bool warp_wide) -> int {
 #if RV_CT_DYN
     if (!dyn) {
@@ -1329,7 +1329,7 @@ void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
                          const int32_t* counts_dev, const uint8_t* tab, int64_t pad_row,
                          const uint8_t* tphi, const int32_t* cidx, const uint32_t* lidx,
                          unsigned long long* pairs, int num_sms, cudaStream_t s,
-                         int32_t* work) {
+                         int32_t* work, bool static_order) {
   static std::atomic<uint64_t> attr_done{0};
   const size_t b0 = sizeof(CtSmem) + 1024, b1 = b0;
   if (first_launch_on_device(attr_done)) {
@@ -1341,10 +1341,11 @@ void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
   }
   if (mode == RV_MODE_FINAL)
     rv_vote_cull_tc_kernel<true><<<num_sms, kCtThreads, b1, s>>>(segs, items, counts_dev, tab, pad_row,
-                                                                tphi, cidx, lidx, pairs, work);
+                                                                tphi, cidx, lidx, pairs, work, static_order ? 1 : 0);
   else
     rv_vote_cull_tc_kernel<false><<<num_sms, kCtThreads, b0, s>>>(segs, items, counts_dev, tab, pad_row,
-                                                                 tphi, cidx, lidx, pairs, work);
+                                                                 tphi, cidx, lidx, pairs, work,
+                                                                 static_order ? 1 : 0);
 }
 
 void launch_vote_cull(int mode, const VoteSeg* segs, const CullItem* items,

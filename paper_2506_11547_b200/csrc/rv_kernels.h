@@ -173,7 +173,8 @@ void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
                          const int32_t* counts_dev, const uint8_t* tab, int64_t pad_row,
                          const uint8_t* tphi, const int32_t* cidx, const uint32_t* lidx,
                          unsigned long long* pairs, int num_sms, cudaStream_t s,
-                         int32_t* work);  // the planner's zeroed work counter
+                         int32_t* work,  // the planner's zeroed work counter
+                         bool static_order = false);  // rv_config.ct_sched == 1
 // Level-0 index lists: row offsets lofs[P*m0 + 1] (exclusive prefix of the level-0 counts, each
 // padded to a multiple of 4; lofs[P*m0] = the total), then the compaction of the K3-TC bitmasks
 // (bits0: problem p's rows from m0 * toffs[p] / 32, (toffs[p+1] - toffs[p]) / 32 words each).

@@ -167,7 +167,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
       rv::launch_vote_cull_tc(mode, ctx->vsegs.p, ctx->c_items.p, ctx->c_icnt.p, ctx->tctab_rm.p,
                               ctx->tc_toff.back(), ctx->c_tphi.p, ctx->c_cidx.p, ctx->c_lidx.p,
                               ctx->c_pairs.p, ctx->num_sms, s,
-                              ctx->c_work.p);
+                              ctx->c_work.p, ctx->cfg.ct_sched == 1);
     else
       rv::launch_vote_cull(mode, ctx->vsegs.p, ctx->c_items.p, ctx->c_icnt.p, ctx->c_work.p,
                            ctx->c_pairs.p, ctx->c_phi.p, ctx->c_cidx.p, ctx->c_lidx.p,

@@ -41,7 +41,7 @@ class rv_config(C.Structure):
                 ("chain_len", C.c_int32), ("chain", C.c_int32 * RV_MAX_CHAIN),
                 ("refine_rounds", C.c_int32), ("guard", C.c_float), ("stream", C.c_void_p),
                 ("emulate_world", C.c_int32), ("tensor_vote", C.c_int32), ("cull", C.c_int32),
-                ("planner", C.c_int32)]
+                ("planner", C.c_int32), ("ct_sched", C.c_int32)]
 
 
 class rv_result(C.Structure):
@@ -237,7 +237,7 @@ class RotVote:
                  chain=None, refine_rounds: int = 2, guard: float = 1e-5, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
                  emulate_world: int = 0, tensor_vote: bool = True, cull=True,
-                 planner: str = "device"):
+                 planner: str = "device", ct_sched: str = "auto"):
         """cull: True / "tc" (K3-CT, default), "fp32" (K3-C), False (off).
         planner: "device" (the level loop on the GPU, one host round trip per single solve;
         default), "device_sync" (the device loop with a round trip per level, the one-pass
@@ -246,7 +246,7 @@ class RotVote:
         self._kw = dict(device=device, max_n=max_n, max_problems=max_problems, chain=chain,
                         refine_rounds=refine_rounds, guard=guard, stream=stream, rank=rank,
                         world=world, nccl_id=nccl_id, emulate_world=emulate_world,
-                        tensor_vote=tensor_vote, cull=cull, planner=planner)
+                        tensor_vote=tensor_vote, cull=cull, planner=planner, ct_sched=ct_sched)
         cfg = rot_vote_default_config()
         cfg.device = device
         cfg.rank, cfg.world = rank, world
@@ -270,6 +270,7 @@ class RotVote:
         cfg.tensor_vote = int(bool(tensor_vote))
         cfg.cull = {True: 1, "tc": 1, "fp32": 2, False: 0, None: 0}[cull]
         cfg.planner = {"device": 0, "host": 1, "device_sync": 2}[planner]
+        cfg.ct_sched = {"auto": 0, "static": 1}[ct_sched]
         self.cfg = cfg
         self.device = device
         self.chain = tuple(chain) if chain is not None else DEFAULT_CHAIN

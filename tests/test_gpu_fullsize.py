@@ -110,3 +110,20 @@ def test_culled_vote_full_size(setup):
     ex, _ = oracle.count_cells(pr.x, pr.y, 360, near, tau, 0.0)
     assert np.all(gb <= ex) and np.all(ex <= ga)
     assert ga.max() >= res.votes >= gb.max()
+
+
+def test_k3ct_dynamic_items_equal_static_order(setup):
+    """K3-CT hands out the items of a big level dynamically (a scheduler warp per CTA and a
+    work counter); the counts are integer sums, so every block must get exactly the count of
+    the static item order.  The cfg4 B = 45 level (all 52,461 blocks, ~7,600 items >= 8 per CTA)
+    takes the dynamic path -- a dropped or duplicated item would change some counts."""
+    pr, rv, x, y, res = setup
+    lins = oracle.candidates(45).astype(np.uint32)
+    st = rv.twin(ct_sched="static")
+    try:
+        a_dyn = rv.count_cells_culled(x, y, 15, 45, lins, pr.eps, 0)
+        a_st = st.count_cells_culled(x, y, 15, 45, lins, pr.eps, 0)
+        assert np.array_equal(a_dyn, a_st)
+        assert int(a_dyn.astype(np.int64).sum()) > 0
+    finally:
+        st.close()

@@ -37,7 +37,7 @@ def dev(torch, a):
     return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
 
 
-@pytest.mark.parametrize("n,rho,mu", [(2, 0.0, 1.0), (97, 0.5, 0.02), (300, 0.9, 0.05),
+@pytest.mark.parametrize("n,rho,mu", [(3, 0.0, 1.0), (97, 0.5, 0.02), (300, 0.9, 0.05),
                                       (1200, 0.95, 0.03)])
 def test_rigid_pairs_rotation_translation(rv, torch_cuda, n, rho, mu):
     torch = torch_cuda
