@@ -191,7 +191,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->c_work.release(); ctx->c_items.release(); ctx->c_pairs.release();
   for (cudaEvent_t e : ctx->cevs) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->evs) cudaEventDestroy(e);
-  ctx->up.release(); ctx->down.release();
+  ctx->up.release(); ctx->down.release(); ctx->up2.release(); ctx->down2.release();
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evv0) cudaEventDestroy(ctx->evv0);

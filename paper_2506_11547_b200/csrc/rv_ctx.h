@@ -344,6 +344,7 @@ struct rv_ctx {
     vote_pending = false;
   }
   Staging up, down;
+  Staging up2, down2;           // a second pair for work enqueued while the first is in flight
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evv0 = nullptr, evv1 = nullptr;
   cudaEvent_t ph[8] = {};       // phase boundaries of a one-pass solve (rv_result.t_*_ms)
   // one-pass solves as a CUDA graph: the enqueue sequence of a single solve depends only on
@@ -451,11 +452,20 @@ int eval_request(rv_ctx* ctx, const float* x, const float* y, int64_t n, double 
                  int32_t mode, int64_t m, const uint32_t* lins, uint32_t* cnt_a, uint32_t* cnt_b,
                  bool auto_tc = true);
 // rv_setup.cpp
-// dev_offsets (P == 1 only): the offset tables are written by a kernel from its arguments instead
+// cull_rows = false: the culled levels' row tables (K3-CT / K3-C) are not written (a solve that
+// cannot cull).  dev_offsets (P == 1 only): the offset tables are written by a kernel from its arguments instead
 // of copied from pinned staging (a captured graph must not point at reusable host memory)
 int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
-              std::vector<int64_t>& koff_out, bool dev_offsets = false);
+              std::vector<int64_t>& koff_out, bool dev_offsets = false, bool cull_rows = true);
 int check_bad(rv_ctx* ctx);
+struct RefineOut {            // enqueue_refine's read-back (pinned, valid after the next wait)
+  double* q = nullptr;
+  int32_t* flags = nullptr;
+  uint32_t* ninl = nullptr;
+};
+int enqueue_refine(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
+                   double eps, int32_t rounds, const int64_t* mask_words, uint32_t* masks,
+                   RefineOut& out);
 int run_refine(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
                const int32_t* prob_ids, double eps, const double* qs0, int32_t rounds,
                const int64_t* mask_words, uint32_t* masks, double* q_out, int32_t* flags_out,

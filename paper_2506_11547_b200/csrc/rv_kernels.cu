@@ -890,6 +890,35 @@ __global__ void __launch_bounds__(kR1Threads) rv_refine1_kernel(Refine1Args a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.flags &= (RV_REFINED | RV_DEGENERATE);
 }
 
+// the refinement's start of P problems: q0[p] = the hemisphere-canonical centre rotation of the
+// winner packed in best[p] (count << 32 | ~lin) at resolution B (the host's canonical_cell_quat)
+__global__ void rv_decode_q0_kernel(const unsigned long long* __restrict__ best, int32_t P,
+                                    int32_t B, double* qs) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+    double q[4] = {0.0, 0.0, 0.0, -1.0};
+    const unsigned long long key = best[p];
+    if (key) {
+      const uint32_t lin = 0xffffffffu - (uint32_t)(key & 0xffffffffull);
+      int32_t i, j, k;
+      lin_to_ijk(lin, B, i, j, k);
+      cell_quat(B, i, j, k, q);
+    }
+    bool flip;
+    if (q[3] < -1e-15) flip = false;
+    else if (q[3] > 1e-15) flip = true;
+    else {
+      flip = false;
+      for (int c = 0; c < 3; ++c)
+        if (q[c] != 0.0) { flip = q[c] < 0.0; break; }
+    }
+    for (int c = 0; c < 4; ++c) qs[4 * p + c] = flip ? -q[c] : q[c];
+  }
+}
+void launch_decode_q0(const unsigned long long* best, int32_t P, int32_t B, double* qs,
+                      cudaStream_t s) {
+  rv_decode_q0_kernel<<<(P + 255) / 256, 256, 0, s>>>(best, P, B, qs);
+}
+
 // two int64 constants into device memory as a kernel (a one-pass solve's offsets: a captured
 // graph then carries them in its kernel arguments instead of pointing at host staging)
 __global__ void rv_set_i64x2_kernel(int64_t* d, int64_t v0, int64_t v1) {

@@ -253,6 +253,9 @@ struct Refine1Args {
   uint32_t* bar;         // DEVICE grid-barrier counter, zeroed by launch_refine1
 };
 cudaError_t launch_refine1(const Refine1Args& a, int num_sms, cudaStream_t s);
+// qs[4p..] = canonical centre rotation of the winner packed in best[p] at resolution B
+void launch_decode_q0(const unsigned long long* best, int32_t P, int32_t B, double* qs,
+                      cudaStream_t s);
 // d[0] = v0, d[1] = v1 (one thread)
 void launch_set_i64x2(int64_t* d, int64_t v0, int64_t v1, cudaStream_t s);
 

@@ -2,6 +2,8 @@
 // ancestor culling (rv_cull.cu), the sharded one-problem levels, and the batched entry.
 #include "rv_ctx.h"
 
+#include <functional>
+
 namespace rvi {
 
 // Culling state for a level 0 at B0 (grid_host holds its m0 candidates): the lin -> row table,
@@ -327,10 +329,13 @@ int vote_level_owned(rv_ctx* ctx, const float* x, const float* y, const std::vec
 // (rv_dplan.cu).  Host round trips: one per branch-and-bound level (the size of the next
 // child region) and one at the end; with K3-TC the items are built on the device.
 // ch = the `levels` resolutions searched (ch.size() >= 2).  Fills res[p].
+// before_sync (optional) enqueues more work (the refinement) between the finalize kernels and
+// the one final wait; the data check of run_setup (ctx->bad) is read back with the finalize.
 int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
                         const std::vector<int64_t>& rows, const std::vector<int64_t>& koff,
                         int32_t PL, double eps, const std::vector<int32_t>& ch,
-                        std::vector<rv_plan_result>& res, Trace& tr) {
+                        std::vector<rv_plan_result>& res, Trace& tr,
+                        const std::function<int()>& before_sync) {
   const int L = (int)ch.size();
   cudaStream_t s = ctx->stream;
   int64_t nmax = 0;
@@ -660,27 +665,35 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
                            ctx->dp_best.p, ctx->dp_ties.p, s);
   ctx->launches += 2;
   RV_CUDA(cudaGetLastError(), "launching the level loop");
-  RV_CUDA(ctx->down.ensure((size_t)PL * 24 + (size_t)nph * PL * 4 + 2048), "allocating staging");
-  ctx->down.reset();
-  unsigned long long* hbest = ctx->down.take<unsigned long long>(PL);
-  int32_t* hties = ctx->down.take<int32_t>(PL);
-  int64_t* hlb = ctx->down.take<int64_t>(PL);
-  int32_t* hph = ctx->down.take<int32_t>((size_t)nph * PL);
-  int32_t* herr = ctx->down.take<int32_t>(1);
-  unsigned long long* hcp = ctx->down.take<unsigned long long>(1);
+  // (its own staging: the refinement enqueued by before_sync stages through ctx->down)
+  RV_CUDA(ctx->down2.ensure((size_t)PL * 24 + (size_t)nph * PL * 4 + 2048), "allocating staging");
+  ctx->down2.reset();
+  unsigned long long* hbest = ctx->down2.take<unsigned long long>(PL);
+  int32_t* hties = ctx->down2.take<int32_t>(PL);
+  int64_t* hlb = ctx->down2.take<int64_t>(PL);
+  int32_t* hph = ctx->down2.take<int32_t>((size_t)nph * PL);
+  int32_t* herr = ctx->down2.take<int32_t>(1);
+  unsigned long long* hcp = ctx->down2.take<unsigned long long>(1);
+  unsigned long long* hbad = ctx->down2.take<unsigned long long>(1);
   RV_CUDA(cudaMemcpyAsync(herr, ctx->dp_err.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(hbad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
   if (culled) RV_CUDA(cudaMemcpyAsync(hcp, ctx->c_pairs.p, 8, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hbest, ctx->dp_best.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hties, ctx->dp_ties.p, 4 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hlb, ctx->dp_lb.p, 8 * (size_t)PL, cudaMemcpyDeviceToHost, s), "D2H");
   RV_CUDA(cudaMemcpyAsync(hph, ctx->dp_phase.p, 4 * (size_t)nph * PL, cudaMemcpyDeviceToHost, s),
           "D2H");
+  if (before_sync)
+    if (int rc = before_sync()) return rc;
   RV_SYNC(cudaStreamSynchronize(s), "batched finalize");
   ctx->collect_vote_ms();
   ctx->ev_collect();
   ctx->cev_collect();
   ctx->cull_ready = false;
   if (culled) ctx->cull_pairs += *hcp;
+  if (*hbad != ~0ull)
+    return ctx->fail(RV_EDATA, "correspondence row %llu has a zero-length or non-finite vector",
+                     *hbad);
   if (*herr != 0)
     return ctx->fail(RV_ECUDA, "internal: device level-loop invariant violated (code %d)", *herr);
   tr.mark("  finalize");
@@ -1259,15 +1272,48 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
   Trace tr;
   if (PL > 0) {
     std::vector<int64_t> rows(offsets + pb, offsets + pe + 1), koff;
-    if (int rc = run_setup(ctx, x, y, rows.data(), PL, koff)) return rc;
-    if (int rc = check_bad(ctx)) return rc;
-    tr.mark("setup");
-    int rc = RV_OK;
     const int32_t lev = levels == 0 ? std::min<int32_t>(5, (int32_t)ctx->chain.size()) : levels;
     const std::vector<int32_t> ch(ctx->chain.end() - lev, ctx->chain.end());
+    const bool dev_loop = dplan_applies(ctx, lev, ch[0], eps);
+    // the culling rows only when solve_batched_dplan can cull this batch (P x m0 buckets)
+    bool cull_rows = dev_loop;
+    if (dev_loop && PL > 1) {
+      if (ctx->grid_host_B != ch[0]) {
+        const int64_t m = rv_grid_candidates(ch[0], nullptr, 0);
+        ctx->grid_host.resize(m);
+        rv_grid_candidates(ch[0], ctx->grid_host.data(), m);
+        ctx->grid_host_B = ch[0];
+      }
+      cull_rows = (int64_t)PL * (int64_t)ctx->grid_host.size() <= ((int64_t)1 << 22);
+    }
+    if (int rc = run_setup(ctx, x, y, rows.data(), PL, koff, false, cull_rows)) return rc;
+    // the device loop reads the data check back with its finalize (no round trip here)
+    if (!dev_loop)
+      if (int rc = check_bad(ctx)) return rc;
+    tr.mark("setup");
+    int rc = RV_OK;
     std::vector<rv_plan_result> pres(PL);
-    if (dplan_applies(ctx, lev, ch[0], eps)) {
-      rc = solve_batched_dplan(ctx, x, y, rows, koff, PL, eps, ch, pres, tr);
+    std::vector<int64_t> mw_dev(PL);
+    RefineOut ro;
+    if (dev_loop) {
+      // the refinement starts from the winners decoded on the device and is enqueued before
+      // the finalize's wait: one host round trip for the finalize and the refinement
+      {
+        int64_t w = 0;
+        for (int64_t p = 0; p < pb; ++p) w += (offsets[p + 1] - offsets[p] + 31) / 32;
+        for (int32_t p = 0; p < PL; ++p) {
+          mw_dev[p] = w;
+          w += (rows[p + 1] - rows[p] + 31) / 32;
+        }
+      }
+      auto refine_hook = [&]() -> int {
+        RV_CUDA(ctx->qs.ensure((size_t)PL * 4), "allocating");
+        rv::launch_decode_q0(ctx->dp_best.p, PL, ch.back(), ctx->qs.p, ctx->stream);
+        ctx->launches += 1;
+        return enqueue_refine(ctx, x, y, rows.data(), PL, eps, ctx->cfg.refine_rounds,
+                              mw_dev.data(), masks, ro);
+      };
+      rc = solve_batched_dplan(ctx, x, y, rows, koff, PL, eps, ch, pres, tr, refine_hook);
       if (rc) return rc;
     } else {
       std::vector<rv_plan*> plans(PL, nullptr);
@@ -1413,10 +1459,19 @@ int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_
       }
     }
     tr.mark("results");
-    // rows are absolute: refine over the local offsets table
-    rc = run_refine(ctx, x, y, rows.data(), PL, ids.data(), eps, q0.data(), ctx->cfg.refine_rounds,
-                    mw.data(), masks, qf.data(), fl.data(), ni.data());
-    if (rc) return rc;
+    if (dev_loop) {  // read back with the finalize; no successful round keeps the host's q0
+      for (int32_t p = 0; p < PL; ++p) {
+        fl[p] = ro.flags[p] & (RV_REFINED | RV_DEGENERATE);
+        ni[p] = ro.ninl[p];
+        if (fl[p] & RV_REFINED) std::memcpy(&qf[4 * p], ro.q + 4 * p, 32);
+        else std::memcpy(&qf[4 * p], &q0[4 * p], 32);
+      }
+    } else {
+      // rows are absolute: refine over the local offsets table
+      rc = run_refine(ctx, x, y, rows.data(), PL, ids.data(), eps, q0.data(),
+                      ctx->cfg.refine_rounds, mw.data(), masks, qf.data(), fl.data(), ni.data());
+      if (rc) return rc;
+    }
     tr.mark("refine");
     for (int32_t p = 0; p < PL; ++p) {
       std::memcpy(local[p].q, &qf[4 * p], 32);

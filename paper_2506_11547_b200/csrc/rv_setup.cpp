@@ -6,7 +6,7 @@ namespace rvi {
 
 // ---- K1 for P problems ----------------------------------------------------------------------
 int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
-              std::vector<int64_t>& koff_out, bool dev_offsets) {
+              std::vector<int64_t>& koff_out, bool dev_offsets, bool cull_rows) {
   koff_out.assign(P + 1, 0);
   for (int32_t p = 0; p < P; ++p) koff_out[p + 1] = koff_out[p] + pad4(offsets[p + 1] - offsets[p]);
   const int64_t total = koff_out[P];
@@ -57,8 +57,8 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
     }
     // the culled levels' rows: K3-CT's fp16-split row-major copy, or K3-C's fp32 rows (the
     // culled path cull_prepare will pick: K3-CT unless RV_CULL_TC=0 or a multi-rank batch)
-    const bool ct = ctx->cull_on && ctx->cull_tc;
-    const bool k3c = ctx->cull_on && !ct;
+    const bool ct = cull_rows && ctx->cull_on && ctx->cull_tc;
+    const bool k3c = cull_rows && ctx->cull_on && !ct;
     if (k3c) RV_CUDA(ctx->k12.ensure((size_t)(toff[P] + 8) * 12), "allocating K3-C rows");
     if (ct) RV_CUDA(ctx->tctab_rm.ensure((size_t)(toff[P] + 8) * 64), "allocating K3-CT rows");
     rv::launch_setup_tc(x, y, ctx->rows.p, ctx->toffs.p, P, toff[P] + 8, ctx->tctab.p, ctx->stream,
@@ -145,6 +145,65 @@ int run_refine(rv_ctx* ctx, const float* x, const float* y, const int64_t* offse
   std::memcpy(q_out, dq, (size_t)P * 32);
   for (int32_t p = 0; p < P; ++p) flags_out[p] = df[p] & (RV_REFINED | RV_DEGENERATE);
   std::memcpy(ninl_out, dn, P * 4);
+  return RV_OK;
+}
+
+// The refinement of P problems enqueued without a wait: q0 already in ctx->qs (device), the
+// segment / item tables through ctx->up2 and the outputs into ctx->down (pinned; valid after the
+// caller's next wait).  Same launches and arithmetic as run_refine.
+int enqueue_refine(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets, int32_t P,
+                   double eps, int32_t rounds, const int64_t* mask_words, uint32_t* masks,
+                   RefineOut& out) {
+  std::vector<rv::RefSeg> segs(P);
+  std::vector<rv::RefItem> items;
+  const double tau = std::cos(eps);
+  for (int32_t p = 0; p < P; ++p) {
+    const int64_t n = offsets[p + 1] - offsets[p];
+    segs[p].row = offsets[p];
+    segs[p].mask_word = mask_words ? mask_words[p] : 0;
+    segs[p].n = (int32_t)n;
+    segs[p].tau = tau;
+    segs[p].pad = 0;
+    segs[p].item_begin = (int32_t)items.size();
+    for (int64_t r0 = 0; r0 < n; r0 += rv::kRefRowsPerItem)
+      items.push_back({p, (int32_t)r0, (int32_t)std::min<int64_t>(rv::kRefRowsPerItem, n - r0)});
+    segs[p].item_end = (int32_t)items.size();
+  }
+  RV_CUDA(ctx->rsegs.ensure(P), "allocating");
+  RV_CUDA(ctx->ritems.ensure(items.size()), "allocating");
+  RV_CUDA(ctx->partials.ensure(items.size() * 10), "allocating");
+  RV_CUDA(ctx->flags.ensure(P), "allocating");
+  RV_CUDA(ctx->ninl.ensure(P), "allocating");
+  RV_CUDA(ctx->up2.ensure(P * sizeof(rv::RefSeg) + items.size() * sizeof(rv::RefItem) + 4096),
+          "allocating staging");
+  RV_CUDA(ctx->down.ensure(P * (32 + 8) + 4096), "allocating staging");
+  ctx->up2.reset();
+  rv::RefSeg* hs = ctx->up2.take<rv::RefSeg>(P);
+  std::memcpy(hs, segs.data(), P * sizeof(rv::RefSeg));
+  rv::RefItem* hi = ctx->up2.take<rv::RefItem>(items.size());
+  std::memcpy(hi, items.data(), items.size() * sizeof(rv::RefItem));
+  cudaStream_t s = ctx->stream;
+  RV_CUDA(cudaMemcpyAsync(ctx->rsegs.p, hs, P * sizeof(rv::RefSeg), cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemcpyAsync(ctx->ritems.p, hi, items.size() * sizeof(rv::RefItem),
+                          cudaMemcpyHostToDevice, s), "H2D");
+  RV_CUDA(cudaMemsetAsync(ctx->flags.p, 0, P * sizeof(int32_t), s), "memset");
+  for (int r = 0; r < rounds; ++r) {
+    rv::launch_inliers(x, y, ctx->rsegs.p, ctx->ritems.p, (int32_t)items.size(), ctx->qs.p, nullptr,
+                       ctx->partials.p, s);
+    rv::launch_eig(ctx->rsegs.p, P, ctx->partials.p, ctx->qs.p, ctx->flags.p, ctx->ninl.p, 0, s);
+  }
+  rv::launch_inliers(x, y, ctx->rsegs.p, ctx->ritems.p, (int32_t)items.size(), ctx->qs.p, masks,
+                     ctx->partials.p, s);
+  rv::launch_eig(ctx->rsegs.p, P, ctx->partials.p, ctx->qs.p, ctx->flags.p, ctx->ninl.p, 1, s);
+  ctx->launches += 2 * rounds + 2;
+  RV_CUDA(cudaGetLastError(), "launching refinement");
+  ctx->down.reset();
+  out.q = ctx->down.take<double>((size_t)P * 4);
+  out.flags = ctx->down.take<int32_t>(P);
+  out.ninl = ctx->down.take<uint32_t>(P);
+  RV_CUDA(cudaMemcpyAsync(out.q, ctx->qs.p, (size_t)P * 32, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(out.flags, ctx->flags.p, P * 4, cudaMemcpyDeviceToHost, s), "D2H");
+  RV_CUDA(cudaMemcpyAsync(out.ninl, ctx->ninl.p, P * 4, cudaMemcpyDeviceToHost, s), "D2H");
   return RV_OK;
 }
 
