@@ -229,7 +229,8 @@ struct rv_ctx {
   DevBuf<int64_t> dp_off[3], dp_lb, dp_lb2, dp_actr[2], dp_bring[3];
   DevBuf<int32_t> dp_cnt[3], dp_rcnt, dp_ties, dp_rflag, dp_rany, dp_rdone;
   DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex, dp_lmax;
-  DevBuf<unsigned long long> dp_best;
+  DevBuf<unsigned long long> dp_best, dp_best_r;  // (_r: per-rank winners, sharded one pass)
+  DevBuf<int32_t> dp_ties_r;
   DevBuf<float> rg_m, rg_n;         // NEXT-3: kept pairs
   DevBuf<int32_t> rg_cnt;
   DevBuf<int64_t> rg_off, rg_bins;

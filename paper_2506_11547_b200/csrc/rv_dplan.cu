@@ -196,7 +196,7 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
                               const uint32_t* __restrict__ pub, const int64_t* __restrict__ lb,
                               int32_t P, int32_t Bp, int32_t f, const int64_t* __restrict__ ccap,
                               uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
-                              int32_t* err) {
+                              int32_t* err, Own own) {
   const int64_t total = act_off[P];
   const int32_t Bc = Bp * f;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -207,6 +207,11 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
     if ((int64_t)pub[idx] < lb[p]) continue;
     int32_t i, j, k;
     lin_to_ijk(shared_lins ? plins[e] : plins[idx], Bp, i, j, k);
+    if (own.lut) {  // another rank's subtree: the owner of its level-0 ancestor's group expands it
+      const int32_t r = Bp / own.B0;
+      const int32_t grp = own.lut[ijk_to_lin(i / r, j / r, k / r, own.B0)];
+      if (grp < own.lo || grp >= own.hi) continue;
+    }
     int c = 0;
     for (int a = 0; a < f; ++a)
       for (int b = 0; b < f; ++b)
@@ -767,9 +772,34 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           const int64_t* pcap, const uint32_t* pub, const int64_t* lb, int32_t P,
                           int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
                           uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
-                          int32_t* err, cudaStream_t s) {
+                          int32_t* err, cudaStream_t s, const Own& own) {
   dp_bnb_expand<<<flat_grid(total), 256, 0, s>>>(plins, shared_lins ? 1 : 0, act_off, pcap, pub,
-                                                 lb, P, Bp, f, ccap, clins, ca, cb, ccnt, err);
+                                                 lb, P, Bp, f, ccap, clins, ca, cb, ccnt, err, own);
+}
+
+// ---- one problem over ranks, each searching the subtrees it owns (the one-pass sharded solve)
+// slot r of (best, ties) = rank r's finest-level winner key and its tie count; the merge takes the
+// largest key and sums the ties of the ranks whose winning count equals it
+__global__ void dp_merge_rank_winners(const unsigned long long* __restrict__ best_r,
+                                      const int32_t* __restrict__ ties_r, int32_t W,
+                                      unsigned long long* best, int32_t* ties) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long b = 0;
+  for (int r = 0; r < W; ++r) b = best_r[r] > b ? best_r[r] : b;
+  int32_t t = 0;
+  for (int r = 0; r < W; ++r)
+    if (best_r[r] && (best_r[r] >> 32) == (b >> 32)) t += ties_r[r];
+  *best = b;
+  *ties = t;
+}
+void dp_launch_merge_rank_winners(const unsigned long long* best_r, const int32_t* ties_r,
+                                  int32_t W, unsigned long long* best, int32_t* ties,
+                                  cudaStream_t s) {
+  dp_merge_rank_winners<<<1, 32, 0, s>>>(best_r, ties_r, W, best, ties);
+}
+__global__ void dp_add_i32(int32_t* dst, const int32_t* __restrict__ src) { *dst += *src; }
+void dp_launch_add_i32(int32_t* dst, const int32_t* src, cudaStream_t s) {
+  dp_add_i32<<<1, 1, 0, s>>>(dst, src);
 }
 void dp_launch_expand_ordered(const uint32_t* plins, bool shared_lins, const int64_t* act_off,
                               const int64_t* pcap, const uint32_t* pub, const int64_t* lb,

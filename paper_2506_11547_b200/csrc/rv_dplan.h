@@ -81,6 +81,20 @@ void dp_launch_dive_pick(const uint32_t* lins, const uint32_t* a, const int64_t*
 // lb[p] = max cnt_b of the list
 void dp_launch_max_lo(const uint32_t* b, const int64_t* off, const int32_t* cnt, int64_t* lb,
                       int32_t P, cudaStream_t s);
+// Subtree ownership of a one-problem search over ranks: a block belongs to the rank owning the
+// ancestor group of its level-0 (resolution B0) ancestor, lut[B0 lin] = group, owned groups
+// [lo, hi).  lut == nullptr: everything.
+struct Own {
+  const int32_t* lut = nullptr;
+  int32_t B0 = 0;
+  int64_t lo = 0, hi = 0;
+};
+// best = max_r best_r, ties = sum of ties_r over the ranks whose count equals best's (one thread)
+void dp_launch_merge_rank_winners(const unsigned long long* best_r, const int32_t* ties_r,
+                                  int32_t W, unsigned long long* best, int32_t* ties,
+                                  cudaStream_t s);
+// *dst += *src (one thread: per-rank phase counts summed in order)
+void dp_launch_add_i32(int32_t* dst, const int32_t* src, cudaStream_t s);
 // Flat list kernels (one thread per entry; entries of problem p: act_off[p]..act_off[p+1]
 // stored from cap[p]).  BnB expand: candidate children of parents with UB >= lb[p] into the
 // child region ccap[p] (ccnt zeroed by the caller; the children's count slots are zeroed).
@@ -88,7 +102,7 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           const int64_t* pcap, const uint32_t* pub, const int64_t* lb, int32_t P,
                           int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
                           uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
-                          int32_t* err, cudaStream_t s);
+                          int32_t* err, cudaStream_t s, const Own& own = Own());
 // Ordered BnB expansion (one problem sharded over ranks: every rank builds the identical
 // list): per-parent child counts into pcnt[total parents], their prefix into off[total + 1],
 // then the children in parent order.

@@ -769,8 +769,10 @@ constexpr int64_t kOnePassCap = (int64_t)1 << 22;
 constexpr int64_t kOnePassRecheck = 4096;
 
 bool one_pass_applies(rv_ctx* ctx, int32_t P) {
-  return P == 1 && ctx->cfg.planner == 0 && ctx->tc_on && !ctx->comm &&
-         ctx->effective_world() == 1;
+  if (P != 1 || ctx->cfg.planner != 0 || !ctx->tc_on) return false;
+  const bool sharded = ctx->effective_world() > 1 || ctx->comm != nullptr;
+  // over ranks: the subtree ownership needs the grouped (K3-CT) culling
+  return !sharded || (ctx->cull_on && ctx->cull_tc);
 }
 
 // The read-back slots of a one-pass solve in ctx->grb (pinned)
@@ -800,6 +802,14 @@ struct OnePassRB {
 int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
                      const std::vector<int32_t>& ch, uint32_t* mask, rv_ctx::OnePassHost& hv) {
   const int L = (int)ch.size();
+  // one problem over W ranks (one_pass_applies: grouped culling): level 0 in slabs and the dive's
+  // blocks by owner, each with one all-reduce of fixed size; the branch and bound split into the
+  // subtrees of the owned level-0 groups, searched by each rank on its own (no collective); the
+  // ranks' winners merged at the end.  Loopback (emulate_world): every rank in turn.
+  const int W = ctx->effective_world();
+  const bool sharded = W > 1;
+  const bool nccl_path = ctx->comm != nullptr;
+  const int r_lo = nccl_path ? ctx->cfg.rank : 0, r_hi = nccl_path ? r_lo + 1 : W;
   // the flat kernels loop over the device's own totals; their grids only need to fill the GPU
   auto flat_hint = [&](int64_t m) { return std::min<int64_t>(m, (int64_t)ctx->num_sms * 2 * 256); };
   cudaStream_t s = ctx->stream;
@@ -868,8 +878,12 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   if (cull) {
     RV_CUDA(ctx->cbits.ensure((size_t)m0 * (size_t)(tpad / 32)), "allocating level-0 bitmasks");
     if (int rc = cull_prepare(ctx, B0, m0, PL)) return rc;
-    if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, m0, nmax, true))
+    if (sharded) {  // this rank's slab (i-slab aligned: whole groups), counts all-reduced
+      if (int rc = vote_level0_slabs(ctx, x, y, rows, koff, eps, B0, l0, m0, nmax)) return rc;
+    } else if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, m0, nmax,
+                                   true)) {
       return rc;
+    }
     // the lists: row offsets, then the compaction into a fixed capacity (an eighth of the
     // level-0 pairs; cfg4's lists fill 3%: longer lists raise the error word and the per-level
     // loop, which reads their length back, redoes the solve)
@@ -881,8 +895,12 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     RV_CUDA(ctx->c_lidx.ensure(lcap + 4), "allocating level-0 lists");
     RV_CUDA(ctx->c_fill.ensure(NB), "allocating");
     rv::launch_cull_rows(ctx->l0cnt.p, PL, m0, ctx->c_lofs.p, s, gr);
+    // (a rank compacts the lists of its own groups; loopback: all)
+    const int64_t row_lo = nccl_path && sharded ? ctx->cull_g[ctx->cfg.rank] : 0;
+    const int64_t row_hi = nccl_path && sharded ? ctx->cull_g[ctx->cfg.rank + 1] : NB;
     rv::launch_cull_compact(ctx->cbits.p, ctx->toffs.p, PL, m0, ctx->cull_wpc_max, ctx->c_lofs.p,
-                            ctx->c_fill.p, ctx->c_lidx.p, s, 0, NB, gr, lcap, ctx->dp_err.p);
+                            ctx->c_fill.p, ctx->c_lidx.p, s, row_lo, row_hi, gr, lcap,
+                            ctx->dp_err.p);
     ctx->launches += 2;
     // list lengths = the compaction's fill counters (also per ancestor, where they equal the
     // level-0 counts): a compaction that overflowed wrote nothing and leaves them 0, so no
@@ -920,7 +938,12 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     if (int rc = keep_phase(ctx->dp_cnt[0].p)) return rc;
     const rv::DpList dl{ctx->dp_lins[0].p, 0, 0, ctx->dp_off[0].p, ctx->dp_cnt[0].p,
                         ctx->dp_ca[0].p, ctx->dp_cb[0].p};
-    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], dl, PL, cap, nmax)) return rc;
+    if (sharded) {  // each block voted by its owner, counts all-reduced (fixed size cap)
+      if (int rc = vote_level_owned(ctx, x, y, rows, koff, eps, mode, ch[l], dl, cap, nmax))
+        return rc;
+    } else if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], dl, PL, cap, nmax)) {
+      return rc;
+    }
     if (mode == RV_MODE_BOUND)
       rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, ctx->dp_off[0].p,
                               ctx->dp_cnt[0].p, ch[l], eps, ctx->rows.p, ctx->dp_pick.p, PL, s);
@@ -942,94 +965,149 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   RV_CUDA(ctx->dp_tot.ensure(1), "allocating");
   RV_CUDA(ctx->dp_rdone.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_rflag.ensure(PL), "allocating");
-  RV_CUDA(cudaMemsetAsync(ctx->dp_rdone.p, 0, PL * 4, s), "memset");
-  if (int rc = upload_i64(ctx->dp_actr[1].p, {0, m0})) return rc;
-  {
-    const int64_t f = ch[1] / ch[0];
-    if (int rc = upload_i64(ctx->dp_bring[1].p, {0, std::min<int64_t>(m0 * f * f * f, capl[1])}))
-      return rc;
-  }
-  const uint32_t* plins = ctx->grid_list.p;
-  const uint32_t* pub = ctx->l0cnt.p;
-  bool shared = true;
-  int cur = -1;
-  for (int l = 1; l < L; ++l) {
-    const int nb = cur == 1 ? 0 : 1;
-    const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1];
-    const int64_t f3 = (int64_t)f * f * f;
-    int64_t* pact = ctx->dp_actr[l & 1].p;
-    int64_t* cact = ctx->dp_actr[(l + 1) & 1].p;
-    int64_t* cbase = ctx->dp_bring[l % 3].p;
-    int64_t* pbase = shared ? pact : ctx->dp_bring[(l + 2) % 3].p;
-    int64_t* nbase = ctx->dp_bring[(l + 1) % 3].p;
-    RV_CUDA(ctx->dp_lins[nb].ensure(capl[l]), "allocating");
-    RV_CUDA(ctx->dp_ca[nb].ensure(capl[l]), "allocating");
-    RV_CUDA(ctx->dp_cb[nb].ensure(capl[l]), "allocating");
-    RV_CUDA(ctx->dp_cnt[nb].ensure(PL), "allocating");
-    RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
-    rv::dp_launch_bnb_expand(plins, shared, pact, pbase, pub, ctx->dp_lb.p, PL,
-                             flat_hint(shared ? m0 : capl[l - 1]), Bp, f, cbase, ctx->dp_lins[nb].p,
-                             ctx->dp_ca[nb].p, ctx->dp_cb[nb].p, ctx->dp_cnt[nb].p, ctx->dp_err.p, s);
-    int64_t nf3 = 1;
-    if (l + 1 < L) {
-      const int64_t nf = ch[l + 1] / ch[l];
-      nf3 = nf * nf * nf;
-    }
-    // re-dive trigger (R18): not taken here -- it raises the error word (bit 8) and the solve
-    // is redone by the per-level loop, which takes it
-    rv::RediveCheck chk{cur >= 0 ? ctx->dp_cnt[cur].p : nullptr, f3, ctx->dp_rdone.p,
-                        ctx->dp_rflag.p, ctx->dp_err.p, 8};
-    const rv::OnePass op{ctx->dp_err.p, l + 1 < L ? capl[l + 1] : 0};
-    rv::dp_launch_scan(ctx->dp_cnt[nb].p, PL, nf3, cact, nbase, ctx->dp_tot.p, s,
-                       l >= 2 ? &chk : nullptr, &op);
-    ctx->launches += 2;
-    if (int rc = keep_phase(ctx->dp_cnt[nb].p)) return rc;
-    const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
-    const rv::DpList cl{ctx->dp_lins[nb].p, 0, 0, cbase, ctx->dp_cnt[nb].p, ctx->dp_ca[nb].p,
-                        ctx->dp_cb[nb].p};
-    if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], cl, PL, capl[l], nmax))
-      return rc;
-    plins = ctx->dp_lins[nb].p;
-    pub = ctx->dp_ca[nb].p;
-    shared = false;
-    cur = nb;
-  }
-  nvtxRangePop();
-  RV_CUDA(ctx->record(ph[4], s), "event");
-  // ---- finest level: max lo, exact-known blocks, the fp64 recheck, winner, ties
-  nvtxRangePushA("rv.final");
   const int64_t fcapn = capl[L - 1];
-  const uint32_t* flins = ctx->dp_lins[cur].p;
-  const uint32_t* fhi = ctx->dp_ca[cur].p;
-  const uint32_t* flo = ctx->dp_cb[cur].p;
-  const int64_t* fcap = ctx->dp_bring[(L - 1) % 3].p;
-  int64_t* fact = ctx->dp_actr[L & 1].p;
   RV_CUDA(ctx->dp_rcnt.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_lmax.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_best.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_ties.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_rlins.ensure(fcapn), "allocating");
   RV_CUDA(ctx->dp_ex.ensure(fcapn), "allocating");
-  RV_CUDA(cudaMemsetAsync(ctx->dp_rcnt.p, 0, PL * 4, s), "memset");
-  RV_CUDA(cudaMemsetAsync(ctx->dp_lmax.p, 0, PL * 4, s), "memset");
-  RV_CUDA(cudaMemsetAsync(ctx->dp_best.p, 0, PL * 8, s), "memset");
-  RV_CUDA(cudaMemsetAsync(ctx->dp_ties.p, 0, PL * 4, s), "memset");
-  RV_CUDA(cudaMemsetAsync(ctx->dp_ex.p, 0, (size_t)kOnePassRecheck * 4, s), "memset");
-  rv::dp_launch_final_max(fact, fcap, flo, PL, flat_hint(fcapn), ctx->dp_lmax.p, s);
-  rv::dp_launch_final_split(fact, fcap, flins, fhi, flo, ctx->dp_lmax.p, PL, flat_hint(fcapn),
-                            ctx->dp_best.p, ctx->dp_rlins.p, ctx->dp_rcnt.p, s);
-  ctx->launches += 2;
-  if (int rc = keep_phase(ctx->dp_rcnt.p)) return rc;
-  // (a recheck list longer than kOnePassRecheck blocks exceeds the items' bound: error word)
-  const rv::DpList rl{ctx->dp_rlins.p, 0, 0, fact, ctx->dp_rcnt.p, ctx->dp_ex.p, ctx->dp_ex.p};
-  if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_EXACT, ch[L - 1], rl, PL,
-                          kOnePassRecheck, nmax))
-    return rc;
-  rv::dp_launch_final_rechecked(fact, ctx->dp_rcnt.p, ctx->dp_rlins.p, ctx->dp_ex.p, PL,
-                                kOnePassRecheck, ctx->dp_best.p, s);
-  rv::dp_launch_final_ties(fact, fcap, fhi, flo, ctx->dp_rcnt.p, ctx->dp_ex.p, PL, flat_hint(fcapn),
-                           ctx->dp_best.p, ctx->dp_ties.p, s);
-  ctx->launches += 2;
+  // per-rank winners (sharded): slots r of best_r / ties_r
+  RV_CUDA(ctx->dp_best_r.ensure((size_t)W), "allocating");
+  RV_CUDA(ctx->dp_ties_r.ensure((size_t)W), "allocating");
+  const int ph_bnb = nph;  // the branch-and-bound phases (and the recheck) are summed over ranks
+  if (sharded)
+    RV_CUDA(cudaMemsetAsync(ctx->dp_phase.p + ph_bnb, 0, (size_t)L * 4, s), "memset");
+  for (int rk = r_lo; rk < r_hi; ++rk) {
+    rv::Own own;
+    if (sharded) {
+      own = rv::Own{ctx->lutg.p, B0, ctx->cull_g[rk], ctx->cull_g[rk + 1]};
+      ctx->cull_own_lo = own.lo;
+      ctx->cull_own_hi = own.hi;
+    }
+    int nphr = ph_bnb;
+    auto keep_phase_r = [&](const int32_t* dcnt) -> int {
+      if (!sharded) {
+        ++nphr;
+        return keep_phase(dcnt);
+      }
+      rv::dp_launch_add_i32(ctx->dp_phase.p + nphr, dcnt, s);
+      ctx->launches += 1;
+      ++nphr;
+      return RV_OK;
+    };
+    RV_CUDA(cudaMemsetAsync(ctx->dp_rdone.p, 0, PL * 4, s), "memset");
+    if (int rc = upload_i64(ctx->dp_actr[1].p, {0, m0})) return rc;
+    {
+      const int64_t f = ch[1] / ch[0];
+      if (int rc = upload_i64(ctx->dp_bring[1].p, {0, std::min<int64_t>(m0 * f * f * f, capl[1])}))
+        return rc;
+    }
+    const uint32_t* plins = ctx->grid_list.p;
+    const uint32_t* pub = ctx->l0cnt.p;
+    bool shared = true;
+    int cur = -1;
+    for (int l = 1; l < L; ++l) {
+      const int nb = cur == 1 ? 0 : 1;
+      const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1];
+      const int64_t f3 = (int64_t)f * f * f;
+      int64_t* pact = ctx->dp_actr[l & 1].p;
+      int64_t* cact = ctx->dp_actr[(l + 1) & 1].p;
+      int64_t* cbase = ctx->dp_bring[l % 3].p;
+      int64_t* pbase = shared ? pact : ctx->dp_bring[(l + 2) % 3].p;
+      int64_t* nbase = ctx->dp_bring[(l + 1) % 3].p;
+      RV_CUDA(ctx->dp_lins[nb].ensure(capl[l]), "allocating");
+      RV_CUDA(ctx->dp_ca[nb].ensure(capl[l]), "allocating");
+      RV_CUDA(ctx->dp_cb[nb].ensure(capl[l]), "allocating");
+      RV_CUDA(ctx->dp_cnt[nb].ensure(PL), "allocating");
+      RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
+      // (only level 1's parents -- the shared level-0 grid -- span other ranks' groups)
+      rv::dp_launch_bnb_expand(plins, shared, pact, pbase, pub, ctx->dp_lb.p, PL,
+                               flat_hint(shared ? m0 : capl[l - 1]), Bp, f, cbase,
+                               ctx->dp_lins[nb].p, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p,
+                               ctx->dp_cnt[nb].p, ctx->dp_err.p, s,
+                               shared ? own : rv::Own());
+      int64_t nf3 = 1;
+      if (l + 1 < L) {
+        const int64_t nf = ch[l + 1] / ch[l];
+        nf3 = nf * nf * nf;
+      }
+      // re-dive trigger (R18): not taken here -- it raises the error word (bit 8) and the solve
+      // is redone by the per-level loop, which takes it (sharded: on the rank's own subtrees)
+      rv::RediveCheck chk{cur >= 0 ? ctx->dp_cnt[cur].p : nullptr, f3, ctx->dp_rdone.p,
+                          ctx->dp_rflag.p, ctx->dp_err.p, 8};
+      const rv::OnePass op{ctx->dp_err.p, l + 1 < L ? capl[l + 1] : 0};
+      rv::dp_launch_scan(ctx->dp_cnt[nb].p, PL, nf3, cact, nbase, ctx->dp_tot.p, s,
+                         l >= 2 ? &chk : nullptr, &op);
+      ctx->launches += 2;
+      if (int rc = keep_phase_r(ctx->dp_cnt[nb].p)) return rc;
+      const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
+      const rv::DpList cl{ctx->dp_lins[nb].p, 0, 0, cbase, ctx->dp_cnt[nb].p, ctx->dp_ca[nb].p,
+                          ctx->dp_cb[nb].p};
+      if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], cl, PL, capl[l], nmax))
+        return rc;
+      plins = ctx->dp_lins[nb].p;
+      pub = ctx->dp_ca[nb].p;
+      shared = false;
+      cur = nb;
+    }
+    if (rk == r_lo) RV_CUDA(ctx->record(ph[4], s), "event");
+    // ---- finest level: max lo, exact-known blocks, the fp64 recheck, winner, ties (sharded:
+    // over the rank's subtrees; its max lo <= the global one, so it rechecks a superset)
+    const uint32_t* flins = ctx->dp_lins[cur].p;
+    const uint32_t* fhi = ctx->dp_ca[cur].p;
+    const uint32_t* flo = ctx->dp_cb[cur].p;
+    const int64_t* fcap = ctx->dp_bring[(L - 1) % 3].p;
+    int64_t* fact = ctx->dp_actr[L & 1].p;
+    RV_CUDA(cudaMemsetAsync(ctx->dp_rcnt.p, 0, PL * 4, s), "memset");
+    RV_CUDA(cudaMemsetAsync(ctx->dp_lmax.p, 0, PL * 4, s), "memset");
+    RV_CUDA(cudaMemsetAsync(ctx->dp_best.p, 0, PL * 8, s), "memset");
+    RV_CUDA(cudaMemsetAsync(ctx->dp_ties.p, 0, PL * 4, s), "memset");
+    RV_CUDA(cudaMemsetAsync(ctx->dp_ex.p, 0, (size_t)kOnePassRecheck * 4, s), "memset");
+    rv::dp_launch_final_max(fact, fcap, flo, PL, flat_hint(fcapn), ctx->dp_lmax.p, s);
+    rv::dp_launch_final_split(fact, fcap, flins, fhi, flo, ctx->dp_lmax.p, PL, flat_hint(fcapn),
+                              ctx->dp_best.p, ctx->dp_rlins.p, ctx->dp_rcnt.p, s);
+    ctx->launches += 2;
+    if (int rc = keep_phase_r(ctx->dp_rcnt.p)) return rc;
+    // (a recheck list longer than kOnePassRecheck blocks exceeds the items' bound: error word)
+    const rv::DpList rl{ctx->dp_rlins.p, 0, 0, fact, ctx->dp_rcnt.p, ctx->dp_ex.p, ctx->dp_ex.p};
+    if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_EXACT, ch[L - 1], rl, PL,
+                            kOnePassRecheck, nmax))
+      return rc;
+    rv::dp_launch_final_rechecked(fact, ctx->dp_rcnt.p, ctx->dp_rlins.p, ctx->dp_ex.p, PL,
+                                  kOnePassRecheck, ctx->dp_best.p, s);
+    rv::dp_launch_final_ties(fact, fcap, fhi, flo, ctx->dp_rcnt.p, ctx->dp_ex.p, PL,
+                             flat_hint(fcapn), ctx->dp_best.p, ctx->dp_ties.p, s);
+    ctx->launches += 2;
+    if (sharded) {
+      RV_CUDA(cudaMemcpyAsync(ctx->dp_best_r.p + rk, ctx->dp_best.p, 8, cudaMemcpyDeviceToDevice, s),
+              "D2D");
+      RV_CUDA(cudaMemcpyAsync(ctx->dp_ties_r.p + rk, ctx->dp_ties.p, 4, cudaMemcpyDeviceToDevice, s),
+              "D2D");
+    }
+    if (rk + 1 == r_hi) nph = nphr;
+  }
+  ctx->cull_own_lo = 0;
+  ctx->cull_own_hi = INT64_MAX;
+  if (sharded) {
+    if (nccl_path) {  // the ranks' winners, summed phases, and the error word on every rank
+      const int rk = ctx->cfg.rank;
+      ncclResult_t nr = nccl().AllGather(ctx->dp_best_r.p + rk, ctx->dp_best_r.p, 1, ncclUint64,
+                                         ctx->comm, s);
+      if (nr == ncclSuccess)
+        nr = nccl().AllGather(ctx->dp_ties_r.p + rk, ctx->dp_ties_r.p, 1, ncclInt32, ctx->comm, s);
+      if (nr == ncclSuccess)
+        nr = nccl().AllReduce(ctx->dp_phase.p + ph_bnb, ctx->dp_phase.p + ph_bnb, (size_t)L,
+                              ncclInt32, ncclSum, ctx->comm, s);
+      if (nr == ncclSuccess)
+        nr = nccl().AllReduce(ctx->dp_err.p, ctx->dp_err.p, 1, ncclInt32, ncclMax, ctx->comm, s);
+      if (nr != ncclSuccess)
+        return ctx->fail(RV_ENCCL, "one-pass collectives: %s", nccl().GetErrorString(nr));
+    }
+    rv::dp_launch_merge_rank_winners(ctx->dp_best_r.p, ctx->dp_ties_r.p, W, ctx->dp_best.p,
+                                     ctx->dp_ties.p, s);
+    ctx->launches += 1;
+  }
   nvtxRangePop();
   RV_CUDA(ctx->record(ph[5], s), "event");
   // ---- refinement from the winner (decoded on the device), K6 + K7 in one cooperative launch
