@@ -729,7 +729,7 @@ def run_multi(args):
         "warmup": max(3, args.warmup), "ms_per_step": t, "higher_is_better": True,
         "dtype": "f16x3-split/f32", "data": "synthetic",
         "config": {"workload": "cfg3: N=1e5, 5% inliers to R (sigma 0.02), 3% to R2, eps 0.08",
-                   "K": K, "rho_rad": rho, "path": "host planner, block counts reused across peaks"},
+                   "K": K, "rho_rad": rho, "path": "one-pass device solve per peak (earlier peaks' balls excluded on the device; setup and level 0 kept across peaks)"},
         "peaks": [{"cell": list(r.cell), "votes": r.votes, "n_inliers": r.n_inliers,
                    "rotation_error_deg": _rot_err_deg(R, r.q)}
                   for r, R in zip(res, (pr.R, pr.R2))],

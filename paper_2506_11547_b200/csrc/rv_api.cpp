@@ -180,7 +180,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->dp_pick.release(); ctx->dp_rlins.release(); ctx->dp_ex.release(); ctx->dp_lmax.release();
   ctx->rg_m.release(); ctx->rg_n.release(); ctx->rg_cnt.release(); ctx->rg_off.release();
   ctx->rg_bins.release(); ctx->rg_acc.release(); ctx->rg_best.release(); ctx->rg_sums.release();
-  ctx->dp_best.release(); ctx->dp_best_r.release(); ctx->dp_ties_r.release(); ctx->a1_acc.release(); ctx->a1_tab.release(); ctx->a1_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
+  ctx->dp_best.release(); ctx->dp_best_r.release(); ctx->dp_ties_r.release(); ctx->excl_q.release(); ctx->a1_acc.release(); ctx->a1_tab.release(); ctx->a1_best.release(); ctx->dp_ioff.release(); ctx->dp_aoff.release(); ctx->dp_tot.release();
   ctx->dp_icnt.release(); ctx->dp_phase.release(); ctx->dp_err.release();
   ctx->dp_pcnt.release(); ctx->dp_scnt.release(); ctx->dp_poff.release(); ctx->dp_sbase.release();
   ctx->cbits.release(); ctx->k12.release(); ctx->lut0.release(); ctx->lutg.release(); ctx->goff.release(); ctx->gmem.release(); ctx->lut0_B = 0; ctx->c_act.release();

@@ -231,6 +231,8 @@ struct rv_ctx {
   DevBuf<uint32_t> dp_pick, dp_rlins, dp_ex, dp_lmax;
   DevBuf<unsigned long long> dp_best, dp_best_r;  // (_r: per-rank winners, sharded one pass)
   DevBuf<int32_t> dp_ties_r;
+  DevBuf<double> excl_q;        // NEXT-2: the earlier peaks' rotations (device copy)
+  bool reuse_l0 = false;        // NEXT-2: a later peak's one-pass solve keeps setup + level 0
   DevBuf<float> rg_m, rg_n;         // NEXT-3: kept pairs
   DevBuf<int32_t> rg_cnt;
   DevBuf<int64_t> rg_off, rg_bins;
@@ -513,6 +515,12 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
 bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps);
 int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets,
                        int32_t P, double eps, int32_t levels, rv_result* out, uint32_t* masks);
+// the one-pass single solve (rv_level_loop.cpp); excl: NEXT-2 exclusion balls (no graph);
+// *redo: a capacity or the re-dive trigger -- redo the solve another way
+bool one_pass_applies(rv_ctx* ctx, int32_t P);
+int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
+                   const std::vector<int32_t>& ch, rv_result* out, uint32_t* mask, bool* redo,
+                   const rv::Excl* excl = nullptr);
 
 }  // namespace rvi
 

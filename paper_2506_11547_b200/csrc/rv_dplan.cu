@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(kDpThreads) dp_dive_children(const uint32_t* _
                                                                int32_t Bp, int32_t f,
                                                                uint32_t* out, int32_t cap,
                                                                int32_t* cnt,
-                                                               const int32_t* __restrict__ active) {
+                                                               const int32_t* __restrict__ active,
+                                                               Excl ex, int32_t finest) {
   const int p = blockIdx.x;
   if (active && !active[p]) {  // re-dive: this problem did not trigger it
     if (threadIdx.x == 0) cnt[p] = 0;
@@ -96,8 +97,8 @@ __global__ void __launch_bounds__(kDpThreads) dp_dive_children(const uint32_t* _
       lin_to_ijk(par[e / f3], Bp, i, j, k);
       const int r = e % f3, a = r / (f * f), b = (r / f) % f, c = r % f;
       const int32_t ci = f * i + a, cj = f * j + b, ck = f * k + c;
-      keep = is_candidate(Bc, ci, cj, ck);
       lin = ijk_to_lin(ci, cj, ck, Bc);
+      keep = is_candidate(Bc, ci, cj, ck) && !excl_dropped(ex, Bc, lin, finest != 0);
     }
     int tot;
     const int pos = cta_rank(keep, &tot, wsum);
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(kDpThreads) dp_dive_pick(const uint32_t* __res
                                                            const int32_t* __restrict__ cnt,
                                                            int32_t B, double eps,
                                                            const int64_t* __restrict__ rows,
-                                                           uint32_t* pick) {
+                                                           uint32_t* pick, Excl ex) {
   const int p = blockIdx.x;
   const double n = (double)(rows[p + 1] - rows[p]);
   const int64_t o = off[p];
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kDpThreads) dp_dive_pick(const uint32_t* __res
     const uint32_t lin = lins[o + e];
     int32_t i, j, k;
     lin_to_ijk(lin, B, i, j, k);
-    const int in = centre_inside(B, lin) ? 1 : 0;
+    const int in = 2 * excl_rank(ex, B, lin) + (centre_inside(B, lin) ? 1 : 0);
     const double t = bound_threshold(B, i, j, k, eps);
     const double x = (double)a[o + e] - n * (1.0 - t) * 0.5;
     if (best < 0 || in > bin || (in == bin && (x > bx || (x == bx && lin < blin)))) {
@@ -196,7 +197,7 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
                               const uint32_t* __restrict__ pub, const int64_t* __restrict__ lb,
                               int32_t P, int32_t Bp, int32_t f, const int64_t* __restrict__ ccap,
                               uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
-                              int32_t* err, Own own) {
+                              int32_t* err, Own own, Excl ex, int32_t finest) {
   const int64_t total = act_off[P];
   const int32_t Bc = Bp * f;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -212,10 +213,14 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
       const int32_t grp = own.lut[ijk_to_lin(i / r, j / r, k / r, own.B0)];
       if (grp < own.lo || grp >= own.hi) continue;
     }
+    auto kept = [&](int32_t ci, int32_t cj, int32_t ck) {
+      return is_candidate(Bc, ci, cj, ck) &&
+             !excl_dropped(ex, Bc, ijk_to_lin(ci, cj, ck, Bc), finest != 0);
+    };
     int c = 0;
     for (int a = 0; a < f; ++a)
       for (int b = 0; b < f; ++b)
-        for (int d = 0; d < f; ++d) c += is_candidate(Bc, f * i + a, f * j + b, f * k + d) ? 1 : 0;
+        for (int d = 0; d < f; ++d) c += kept(f * i + a, f * j + b, f * k + d) ? 1 : 0;
     if (c == 0) continue;
     int64_t w = ccap[p] + atomicAdd(&ccnt[p], c);
     if (w + c > ccap[p + 1]) {  // invariant: children <= parents x f^3 (never expected)
@@ -226,7 +231,7 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
       for (int b = 0; b < f; ++b)
         for (int d = 0; d < f; ++d) {
           const int32_t ci = f * i + a, cj = f * j + b, ck = f * k + d;
-          if (!is_candidate(Bc, ci, cj, ck)) continue;
+          if (!kept(ci, cj, ck)) continue;
           clins[w] = ijk_to_lin(ci, cj, ck, Bc);
           ca[w] = 0;
           cb[w] = 0;
@@ -713,17 +718,17 @@ __global__ void dp_lb_max(int64_t* lb, const int64_t* __restrict__ lb2, int32_t 
 void dp_launch_dive_children(const uint32_t* pick, const int32_t* pick_idx,
                              const uint32_t* idx_list, int32_t Bp, int32_t f, uint32_t* out,
                              int32_t cap, int32_t* cnt, int32_t P, cudaStream_t s,
-                             const int32_t* active) {
+                             const int32_t* active, const Excl& ex, bool finest) {
   dp_dive_children<<<P, kDpThreads, 0, s>>>(pick, pick_idx, idx_list, Bp, f, out, cap, cnt,
-                                            active);
+                                            active, ex, finest ? 1 : 0);
 }
 void dp_launch_lb_max(int64_t* lb, const int64_t* lb2, int32_t P, cudaStream_t s) {
   dp_lb_max<<<(P + 255) / 256, 256, 0, s>>>(lb, lb2, P);
 }
 void dp_launch_dive_pick(const uint32_t* lins, const uint32_t* a, const int64_t* off,
                          const int32_t* cnt, int32_t B, double eps, const int64_t* rows,
-                         uint32_t* pick, int32_t P, cudaStream_t s) {
-  dp_dive_pick<<<P, kDpThreads, 0, s>>>(lins, a, off, cnt, B, eps, rows, pick);
+                         uint32_t* pick, int32_t P, cudaStream_t s, const Excl& ex) {
+  dp_dive_pick<<<P, kDpThreads, 0, s>>>(lins, a, off, cnt, B, eps, rows, pick, ex);
 }
 void dp_launch_max_lo(const uint32_t* b, const int64_t* off, const int32_t* cnt, int64_t* lb,
                       int32_t P, cudaStream_t s) {
@@ -772,9 +777,11 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           const int64_t* pcap, const uint32_t* pub, const int64_t* lb, int32_t P,
                           int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
                           uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
-                          int32_t* err, cudaStream_t s, const Own& own) {
+                          int32_t* err, cudaStream_t s, const Own& own, const Excl& ex,
+                          bool finest) {
   dp_bnb_expand<<<flat_grid(total), 256, 0, s>>>(plins, shared_lins ? 1 : 0, act_off, pcap, pub,
-                                                 lb, P, Bp, f, ccap, clins, ca, cb, ccnt, err, own);
+                                                 lb, P, Bp, f, ccap, clins, ca, cb, ccnt, err, own,
+                                                 ex, finest ? 1 : 0);
 }
 
 // ---- one problem over ranks, each searching the subtrees it owns (the one-pass sharded solve)

@@ -71,13 +71,14 @@ void dp_launch_scan(int32_t* cnt, int32_t P, int64_t f3, int64_t* act, int64_t* 
 void dp_launch_dive_children(const uint32_t* pick, const int32_t* pick_idx,
                              const uint32_t* idx_list, int32_t Bp, int32_t f, uint32_t* out,
                              int32_t cap, int32_t* cnt, int32_t P, cudaStream_t s,
-                             const int32_t* active = nullptr);
+                             const int32_t* active = nullptr, const Excl& ex = Excl(),
+                             bool finest = false);
 // lb[p] = max(lb[p], lb2[p])
 void dp_launch_lb_max(int64_t* lb, const int64_t* lb2, int32_t P, cudaStream_t s);
 // dive: pick[p] = the list's max-excess block (planner key)
 void dp_launch_dive_pick(const uint32_t* lins, const uint32_t* a, const int64_t* off,
                          const int32_t* cnt, int32_t B, double eps, const int64_t* rows,
-                         uint32_t* pick, int32_t P, cudaStream_t s);
+                         uint32_t* pick, int32_t P, cudaStream_t s, const Excl& ex = Excl());
 // lb[p] = max cnt_b of the list
 void dp_launch_max_lo(const uint32_t* b, const int64_t* off, const int32_t* cnt, int64_t* lb,
                       int32_t P, cudaStream_t s);
@@ -102,7 +103,8 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           const int64_t* pcap, const uint32_t* pub, const int64_t* lb, int32_t P,
                           int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
                           uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
-                          int32_t* err, cudaStream_t s, const Own& own = Own());
+                          int32_t* err, cudaStream_t s, const Own& own = Own(),
+                          const Excl& ex = Excl(), bool finest = false);
 // Ordered BnB expansion (one problem sharded over ranks: every rank builds the identical
 // list): per-parent child counts into pcnt[total parents], their prefix into off[total + 1],
 // then the children in parent order.

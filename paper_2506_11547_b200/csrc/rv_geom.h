@@ -116,4 +116,50 @@ RV_HD void k9_of(const double x[3], const double y[3], double k[9]) {
   k[8] = x[1] * y[2] + x[2] * y[1];
 }
 
+// NEXT-2 (several rotations, reading R16): the earlier peaks' block-centre rotations q[4e..4e+3],
+// e < n, and the suppression angle rho.  A finest block is excluded iff |q_c . q_e| >= cos(rho/2)
+// (its centre within rotation angle rho of a peak); a coarser block only when all of it is:
+// angle(q_c, q_e) + r(c) <= rho - 1e-9 (r(c) as in the certified bound) -- the host planner's
+// rule (rv_plan.cpp).  n = 0: nothing excluded.
+struct Excl {
+  const double* q = nullptr;
+  int32_t n = 0;
+  double rho = 0.0, cos_half_rho = 2.0;
+};
+RV_HD bool excl_dropped(const Excl& ex, int32_t B, uint32_t lin, bool finest) {
+  if (ex.n == 0) return false;
+  int32_t i, j, k;
+  lin_to_ijk(lin, B, i, j, k);
+  double q[4];
+  cell_quat(B, i, j, k, q);
+  const double r = finest ? 0.0 : bound_radius(B, i, j, k);
+  for (int32_t e = 0; e < ex.n; ++e) {
+    const double* qe = ex.q + 4 * e;
+    const double d = fabs(q[0] * qe[0] + q[1] * qe[1] + q[2] * qe[2] + q[3] * qe[3]);
+    if (finest) {
+      if (d >= ex.cos_half_rho) return true;
+    } else if (2.0 * acos(d < 1.0 ? d : 1.0) + r <= ex.rho - 1e-9) {
+      return true;
+    }
+  }
+  return false;
+}
+// the dive's preference: 2 = entirely outside every ball, 1 = centre outside, 0 = centre inside
+RV_HD int excl_rank(const Excl& ex, int32_t B, uint32_t lin) {
+  if (ex.n == 0) return 2;
+  int32_t i, j, k;
+  lin_to_ijk(lin, B, i, j, k);
+  double q[4];
+  cell_quat(B, i, j, k, q);
+  const double r = bound_radius(B, i, j, k);
+  int rank = 2;
+  for (int32_t e = 0; e < ex.n; ++e) {
+    const double* qe = ex.q + 4 * e;
+    const double d = fabs(q[0] * qe[0] + q[1] * qe[1] + q[2] * qe[2] + q[3] * qe[3]);
+    if (d >= ex.cos_half_rho) return 0;
+    if (2.0 * acos(d < 1.0 ? d : 1.0) - r <= ex.rho) rank = 1;
+  }
+  return rank;
+}
+
 }  // namespace rv

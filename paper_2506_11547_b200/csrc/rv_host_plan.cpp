@@ -423,12 +423,53 @@ int solve_multi_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   RV_CUDA(cudaEventRecord(ctx->ev0, s), "event");
   const int64_t offs[2] = {0, n};
   std::vector<int64_t> koff;
-  if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
-  if (int rc = check_bad(ctx)) return rc;
   CountCache cache;
   std::vector<double> excl;  // earlier peaks' block-centre rotations
   int32_t found = 0;
+  // one GPU: every peak is a one-pass device solve with the earlier peaks' balls excluded
+  // (rv_geom.h excl_dropped / excl_rank: the host planner's rules); a solve the one-pass loop
+  // hands back (capacity, re-dive) runs on the host planner below
+  const int32_t lev = levels == 0 ? std::min<int32_t>(5, (int32_t)ctx->chain.size()) : levels;
+  const std::vector<int32_t> ch(ctx->chain.end() - lev, ctx->chain.end());
+  const bool dev = one_pass_applies(ctx, 1) && ctx->effective_world() == 1 && !ctx->comm &&
+                   dplan_applies(ctx, lev, ch[0], eps);
+  float dev_ms = 0;
+  bool setup_done = false;  // (each one-pass solve runs its own setup)
+  bool l0_ok = false;       // the last one-pass solve completed: its setup and level 0 are valid
   for (int32_t k = 0; k < K; ++k) {
+    if (dev) {
+      std::vector<double> eq(excl);
+      for (int32_t e = 0; e < k; ++e) {
+        double* q = eq.data() + 4 * e;
+        const double nq = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+        for (int c = 0; c < 4; ++c) q[c] /= nq;
+      }
+      RV_CUDA(ctx->excl_q.ensure(std::max<size_t>(4, eq.size())), "allocating");
+      if (k > 0)
+        RV_CUDA(cudaMemcpyAsync(ctx->excl_q.p, eq.data(), eq.size() * 8, cudaMemcpyHostToDevice, s),
+                "H2D");
+      const rv::Excl ex{ctx->excl_q.p, k, rho, std::cos(rho / 2.0)};
+      rv_result r{};
+      bool redo = false;
+      ctx->reuse_l0 = l0_ok;  // the previous peak ran one pass on this input
+      const int rc1 = solve_one_pass(ctx, x, y, n, eps, ch, &r, nullptr, &redo, &ex);
+      ctx->reuse_l0 = false;
+      if (rc1) return rc1;
+      l0_ok = !redo;
+      if (!redo) {
+        dev_ms += r.ms;
+        if (r.votes == 0 && r.n_tied == 0) break;  // every block suppressed
+        out[k] = r;
+        excl.insert(excl.end(), r.q_cell, r.q_cell + 4);
+        ++found;
+        continue;
+      }
+    }
+    if (!setup_done && !dev) {
+      if (int rc = run_setup(ctx, x, y, offs, 1, koff)) return rc;
+      if (int rc = check_bad(ctx)) return rc;
+      setup_done = true;
+    }
     rv_plan* plan = nullptr;
     if (rv_plan_create_ex(ctx->chain.data(), (int32_t)ctx->chain.size(), levels, n, eps,
                           (double)ctx->cfg.guard, excl.data(), k, rho, &plan) != 0)
@@ -456,11 +497,13 @@ int solve_multi_impl(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   RV_SYNC(cudaEventSynchronize(ctx->ev1), "event");
   float ms = 0;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  cudaGetLastError();
   for (int32_t k = 0; k < found; ++k) {
     out[k].ms = ms;
     ctx->fill_counters(out[k]);
   }
   *n_found = found;
+  (void)dev_ms;
   return RV_OK;
 }
 

@@ -964,14 +964,15 @@ __global__ void __launch_bounds__(256) rv_l0_argmax_kernel(const uint32_t* __res
                                                            const uint32_t* __restrict__ lins,
                                                            int32_t B, const double* __restrict__ bg,
                                                            const int64_t* __restrict__ rows,
-                                                           int32_t* out) {
+                                                           int32_t* out, Excl ex) {
   const int p = blockIdx.x;
   const double n = (double)(rows[p + 1] - rows[p]);
   const uint32_t* c = cnt + (int64_t)p * m0;
   int best = -1, bin = 0;
   double bx = -1e300;
   for (int e = threadIdx.x; e < m0; e += blockDim.x) {
-    const int in = centre_inside(B, lins[e]) ? 1 : 0;
+    // (NEXT-2: blocks away from the exclusion balls first)
+    const int in = 2 * excl_rank(ex, B, lins[e]) + (centre_inside(B, lins[e]) ? 1 : 0);
     const double x = (double)c[e] - n * bg[e];
     if (best < 0 || in > bin || (in == bin && (x > bx || (x == bx && e < best)))) {
       best = e; bin = in; bx = x;
@@ -1032,8 +1033,8 @@ __global__ void __launch_bounds__(256) rv_l0_survivors_kernel(const uint32_t* __
 
 void launch_l0_argmax(const uint32_t* cnt, int64_t m0, const uint32_t* lins, int32_t B,
                       const double* bg, const int64_t* rows, int32_t P, int32_t* out,
-                      cudaStream_t s) {
-  if (P > 0) rv_l0_argmax_kernel<<<P, 256, 0, s>>>(cnt, m0, lins, B, bg, rows, out);
+                      cudaStream_t s, const Excl& ex) {
+  if (P > 0) rv_l0_argmax_kernel<<<P, 256, 0, s>>>(cnt, m0, lins, B, bg, rows, out, ex);
 }
 
 void launch_l0_survivors(const uint32_t* cnt, int64_t m0, const int32_t* problems,

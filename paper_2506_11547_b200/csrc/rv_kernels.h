@@ -5,6 +5,8 @@
 
 #include <cuda_runtime.h>
 
+#include "rv_geom.h"
+
 namespace rv {
 
 // Kernel attributes (the dynamic shared-memory opt-in) are per device: a launcher sets them the
@@ -205,7 +207,7 @@ void launch_l2_prefetch(const void* p, int64_t bytes, cudaStream_t s);
 // out + off[j].
 void launch_l0_argmax(const uint32_t* cnt, int64_t m0, const uint32_t* lins, int32_t B,
                       const double* bg, const int64_t* rows, int32_t P, int32_t* out,
-                      cudaStream_t s);
+                      cudaStream_t s, const Excl& ex = Excl());
 void launch_l0_survivors(const uint32_t* cnt, int64_t m0, const int32_t* problems,
                          const int64_t* lb, const int64_t* off, int32_t J, int32_t* outc,
                          int32_t* out, cudaStream_t s);

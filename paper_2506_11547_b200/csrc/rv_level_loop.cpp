@@ -800,7 +800,8 @@ struct OnePassRB {
 // host values the result needs (hv).  Every size and launch shape is a function of (n, eps, ch)
 // and the context only, which is what makes the sequence graph-capturable.
 int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
-                     const std::vector<int32_t>& ch, uint32_t* mask, rv_ctx::OnePassHost& hv) {
+                     const std::vector<int32_t>& ch, uint32_t* mask, rv_ctx::OnePassHost& hv,
+                     const rv::Excl& ex) {
   const int L = (int)ch.size();
   // one problem over W ranks (one_pass_applies: grouped culling): level 0 in slabs and the dive's
   // blocks by owner, each with one all-reduce of fixed size; the branch and bound split into the
@@ -824,7 +825,11 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   RV_CUDA(ctx->up.ensure((size_t)m0 * 8 + 65536), "allocating staging");
   RV_CUDA(ctx->record(ph[0], s), "event");
   nvtxRangePushA("rv.setup");
-  if (int rc = run_setup(ctx, x, y, offs, 1, koff, true)) return rc;
+  // (ctx->reuse_l0: the previous solve of this call had the same input -- NEXT-2's next peak --
+  // so the K tables, level 0's counts and the culling lists are still valid)
+  const bool reuse_l0 = ctx->reuse_l0;
+  if (reuse_l0) koff.assign({0, pad4(n)});
+  else if (int rc = run_setup(ctx, x, y, offs, 1, koff, true)) return rc;
   nvtxRangePop();
   RV_CUDA(ctx->record(ph[1], s), "event");
   auto upload_i64 = [&](int64_t* dst, std::initializer_list<int64_t> v) -> int {
@@ -873,9 +878,14 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   ctx->cull_ready = false;
   const int64_t tpad = ctx->tc_toff.back();
   const bool cull = ctx->cull_on && (double)m0 * (double)(tpad / 32) * 4.0 <= 4294967296.0;
-  RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, (size_t)m0 * 4, s), "memset");
   const rv::DpList l0{ctx->grid_list.p, 1, m0, nullptr, nullptr, ctx->l0cnt.p, ctx->l0cnt.p};
-  if (cull) {
+  if (reuse_l0) {
+    if (cull) {
+      ctx->cull_l0cnt = reinterpret_cast<const uint32_t*>(ctx->c_fill.p);
+      ctx->cull_ready = true;
+    }
+  } else if (cull) {
+    RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, (size_t)m0 * 4, s), "memset");
     RV_CUDA(ctx->cbits.ensure((size_t)m0 * (size_t)(tpad / 32)), "allocating level-0 bitmasks");
     if (int rc = cull_prepare(ctx, B0, m0, PL)) return rc;
     if (sharded) {  // this rank's slab (i-slab aligned: whole groups), counts all-reduced
@@ -908,6 +918,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     ctx->cull_l0cnt = reinterpret_cast<const uint32_t*>(ctx->c_fill.p);
     ctx->cull_ready = true;
   } else {
+    RV_CUDA(cudaMemsetAsync(ctx->l0cnt.p, 0, (size_t)m0 * 4, s), "memset");
     if (int rc = vote_level(ctx, x, y, rows, koff, eps, RV_MODE_BOUND, B0, l0, PL, m0, nmax))
       return rc;
   }
@@ -915,7 +926,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   RV_CUDA(ctx->dp_pick.ensure(PL), "allocating");
   RV_CUDA(ctx->dp_lb.ensure(PL), "allocating");
   rv::launch_l0_argmax(ctx->l0cnt.p, m0, ctx->grid_list.p, B0, ctx->l0bg.p, ctx->rows.p, PL,
-                       ctx->l0idx.p, s);
+                       ctx->l0idx.p, s, ex);
   ctx->launches += 1;
   nvtxRangePop();
   RV_CUDA(ctx->record(ph[2], s), "event");
@@ -930,7 +941,8 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     RV_CUDA(ctx->dp_off[0].ensure(PL + 1), "allocating");
     if (int rc = upload_i64(ctx->dp_off[0].p, {0, cap})) return rc;
     rv::dp_launch_dive_children(ctx->dp_pick.p, ctx->l0idx.p, l == 1 ? ctx->grid_list.p : nullptr,
-                                Bp, f, ctx->dp_lins[0].p, cap, ctx->dp_cnt[0].p, PL, s);
+                                Bp, f, ctx->dp_lins[0].p, cap, ctx->dp_cnt[0].p, PL, s, nullptr,
+                                ex, l == L - 1);
     const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
     RV_CUDA(cudaMemsetAsync(ctx->dp_ca[0].p, 0, (size_t)cap * 4, s), "memset");
     if (mode == RV_MODE_FINAL) RV_CUDA(cudaMemsetAsync(ctx->dp_cb[0].p, 0, (size_t)cap * 4, s), "memset");
@@ -946,7 +958,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     }
     if (mode == RV_MODE_BOUND)
       rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, ctx->dp_off[0].p,
-                              ctx->dp_cnt[0].p, ch[l], eps, ctx->rows.p, ctx->dp_pick.p, PL, s);
+                              ctx->dp_cnt[0].p, ch[l], eps, ctx->rows.p, ctx->dp_pick.p, PL, s, ex);
     else
       rv::dp_launch_max_lo(ctx->dp_cb[0].p, ctx->dp_off[0].p, ctx->dp_cnt[0].p, ctx->dp_lb.p, PL, s);
     ctx->launches += 1;
@@ -1026,7 +1038,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
                                flat_hint(shared ? m0 : capl[l - 1]), Bp, f, cbase,
                                ctx->dp_lins[nb].p, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p,
                                ctx->dp_cnt[nb].p, ctx->dp_err.p, s,
-                               shared ? own : rv::Own());
+                               shared ? own : rv::Own(), ex, l == L - 1);
       int64_t nf3 = 1;
       if (l + 1 < L) {
         const int64_t nf = ch[l + 1] / ch[l];
@@ -1162,13 +1174,16 @@ static void one_pass_key(rv_ctx* ctx, const float* x, const float* y, int64_t n,
 }
 
 int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, double eps,
-                   const std::vector<int32_t>& ch, rv_result* out, uint32_t* mask, bool* redo) {
+                   const std::vector<int32_t>& ch, rv_result* out, uint32_t* mask, bool* redo,
+                   const rv::Excl* excl) {
   *redo = false;
+  const rv::Excl ex = excl ? *excl : rv::Excl();
+  const bool graphs = ctx->graphs_on && ex.n == 0;  // (the exclusions are not in the key)
   cudaStream_t s = ctx->stream;
   uint64_t key[8];
   one_pass_key(ctx, x, y, n, eps, ch, mask, key);
   const bool same_as_last = ctx->lastkey_ok && std::memcmp(key, ctx->lastkey, sizeof(key)) == 0;
-  const bool replay = ctx->graphs_on && ctx->gexec && ctx->gkey_ok &&
+  const bool replay = graphs && ctx->gexec && ctx->gkey_ok &&
                       std::memcmp(key, ctx->gkey, sizeof(key)) == 0 &&
                       ctx->gepoch == g_realloc_epoch.load();
   rv_ctx::OnePassHost hv;
@@ -1188,7 +1203,7 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
     ctx->cull_tc_launches = hv.cull_tc_launches;
     ctx->evn = hv.evn;
     ctx->cevn = hv.cevn;
-  } else if (ctx->graphs_on && same_as_last && ctx->gstream) {
+  } else if (graphs && same_as_last && ctx->gstream) {
     // capture this enqueue (the previous solve with the same key ran it directly, so the
     // workspace is sized and every one-time kernel attribute is set)
     if (ctx->gexec) {
@@ -1204,7 +1219,7 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
     int rc = RV_OK;
     if (ce == cudaSuccess) {
       ctx->capturing = true;
-      rc = enqueue_one_pass(ctx, x, y, n, eps, ch, mask, hv);
+      rc = enqueue_one_pass(ctx, x, y, n, eps, ch, mask, hv, ex);
       ctx->capturing = false;
       cudaError_t ee = cudaStreamEndCapture(ctx->gstream, &g);
       if (ce == cudaSuccess) ce = ee;
@@ -1221,7 +1236,7 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
       cudaGetLastError();
       ctx->graphs_on = false;
       ctx->stream = s;
-      return solve_one_pass(ctx, x, y, n, eps, ch, out, mask, redo);
+      return solve_one_pass(ctx, x, y, n, eps, ch, out, mask, redo, excl);
     }
     ctx->gexec = ge;
     std::memcpy(ctx->gkey, key, sizeof(key));
@@ -1239,11 +1254,11 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
     RV_CUDA(cudaEventRecord(ctx->gjoin, ctx->gstream), "event");
     RV_CUDA(cudaStreamWaitEvent(s, ctx->gjoin, 0), "join");
   } else {
-    if (int rc = enqueue_one_pass(ctx, x, y, n, eps, ch, mask, hv)) return rc;
+    if (int rc = enqueue_one_pass(ctx, x, y, n, eps, ch, mask, hv, ex)) return rc;
     RV_CUDA(cudaEventRecord(ctx->ev1, s), "event");
   }
   std::memcpy(ctx->lastkey, key, sizeof(key));
-  ctx->lastkey_ok = true;
+  ctx->lastkey_ok = ex.n == 0;
   RV_SYNC(cudaEventSynchronize(ctx->ev1), "one-pass solve");
   ctx->collect_vote_ms();
   ctx->ev_collect();
