@@ -857,7 +857,16 @@ constexpr int kCtStages = RV_CT_STAGES;  // 16 KB gathered stages in flight
 #ifndef RV_CT_PROD
 #define RV_CT_PROD 4  // gathering warps
 #endif
+#ifndef RV_CT_SPLIT
+#define RV_CT_SPLIT 1  // gathering warps per stage (a team; stage k -> team k mod (PROD / SPLIT));
+                       // measured: 16 warps in teams of 4 (with 8 epilogue warps) 0.75 vs 0.68 ms
+                       // on cfg4's level 1, 8 / 12 warps and 11 stages no better
+                       // (profiles/r02_k3ct_gather_teams.log): the gather is not issue-bound
+#endif
 constexpr int kCtProd = RV_CT_PROD;
+constexpr int kCtSplit = RV_CT_SPLIT;
+constexpr int kCtTeams = kCtProd / kCtSplit;
+static_assert(kCtProd % kCtSplit == 0, "gathering warps come in whole teams");
 constexpr int kCtN = 256;                            // gathered entries per stage
 #ifndef RV_CT_PP
 #define RV_CT_PP 0  // 1: ping-pong epilogue (alternate stages per warp group): measured slower at NA = 1
@@ -954,7 +963,7 @@ __global__ void __launch_bounds__(kCtThreads)
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kCtStages; ++i) {
-      bar_init(&sm.full[i], 32);  // one cp.async arrive per lane of the stage's gathering warp
+      bar_init(&sm.full[i], 32 * kCtSplit);  // one cp.async arrive per lane of the stage's team
       bar_init(&sm.empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -1002,7 +1011,9 @@ __global__ void __launch_bounds__(kCtThreads)
 
   if (warp < kCtProd) {
     // ---------------- gather ----------------
-    const int pw = warp;
+    // team tm = warp / kCtSplit gathers the stages k = tm, tm + teams, ... of an item's stage
+    // sequence; warp part pt of the team gathers the stage's rows [pt N / split, (pt+1) N / split)
+    const int pw = warp / kCtSplit, pt = warp % kCtSplit;
     uint32_t gs = 0, gi = 0;
     for (;; ++gi) {
       const int idx = next_item(true);
@@ -1011,7 +1022,7 @@ __global__ void __launch_bounds__(kCtThreads)
       const int64_t toff = segs[it.seg].koff;
       const int na = ct_na(it);
       const int N = kCtN / na;  // entries per stage
-      if (pw == 0 && lane == 0) {  // the item's na x 128 block rows (rows past its blocks: ignored)
+      if (warp == 0 && lane == 0) {  // the item's na x 128 block rows (rows past its blocks: ignored)
         const uint32_t ab = gi & 1;
         if (gi >= 2) bar_wait(&sm.aempty[ab], ((gi >> 1) - 1) & 1);
         const int64_t row0 = FIN ? 2 * (int64_t)it.pos0 : it.pos0;  // multiple of 8
@@ -1023,36 +1034,41 @@ __global__ void __launch_bounds__(kCtThreads)
       // a stage's N indices (N / 32 per lane: entry r*32 + lane) are loaded RV_CT_LOOK of this
       // warp's stages ahead into a register ring whose slots are reused in place
       constexpr int kLook = RV_CT_LOOK;
-      uint32_t ring[kLook][8];
-      auto load_idx = [&](int k, uint32_t (&ix)[8]) {
+      // this warp's kIx index registers of a stage: entries r * 32 + lane, r in its part
+      constexpr int kIx = 8 / kCtSplit;
+      auto load_idx = [&](int k, uint32_t (&ix)[kIx]) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int q = 0; q < kIx; ++q) {
+          const int r = pt * kIx + q;
           const int ge = k * N + r * 32 + lane;
-          ix[r] = (RV_CT_ABL & 8) ? (uint32_t)ge
+          ix[q] = (RV_CT_ABL & 8) ? (uint32_t)ge
                   : (r * 32 < N && ge < it.ne) ? __ldcs(li + ge) : 0xffffffffu;  // streamed once
         }
       };
-      const int k0 = (int)((pw - (int)(gs % kCtProd) + kCtProd) % kCtProd);
+      const int k0 = (int)((pw - (int)(gs % kCtTeams) + kCtTeams) % kCtTeams);
+      uint32_t ring[kLook][kIx];
 #pragma unroll
-      for (int d = 0; d < kLook; ++d) load_idx(k0 + d * kCtProd, ring[d]);
-      for (int kb = k0; kb < ns; kb += kLook * kCtProd) {
+      for (int d = 0; d < kLook; ++d) load_idx(k0 + d * kCtTeams, ring[d]);
+      for (int kb = k0; kb < ns; kb += kLook * kCtTeams) {
 #pragma unroll
         for (int d = 0; d < kLook; ++d) {
-          const int k = kb + d * kCtProd;
+          const int k = kb + d * kCtTeams;
           if (k >= ns) break;
           const uint32_t gk = gs + (uint32_t)k, st = gk % kCtStages;
-          if (lane == 0) CT_STAMP(0, gk);
-          uint32_t cur[8];
+          if (lane == 0 && pt == 0) CT_STAMP(0, gk);
+          uint32_t cur[kIx];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) cur[r] = ring[d][r];
-          load_idx(k + kLook * kCtProd, ring[d]);
+          for (int q = 0; q < kIx; ++q) cur[q] = ring[d][q];
+          load_idx(k + kLook * kCtTeams, ring[d]);
           if (gk >= (uint32_t)kCtStages) bar_wait(&sm.empty[st], ((gk / kCtStages) - 1) & 1);
-          // four lanes per row, one 16-byte chunk each: a copy instruction covers 8 whole rows
+          // four lanes per row, one 16-byte chunk each: a copy instruction covers 8 whole rows;
+          // this warp's row octets j in [pt * 32 / split, (pt + 1) * 32 / split)
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
+          for (int jj = 0; jj < 32 / kCtSplit; ++jj) {
+            const int j = pt * (32 / kCtSplit) + jj;
             if (8 * j >= N) break;  // warp-uniform
             const int e = 8 * j + (lane >> 2), c = lane & 3;  // stage row, chunk
-            const uint32_t ix = __shfl_sync(0xffffffffu, cur[j >> 2], e & 31);
+            const uint32_t ix = __shfl_sync(0xffffffffu, cur[(j >> 2) - pt * kIx], e & 31);
             const int64_t g = ix != 0xffffffffu ? toff + (int64_t)ix : pad_row;
             uint8_t* dst = sm.b[st] + (e >> 3) * 512 + (e & 7) * 16 + c * 128;
 #ifndef RV_CT_CA
@@ -1072,7 +1088,7 @@ __global__ void __launch_bounds__(kCtThreads)
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
                            su32(&sm.full[st]))
                        : "memory");
-          if (lane == 0) CT_STAMP(1, gk);
+          if (lane == 0 && pt == 0) CT_STAMP(1, gk);
         }
       }
       gs += (uint32_t)ns;
