@@ -233,6 +233,8 @@ struct rv_ctx {
   DevBuf<int32_t> dp_ties_r;
   DevBuf<double> excl_q;        // NEXT-2: the earlier peaks' rotations (device copy)
   bool reuse_l0 = false;        // NEXT-2: a later peak's one-pass solve keeps setup + level 0
+  int64_t op_cap = (int64_t)1 << 18;  // one-pass level-list capacity (blocks; grows on overflow)
+  int32_t op_lshift = 4;        // one-pass culling-list capacity: level-0 pairs >> this
   DevBuf<float> rg_m, rg_n;         // NEXT-3: kept pairs
   DevBuf<int32_t> rg_cnt;
   DevBuf<int64_t> rg_off, rg_bins;

@@ -758,14 +758,17 @@ int solve_batched_dplan(rv_ctx* ctx, const float* x, const float* y,
 // the dive, every branch-and-bound level, the finest level with its exact recheck, and the
 // refinement -- is enqueued without a single host round trip; the host reads everything back
 // once at the end.  What the per-level loop (solve_batched_dplan) learns from its round trips is
-// replaced by fixed, data-independent capacities: the level lists hold up to kOnePassCap blocks
+// replaced by data-independent capacities: the level lists hold up to ctx->op_cap blocks
 // (min with the grid's candidate count), the culling lists up to a quarter of the level-0 pairs
 // (the per-level loop's own culling limit), the exact recheck up to kOnePassRecheck blocks.  A
 // device-side violation (a longer list, or the re-dive trigger R18, which this loop does not
 // take) raises the solve's error word; the level scans then empty every later level, and the
 // host redoes the solve with the per-level loop (rv_result.flags |= RV_RETRIED).  Every decision
 // is the per-level loop's, so both give the same result.
-constexpr int64_t kOnePassCap = (int64_t)1 << 22;
+// capacities start small (a first solve allocates little) and grow 8x (level lists, up to
+// kOnePassCapMax blocks) or 2x (culling lists, up to a quarter of the level-0 pairs) after a
+// solve that outgrew them; the grown sizes stay with the context
+constexpr int64_t kOnePassCapMax = (int64_t)1 << 22;
 constexpr int64_t kOnePassRecheck = 4096;
 
 bool one_pass_applies(rv_ctx* ctx, int32_t P) {
@@ -900,7 +903,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     rv::CullGroups gr;
     if (ctx->cull_grouped) gr = rv::CullGroups{ctx->goff.p, ctx->gmem.p, ctx->cull_G};
     const int64_t NB = ctx->cull_G;
-    const int64_t lcap = std::min<int64_t>((int64_t)1 << 29, m0 * tpad / 8) + 4 * NB;
+    const int64_t lcap = std::min<int64_t>((int64_t)1 << 29, (m0 * tpad) >> ctx->op_lshift) + 4 * NB;
     RV_CUDA(ctx->c_lofs.ensure(NB + 1), "allocating");
     RV_CUDA(ctx->c_lidx.ensure(lcap + 4), "allocating level-0 lists");
     RV_CUDA(ctx->c_fill.ensure(NB), "allocating");
@@ -970,7 +973,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   nvtxRangePushA("rv.bnb");
   std::vector<int64_t> capl(L, 0);
   for (int l = 1; l < L; ++l)
-    capl[l] = std::min<int64_t>(kOnePassCap, (int64_t)ch[l] * ch[l] * ch[l]);  // (B^3 >= candidates;
+    capl[l] = std::min<int64_t>(ctx->op_cap, (int64_t)ch[l] * ch[l] * ch[l]);  // (B^3 >= candidates;
                                                                               // counting them costs ms)
   for (int r = 0; r < 2; ++r) RV_CUDA(ctx->dp_actr[r].ensure(PL + 1), "allocating");
   for (int r = 0; r < 3; ++r) RV_CUDA(ctx->dp_bring[r].ensure(PL + 1), "allocating");
@@ -1275,6 +1278,9 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
   if (*rb.err != 0) {  // a capacity or the re-dive: the per-level loop redoes the solve
     *redo = true;
     ctx->redo_reason = *rb.err;
+    if ((*rb.err & 16) && ctx->op_lshift > 2) --ctx->op_lshift;  // culling lists
+    if ((*rb.err & 3) && ctx->op_cap < kOnePassCapMax)             // level lists / items
+      ctx->op_cap = std::min<int64_t>(kOnePassCapMax, ctx->op_cap * 8);
     return RV_OK;
   }
   // ---- the result (as solve_batched_dplan + fill_result + run_refine)
