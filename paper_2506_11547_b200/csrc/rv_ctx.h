@@ -438,10 +438,12 @@ struct rv_ctx {
     cudaError_t e_ = (call);                              \
     if (e_ != cudaSuccess) return ctx->cuda_fail(e_, what); \
   } while (0)
-#define RV_CUDA(call, what)                               \
-  do {                                                    \
-    cudaError_t e_ = (call);                              \
-    if (e_ != cudaSuccess) return ctx->cuda_fail(e_, what); \
+#define RV_STR2(x) #x
+#define RV_STR(x) RV_STR2(x)
+#define RV_CUDA(call, what)                                                        \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) return ctx->cuda_fail(e_, what " (" __FILE__ ":" RV_STR(__LINE__) ")"); \
   } while (0)
 
 namespace rvi {

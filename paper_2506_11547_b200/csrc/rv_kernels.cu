@@ -919,6 +919,19 @@ void launch_decode_q0(const unsigned long long* best, int32_t P, int32_t B, doub
   rv_decode_q0_kernel<<<(P + 255) / 256, 256, 0, s>>>(best, P, B, qs);
 }
 
+// up to kSetMax int64 pairs into device memory in one launch (a one-pass solve's offset tables,
+// carried by the kernel's arguments)
+__global__ void rv_set_consts_kernel(SetList l) {
+  const int t = threadIdx.x;
+  if (t < l.n) {
+    l.dst[t][0] = l.v0[t];
+    l.dst[t][1] = l.v1[t];
+  }
+}
+void launch_set_consts(const SetList& l, cudaStream_t s) {
+  if (l.n > 0) rv_set_consts_kernel<<<1, 32, 0, s>>>(l);
+}
+
 // two int64 constants into device memory as a kernel (a one-pass solve's offsets: a captured
 // graph then carries them in its kernel arguments instead of pointing at host staging)
 __global__ void rv_set_i64x2_kernel(int64_t* d, int64_t v0, int64_t v1) {

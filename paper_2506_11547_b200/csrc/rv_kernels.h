@@ -258,6 +258,19 @@ cudaError_t launch_refine1(const Refine1Args& a, int num_sms, cudaStream_t s);
 // qs[4p..] = canonical centre rotation of the winner packed in best[p] at resolution B
 void launch_decode_q0(const unsigned long long* best, int32_t P, int32_t B, double* qs,
                       cudaStream_t s);
+// pairs dst[k][0..1] = (v0[k], v1[k]), k < n, in one launch
+struct SetList {
+  static constexpr int kMax = 16;
+  int64_t* dst[kMax];
+  int64_t v0[kMax], v1[kMax];
+  int32_t n = 0;
+  bool add(int64_t* d, int64_t a, int64_t b) {
+    if (n >= kMax) return false;
+    dst[n] = d; v0[n] = a; v1[n] = b; ++n;
+    return true;
+  }
+};
+void launch_set_consts(const SetList& l, cudaStream_t s);
 // d[0] = v0, d[1] = v1 (one thread)
 void launch_set_i64x2(int64_t* d, int64_t v0, int64_t v1, cudaStream_t s);
 

@@ -778,6 +778,19 @@ bool one_pass_applies(rv_ctx* ctx, int32_t P) {
   return !sharded || (ctx->cull_on && ctx->cull_tc);
 }
 
+#ifndef RV_OP_CHECK
+#define RV_OP_CHECK 0  // debug builds: wait and check after each phase of a one-pass solve
+#endif
+#if RV_OP_CHECK
+#define OP_CHECK(what)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = cudaStreamSynchronize(s);                                           \
+    if (e_ != cudaSuccess) return ctx->fail(RV_ECUDA, "one-pass %s: %s", what, cudaGetErrorString(e_)); \
+  } while (0)
+#else
+#define OP_CHECK(what) do { } while (0)
+#endif
+
 // The read-back slots of a one-pass solve in ctx->grb (pinned)
 struct OnePassRB {
   unsigned long long *best, *cp, *bad;
@@ -828,6 +841,35 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   RV_CUDA(ctx->up.ensure((size_t)m0 * 8 + 65536), "allocating staging");
   RV_CUDA(ctx->record(ph[0], s), "event");
   nvtxRangePushA("rv.setup");
+  // every offset pair of the solve in one launch: rows, K / TC table offsets, the dive levels'
+  // list offsets (one pair per level), the branch and bound's first act / base
+  {
+    RV_CUDA(ctx->rows.ensure(2), "allocating offsets");
+    RV_CUDA(ctx->koffs.ensure(2), "allocating offsets");
+    RV_CUDA(ctx->toffs.ensure(2), "allocating offsets");
+    RV_CUDA(ctx->dp_off[0].ensure(2 * (size_t)L), "allocating");
+    for (int r = 0; r < 2; ++r) RV_CUDA(ctx->dp_actr[r].ensure(2), "allocating");
+    for (int r = 0; r < 3; ++r) RV_CUDA(ctx->dp_bring[r].ensure(2), "allocating");
+    rv::SetList sl;
+    sl.add(ctx->rows.p, 0, n);
+    sl.add(ctx->koffs.p, 0, pad4(n));
+    sl.add(ctx->toffs.p, 0, (n + rv::kTcN - 1) / rv::kTcN * rv::kTcN);
+    for (int l = 1; l < L; ++l) {
+      const int64_t f = ch[l] / ch[l - 1];
+      sl.add(ctx->dp_off[0].p + 2 * l, 0, 27 * f * f * f);
+    }
+    if (!sharded) {  // (the branch and bound's rings start here; per rank when sharded)
+      const int64_t f = ch[1] / ch[0];
+      sl.add(ctx->dp_actr[1].p, 0, m0);
+      sl.add(ctx->dp_bring[1].p, 0,
+             std::min<int64_t>(m0 * f * f * f,
+                               std::min<int64_t>(ctx->op_cap, (int64_t)ch[1] * ch[1] * ch[1])));
+    }
+    OP_CHECK("before the offsets");
+    rv::launch_set_consts(sl, s);
+    ctx->launches += 1;
+    OP_CHECK("offsets");
+  }
   // (ctx->reuse_l0: the previous solve of this call had the same input -- NEXT-2's next peak --
   // so the K tables, level 0's counts and the culling lists are still valid)
   const bool reuse_l0 = ctx->reuse_l0;
@@ -835,6 +877,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   else if (int rc = run_setup(ctx, x, y, offs, 1, koff, true)) return rc;
   nvtxRangePop();
   RV_CUDA(ctx->record(ph[1], s), "event");
+  OP_CHECK("setup");
   auto upload_i64 = [&](int64_t* dst, std::initializer_list<int64_t> v) -> int {
     rv::launch_set_i64x2(dst, *v.begin(), *(v.begin() + 1), s);  // kernel arguments, see run_setup
     ctx->launches += 1;
@@ -933,6 +976,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   ctx->launches += 1;
   nvtxRangePop();
   RV_CUDA(ctx->record(ph[2], s), "event");
+  OP_CHECK("level0");
   // ---- dive (fixed sizes: the 27-neighbourhood's children)
   nvtxRangePushA("rv.dive");
   for (int l = 1; l < L; ++l) {
@@ -941,8 +985,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     RV_CUDA(ctx->dp_ca[0].ensure(cap), "allocating");
     RV_CUDA(ctx->dp_cb[0].ensure(cap), "allocating");
     RV_CUDA(ctx->dp_cnt[0].ensure(PL), "allocating");
-    RV_CUDA(ctx->dp_off[0].ensure(PL + 1), "allocating");
-    if (int rc = upload_i64(ctx->dp_off[0].p, {0, cap})) return rc;
+    int64_t* doff = ctx->dp_off[0].p + 2 * l;  // {0, cap}, written at the start
     rv::dp_launch_dive_children(ctx->dp_pick.p, ctx->l0idx.p, l == 1 ? ctx->grid_list.p : nullptr,
                                 Bp, f, ctx->dp_lins[0].p, cap, ctx->dp_cnt[0].p, PL, s, nullptr,
                                 ex, l == L - 1);
@@ -951,7 +994,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     if (mode == RV_MODE_FINAL) RV_CUDA(cudaMemsetAsync(ctx->dp_cb[0].p, 0, (size_t)cap * 4, s), "memset");
     ctx->launches += 1;
     if (int rc = keep_phase(ctx->dp_cnt[0].p)) return rc;
-    const rv::DpList dl{ctx->dp_lins[0].p, 0, 0, ctx->dp_off[0].p, ctx->dp_cnt[0].p,
+    const rv::DpList dl{ctx->dp_lins[0].p, 0, 0, doff, ctx->dp_cnt[0].p,
                         ctx->dp_ca[0].p, ctx->dp_cb[0].p};
     if (sharded) {  // each block voted by its owner, counts all-reduced (fixed size cap)
       if (int rc = vote_level_owned(ctx, x, y, rows, koff, eps, mode, ch[l], dl, cap, nmax))
@@ -960,14 +1003,15 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
       return rc;
     }
     if (mode == RV_MODE_BOUND)
-      rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, ctx->dp_off[0].p,
+      rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, doff,
                               ctx->dp_cnt[0].p, ch[l], eps, ctx->rows.p, ctx->dp_pick.p, PL, s, ex);
     else
-      rv::dp_launch_max_lo(ctx->dp_cb[0].p, ctx->dp_off[0].p, ctx->dp_cnt[0].p, ctx->dp_lb.p, PL, s);
+      rv::dp_launch_max_lo(ctx->dp_cb[0].p, doff, ctx->dp_cnt[0].p, ctx->dp_lb.p, PL, s);
     ctx->launches += 1;
   }
   nvtxRangePop();
   RV_CUDA(ctx->record(ph[3], s), "event");
+  OP_CHECK("dive");
   // ---- branch and bound from the level-0 survivors: lists alternate between sets 0 and 1 at
   // fixed capacities; offsets in the rings as in the per-level loop
   nvtxRangePushA("rv.bnb");
@@ -1012,8 +1056,8 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
       return RV_OK;
     };
     RV_CUDA(cudaMemsetAsync(ctx->dp_rdone.p, 0, PL * 4, s), "memset");
-    if (int rc = upload_i64(ctx->dp_actr[1].p, {0, m0})) return rc;
-    {
+    if (sharded) {  // (one rank: written with the solve's other offsets at the start)
+      if (int rc = upload_i64(ctx->dp_actr[1].p, {0, m0})) return rc;
       const int64_t f = ch[1] / ch[0];
       if (int rc = upload_i64(ctx->dp_bring[1].p, {0, std::min<int64_t>(m0 * f * f * f, capl[1])}))
         return rc;
@@ -1125,6 +1169,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   }
   nvtxRangePop();
   RV_CUDA(ctx->record(ph[5], s), "event");
+  OP_CHECK("bnb+final");
   // ---- refinement from the winner (decoded on the device), K6 + K7 in one cooperative launch
   nvtxRangePushA("rv.refine");
   RV_CUDA(ctx->partials.ensure((size_t)((n + rv::kRefRowsPerItem - 1) / rv::kRefRowsPerItem) * 10),
@@ -1140,6 +1185,7 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   ctx->launches += 1;
   nvtxRangePop();
   RV_CUDA(ctx->record(ph[6], s), "event");
+  OP_CHECK("refine");
   // ---- the one read-back (into the pinned block; the host reads it after one wait)
   OnePassRB rb(ctx->grb);
   if (nph > 3 * L + 1) return ctx->fail(RV_ECUDA, "internal: phase slots");

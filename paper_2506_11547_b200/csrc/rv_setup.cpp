@@ -19,10 +19,9 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
   RV_CUDA(ctx->bad.ensure(1), "allocating flag");
   RV_CUDA(ctx->up.ensure(3 * (P + 1) * sizeof(int64_t) + 2048), "allocating staging");
   ctx->up.reset();
-  if (dev_offsets) {  // one problem: the offsets as kernel arguments (graph-capturable)
-    rv::launch_set_i64x2(ctx->rows.p, offsets[0], offsets[1], ctx->stream);
-    rv::launch_set_i64x2(ctx->koffs.p, koff_out[0], koff_out[1], ctx->stream);
-    ctx->launches += 2;
+  if (dev_offsets) {
+    // one problem: the caller wrote rows / koffs / toffs with launch_set_consts (the offsets
+    // as kernel arguments, graph-capturable)
   } else {
     int64_t* hrows = ctx->up.take<int64_t>(P + 1);
     int64_t* hk = ctx->up.take<int64_t>(P + 1);
@@ -47,8 +46,7 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
     RV_CUDA(ctx->tctab.ensure((size_t)(toff[P] + 8) * 64), "allocating K3-TC table");
     RV_CUDA(ctx->toffs.ensure(P + 1), "allocating offsets");
     if (dev_offsets) {
-      rv::launch_set_i64x2(ctx->toffs.p, toff[0], toff[1], ctx->stream);
-      ctx->launches += 1;
+      // (written by the caller, see above)
     } else {
       int64_t* ht = ctx->up.take<int64_t>(P + 1);  // staging sized for it above
       std::memcpy(ht, toff.data(), (P + 1) * sizeof(int64_t));
