@@ -32,6 +32,11 @@ sys.path.insert(0, ROOT)
 METRIC = "corr×cell votes/s and ms/solve at N=1e6, 99% outliers, 1/2/4/8 B200"
 UNIT = "corr×cell votes/s"
 WORKLOAD = "cfg4: N=1e6 fp32 correspondences, 1% inliers (sigma=0.01), 99% uniform-S2 outliers, eps=0.05"
+WORKLOADS = {  # the other single-problem configs (extra lines, BASELINE.json configs 1-3)
+    "cfg1": "cfg1: N=100, 50 inliers (sigma=0.01), 50 uniform-S2 outliers, eps=0.05",
+    "cfg2": "cfg2: N=1e4, 10% inliers (sigma=0.01), 90% uniform-S2 outliers, eps=0.05",
+    "cfg3": "cfg3: N=1e5, 5% inliers to R (sigma=0.02), 3% to R2, 92% uniform outliers, eps=0.08",
+    "cfg4": WORKLOAD}
 FLOP_PER_PAIR = 18          # 9 FMA per (correspondence, cell) pair in the traceless 9-entry form
 SURVEY_FLOP_PER_PAIR = 20   # 10 FMA per pair (the 10-entry form) -- the roofline unit
 PAPER_CONTEXT = ("< 0.5 s per solve at N = 1e6, 99% outliers on a GeForce RTX 4080 + i7 CPU, "
@@ -75,7 +80,7 @@ def parse():
                     help="alg1: the paper's Algorithm 1 (NEXT-4 baseline, extra line); "
                          "multi: two rotations of config 3 (NEXT-2, extra line); "
                          "rigid: rigid pose, the paper's synthetic setting (NEXT-3, extra line)")
-    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg5"],
+    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg5 (4096 x 1000 batched problems) is an extra measurement, "
                          "not the metric's bench line")
     return ap.parse_args()
@@ -387,7 +392,7 @@ def run_ours(args):
     from paper_2506_11547_b200 import RotVote
 
     world, rank, local, nccl_id = _dist_setup(args)
-    pr = datagen.cfg4()
+    pr = getattr(datagen, args.workload)()
     stream = torch.cuda.current_stream()
     chain = tuple(int(c) for c in args.chain.split(","))
     rv = RotVote(device=local, max_n=pr.n, rank=rank, world=world, nccl_id=nccl_id,
@@ -464,7 +469,8 @@ def run_ours(args):
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
         "dtype": "f16x3-split/f32" if args.vote == "tc" else "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "levels": args.levels or min(5, len(chain)),
+        "config": {"workload": WORKLOADS.get(args.workload, WORKLOAD),
+                   "levels": args.levels or min(5, len(chain)),
                    "vote_path": args.vote + ("+cull" if cull_ms > 0 else ""),
                    "chain": list(chain[-(args.levels or min(5, len(chain))):]),
                    "l2": "flushed between steps (512 MB write)",
@@ -496,14 +502,14 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         host = _host_info()
-        full = oracle_full_solve("cfg4") if args.cpu_full else None
+        full = oracle_full_solve(args.workload) if args.cpu_full else None
         if full is not None:
             r0 = res
             B = r0.B
             lin = (r0.cell[0] * B + r0.cell[1]) * B + r0.cell[2]
             line["cpu_baseline"] = {
                 "value": full["pairs"] / full["s"], "unit": UNIT, "cores": 1, "kind": "oracle",
-                "sample": f"one complete certified solve of cfg4 by the oracle, pinned to core "
+                "sample": f"one complete certified solve of {args.workload} by the oracle, pinned to core "
                           f"{full['affinity']} (taskset): {full['cells']} blocks x 1e6 "
                           f"correspondences, exact fp64 counts",
                 "ms_per_solve": 1e3 * full["s"],
