@@ -515,7 +515,7 @@ int cull_build_lists(rv_ctx* ctx, int32_t PL, int64_t m0, const uint32_t* l0cnt,
 int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
                const std::vector<int64_t>& koff, double eps, int32_t mode, int32_t B,
                const rv::DpList& Ld, int32_t PL, int64_t entries_bound, int64_t nmax,
-               bool emit_bits = false);
+               bool emit_bits = false, const rv::DiveStep* dive = nullptr);
 bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps);
 int solve_batched_impl(rv_ctx* ctx, const float* x, const float* y, const int64_t* offsets,
                        int32_t P, double eps, int32_t levels, rv_result* out, uint32_t* masks);

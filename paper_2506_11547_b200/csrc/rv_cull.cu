@@ -42,6 +42,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/rotvote.h"
+#include "rv_dive.cuh"
 #include "rv_dplan.h"
 #include "rv_geom.h"
 #include "rv_kernels.h"
@@ -545,7 +546,38 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
     const float* k12, int64_t* act, int32_t* acnt, int32_t* tanc, int32_t* tslot, int64_t* aoff,
     int64_t* ioff, int32_t* cidx, float* phi, uint8_t* tphi, float tc_guard, VoteSeg* segs,
     int32_t* counts, int32_t* work, CullItem* items, int64_t target, int64_t max_items,
-    int32_t* err, int64_t own_lo, int64_t own_hi, int32_t cpi) {
+    int32_t* err, int64_t own_lo, int64_t own_hi, int32_t cpi, DiveStep d) {
+  if (d.on) {  // the one-pass dive level: pick, children, zeroed counts, phase (rv_dplan.h)
+    __shared__ uint32_t s_par[27];
+    __shared__ int s_i[34];
+    __shared__ DiveKey s_k[33];
+    const double n = (double)(rows[1] - rows[0]);
+    const uint32_t pick = d.prev_lins
+        ? dive_pick_cta(d.prev_lins + d.prev_off[0], d.prev_a + d.prev_off[0], d.prev_cnt[0],
+                        d.pickB, eps, n, d.ex, s_k)
+        : d.grid_list[d.l0idx[0]];
+    if (threadIdx.x == 0 && d.pick_out) *d.pick_out = pick;
+#ifdef RV_OP_CHECK
+#if RV_OP_CHECK
+    if (threadIdx.x == 0)
+      printf("dive step: prev %p m %d o %lld pickB %d Bp %d f %d cap %d pick %u first %u\n",
+             (const void*)d.prev_lins, d.prev_lins ? d.prev_cnt[0] : -1,
+             d.prev_lins ? (long long)d.prev_off[0] : -1LL, d.pickB, d.Bp, d.f, d.cap, pick,
+             d.prev_lins ? d.prev_lins[0] : 0u);
+#endif
+#endif
+    const int c = dive_children_cta(pick, d.Bp, d.f, d.out, d.cap, d.ex, d.finest != 0, s_par, s_i);
+    for (int e = threadIdx.x; e < d.cap; e += blockDim.x) {
+      d.ca[e] = 0;
+      if (d.cb) d.cb[e] = 0;
+    }
+    if (threadIdx.x == 0) {
+      *d.out_cnt = c;
+      if (d.phase) *d.phase = c;
+    }
+    __threadfence_block();
+    __syncthreads();
+  }
 #if RV_PS_TIMING
   long long t0 = clock64();
 #endif
@@ -1403,7 +1435,7 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
                       CullItem* items, int64_t entries_bound, int64_t max_items, int32_t* err,
-                      cudaStream_t s, int64_t own_lo, int64_t own_hi) {
+                      cudaStream_t s, int64_t own_lo, int64_t own_hi, const DiveStep* dive) {
   const int64_t NB = (int64_t)P * m0;
   // items: ~8 per resident K3-C warp; K3-CT (one CTA per SM, tphi set) ~4 per CTA, since its
   // per-item cost (the block rows, the column reduction) is larger
@@ -1417,9 +1449,10 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
                                        lofs, k12, cs.act, cs.acnt, cs.tanc, cs.tslot, cs.aoff,
                                        cs.ioff, cs.cidx, cs.phi, cs.tphi, cs.tc_guard, segs,
                                        cs.counts, cs.work, items, target, max_items, err, own_lo,
-                                       own_hi, cpi);
+                                       own_hi, cpi, dive ? *dive : DiveStep());
     return 1;
   }
+  if (dive && dive->on) return -1;  // a folded dive level needs the one-CTA planner
   const bool small = NB <= (1 << 16);
   if (!small) cudaMemsetAsync(cs.acnt, 0, (size_t)NB * 4, s);
   cull_act<<<1, 1024, 0, s>>>(L, P, cs.act, cs.acnt, small ? NB : 0);

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/rotvote.h"
+#include "rv_dive.cuh"
 #include "rv_dplan.h"
 #include "rv_geom.h"
 
@@ -29,38 +30,7 @@ namespace {
 
 constexpr int kDpThreads = 256;
 
-// CTA-wide ordered compaction helper: returns this thread's output position among the
-// threads with keep == true (in thread order) and writes the CTA total to *total.
-__device__ __forceinline__ int cta_rank(bool keep, int* total, int* wsum) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-  if (lane == 0) wsum[warp] = __popc(bal);
-  __syncthreads();
-  int before = 0, tot = 0;
-  for (int w = 0; w < kDpThreads / 32; ++w) {
-    if (w < warp) before += wsum[w];
-    tot += wsum[w];
-  }
-  __syncthreads();
-  *total = tot;
-  return before + __popc(bal & ((1u << lane) - 1u));
-}
-
-// the 27-neighbourhood of (i,j,k) at resolution B, candidates only, ascending lin: the offsets
-// (a,b,c) in lexicographic order give ascending lin
-__device__ int neighbourhood(int32_t B, uint32_t lin, uint32_t out[27]) {
-  int32_t i, j, k;
-  lin_to_ijk(lin, B, i, j, k);
-  int m = 0;
-  for (int a = -1; a <= 1; ++a)
-    for (int b = -1; b <= 1; ++b)
-      for (int c = -1; c <= 1; ++c) {
-        const int32_t ni = i + a, nj = j + b, nk = k + c;
-        if (ni < 0 || nj < 0 || nk < 0 || ni >= B || nj >= B || nk >= B) continue;
-        if (is_candidate(B, ni, nj, nk)) out[m++] = ijk_to_lin(ni, nj, nk, B);
-      }
-  return m;
-}
+// (the dive helpers: rv_dive.cuh)
 
 }  // namespace
 
@@ -81,31 +51,10 @@ __global__ void __launch_bounds__(kDpThreads) dp_dive_children(const uint32_t* _
     return;
   }
   __shared__ uint32_t par[27];
-  __shared__ int npar, wsum[kDpThreads / 32];
-  if (threadIdx.x == 0)
-    npar = neighbourhood(Bp, idx_list ? idx_list[pick_idx[p]] : pick[p], par);
-  __syncthreads();
-  const int f3 = f * f * f, total = npar * f3;
-  const int32_t Bc = Bp * f;
-  int base = 0;
-  for (int e0 = 0; e0 < total; e0 += kDpThreads) {
-    const int e = e0 + threadIdx.x;
-    bool keep = false;
-    uint32_t lin = 0;
-    if (e < total) {
-      int32_t i, j, k;
-      lin_to_ijk(par[e / f3], Bp, i, j, k);
-      const int r = e % f3, a = r / (f * f), b = (r / f) % f, c = r % f;
-      const int32_t ci = f * i + a, cj = f * j + b, ck = f * k + c;
-      lin = ijk_to_lin(ci, cj, ck, Bc);
-      keep = is_candidate(Bc, ci, cj, ck) && !excl_dropped(ex, Bc, lin, finest != 0);
-    }
-    int tot;
-    const int pos = cta_rank(keep, &tot, wsum);
-    if (keep && base + pos < cap) out[(int64_t)p * cap + base + pos] = lin;
-    base += tot;
-  }
-  if (threadIdx.x == 0) cnt[p] = base < cap ? base : cap;
+  __shared__ int sh[34];
+  const uint32_t pk = idx_list ? idx_list[pick_idx[p]] : pick[p];
+  const int c = dive_children_cta(pk, Bp, f, out + (int64_t)p * cap, cap, ex, finest != 0, par, sh);
+  if (threadIdx.x == 0) cnt[p] = c;
 }
 
 // Dive pick over the problem's list (lins, a) of cnt[p] blocks at list + off[p].
@@ -117,41 +66,11 @@ __global__ void __launch_bounds__(kDpThreads) dp_dive_pick(const uint32_t* __res
                                                            const int64_t* __restrict__ rows,
                                                            uint32_t* pick, Excl ex) {
   const int p = blockIdx.x;
-  const double n = (double)(rows[p + 1] - rows[p]);
+  __shared__ DiveKey sh[33];
   const int64_t o = off[p];
-  const int m = cnt[p];
-  int best = -1, bin = 0;
-  double bx = -1e300;
-  uint32_t blin = 0;
-  for (int e = threadIdx.x; e < m; e += blockDim.x) {
-    const uint32_t lin = lins[o + e];
-    int32_t i, j, k;
-    lin_to_ijk(lin, B, i, j, k);
-    const int in = 2 * excl_rank(ex, B, lin) + (centre_inside(B, lin) ? 1 : 0);
-    const double t = bound_threshold(B, i, j, k, eps);
-    const double x = (double)a[o + e] - n * (1.0 - t) * 0.5;
-    if (best < 0 || in > bin || (in == bin && (x > bx || (x == bx && lin < blin)))) {
-      best = e; bin = in; bx = x; blin = lin;
-    }
-  }
-  __shared__ int sb[kDpThreads], si[kDpThreads];
-  __shared__ double sx[kDpThreads];
-  __shared__ uint32_t sl[kDpThreads];
-  sb[threadIdx.x] = best; si[threadIdx.x] = bin; sx[threadIdx.x] = bx; sl[threadIdx.x] = blin;
-  __syncthreads();
-  for (int w = kDpThreads / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      const int o2 = threadIdx.x + w;
-      if (sb[o2] >= 0) {
-        const int t = threadIdx.x;
-        const bool take = sb[t] < 0 || si[o2] > si[t] ||
-                          (si[o2] == si[t] && (sx[o2] > sx[t] || (sx[o2] == sx[t] && sl[o2] < sl[t])));
-        if (take) { sb[t] = sb[o2]; si[t] = si[o2]; sx[t] = sx[o2]; sl[t] = sl[o2]; }
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) pick[p] = sl[0];
+  const uint32_t pk = dive_pick_cta(lins + o, a + o, cnt[p], B, eps,
+                                    (double)(rows[p + 1] - rows[p]), ex, sh);
+  if (threadIdx.x == 0) pick[p] = pk;
 }
 
 // lb*[p] = max cnt_b over the problem's list

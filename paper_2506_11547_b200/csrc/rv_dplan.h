@@ -156,6 +156,31 @@ struct CullScratch {
   float tc_guard;   // the guard of those rows' thresholds (guard + the TC error margin)
   int32_t ct_na;    // K3-CT: A blocks of 128 rows per item (1 or 2)
 };
+// A dive level of the one-pass solve folded into the small planner's CTA (one launch instead of
+// pick + children + zeroing + phase copy + planning): pick over the previous dive level's list
+// (prev_lins / prev_a / prev_off[0] / prev_cnt[0] at resolution pickB; prev_lins == nullptr:
+// the level-0 start grid_list[l0idx[0]]), the ordered children of its neighbourhood at
+// Bc = f Bp into out (cap, count *out_cnt, also *phase), their count slots ca / cb (cb may be
+// null) zeroed.  The planner then plans the new list (L must describe out / out_cnt / ca / cb).
+struct DiveStep {
+  int32_t on = 0;
+  const uint32_t* prev_lins = nullptr;
+  const uint32_t* prev_a = nullptr;
+  const int64_t* prev_off = nullptr;
+  const int32_t* prev_cnt = nullptr;
+  int32_t pickB = 0;
+  const int32_t* l0idx = nullptr;
+  const uint32_t* grid_list = nullptr;
+  uint32_t* pick_out = nullptr;
+  Excl ex;
+  int32_t finest = 0;
+  int32_t Bp = 0, f = 0, cap = 0;
+  uint32_t* out = nullptr;
+  int32_t* out_cnt = nullptr;
+  uint32_t* ca = nullptr;
+  uint32_t* cb = nullptr;
+  int32_t* phase = nullptr;
+};
 // returns the number of kernels it launched (one CTA does everything for small levels)
 // own_lo .. own_hi: the level-0 rows (ancestors) this rank votes (blocks of other ancestors
 // are left at zero for the count all-reduce)
@@ -164,7 +189,8 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
                       CullItem* items, int64_t entries_bound, int64_t max_items, int32_t* err,
-                      cudaStream_t s, int64_t own_lo = 0, int64_t own_hi = INT64_MAX);
+                      cudaStream_t s, int64_t own_lo = 0, int64_t own_hi = INT64_MAX,
+                      const DiveStep* dive = nullptr);
 // items needed for at most `entries` list entries
 int64_t cull_items_bound(int64_t entries, int num_sms);
 

@@ -122,7 +122,7 @@ bool dplan_applies(rv_ctx* ctx, int32_t levels_eff, int32_t B0, double eps) {
 int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<int64_t>& rows,
                const std::vector<int64_t>& koff, double eps, int32_t mode, int32_t B,
                const rv::DpList& Ld, int32_t PL, int64_t entries_bound, int64_t nmax,
-               bool emit_bits) {
+               bool emit_bits, const rv::DiveStep* dive) {
   cudaStream_t s = ctx->stream;
   if (ctx->cull_ready && mode != RV_MODE_EXACT) {
     const int64_t eb = std::max<int64_t>(1, entries_bound);
@@ -148,12 +148,15 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                              ctx->c_icnt.p, ctx->c_work.p,
                              ctx->cull_grouped ? ctx->c_tphi.p : nullptr,
                              ctx->cfg.guard + kTcExtraGuard, ctx->cull_na};
-    ctx->launches += rv::launch_cull_items(Ld, ctx->rows.p, ctx->toffs.p, PL, B, ctx->cull_B0,
-                                           ctx->cull_grouped ? ctx->lutg.p : ctx->lut0.p,
-                                           ctx->cull_G, ctx->cull_l0cnt,
-                                           ctx->c_lofs.p, ctx->k12.p, eps, mode, ctx->cfg.guard,
-                                           ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, eb, mi,
-                                           ctx->dp_err.p, s, ctx->cull_own_lo, ctx->cull_own_hi);
+    const int nl = rv::launch_cull_items(Ld, ctx->rows.p, ctx->toffs.p, PL, B, ctx->cull_B0,
+                                         ctx->cull_grouped ? ctx->lutg.p : ctx->lut0.p,
+                                         ctx->cull_G, ctx->cull_l0cnt,
+                                         ctx->c_lofs.p, ctx->k12.p, eps, mode, ctx->cfg.guard,
+                                         ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, eb, mi,
+                                         ctx->dp_err.p, s, ctx->cull_own_lo, ctx->cull_own_hi,
+                                         dive);
+    if (nl < 0) return ctx->fail(RV_ECUDA, "internal: a folded dive level needs the small planner");
+    ctx->launches += nl;
 #ifndef RV_CT_PREFETCH
 #define RV_CT_PREFETCH 0  // measured: no gain (K3-CT 0.843 vs 0.844 ms), +25 us
 #endif
@@ -784,8 +787,11 @@ bool one_pass_applies(rv_ctx* ctx, int32_t P) {
 #if RV_OP_CHECK
 #define OP_CHECK(what)                                                                   \
   do {                                                                                   \
-    cudaError_t e_ = cudaStreamSynchronize(s);                                           \
+    cudaError_t e_ = ctx->capturing ? cudaSuccess : cudaStreamSynchronize(s);            \
     if (e_ != cudaSuccess) return ctx->fail(RV_ECUDA, "one-pass %s: %s", what, cudaGetErrorString(e_)); \
+    int32_t w_ = 0;                                                                      \
+    if (!ctx->capturing && ctx->dp_err.p) cudaMemcpy(&w_, ctx->dp_err.p, 4, cudaMemcpyDeviceToHost); \
+    if (w_) fprintf(stderr, "[rv] one-pass %s: error word %d\n", what, w_);             \
   } while (0)
 #else
 #define OP_CHECK(what) do { } while (0)
@@ -978,6 +984,18 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
   RV_CUDA(ctx->record(ph[2], s), "event");
   OP_CHECK("level0");
   // ---- dive (fixed sizes: the 27-neighbourhood's children)
+  // the dive's list buffers at the largest level's size up front: a folded level picks from the
+  // previous level's list in place, so nothing may reallocate them between two dive levels
+  {
+    int64_t capmax = 1;
+    for (int l = 1; l < L; ++l) {
+      const int64_t f = ch[l] / ch[l - 1];
+      capmax = std::max<int64_t>(capmax, 27 * f * f * f);
+    }
+    RV_CUDA(ctx->dp_lins[0].ensure(capmax), "allocating");
+    RV_CUDA(ctx->dp_ca[0].ensure(capmax), "allocating");
+    RV_CUDA(ctx->dp_cb[0].ensure(capmax), "allocating");
+  }
   nvtxRangePushA("rv.dive");
   for (int l = 1; l < L; ++l) {
     const int32_t Bp = ch[l - 1], f = ch[l] / ch[l - 1], cap = 27 * f * f * f;
@@ -986,28 +1004,80 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
     RV_CUDA(ctx->dp_cb[0].ensure(cap), "allocating");
     RV_CUDA(ctx->dp_cnt[0].ensure(PL), "allocating");
     int64_t* doff = ctx->dp_off[0].p + 2 * l;  // {0, cap}, written at the start
+    const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
+    const rv::DpList dl{ctx->dp_lins[0].p, 0, 0, doff, ctx->dp_cnt[0].p,
+                        ctx->dp_ca[0].p, ctx->dp_cb[0].p};
+    // one rank, culled, a small level: the pick (over the previous dive level), the children,
+    // their zeroed counts and the phase count run inside the one-CTA planner (rv_dplan.h
+    // DiveStep) -- one launch instead of five
+    const bool fold = !sharded && ctx->cull_ready && cap <= 8192 && ctx->cull_G <= (1 << 14);
+    if (fold) {
+      rv::DiveStep d;
+      d.on = 1;
+      if (l > 1) {
+        d.prev_lins = ctx->dp_lins[0].p;
+        d.prev_a = ctx->dp_ca[0].p;
+        d.prev_off = ctx->dp_off[0].p + 2 * (l - 1);
+        d.prev_cnt = ctx->dp_cnt[0].p;
+        d.pickB = ch[l - 1];
+      }
+      d.l0idx = ctx->l0idx.p;
+      d.grid_list = ctx->grid_list.p;
+      d.pick_out = ctx->dp_pick.p;
+      d.ex = ex;
+      d.finest = l == L - 1;
+      d.Bp = Bp;
+      d.f = f;
+      d.cap = cap;
+      d.out = ctx->dp_lins[0].p;
+      d.out_cnt = ctx->dp_cnt[0].p;
+      d.ca = ctx->dp_ca[0].p;
+      d.cb = mode == RV_MODE_FINAL ? ctx->dp_cb[0].p : nullptr;
+      d.phase = ctx->dp_phase.p + nph;
+      ++nph;
+      if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], dl, PL, cap, nmax, false, &d))
+        return rc;
+      if (mode == RV_MODE_FINAL) {
+        rv::dp_launch_max_lo(ctx->dp_cb[0].p, doff, ctx->dp_cnt[0].p, ctx->dp_lb.p, PL, s);
+        ctx->launches += 1;
+      }
+      OP_CHECK("dive level (folded)");
+#if RV_OP_CHECK
+      if (!ctx->capturing) {
+        int32_t c_ = 0;
+        int64_t lb_ = 0;
+        uint32_t pk_ = 0, a_[4] = {0, 0, 0, 0};
+        cudaMemcpy(&c_, ctx->dp_cnt[0].p, 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&pk_, ctx->dp_pick.p, 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(a_, ctx->dp_ca[0].p, 16, cudaMemcpyDeviceToHost);
+        if (mode == RV_MODE_FINAL) cudaMemcpy(&lb_, ctx->dp_lb.p, 8, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[rv] dive level %d: pick %u, %d blocks, counts %u %u %u %u, lb %lld\n", l,
+                pk_, c_, a_[0], a_[1], a_[2], a_[3], (long long)lb_);
+      }
+#endif
+      continue;
+    }
+    if (l > 1)  // the previous level's pick (a folded level picks by itself)
+      rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, ctx->dp_off[0].p + 2 * (l - 1),
+                              ctx->dp_cnt[0].p, ch[l - 1], eps, ctx->rows.p, ctx->dp_pick.p, PL, s,
+                              ex);
     rv::dp_launch_dive_children(ctx->dp_pick.p, ctx->l0idx.p, l == 1 ? ctx->grid_list.p : nullptr,
                                 Bp, f, ctx->dp_lins[0].p, cap, ctx->dp_cnt[0].p, PL, s, nullptr,
                                 ex, l == L - 1);
-    const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
     RV_CUDA(cudaMemsetAsync(ctx->dp_ca[0].p, 0, (size_t)cap * 4, s), "memset");
     if (mode == RV_MODE_FINAL) RV_CUDA(cudaMemsetAsync(ctx->dp_cb[0].p, 0, (size_t)cap * 4, s), "memset");
-    ctx->launches += 1;
+    ctx->launches += l > 1 ? 2 : 1;
     if (int rc = keep_phase(ctx->dp_cnt[0].p)) return rc;
-    const rv::DpList dl{ctx->dp_lins[0].p, 0, 0, doff, ctx->dp_cnt[0].p,
-                        ctx->dp_ca[0].p, ctx->dp_cb[0].p};
     if (sharded) {  // each block voted by its owner, counts all-reduced (fixed size cap)
       if (int rc = vote_level_owned(ctx, x, y, rows, koff, eps, mode, ch[l], dl, cap, nmax))
         return rc;
     } else if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], dl, PL, cap, nmax)) {
       return rc;
     }
-    if (mode == RV_MODE_BOUND)
-      rv::dp_launch_dive_pick(ctx->dp_lins[0].p, ctx->dp_ca[0].p, doff,
-                              ctx->dp_cnt[0].p, ch[l], eps, ctx->rows.p, ctx->dp_pick.p, PL, s, ex);
-    else
+    if (mode == RV_MODE_FINAL) {
       rv::dp_launch_max_lo(ctx->dp_cb[0].p, doff, ctx->dp_cnt[0].p, ctx->dp_lb.p, PL, s);
-    ctx->launches += 1;
+      ctx->launches += 1;
+    }
   }
   nvtxRangePop();
   RV_CUDA(ctx->record(ph[3], s), "event");

@@ -167,3 +167,23 @@ def test_graph_replay_equals_direct(torch_cuda):
         assert np.array_equal(r.q, ref2.q)
     finally:
         rv.close()
+
+
+@pytest.mark.parametrize("chain", [(15, 45, 180, 360), (15, 45, 90, 180, 360),
+                                   (5, 15, 45, 90, 180, 360), (15, 45, 360)])
+def test_one_pass_chains_no_retry(torch_cuda, chain):
+    """Resolution chains with every dive-level size (f = 2, 3, 4, 8): the one-pass solve must
+    finish in one pass (a retry would hide a broken one-pass level behind the per-level loop's
+    correct answer) and equal the per-level loop bit for bit."""
+    from paper_2506_11547_b200 import RotVote
+    pr = datagen.make_problem(30000, 600, 0.01, 0.05, seed=17)
+    rv = RotVote(max_n=pr.n, chain=chain)
+    sync = rv.twin(planner="device_sync")
+    try:
+        a, ma = solve_all(torch_cuda, rv, pr)
+        b, mb = solve_all(torch_cuda, sync, pr)
+        same(a, b, ma, mb)
+        assert a.host_syncs == 1 and not a.flags & RV_RETRIED, (a.host_syncs, a.flags)
+    finally:
+        rv.close()
+        sync.close()
