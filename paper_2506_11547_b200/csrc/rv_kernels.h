@@ -142,9 +142,16 @@ void launch_vote(int mode, int groups, const float* k9, int64_t stride, const Vo
 // k12 != nullptr: also the 48-byte fp32 K rows of the culled vote ([toffs rows][12], the same
 // fp64 -> fp32 rounding as K1); tab_rm != nullptr: the table's rows again, row-major (64 B each,
 // contiguous: K3-CT's gather source).
+// K1 fused into K1-TC for one problem (P == 1, rows 0 .. n): also K1's fp32 table (k9 [9][stride],
+// rows g < n_pad, zero padding) and its data check (bad); k9 == nullptr: K1-TC alone
+struct K9Out {
+  float* k9 = nullptr;
+  int64_t stride = 0, n_pad = 0;
+  unsigned long long* bad = nullptr;
+};
 void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const int64_t* toffs,
                      int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s,
-                     float* k12 = nullptr, uint8_t* tab_rm = nullptr);
+                     float* k12 = nullptr, uint8_t* tab_rm = nullptr, const K9Out& k9o = K9Out());
 
 // K3-TC: BOUND-mode vote on tcgen05 (items: ncell <= kTcM, i0/ni multiples of kTcN, koff
 // in table rows); final_mode: RV_MODE_FINAL counts at tau -/+ guard (items: ncell <= kTcM/2).

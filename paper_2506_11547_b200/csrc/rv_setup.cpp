@@ -33,9 +33,13 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
             "copying offsets");
   }
   RV_CUDA(cudaMemsetAsync(ctx->bad.p, 0xff, sizeof(unsigned long long), ctx->stream), "memset");
-  rv::launch_setup(x, y, ctx->rows.p, ctx->koffs.p, P, total, ctx->k9.p, ctx->stride, ctx->bad.p,
-                   ctx->stream);
-  ctx->launches += 1;
+  // one problem with the tensor-core tables: K1 runs inside K1-TC (x, y read once)
+  const bool fused = ctx->tc_on && P == 1;
+  if (!fused) {
+    rv::launch_setup(x, y, ctx->rows.p, ctx->koffs.p, P, total, ctx->k9.p, ctx->stride, ctx->bad.p,
+                     ctx->stream);
+    ctx->launches += 1;
+  }
   if (ctx->tc_on) {
     std::vector<int64_t> toff(P + 1, 0);
     for (int32_t p = 0; p < P; ++p) {
@@ -59,8 +63,10 @@ int run_setup(rv_ctx* ctx, const float* x, const float* y, const int64_t* offset
     const bool k3c = cull_rows && ctx->cull_on && !ct;
     if (k3c) RV_CUDA(ctx->k12.ensure((size_t)(toff[P] + 8) * 12), "allocating K3-C rows");
     if (ct) RV_CUDA(ctx->tctab_rm.ensure((size_t)(toff[P] + 8) * 64), "allocating K3-CT rows");
+    rv::K9Out k9o;
+    if (fused) k9o = rv::K9Out{ctx->k9.p, ctx->stride, total, ctx->bad.p};
     rv::launch_setup_tc(x, y, ctx->rows.p, ctx->toffs.p, P, toff[P] + 8, ctx->tctab.p, ctx->stream,
-                        k3c ? ctx->k12.p : nullptr, ct ? ctx->tctab_rm.p : nullptr);
+                        k3c ? ctx->k12.p : nullptr, ct ? ctx->tctab_rm.p : nullptr, k9o);
     ctx->launches += 1;
     ctx->tc_toff = toff;
   }

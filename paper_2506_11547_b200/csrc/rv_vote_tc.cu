@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
                                                           int32_t P, int64_t total_pad,
                                                           uint8_t* __restrict__ tab,
                                                           float* __restrict__ k12,
-                                                          uint8_t* __restrict__ tab_rm) {
+                                                          uint8_t* __restrict__ tab_rm,
+                                                          K9Out k9o) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total_pad;
        g += (int64_t)gridDim.x * blockDim.x) {
     int32_t lo = 0, hi = P;
@@ -98,12 +99,20 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
       const int64_t r = rows[lo] + i;
       double a[3] = {x[3 * r], x[3 * r + 1], x[3 * r + 2]};
       double b[3] = {y[3 * r], y[3 * r + 1], y[3 * r + 2]};
-      const double ia = 1.0 / sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
-      const double ib = 1.0 / sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+      double na = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+      double nb = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+      if (k9o.k9 && (!(na > 0.0) || !(nb > 0.0) || !isfinite(na) || !isfinite(nb))) {
+        atomicMin(k9o.bad, (unsigned long long)r);  // K1's data check (one problem)
+        na = nb = 1.0;
+      }
+      const double ia = 1.0 / na, ib = 1.0 / nb;
 #pragma unroll
       for (int c = 0; c < 3; ++c) { a[c] *= ia; b[c] *= ib; }
       double k[9];
       k9_of(a, b, k);
+      if (k9o.k9)  // K1's fp32 table of the one problem (K1 fused: x, y read once)
+#pragma unroll
+        for (int j = 0; j < 9; ++j) k9o.k9[j * k9o.stride + g] = (float)k[j];
 #pragma unroll
       for (int j = 0; j < 9; ++j) {
         const __half h = __double2half(k[j]);
@@ -121,6 +130,9 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
         kr[2] = make_float4((float)k[8], 0.0f, 0.0f, 0.0f);
       }
     } else {
+      if (k9o.k9 && g < k9o.n_pad)  // K1's zero padding (s = 0 for every q)
+#pragma unroll
+        for (int j = 0; j < 9; ++j) k9o.k9[j * k9o.stride + g] = 0.0f;
       v[29] = __float2half_rn(1.0f);  // padding row: S' = -1
       if (k12) {
         float4* kr = reinterpret_cast<float4*>(k12 + g * 12);
@@ -144,12 +156,12 @@ __global__ void __launch_bounds__(256) rv_setup_tc_kernel(const float* __restric
 
 void launch_setup_tc(const float* x, const float* y, const int64_t* rows, const int64_t* toffs,
                      int32_t P, int64_t total_pad, uint8_t* tab, cudaStream_t s, float* k12,
-                     uint8_t* tab_rm) {
+                     uint8_t* tab_rm, const K9Out& k9o) {
   int64_t blocks = (total_pad + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   rv_setup_tc_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, y, rows, toffs, P, total_pad, tab, k12,
-                                                       tab_rm);
+                                                       tab_rm, k9o);
 }
 
 // ------------------------------------------------------------------------------------------
