@@ -132,6 +132,8 @@ int rot_vote_create(const rv_config* cfg, rv_ctx** out) {
     e = ctx->k9.ensure((size_t)9 * ctx->stride);
   }
   if (e == cudaSuccess) e = ctx->bad.ensure(1);
+  if (e == cudaSuccess) e = ctx->dp_tdone.ensure(1);  // tail-scan counter: zero between launches
+  if (e == cudaSuccess) e = cudaMemset(ctx->dp_tdone.p, 0, ctx->dp_tdone.cap * 4);
   if (e == cudaSuccess) e = ctx->up.ensure(1 << 20);
   if (e == cudaSuccess) e = ctx->down.ensure(1 << 20);
   if (e != cudaSuccess) {
@@ -164,7 +166,7 @@ void rot_vote_destroy(rv_ctx* ctx) {
   ctx->k9.release(); ctx->lins.release(); ctx->cnt.release(); ctx->vsegs.release();
   ctx->vitems.release(); ctx->rsegs.release(); ctx->ritems.release(); ctx->partials.release();
   ctx->qs.release(); ctx->flags.release(); ctx->ninl.release(); ctx->rows.release();
-  ctx->koffs.release(); ctx->bad.release(); ctx->hx.release(); ctx->hy.release();
+  ctx->koffs.release(); ctx->bad.release(); ctx->dp_tdone.release(); ctx->hx.release(); ctx->hy.release();
   ctx->hmask.release(); ctx->gather.release(); ctx->grid_list.release();
   ctx->l0cnt.release(); ctx->l0bg.release(); ctx->l0idx.release(); ctx->l0aux.release();
   ctx->l0surv.release(); ctx->atab.release(); ctx->ablk.release();

@@ -247,6 +247,7 @@ struct rv_ctx {
   DevBuf<unsigned long long> a1_best;
   int32_t a1_J = 0;
   DevBuf<int64_t> dp_ioff, dp_aoff, dp_tot;
+  DevBuf<int32_t> dp_tdone;  // last-CTA counter of the tail scans (zeroed at create)
   DevBuf<int32_t> dp_icnt, dp_phase, dp_err, dp_pcnt, dp_scnt;
   DevBuf<int64_t> dp_poff, dp_sbase;
   // event pairs around the batched vote launches (read after the final sync)
@@ -287,6 +288,7 @@ struct rv_ctx {
   DevBuf<uint32_t> c_lidx;       //   and the lists
   DevBuf<int32_t> c_fill;        //   compaction fill counters
   const uint32_t* cull_l0cnt = nullptr;  // the level-0 counts (= list lengths) of this solve
+  const int64_t* cull_pre_act = nullptr;  // see launch_cull_items (one-pass branch and bound)
   int64_t cull_own_lo = 0, cull_own_hi = INT64_MAX;  // level-0 rows a K3-C launch votes
   DevBuf<float> k12;
   DevBuf<int32_t> lut0;

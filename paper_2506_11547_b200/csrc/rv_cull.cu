@@ -1435,7 +1435,8 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
                       CullItem* items, int64_t entries_bound, int64_t max_items, int32_t* err,
-                      cudaStream_t s, int64_t own_lo, int64_t own_hi, const DiveStep* dive) {
+                      cudaStream_t s, int64_t own_lo, int64_t own_hi, const DiveStep* dive,
+                      const int64_t* pre_act) {
   const int64_t NB = (int64_t)P * m0;
   // items: ~8 per resident K3-C warp; K3-CT (one CTA per SM, tphi set) ~4 per CTA, since its
   // per-item cost (the block rows, the column reduction) is larger
@@ -1454,16 +1455,19 @@ int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs
   }
   if (dive && dive->on) return -1;  // a folded dive level needs the one-CTA planner
   const bool small = NB <= (1 << 16);
-  if (!small) cudaMemsetAsync(cs.acnt, 0, (size_t)NB * 4, s);
-  cull_act<<<1, 1024, 0, s>>>(L, P, cs.act, cs.acnt, small ? NB : 0);
-  cull_count<<<148 * 8, 256, 0, s>>>(L, P, B, B0, lut0, m0, cs.act, cs.acnt, cs.tanc, cs.tslot, err,
+  const int64_t* act = pre_act ? pre_act : cs.act;
+  if (!pre_act) {
+    if (!small) cudaMemsetAsync(cs.acnt, 0, (size_t)NB * 4, s);
+    cull_act<<<1, 1024, 0, s>>>(L, P, cs.act, cs.acnt, small ? NB : 0);
+  }
+  cull_count<<<148 * 8, 256, 0, s>>>(L, P, B, B0, lut0, m0, act, cs.acnt, cs.tanc, cs.tslot, err,
                                      own_lo, own_hi);
   cull_scan<<<1, 1024, 0, s>>>(L, rows, toffs, P, B, eps, m0, l0cnt, k12, cs.acnt, cs.aoff, cs.ioff,
                                segs, cs.counts, cs.work, target, max_items, err, cpi);
-  cull_fill<<<148 * 8, 256, 0, s>>>(L, P, B, eps, mode, guard, m0, cs.act, cs.aoff, cs.tanc, cs.tslot,
+  cull_fill<<<148 * 8, 256, 0, s>>>(L, P, B, eps, mode, guard, m0, act, cs.aoff, cs.tanc, cs.tslot,
                                     cs.cidx, cs.phi, cs.tphi, cs.tc_guard, cs.acnt, l0cnt, lofs,
                                     cs.ioff, cs.counts, items, err, cpi);
-  return 4;
+  return pre_act ? 3 : 4;
 }
 
 int64_t cull_items_bound(int64_t entries, int num_sms) {

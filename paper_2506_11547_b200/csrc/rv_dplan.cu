@@ -116,7 +116,10 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
                               const uint32_t* __restrict__ pub, const int64_t* __restrict__ lb,
                               int32_t P, int32_t Bp, int32_t f, const int64_t* __restrict__ ccap,
                               uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
-                              int32_t* err, Own own, Excl ex, int32_t finest) {
+                              int32_t* err, Own own, Excl ex, int32_t finest, TailScan ts) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < ts.zero_n;
+       b += (int64_t)gridDim.x * blockDim.x)
+    ts.zero_buf[b] = 0;
   const int64_t total = act_off[P];
   const int32_t Bc = Bp * f;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -156,6 +159,44 @@ __global__ void dp_bnb_expand(const uint32_t* __restrict__ plins, int32_t shared
           cb[w] = 0;
           ++w;
         }
+  }
+  if (ts.done) {  // the one-problem scan, by the last CTA to finish (see TailScan)
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(ts.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      volatile int32_t* vc = ccnt;
+      int32_t c = vc[0];
+      if (ts.rc.flags) {  // re-dive trigger (R18), once per problem
+        const int32_t fl = (!ts.rc.done[0] && ts.rc.pcnt[0] > 0 && c >= 16384 &&
+                            2 * (int64_t)c > (int64_t)ts.rc.pcnt[0] * ts.rc.f3) ? 1 : 0;
+        ts.rc.flags[0] = fl;
+        if (fl) {
+          ts.rc.done[0] = 1;
+          atomicOr(ts.rc.any, ts.rc.any_bit);
+        }
+      }
+      if (ts.op.err && *reinterpret_cast<volatile int32_t*>(ts.op.err)) {  // abandon the level
+        c = 0;
+        ccnt[0] = 0;
+      }
+      const int64_t nb = (int64_t)c * ts.f3;
+      ts.act[0] = 0;
+      ts.act[1] = c;
+      if (ts.next_base) {
+        ts.next_base[0] = 0;
+        ts.next_base[1] = ts.op.cap_lim > 0 && nb > ts.op.cap_lim ? ts.op.cap_lim : nb;
+      }
+      *ts.total = c;
+      if (ts.phase) *ts.phase = ts.phase_add ? *ts.phase + c : c;
+      if (ts.zero_next) *ts.zero_next = 0;
+      *ts.done = 0;
+    }
   }
 }
 
@@ -697,10 +738,10 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
                           uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
                           int32_t* err, cudaStream_t s, const Own& own, const Excl& ex,
-                          bool finest) {
+                          bool finest, const TailScan& ts) {
   dp_bnb_expand<<<flat_grid(total), 256, 0, s>>>(plins, shared_lins ? 1 : 0, act_off, pcap, pub,
                                                  lb, P, Bp, f, ccap, clins, ca, cb, ccnt, err, own,
-                                                 ex, finest ? 1 : 0);
+                                                 ex, finest ? 1 : 0, ts);
 }
 
 // ---- one problem over ranks, each searching the subtrees it owns (the one-pass sharded solve)

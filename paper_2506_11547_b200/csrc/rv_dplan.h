@@ -90,6 +90,24 @@ struct Own {
   int32_t B0 = 0;
   int64_t lo = 0, hi = 0;
 };
+// One problem (P == 1): the level's scan run by the expansion's last CTA (no separate launch):
+// act = {0, c}, next_base = {0, min(c f3, cap_lim)}, *total = c, the phase slot, the re-dive check
+// and the one-pass error word as dp_scan does (c = *ccnt, 0 when the word is raised).  done: a
+// zeroed counter the last CTA resets.
+struct TailScan {
+  uint32_t* done = nullptr;   // nullptr: no tail scan
+  int64_t f3 = 1;
+  int64_t* act = nullptr;
+  int64_t* next_base = nullptr;
+  int64_t* total = nullptr;
+  int32_t* phase = nullptr;    // the phase slot: = c, or += c when phase_add (ranks' subtrees)
+  int32_t phase_add = 0;
+  int32_t* zero_next = nullptr;  // a count to zero after the re-dive check (the next level's)
+  int32_t* zero_buf = nullptr;   // zeroed by the whole grid first (the cull bucket counters)
+  int64_t zero_n = 0;
+  RediveCheck rc{nullptr, 0, nullptr, nullptr, nullptr, 1};
+  OnePass op{nullptr, 0};
+};
 // best = max_r best_r, ties = sum of ties_r over the ranks whose count equals best's (one thread)
 void dp_launch_merge_rank_winners(const unsigned long long* best_r, const int32_t* ties_r,
                                   int32_t W, unsigned long long* best, int32_t* ties,
@@ -104,7 +122,8 @@ void dp_launch_bnb_expand(const uint32_t* plins, bool shared_lins, const int64_t
                           int64_t total, int32_t Bp, int32_t f, const int64_t* ccap,
                           uint32_t* clins, uint32_t* ca, uint32_t* cb, int32_t* ccnt,
                           int32_t* err, cudaStream_t s, const Own& own = Own(),
-                          const Excl& ex = Excl(), bool finest = false);
+                          const Excl& ex = Excl(), bool finest = false,
+                          const TailScan& ts = TailScan());
 // Ordered BnB expansion (one problem sharded over ranks: every rank builds the identical
 // list): per-parent child counts into pcnt[total parents], their prefix into off[total + 1],
 // then the children in parent order.
@@ -183,14 +202,16 @@ struct DiveStep {
 };
 // returns the number of kernels it launched (one CTA does everything for small levels)
 // own_lo .. own_hi: the level-0 rows (ancestors) this rank votes (blocks of other ancestors
-// are left at zero for the count all-reduce)
+// are left at zero for the count all-reduce).  pre_act: the lists' prefix (act[0..P]) already
+// on the device and the bucket counters (P * m0) already zeroed -- the one-problem branch and
+// bound, whose expansion does both (TailScan) -- so the act launch is skipped
 int launch_cull_items(const DpList& L, const int64_t* rows, const int64_t* toffs, int32_t P,
                       int32_t B, int32_t B0, const int32_t* lut0, int64_t m0,
                       const uint32_t* l0cnt, const int64_t* lofs, const float* k12, double eps,
                       int mode, float guard, int num_sms, const CullScratch& cs, VoteSeg* segs,
                       CullItem* items, int64_t entries_bound, int64_t max_items, int32_t* err,
                       cudaStream_t s, int64_t own_lo = 0, int64_t own_hi = INT64_MAX,
-                      const DiveStep* dive = nullptr);
+                      const DiveStep* dive = nullptr, const int64_t* pre_act = nullptr);
 // items needed for at most `entries` list entries
 int64_t cull_items_bound(int64_t entries, int num_sms);
 

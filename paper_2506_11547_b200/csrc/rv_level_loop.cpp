@@ -154,7 +154,7 @@ int vote_level(rv_ctx* ctx, const float* x, const float* y, const std::vector<in
                                          ctx->c_lofs.p, ctx->k12.p, eps, mode, ctx->cfg.guard,
                                          ctx->num_sms, cs, ctx->vsegs.p, ctx->c_items.p, eb, mi,
                                          ctx->dp_err.p, s, ctx->cull_own_lo, ctx->cull_own_hi,
-                                         dive);
+                                         dive, ctx->cull_pre_act);
     if (nl < 0) return ctx->fail(RV_ECUDA, "internal: a folded dive level needs the small planner");
     ctx->launches += nl;
 #ifndef RV_CT_PREFETCH
@@ -1149,32 +1149,50 @@ int enqueue_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, dou
       RV_CUDA(ctx->dp_ca[nb].ensure(capl[l]), "allocating");
       RV_CUDA(ctx->dp_cb[nb].ensure(capl[l]), "allocating");
       RV_CUDA(ctx->dp_cnt[nb].ensure(PL), "allocating");
-      RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
-      // (only level 1's parents -- the shared level-0 grid -- span other ranks' groups)
-      rv::dp_launch_bnb_expand(plins, shared, pact, pbase, pub, ctx->dp_lb.p, PL,
-                               flat_hint(shared ? m0 : capl[l - 1]), Bp, f, cbase,
-                               ctx->dp_lins[nb].p, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p,
-                               ctx->dp_cnt[nb].p, ctx->dp_err.p, s,
-                               shared ? own : rv::Own(), ex, l == L - 1);
+      // (level 1: zeroed here; a deeper level's count by the previous level's tail scan)
+      if (l == 1) RV_CUDA(cudaMemsetAsync(ctx->dp_cnt[nb].p, 0, PL * 4, s), "memset");
       int64_t nf3 = 1;
       if (l + 1 < L) {
         const int64_t nf = ch[l + 1] / ch[l];
         nf3 = nf * nf * nf;
       }
-      // re-dive trigger (R18): not taken here -- it raises the error word (bit 8) and the solve
+      // The level's scan runs in the expansion's last CTA (one problem: rv_dplan.h TailScan).
+      // Re-dive trigger (R18): not taken here -- it raises the error word (bit 8) and the solve
       // is redone by the per-level loop, which takes it (sharded: on the rank's own subtrees)
-      rv::RediveCheck chk{cur >= 0 ? ctx->dp_cnt[cur].p : nullptr, f3, ctx->dp_rdone.p,
-                          ctx->dp_rflag.p, ctx->dp_err.p, 8};
-      const rv::OnePass op{ctx->dp_err.p, l + 1 < L ? capl[l + 1] : 0};
-      rv::dp_launch_scan(ctx->dp_cnt[nb].p, PL, nf3, cact, nbase, ctx->dp_tot.p, s,
-                         l >= 2 ? &chk : nullptr, &op);
-      ctx->launches += 2;
-      if (int rc = keep_phase_r(ctx->dp_cnt[nb].p)) return rc;
+      rv::TailScan ts;
+      ts.done = reinterpret_cast<uint32_t*>(ctx->dp_tdone.p);
+      ts.f3 = nf3;
+      ts.act = cact;
+      ts.next_base = nbase;
+      ts.total = ctx->dp_tot.p;
+      ts.phase = ctx->dp_phase.p + nphr;
+      ts.phase_add = sharded ? 1 : 0;
+      ts.zero_next = l + 1 < L ? ctx->dp_cnt[nb ^ 1].p : nullptr;
+      if (l >= 2)
+        ts.rc = rv::RediveCheck{ctx->dp_cnt[cur].p, f3, ctx->dp_rdone.p, ctx->dp_rflag.p,
+                                ctx->dp_err.p, 8};
+      ts.op = rv::OnePass{ctx->dp_err.p, l + 1 < L ? capl[l + 1] : 0};
+      if (ctx->cull_ready) {  // the level's cull bucket counters and list prefix (= cact)
+        RV_CUDA(ctx->c_acnt.ensure((size_t)PL * ctx->cull_G), "allocating");
+        ts.zero_buf = ctx->c_acnt.p;
+        ts.zero_n = (int64_t)PL * ctx->cull_G;
+      }
+      // (only level 1's parents -- the shared level-0 grid -- span other ranks' groups)
+      rv::dp_launch_bnb_expand(plins, shared, pact, pbase, pub, ctx->dp_lb.p, PL,
+                               flat_hint(shared ? m0 : capl[l - 1]), Bp, f, cbase,
+                               ctx->dp_lins[nb].p, ctx->dp_ca[nb].p, ctx->dp_cb[nb].p,
+                               ctx->dp_cnt[nb].p, ctx->dp_err.p, s,
+                               shared ? own : rv::Own(), ex, l == L - 1, ts);
+      ctx->launches += 1;
+      ++nphr;
+      if (!sharded) ++nph;  // (keep_phase's slot; one rank: nph == nphr)
       const int32_t mode = l == L - 1 ? RV_MODE_FINAL : RV_MODE_BOUND;
       const rv::DpList cl{ctx->dp_lins[nb].p, 0, 0, cbase, ctx->dp_cnt[nb].p, ctx->dp_ca[nb].p,
                           ctx->dp_cb[nb].p};
-      if (int rc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], cl, PL, capl[l], nmax))
-        return rc;
+      ctx->cull_pre_act = ctx->cull_ready ? cact : nullptr;
+      const int vrc = vote_level(ctx, x, y, rows, koff, eps, mode, ch[l], cl, PL, capl[l], nmax);
+      ctx->cull_pre_act = nullptr;
+      if (vrc) return vrc;
       plins = ctx->dp_lins[nb].p;
       pub = ctx->dp_ca[nb].p;
       shared = false;
