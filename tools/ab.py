@@ -79,7 +79,7 @@ def run(args):
             env["RV_LIB"] = os.path.join(OUT, f"librotvote_{name}.so")
         args = [MICRO, name] if micro else [CODE, chain, cfg, name]
         subprocess.run([sys.executable, "-c", *args], env=env, cwd=os.path.dirname(HERE),
-                       timeout=600)
+                       timeout=int(os.environ.get("AB_TIMEOUT", "600")))
 
 
 if __name__ == "__main__":
