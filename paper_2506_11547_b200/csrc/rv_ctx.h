@@ -434,14 +434,14 @@ struct rv_ctx {
 };
 
 // a host wait on the device inside a call (counted in rv_result.host_syncs)
-#define RV_SYNC(call, what)                               \
-  do {                                                    \
-    ctx->host_syncs += 1;                                 \
-    cudaError_t e_ = (call);                              \
-    if (e_ != cudaSuccess) return ctx->cuda_fail(e_, what); \
-  } while (0)
 #define RV_STR2(x) #x
 #define RV_STR(x) RV_STR2(x)
+#define RV_SYNC(call, what)                                                        \
+  do {                                                                             \
+    ctx->host_syncs += 1;                                                          \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) return ctx->cuda_fail(e_, what " (" __FILE__ ":" RV_STR(__LINE__) ")"); \
+  } while (0)
 #define RV_CUDA(call, what)                                                        \
   do {                                                                             \
     cudaError_t e_ = (call);                                                       \

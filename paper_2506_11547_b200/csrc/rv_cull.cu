@@ -911,6 +911,16 @@ constexpr int kCtEpi0 = kCtProd + 1;                 // first epilogue warp
 #ifndef RV_CT_DYN
 #define RV_CT_DYN 1  // items handed out dynamically (a scheduler warp + a work counter)
 #endif
+#ifndef RV_CT_SL
+#define RV_CT_SL 1  // accumulator slices per stage: the stage's kCtN TMEM columns are filled by
+                    // RV_CT_SL groups of MMAs (N = kCtN / RV_CT_SL columns each) with their own
+                    // full / empty barriers, so the epilogue warps of a slice start after its MMAs
+                    // and the issuer refills a slice as soon as its 4 warps have read it -- a
+                    // 2 * RV_CT_SL deep accumulator ring instead of 2
+#endif
+constexpr int kCtSl = RV_CT_SL;
+static_assert(kCtSl == 1 || kCtSl == 2 || kCtSl == 4, "1, 2 or 4 accumulator slices");
+static_assert(kCtEpq % kCtSl == 0 && (!RV_CT_PP || kCtSl == 1), "whole epilogue warps per slice");
 constexpr int kCtIR = 8;  // item ring (dynamic scheduling)
 constexpr int kCtSched = kCtEpi0 + 4 * kCtEpq;  // the scheduler warp
 constexpr int kCtThreads = (kCtProd + 1 + 4 * kCtEpq + RV_CT_DYN) * 32;
@@ -938,7 +948,8 @@ __device__ long long g_ct_trace[7][kCtTraceN];
 struct CtSmem {
   uint8_t b[kCtStages][kCtN * 64];  // gathered correspondence rows (B operand)
   uint8_t a[2][kCtMaxNa * 128 * 64];  // the item's block rows (A operand), double-buffered
-  uint64_t full[kCtStages], empty[kCtStages], afull[2], aempty[2], tfull[2], tempty[2];
+  uint64_t full[kCtStages], empty[kCtStages], afull[2], aempty[2];
+  uint64_t tfull[2 * kCtSl], tempty[2 * kCtSl];  // per (accumulator, slice)
   uint64_t ifull[kCtIR], iempty[kCtIR];
   int32_t iring[kCtIR];
   uint32_t tmem_base;
@@ -951,6 +962,10 @@ __device__ __forceinline__ void ct_sign_fma(uint32_t& acc, uint32_t bits, uint32
   asm volatile("mad.hi.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(bits), "r"(two));
 }
 
+#ifndef RV_CT_COUNT
+#define RV_CT_COUNT 0  // the sign count: 0 two funnel-shift chains + popcount, 1 four chains,
+                       // 2 LEA.HI / IMAD.HI alternating (K3-TC's), 3 LEA.HI only
+#endif
 #ifndef RV_CT_SPIN
 #define RV_CT_SPIN 0  // tuning: poll the pipeline barriers with test_wait instead of try_wait
 #endif
@@ -981,7 +996,8 @@ __global__ void __launch_bounds__(kCtThreads)
   extern __shared__ __align__(1024) uint8_t ct_raw[];
   CtSmem& sm = *reinterpret_cast<CtSmem*>((reinterpret_cast<uintptr_t>(ct_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t n_items = counts_dev[0];
+  // (broadcast: the MMA warp's loop control must be provably warp-uniform, see below)
+  const int32_t n_items = __shfl_sync(0xffffffffu, counts_dev[0], 0);
   // A blocks of an item: its rows (FIN: two per block) in 128-row blocks, at most kCtMaxNa
   auto ct_na = [](const CullItem& it) -> int {
     const int rows = FIN ? 2 * it.ncell : it.ncell;
@@ -1001,8 +1017,10 @@ __global__ void __launch_bounds__(kCtThreads)
     for (int i = 0; i < 2; ++i) {
       bar_init(&sm.afull[i], 1);
       bar_init(&sm.aempty[i], 1);
+    }
+    for (int i = 0; i < 2 * kCtSl; ++i) {
       bar_init(&sm.tfull[i], 1);
-      bar_init(&sm.tempty[i], RV_CT_PP ? 8 : 4 * kCtEpq);  // the epilogue warps reading it
+      bar_init(&sm.tempty[i], RV_CT_PP ? 8 : 4 * kCtEpq / kCtSl);  // the epilogue warps reading it
     }
     for (int i = 0; i < kCtIR; ++i) {
       bar_init(&sm.ifull[i], 1);                         // the scheduler
@@ -1128,43 +1146,63 @@ __global__ void __launch_bounds__(kCtThreads)
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == kCtProd) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      uint32_t gs = 0, gi = 0;
-      for (;; ++gi) {
-        const int idx = next_item(false);
-        if (idx < 0) break;
-        const CullItem it = items[idx];
-        const int na = ct_na(it);
-        const uint32_t N = (uint32_t)(kCtN / na), idesc = idesc_f16(N);
-        const int ns = (it.ne + (int)N - 1) / (int)N;
-        const uint32_t ab = gi & 1;
-        bar_wait(&sm.afull[ab], (gi >> 1) & 1);
-        const uint32_t a0 = su32(sm.a[ab]);
-        for (int k = 0; k < ns; ++k, ++gs) {
-          const uint32_t st = gs % kCtStages, acc = gs & 1;
-          if (!(RV_CT_ABL & 64)) ct_wait(&sm.full[st], (gs / kCtStages) & 1);
-          CT_STAMP(2, gs);
+    // The whole warp walks the loop with warp-uniform values (item fields broadcast from lane 0)
+    // and one elected lane issues, so ptxas keeps the tcgen05 operands in uniform registers; the
+    // descriptors are (lo0 + tile offset, hi) pairs.  (Issued from inside `if (lane == 0)` every
+    // operand took an ELECT / R2UR loop: ~90 dependent instructions and ~1100 clk per stage on
+    // an SMSP shared with four counting epilogue warps -- the stage period, per-stage trace.)
+    constexpr uint32_t dhi = smem_desc_hi(512);
+    const uint32_t blo0 = smem_desc_lo(su32(sm.b[0]), 128);
+    const uint32_t alo0 = smem_desc_lo(su32(sm.a[0]), 128);
+    uint32_t gs = 0, gi = 0;
+    for (;; ++gi) {
+      const int idx = __shfl_sync(0xffffffffu, next_item(true), 0);
+      if (idx < 0) break;
+      const int it_ne = __shfl_sync(0xffffffffu, items[idx].ne, 0);
+      const int it_ncell = __shfl_sync(0xffffffffu, items[idx].ncell, 0);
+      const int rows = FIN ? 2 * it_ncell : it_ncell;
+      const int na = rows > 128 ? kCtMaxNa : 1;
+      const uint32_t N = (uint32_t)(kCtN / na);
+      const int ns = (it_ne + (int)N - 1) / (int)N;
+      const uint32_t ab = gi & 1;
+      bar_wait(&sm.afull[ab], (gi >> 1) & 1);
+      const uint32_t alo = alo0 + ab * (uint32_t)((kCtMaxNa * 128 * 64) >> 4);
+      for (int k = 0; k < ns; ++k, ++gs) {
+        const uint32_t st = gs % kCtStages, acc = gs & 1;
+        if (!(RV_CT_ABL & 64)) ct_wait(&sm.full[st], (gs / kCtStages) & 1);
+        if (lane == 0) CT_STAMP(2, gs);
 #if RV_CT_FENCE
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #endif
-          if (gs >= 2 && !(RV_CT_ABL & 32)) ct_wait(&sm.tempty[acc], ((gs >> 1) - 1) & 1);
-          CT_STAMP(3, gs);
-          tc_fence_after();
-          const uint32_t b0 = su32(sm.b[st]);
-          // sub-accumulator h (columns h*N .. h*N+N of the stage's kCtN) = A block h x the stage
-          for (int h = 0; h < na; ++h)
+        const uint32_t blo = blo0 + st * (uint32_t)((kCtN * 64) >> 4);
+        // slice sl = the stage's columns [sl SW, sl SW + SW), issued in units of min(SW, N)
+        // columns: unit at column c = A block c / N x the stage's rows c % N ...
+        constexpr uint32_t SW = kCtN / kCtSl;
+        const uint32_t U = SW < N ? SW : N, idu = idesc_f16(U), nsh = na == 1 ? 8u : 7u;
 #pragma unroll
-            for (int kk = 0; kk < 2; ++kk)
-              if (!(RV_CT_ABL & 2))
-                mma_f16_i(tmem + acc * kCtN + (uint32_t)h * N,
-                          smem_desc(a0 + (uint32_t)h * (128 * 64) + 256 * kk, 128, 512),
-                          smem_desc(b0 + 256 * kk, 128, 512), idesc, (uint32_t)kk);
-          mma_commit(&sm.empty[st]);
-          mma_commit(&sm.tfull[acc]);
-          CT_STAMP(4, gs);
+        for (int sl = 0; sl < kCtSl; ++sl) {
+          if (gs >= 2 && !(RV_CT_ABL & 32))
+            ct_wait(&sm.tempty[acc * kCtSl + sl], ((gs >> 1) - 1) & 1);
+          if (lane == 0 && sl == 0) CT_STAMP(3, gs);
+          tc_fence_after();
+          if (elect_one()) {
+            for (uint32_t c = sl * SW; c < (sl + 1) * SW; c += U) {
+              const uint32_t h = c >> nsh, brow = c & (N - 1);
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk)
+                if (!(RV_CT_ABL & 2))
+                  mma_f16_i(tmem + acc * kCtN + c, desc64(alo + h * ((128 * 64) >> 4) + 16 * kk, dhi),
+                            desc64(blo + brow * 4 + 16 * kk, dhi), idu, (uint32_t)kk);
+            }
+            if (sl == kCtSl - 1) mma_commit(&sm.empty[st]);
+            mma_commit(&sm.tfull[acc * kCtSl + sl]);
+          }
+          __syncwarp();
         }
-        mma_commit(&sm.aempty[ab]);
+        if (lane == 0) CT_STAMP(4, gs);
       }
+      if (elect_one()) mma_commit(&sm.aempty[ab]);
+      __syncwarp();
     }
   } else if (warp < kCtSched) {
 #if RV_CT_PP
@@ -1239,6 +1277,9 @@ __global__ void __launch_bounds__(kCtThreads)
     // ---------------- epilogue (4 kCtEpq warps: lane quarter warp % 4, a column slice each) ---
     const int ew = warp - kCtEpi0, slice = ew >> 2;
     constexpr int kCols = kCtN / kCtEpq;  // columns of a stage per warp
+    const int msl = (slice * kCols) / (kCtN / kCtSl);  // the accumulator slice of its columns
+    const uint32_t two = pad_row >= 0 ? 2u : 3u;  // a runtime 2 (keeps IMAD.HI, RV_CT_COUNT 2)
+    (void)two;
     const uint32_t lane_addr =
         tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(slice * kCols);
     uint32_t gs = 0;
@@ -1256,7 +1297,7 @@ __global__ void __launch_bounds__(kCtThreads)
       uint32_t n0 = 0, n1 = 0;
       for (int k = 0; k < ns; ++k) {
         const uint32_t g = gs + (uint32_t)k, acc = g & 1;
-        ct_wait(&sm.tfull[acc], (g >> 1) & 1);
+        ct_wait(&sm.tfull[acc * kCtSl + msl], (g >> 1) & 1);
         if (ew == 0 && lane == 0) CT_STAMP(5, g);
         tc_fence_after();
         if (active && !(RV_CT_ABL & 4)) {
@@ -1270,9 +1311,10 @@ __global__ void __launch_bounds__(kCtThreads)
             if (rr == kCols / 64 - 1) {
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) bar_arrive(&sm.tempty[acc]);
+              if (lane == 0) bar_arrive(&sm.tempty[acc * kCtSl + msl]);
               if (ew == 0 && lane == 0) CT_STAMP(6, g);
             }
+#if RV_CT_COUNT == 0
             // sign bits -> one word per 32 columns (shf funnel: w = w << 1 | sign); negatives
             // = its popcount
             uint32_t w0 = 0u, w1 = 0u;
@@ -1283,11 +1325,47 @@ __global__ void __launch_bounds__(kCtThreads)
             }
             n0 += __popc(w0);
             n1 += __popc(w1);
+#elif RV_CT_COUNT == 1  // four funnel chains (half words)
+            uint32_t w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w0) : "r"(r[0][e]));
+              asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w1) : "r"(r[1][e]));
+              asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w2) : "r"(r[0][e + 16]));
+              asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w3) : "r"(r[1][e + 16]));
+            }
+            n0 += __popc(w0) + __popc(w2);
+            n1 += __popc(w1) + __popc(w3);
+#else  // 2: K3-TC's count, alternating LEA.HI (ALU pipe) and IMAD.HI (FMA pipe); 3: LEA.HI only
+            uint32_t c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u, c4 = 0u, c5 = 0u, c6 = 0u, c7 = 0u;
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+              for (int e = 0; e < 32; e += 8) {
+                ct_sign_alu(c0, r[q][e]);
+                ct_sign_alu(c2, r[q][e + 2]);
+                ct_sign_alu(c4, r[q][e + 4]);
+                ct_sign_alu(c6, r[q][e + 6]);
+                if (RV_CT_COUNT == 2) {
+                  ct_sign_fma(c1, r[q][e + 1], two);
+                  ct_sign_fma(c3, r[q][e + 3], two);
+                  ct_sign_fma(c5, r[q][e + 5], two);
+                  ct_sign_fma(c7, r[q][e + 7], two);
+                } else {
+                  ct_sign_alu(c1, r[q][e + 1]);
+                  ct_sign_alu(c3, r[q][e + 3]);
+                  ct_sign_alu(c5, r[q][e + 5]);
+                  ct_sign_alu(c7, r[q][e + 7]);
+                }
+              }
+            n0 += (c0 + c1) + (c2 + c3);
+            n1 += (c4 + c5) + (c6 + c7);
+#endif
           }
         } else {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) bar_arrive(&sm.tempty[acc]);
+          if (lane == 0) bar_arrive(&sm.tempty[acc * kCtSl + msl]);
         }
       }
       gs += (uint32_t)ns;

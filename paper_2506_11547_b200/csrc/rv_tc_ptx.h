@@ -53,6 +53,35 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 
+// The descriptor of smem_desc(saddr, lbo, sbo) as two words: the high word (SBO, version) is
+// the same for every tile of a kernel and the low word is linear in the tile's address, so an
+// MMA issuer keeps (lo0, hi) and adds (bytes >> 4) per tile -- one uniform add per MMA instead of
+// rebuilding the 64-bit value.  Valid while (saddr + offsets) >> 4 stays below 2^14 (256 KB).
+__device__ __forceinline__ uint32_t smem_desc_lo(uint32_t saddr, uint32_t lbo) {
+  return ((saddr >> 4) & 0x3FFFu) | (((lbo >> 4) & 0x3FFFu) << 16);
+}
+__host__ __device__ constexpr uint32_t smem_desc_hi(uint32_t sbo) {
+  return ((sbo >> 4) & 0x3FFFu) | (1u << 14);
+}
+__device__ __forceinline__ uint64_t desc64(uint32_t lo, uint32_t hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(hi));
+  return d;
+}
+// One lane of a converged warp (the MMA issuer: the whole warp walks the pipeline loop with
+// warp-uniform values, so the tcgen05 operands live in uniform registers; issuing from inside an
+// `if (lane == 0)` region instead makes ptxas move every operand with an ELECT / R2UR loop per
+// instruction -- ~90 dependent instructions per stage, which bounded K3-CT's stage period)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    su32(b))

@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                       int32_t n_items_host, const int32_t* __restrict__ counts_dev, float guard,
                       float* dump, int64_t dump_ld) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int32_t n_items = counts_dev ? counts_dev[0] : n_items_host;
+  const int32_t n_items =
+      counts_dev ? __shfl_sync(0xffffffffu, counts_dev[0], 0) : n_items_host;  // (warp-uniform)
   TcSmem& sm = *reinterpret_cast<TcSmem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -301,22 +302,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
+  // The two issuing warps walk their loops whole, with warp-uniform values (item fields broadcast
+  // from lane 0), and one elected lane issues: the bulk-copy and tcgen05 operands then live in
+  // uniform registers.  (Issued from inside `if (lane == 0)`, ptxas moved every operand through
+  // an ELECT / R2UR loop per instruction: ~90 dependent instructions per tile in the MMA warp.)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
-    if (lane == 0) {
-      uint32_t gt = 0, gi = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
-        const VoteItem it = items[idx];
-        const uint32_t ab = gi % kTcABufs;
-        if (gi >= (uint32_t)kTcABufs) bar_wait(&sm.aempty[ab], ((gi / kTcABufs) - 1) & 1);
+    uint32_t gt = 0, gi = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
+      const VoteItem it = items[idx];
+      const int it_ablk = __shfl_sync(0xffffffffu, it.ablk, 0);
+      const int it_ni = __shfl_sync(0xffffffffu, it.ni, 0);
+      const int64_t row0 = __shfl_sync(0xffffffffu, segs[it.seg].koff + it.i0, 0);
+      const uint32_t ab = gi % kTcABufs;
+      if (gi >= (uint32_t)kTcABufs) bar_wait(&sm.aempty[ab], ((gi / kTcABufs) - 1) & 1);
+      if (elect_one()) {
         bar_expect_tx(&sm.afull[ab], (uint32_t)kTcABlockBytes);
-        bulk_g2s(sm.a[ab], atab + (int64_t)it.ablk * kTcABlockBytes, (uint32_t)kTcABlockBytes,
+        bulk_g2s(sm.a[ab], atab + (int64_t)it_ablk * kTcABlockBytes, (uint32_t)kTcABlockBytes,
                  &sm.afull[ab]);
-        const uint8_t* src = tab + (segs[it.seg].koff + it.i0) * 64;
-        const int ntiles = it.ni / kTcN;  // it.i0, it.ni are multiples of kTcN
-        for (int t = 0; t < ntiles; ++t, ++gt) {
-          const uint32_t s = gt % kTcStages;
-          if (gt >= (uint32_t)kTcStages) bar_wait(&sm.empty[s], ((gt / kTcStages) - 1) & 1);
+      }
+      __syncwarp();
+      const uint8_t* src = tab + row0 * 64;
+      const int ntiles = it_ni / kTcN;  // it.i0, it.ni are multiples of kTcN
+      for (int t = 0; t < ntiles; ++t, ++gt) {
+        const uint32_t s = gt % kTcStages;
+        if (gt >= (uint32_t)kTcStages) bar_wait(&sm.empty[s], ((gt / kTcStages) - 1) & 1);
+        if (elect_one()) {
           if (ABL & 4) {
             bar_arrive(&sm.full[s]);
           } else {
@@ -324,34 +335,40 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             bulk_g2s(sm.b[s], src + (int64_t)t * kTileBytes, kTileBytes, &sm.full[s]);
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      uint32_t gt = 0, gi = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
-        const int ntiles = items[idx].ni / kTcN;
-        const uint32_t ab = gi % kTcABufs;
-        bar_wait(&sm.afull[ab], (gi / kTcABufs) & 1);
-        const uint32_t a0 = su32(sm.a[ab]);
-        for (int t = 0; t < ntiles; ++t, ++gt) {
-          const uint32_t s = gt % kTcStages, b = gt % kTcAcc;
-          bar_wait(&sm.full[s], (gt / kTcStages) & 1);
-          if (gt >= (uint32_t)kTcAcc) bar_wait(&sm.tempty[b], ((gt / kTcAcc) - 1) & 1);
-          tc_fence_after();
-          const uint32_t b0 = su32(sm.b[s]);
+    constexpr uint32_t dhi = smem_desc_hi(512);
+    const uint32_t blo0 = smem_desc_lo(su32(sm.b[0]), 128);
+    const uint32_t alo0 = smem_desc_lo(su32(sm.a[0]), 128);
+    uint32_t gt = 0, gi = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x, ++gi) {
+      const int ntiles = __shfl_sync(0xffffffffu, items[idx].ni, 0) / kTcN;
+      const uint32_t ab = gi % kTcABufs;
+      bar_wait(&sm.afull[ab], (gi / kTcABufs) & 1);
+      const uint32_t alo = alo0 + ab * (uint32_t)(sizeof(sm.a[0]) >> 4);
+      for (int t = 0; t < ntiles; ++t, ++gt) {
+        const uint32_t s = gt % kTcStages, b = gt % kTcAcc;
+        bar_wait(&sm.full[s], (gt / kTcStages) & 1);
+        if (gt >= (uint32_t)kTcAcc) bar_wait(&sm.tempty[b], ((gt / kTcAcc) - 1) & 1);
+        tc_fence_after();
+        const uint32_t blo = blo0 + s * (uint32_t)(sizeof(sm.b[0]) >> 4);
+        if (elect_one()) {
           if (!(ABL & 2)) {
 #pragma unroll
             for (int k = 0; k < 2; ++k)
-              mma_f16(tmem + b * kTcN, smem_desc(a0 + 256 * k, 128, 512),
-                      smem_desc(b0 + 256 * k, 128, 512), (uint32_t)k);
+              mma_f16(tmem + b * kTcN, desc64(alo + 16 * k, dhi), desc64(blo + 16 * k, dhi),
+                      (uint32_t)k);
           }
           mma_commit(&sm.empty[s]);  // smem slot free once these MMAs completed
           mma_commit(&sm.tfull[b]);  // accumulator b ready
         }
-        mma_commit(&sm.aempty[ab]);  // A buffer free once the item's MMAs completed
+        __syncwarp();
       }
+      if (elect_one()) mma_commit(&sm.aempty[ab]);  // A buffer free once the item's MMAs completed
+      __syncwarp();
     }
   } else {
     // ---------------- epilogue: count sign bits (warps 2..9) ----------------
