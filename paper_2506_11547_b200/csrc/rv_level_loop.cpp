@@ -1352,6 +1352,14 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
     RV_CUDA(cudaStreamWaitEvent(ctx->gstream, ctx->gfork, 0), "fork");
     ctx->stream = ctx->gstream;
     cudaGraph_t g = nullptr;
+    // A workspace buffer reallocated while capturing leaves the nodes captured before it with
+    // the freed pointer (nothing runs during a capture, so -- unlike a direct enqueue -- the
+    // earlier kernels have not finished with it): such a graph must never be launched.  It
+    // happens when the previous solve grew a capacity (overflow / retry), so the capture is
+    // discarded and this solve runs directly; the next one captures.
+    const uint64_t epoch0 = g_realloc_epoch.load();
+    const int64_t c_l = ctx->launches, c_v = ctx->vote_launches, c_c = ctx->cull_launches,
+                  c_t = ctx->cull_tc_launches;
     cudaError_t ce = cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeRelaxed);
     int rc = RV_OK;
     if (ce == cudaSuccess) {
@@ -1365,6 +1373,15 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
     if (rc) {
       if (g) cudaGraphDestroy(g);
       return rc;
+    }
+    if (ce == cudaSuccess && g_realloc_epoch.load() != epoch0) {
+      cudaGraphDestroy(g);
+      ctx->launches = c_l;
+      ctx->vote_launches = c_v;
+      ctx->cull_launches = c_c;
+      ctx->cull_tc_launches = c_t;
+      ctx->lastkey_ok = false;  // (run directly below; the solve after this one captures)
+      return solve_one_pass(ctx, x, y, n, eps, ch, out, mask, redo, excl);
     }
     cudaGraphExec_t ge = nullptr;
     if (ce == cudaSuccess) ce = cudaGraphInstantiateWithFlags(&ge, g, 0);
@@ -1411,6 +1428,7 @@ int solve_one_pass(rv_ctx* ctx, const float* x, const float* y, int64_t n, doubl
                      *rb.bad);
   if (*rb.err != 0) {  // a capacity or the re-dive: the per-level loop redoes the solve
     *redo = true;
+    ctx->lastkey_ok = false;  // (capacities may grow: the next solve sizes the workspace directly)
     ctx->redo_reason = *rb.err;
     if ((*rb.err & 16) && ctx->op_lshift > 2) --ctx->op_lshift;  // culling lists
     if ((*rb.err & 3) && ctx->op_cap < kOnePassCapMax)             // level lists / items

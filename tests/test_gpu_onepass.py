@@ -121,6 +121,42 @@ def test_one_pass_retry_path(torch_cuda):
         sync.close()
 
 
+def test_repeated_solves_after_a_retry(torch_cuda):
+    """The same solve (same buffers: the graph key) repeated after the one-pass loop handed it to
+    the per-level loop.  The retry grows capacities, so the next enqueue reallocates workspace:
+    it must run directly, never as a capture (a graph captured across a reallocation keeps freed
+    pointers in its earlier nodes -- an illegal access at launch, found with the rigid pose at
+    99% outliers).  A growing problem size on one context walks the same reallocation path."""
+    from paper_2506_11547_b200 import RotVote
+    pr = datagen.make_problem(3000, 900, 0.01, 0.6, seed=7)
+    rv = RotVote(max_n=40000, chain=(15, 45, 90, 180, 360))
+    try:
+        x, y = dev(torch_cuda, pr.x), dev(torch_cuda, pr.y)
+        mask = torch_cuda.zeros((pr.n + 31) // 32, dtype=torch_cuda.int32, device="cuda")
+        ref = rv.solve(x, y, pr.eps, mask=mask)
+        m_ref = mask.cpu().numpy()
+        assert ref.flags & RV_RETRIED
+        for k in range(5):
+            mask.zero_()
+            r = rv.solve(x, y, pr.eps, mask=mask)
+            same(r, ref, mask.cpu().numpy(), m_ref)
+        # larger problems on the same context (every workspace buffer grows), each solved
+        # three times: direct, capture, replay
+        for n in (6000, 20000, 40000):
+            pb = datagen.make_problem(n, n // 10, 0.01, 0.05, seed=n)
+            xb, yb = dev(torch_cuda, pb.x), dev(torch_cuda, pb.y)
+            mb = torch_cuda.zeros((n + 31) // 32, dtype=torch_cuda.int32, device="cuda")
+            first = rv.solve(xb, yb, pb.eps, mask=mb)
+            m_first = mb.cpu().numpy()
+            for k in range(3):
+                mb.zero_()
+                r = rv.solve(xb, yb, pb.eps, mask=mb)
+                same(r, first, mb.cpu().numpy(), m_first)
+        torch_cuda.cuda.synchronize()
+    finally:
+        rv.close()
+
+
 def test_one_pass_full_size_cfg4(torch_cuda):
     """The bench's workload (cfg4, chain 15-45-180-360): one pass, identical to the per-level
     loop, and the oracle's winner (the full oracle solve is in test_gpu_fullsize.py)."""

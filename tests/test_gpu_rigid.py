@@ -89,6 +89,30 @@ def test_rigid_paper_setting(rv, torch_cuda):
     assert np.linalg.norm(r["t_mean"] - p.t) < 0.02     # the paper's success bar
 
 
+def test_rigid_99_percent_outliers_repeated(torch_cuda):
+    """P:797-801 at 99% outliers, the same scene three times on one context: the rotation vote
+    of the pairs takes the re-dive (reading R18), i.e. the one-pass loop hands it to the per-level
+    loop, and the repeated call must neither capture a graph across the retry's reallocations
+    nor change its answer."""
+    from scipy.spatial.transform import Rotation as Rot
+    from paper_2506_11547_b200 import RotVote
+    torch = torch_cuda
+    p = datagen.make_rigid(5000, 0.99, 0.01, seed=0)
+    ctx = RotVote(max_n=4_000_000)
+    try:
+        x, y = dev(torch, p.x), dev(torch, p.y)
+        rs = [ctx.rigid(x, y, 0.05, 0.05) for _ in range(3)]
+        torch.cuda.synchronize()
+    finally:
+        ctx.close()
+    for r in rs[1:]:
+        assert r["rot_votes"] == rs[0]["rot_votes"] and np.array_equal(r["q"], rs[0]["q"])
+        assert np.array_equal(r["t_cell"], rs[0]["t_cell"])
+    w, a, b, c = rs[0]["q"]
+    err = np.degrees((Rot.from_matrix(p.R).inv() * Rot.from_quat([a, b, c, w])).magnitude())
+    assert err < 0.5 and np.linalg.norm(rs[0]["t_mean"] - p.t) < 0.02
+
+
 def test_rigid_rejects_bad_input(rv, torch_cuda):
     from paper_2506_11547_b200 import RotVoteError
     torch = torch_cuda
