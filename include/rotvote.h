@@ -146,9 +146,15 @@ typedef struct {
  * default chain, refine_rounds 2, guard 1e-5, stream NULL, tensor_vote 1, cull 1. */
 void rot_vote_default_config(rv_config* cfg);
 
-/* Create a context.  Allocates all workspace for cfg->max_n correspondences on
- * cfg->device; world > 1 initialises NCCL (ncclCommInitRank, collective across
- * ranks).  *out = NULL on failure.  Errors: RV_EINVAL, RV_ECUDA, RV_ENCCL, RV_ENOMEM. */
+/* Create a context.  Allocates the K table for cfg->max_n correspondences, the streams, events
+ * and pinned staging on cfg->device; world > 1 initialises NCCL (ncclCommInitRank, collective
+ * across ranks).  The level workspace (block lists, pass bitmasks, culling lists, item tables)
+ * is owned by the context too but sized by the first solve of a given (n, eps, chain) and kept:
+ * that solve allocates (RV_ENOMEM if it cannot), later solves of the same or a smaller size do
+ * not, and a one-pass solve whose fixed capacities prove too small is redone by the per-level
+ * loop (rv_result.flags & RV_RETRIED) with the capacities grown for the next call.  Deviation
+ * from SURVEY 8(b) "solve does not allocate": true from the second solve of a size on.
+ * *out = NULL on failure.  Errors: RV_EINVAL, RV_ECUDA, RV_ENCCL, RV_ENOMEM. */
 int rot_vote_create(const rv_config* cfg, rv_ctx** out);
 
 /* Release everything the context owns.  NULL is a no-op. */
