@@ -888,7 +888,8 @@ __global__ void __launch_bounds__(kCullThreads, kCullCtasPerSm)
 #endif
 constexpr int kCtStages = RV_CT_STAGES;  // 16 KB gathered stages in flight
 #ifndef RV_CT_PROD
-#define RV_CT_PROD 4  // gathering warps
+#define RV_CT_PROD 8  // gathering warps (8: one per stage slot; 4 -> 8 measured -2.5% on the
+                      // culled votes of a cfg4 solve once the issuer was warp-uniform, round 2)
 #endif
 #ifndef RV_CT_SPLIT
 #define RV_CT_SPLIT 1  // gathering warps per stage (a team; stage k -> team k mod (PROD / SPLIT));
@@ -900,6 +901,9 @@ constexpr int kCtProd = RV_CT_PROD;
 constexpr int kCtSplit = RV_CT_SPLIT;
 constexpr int kCtTeams = kCtProd / kCtSplit;
 static_assert(kCtProd % kCtSplit == 0, "gathering warps come in whole teams");
+static_assert(kCtProd / kCtSplit <= RV_CT_STAGES,
+              "a team per stage slot at most: with more teams than slots two teams fill one slot "
+              "out of order and the ring deadlocks");
 constexpr int kCtN = 256;                            // gathered entries per stage
 #ifndef RV_CT_PP
 #define RV_CT_PP 0  // 1: ping-pong epilogue (alternate stages per warp group): measured slower at NA = 1
@@ -976,6 +980,9 @@ __device__ __forceinline__ void ct_sign_fma(uint32_t& acc, uint32_t bits, uint32
   asm volatile("mad.hi.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(bits), "r"(two));
 }
 
+#ifndef RV_CT_EPIPE
+#define RV_CT_EPIPE 0  // 1: software-pipelined epilogue (next round's TMEM load under this round's count)
+#endif
 #ifndef RV_CT_COUNT
 #define RV_CT_COUNT 0  // the sign count: 0 two funnel-shift chains + popcount, 1 four chains,
                        // 2 LEA.HI / IMAD.HI alternating (K3-TC's), 3 LEA.HI only
@@ -1278,6 +1285,75 @@ __global__ void __launch_bounds__(kCtThreads)
       gs += (uint32_t)ns;
       if (active && m < nrows) {
         const uint32_t pass = mine * kCols - (n0 + n1);
+        if (pass) {
+          const VoteSeg& sg = segs[it.seg];
+          const int32_t e = cidx[it.pos0 + (FIN ? (m >> 1) : m)];
+          atomicAdd(FIN && (m & 1) ? &sg.cnt_b[e] : &sg.cnt_a[e], pass);
+        }
+      }
+      if (ew == 0 && lane == 0 && pairs)
+        atomicAdd(pairs, (unsigned long long)it.ne * (unsigned long long)it.ncell);
+    }
+#elif RV_CT_EPIPE
+    // ---------------- epilogue, software-pipelined (4 kCtEpq warps, a column slice each) -------
+    // Rounds of 32 columns in two register sets X / Y: the next round's tcgen05.ld is in flight
+    // while the current round is counted, so a warp's own TMEM reads and sign counts overlap
+    // (the lockstep loop reads, waits, counts; the warps of an SMSP then all read and all count
+    // at the same time).  The last round of a stage is counted under the first load of the next.
+    const int ew = warp - kCtEpi0, slice = ew >> 2;
+    constexpr int kCols = kCtN / kCtEpq;  // columns of a stage per warp
+    static_assert(kCols % 64 == 0, "two register sets of 32 columns");
+    const int msl = (slice * kCols) / (kCtN / kCtSl);  // the accumulator slice of its columns
+    const uint32_t lane_addr =
+        tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(slice * kCols);
+    uint32_t gs = 0;
+    for (;;) {
+      const int idx = next_item(true);
+      if (idx < 0) break;
+      const CullItem it = items[idx];
+      const int na = ct_na(it);
+      const int ns = (it.ne + kCtN / na - 1) / (kCtN / na);
+      const int nrows = FIN ? 2 * it.ncell : it.ncell;
+      const int h = na == 1 ? 0 : (slice * kCols) / (kCtN / na);
+      const int m = 128 * h + 32 * (warp & 3) + lane;
+      const bool active = 128 * h + 32 * (warp & 3) < nrows;  // warp-uniform
+      uint32_t nneg = 0;
+      uint32_t X[32], Y[32];
+      bool pend = false;  // Y holds a loaded, uncounted round
+      auto count = [&](uint32_t (&r)[32]) {
+        uint32_t w = 0u;
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          asm volatile("shf.l.clamp.b32 %0, %1, %0, 1;" : "+r"(w) : "r"(r[e]));
+        nneg += __popc(w);
+      };
+      for (int k = 0; k < ns; ++k) {
+        const uint32_t g = gs + (uint32_t)k, acc = g & 1;
+        ct_wait(&sm.tfull[acc * kCtSl + msl], (g >> 1) & 1);
+        if (ew == 0 && lane == 0) CT_STAMP(5, g);
+        tc_fence_after();
+        if (active && !(RV_CT_ABL & 4)) {
+          const uint32_t base = lane_addr + acc * kCtN;
+#pragma unroll
+          for (int rr = 0; rr < kCols / 32; rr += 2) {
+            RV_TCX_LD32(X, base + (uint32_t)(rr * 32));
+            if (pend) count(Y);
+            tmem_wait_ld();
+            RV_TCX_LD32(Y, base + (uint32_t)(rr * 32 + 32));
+            count(X);
+            tmem_wait_ld();
+            pend = true;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(&sm.tempty[acc * kCtSl + msl]);
+        if (ew == 0 && lane == 0) CT_STAMP(6, g);
+      }
+      if (pend) count(Y);
+      gs += (uint32_t)ns;
+      if (active && m < nrows) {
+        const uint32_t pass = (uint32_t)ns * kCols - nneg;
         if (pass) {
           const VoteSeg& sg = segs[it.seg];
           const int32_t e = cidx[it.pos0 + (FIN ? (m >> 1) : m)];
