@@ -364,6 +364,23 @@ def _roofline(args, vote_pairs, vote_ms, ms_per_step, cull_pairs=0, cull_ms=0.0,
             "vote_share_of_step": (vote_ms / steps) / ms_per_step}
 
 
+HOST_AFFINITY = "unchanged"
+
+
+def _bind_near_gpu(device):
+    """Run this process on the CPUs next to the GPU (NVML's ideal affinity: the NUMA node of its
+    PCIe root), so the pinned host buffers of the e2e arm are allocated there -- what a
+    deployment does with numactl; a no-op where NVML or the call is unavailable."""
+    global HOST_AFFINITY
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByIndex(device))
+        HOST_AFFINITY = "gpu-local cpus (nvmlDeviceSetCpuAffinity): %d" % len(os.sched_getaffinity(0))
+    except Exception as e:  # noqa: BLE001
+        HOST_AFFINITY = "unchanged (%s)" % type(e).__name__
+
+
 def _dist_setup(args):
     import torch
     import torch.distributed as dist
@@ -374,6 +391,7 @@ def _dist_setup(args):
     if world == 1 and args.gpus > 1:
         raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
     torch.cuda.set_device(local)
+    _bind_near_gpu(local)
     nccl_id = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -483,7 +501,9 @@ def run_ours(args):
                    "evaluated_pairs_per_solve": evaluated,
                    "evaluated_votes_per_s": evaluated / (ms_per_step / 1e3)},
         "roofline": roofline,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(2 * pr.x.nbytes),
+        "e2e": {"value": e2e_value, "unit": UNIT, "host_affinity": HOST_AFFINITY,
+                "ms_each": [round(v, 3) for v in e2e_ms],
+                "h2d_bytes_per_step": int(2 * pr.x.nbytes),
                 "d2h_bytes_per_step": int(hmask.numel() * 4),
                 "ms_per_step": sum(e2e_ms) / len(e2e_ms)},
         "gpu_launches": launches,
