@@ -240,9 +240,18 @@ __global__ void __launch_bounds__(1024) cull_rows(const uint32_t* __restrict__ l
 // list's order is irrelevant (counts are sums), so the rows' segments are compacted in
 // parallel; each row ends with fill[b] entries (ungrouped: exactly l0cnt[b], K3-TC's count
 // being the popcount of its words).
-constexpr int kCompactSeg = 256;
-constexpr int kCompactStage = 1024;  // entries staged in shared memory per warp
-__global__ void __launch_bounds__(256) cull_compact(const uint32_t* __restrict__ bits0,
+#ifndef RV_COMPACT_SEG
+#define RV_COMPACT_SEG 256  // bitmask words per warp task (128 or 256)
+#endif
+#ifndef RV_COMPACT_STAGE
+#define RV_COMPACT_STAGE 1024
+#endif
+#ifndef RV_COMPACT_MINB
+#define RV_COMPACT_MINB 1  // __launch_bounds__ minimum CTAs per SM (register cap)
+#endif
+constexpr int kCompactSeg = RV_COMPACT_SEG;
+constexpr int kCompactStage = RV_COMPACT_STAGE;  // entries staged in shared memory per warp
+__global__ void __launch_bounds__(256, RV_COMPACT_MINB) cull_compact(const uint32_t* __restrict__ bits0,
                                                     const int64_t* __restrict__ toffs, int64_t m0,
                                                     int64_t G, const int32_t* __restrict__ goff,
                                                     const int32_t* __restrict__ gmem,

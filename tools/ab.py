@@ -17,14 +17,15 @@ pr = getattr(datagen, cfg)()
 x, y = torch.from_numpy(pr.x).cuda(), torch.from_numpy(pr.y).cuda()
 rv = RotVote(max_n=pr.n, chain=chain, stream=torch.cuda.current_stream())
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-ms, cm, vm, la = [], [], [], []
+ms, cm, vm, la, rs = [], [], [], [], []
 for i in range(18):
     flush.zero_(); torch.cuda.synchronize()
     r = rv.solve(x, y, pr.eps)
     if i >= 3:
-        ms.append(r.ms); cm.append(r.cull_ms); vm.append(r.vote_ms); la.append(r.launches)
+        ms.append(r.ms); cm.append(r.cull_ms); vm.append(r.vote_ms); la.append(r.launches); rs.append(r)
 med = lambda v: sorted(v)[len(v) // 2]
-print(f"{sys.argv[3]:>10s} {cfg}: solve {med(ms):.3f} ms (min {min(ms):.3f})  K3-CT {med(cm):.3f}  "
+l0 = med([v.phase_ms["level0"] for v in rs]) if rs and getattr(rs[0], "phase_ms", None) else 0.0
+print(f"{sys.argv[3]:>10s} {cfg}: solve {med(ms):.3f} ms (min {min(ms):.3f})  level0 {l0:.3f}  K3-CT {med(cm):.3f}  "
       f"K3-TC {med(vm):.3f}  launches {la[-1]}  cell {r.cell} votes {r.votes} ties {r.n_tied}", flush=True)
 """
 
