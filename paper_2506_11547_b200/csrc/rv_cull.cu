@@ -556,6 +556,9 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
     int64_t* ioff, int32_t* cidx, float* phi, uint8_t* tphi, float tc_guard, VoteSeg* segs,
     int32_t* counts, int32_t* work, CullItem* items, int64_t target, int64_t max_items,
     int32_t* err, int64_t own_lo, int64_t own_hi, int32_t cpi, DiveStep d) {
+#if RV_PS_TIMING
+  const long long tz = clock64();
+#endif
   if (d.on) {  // the one-pass dive level: pick, children, zeroed counts, phase (rv_dplan.h)
     __shared__ uint32_t s_par[27];
     __shared__ int s_i[34];
@@ -615,8 +618,19 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
   if (!(RV_PS_ABL & 1))
     cull_scatter_body(L, P, B, eps, mode, guard, m0, act, aoff, tanc, tslot, cidx, phi, tphi,
                       tc_guard);
+#if RV_PS_TIMING
+  __syncthreads();
+  long long t4 = clock64();
+#endif
   if (!(RV_PS_ABL & 2))
     cull_items_body(P, m0, acnt, l0cnt, lofs, aoff, ioff, counts, items, err, cpi);
+#if RV_PS_TIMING
+  __syncthreads();
+  long long t5 = clock64();
+  if (threadIdx.x == 0)
+    printf("plan_small cycles: dive %lld act %lld count %lld scan %lld scatter %lld items %lld (B %d, T %lld)\n",
+           t0 - tz, t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4, B, (long long)act[P]);
+#endif
 }
 
 // ---- K3-C ------------------------------------------------------------------------------------
