@@ -607,10 +607,7 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
                  target, max_items, err, cpi);
   __syncthreads();
 #if RV_PS_TIMING
-  long long t3 = clock64();
-  if (threadIdx.x == 0)
-    printf("plan_small cycles: act %lld count %lld scan %lld (NB %lld, T %lld)\n", t1 - t0, t2 - t1,
-           t3 - t2, (long long)P * m0, (long long)act[P]);
+  long long t3 = clock64();  // (no printf here: it would delay warp 0 into the next phase)
 #endif
 #ifndef RV_PS_ABL
 #define RV_PS_ABL 0  // tuning only: 1 skip the scatter, 2 skip the items (wrong results)
@@ -628,8 +625,8 @@ __global__ void __launch_bounds__(1024) cull_plan_small(
   __syncthreads();
   long long t5 = clock64();
   if (threadIdx.x == 0)
-    printf("plan_small cycles: dive %lld act %lld count %lld scan %lld scatter %lld items %lld (B %d, T %lld)\n",
-           t0 - tz, t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4, B, (long long)act[P]);
+    printf("plan_small cycles: dive %lld act %lld count %lld scan %lld scatter %lld items %lld (B %d, T %lld) [abs t3 %lld t4 %lld]\n",
+           t0 - tz, t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4, B, (long long)act[P], t3 % 100000000LL, t4 % 100000000LL);
 #endif
 }
 
