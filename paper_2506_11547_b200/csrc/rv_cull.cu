@@ -1575,6 +1575,47 @@ void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
                          (int)b1);
     mark_device_done(attr_done);
   }
+#ifndef RV_CT_PERSIST
+#define RV_CT_PERSIST 0  // 1: the gather source as a persisting L2 access-policy window of the launch
+#endif
+#if RV_CT_PERSIST
+  // The gathered rows are re-read ~39 times per correspondence while the index lists stream
+  // through L2 once: mark the table persisting (and everything else streaming) for this launch.
+  static std::atomic<uint64_t> lim_done{0};
+  static size_t max_win = 0;
+  if (first_launch_on_device(lim_done)) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceProp pr{};
+    cudaGetDeviceProperties(&pr, dev);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)pr.persistingL2CacheMaxSize);
+    max_win = (size_t)pr.accessPolicyMaxWindowSize;
+    mark_device_done(lim_done);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)num_sms);
+  cfg.blockDim = dim3(kCtThreads);
+  cfg.dynamicSmemBytes = b0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[0].val.accessPolicyWindow.base_ptr = const_cast<uint8_t*>(tab);
+  size_t nb = (size_t)(pad_row + 8) * 64;
+  if (max_win && nb > max_win) nb = max_win;
+  at[0].val.accessPolicyWindow.num_bytes = nb;
+  at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+  at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const int so = static_order ? 1 : 0;
+  if (mode == RV_MODE_FINAL)
+    cudaLaunchKernelEx(&cfg, rv_vote_cull_tc_kernel<true>, segs, items, counts_dev, tab, pad_row, tphi,
+                       cidx, lidx, pairs, work, so);
+  else
+    cudaLaunchKernelEx(&cfg, rv_vote_cull_tc_kernel<false>, segs, items, counts_dev, tab, pad_row, tphi,
+                       cidx, lidx, pairs, work, so);
+#else
   if (mode == RV_MODE_FINAL)
     rv_vote_cull_tc_kernel<true><<<num_sms, kCtThreads, b1, s>>>(segs, items, counts_dev, tab, pad_row,
                                                                 tphi, cidx, lidx, pairs, work, static_order ? 1 : 0);
@@ -1582,6 +1623,7 @@ void launch_vote_cull_tc(int mode, const VoteSeg* segs, const CullItem* items,
     rv_vote_cull_tc_kernel<false><<<num_sms, kCtThreads, b0, s>>>(segs, items, counts_dev, tab, pad_row,
                                                                  tphi, cidx, lidx, pairs, work,
                                                                  static_order ? 1 : 0);
+#endif
 }
 
 void launch_vote_cull(int mode, const VoteSeg* segs, const CullItem* items,
